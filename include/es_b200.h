@@ -1,0 +1,175 @@
+/*
+ * es_b200.h -- C ABI of the B200 exact-simulation (ES) engine.
+ *
+ * Drop-in boundary for the reference ES engine (cecprove/es.py).  The
+ * reference has no FFI; its seam is the Python function contract
+ * ("the identical InstrProgram abstraction is the seam where
+ * a device kernel would attach").  Each entry point below
+ * replaces one reference interface, cited per function.  Plain pointers and
+ * sizes only; the Python host layer (paper_2512_06627_b200/es.py) binds it
+ * with ctypes, which drops the GIL for the duration of each call.
+ *
+ * Ownership: the caller owns every input array for the duration of a call.
+ * The library owns device buffers, streams and JIT modules (released by
+ * es_shutdown).  All entry points are re-entrant across host threads.
+ *
+ * Errors: every int-returning entry point returns ES_OK (0) or a negative
+ * ES_E* code; es_last_error() gives a thread-local message.
+ */
+#ifndef ES_B200_H
+#define ES_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* op codes of the reference program (es.py:27-30) */
+#define ES_OP_LOAD_PI 0
+#define ES_OP_AND 1
+#define ES_OP_XOR 2
+#define ES_OP_OUTPUT 3
+
+/* reference ceiling (es.py:25) */
+#define ES_MAX_PIS 40
+
+/* return codes */
+#define ES_OK 0
+#define ES_E_TOO_MANY_INPUTS (-1) /* TooManyInputs (es.py:39-40, 97-98) */
+#define ES_E_CUDA (-2)            /* CUDA / JIT failure; es_last_error() says which */
+#define ES_E_BAD_PROGRAM (-3)     /* malformed program or graph */
+#define ES_E_BAD_ARG (-4)         /* e.g. workers < 1 (es.py:260-261) */
+#define ES_E_NO_DEVICE (-5)       /* no CUDA device visible */
+
+/* EsResult.verdict (es.py:34-36) */
+#define ES_EXHAUSTED_ZERO 0
+#define ES_COUNTEREXAMPLE 1
+#define ES_BUDGET_EXCEEDED 2
+
+/* reason attached to ES_BUDGET_EXCEEDED */
+#define ES_REASON_NONE 0
+#define ES_REASON_TIMEOUT 1
+#define ES_REASON_CANCELLED 2
+
+/* engines */
+#define ES_ENGINE_AUTO 0   /* JIT straight-line kernel when it pays, else interpreter */
+#define ES_ENGINE_JIT 1    /* K1: per-program LOP3 straight-line kernel (registers) */
+#define ES_ENGINE_INTERP 2 /* K2: shared-memory interpreter of the program */
+
+/*
+ * The reference InstrProgram as structure-of-arrays -- exactly the arrays
+ * es.py:_encode builds (es.py:232-249), with negations as 0/1 bytes.
+ * InstrProgram (es.py:66-73) / Instr (es.py:43-63).
+ */
+typedef struct es_prog {
+    int32_t num_instrs;
+    int32_t num_registers; /* peak live registers (es.py:163) */
+    int32_t num_pis;
+    const int8_t *op;
+    const int32_t *dst;
+    const int32_t *src0; /* -1 = constant-0 rail (OUTPUT only) */
+    const uint8_t *neg0;
+    const int32_t *src1;
+    const uint8_t *neg1;
+    const int32_t *pi; /* 1-based PI index, LOAD_PI only */
+} es_prog;
+
+/* Options of one run (run_exhaustive's workers/budget/cancel, es.py:252-253). */
+typedef struct es_run_opts {
+    int32_t device;         /* CUDA ordinal */
+    int32_t engine;         /* ES_ENGINE_* */
+    double budget_s;        /* < 0: none; 0.0 -> BUDGET_EXCEEDED before any work */
+    const volatile int32_t *cancel_flag; /* host flag polled between slices; may be NULL */
+    double slice_ms;        /* target device time per launch slice (budget/cancel granularity) */
+    int32_t block_threads;  /* 0: default */
+    int32_t flags;          /* bit0: skip witness re-check on host; bit1: verbose */
+} es_run_opts;
+
+/* EsResult (es.py:76-84) plus engine statistics. */
+typedef struct es_result {
+    int32_t verdict;            /* ES_EXHAUSTED_ZERO | ES_COUNTEREXAMPLE | ES_BUDGET_EXCEEDED */
+    int32_t reason;             /* ES_REASON_* (BUDGET_EXCEEDED only) */
+    int32_t engine;             /* engine that ran (ES_ENGINE_JIT / _INTERP) */
+    int32_t num_luts;           /* LOP3 ops per 32-pattern word after mapping (JIT) */
+    uint64_t witness_index;     /* pattern p, PI i+1 = bit i of p (es.py:315-320) */
+    uint64_t patterns_evaluated;/* reference workers=1 accounting (es.py:313, 333) */
+    uint64_t patterns_swept;    /* patterns this engine actually simulated */
+    double compile_ms;          /* host map + schedule + codegen */
+    double jit_ms;              /* PTX -> SASS + module load (0 on a cache hit) */
+    double device_ms;           /* CUDA-event time of the kernel slices */
+    double wall_ms;             /* whole call */
+    int32_t launches;           /* kernel launches issued */
+    int32_t regs_per_thread;    /* JIT kernel register count */
+} es_result;
+
+/*
+ * compile_program (es.py:87-163): the reference schedule, instruction for
+ * instruction (cone marking, fanin refcounts, lazy PI loads, LIFO register
+ * reuse).  Input: the XAG as packed gates, literal = node*2+neg (xag.py:28-33),
+ * kind 0 = AND, 1 = XOR (xag.py:16-18).  Output arrays must hold
+ * num_pis + num_gates + 1 entries.  Returns the instruction count (> 0) or
+ * ES_E_TOO_MANY_INPUTS / ES_E_BAD_PROGRAM.
+ */
+int32_t es_compile(int32_t num_pis, int32_t num_gates, const uint8_t *kind,
+                   const uint32_t *in0, const uint32_t *in1, uint32_t out_lit,
+                   int8_t *op, int32_t *dst, int32_t *src0, uint8_t *neg0,
+                   int32_t *src1, uint8_t *neg1, int32_t *pi,
+                   int32_t *num_registers);
+
+/*
+ * run_exhaustive (es.py:252-339) on one GPU: sweep all 2^num_pis patterns and
+ * return the MINIMUM-index pattern whose output is 1 (== the reference's
+ * workers=1 witness), EXHAUSTED_ZERO, or BUDGET_EXCEEDED.
+ */
+int32_t es_run(const es_prog *prog, const es_run_opts *opts, es_result *out);
+
+/*
+ * Batched run_exhaustive over many independent programs (the sweep's
+ * sub-miter stream, sweep.py:225-255): one interpreter launch covers all
+ * jobs.  outs[i] receives job i's result.
+ */
+int32_t es_run_batch(int32_t n_jobs, const es_prog *progs, const es_run_opts *opts,
+                     es_result *outs);
+
+/*
+ * Sharded sweep for one rank of a multi-GPU job.  Prepares the
+ * JIT kernel for `prog` and returns an opaque session.  es_session_launch
+ * enqueues, on `stream` (a cudaStream_t, e.g. torch's current stream), the
+ * kernel over global chunks [chunk_begin, chunk_end) restricted to
+ * chunk % world == rank; it atomically lowers *best (a device uint64 the
+ * caller owns, initialised to 2^num_pis) to the minimum failing pattern it
+ * finds and skips chunks above *best.  The caller reduces *best across ranks
+ * (NCCL MIN) between launches.  Asynchronous: no host synchronisation.
+ */
+typedef struct es_session es_session;
+int32_t es_session_open(const es_prog *prog, const es_run_opts *opts, es_session **out);
+int32_t es_session_geometry(const es_session *s, uint64_t *n_chunks, uint64_t *patterns_per_chunk,
+                            int32_t *num_luts, int32_t *regs_per_thread);
+int32_t es_session_launch(es_session *s, void *stream, uint64_t *best_dev,
+                          uint64_t chunk_begin, uint64_t chunk_end, int32_t rank,
+                          int32_t world);
+void es_session_close(es_session *s);
+
+/* Engine-internal views for tests and profiling. */
+/* LUT-3 mapping statistics of a program: LOP3s per word, schedule peak live. */
+int32_t es_map_stats(const es_prog *prog, int32_t *num_luts, int32_t *peak_live,
+                     int32_t *num_gates);
+/* Evaluate the mapped+scheduled LUT program on the CPU for words [w0, w0+nw)
+ * (32 patterns per word, the kernel's layout): writes the output words.
+ * Lets GPU-less CI check the mapper bit-exactly. */
+int32_t es_map_eval(const es_prog *prog, uint64_t w0, uint64_t nw, uint32_t *out_words);
+/* The PTX the JIT path would compile for `prog` (buf NULL -> returns size). */
+int64_t es_emit_ptx(const es_prog *prog, int32_t block_threads, char *buf, int64_t cap);
+/* Compile PTX to SASS without a GPU (build-time check); returns cubin bytes or < 0. */
+int64_t es_jit_check(const es_prog *prog, int32_t block_threads, int32_t *regs_per_thread,
+                     int32_t *spill_bytes, char *log, int64_t log_cap);
+
+const char *es_last_error(void);
+const char *es_version(void);
+void es_shutdown(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ES_B200_H */

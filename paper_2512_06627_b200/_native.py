@@ -1,0 +1,132 @@
+"""ctypes binding of libes_b200.so (include/es_b200.h).
+
+There is no CPU fallback: if the library is missing or cannot be loaded, every
+engine call raises.  ctypes releases the GIL for the duration of each call, so
+the engine can race SAT/BDD threads exactly like the reference's ES thread
+(sched.py:232-257).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libes_b200.so")
+
+ES_OK = 0
+ES_E_TOO_MANY_INPUTS = -1
+ES_E_CUDA = -2
+ES_E_BAD_PROGRAM = -3
+ES_E_BAD_ARG = -4
+ES_E_NO_DEVICE = -5
+
+ENGINE_AUTO, ENGINE_JIT, ENGINE_INTERP = 0, 1, 2
+ENGINES = {"auto": ENGINE_AUTO, "jit": ENGINE_JIT, "interp": ENGINE_INTERP}
+
+# every symbol include/es_b200.h declares
+EXPORTS = ("es_compile", "es_run", "es_run_batch", "es_session_open", "es_session_geometry",
+           "es_session_launch", "es_session_close", "es_map_stats", "es_map_eval",
+           "es_emit_ptx", "es_jit_check", "es_last_error", "es_version", "es_shutdown")
+
+_P = ctypes.c_void_p
+
+
+class EsProg(ctypes.Structure):
+    _fields_ = [("num_instrs", ctypes.c_int32), ("num_registers", ctypes.c_int32),
+                ("num_pis", ctypes.c_int32), ("op", _P), ("dst", _P), ("src0", _P),
+                ("neg0", _P), ("src1", _P), ("neg1", _P), ("pi", _P)]
+
+
+class EsRunOpts(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int32), ("engine", ctypes.c_int32),
+                ("budget_s", ctypes.c_double), ("cancel_flag", _P),
+                ("slice_ms", ctypes.c_double), ("block_threads", ctypes.c_int32),
+                ("flags", ctypes.c_int32)]
+
+
+class EsResult(ctypes.Structure):
+    _fields_ = [("verdict", ctypes.c_int32), ("reason", ctypes.c_int32),
+                ("engine", ctypes.c_int32), ("num_luts", ctypes.c_int32),
+                ("witness_index", ctypes.c_uint64), ("patterns_evaluated", ctypes.c_uint64),
+                ("patterns_swept", ctypes.c_uint64), ("compile_ms", ctypes.c_double),
+                ("jit_ms", ctypes.c_double), ("device_ms", ctypes.c_double),
+                ("wall_ms", ctypes.c_double), ("launches", ctypes.c_int32),
+                ("regs_per_thread", ctypes.c_int32)]
+
+
+class NativeError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"es_b200 error {code}: {msg}")
+        self.code = code
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    """Load the native engine (fails loudly; never falls back)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise NativeError(ES_E_CUDA, f"{LIB_PATH} is missing: run "
+                              "`python -m paper_2512_06627_b200.build` (or __graft_entry__.build())")
+        L = ctypes.CDLL(LIB_PATH)
+        L.es_compile.argtypes = [ctypes.c_int32, ctypes.c_int32, _P, _P, _P, ctypes.c_uint32,
+                                 _P, _P, _P, _P, _P, _P, _P, _P]
+        L.es_compile.restype = ctypes.c_int32
+        L.es_run.argtypes = [ctypes.POINTER(EsProg), ctypes.POINTER(EsRunOpts),
+                             ctypes.POINTER(EsResult)]
+        L.es_run.restype = ctypes.c_int32
+        L.es_run_batch.argtypes = [ctypes.c_int32, ctypes.POINTER(EsProg),
+                                   ctypes.POINTER(EsRunOpts), ctypes.POINTER(EsResult)]
+        L.es_run_batch.restype = ctypes.c_int32
+        L.es_session_open.argtypes = [ctypes.POINTER(EsProg), ctypes.POINTER(EsRunOpts),
+                                      ctypes.POINTER(_P)]
+        L.es_session_open.restype = ctypes.c_int32
+        L.es_session_geometry.argtypes = [_P, ctypes.POINTER(ctypes.c_uint64),
+                                          ctypes.POINTER(ctypes.c_uint64),
+                                          ctypes.POINTER(ctypes.c_int32),
+                                          ctypes.POINTER(ctypes.c_int32)]
+        L.es_session_geometry.restype = ctypes.c_int32
+        L.es_session_launch.argtypes = [_P, _P, _P, ctypes.c_uint64, ctypes.c_uint64,
+                                        ctypes.c_int32, ctypes.c_int32]
+        L.es_session_launch.restype = ctypes.c_int32
+        L.es_session_close.argtypes = [_P]
+        L.es_session_close.restype = None
+        L.es_map_stats.argtypes = [ctypes.POINTER(EsProg), ctypes.POINTER(ctypes.c_int32),
+                                   ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
+        L.es_map_stats.restype = ctypes.c_int32
+        L.es_map_eval.argtypes = [ctypes.POINTER(EsProg), ctypes.c_uint64, ctypes.c_uint64, _P]
+        L.es_map_eval.restype = ctypes.c_int32
+        L.es_emit_ptx.argtypes = [ctypes.POINTER(EsProg), ctypes.c_int32, ctypes.c_char_p,
+                                  ctypes.c_int64]
+        L.es_emit_ptx.restype = ctypes.c_int64
+        L.es_jit_check.argtypes = [ctypes.POINTER(EsProg), ctypes.c_int32,
+                                   ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
+                                   ctypes.c_char_p, ctypes.c_int64]
+        L.es_jit_check.restype = ctypes.c_int64
+        L.es_last_error.argtypes = []
+        L.es_last_error.restype = ctypes.c_char_p
+        L.es_version.argtypes = []
+        L.es_version.restype = ctypes.c_char_p
+        L.es_shutdown.argtypes = []
+        L.es_shutdown.restype = None
+        _lib = L
+        return L
+
+
+def last_error() -> str:
+    return lib().es_last_error().decode(errors="replace")
+
+
+def check(rc: int) -> int:
+    if rc < 0:
+        raise NativeError(rc, last_error())
+    return rc

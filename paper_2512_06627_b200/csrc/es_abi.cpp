@@ -1,0 +1,149 @@
+// es_abi.cpp -- extern "C" entry points declared in include/es_b200.h.
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "es_core.h"
+#include "es_jit.h"
+
+namespace es {
+
+thread_local std::string t_err;
+void set_error(const std::string &m) { t_err = m; }
+
+int run_one(const es_prog *prog, const es_run_opts *opts, es_result *out);
+int run_batch(int n_jobs, const es_prog *progs, const es_run_opts *opts, es_result *outs);
+int session_open(const es_prog *prog, const es_run_opts *opts, void **out);
+int session_geometry(const void *s, uint64_t *n_chunks, uint64_t *ppc, int32_t *luts, int32_t *regs);
+int session_launch(void *s, void *stream, uint64_t *best_dev, uint64_t chunk_begin,
+                   uint64_t chunk_end, int rank, int world);
+void session_close(void *s);
+void runtime_shutdown();
+
+static int map_prog(const es_prog *prog, LutNet *net) {
+    if (!prog || prog->num_instrs < 1) { set_error("empty program"); return ES_E_BAD_PROGRAM; }
+    Dag dag;
+    std::string err;
+    int rc = build_dag(*prog, &dag, &err);
+    if (rc != ES_OK) { set_error(err); return rc; }
+    map_luts(dag, net);
+    return ES_OK;
+}
+
+}  // namespace es
+
+using namespace es;
+
+extern "C" {
+
+int32_t es_compile(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+                   const uint32_t *in1, uint32_t out_lit, int8_t *op, int32_t *dst, int32_t *src0,
+                   uint8_t *neg0, int32_t *src1, uint8_t *neg1, int32_t *pi,
+                   int32_t *num_registers) {
+    int32_t rc = ref_compile(num_pis, num_gates, kind, in0, in1, out_lit, op, dst, src0, neg0,
+                             src1, neg1, pi, num_registers);
+    if (rc == ES_E_TOO_MANY_INPUTS) set_error(std::to_string(num_pis) + " PIs exceeds the 40 ceiling");
+    else if (rc < 0) set_error("malformed XAG");
+    return rc;
+}
+
+int32_t es_run(const es_prog *prog, const es_run_opts *opts, es_result *out) {
+    if (!prog || !out) { set_error("null argument"); return ES_E_BAD_ARG; }
+    return run_one(prog, opts, out);
+}
+
+int32_t es_run_batch(int32_t n_jobs, const es_prog *progs, const es_run_opts *opts,
+                     es_result *outs) {
+    if (n_jobs < 0 || (n_jobs > 0 && (!progs || !outs))) { set_error("bad batch"); return ES_E_BAD_ARG; }
+    return run_batch(n_jobs, progs, opts, outs);
+}
+
+int32_t es_session_open(const es_prog *prog, const es_run_opts *opts, es_session **out) {
+    void *s = nullptr;
+    int rc = session_open(prog, opts, &s);
+    *out = (es_session *)s;
+    return rc;
+}
+
+int32_t es_session_geometry(const es_session *s, uint64_t *n_chunks, uint64_t *ppc,
+                            int32_t *num_luts, int32_t *regs) {
+    if (!s) return ES_E_BAD_ARG;
+    return session_geometry(s, n_chunks, ppc, num_luts, regs);
+}
+
+int32_t es_session_launch(es_session *s, void *stream, uint64_t *best_dev, uint64_t chunk_begin,
+                          uint64_t chunk_end, int32_t rank, int32_t world) {
+    if (!s || !best_dev) { set_error("null argument"); return ES_E_BAD_ARG; }
+    return session_launch(s, stream, best_dev, chunk_begin, chunk_end, rank, world);
+}
+
+void es_session_close(es_session *s) { session_close(s); }
+
+int32_t es_map_stats(const es_prog *prog, int32_t *num_luts, int32_t *peak_live,
+                     int32_t *num_gates) {
+    LutNet net;
+    int rc = map_prog(prog, &net);
+    if (rc != ES_OK) return rc;
+    if (num_luts) *num_luts = (int32_t)net.luts.size();
+    if (peak_live) *peak_live = net.peak_live;
+    if (num_gates) *num_gates = net.num_gates;
+    return ES_OK;
+}
+
+int32_t es_map_eval(const es_prog *prog, uint64_t w0, uint64_t nw, uint32_t *out_words) {
+    LutNet net;
+    int rc = map_prog(prog, &net);
+    if (rc != ES_OK) return rc;
+    eval_lutnet(net, w0, nw, out_words);
+    return ES_OK;
+}
+
+int64_t es_emit_ptx(const es_prog *prog, int32_t block_threads, char *buf, int64_t cap) {
+    LutNet net;
+    int rc = map_prog(prog, &net);
+    if (rc != ES_OK) return rc;
+    std::string ptx, err;
+    if (!splice_body(net, block_threads > 0 ? block_threads : 256, &ptx, &err)) {
+        set_error(err);
+        return ES_E_BAD_ARG;
+    }
+    if (buf && cap > 0) {
+        const int64_t n = std::min<int64_t>(cap - 1, (int64_t)ptx.size());
+        std::memcpy(buf, ptx.data(), (size_t)n);
+        buf[n] = '\0';
+    }
+    return (int64_t)ptx.size() + 1;
+}
+
+int64_t es_jit_check(const es_prog *prog, int32_t block_threads, int32_t *regs_per_thread,
+                     int32_t *spill_bytes, char *log, int64_t log_cap) {
+    LutNet net;
+    int rc = map_prog(prog, &net);
+    if (rc != ES_OK) return rc;
+    std::string ptx, err, info;
+    if (!splice_body(net, block_threads > 0 ? block_threads : 256, &ptx, &err)) {
+        set_error(err);
+        return ES_E_BAD_ARG;
+    }
+    std::vector<char> cubin;
+    rc = ptx_to_cubin(ptx, &cubin, &info, &err);
+    if (rc != ES_OK) { set_error(err); return rc; }
+    int regs = -1, spill = 0;
+    parse_ptxas_info(info, &regs, &spill);
+    if (regs_per_thread) *regs_per_thread = regs;
+    if (spill_bytes) *spill_bytes = spill;
+    if (log && log_cap > 0) {
+        const int64_t n = std::min<int64_t>(log_cap - 1, (int64_t)info.size());
+        std::memcpy(log, info.data(), (size_t)n);
+        log[n] = '\0';
+    }
+    return (int64_t)cubin.size();
+}
+
+const char *es_last_error(void) { return t_err.c_str(); }
+
+const char *es_version(void) { return "es_b200 0.1 (sm_100a)"; }
+
+void es_shutdown(void) { runtime_shutdown(); }
+
+}  // extern "C"

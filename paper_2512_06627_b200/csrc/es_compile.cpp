@@ -1,0 +1,505 @@
+// es_compile.cpp -- host compiler of the B200 ES engine.
+//
+//  * ref_compile : compile_program (cecprove/es.py:87-163), instruction-exact:
+//                  output-cone marking (:103-111), fanin refcounts (:113-119),
+//                  topological emission with lazy PI loads (:138-150), fanins
+//                  consumed before dst allocation (:151-156), LIFO pool
+//                  (:126-136), output-is-PI (:160-161), constant output (:99-101).
+//  * build_dag   : the register program back to an SSA graph, so any
+//                  InstrProgram (the reference's seam) can be run.
+//  * map_luts    : LUT-3 cover of the cone.  A LOP3 evaluates any 3-input
+//                  function of 32-bit words in one ALU issue, so covering the
+//                  XAG with 3-feasible cuts cuts the issue count well below the
+//                  gate count (a full adder is 2 LOP3 instead of 5 gates).
+//                  Low PIs 1..5 are per-bit constants of a 32-bit word
+//                  (0xAAAAAAAA ...): nodes over them fold to constants.
+//  * schedule    : DFS order that keeps the live set small enough to stay in
+//                  registers (the reason the reference recycles registers,
+//                  es.py:9-10; here the register file is the SM's).
+//  * emit_body_ptx / eval_lutnet : the kernel body and its CPU model.
+#include <algorithm>
+#include <cstring>
+#include <functional>
+#include <sstream>
+#include <unordered_map>
+
+#include "es_core.h"
+
+namespace es {
+
+const uint32_t kLaneMask[kLanePis] = {0xAAAAAAAAu, 0xCCCCCCCCu, 0xF0F0F0F0u,
+                                      0xFF00FF00u, 0xFFFF0000u};
+
+uint32_t lane_valid_mask(int num_pis) {
+    return num_pis >= kLanePis ? 0xFFFFFFFFu : ((1u << (1u << num_pis)) - 1u);
+}
+
+// ---------------------------------------------------------------------------
+// compile_program, reference schedule (es.py:87-163)
+// ---------------------------------------------------------------------------
+int32_t ref_compile(int32_t num_pis, int32_t num_gates, const uint8_t *kind,
+                    const uint32_t *in0, const uint32_t *in1, uint32_t out_lit,
+                    int8_t *op, int32_t *dst, int32_t *src0, uint8_t *neg0,
+                    int32_t *src1, uint8_t *neg1, int32_t *pi, int32_t *num_registers) {
+    if (num_pis > ES_MAX_PIS) return ES_E_TOO_MANY_INPUTS;
+    if (num_pis < 0 || num_gates < 0) return ES_E_BAD_PROGRAM;
+    const int first = 1 + num_pis, nn = first + num_gates;
+    const int onode = (int)(out_lit >> 1);
+    const bool oneg = out_lit & 1;
+    if (onode >= nn) return ES_E_BAD_PROGRAM;
+    int n = 0;
+    auto put = [&](int o, int d, int a, bool na, int b, bool nb, int p) {
+        op[n] = (int8_t)o; dst[n] = d; src0[n] = a; neg0[n] = na; src1[n] = b;
+        neg1[n] = nb; pi[n] = p; ++n;
+    };
+    if (onode == 0) {
+        put(ES_OP_OUTPUT, 0, -1, oneg, -1, false, 0);
+        *num_registers = 0;
+        return n;
+    }
+    std::vector<uint8_t> live(nn, 0);
+    live[onode] = 1;
+    for (int v = nn - 1; v >= first; --v) {
+        if (!live[v]) continue;
+        const int g = v - first;
+        const int a = (int)(in0[g] >> 1), b = (int)(in1[g] >> 1);
+        if (a >= v || b >= v || a == 0 || b == 0) return ES_E_BAD_PROGRAM;
+        live[a] = live[b] = 1;
+    }
+    std::vector<int32_t> refs(nn, 0), reg(nn, -1), pool;
+    refs[onode] += 1;
+    for (int v = first; v < nn; ++v)
+        if (live[v]) { refs[in0[v - first] >> 1]++; refs[in1[v - first] >> 1]++; }
+    int peak = 0;
+    auto alloc = [&]() -> int {
+        if (!pool.empty()) { int r = pool.back(); pool.pop_back(); return r; }
+        return peak++;
+    };
+    auto load_pi = [&](int v) {
+        if (reg[v] < 0) { reg[v] = alloc(); put(ES_OP_LOAD_PI, reg[v], -1, false, -1, false, v); }
+    };
+    auto consume = [&](int v) { if (--refs[v] == 0) pool.push_back(reg[v]); };
+    for (int v = first; v < nn; ++v) {
+        if (!live[v]) continue;
+        const int g = v - first;
+        const int a = (int)(in0[g] >> 1), b = (int)(in1[g] >> 1);
+        if (a <= num_pis) load_pi(a);
+        if (b <= num_pis) load_pi(b);
+        const int ra = reg[a], rb = reg[b];
+        consume(a);
+        consume(b);
+        reg[v] = alloc();
+        put(kind[g] ? ES_OP_XOR : ES_OP_AND, reg[v], ra, in0[g] & 1, rb, in1[g] & 1, 0);
+    }
+    if (onode <= num_pis) load_pi(onode);
+    put(ES_OP_OUTPUT, 0, reg[onode], oneg, -1, false, 0);
+    *num_registers = peak;
+    return n;
+}
+
+// ---------------------------------------------------------------------------
+// register program -> SSA graph
+// ---------------------------------------------------------------------------
+int build_dag(const es_prog &p, Dag *dag, std::string *err) {
+    auto fail = [&](const std::string &m) { if (err) *err = m; return ES_E_BAD_PROGRAM; };
+    if (p.num_pis < 0) return fail("negative PI count");
+    if (p.num_pis > ES_MAX_PIS) return ES_E_TOO_MANY_INPUTS;
+    if (p.num_instrs < 1) return fail("empty program");
+    if (p.op[p.num_instrs - 1] != ES_OP_OUTPUT) return fail("last instruction is not OUTPUT");
+    dag->num_pis = p.num_pis;
+    dag->is_xor.clear(); dag->f0.clear(); dag->f1.clear(); dag->n0.clear(); dag->n1.clear();
+    const int R = std::max(p.num_registers, 0);
+    std::vector<int32_t> node_of(R, -1);
+    int next = 1 + p.num_pis;
+    for (int i = 0; i < p.num_instrs; ++i) {
+        const int o = p.op[i];
+        if (o == ES_OP_OUTPUT) {
+            if (i != p.num_instrs - 1) return fail("OUTPUT before the end");
+            if (p.src0[i] < 0) { dag->out_node = 0; dag->out_neg = p.neg0[i]; break; }
+            if (p.src0[i] >= R || node_of[p.src0[i]] < 0) return fail("OUTPUT reads an undefined register");
+            dag->out_node = node_of[p.src0[i]];
+            dag->out_neg = p.neg0[i];
+            break;
+        }
+        if (p.dst[i] < 0 || p.dst[i] >= R) return fail("dst register out of range");
+        if (o == ES_OP_LOAD_PI) {
+            if (p.pi[i] < 1 || p.pi[i] > p.num_pis) return fail("LOAD_PI index out of range");
+            node_of[p.dst[i]] = p.pi[i];
+        } else if (o == ES_OP_AND || o == ES_OP_XOR) {
+            const int a = p.src0[i], b = p.src1[i];
+            if (a < 0 || a >= R || b < 0 || b >= R || node_of[a] < 0 || node_of[b] < 0)
+                return fail("gate reads an undefined register");
+            dag->is_xor.push_back(o == ES_OP_XOR);
+            dag->f0.push_back(node_of[a]);
+            dag->n0.push_back(p.neg0[i] ? 1 : 0);
+            dag->f1.push_back(node_of[b]);
+            dag->n1.push_back(p.neg1[i] ? 1 : 0);
+            node_of[p.dst[i]] = next++;
+        } else {
+            return fail("unknown opcode");
+        }
+    }
+    return ES_OK;
+}
+
+// ---------------------------------------------------------------------------
+// LUT-3 mapping
+// ---------------------------------------------------------------------------
+namespace {
+
+struct Cut {
+    int32_t leaf[3];
+    uint8_t n;
+    uint8_t tt;  // over leaf k = bit k of the minterm index; replicated over unused vars
+    float af;
+};
+
+inline uint8_t expand_tt(const Cut &c, const int32_t *L, int nL) {
+    int pos[3] = {0, 0, 0};
+    for (int k = 0; k < c.n; ++k)
+        for (int q = 0; q < nL; ++q)
+            if (L[q] == c.leaf[k]) pos[k] = q;
+    uint8_t r = 0;
+    for (int i = 0; i < 8; ++i) {
+        int j = 0;
+        for (int k = 0; k < c.n; ++k) j |= ((i >> pos[k]) & 1) << k;
+        r |= ((c.tt >> j) & 1) << i;
+    }
+    return r;
+}
+
+inline bool depends(uint8_t tt, int k) {
+    for (int i = 0; i < 8; ++i)
+        if (((tt >> i) & 1) != ((tt >> (i ^ (1 << k))) & 1)) return true;
+    return false;
+}
+
+inline uint8_t drop_var(uint8_t tt, int k) {
+    uint8_t r = 0;
+    for (int i = 0; i < 8; ++i) {
+        int lo = i & ((1 << k) - 1);
+        int src = lo | ((i >> k) << (k + 1));
+        src &= 7;
+        r |= ((tt >> src) & 1) << i;
+    }
+    return r;
+}
+
+// canonical replicated form of a tt over n vars
+inline uint8_t replicate(uint8_t tt, int n) {
+    uint8_t r = 0;
+    for (int i = 0; i < 8; ++i) r |= ((tt >> (i & ((1 << n) - 1))) & 1) << i;
+    return r;
+}
+
+inline uint32_t lut3(uint8_t tt, uint32_t a /*leaf2*/, uint32_t b /*leaf1*/, uint32_t c /*leaf0*/) {
+    uint32_t r = 0;
+    for (int i = 0; i < 8; ++i)
+        if ((tt >> i) & 1) r |= ((i & 4) ? a : ~a) & ((i & 2) ? b : ~b) & ((i & 1) ? c : ~c);
+    return r;
+}
+
+constexpr int kMaxCuts = 10;
+
+}  // namespace
+
+void map_luts(const Dag &dag, LutNet *net) {
+    const int N = dag.num_nodes(), FG = dag.first_gate();
+    const int P = dag.num_pis;
+    net->num_pis = P;
+    net->luts.clear();
+    net->pis_used.clear();
+    net->is_const.assign(N, 0);
+    net->const_val.assign(N, 0);
+    net->out_node = dag.out_node;
+    net->out_neg = dag.out_neg;
+    net->num_gates = 0;
+    net->peak_live = 0;
+
+    std::vector<uint8_t> cone(N, 0);
+    cone[dag.out_node] = 1;
+    for (int v = N - 1; v >= FG; --v) {
+        if (!cone[v]) continue;
+        const int g = v - FG;
+        cone[dag.f0[g]] = cone[dag.f1[g]] = 1;
+    }
+    // constant folding: node 0, lane PIs 1..5, and gates over constants only
+    std::vector<uint8_t> &isc = net->is_const;
+    std::vector<uint32_t> &cv = net->const_val;
+    isc[0] = 1; cv[0] = 0;
+    for (int j = 1; j <= std::min(P, kLanePis); ++j) { isc[j] = 1; cv[j] = kLaneMask[j - 1]; }
+    std::vector<int32_t> fo(N, 0);
+    fo[dag.out_node] += 1;
+    for (int v = FG; v < N; ++v) {
+        if (!cone[v]) continue;
+        const int g = v - FG;
+        net->num_gates++;
+        fo[dag.f0[g]]++; fo[dag.f1[g]]++;
+        const int a = dag.f0[g], b = dag.f1[g];
+        if (isc[a] && isc[b]) {
+            uint32_t x = cv[a] ^ (dag.n0[g] ? ~0u : 0u), y = cv[b] ^ (dag.n1[g] ? ~0u : 0u);
+            isc[v] = 1;
+            cv[v] = dag.is_xor[g] ? (x ^ y) : (x & y);
+        }
+    }
+    auto is_gate_lut = [&](int v) { return v >= FG && cone[v] && !isc[v]; };
+
+    // priority cut enumeration in topological order
+    std::vector<std::vector<Cut>> cuts(N);
+    std::vector<float> af(N, 0.f);
+    auto trivial = [](int v) { Cut c{}; c.leaf[0] = v; c.leaf[1] = c.leaf[2] = -1; c.n = 1; c.tt = 0xAA; c.af = 0; return c; };
+    for (int v = 1; v <= P; ++v) cuts[v].push_back(trivial(v));
+    std::vector<Cut> cand;
+    for (int v = FG; v < N; ++v) {
+        if (!cone[v]) continue;
+        if (isc[v]) { cuts[v].push_back(trivial(v)); continue; }
+        const int g = v - FG;
+        const int a = dag.f0[g], b = dag.f1[g];
+        const bool x = dag.is_xor[g];
+        cand.clear();
+        const std::vector<Cut> &ca = cuts[a], &cb = cuts[b];
+        for (const Cut &c0 : ca) {
+            for (const Cut &c1 : cb) {
+                int32_t L[3];
+                int nL = 0, i = 0, j = 0;
+                bool ok = true;
+                while (i < c0.n || j < c1.n) {
+                    int32_t pick;
+                    if (j >= c1.n || (i < c0.n && c0.leaf[i] < c1.leaf[j])) pick = c0.leaf[i++];
+                    else if (i >= c0.n || c1.leaf[j] < c0.leaf[i]) pick = c1.leaf[j++];
+                    else { pick = c0.leaf[i]; ++i; ++j; }
+                    if (nL == 3) { ok = false; break; }
+                    L[nL++] = pick;
+                }
+                if (!ok) continue;
+                uint8_t t0 = expand_tt(c0, L, nL), t1 = expand_tt(c1, L, nL);
+                if (dag.n0[g]) t0 = ~t0;
+                if (dag.n1[g]) t1 = ~t1;
+                uint8_t tt = x ? (uint8_t)(t0 ^ t1) : (uint8_t)(t0 & t1);
+                // support reduction
+                for (int k = nL - 1; k >= 0; --k) {
+                    if (!depends(tt, k)) {
+                        tt = drop_var(tt, k);
+                        for (int q = k; q + 1 < nL; ++q) L[q] = L[q + 1];
+                        --nL;
+                    }
+                }
+                Cut c{};
+                c.n = (uint8_t)nL;
+                for (int q = 0; q < 3; ++q) c.leaf[q] = q < nL ? L[q] : -1;
+                c.tt = replicate(tt, nL);
+                float s = 1.f;
+                for (int q = 0; q < nL; ++q) s += af[L[q]] / (float)std::max(1, fo[L[q]]);
+                c.af = s;
+                cand.push_back(c);
+            }
+        }
+        // a constant function makes the node a constant
+        bool became_const = false;
+        for (const Cut &c : cand) {
+            if (c.n == 0) {
+                isc[v] = 1;
+                cv[v] = (c.tt & 1) ? ~0u : 0u;
+                became_const = true;
+                break;
+            }
+        }
+        if (became_const) { cuts[v].push_back(trivial(v)); continue; }
+        std::sort(cand.begin(), cand.end(), [](const Cut &p, const Cut &q) {
+            if (p.af != q.af) return p.af < q.af;
+            return p.n < q.n;
+        });
+        std::vector<Cut> &cs = cuts[v];
+        for (const Cut &c : cand) {
+            bool dup = false;
+            for (const Cut &d : cs)
+                if (d.n == c.n && d.leaf[0] == c.leaf[0] && d.leaf[1] == c.leaf[1] && d.leaf[2] == c.leaf[2]) { dup = true; break; }
+            if (dup) continue;
+            cs.push_back(c);
+            if ((int)cs.size() >= kMaxCuts) break;
+        }
+        af[v] = cs.empty() ? 1.f : cs[0].af;
+        cs.push_back(trivial(v));  // last: used only as a leaf of fanout cuts
+    }
+
+    // cover: best cut per node, then exact-area recovery
+    std::vector<int> best(N, 0), mref(N, 0);
+    std::function<int(int, const Cut &)> ref_cut, deref_cut;
+    ref_cut = [&](int v, const Cut &c) {
+        int area = 1;
+        for (int q = 0; q < c.n; ++q) {
+            int l = c.leaf[q];
+            if (is_gate_lut(l) && mref[l]++ == 0) area += ref_cut(l, cuts[l][best[l]]);
+        }
+        return area;
+    };
+    deref_cut = [&](int v, const Cut &c) {
+        int area = 1;
+        for (int q = 0; q < c.n; ++q) {
+            int l = c.leaf[q];
+            if (is_gate_lut(l) && --mref[l] == 0) area += deref_cut(l, cuts[l][best[l]]);
+        }
+        return area;
+    };
+    const int out = dag.out_node;
+    if (is_gate_lut(out)) {
+        mref[out] = 1;
+        ref_cut(out, cuts[out][best[out]]);
+        for (int pass = 0; pass < 3; ++pass) {
+            for (int v = FG; v < N; ++v) {
+                if (!is_gate_lut(v) || mref[v] == 0) continue;
+                deref_cut(v, cuts[v][best[v]]);
+                int bi = best[v], ba = 1 << 30;
+                float baf = 1e30f;
+                const int nc = (int)cuts[v].size() - 1;  // exclude trivial
+                for (int ci = 0; ci < nc; ++ci) {
+                    int a = ref_cut(v, cuts[v][ci]);
+                    deref_cut(v, cuts[v][ci]);
+                    if (a < ba || (a == ba && cuts[v][ci].af < baf)) { ba = a; bi = ci; baf = cuts[v][ci].af; }
+                }
+                best[v] = bi;
+                ref_cut(v, cuts[v][best[v]]);
+            }
+        }
+    }
+
+    // schedule: DFS post-order, children by decreasing register need
+    std::vector<int> need(N, 0), users(N, 0);
+    std::vector<uint8_t> pi_used(P + 1, 0);
+    for (int v = FG; v < N; ++v) {
+        if (!is_gate_lut(v) || mref[v] == 0) continue;
+        const Cut &c = cuts[v][best[v]];
+        for (int q = 0; q < c.n; ++q) {
+            int l = c.leaf[q];
+            if (is_gate_lut(l)) users[l]++;
+            else if (l >= 1 && l <= P && !isc[l]) pi_used[l] = 1;
+        }
+    }
+    if (out >= 1 && out <= P && !isc[out]) pi_used[out] = 1;
+    for (int j = 1; j <= P; ++j) if (pi_used[j]) net->pis_used.push_back(j);
+    std::vector<uint8_t> done(N, 0);
+    std::vector<int> order;
+    if (is_gate_lut(out)) {
+        // need() bottom-up in topological order
+        for (int v = FG; v < N; ++v) {
+            if (!is_gate_lut(v) || mref[v] == 0) continue;
+            const Cut &c = cuts[v][best[v]];
+            int kn[3], k = 0;
+            for (int q = 0; q < c.n; ++q) if (is_gate_lut(c.leaf[q])) kn[k++] = need[c.leaf[q]];
+            std::sort(kn, kn + k, std::greater<int>());
+            int nd = 1;
+            for (int q = 0; q < k; ++q) nd = std::max(nd, kn[q] + q);
+            need[v] = nd;
+        }
+        // iterative DFS
+        std::vector<int> st{out};
+        while (!st.empty()) {
+            const int v = st.back();
+            if (done[v]) { st.pop_back(); continue; }
+            const Cut &c = cuts[v][best[v]];
+            int pick = -1;
+            for (int q = 0; q < c.n; ++q) {  // highest-need pending child first
+                int l = c.leaf[q];
+                if (is_gate_lut(l) && !done[l] && (pick < 0 || need[l] > need[pick])) pick = l;
+            }
+            if (pick >= 0) { st.push_back(pick); continue; }
+            done[v] = 1;
+            order.push_back(v);
+            st.pop_back();
+        }
+    }
+    // emit LUTs and measure the live set
+    std::vector<int> remaining = users;
+    if (is_gate_lut(out)) remaining[out] += 1;
+    int live = 0;
+    for (int v : order) {
+        const Cut &c = cuts[v][best[v]];
+        Lut L{};
+        L.node = v;
+        L.nleaves = c.n;
+        for (int q = 0; q < 3; ++q) L.leaf[q] = q < c.n ? c.leaf[q] : c.leaf[0];
+        L.tt = c.tt;
+        if (v == out && dag.out_neg) L.tt = (uint8_t)~L.tt;
+        net->luts.push_back(L);
+        int freed = 0;
+        for (int q = 0; q < c.n; ++q) {
+            int l = c.leaf[q];
+            bool seen = false;
+            for (int r = 0; r < q; ++r) seen |= c.leaf[r] == l;
+            if (seen || !is_gate_lut(l)) continue;
+            if (--remaining[l] == 0) ++freed;
+        }
+        live = live - freed + 1;
+        net->peak_live = std::max(net->peak_live, live);
+    }
+    if (is_gate_lut(out)) net->out_neg = false;  // folded into the root LUT
+}
+
+// ---------------------------------------------------------------------------
+// CPU model of the mapped program (same word layout as the kernel)
+// ---------------------------------------------------------------------------
+void eval_lutnet(const LutNet &net, uint64_t w0, uint64_t nw, uint32_t *out) {
+    const int N = (int)net.is_const.size();
+    std::vector<uint32_t> val(N, 0);
+    for (int v = 0; v < N; ++v) if (net.is_const[v]) val[v] = net.const_val[v];
+    const uint32_t valid = lane_valid_mask(net.num_pis);
+    for (uint64_t k = 0; k < nw; ++k) {
+        const uint64_t w = w0 + k;
+        for (int j : net.pis_used) val[j] = ((w >> (j - 6)) & 1) ? ~0u : 0u;
+        for (const Lut &L : net.luts)
+            val[L.node] = lut3(L.tt, val[L.leaf[2]], val[L.leaf[1]], val[L.leaf[0]]);
+        uint32_t o = val[net.out_node];
+        if (net.out_neg) o = ~o;
+        out[k] = o & valid;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// PTX body for the K1 skeleton
+// ---------------------------------------------------------------------------
+std::string emit_body_ptx(const LutNet &net, const std::string &out,
+                          const std::string &wlo, const std::string &whi) {
+    const int N = (int)net.is_const.size();
+    std::ostringstream s;
+    // register names per node
+    std::vector<int> lut_idx(N, -1);
+    for (size_t i = 0; i < net.luts.size(); ++i) lut_idx[net.luts[i].node] = (int)i;
+    std::unordered_map<uint32_t, int> cidx;
+    std::vector<uint32_t> consts;
+    auto name = [&](int v) -> std::string {
+        if (lut_idx[v] >= 0) return "%esq" + std::to_string(lut_idx[v]);
+        if (net.is_const[v]) {
+            uint32_t c = net.const_val[v];
+            auto it = cidx.find(c);
+            int k;
+            if (it == cidx.end()) { k = (int)consts.size(); cidx[c] = k; consts.push_back(c); }
+            else k = it->second;
+            return "%esk" + std::to_string(k);
+        }
+        return "%esm" + std::to_string(v);  // PI mask
+    };
+    std::ostringstream body;
+    for (const Lut &L : net.luts) {
+        body << "lop3.b32 " << name(L.node) << ", " << name(L.leaf[2]) << ", " << name(L.leaf[1])
+             << ", " << name(L.leaf[0]) << ", " << (int)L.tt << ";\n";
+    }
+    const std::string oname = name(net.out_node);
+    s << "{\n";
+    if (!net.luts.empty()) s << ".reg .b32 %esq<" << net.luts.size() << ">;\n";
+    if (!consts.empty()) s << ".reg .b32 %esk<" << consts.size() << ">;\n";
+    if (!net.pis_used.empty()) s << ".reg .b32 %esm<" << (net.num_pis + 1) << ">;\n";
+    for (size_t k = 0; k < consts.size(); ++k) s << "mov.b32 %esk" << k << ", " << consts[k] << ";\n";
+    for (int j : net.pis_used) {
+        const int bit = j - 6;
+        const std::string &src = bit < 32 ? wlo : whi;
+        s << "shl.b32 %esm" << j << ", " << src << ", " << (31 - (bit & 31)) << ";\n";
+        s << "shr.s32 %esm" << j << ", %esm" << j << ", 31;\n";
+    }
+    s << body.str();
+    if (net.out_neg) s << "not.b32 " << out << ", " << oname << ";\n";
+    else s << "mov.b32 " << out << ", " << oname << ";\n";
+    s << "}\n";
+    return s.str();
+}
+
+}  // namespace es

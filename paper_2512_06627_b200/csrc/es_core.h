@@ -1,0 +1,88 @@
+// es_core.h -- internal IR of the B200 ES engine (not part of the C ABI).
+//
+// Pipeline (host, C++):
+//   es_prog (reference InstrProgram, es.py:66-73)
+//     -> Dag        SSA graph rebuilt from the register program
+//     -> LutNet     LUT-3 cover (one LOP3 per LUT), constant-folded low PIs
+//     -> schedule   register-pressure-aware topological order
+//     -> PTX body   spliced into the hand-written K1 skeleton (k1_skeleton.cu)
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/es_b200.h"
+
+namespace es {
+
+// Pattern layout shared by every engine (kernel, CPU model, witness decode):
+// pattern p = 32*w + b.  Bit b of a 32-bit word carries PIs 1..5
+// (PI j = bit j-1 of b), the word index w carries PIs 6.. (PI j = bit j-6 of
+// w).  This is the reference's pattern numbering (es.py:315-320) with 32-bit
+// instead of 64-bit words.
+constexpr int kWordBits = 32;
+constexpr int kLanePis = 5;
+extern const uint32_t kLaneMask[kLanePis];  // 0xAAAAAAAA, 0xCCCCCCCC, ...
+
+// Node ids: 0 = constant FALSE, 1..num_pis = PIs, then gates.
+struct Dag {
+    int num_pis = 0;
+    std::vector<uint8_t> is_xor;     // per gate
+    std::vector<int32_t> f0, f1;     // fanin node ids, per gate
+    std::vector<uint8_t> n0, n1;     // fanin complement flags, per gate
+    int32_t out_node = 0;
+    bool out_neg = false;
+    int num_nodes() const { return 1 + num_pis + (int)is_xor.size(); }
+    int first_gate() const { return 1 + num_pis; }
+    bool is_pi(int v) const { return v >= 1 && v <= num_pis; }
+};
+
+// Rebuild the SSA graph from a reference register program.  Returns ES_OK or
+// ES_E_BAD_PROGRAM (undefined source register, missing/extra OUTPUT, ...).
+int build_dag(const es_prog &p, Dag *dag, std::string *err);
+
+// One LUT: out = f(leaf0, leaf1, leaf2); tt bit i = f at leaf_k = bit k of i
+// (so PTX `lop3.b32 d, leaf2, leaf1, leaf0, tt` computes it).  Leaves are
+// node ids; a leaf is a PI, a folded constant, or another LUT.
+struct Lut {
+    int32_t node;
+    int32_t leaf[3];
+    uint8_t nleaves;
+    uint8_t tt;
+};
+
+struct LutNet {
+    int num_pis = 0;
+    std::vector<Lut> luts;                // in schedule order (topological)
+    std::vector<uint8_t> is_const;        // per node: value is a compile-time word
+    std::vector<uint32_t> const_val;      // per node (valid when is_const)
+    // output: either a LUT/PI/constant node with optional inversion folded in
+    int32_t out_node = 0;
+    bool out_neg = false;                 // inversion still to apply (only when out is a leaf)
+    int num_gates = 0;                    // AND+XOR gates in the output cone
+    int peak_live = 0;                    // max simultaneously live LUT values in the schedule
+    std::vector<int32_t> pis_used;        // PIs >= 6 referenced as leaves
+};
+
+// LUT-3 technology mapping (priority cuts + area flow + exact-area recovery)
+// followed by a live-range-minimising schedule.
+void map_luts(const Dag &dag, LutNet *net);
+
+// Reference compile_program (es.py:87-163), exact.
+int32_t ref_compile(int32_t num_pis, int32_t num_gates, const uint8_t *kind,
+                    const uint32_t *in0, const uint32_t *in1, uint32_t out_lit,
+                    int8_t *op, int32_t *dst, int32_t *src0, uint8_t *neg0,
+                    int32_t *src1, uint8_t *neg1, int32_t *pi, int32_t *num_registers);
+
+// CPU model of the LUT program over words [w0, w0+nw): bit-exact with K1.
+void eval_lutnet(const LutNet &net, uint64_t w0, uint64_t nw, uint32_t *out);
+
+// PTX body for the K1 skeleton: reads the word index from (wlo, whi) and
+// writes the output word to `out` (register names from the skeleton).
+std::string emit_body_ptx(const LutNet &net, const std::string &out,
+                          const std::string &wlo, const std::string &whi);
+
+uint32_t lane_valid_mask(int num_pis);
+
+}  // namespace es

@@ -1,0 +1,160 @@
+// es_jit.cpp -- per-program JIT of K1: splice the generated LOP3 body into the
+// hand-written skeleton PTX (k1_skeleton.cu), compile it to sm_100a SASS with
+// the in-process PTX compiler (libnvptxcompiler_static, no driver JIT, no
+// GPU needed), load it with cudaLibraryLoadData.  Modules are cached by a
+// hash of the final PTX, so a program is compiled once per process.
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include <cuda_runtime.h>
+#include <nvPTXCompiler.h>
+
+#include "es_jit.h"
+
+namespace es {
+
+#include "k1_skeleton_ptx.inc"  // const char *kK1Ptx128, *kK1Ptx256, *kK1Ptx512
+
+static const char *skeleton_for(int threads) {
+    switch (threads) {
+        case 128: return kK1Ptx128;
+        case 256: return kK1Ptx256;
+        case 512: return kK1Ptx512;
+        default: return nullptr;
+    }
+}
+
+bool splice_body(const LutNet &net, int threads, std::string *ptx, std::string *err) {
+    const char *sk = skeleton_for(threads);
+    if (!sk) { *err = "unsupported K1 block size " + std::to_string(threads); return false; }
+    std::string s(sk);
+    const std::string marker = "// ES_BODY ";
+    size_t at = s.find(marker);
+    if (at == std::string::npos || s.find(marker, at + 1) != std::string::npos) {
+        *err = "K1 skeleton must contain exactly one ES_BODY marker";
+        return false;
+    }
+    size_t eol = s.find('\n', at);
+    std::string args = s.substr(at + marker.size(), eol - at - marker.size());
+    char out[64], wlo[64], whi[64];
+    if (sscanf(args.c_str(), "%63s %63s %63s", out, wlo, whi) != 3) {
+        *err = "cannot parse ES_BODY operands: " + args;
+        return false;
+    }
+    std::string body = emit_body_ptx(net, out, wlo, whi);
+    s.replace(at, eol - at, body);
+    *ptx = std::move(s);
+    return true;
+}
+
+static uint64_t fnv1a(const std::string &s) {
+    uint64_t h = 1469598103934665603ull;
+    for (unsigned char c : s) { h ^= c; h *= 1099511628211ull; }
+    return h;
+}
+
+int ptx_to_cubin(const std::string &ptx, std::vector<char> *cubin, std::string *info,
+                 std::string *err) {
+    nvPTXCompilerHandle h = nullptr;
+    if (nvPTXCompilerCreate(&h, ptx.size(), ptx.c_str()) != NVPTXCOMPILE_SUCCESS) {
+        *err = "nvPTXCompilerCreate failed";
+        return ES_E_CUDA;
+    }
+    const char *opts[] = {"--gpu-name=sm_100a", "--verbose", "-O3"};
+    nvPTXCompileResult r = nvPTXCompilerCompile(h, 3, opts);
+    size_t n = 0;
+    if (r != NVPTXCOMPILE_SUCCESS) {
+        nvPTXCompilerGetErrorLogSize(h, &n);
+        std::string log(n, '\0');
+        if (n) nvPTXCompilerGetErrorLog(h, &log[0]);
+        *err = "PTX compile failed (" + std::to_string((int)r) + "): " + log;
+        nvPTXCompilerDestroy(&h);
+        return ES_E_CUDA;
+    }
+    nvPTXCompilerGetCompiledProgramSize(h, &n);
+    cubin->resize(n);
+    nvPTXCompilerGetCompiledProgram(h, cubin->data());
+    size_t m = 0;
+    nvPTXCompilerGetInfoLogSize(h, &m);
+    info->assign(m, '\0');
+    if (m) nvPTXCompilerGetInfoLog(h, &(*info)[0]);
+    nvPTXCompilerDestroy(&h);
+    return ES_OK;
+}
+
+void parse_ptxas_info(const std::string &info, int *regs, int *spill_bytes) {
+    // "... Used 118 registers, ..." and "... N bytes spill stores, M bytes spill loads"
+    *regs = -1;
+    *spill_bytes = 0;
+    size_t p = info.find("Used ");
+    if (p != std::string::npos) *regs = atoi(info.c_str() + p + 5);
+    p = info.find("bytes spill stores");
+    if (p != std::string::npos) {
+        size_t q = info.rfind(',', p);
+        size_t start = q == std::string::npos ? 0 : q + 1;
+        int st = atoi(info.c_str() + start);
+        size_t r = info.find("bytes spill loads", p);
+        int ld = 0;
+        if (r != std::string::npos) {
+            size_t q2 = info.rfind(',', r);
+            ld = atoi(info.c_str() + (q2 == std::string::npos ? 0 : q2 + 1));
+        }
+        *spill_bytes = st + ld;
+    }
+}
+
+namespace {
+std::mutex g_jit_mu;
+std::unordered_map<uint64_t, JitKernel *> g_cache;
+}  // namespace
+
+int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std::string *err) {
+    std::string ptx;
+    if (!splice_body(net, threads, &ptx, err)) return ES_E_BAD_PROGRAM;
+    const uint64_t key = fnv1a(ptx) ^ (uint64_t)threads;
+    std::lock_guard<std::mutex> lk(g_jit_mu);
+    auto it = g_cache.find(key);
+    if (it != g_cache.end()) { *out = it->second; *jit_ms = 0.0; return ES_OK; }
+    auto t0 = now_ms();
+    std::vector<char> cubin;
+    std::string info;
+    int rc = ptx_to_cubin(ptx, &cubin, &info, err);
+    if (rc != ES_OK) return rc;
+    JitKernel *k = new JitKernel();
+    k->threads = threads;
+    parse_ptxas_info(info, &k->regs, &k->spill_bytes);
+    cudaError_t e = cudaLibraryLoadData(&k->lib, cubin.data(), nullptr, nullptr, 0, nullptr,
+                                        nullptr, 0);
+    if (e != cudaSuccess) {
+        *err = std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e);
+        delete k;
+        return ES_E_CUDA;
+    }
+    e = cudaLibraryGetKernel(&k->kernel, k->lib, "es_k1");
+    if (e != cudaSuccess) {
+        *err = std::string("cudaLibraryGetKernel: ") + cudaGetErrorString(e);
+        cudaLibraryUnload(k->lib);
+        delete k;
+        return ES_E_CUDA;
+    }
+    *jit_ms = now_ms() - t0;
+    k->jit_ms = *jit_ms;
+    g_cache[key] = k;
+    *out = k;
+    return ES_OK;
+}
+
+void jit_clear() {
+    std::lock_guard<std::mutex> lk(g_jit_mu);
+    for (auto &kv : g_cache) {
+        cudaLibraryUnload(kv.second->lib);
+        delete kv.second;
+    }
+    g_cache.clear();
+}
+
+}  // namespace es

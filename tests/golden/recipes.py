@@ -1,0 +1,130 @@
+"""Deterministic recipes for every golden circuit (shared by the fixture
+generator and the tests that replay the fixtures).
+
+A recipe is a small dict; ``build_*`` turns it into an ``Xag`` with this
+repo's generators.  ``xag_sha``/``prog_sha`` fingerprint circuits and
+instruction programs so fixtures stay small while still pinning
+gate-for-gate and instruction-for-instruction parity.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import random
+
+from paper_2512_06627_b200 import miter as M
+from paper_2512_06627_b200.xag import random_xag
+
+
+def xag_sha(x) -> str:
+    body = [x.num_pis,
+            [[int(g.kind), g.in0.node * 2 + int(g.in0.neg), g.in1.node * 2 + int(g.in1.neg)]
+             for g in x.gates],
+            [o.node * 2 + int(o.neg) for o in x.outputs]]
+    return hashlib.sha256(json.dumps(body, separators=(",", ":")).encode()).hexdigest()[:20]
+
+
+def prog_sha(rows, num_registers: int) -> str:
+    body = [num_registers, [[int(v) for v in r] for r in rows]]
+    return hashlib.sha256(json.dumps(body, separators=(",", ":")).encode()).hexdigest()[:20]
+
+
+# --- random populations -------------------------------------------------------
+
+def random_population() -> list[dict]:
+    specs = []
+    # test_acceptance.py:82-101 oracle-agreement population
+    rng = random.Random(2024)
+    for k in range(500):
+        specs.append({"pop": "acceptance500", "n_pis": rng.randint(1, 14),
+                      "n_gates": rng.randint(0, 300), "seed": k})
+    # test_es.py:58-67 and :70-78 hypothesis ranges
+    for s in range(0, 301):
+        specs.append({"pop": "tt6x40", "n_pis": 6, "n_gates": 40, "seed": s})
+    for s in range(0, 101):
+        specs.append({"pop": "workers7x50", "n_pis": 7, "n_gates": 50, "seed": s})
+    # wider random cones: multi-word / multi-batch geometry on the GPU
+    rng = random.Random(7)
+    for k in range(60):
+        specs.append({"pop": "wide", "n_pis": rng.randint(15, 24),
+                      "n_gates": rng.randint(100, 1500), "seed": 10_000 + k})
+    return specs
+
+
+def build_random(spec: dict):
+    return random_xag(spec["n_pis"], spec["n_gates"], spec["seed"])
+
+
+# --- named miters -------------------------------------------------------------
+
+# single-gate faults of the config miters whose reference min-index witness
+# is deep (found by tests/golden/find_deep_faults.py; the index itself is the
+# fixture the reference run pins)
+DEEP_FAULTS = {
+    "mult12_array_wallace": [1108, 1210, 941],
+    "mult16_array_booth": [2204, 1953, 1406, 1882, 1220],
+}
+
+
+def miter_population() -> list[dict]:
+    specs: list[dict] = []
+    for w in range(2, 15):
+        specs.append({"name": f"mult{w}_array_diagonal", "kind": "mult", "w": w,
+                      "a": "array", "b": "diagonal", "full_program": w == 3})
+    for w in range(1, 9):
+        specs.append({"name": f"adder{w}_ripple_lookahead", "kind": "adder", "w": w,
+                      "a": "ripple", "b": "lookahead", "full_program": w == 8})
+    for w in range(3, 13):
+        specs.append({"name": f"mult{w}_array_wallace", "kind": "mult", "w": w,
+                      "a": "array", "b": "wallace"})
+    for w in range(2, 15, 2):
+        specs.append({"name": f"mult{w}_array_booth", "kind": "mult", "w": w,
+                      "a": "array", "b": "booth"})
+    # the reference's own fault model on its own miters (mutate, miter.py:141)
+    for w in range(3, 9):
+        for s in range(6):
+            specs.append({"name": f"mult{w}_array_diagonal_mut{s}", "kind": "mult", "w": w,
+                          "a": "array", "b": "diagonal", "mutate_seed": s})
+    for w in (4, 6, 8):
+        for s in range(4):
+            specs.append({"name": f"adder{w}_ripple_lookahead_mut{s}", "kind": "adder",
+                          "w": w, "a": "ripple", "b": "lookahead", "mutate_seed": s})
+    for s in range(4):
+        specs.append({"name": f"mult8_array_booth_mut{s}", "kind": "mult", "w": 8,
+                      "a": "array", "b": "booth", "mutate_seed": s})
+    for base, idxs in DEEP_FAULTS.items():
+        w = int(base[4:6])
+        _, a, b = base.split("_")
+        for gi in idxs:
+            specs.append({"name": f"{base}_flip{gi}", "kind": "mult", "w": w, "a": a, "b": b,
+                          "flip_gate": gi})
+    specs.append({"name": "mult16_array_booth", "kind": "mult", "w": 16, "a": "array",
+                  "b": "booth", "ref_workers": 8})
+    return specs
+
+
+def build_miter_recipe(spec: dict):
+    if spec["kind"] == "mult":
+        x = M.gen_multiplier_miter(spec["w"], spec["a"], spec["b"])
+    elif spec["kind"] == "adder":
+        x = M.gen_adder_miter(spec["w"], spec["a"], spec["b"])
+    else:
+        raise ValueError(spec["kind"])
+    if "mutate_seed" in spec:
+        x = M.mutate(x, seed=spec["mutate_seed"])
+    if "flip_gate" in spec:
+        x = M.flip_gate(x, spec["flip_gate"])
+    return x
+
+
+def build_with_reference(spec: dict, ref_miter, ref_xag):
+    """Same circuit from the reference's own generators, when it has them."""
+    if spec["kind"] != "mult" or {spec["a"], spec["b"]} - {"array", "diagonal"}:
+        return None
+    x = ref_miter.gen_multiplier_miter(spec["w"], spec["a"], spec["b"])
+    if "mutate_seed" in spec:
+        x = ref_miter.mutate(x, seed=spec["mutate_seed"])
+    if "flip_gate" in spec:
+        return None
+    return x
