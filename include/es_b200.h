@@ -165,6 +165,11 @@ int64_t es_emit_ptx(const es_prog *prog, int32_t block_threads, char *buf, int64
 int64_t es_jit_check(const es_prog *prog, int32_t block_threads, int32_t *regs_per_thread,
                      int32_t *spill_bytes, char *log, int64_t log_cap);
 
+/* Measured ALU-pipe peak: lane-LOP3 operations per second on `device` (one
+ * lane-op evaluates one 2/3-input gate over 32 patterns).  The roofline
+ * denominator of the bench. */
+int32_t es_alu_peak(int32_t device, double *lane_ops_per_s, double *ms);
+
 const char *es_last_error(void);
 const char *es_version(void);
 void es_shutdown(void);

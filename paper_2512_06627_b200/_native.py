@@ -28,7 +28,8 @@ ENGINES = {"auto": ENGINE_AUTO, "jit": ENGINE_JIT, "interp": ENGINE_INTERP}
 # every symbol include/es_b200.h declares
 EXPORTS = ("es_compile", "es_run", "es_run_batch", "es_session_open", "es_session_geometry",
            "es_session_launch", "es_session_close", "es_map_stats", "es_map_eval",
-           "es_emit_ptx", "es_jit_check", "es_last_error", "es_version", "es_shutdown")
+           "es_emit_ptx", "es_jit_check", "es_alu_peak", "es_last_error", "es_version",
+           "es_shutdown")
 
 _P = ctypes.c_void_p
 
@@ -112,6 +113,9 @@ def lib():
                                    ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
                                    ctypes.c_char_p, ctypes.c_int64]
         L.es_jit_check.restype = ctypes.c_int64
+        L.es_alu_peak.argtypes = [ctypes.c_int32, ctypes.POINTER(ctypes.c_double),
+                                  ctypes.POINTER(ctypes.c_double)]
+        L.es_alu_peak.restype = ctypes.c_int32
         L.es_last_error.argtypes = []
         L.es_last_error.restype = ctypes.c_char_p
         L.es_version.argtypes = []

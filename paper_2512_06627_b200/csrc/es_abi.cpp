@@ -19,6 +19,7 @@ int session_launch(void *s, void *stream, uint64_t *best_dev, uint64_t chunk_beg
                    uint64_t chunk_end, int rank, int world);
 void session_close(void *s);
 void runtime_shutdown();
+int alu_peak(int dev, double *lane_ops_per_s, double *ms_out);
 
 static int map_prog(const es_prog *prog, LutNet *net) {
     if (!prog || prog->num_instrs < 1) { set_error("empty program"); return ES_E_BAD_PROGRAM; }
@@ -138,6 +139,11 @@ int64_t es_jit_check(const es_prog *prog, int32_t block_threads, int32_t *regs_p
         log[n] = '\0';
     }
     return (int64_t)cubin.size();
+}
+
+int32_t es_alu_peak(int32_t device, double *lane_ops_per_s, double *ms) {
+    if (!lane_ops_per_s) return ES_E_BAD_ARG;
+    return alu_peak(device, lane_ops_per_s, ms);
 }
 
 const char *es_last_error(void) { return t_err.c_str(); }

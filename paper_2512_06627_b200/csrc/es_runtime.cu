@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -125,6 +126,32 @@ __global__ void __launch_bounds__(128) es_k2(const K2Job *__restrict__ jobs,
 }
 
 // ---------------------------------------------------------------------------
+// ALU-pipe peak microbenchmark: 8 independent LOP3 chains per thread, enough
+// warps to saturate every SMSP.  Gives the measured roofline denominator for
+// bit-parallel simulation (lane-LOP3/s); MEASURED_PEAKS.json has no integer
+// figure.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) es_alu_peak_kernel(unsigned *sink, int iters, unsigned seed) {
+    unsigned a0 = seed ^ threadIdx.x, a1 = a0 * 3u, a2 = a0 * 5u, a3 = a0 * 7u;
+    unsigned a4 = a0 * 11u, a5 = a0 * 13u, a6 = a0 * 17u, a7 = a0 * 19u;
+#define ES_L3(d, x, y, z, lut) asm volatile("lop3.b32 %0, %1, %2, %3, " #lut ";" : "=r"(d) : "r"(x), "r"(y), "r"(z))
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            ES_L3(a0, a0, a1, a2, 0x96); ES_L3(a1, a1, a2, a3, 0xE8);
+            ES_L3(a2, a2, a3, a4, 0x96); ES_L3(a3, a3, a4, a5, 0xE8);
+            ES_L3(a4, a4, a5, a6, 0x96); ES_L3(a5, a5, a6, a7, 0xE8);
+            ES_L3(a6, a6, a7, a0, 0x96); ES_L3(a7, a7, a0, a1, 0xE8);
+        }
+    }
+#undef ES_L3
+    const unsigned r = a0 ^ a1 ^ a2 ^ a3 ^ a4 ^ a5 ^ a6 ^ a7;
+    if (r == 0x9E3779B9u) sink[0] = r;
+}
+
+int alu_peak(int dev, double *lane_ops_per_s, double *ms_out);
+
+// ---------------------------------------------------------------------------
 // per-thread, per-device context
 // ---------------------------------------------------------------------------
 namespace {
@@ -216,10 +243,16 @@ struct K1Plan {
     uint32_t valid = 0;
 };
 
-int k1_prepare(const LutNet &net, int threads, int sms, K1Plan *pl, double *jit_ms) {
+int k1_prepare(const LutNet &net, int threads, int sms, K1Plan *pl, double *jit_ms,
+               JitKernel *cached = nullptr) {
     std::string err;
-    int rc = jit_get(net, threads, &pl->jk, jit_ms, &err);
-    if (rc != ES_OK) { set_error(err); return rc; }
+    if (cached) {
+        pl->jk = cached;
+        *jit_ms = 0.0;
+    } else {
+        int rc = jit_get(net, threads, &pl->jk, jit_ms, &err);
+        if (rc != ES_OK) { set_error(err); return rc; }
+    }
     pl->threads = threads;
     const int P = net.num_pis;
     pl->total_words = 1ull << std::max(P - 5, 0);
@@ -252,12 +285,13 @@ int k1_launch(const K1Plan &pl, cudaStream_t st, unsigned long long *best, unsig
 }
 
 static int run_k1(const LutNet &net, int G, const es_run_opts &o, Ctx *c, double deadline,
-                  es_result *r) {
+                  es_result *r, JitKernel **jk_cache) {
     const int threads = o.block_threads > 0 ? o.block_threads : 128;
     K1Plan pl;
     double jit_ms = 0;
-    int rc = k1_prepare(net, threads, c->sms, &pl, &jit_ms);
+    int rc = k1_prepare(net, threads, c->sms, &pl, &jit_ms, *jk_cache);
     if (rc != ES_OK) return rc;
+    *jk_cache = pl.jk;
     r->engine = ES_ENGINE_JIT;
     r->jit_ms = jit_ms;
     r->regs_per_thread = pl.jk->regs;
@@ -470,6 +504,52 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
 // ---------------------------------------------------------------------------
 // public drivers
 // ---------------------------------------------------------------------------
+// Mapped programs cached by a hash of the program arrays: a warm call skips
+// graph rebuild, mapping, PTX emission and the JIT-cache lookup.
+struct MappedProg {
+    LutNet net;
+    int G = 0;
+    JitKernel *jk[3] = {nullptr, nullptr, nullptr};  // per block size 128/256/512
+    std::mutex mu;
+};
+
+static uint64_t prog_hash(const es_prog &p) {
+    uint64_t h = 1469598103934665603ull;
+    auto mix = [&](const void *d, size_t n) {
+        const unsigned char *b = (const unsigned char *)d;
+        for (size_t i = 0; i < n; ++i) { h ^= b[i]; h *= 1099511628211ull; }
+    };
+    mix(&p.num_instrs, 4); mix(&p.num_registers, 4); mix(&p.num_pis, 4);
+    const size_t n = (size_t)p.num_instrs;
+    mix(p.op, n); mix(p.dst, 4 * n); mix(p.src0, 4 * n); mix(p.neg0, n);
+    mix(p.src1, 4 * n); mix(p.neg1, n); mix(p.pi, 4 * n);
+    return h;
+}
+
+static std::mutex g_mapped_mu;
+static std::vector<std::pair<uint64_t, std::shared_ptr<MappedProg>>> g_mapped;
+
+static int get_mapped(const es_prog &p, std::shared_ptr<MappedProg> *out) {
+    const uint64_t key = prog_hash(p);
+    {
+        std::lock_guard<std::mutex> lk(g_mapped_mu);
+        for (auto &kv : g_mapped)
+            if (kv.first == key) { *out = kv.second; return ES_OK; }
+    }
+    Dag dag;
+    std::string err;
+    int rc = build_dag(p, &dag, &err);
+    if (rc != ES_OK) { set_error(err); return rc; }
+    auto mp = std::make_shared<MappedProg>();
+    map_luts(dag, &mp->net);
+    for (int i = 0; i < p.num_instrs; ++i) mp->G += (p.op[i] == ES_OP_AND || p.op[i] == ES_OP_XOR);
+    std::lock_guard<std::mutex> lk(g_mapped_mu);
+    if (g_mapped.size() >= 4096) g_mapped.clear();  // bound host memory for long sweeps
+    g_mapped.push_back({key, mp});
+    *out = mp;
+    return ES_OK;
+}
+
 static bool constant_rail(const es_prog &p, es_result *r) {
     // es.py:265-270: OUTPUT reading the constant rail needs no sweep
     const int last = p.num_instrs - 1;
@@ -510,15 +590,12 @@ int run_one(const es_prog *prog, const es_run_opts *opts, es_result *out) {
         out->wall_ms = now_ms() - t0;
         return ES_OK;
     }
-    Dag dag;
-    std::string err;
-    rc = build_dag(*prog, &dag, &err);
-    if (rc != ES_OK) { set_error(err); return rc; }
-    LutNet net;
-    map_luts(dag, &net);
+    std::shared_ptr<MappedProg> mp;
+    rc = get_mapped(*prog, &mp);
+    if (rc != ES_OK) return rc;
+    const LutNet &net = mp->net;
+    const int G = mp->G;
     out->num_luts = (int)net.luts.size();
-    int G = 0;
-    for (int i = 0; i < prog->num_instrs; ++i) G += (prog->op[i] == ES_OP_AND || prog->op[i] == ES_OP_XOR);
     out->compile_ms = now_ms() - t0;
     Ctx *c = nullptr;
     rc = get_ctx(o.device, &c);
@@ -533,7 +610,10 @@ int run_one(const es_prog *prog, const es_run_opts *opts, es_result *out) {
         std::vector<int> act{0};
         rc = run_k2(1, prog, act, o, c, deadline, out);
     } else {
-        rc = run_k1(net, G, o, c, deadline, out);
+        const int threads = o.block_threads > 0 ? o.block_threads : 128;
+        const int slot = threads == 128 ? 0 : threads == 256 ? 1 : 2;
+        std::lock_guard<std::mutex> lk(mp->mu);
+        rc = run_k1(net, G, o, c, deadline, out, &mp->jk[slot]);
     }
     out->wall_ms = now_ms() - t0;
     return rc;
@@ -634,6 +714,27 @@ void session_close(void *sp) {
     delete s;
 }
 
+int alu_peak(int dev, double *lane_ops_per_s, double *ms_out) {
+    Ctx *c = nullptr;
+    int rc = get_ctx(dev, &c);
+    if (rc != ES_OK) return rc;
+    const int threads = 256, iters = 4096;
+    const int grid = c->sms * 8;
+    unsigned *sink = c->d_counter + 8;
+    es_alu_peak_kernel<<<grid, threads, 0, c->stream>>>(sink, 64, 1u);  // warm-up
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(c->ev_start, c->stream));
+    es_alu_peak_kernel<<<grid, threads, 0, c->stream>>>(sink, iters, 1u);
+    CK(cudaEventRecord(c->ev_stop, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, c->ev_start, c->ev_stop));
+    const double ops = (double)grid * threads * (double)iters * 64.0;
+    *lane_ops_per_s = ops / (ms * 1e-3);
+    if (ms_out) *ms_out = ms;
+    return ES_OK;
+}
+
 void runtime_shutdown() {
     for (Ctx *c : t_ctx) {
         cudaSetDevice(c->dev);
@@ -648,6 +749,10 @@ void runtime_shutdown() {
         delete c;
     }
     t_ctx.clear();
+    {
+        std::lock_guard<std::mutex> lk(g_mapped_mu);
+        g_mapped.clear();
+    }
     jit_clear();
 }
 

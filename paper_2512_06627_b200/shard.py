@@ -1,0 +1,172 @@
+"""Multi-GPU exact simulation: one process per GPU, the 2^n input space
+sharded across ranks.
+
+Chunks of the pattern space are dealt round-robin to ranks (chunk % world ==
+rank) and swept in increasing order by each rank's K1 kernel.  The only
+exchange is the 8-byte minimum failing pattern: after every launch slice the
+ranks all-reduce it with MIN over NCCL, so a counterexample found by any GPU
+stops every GPU at the next chunk claim (global early termination), and the
+final value is the minimum-index witness -- bit-exact with the reference's
+single-worker sweep (es.py:297-320) for any world size.
+
+torch is used only as plumbing: device memory for the 8-byte word, the
+stream, and torch.distributed's NCCL all-reduce.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+from . import _native as N
+from .es import (BUDGET_EXCEEDED, ES_COUNTEREXAMPLE, EXHAUSTED_ZERO, EsResult, as_program,
+                 _opts)
+
+
+class Session:
+    """A program JIT-compiled for one device, launchable on any stream."""
+
+    def __init__(self, prog, device: int = 0, block_threads: int = 0):
+        self.prog = as_program(prog)
+        self.device = device
+        opts = _opts(device, "jit", None, None, 20.0, block_threads)
+        h = ctypes.c_void_p()
+        N.check(N.lib().es_session_open(ctypes.byref(self.prog.as_struct()), ctypes.byref(opts),
+                                        ctypes.byref(h)))
+        self._h = h
+        nc, ppc = ctypes.c_uint64(), ctypes.c_uint64()
+        luts, regs = ctypes.c_int32(), ctypes.c_int32()
+        N.check(N.lib().es_session_geometry(h, ctypes.byref(nc), ctypes.byref(ppc),
+                                            ctypes.byref(luts), ctypes.byref(regs)))
+        self.n_chunks = nc.value
+        self.patterns_per_chunk = ppc.value
+        self.num_luts = luts.value
+        self.regs_per_thread = regs.value
+
+    def launch(self, stream: int, best_ptr: int, chunk_begin: int, chunk_end: int,
+               rank: int = 0, world: int = 1) -> None:
+        N.check(N.lib().es_session_launch(self._h, ctypes.c_void_p(stream), ctypes.c_void_p(best_ptr),
+                                          chunk_begin, chunk_end, rank, world))
+
+    def close(self) -> None:
+        if self._h:
+            N.lib().es_session_close(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def rank_chunks(chunk_begin: int, chunk_end: int, rank: int, world: int) -> range:
+    """Chunks one rank sweeps in a launch over [chunk_begin, chunk_end):
+    its residue class mod world.  Mirrors session_launch (es_runtime.cu)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad shard")
+    first = chunk_begin + (rank - chunk_begin % world) % world
+    return range(first, chunk_end, world)
+
+
+def slice_bounds(n_chunks: int, slices: int) -> list[int]:
+    """Launch-slice boundaries; a MIN all-reduce follows every slice."""
+    s = max(1, min(slices, n_chunks))
+    return [n_chunks * i // s for i in range(s + 1)]
+
+
+def sharded_loop(n_chunks: int, slices: int, launch, reduce) -> int:
+    """The rank-side schedule of a sharded sweep: launch a slice, reduce the
+    minimum across ranks, repeat.  Returns the number of slices."""
+    b = slice_bounds(n_chunks, slices)
+    for i in range(len(b) - 1):
+        launch(b[i], b[i + 1])
+        reduce()
+    return len(b) - 1
+
+
+_sessions: dict[tuple[int, int], Session] = {}
+
+
+def session_for(prog, device: int) -> Session:
+    p = as_program(prog)
+    key = (hash(bytes(p.op) + bytes(p.dst) + bytes(p.src0) + bytes(p.src1) + bytes(p.neg0)
+                + bytes(p.neg1) + bytes(p.pi)) ^ p.num_pis, device)
+    s = _sessions.get(key)
+    if s is None:
+        s = _sessions[key] = Session(p, device)
+    return s
+
+
+def sweep_sharded(prog, group=None, device: int | None = None, slices: int | None = None,
+                  best=None) -> EsResult:
+    """run_exhaustive sharded over the ranks of ``group`` (collective call).
+
+    Every rank must call it with the same program.  ``slices`` launch slices
+    separate the MIN all-reduces (early-termination granularity); default 1
+    on a single rank, 8 otherwise.  Returns the same EsResult on every rank.
+    """
+    import torch
+    import torch.distributed as dist
+
+    p = as_program(prog)
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    rank = dist.get_rank(group) if world > 1 else 0
+    dev = torch.cuda.current_device() if device is None else device
+    last = len(p) - 1
+    if p.src0[last] < 0:  # constant rail, es.py:265-270
+        if p.neg0[last]:
+            return EsResult(ES_COUNTEREXAMPLE, (0,) * p.num_pis, 0, 0)
+        return EsResult(EXHAUSTED_ZERO, None, 1 << p.num_pis)
+    sess = session_for(p, dev)
+    sentinel = 1 << p.num_pis
+    if best is None:
+        best = torch.empty(1, dtype=torch.int64, device=f"cuda:{dev}")
+    best.fill_(sentinel)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    S = slices or (1 if world == 1 else 8)
+
+    def launch(lo: int, hi: int) -> None:
+        sess.launch(stream, best.data_ptr(), lo, hi, rank, world)
+
+    def reduce() -> None:
+        if world > 1:
+            dist.all_reduce(best, op=dist.ReduceOp.MIN, group=group)
+
+    sharded_loop(sess.n_chunks, S, launch, reduce)
+    b = int(best.item())
+    if b < sentinel:
+        lo = min(p.num_pis, 14)
+        return EsResult(ES_COUNTEREXAMPLE, tuple((b >> i) & 1 for i in range(p.num_pis)),
+                        ((b >> lo) + 1) << lo, b)
+    return EsResult(EXHAUSTED_ZERO, None, sentinel)
+
+
+def alu_peak(device: int = 0) -> tuple[float, float]:
+    """Measured lane-LOP3/s of the device (and the microbenchmark's ms)."""
+    v, ms = ctypes.c_double(), ctypes.c_double()
+    N.check(N.lib().es_alu_peak(device, ctypes.byref(v), ctypes.byref(ms)))
+    return v.value, ms.value
+
+
+def es_check_sharded(sm, group=None, device: int | None = None,
+                     slices: int | None = None):
+    """``es_check`` (es.py:342-365) with the sweep sharded over ``group``."""
+    import time
+
+    from .es import TooManyInputs, compile_program
+    from .miter import evaluate
+    from .verdict import COUNTEREXAMPLE, EQUIVALENT, UNKNOWN, CheckResult
+
+    t0 = time.monotonic()
+    try:
+        prog = compile_program(sm.circuit)
+    except TooManyInputs:
+        return CheckResult(UNKNOWN, reason="ineligible", engine="es")
+    r = sweep_sharded(prog, group, device, slices)
+    stats = {"patterns": r.patterns_evaluated, "registers": prog.num_registers,
+             "wall_time": time.monotonic() - t0}
+    if r.verdict == EXHAUSTED_ZERO:
+        return CheckResult(EQUIVALENT, engine="es", stats=stats)
+    if evaluate(sm.circuit, r.witness) != 1:
+        raise AssertionError("exhaustive-simulation witness failed re-check")
+    return CheckResult(COUNTEREXAMPLE, witness=r.witness, engine="es", stats=stats)

@@ -1,0 +1,34 @@
+"""K1 JIT on the CPU: spliced PTX compiles to sm_100a SASS in process, with
+no spills, for every configuration miter (no GPU needed)."""
+import pytest
+
+from paper_2512_06627_b200 import es
+from paper_2512_06627_b200 import miter as M
+
+
+@pytest.mark.parametrize("name,x", [
+    ("adder8", M.gen_adder_miter(8)),
+    ("mult12", M.gen_multiplier_miter(12, "array", "wallace")),
+    ("mult16", M.gen_multiplier_miter(16, "array", "booth")),
+    ("mult16_fault", M.flip_gate(M.gen_multiplier_miter(16, "array", "booth"), 1953)),
+])
+def test_jit_compiles_without_spills(name, x):
+    j = es.jit_check(es.compile_program(x), block_threads=128)
+    assert j["cubin_bytes"] > 0
+    assert 0 < j["regs"] <= 255
+    assert j["spill_bytes"] == 0, j["log"]
+
+
+def test_ptx_has_one_body_and_lop3():
+    p = es.compile_program(M.gen_multiplier_miter(6, "array", "booth"))
+    ptx = es.emit_ptx(p, 256)
+    assert ".entry es_k1" in ptx and ".target sm_100a" in ptx
+    assert ptx.count("lop3.b32") == es.map_stats(p)["luts"]
+    assert "ES_BODY" not in ptx
+    assert "atom.global.min.u64" in ptx
+
+
+def test_unsupported_block_size():
+    p = es.compile_program(M.gen_multiplier_miter(3, "array", "diagonal"))
+    with pytest.raises(Exception):
+        es.emit_ptx(p, 96)
