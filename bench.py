@@ -74,6 +74,74 @@ class _Sub:
         self.id = 0
 
 
+def cones_work(batch, results) -> tuple[int, int, int]:
+    """(gate-patterns, EQ count, NEQ count) of one batched verdict."""
+    work = eq = neq = 0
+    for i, r in enumerate(results):
+        if r is None:
+            continue
+        inf = batch.info(i)
+        pats = (1 << inf["num_pis"]) if r.witness_index is None else r.patterns_evaluated
+        work += inf["G"] * pats
+        eq += r.witness_index is None
+        neq += r.witness_index is not None
+    return work, eq, neq
+
+
+def measure_cones(steps: int, warmup: int, rank: int = 0, world: int = 1, count: int = 10_000):
+    """Config 4: one batched ES verdict over ~10k candidate-pair cones.
+    Device time = the library's CUDA events around the kernel slices (inputs
+    resident); e2e = NativeBatch.run wall time (program upload + results)."""
+    from paper_2512_06627_b200 import cones
+
+    t = time.perf_counter()
+    batch = cones.config4_batch(count)
+    host_ms = 1e3 * (time.perf_counter() - t)
+    if world > 1:
+        batch.select(list(range(rank, len(batch), world)))
+    for _ in range(warmup):
+        res = batch.run()
+    dev_ms, wall_ms = [], []
+    for _ in range(steps):
+        t = time.perf_counter()
+        res = batch.run()
+        wall_ms.append(1e3 * (time.perf_counter() - t))
+        dev_ms.append(max(r.stats["device_ms"] for r in res if r is not None))
+    work, eq, neq = cones_work(batch, res)
+    return {"jobs": len(batch), "eq": eq, "neq": neq, "gate_patterns": work,
+            "device_ms": statistics.mean(dev_ms), "e2e_ms": statistics.mean(wall_ms),
+            "extract_compile_ms": host_ms, "value": work / (statistics.mean(dev_ms) * 1e-3),
+            "e2e_value": work / (statistics.mean(wall_ms) * 1e-3)}
+
+
+def measure_other_configs(local: int) -> dict:
+    """Short warm measurements of the other BASELINE.json configs on 1 GPU."""
+    from paper_2512_06627_b200 import es
+
+    out = {}
+    for name in ("adder8", "mult12", "mult16_neq"):
+        x, desc = build_workload(name)
+        t = time.perf_counter()
+        p = es.compile_program(x)
+        cold = es.run_exhaustive(p, engine="auto", device=local)
+        cold_ms = 1e3 * (time.perf_counter() - t)
+        devs, walls = [], []
+        for _ in range(10):
+            t = time.perf_counter()
+            r = es.es_check(_Sub(x), engine="auto", device=local)
+            walls.append(1e3 * (time.perf_counter() - t))
+            devs.append(r.stats["device_ms"])
+        pats = (1 << x.num_pis) if r.verdict == "EQUIVALENT" else r.stats["patterns"]
+        dev = statistics.median(devs)
+        out[name] = {"workload": desc, "verdict": r.verdict,
+                     "witness_index": None if r.witness is None else
+                     sum(b << i for i, b in enumerate(r.witness)),
+                     "engine": r.stats["engine"], "device_ms": dev,
+                     "e2e_ms": statistics.median(walls), "cold_ms": cold_ms,
+                     "gate_patterns_per_s": p.num_gates * pats / (dev * 1e-3)}
+    return out
+
+
 # --- clocks ----------------------------------------------------------------
 
 class ClockSampler:
@@ -223,6 +291,9 @@ def run_b200(args) -> None:
 
     from paper_2512_06627_b200 import es, shard
 
+    if args.config == "cones":
+        run_cones(args, rank, world, local, dev)
+        return
     x, desc = build_workload(args.config)
     sm = _Sub(x)
     P = x.num_pis
@@ -371,6 +442,47 @@ def run_b200(args) -> None:
         }
         if cpu is not None:
             line["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        if world == 1 and not args.no_extras:
+            extras = measure_other_configs(local)
+            extras["cones"] = {"workload": "config 4: ~10k candidate-pair cones (14-24 PIs) of "
+                                           "16x16 multiplier miters, one batched launch",
+                               **measure_cones(5, 2)}
+            line["other_configs"] = extras
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_cones(args, rank, world, local, dev) -> None:
+    """Config 4 as the headline workload (--config cones)."""
+    import torch
+    import torch.distributed as dist
+
+    with ClockSampler(local) as clk:
+        m = measure_cones(args.steps, args.warmup, rank, world)
+    t = torch.tensor([m["device_ms"], m["e2e_ms"]], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        w = torch.tensor([m["gate_patterns"]], dtype=torch.float64, device=dev)
+        dist.all_reduce(w)
+        work = float(w.item())
+    else:
+        work = m["gate_patterns"]
+    dev_ms, e2e_ms = float(t[0]), float(t[1])
+    if rank == 0:
+        line = {"metric": METRIC, "value": work / (dev_ms * 1e-3), "unit": UNIT,
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": dev_ms, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "u32 (bit-parallel words)", "data": "synthetic",
+                "config": {"workload": "config 4: ~10k candidate-pair cones (14-24 PIs) of 16x16 "
+                                       "multiplier miters, batched K2 launch",
+                           "jobs_rank0": m["jobs"], "eq_rank0": m["eq"], "neq_rank0": m["neq"],
+                           "extract_compile_ms": m["extract_compile_ms"],
+                           "parallelism": f"jobs dealt round-robin over {world} GPU(s)"},
+                "e2e": {"value": work / (e2e_ms * 1e-3), "unit": UNIT,
+                        "ms_per_step": e2e_ms, "h2d_bytes_per_step": None,
+                        "d2h_bytes_per_step": None},
+                "gpu_launches": args.steps * world, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -386,6 +498,7 @@ def main() -> None:
     ap.add_argument("--slices", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-extras", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

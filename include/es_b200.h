@@ -41,6 +41,7 @@ extern "C" {
 #define ES_E_BAD_PROGRAM (-3)     /* malformed program or graph */
 #define ES_E_BAD_ARG (-4)         /* e.g. workers < 1 (es.py:260-261) */
 #define ES_E_NO_DEVICE (-5)       /* no CUDA device visible */
+#define ES_E_WITNESS (-6)         /* witness failed re-check (es.py:360-361 AssertionError) */
 
 /* EsResult.verdict (es.py:34-36) */
 #define ES_EXHAUSTED_ZERO 0
@@ -150,6 +151,33 @@ int32_t es_session_launch(es_session *s, void *stream, uint64_t *best_dev,
                           uint64_t chunk_begin, uint64_t chunk_end, int32_t rank,
                           int32_t world);
 void es_session_close(es_session *s);
+
+/*
+ * Sub-miter batches: extract the cone-local miter
+ * of each candidate pair of a parent XAG exactly as extract_submiter does
+ * (sweep.py:92-158; merges = the sweep's proven-node map, node -> packed
+ * literal), compile each with the reference schedule (es.py:87-163), on
+ * n_threads host threads (0 = all), then run them all in one batched device
+ * sweep.  es_batch_run re-checks every witness on its sub-miter (es.py:360)
+ * and returns ES_E_WITNESS on a mismatch.  Jobs over 40 PIs report
+ * verdict ES_BUDGET_EXCEEDED with reason -1 (ineligible, es.py:350-351).
+ */
+typedef struct es_batch es_batch;
+int32_t es_batch_extract(int32_t num_pis, int32_t num_gates, const uint8_t *kind,
+                         const uint32_t *in0, const uint32_t *in1, int32_t n_merges,
+                         const int32_t *merge_node, const uint32_t *merge_lit, int32_t n_pairs,
+                         const int32_t *a, const int32_t *b, const uint8_t *polarity,
+                         int32_t n_threads, es_batch **out);
+int32_t es_batch_size(const es_batch *b);
+int32_t es_batch_info(const es_batch *b, int32_t i, int32_t *num_pis, int32_t *num_gates,
+                      uint64_t *hash, int32_t *num_instrs, int32_t *num_registers, int32_t *G);
+int32_t es_batch_xag(const es_batch *b, int32_t i, uint8_t *kind, uint32_t *in0, uint32_t *in1,
+                     uint32_t *out_lit, int32_t *pi_map);
+int32_t es_batch_select(es_batch *b, int32_t n, const int32_t *idx);
+int32_t es_batch_run(es_batch *b, const es_run_opts *opts, es_result *outs);
+/* Move every sub-miter of src to the end of dst (src becomes empty). */
+int32_t es_batch_merge(es_batch *dst, es_batch *src);
+void es_batch_free(es_batch *b);
 
 /* Engine-internal views for tests and profiling. */
 /* LUT-3 mapping statistics of a program: LOP3s per word, schedule peak live. */

@@ -21,6 +21,7 @@ ES_E_CUDA = -2
 ES_E_BAD_PROGRAM = -3
 ES_E_BAD_ARG = -4
 ES_E_NO_DEVICE = -5
+ES_E_WITNESS = -6
 
 ENGINE_AUTO, ENGINE_JIT, ENGINE_INTERP = 0, 1, 2
 ENGINES = {"auto": ENGINE_AUTO, "jit": ENGINE_JIT, "interp": ENGINE_INTERP}
@@ -28,8 +29,9 @@ ENGINES = {"auto": ENGINE_AUTO, "jit": ENGINE_JIT, "interp": ENGINE_INTERP}
 # every symbol include/es_b200.h declares
 EXPORTS = ("es_compile", "es_run", "es_run_batch", "es_session_open", "es_session_geometry",
            "es_session_launch", "es_session_close", "es_map_stats", "es_map_eval",
-           "es_emit_ptx", "es_jit_check", "es_alu_peak", "es_last_error", "es_version",
-           "es_shutdown")
+           "es_emit_ptx", "es_jit_check", "es_alu_peak", "es_batch_extract", "es_batch_size",
+           "es_batch_info", "es_batch_xag", "es_batch_select", "es_batch_run", "es_batch_merge", "es_batch_free",
+           "es_last_error", "es_version", "es_shutdown")
 
 _P = ctypes.c_void_p
 
@@ -116,6 +118,24 @@ def lib():
         L.es_alu_peak.argtypes = [ctypes.c_int32, ctypes.POINTER(ctypes.c_double),
                                   ctypes.POINTER(ctypes.c_double)]
         L.es_alu_peak.restype = ctypes.c_int32
+        L.es_batch_extract.argtypes = [ctypes.c_int32, ctypes.c_int32, _P, _P, _P, ctypes.c_int32,
+                                       _P, _P, ctypes.c_int32, _P, _P, _P, ctypes.c_int32,
+                                       ctypes.POINTER(_P)]
+        L.es_batch_extract.restype = ctypes.c_int32
+        L.es_batch_size.argtypes = [_P]
+        L.es_batch_size.restype = ctypes.c_int32
+        L.es_batch_info.argtypes = [_P, ctypes.c_int32, _P, _P, _P, _P, _P, _P]
+        L.es_batch_info.restype = ctypes.c_int32
+        L.es_batch_xag.argtypes = [_P, ctypes.c_int32, _P, _P, _P, _P, _P]
+        L.es_batch_xag.restype = ctypes.c_int32
+        L.es_batch_select.argtypes = [_P, ctypes.c_int32, _P]
+        L.es_batch_select.restype = ctypes.c_int32
+        L.es_batch_run.argtypes = [_P, ctypes.POINTER(EsRunOpts), ctypes.POINTER(EsResult)]
+        L.es_batch_run.restype = ctypes.c_int32
+        L.es_batch_merge.argtypes = [_P, _P]
+        L.es_batch_merge.restype = ctypes.c_int32
+        L.es_batch_free.argtypes = [_P]
+        L.es_batch_free.restype = None
         L.es_last_error.argtypes = []
         L.es_last_error.restype = ctypes.c_char_p
         L.es_version.argtypes = []

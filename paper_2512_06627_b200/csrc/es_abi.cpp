@@ -4,6 +4,7 @@
 #include <vector>
 
 #include "es_core.h"
+#include "es_extract.h"
 #include "es_jit.h"
 
 namespace es {
@@ -30,6 +31,10 @@ static int map_prog(const es_prog *prog, LutNet *net) {
     map_luts(dag, net);
     return ES_OK;
 }
+
+struct Batch {
+    std::vector<SubMiterC> subs;
+};
 
 }  // namespace es
 
@@ -145,6 +150,103 @@ int32_t es_alu_peak(int32_t device, double *lane_ops_per_s, double *ms) {
     if (!lane_ops_per_s) return ES_E_BAD_ARG;
     return alu_peak(device, lane_ops_per_s, ms);
 }
+
+int32_t es_batch_extract(int32_t num_pis, int32_t num_gates, const uint8_t *kind,
+                         const uint32_t *in0, const uint32_t *in1, int32_t n_merges,
+                         const int32_t *merge_node, const uint32_t *merge_lit, int32_t n_pairs,
+                         const int32_t *a, const int32_t *b, const uint8_t *polarity,
+                         int32_t n_threads, es_batch **out) {
+    if (!out || n_pairs < 0 || num_pis < 0 || num_gates < 0) { set_error("bad argument"); return ES_E_BAD_ARG; }
+    Batch *bt = new Batch();
+    std::string err;
+    int rc = extract_compile(num_pis, num_gates, kind, in0, in1, n_merges, merge_node, merge_lit,
+                             n_pairs, a, b, polarity, n_threads, &bt->subs, &err);
+    if (rc != ES_OK) { set_error(err); delete bt; return rc; }
+    *out = (es_batch *)bt;
+    return ES_OK;
+}
+
+int32_t es_batch_size(const es_batch *bp) { return bp ? (int32_t)((const Batch *)bp)->subs.size() : ES_E_BAD_ARG; }
+
+int32_t es_batch_info(const es_batch *bp, int32_t i, int32_t *num_pis, int32_t *num_gates,
+                      uint64_t *hash, int32_t *num_instrs, int32_t *num_registers, int32_t *G) {
+    const Batch *bt = (const Batch *)bp;
+    if (!bt || i < 0 || i >= (int32_t)bt->subs.size()) { set_error("index out of range"); return ES_E_BAD_ARG; }
+    const SubMiterC &s = bt->subs[i];
+    if (num_pis) *num_pis = s.num_pis;
+    if (num_gates) *num_gates = (int32_t)s.kind.size();
+    if (hash) *hash = s.hash;
+    if (num_instrs) *num_instrs = s.too_many_inputs ? 0 : (int32_t)s.op.size();
+    if (num_registers) *num_registers = s.num_registers;
+    if (G) {
+        int g = 0;
+        for (int8_t o : s.op) g += (o == ES_OP_AND || o == ES_OP_XOR);
+        *G = g;
+    }
+    return s.too_many_inputs ? ES_E_TOO_MANY_INPUTS : ES_OK;
+}
+
+int32_t es_batch_xag(const es_batch *bp, int32_t i, uint8_t *kind, uint32_t *in0, uint32_t *in1,
+                     uint32_t *out_lit, int32_t *pi_map) {
+    const Batch *bt = (const Batch *)bp;
+    if (!bt || i < 0 || i >= (int32_t)bt->subs.size()) { set_error("index out of range"); return ES_E_BAD_ARG; }
+    const SubMiterC &s = bt->subs[i];
+    if (kind) std::memcpy(kind, s.kind.data(), s.kind.size());
+    if (in0) std::memcpy(in0, s.in0.data(), 4 * s.in0.size());
+    if (in1) std::memcpy(in1, s.in1.data(), 4 * s.in1.size());
+    if (out_lit) *out_lit = s.out_lit;
+    if (pi_map) std::memcpy(pi_map, s.pi_map.data(), 4 * s.pi_map.size());
+    return ES_OK;
+}
+
+int32_t es_batch_select(es_batch *bp, int32_t n, const int32_t *idx) {
+    Batch *bt = (Batch *)bp;
+    if (!bt || n < 0) { set_error("bad argument"); return ES_E_BAD_ARG; }
+    std::vector<SubMiterC> keep;
+    keep.reserve(n);
+    for (int k = 0; k < n; ++k) {
+        if (idx[k] < 0 || idx[k] >= (int32_t)bt->subs.size()) { set_error("index out of range"); return ES_E_BAD_ARG; }
+        keep.push_back(bt->subs[idx[k]]);
+    }
+    bt->subs.swap(keep);
+    return ES_OK;
+}
+
+int32_t es_batch_run(es_batch *bp, const es_run_opts *opts, es_result *outs) {
+    Batch *bt = (Batch *)bp;
+    if (!bt || !outs) { set_error("bad argument"); return ES_E_BAD_ARG; }
+    const int n = (int)bt->subs.size();
+    std::vector<es_prog> progs;
+    std::vector<int> where;
+    for (int i = 0; i < n; ++i) {
+        std::memset(&outs[i], 0, sizeof(es_result));
+        if (bt->subs[i].too_many_inputs) { outs[i].verdict = ES_BUDGET_EXCEEDED; outs[i].reason = -1; continue; }
+        progs.push_back(bt->subs[i].view());
+        where.push_back(i);
+    }
+    std::vector<es_result> rs(progs.size());
+    int rc = run_batch((int)progs.size(), progs.data(), opts, rs.data());
+    if (rc != ES_OK) return rc;
+    for (size_t k = 0; k < where.size(); ++k) {
+        outs[where[k]] = rs[k];
+        if (rs[k].verdict == ES_COUNTEREXAMPLE &&
+            evaluate_sub(bt->subs[where[k]], rs[k].witness_index) != 1) {
+            set_error("exhaustive-simulation witness failed re-check (job " + std::to_string(where[k]) + ")");
+            return ES_E_WITNESS;
+        }
+    }
+    return ES_OK;
+}
+
+int32_t es_batch_merge(es_batch *dst, es_batch *src) {
+    Batch *d = (Batch *)dst, *s = (Batch *)src;
+    if (!d || !s || d == s) { set_error("bad argument"); return ES_E_BAD_ARG; }
+    for (auto &x : s->subs) d->subs.push_back(std::move(x));
+    s->subs.clear();
+    return ES_OK;
+}
+
+void es_batch_free(es_batch *bp) { delete (Batch *)bp; }
 
 const char *es_last_error(void) { return t_err.c_str(); }
 

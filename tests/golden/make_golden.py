@@ -87,9 +87,34 @@ def row(x, ref_x=None, full_program=False, workers=1):
     return out
 
 
+def cone_rows(limit: int = 240):
+    """Config-4 fixtures: sub-miters cut by the REFERENCE's extract_submiter
+    (sweep.py:92-158) for candidate pairs of the array-vs-Booth 16x16 miter."""
+    from cecprove import sweep as ref_sweep
+    from paper_2512_06627_b200 import cones
+
+    m, pairs = next(cones.config4_pairs())
+    rm = to_ref(m)
+    rows = []
+    for k, (a, b, pol) in enumerate(pairs[:limit]):
+        sm = ref_sweep.extract_submiter(rm, a, b, {}, polarity=pol, sm_id=k)
+        r = row(sm.circuit)
+        r.update({"pair": [a, b, int(pol)], "pi_map": list(sm.pi_map)})
+        rows.append(r)
+    return rows
+
+
 def main() -> None:
     t_start = time.monotonic()
     fixtures: dict[str, list] = {}
+    path = os.path.join(HERE, "golden.json")
+    if "--only-cones" in sys.argv:
+        doc = json.load(open(path))
+        doc["fixtures"]["cones"] = cone_rows()
+        with open(path, "w") as fh:
+            json.dump(doc, fh, separators=(",", ":"))
+        print(f"cones: {len(doc['fixtures']['cones'])} rows, {time.monotonic() - t_start:.1f}s")
+        return
 
     # 1. random XAG populations of the reference's own tests
     rand_rows = []
@@ -114,8 +139,9 @@ def main() -> None:
         print(f"  {spec['name']}: {r['verdict']} idx={r.get('witness_index')} "
               f"G={r.get('G')} {r.get('ref_seconds')}s", flush=True)
     fixtures["miters"] = miter_rows
+    fixtures["cones"] = cone_rows()
 
-    with open(os.path.join(HERE, "golden.json"), "w") as fh:
+    with open(path, "w") as fh:
         json.dump({"generator": "tests/golden/make_golden.py",
                    "reference": "cecprove (arxiv 2512.06627 package) es.py/eval.py",
                    "fixtures": fixtures}, fh, separators=(",", ":"))

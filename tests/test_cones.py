@@ -1,0 +1,101 @@
+"""Config 4: sub-miter extraction (C++ es_batch_extract and the Python
+mirror) against the reference's own extract_submiter (golden "cones" rows,
+generated with cecprove.sweep.extract_submiter), and the batched device
+sweep against the reference's run_exhaustive(workers=1) on those cones."""
+import pytest
+
+from paper_2512_06627_b200 import cones, es
+from tests.golden import recipes
+
+
+@pytest.fixture(scope="module")
+def round0():
+    m, pairs = next(cones.config4_pairs())
+    return m, pairs
+
+
+def test_cpp_extraction_matches_reference(golden, round0):
+    m, pairs = round0
+    rows = golden["cones"]
+    nb = cones.NativeBatch(m, [tuple(r["pair"]) for r in rows])
+    assert len(nb) == len(rows)
+    for i, g in enumerate(rows):
+        sm = nb.submiter(i)
+        assert recipes.xag_sha(sm.circuit) == g["xag_sha"], i
+        assert list(sm.pi_map) == g["pi_map"]
+        inf = nb.info(i)
+        assert inf["num_registers"] == g["num_registers"] and inf["G"] == g["G"]
+        p = es.compile_program(sm.circuit)
+        assert recipes.prog_sha(p.rows(), p.num_registers) == g["prog_sha"]
+
+
+def test_python_mirror_matches_reference(golden, round0):
+    m, _ = round0
+    for g in golden["cones"][:60]:
+        a, b, pol = g["pair"]
+        sm = cones.extract_submiter(m, a, b, polarity=bool(pol))
+        assert recipes.xag_sha(sm.circuit) == g["xag_sha"]
+        assert list(sm.pi_map) == g["pi_map"]
+
+
+def test_pairs_are_in_range_and_deterministic(round0):
+    m, pairs = round0
+    m2, pairs2 = next(cones.config4_pairs())
+    assert pairs[:50] == pairs2[:50]
+    nb = cones.NativeBatch(m, pairs[:200])
+    for i in range(len(nb)):
+        assert 14 <= nb.info(i)["num_pis"] <= 24
+
+
+def test_config4_workload_shape():
+    b = cones.config4_batch(1500)
+    assert len(b) == 1500
+    hs = {b.info(i)["hash"] for i in range(len(b))}
+    assert len(hs) == 1500
+
+
+def test_merges_collapse_nodes(round0):
+    """A merge map (proven node -> earlier representative) is honoured like
+    sweep.py:84-89: extracting (a, b) with the later node merged onto the
+    earlier one is constant; a cyclic map fails loudly, not by crashing."""
+    from paper_2512_06627_b200 import _native as N
+    from paper_2512_06627_b200.xag import Lit
+    m, pairs = round0
+    a, b, pol = pairs[0]
+    lo, hi = min(a, b), max(a, b)
+    nb = cones.NativeBatch(m, [(a, b, pol)], merges={hi: Lit(lo, pol)})
+    sm = nb.submiter(0)
+    py = cones.extract_submiter(m, a, b, merges={hi: Lit(lo, pol)}, polarity=pol)
+    assert recipes.xag_sha(sm.circuit) == recipes.xag_sha(py.circuit)
+    assert sm.circuit.outputs[0].node == 0
+    # other pairs keep extracting identically under a merge map
+    extra = pairs[1:40]
+    nb = cones.NativeBatch(m, extra, merges={hi: Lit(lo, pol)})
+    for i, (x, y, q) in enumerate(extra):
+        try:
+            py = cones.extract_submiter(m, x, y, merges={hi: Lit(lo, pol)}, polarity=q)
+        except KeyError:
+            continue
+        assert recipes.xag_sha(nb.submiter(i).circuit) == recipes.xag_sha(py.circuit)
+
+
+@pytest.mark.gpu
+def test_batched_sweep_matches_reference(golden, round0, gpu):
+    m, _ = round0
+    rows = golden["cones"]
+    nb = cones.NativeBatch(m, [tuple(r["pair"]) for r in rows])
+    res = nb.run()
+    for g, r in zip(rows, res):
+        assert r.verdict == g["verdict"]
+        assert r.witness_index == g["witness_index"]
+        assert r.patterns_evaluated == g["patterns_evaluated"]
+
+
+@pytest.mark.gpu
+def test_config4_batch_vs_single_runs(gpu):
+    b = cones.config4_batch(600)
+    res = b.run()
+    for i in range(0, 600, 20):
+        sm = b.submiter(i)
+        r = es.run_exhaustive(es.compile_program(sm.circuit), engine="jit")
+        assert (r.verdict, r.witness_index) == (res[i].verdict, res[i].witness_index), i
