@@ -77,12 +77,12 @@ class _Sub:
 def cones_work(batch, results) -> tuple[int, int, int]:
     """(gate-patterns, EQ count, NEQ count) of one batched verdict."""
     work = eq = neq = 0
+    tab = batch.table()
     for i, r in enumerate(results):
         if r is None:
             continue
-        inf = batch.info(i)
-        pats = (1 << inf["num_pis"]) if r.witness_index is None else r.patterns_evaluated
-        work += inf["G"] * pats
+        pats = (1 << int(tab["num_pis"][i])) if r.witness_index is None else r.patterns_evaluated
+        work += int(tab["G"][i]) * pats
         eq += r.witness_index is None
         neq += r.witness_index is not None
     return work, eq, neq

@@ -171,6 +171,9 @@ int32_t es_batch_extract(int32_t num_pis, int32_t num_gates, const uint8_t *kind
 int32_t es_batch_size(const es_batch *b);
 int32_t es_batch_info(const es_batch *b, int32_t i, int32_t *num_pis, int32_t *num_gates,
                       uint64_t *hash, int32_t *num_instrs, int32_t *num_registers, int32_t *G);
+/* Per-job arrays for the whole batch (each may be NULL). */
+int32_t es_batch_table(const es_batch *b, int32_t *num_pis, int32_t *num_gates, int32_t *G,
+                       uint64_t *hash);
 int32_t es_batch_xag(const es_batch *b, int32_t i, uint8_t *kind, uint32_t *in0, uint32_t *in1,
                      uint32_t *out_lit, int32_t *pi_map);
 int32_t es_batch_select(es_batch *b, int32_t n, const int32_t *idx);
@@ -187,6 +190,12 @@ int32_t es_map_stats(const es_prog *prog, int32_t *num_luts, int32_t *peak_live,
  * (32 patterns per word, the kernel's layout): writes the output words.
  * Lets GPU-less CI check the mapper bit-exactly. */
 int32_t es_map_eval(const es_prog *prog, uint64_t w0, uint64_t nw, uint32_t *out_words);
+/* K2 interpreter program of `prog`: gates, slots (PI + recycled), stores
+ * issued and operands forwarded from the accumulator. */
+int32_t es_k2_stats(const es_prog *prog, int32_t *num_gates, int32_t *num_slots,
+                    int32_t *stores, int32_t *acc_reads);
+/* CPU model of the K2 program over words [w0, w0+nw) (bit-exact with K2). */
+int32_t es_k2_eval(const es_prog *prog, uint64_t w0, uint64_t nw, uint32_t *out_words);
 /* The PTX the JIT path would compile for `prog` (buf NULL -> returns size). */
 int64_t es_emit_ptx(const es_prog *prog, int32_t block_threads, char *buf, int64_t cap);
 /* Compile PTX to SASS without a GPU (build-time check); returns cubin bytes or < 0. */

@@ -28,9 +28,9 @@ ENGINES = {"auto": ENGINE_AUTO, "jit": ENGINE_JIT, "interp": ENGINE_INTERP}
 
 # every symbol include/es_b200.h declares
 EXPORTS = ("es_compile", "es_run", "es_run_batch", "es_session_open", "es_session_geometry",
-           "es_session_launch", "es_session_close", "es_map_stats", "es_map_eval",
+           "es_session_launch", "es_session_close", "es_map_stats", "es_map_eval", "es_k2_stats", "es_k2_eval",
            "es_emit_ptx", "es_jit_check", "es_alu_peak", "es_batch_extract", "es_batch_size",
-           "es_batch_info", "es_batch_xag", "es_batch_select", "es_batch_run", "es_batch_merge", "es_batch_free",
+           "es_batch_info", "es_batch_table", "es_batch_xag", "es_batch_select", "es_batch_run", "es_batch_merge", "es_batch_free",
            "es_last_error", "es_version", "es_shutdown")
 
 _P = ctypes.c_void_p
@@ -108,6 +108,10 @@ def lib():
         L.es_map_stats.restype = ctypes.c_int32
         L.es_map_eval.argtypes = [ctypes.POINTER(EsProg), ctypes.c_uint64, ctypes.c_uint64, _P]
         L.es_map_eval.restype = ctypes.c_int32
+        L.es_k2_stats.argtypes = [ctypes.POINTER(EsProg), _P, _P, _P, _P]
+        L.es_k2_stats.restype = ctypes.c_int32
+        L.es_k2_eval.argtypes = [ctypes.POINTER(EsProg), ctypes.c_uint64, ctypes.c_uint64, _P]
+        L.es_k2_eval.restype = ctypes.c_int32
         L.es_emit_ptx.argtypes = [ctypes.POINTER(EsProg), ctypes.c_int32, ctypes.c_char_p,
                                   ctypes.c_int64]
         L.es_emit_ptx.restype = ctypes.c_int64
@@ -126,6 +130,8 @@ def lib():
         L.es_batch_size.restype = ctypes.c_int32
         L.es_batch_info.argtypes = [_P, ctypes.c_int32, _P, _P, _P, _P, _P, _P]
         L.es_batch_info.restype = ctypes.c_int32
+        L.es_batch_table.argtypes = [_P, _P, _P, _P, _P]
+        L.es_batch_table.restype = ctypes.c_int32
         L.es_batch_xag.argtypes = [_P, ctypes.c_int32, _P, _P, _P, _P, _P]
         L.es_batch_xag.restype = ctypes.c_int32
         L.es_batch_select.argtypes = [_P, ctypes.c_int32, _P]

@@ -186,6 +186,16 @@ class NativeBatch:
                 "num_instrs": v[2].value, "num_registers": v[3].value, "G": v[4].value,
                 "eligible": rc == 0}
 
+    def table(self) -> dict:
+        """Per-job arrays: num_pis, num_gates, G, hash."""
+        n = len(self)
+        out = {"num_pis": np.zeros(n, np.int32), "num_gates": np.zeros(n, np.int32),
+               "G": np.zeros(n, np.int32), "hash": np.zeros(n, np.uint64)}
+        N.check(N.lib().es_batch_table(self._h, out["num_pis"].ctypes.data,
+                                       out["num_gates"].ctypes.data, out["G"].ctypes.data,
+                                       out["hash"].ctypes.data))
+        return out
+
     def submiter(self, i: int) -> SubMiter:
         inf = self.info(i)
         ng, n = inf["num_gates"], inf["num_pis"]
@@ -218,13 +228,9 @@ class NativeBatch:
         with _CancelWatcher(cancel) as cw:
             opts = _opts(device, "interp", budget, cw.address, 20.0, 0)
             N.check(N.lib().es_batch_run(self._h, ctypes.byref(opts), outs))
-        res = []
-        for i in range(n):
-            if outs[i].reason == -1:
-                res.append(None)  # ineligible (> 40 PIs)
-            else:
-                res.append(_to_esresult(outs[i], self.info(i)["num_pis"]))
-        return res
+        pis = self.table()["num_pis"]
+        return [None if outs[i].reason == -1 else _to_esresult(outs[i], int(pis[i]))
+                for i in range(n)]
 
     def extend(self, other: "NativeBatch") -> None:
         """Move all of ``other``'s sub-miters to the end of this batch."""
@@ -285,12 +291,13 @@ def config4_batches(count: int = 10_000, lo: int = 14, hi: int = 24, seed: int =
         if total >= count:
             break
         nb = NativeBatch(m, pairs, threads=threads)
+        tab = nb.table()
         keep = []
         for i in range(len(nb)):
-            inf = nb.info(i)
-            if not lo <= inf["num_pis"] <= hi or inf["hash"] in seen:
+            h = int(tab["hash"][i])
+            if not lo <= tab["num_pis"][i] <= hi or h in seen:
                 continue
-            seen.add(inf["hash"])
+            seen.add(h)
             keep.append(i)
             if total + len(keep) >= count:
                 break

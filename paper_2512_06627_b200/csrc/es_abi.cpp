@@ -6,6 +6,7 @@
 #include "es_core.h"
 #include "es_extract.h"
 #include "es_jit.h"
+#include "es_k2prog.h"
 
 namespace es {
 
@@ -104,6 +105,39 @@ int32_t es_map_eval(const es_prog *prog, uint64_t w0, uint64_t nw, uint32_t *out
     return ES_OK;
 }
 
+int32_t es_k2_stats(const es_prog *prog, int32_t *num_gates, int32_t *num_slots,
+                    int32_t *stores, int32_t *acc_reads) {
+    if (!prog || prog->num_instrs < 1) { set_error("empty program"); return ES_E_BAD_PROGRAM; }
+    Dag dag;
+    std::string err;
+    int rc = build_dag(*prog, &dag, &err);
+    if (rc != ES_OK) { set_error(err); return rc; }
+    K2Prog kp;
+    build_k2prog(dag, &kp);
+    int st = 0, acc = 0;
+    for (const K2Gate &g : kp.gates) {
+        st += (g.ctl & K2_STORE) != 0;
+        acc += ((g.ctl & K2_A_ACC) != 0) + ((g.ctl & K2_B_ACC) != 0);
+    }
+    if (num_gates) *num_gates = (int32_t)kp.gates.size();
+    if (num_slots) *num_slots = kp.num_slots;
+    if (stores) *stores = st;
+    if (acc_reads) *acc_reads = acc;
+    return ES_OK;
+}
+
+int32_t es_k2_eval(const es_prog *prog, uint64_t w0, uint64_t nw, uint32_t *out_words) {
+    if (!prog || prog->num_instrs < 1) { set_error("empty program"); return ES_E_BAD_PROGRAM; }
+    Dag dag;
+    std::string err;
+    int rc = build_dag(*prog, &dag, &err);
+    if (rc != ES_OK) { set_error(err); return rc; }
+    K2Prog kp;
+    build_k2prog(dag, &kp);
+    eval_k2prog(kp, w0, nw, out_words);
+    return ES_OK;
+}
+
 int64_t es_emit_ptx(const es_prog *prog, int32_t block_threads, char *buf, int64_t cap) {
     LutNet net;
     int rc = map_prog(prog, &net);
@@ -184,6 +218,24 @@ int32_t es_batch_info(const es_batch *bp, int32_t i, int32_t *num_pis, int32_t *
         *G = g;
     }
     return s.too_many_inputs ? ES_E_TOO_MANY_INPUTS : ES_OK;
+}
+
+int32_t es_batch_table(const es_batch *bp, int32_t *num_pis, int32_t *num_gates, int32_t *G,
+                       uint64_t *hash) {
+    const Batch *bt = (const Batch *)bp;
+    if (!bt) { set_error("bad argument"); return ES_E_BAD_ARG; }
+    for (size_t i = 0; i < bt->subs.size(); ++i) {
+        const SubMiterC &s = bt->subs[i];
+        if (num_pis) num_pis[i] = s.num_pis;
+        if (num_gates) num_gates[i] = (int32_t)s.kind.size();
+        if (G) {
+            int g = 0;
+            for (int8_t o : s.op) g += (o == ES_OP_AND || o == ES_OP_XOR);
+            G[i] = g;
+        }
+        if (hash) hash[i] = s.hash;
+    }
+    return ES_OK;
 }
 
 int32_t es_batch_xag(const es_batch *bp, int32_t i, uint8_t *kind, uint32_t *in0, uint32_t *in1,

@@ -11,6 +11,8 @@
 //   * patterns_evaluated follows the reference's workers=1 accounting
 //     (whole 2^min(n,14)-pattern batches up to and including the hit).
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -22,6 +24,7 @@
 
 #include "es_core.h"
 #include "es_jit.h"
+#include "es_k2prog.h"
 
 namespace es {
 
@@ -40,19 +43,20 @@ struct K1Params {
 };
 
 // ---------------------------------------------------------------------------
-// K2: shared-memory interpreter of the reference register program
+// K2: shared-memory interpreter (es_k2prog.cpp builds its programs)
 // ---------------------------------------------------------------------------
-// Instruction word (uint2): x = dst | op<<16 | neg0<<18 | neg1<<19 | pi<<20,
-// y = src0 | src1<<16.  Slots live in shared memory, slot r of thread t at
-// [r*T + t] (consecutive threads -> consecutive banks, conflict free).
+// Per CTA: the current job's program staged in shared memory (24-byte
+// records), then the slot file: slot s of thread t, word k at byte
+// s*T*W*4 + t*W*4 + k*4 -- every thread owns its columns, so the gate loop
+// needs no barrier, and each access is one W-wide vector (LDS.32/64/128).
 struct K2Job {
-    const uint2 *code;
+    const K2Gate *code;          // device image: a/b/d are byte offsets
     unsigned long long *best;
     unsigned long long total_words;
-    int n_instrs;
-    int num_regs;
+    int n_gates;
+    int num_pis;
     unsigned valid_mask;
-    int pad;
+    unsigned out_mask;
 };
 
 struct K2Item {
@@ -64,15 +68,41 @@ struct K2Item {
 __constant__ unsigned c_lane_mask[5] = {0xAAAAAAAAu, 0xCCCCCCCCu, 0xF0F0F0F0u, 0xFF00FF00u,
                                         0xFFFF0000u};
 
+template <int W> struct VecT;
+template <> struct VecT<1> { typedef unsigned type; };
+template <> struct VecT<2> { typedef uint2 type; };
+template <> struct VecT<4> { typedef uint4 type; };
+
+template <int W>
+__device__ __forceinline__ typename VecT<W>::type vload(const unsigned char *p) {
+    return *reinterpret_cast<const typename VecT<W>::type *>(p);
+}
+template <int W>
+__device__ __forceinline__ void vstore(unsigned char *p, const unsigned (&v)[W]) {
+    if constexpr (W == 1) *reinterpret_cast<unsigned *>(p) = v[0];
+    if constexpr (W == 2) *reinterpret_cast<uint2 *>(p) = make_uint2(v[0], v[1]);
+    if constexpr (W == 4) *reinterpret_cast<uint4 *>(p) = make_uint4(v[0], v[1], v[2], v[3]);
+}
+template <int W>
+__device__ __forceinline__ void unpack(const typename VecT<W>::type &x, unsigned (&v)[W]) {
+    if constexpr (W == 1) v[0] = x;
+    if constexpr (W == 2) { v[0] = x.x; v[1] = x.y; }
+    if constexpr (W == 4) { v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w; }
+}
+
+template <int W>
 __global__ void __launch_bounds__(128) es_k2(const K2Job *__restrict__ jobs,
                                              const K2Item *__restrict__ items,
                                              unsigned long long item_begin,
-                                             unsigned long long item_end,
-                                             unsigned *counter) {
-    extern __shared__ unsigned slots[];
+                                             unsigned long long item_end, unsigned *counter,
+                                             int prog_bytes) {
+    extern __shared__ __align__(16) unsigned char smem[];
     __shared__ unsigned long long s_item;
+    K2Gate *prog = reinterpret_cast<K2Gate *>(smem);
     const unsigned T = blockDim.x, t = threadIdx.x, lane = t & 31u;
+    unsigned char *mine = smem + prog_bytes + t * W * 4;
     const unsigned long long kStop = ~0ull, kSkip = ~0ull - 1;
+    int cur_job = -1;
     for (;;) {
         if (t == 0) {
             unsigned long long k = item_begin + atomicAdd(counter, 1u);
@@ -86,40 +116,78 @@ __global__ void __launch_bounds__(128) es_k2(const K2Job *__restrict__ jobs,
         }
         __syncthreads();
         const unsigned long long k = s_item;
-        __syncthreads();
         if (k == kStop) break;
-        if (k == kSkip) continue;
+        if (k == kSkip) { __syncthreads(); continue; }
         const K2Item it = items[k];
         const K2Job job = jobs[it.job];
-        for (unsigned base = 0; base < it.n_words; base += T) {
-            const unsigned long long w = it.w0 + base + t;
-            unsigned out = 0;
-            for (int i = 0; i < job.n_instrs; ++i) {
-                const uint2 ins = __ldg(&job.code[i]);
-                const unsigned op = (ins.x >> 16) & 3u;
-                const unsigned d = ins.x & 0xFFFFu;
-                const unsigned m0 = (ins.x & (1u << 18)) ? ~0u : 0u;
-                if (op == 0u) {  // LOAD_PI
-                    const int j = (int)(ins.x >> 20) - 1;
-                    const unsigned v = j < 5 ? c_lane_mask[j] : (((w >> (j - 5)) & 1ull) ? ~0u : 0u);
-                    slots[d * T + t] = v;
-                } else if (op == 3u) {  // OUTPUT
-                    out = (slots[(ins.y & 0xFFFFu) * T + t] ^ m0) & job.valid_mask;
-                    break;
-                } else {
-                    const unsigned m1 = (ins.x & (1u << 19)) ? ~0u : 0u;
-                    const unsigned a = slots[(ins.y & 0xFFFFu) * T + t] ^ m0;
-                    const unsigned b = slots[(ins.y >> 16) * T + t] ^ m1;
-                    slots[d * T + t] = op == 1u ? (a & b) : (a ^ b);
-                }
+        if (it.job != cur_job) {  // stage the program (uniform branch)
+            const uint2 *src = reinterpret_cast<const uint2 *>(job.code);
+            uint2 *dst = reinterpret_cast<uint2 *>(prog);
+            for (int q = t; q < job.n_gates * 3; q += T) dst[q] = __ldg(&src[q]);
+            cur_job = it.job;
+        }
+        __syncthreads();
+        for (unsigned base = 0; base < it.n_words; base += T * W) {
+            const unsigned long long w = it.w0 + base + (unsigned long long)t * W;
+            // PI words into slots 0..n-1
+            for (int j = 0; j < job.num_pis; ++j) {
+                unsigned v[W];
+#pragma unroll
+                for (int q = 0; q < W; ++q)
+                    v[q] = j < 5 ? c_lane_mask[j] : ((((w + q) >> (j - 5)) & 1ull) ? ~0u : 0u);
+                vstore<W>(mine + (unsigned)j * T * W * 4, v);
             }
-            if (w >= job.total_words || base + t >= it.n_words) out = 0;
-            const unsigned hit = __ballot_sync(0xffffffffu, out != 0u);
+            unsigned acc[W];
+#pragma unroll
+            for (int q = 0; q < W; ++q) acc[q] = 0;
+#pragma unroll 2
+            for (int i = 0; i < job.n_gates; ++i) {
+                const K2Gate g = prog[i];
+                unsigned a[W], b[W], r[W];
+                if (g.ctl & 2u) {
+#pragma unroll
+                    for (int q = 0; q < W; ++q) a[q] = acc[q];
+                } else {
+                    unpack<W>(vload<W>(mine + g.a), a);
+                }
+                if (g.ctl & 4u) {
+#pragma unroll
+                    for (int q = 0; q < W; ++q) b[q] = acc[q];
+                } else {
+                    unpack<W>(vload<W>(mine + g.b), b);
+                }
+                if (g.ctl & 1u) {
+#pragma unroll
+                    for (int q = 0; q < W; ++q) r[q] = a[q] ^ b[q] ^ g.ma;
+                } else {
+#pragma unroll
+                    for (int q = 0; q < W; ++q) r[q] = (a[q] ^ g.ma) & (b[q] ^ g.mb);
+                }
+                if (g.ctl & 8u) vstore<W>(mine + g.d, r);
+#pragma unroll
+                for (int q = 0; q < W; ++q) acc[q] = r[q];
+            }
+            // outputs; lanes hold W consecutive words each, so the warp's first
+            // failing word is in its lowest active lane, lowest q
+            unsigned any = 0, outw[W];
+#pragma unroll
+            for (int q = 0; q < W; ++q) {
+                unsigned o = (acc[q] ^ job.out_mask) & job.valid_mask;
+                if (w + q >= job.total_words || base + t * W + q >= it.n_words) o = 0;
+                outw[q] = o;
+                any |= o;
+            }
+            const unsigned hit = __ballot_sync(0xffffffffu, any != 0u);
             if (hit) {
                 const int l = __ffs(hit) - 1;
-                const unsigned o = __shfl_sync(0xffffffffu, out, l);
-                const unsigned long long wl = __shfl_sync(0xffffffffu, w, l);
-                if (lane == 0) atomicMin(job.best, (wl << 5) | (unsigned long long)(__ffs(o) - 1));
+                if ((int)lane == l) {
+                    int q = 0;
+                    unsigned v = 0;
+#pragma unroll
+                    for (int z = W - 1; z >= 0; --z)
+                        if (outw[z]) { q = z; v = outw[z]; }
+                    atomicMin(job.best, ((w + q) << 5) | (unsigned long long)(__ffs(v) - 1));
+                }
             }
         }
     }
@@ -363,134 +431,167 @@ static int run_k1(const LutNet &net, int G, const es_run_opts &o, Ctx *c, double
 // ---------------------------------------------------------------------------
 // K2 driver (single program or batch)
 // ---------------------------------------------------------------------------
-static void encode_k2(const es_prog &p, std::vector<uint2> *code) {
-    for (int i = 0; i < p.num_instrs; ++i) {
-        uint2 w;
-        w.x = (unsigned)(p.dst[i] & 0xFFFF) | ((unsigned)(p.op[i] & 3) << 16) |
-              ((p.neg0[i] ? 1u : 0u) << 18) | ((p.neg1[i] ? 1u : 0u) << 19) |
-              ((unsigned)(p.pi[i] & 63) << 20);
-        w.y = (unsigned)(std::max(p.src0[i], 0) & 0xFFFF) |
-              ((unsigned)(std::max(p.src1[i], 0) & 0xFFFF) << 16);
-        code->push_back(w);
-    }
+template <int W>
+static int launch_k2(int grid, size_t smem, cudaStream_t st, const K2Job *jobs, const K2Item *items,
+                     uint64_t begin, uint64_t end, unsigned *counter, int prog_bytes) {
+    es_k2<W><<<grid, 128, smem, st>>>(jobs, items, begin, end, counter, prog_bytes);
+    CK(cudaGetLastError());
+    return ES_OK;
 }
 
-static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &active,
-                  const es_run_opts &o, Ctx *c, double deadline, es_result *outs) {
+template <int W>
+static int k2_occupancy(size_t smem, int *nb) {
+    CK(cudaFuncSetAttribute(es_k2<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(nb, es_k2<W>, 128, smem));
+    return ES_OK;
+}
+
+// One launch group: jobs sharing a words-per-thread width W.  Items are dealt
+// round-robin across jobs (item r of every job before item r+1 of any job),
+// so a non-equivalent job's first item settles its minimum before its later
+// items are claimed -- those are then skipped -- while every item below the
+// final minimum is still fully evaluated.
+static int run_k2_group(const std::vector<int> &group, const es_prog *progs,
+                        const std::vector<K2Prog> &kps, const es_run_opts &o, Ctx *c,
+                        double deadline, es_result *outs, double *device_ms) {
     const int T = 128;
-    std::vector<uint2> code;
-    std::vector<size_t> code_off(n_jobs, 0);
-    int max_regs = 1;
-    for (int j : active) {
-        code_off[j] = code.size();
-        encode_k2(progs[j], &code);
-        max_regs = std::max(max_regs, progs[j].num_registers);
+    int max_slots = 1, max_gates = 1;
+    for (int j : group) {
+        max_slots = std::max(max_slots, kps[j].num_slots);
+        max_gates = std::max(max_gates, (int)kps[j].gates.size());
     }
-    const size_t smem = (size_t)max_regs * T * 4;
+    const int prog_bytes = ((max_gates * 24) + 15) & ~15;
     int dev_smem = 0;
     CK(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->dev));
-    if (smem + 64 > (size_t)dev_smem) {
-        set_error("program needs " + std::to_string(max_regs) + " registers: too many for the K2 shared-memory interpreter");
+    auto smem_for = [&](int W) { return (size_t)prog_bytes + (size_t)max_slots * T * W * 4; };
+    int W = 0;
+    for (int cand : {4, 2, 1})
+        if (2 * (smem_for(cand) + 1024) <= (size_t)dev_smem + 1024) { W = cand; break; }
+    if (!W)
+        for (int cand : {2, 1})
+            if (smem_for(cand) <= (size_t)dev_smem) { W = cand; break; }
+    if (!W) {
+        set_error("program needs " + std::to_string(max_slots) + " slots: too many for the K2 interpreter");
         return ES_E_BAD_PROGRAM;
     }
-    CK(cudaFuncSetAttribute(es_k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    // items: per job, increasing word order; ~2^11 words each
-    std::vector<K2Item> items;
-    std::vector<K2Job> jobs(n_jobs);
-    std::vector<uint64_t> job_items_end(n_jobs, 0);
-    for (int j : active) {
-        const int P = progs[j].num_pis;
-        const uint64_t tw = 1ull << std::max(P - 5, 0);
-        const uint64_t step = std::min<uint64_t>(tw, 2048);
-        for (uint64_t w = 0; w < tw; w += step) {
-            K2Item it;
-            it.w0 = w;
-            it.n_words = (unsigned)std::min<uint64_t>(step, tw - w);
-            it.job = j;
-            items.push_back(it);
+    const size_t smem = smem_for(W);
+    const uint32_t stride = (uint32_t)T * W * 4;
+    const int G = (int)group.size();
+    std::vector<K2Gate> code;
+    std::vector<size_t> off(G, 0);
+    for (int q = 0; q < G; ++q) {
+        off[q] = code.size();
+        for (K2Gate g : kps[group[q]].gates) {
+            g.a *= stride; g.b *= stride; g.d *= stride;
+            code.push_back(g);
         }
-        job_items_end[j] = items.size();
     }
-    uint2 *d_code = nullptr;
-    K2Job *d_jobs = nullptr;
-    K2Item *d_items = nullptr;
-    unsigned long long *d_best = nullptr;
-    CK(cudaMallocAsync(&d_code, std::max<size_t>(code.size(), 1) * sizeof(uint2), c->stream));
-    CK(cudaMallocAsync(&d_jobs, n_jobs * sizeof(K2Job), c->stream));
-    CK(cudaMallocAsync(&d_items, std::max<size_t>(items.size(), 1) * sizeof(K2Item), c->stream));
-    CK(cudaMallocAsync(&d_best, n_jobs * sizeof(unsigned long long), c->stream));
-    std::vector<unsigned long long> h_best(n_jobs, 0);
-    for (int j : active) {
-        K2Job &J = jobs[j];
-        J.code = d_code + code_off[j];
-        J.best = d_best + j;
+    std::vector<K2Job> jobs(G);
+    std::vector<unsigned long long> h_best(G, 0);
+    std::vector<uint64_t> n_items(G), item_words(G);
+    uint64_t max_items = 0;
+    for (int q = 0; q < G; ++q) {
+        const int P = progs[group[q]].num_pis;
+        const uint64_t tw = 1ull << std::max(P - 5, 0);
+        item_words[q] = std::min<uint64_t>(tw, 4096);
+        n_items[q] = (tw + item_words[q] - 1) / item_words[q];
+        max_items = std::max(max_items, n_items[q]);
+        h_best[q] = 1ull << P;
+    }
+    std::vector<K2Item> items;
+    std::vector<uint64_t> last_pos(G, 0);  // position of each job's last item
+    for (uint64_t r = 0; r < max_items; ++r)
+        for (int q = 0; q < G; ++q)
+            if (r < n_items[q]) {
+                const uint64_t tw = 1ull << std::max(progs[group[q]].num_pis - 5, 0);
+                const uint64_t w0 = r * item_words[q];
+                items.push_back(K2Item{w0, (unsigned)std::min<uint64_t>(item_words[q], tw - w0), q});
+                last_pos[q] = items.size();
+            }
+    uint8_t *d_buf = nullptr;
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const size_t code_b = std::max<size_t>(code.size(), 1) * sizeof(K2Gate);
+    const size_t jobs_b = (size_t)G * sizeof(K2Job);
+    const size_t items_b = std::max<size_t>(items.size(), 1) * sizeof(K2Item);
+    const size_t best_b = (size_t)G * 8;
+    CK(cudaMallocAsync(&d_buf, al(code_b) + al(jobs_b) + al(items_b) + al(best_b), c->stream));
+    K2Gate *d_code = (K2Gate *)d_buf;
+    K2Job *d_jobs = (K2Job *)(d_buf + al(code_b));
+    K2Item *d_items = (K2Item *)(d_buf + al(code_b) + al(jobs_b));
+    unsigned long long *d_best = (unsigned long long *)(d_buf + al(code_b) + al(jobs_b) + al(items_b));
+    for (int q = 0; q < G; ++q) {
+        const int j = group[q];
+        K2Job &J = jobs[q];
+        J.code = d_code + off[q];
+        J.best = d_best + q;
         J.total_words = 1ull << std::max(progs[j].num_pis - 5, 0);
-        J.n_instrs = progs[j].num_instrs;
-        J.num_regs = progs[j].num_registers;
+        J.n_gates = (int)kps[j].gates.size();
+        J.num_pis = progs[j].num_pis;
         J.valid_mask = lane_valid_mask(progs[j].num_pis);
-        h_best[j] = 1ull << progs[j].num_pis;
+        J.out_mask = kps[j].out_mask;
     }
-    CK(cudaMemcpyAsync(d_code, code.data(), code.size() * sizeof(uint2), cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(d_jobs, jobs.data(), n_jobs * sizeof(K2Job), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(d_code, code.data(), code.size() * sizeof(K2Gate), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(d_jobs, jobs.data(), jobs_b, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(d_items, items.data(), items.size() * sizeof(K2Item), cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(d_best, h_best.data(), n_jobs * sizeof(unsigned long long), cudaMemcpyHostToDevice, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-
-    int nb = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, es_k2, T, smem));
+    CK(cudaMemcpyAsync(d_best, h_best.data(), best_b, cudaMemcpyHostToDevice, c->stream));
+    int nb = 0, rc = ES_OK;
+    rc = W == 4 ? k2_occupancy<4>(smem, &nb) : W == 2 ? k2_occupancy<2>(smem, &nb) : k2_occupancy<1>(smem, &nb);
+    if (rc != ES_OK) return rc;
     nb = std::max(nb, 1);
-    const uint64_t n_items = items.size();
+    const uint64_t NI = items.size();
     const bool sliced = deadline >= 0 || o.cancel_flag != nullptr;
-    const uint64_t per_slice = sliced ? std::max<uint64_t>((uint64_t)c->sms * nb * 4, 1) : n_items;
+    const uint64_t per_slice = sliced ? std::max<uint64_t>((uint64_t)c->sms * nb * 8, 1) : NI;
     CK(cudaEventRecord(c->ev_start, c->stream));
     uint64_t done_items = 0;
     int launches = 0, stop_reason = 0;
     bool stopped = false;
-    for (uint64_t begin = 0; begin < n_items; begin += per_slice) {
+    for (uint64_t begin = 0; begin < NI; begin += per_slice) {
         if (stop_requested(o, deadline, &stop_reason)) { stopped = true; break; }
-        const uint64_t end = std::min(n_items, begin + per_slice);
+        const uint64_t end = std::min(NI, begin + per_slice);
         CK(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned), c->stream));
         const int grid = (int)std::min<uint64_t>(end - begin, (uint64_t)c->sms * nb);
-        es_k2<<<grid, T, smem, c->stream>>>(d_jobs, d_items, begin, end, c->d_counter);
-        CK(cudaGetLastError());
+        rc = W == 4 ? launch_k2<4>(grid, smem, c->stream, d_jobs, d_items, begin, end, c->d_counter, prog_bytes)
+           : W == 2 ? launch_k2<2>(grid, smem, c->stream, d_jobs, d_items, begin, end, c->d_counter, prog_bytes)
+                    : launch_k2<1>(grid, smem, c->stream, d_jobs, d_items, begin, end, c->d_counter, prog_bytes);
+        if (rc != ES_OK) return rc;
         ++launches;
         if (sliced) { CK(cudaStreamSynchronize(c->stream)); }
         done_items = end;
     }
     CK(cudaEventRecord(c->ev_stop, c->stream));
-    CK(cudaMemcpyAsync(h_best.data(), d_best, n_jobs * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(h_best.data(), d_best, best_b, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaFreeAsync(d_buf, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, c->ev_start, c->ev_stop));
-    CK(cudaFreeAsync(d_code, c->stream));
-    CK(cudaFreeAsync(d_jobs, c->stream));
-    CK(cudaFreeAsync(d_items, c->stream));
-    CK(cudaFreeAsync(d_best, c->stream));
-    for (int j : active) {
+    *device_ms += ms;
+    std::vector<uint64_t> done_cnt(G, 0);
+    if (done_items >= NI) {
+        done_cnt = n_items;
+    } else {
+        for (uint64_t x = 0; x < done_items; ++x) done_cnt[items[x].job]++;
+    }
+    for (int q = 0; q < G; ++q) {
+        const int j = group[q];
         es_result *r = &outs[j];
         const int P = progs[j].num_pis;
         const uint64_t sentinel = 1ull << P;
         r->engine = ES_ENGINE_INTERP;
-        r->device_ms = ms;
-        r->launches = launches;
-        // items of job j that were in completed slices
-        uint64_t first_item = job_items_end[j];
-        for (uint64_t q = 0; q < (uint64_t)job_items_end[j]; ++q) {
-            if (items[q].job == j) { first_item = q; break; }
-        }
-        uint64_t covered = 0;
-        if (done_items > first_item)
-            covered = std::min<uint64_t>(done_items, job_items_end[j]) - first_item;
-        const uint64_t step_patterns = (uint64_t)std::min<uint64_t>(1ull << std::max(P - 5, 0), 2048) * 32;
-        if (h_best[j] < sentinel) {
+        r->launches += launches;
+        r->num_luts = (int)kps[j].gates.size();
+        r->regs_per_thread = W;  // K2: words per thread
+        const uint64_t covered = done_cnt[q];  // this job's items in completed launches
+        const uint64_t item_patterns = item_words[q] * 32;
+        if (h_best[q] < sentinel) {
             r->verdict = ES_COUNTEREXAMPLE;
-            r->witness_index = h_best[j];
-            r->patterns_evaluated = ref_patterns_for_hit(h_best[j], P);
-            r->patterns_swept = std::min<uint64_t>(covered * step_patterns, sentinel);
-        } else if (stopped && done_items < job_items_end[j]) {
+            r->witness_index = h_best[q];
+            r->patterns_evaluated = ref_patterns_for_hit(h_best[q], P);
+            r->patterns_swept = std::min<uint64_t>(covered * item_patterns, sentinel);
+        } else if (stopped && done_items < last_pos[q]) {
             r->verdict = ES_BUDGET_EXCEEDED;
             r->reason = stop_reason;
-            r->patterns_evaluated = std::min<uint64_t>(covered * step_patterns, sentinel);
+            // contiguous prefix of the job's space that is complete
+            r->patterns_evaluated = std::min<uint64_t>(covered * item_patterns, sentinel);
             r->patterns_swept = r->patterns_evaluated;
         } else {
             r->verdict = ES_EXHAUSTED_ZERO;
@@ -498,6 +599,49 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
             r->patterns_swept = sentinel;
         }
     }
+    return ES_OK;
+}
+
+static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &active,
+                  const es_run_opts &o, Ctx *c, double deadline, es_result *outs) {
+    // host: K2 programs (schedule, accumulator forwarding), in parallel
+    std::vector<K2Prog> kps(n_jobs);
+    std::vector<int> bad(n_jobs, 0);
+    {
+        std::atomic<size_t> next{0};
+        auto work = [&]() {
+            for (;;) {
+                const size_t q = next.fetch_add(1);
+                if (q >= active.size()) return;
+                const int j = active[q];
+                Dag dag;
+                std::string err;
+                if (build_dag(progs[j], &dag, &err) != ES_OK) { bad[j] = 1; continue; }
+                build_k2prog(dag, &kps[j]);
+            }
+        };
+        const int nt = (int)std::min<size_t>(std::max(1u, std::thread::hardware_concurrency()),
+                                             std::max<size_t>(1, active.size() / 64));
+        std::vector<std::thread> th;
+        for (int q = 1; q < nt; ++q) th.emplace_back(work);
+        work();
+        for (auto &x : th) x.join();
+    }
+    for (int j : active)
+        if (bad[j]) { set_error("malformed program in batch (job " + std::to_string(j) + ")"); return ES_E_BAD_PROGRAM; }
+    // launch groups by slot count: small programs get 4 words per thread
+    std::vector<int> g4, g2, g1;
+    for (int j : active) {
+        const int sl = kps[j].num_slots;
+        (sl <= 44 ? g4 : sl <= 88 ? g2 : g1).push_back(j);
+    }
+    double dev_ms = 0;
+    for (auto *grp : {&g4, &g2, &g1}) {
+        if (grp->empty()) continue;
+        int rc = run_k2_group(*grp, progs, kps, o, c, deadline, outs, &dev_ms);
+        if (rc != ES_OK) return rc;
+    }
+    for (int j : active) outs[j].device_ms = dev_ms;
     return ES_OK;
 }
 
@@ -604,7 +748,7 @@ int run_one(const es_prog *prog, const es_run_opts *opts, es_result *out) {
     if (engine == ES_ENGINE_AUTO) {
         // the interpreter beats JIT compile latency on small sweeps
         const double work = (double)G * std::ldexp(1.0, prog->num_pis);
-        engine = work < 4e12 && prog->num_registers * 128 * 4 <= 200 * 1024 ? ES_ENGINE_INTERP : ES_ENGINE_JIT;
+        engine = work < 4e12 ? ES_ENGINE_INTERP : ES_ENGINE_JIT;
     }
     if (engine == ES_ENGINE_INTERP) {
         std::vector<int> act{0};

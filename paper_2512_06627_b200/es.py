@@ -371,6 +371,23 @@ def map_eval(p, w0: int, nw: int) -> np.ndarray:
     return out
 
 
+def k2_stats(p) -> dict:
+    """The K2 interpreter's program for ``p``: gates, slots, stores, forwards."""
+    prog = as_program(p)
+    v = [ctypes.c_int32() for _ in range(4)]
+    N.check(N.lib().es_k2_stats(ctypes.byref(prog.as_struct()), *[ctypes.byref(x) for x in v]))
+    return {"gates": v[0].value, "slots": v[1].value, "stores": v[2].value,
+            "acc_reads": v[3].value}
+
+
+def k2_eval(p, w0: int, nw: int) -> np.ndarray:
+    """CPU model of the K2 interpreter: output words [w0, w0+nw)."""
+    prog = as_program(p)
+    out = np.zeros(nw, dtype=np.uint32)
+    N.check(N.lib().es_k2_eval(ctypes.byref(prog.as_struct()), w0, nw, out.ctypes.data))
+    return out
+
+
 def emit_ptx(p, block_threads: int = 256) -> str:
     prog = as_program(p)
     L = N.lib()
