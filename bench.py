@@ -74,18 +74,19 @@ class _Sub:
         self.id = 0
 
 
-def cones_work(batch, results) -> tuple[int, int, int]:
-    """(gate-patterns, EQ count, NEQ count) of one batched verdict."""
-    work = eq = neq = 0
+def cones_work(batch, rec) -> tuple[int, int, int]:
+    """(gate-patterns, EQ count, NEQ count) of one batched verdict; ``rec`` is
+    NativeBatch.run_arrays()'s es_result array."""
+    import numpy as np
+
     tab = batch.table()
-    for i, r in enumerate(results):
-        if r is None:
-            continue
-        pats = (1 << int(tab["num_pis"][i])) if r.witness_index is None else r.patterns_evaluated
-        work += int(tab["G"][i]) * pats
-        eq += r.witness_index is None
-        neq += r.witness_index is not None
-    return work, eq, neq
+    ok = rec["reason"] != -1
+    eq = ok & (rec["verdict"] == 0)
+    neq = ok & (rec["verdict"] == 1)
+    pats = np.where(eq, np.left_shift(np.uint64(1), tab["num_pis"].astype(np.uint64)),
+                    rec["patterns_evaluated"])
+    work = int((tab["G"].astype(np.float64) * pats.astype(np.float64))[eq | neq].sum())
+    return work, int(eq.sum()), int(neq.sum())
 
 
 def measure_cones(steps: int, warmup: int, rank: int = 0, world: int = 1, count: int = 10_000):
@@ -100,13 +101,13 @@ def measure_cones(steps: int, warmup: int, rank: int = 0, world: int = 1, count:
     if world > 1:
         batch.select(list(range(rank, len(batch), world)))
     for _ in range(warmup):
-        res = batch.run()
+        res = batch.run_arrays()
     dev_ms, wall_ms = [], []
     for _ in range(steps):
         t = time.perf_counter()
-        res = batch.run()
+        res = batch.run_arrays()
         wall_ms.append(1e3 * (time.perf_counter() - t))
-        dev_ms.append(max(r.stats["device_ms"] for r in res if r is not None))
+        dev_ms.append(float(res["device_ms"].max()))
     work, eq, neq = cones_work(batch, res)
     return {"jobs": len(batch), "eq": eq, "neq": neq, "gate_patterns": work,
             "device_ms": statistics.mean(dev_ms), "e2e_ms": statistics.mean(wall_ms),

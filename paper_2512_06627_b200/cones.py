@@ -216,21 +216,35 @@ class NativeBatch:
         N.check(N.lib().es_batch_select(self._h, len(idx), idx.ctypes.data))
         self.origins = [self.origins[i] for i in idx]
 
-    def run(self, budget: float | None = None, cancel=None, device: int = 0):
-        """Batched run_exhaustive over every sub-miter; returns EsResults
-        (witnesses already re-checked on the sub-miter by the library)."""
-        from .es import BUDGET_EXCEEDED, EsResult, _CancelWatcher, _opts, _to_esresult
+    def run_arrays(self, budget: float | None = None, cancel=None, device: int = 0) -> np.ndarray:
+        """Batched run_exhaustive over every sub-miter (witnesses re-checked on
+        the sub-miter by the library); the raw es_result records as a numpy
+        structured array (fields of include/es_b200.h es_result)."""
+        from .es import _CancelWatcher, _opts
 
         n = len(self)
-        if budget is not None and budget <= 0:
-            return [EsResult(BUDGET_EXCEEDED) for _ in range(n)]
         outs = (N.EsResult * n)()
+        if budget is not None and budget <= 0:
+            for i in range(n):
+                outs[i].verdict = 2
+                outs[i].reason = 1
+            return np.ctypeslib.as_array(outs)
         with _CancelWatcher(cancel) as cw:
             opts = _opts(device, "interp", budget, cw.address, 20.0, 0)
             N.check(N.lib().es_batch_run(self._h, ctypes.byref(opts), outs))
+        return np.ctypeslib.as_array(outs)
+
+    def run(self, budget: float | None = None, cancel=None, device: int = 0):
+        """As run_arrays, as a list of EsResult (None for ineligible jobs)."""
+        from .es import _to_esresult
+
+        outs = self.run_arrays(budget, cancel, device)
         pis = self.table()["num_pis"]
-        return [None if outs[i].reason == -1 else _to_esresult(outs[i], int(pis[i]))
-                for i in range(n)]
+        res = []
+        for i in range(len(outs)):
+            rec = N.EsResult.from_buffer_copy(outs[i].tobytes())
+            res.append(None if rec.reason == -1 else _to_esresult(rec, int(pis[i])))
+        return res
 
     def extend(self, other: "NativeBatch") -> None:
         """Move all of ``other``'s sub-miters to the end of this batch."""

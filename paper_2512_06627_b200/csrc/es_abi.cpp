@@ -1,4 +1,6 @@
 // es_abi.cpp -- extern "C" entry points declared in include/es_b200.h.
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -14,7 +16,8 @@ thread_local std::string t_err;
 void set_error(const std::string &m) { t_err = m; }
 
 int run_one(const es_prog *prog, const es_run_opts *opts, es_result *out);
-int run_batch(int n_jobs, const es_prog *progs, const es_run_opts *opts, es_result *outs);
+int run_batch(int n_jobs, const es_prog *progs, const es_run_opts *opts, es_result *outs,
+              const K2Prog *prebuilt = nullptr);
 int session_open(const es_prog *prog, const es_run_opts *opts, void **out);
 int session_geometry(const void *s, uint64_t *n_chunks, uint64_t *ppc, int32_t *luts, int32_t *regs);
 int session_launch(void *s, void *stream, uint64_t *best_dev, uint64_t chunk_begin,
@@ -269,6 +272,7 @@ int32_t es_batch_run(es_batch *bp, const es_run_opts *opts, es_result *outs) {
     if (!bt || !outs) { set_error("bad argument"); return ES_E_BAD_ARG; }
     const int n = (int)bt->subs.size();
     std::vector<es_prog> progs;
+    std::vector<K2Prog> kps;
     std::vector<int> where;
     for (int i = 0; i < n; ++i) {
         std::memset(&outs[i], 0, sizeof(es_result));
@@ -276,8 +280,14 @@ int32_t es_batch_run(es_batch *bp, const es_run_opts *opts, es_result *outs) {
         progs.push_back(bt->subs[i].view());
         where.push_back(i);
     }
+    const double t0 = now_ms();
+    kps.reserve(where.size());
+    for (int i : where) kps.push_back(bt->subs[i].k2);  // built at extraction
     std::vector<es_result> rs(progs.size());
-    int rc = run_batch((int)progs.size(), progs.data(), opts, rs.data());
+    const double t1 = now_ms();
+    int rc = run_batch((int)progs.size(), progs.data(), opts, rs.data(), kps.data());
+    if (getenv("ES_VERBOSE"))
+        fprintf(stderr, "[es batch] jobs=%d prep=%.2fms run_batch=%.2fms\n", n, t1 - t0, now_ms() - t1);
     if (rc != ES_OK) return rc;
     for (size_t k = 0; k < where.size(); ++k) {
         outs[where[k]] = rs[k];

@@ -211,6 +211,10 @@ int extract_compile(int32_t num_pis, int32_t num_gates, const uint8_t *kind, con
             if (n < 0) { bad.fetch_add(1); continue; }
             s.op.resize(n); s.dst.resize(n); s.src0.resize(n); s.neg0.resize(n);
             s.src1.resize(n); s.neg1.resize(n); s.pi.resize(n);
+            Dag dag;
+            std::string e2;
+            if (build_dag(s.view(), &dag, &e2) != ES_OK) { bad.fetch_add(1); continue; }
+            build_k2prog(dag, &s.k2);
         }
     };
     int T = n_threads > 0 ? n_threads : (int)std::max(1u, std::thread::hardware_concurrency());

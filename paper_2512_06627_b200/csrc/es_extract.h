@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "es_core.h"
+#include "es_k2prog.h"
 
 namespace es {
 
@@ -23,6 +24,7 @@ struct SubMiterC {
     std::vector<int32_t> dst, src0, src1, pi;
     std::vector<uint8_t> neg0, neg1;
     int32_t num_registers = 0;
+    K2Prog k2;  // interpreter program, built with the extraction
     es_prog view() const;
 };
 

@@ -6,7 +6,8 @@
 // it instead of interpreting the reference order verbatim:
 //   * gate-level DFS post-order with children by decreasing register need, so
 //     most gates consume the previous gate's result;
-//   * that operand is read from an accumulator register (no LDS), and a result
+//   * that operand (always operand A) is read from an accumulator register
+//     (no LDS; a non-accumulator A is loaded straight into it), and a result
 //     whose only consumer is the next gate is never stored (no STS);
 //   * the remaining live values get LIFO-recycled slots after the PI slots
 //     (fanins are freed before the destination is allocated, as es.py:151-156);
@@ -89,7 +90,8 @@ static void emit_k2(const Dag &dag, const std::vector<int> &order, const std::ve
                     std::vector<int> refs, K2Prog *kp) {
     const int N = dag.num_nodes(), FG = dag.first_gate(), P = dag.num_pis;
     auto is_gate = [&](int v) { return v >= FG && cone[v]; };
-    // slots: 0..P-1 hold the PI words; gates above, LIFO-recycled
+    // slots: 0..P-1 hold the PI words (filled once per word batch); gates
+    // above, LIFO-recycled
     std::vector<int> slot(N, -1), pool;
     for (int j = 1; j <= P; ++j) slot[j] = j - 1;
     int top = P;
@@ -109,12 +111,16 @@ static void emit_k2(const Dag &dag, const std::vector<int> &order, const std::ve
     for (size_t i = 0; i < order.size(); ++i) {
         const int v = order[i], gi = v - FG;
         const int prev = i > 0 ? order[i - 1] : -1;
-        const int fa = dag.f0[gi], fb = dag.f1[gi];
+        int fa = dag.f0[gi], fb = dag.f1[gi];
+        uint32_t na = dag.n0[gi], nb = dag.n1[gi];
+        // only operand A may come from the accumulator: swap a previous-gate
+        // operand into A (AND and XOR are symmetric)
+        if (fb == prev && fa != prev) { std::swap(fa, fb); std::swap(na, nb); }
         K2Gate g{};
         uint32_t ctl = dag.is_xor[gi] ? K2_XOR : 0u;
         if (fa == prev) ctl |= K2_A_ACC; else g.a = (uint32_t)slot[fa];
-        if (fb == prev) ctl |= K2_B_ACC; else g.b = (uint32_t)slot[fb];
-        const uint32_t ma = dag.n0[gi] ? ~0u : 0u, mb = dag.n1[gi] ? ~0u : 0u;
+        g.b = (uint32_t)slot[fb];  // == prev only for AND(x, x): then x was stored
+        const uint32_t ma = na ? ~0u : 0u, mb = nb ? ~0u : 0u;
         if (dag.is_xor[gi]) { g.ma = ma ^ mb; g.mb = 0; }
         else { g.ma = ma; g.mb = mb; }
         // consume fanins; a slot frees when its last reader has read it
@@ -122,11 +128,10 @@ static void emit_k2(const Dag &dag, const std::vector<int> &order, const std::ve
             if (!is_gate(f)) continue;
             if (--refs[f] == 0 && slot[f] >= 0) pool.push_back(slot[f]);
         }
-        // store unless every remaining use is the very next gate (or the output)
+        // store unless the only remaining use is operand A of the next gate
+        // (or the output, which reads the accumulator after the last gate)
         const int next = i + 1 < order.size() ? order[i + 1] : -1;
-        int next_uses = 0;
-        if (next >= 0) next_uses = (dag.f0[next - FG] == v) + (dag.f1[next - FG] == v);
-        else next_uses = 1;  // the output reads the accumulator after the last gate
+        const int next_uses = next < 0 ? 1 : ((dag.f0[next - FG] == v || dag.f1[next - FG] == v) ? 1 : 0);
         if (refs[v] > next_uses) {
             ctl |= K2_STORE;
             slot[v] = alloc();
@@ -150,7 +155,7 @@ void eval_k2prog(const K2Prog &kp, uint64_t w0, uint64_t nw, uint32_t *out) {
         uint32_t acc = 0;
         for (const K2Gate &g : kp.gates) {
             const uint32_t a = (g.ctl & K2_A_ACC) ? acc : s[g.a];
-            const uint32_t b = (g.ctl & K2_B_ACC) ? acc : s[g.b];
+            const uint32_t b = s[g.b];
             const uint32_t r = (g.ctl & K2_XOR) ? (a ^ b ^ g.ma) : ((a ^ g.ma) & (b ^ g.mb));
             if (g.ctl & K2_STORE) s[g.d] = r;
             acc = r;

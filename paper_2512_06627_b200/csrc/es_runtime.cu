@@ -14,6 +14,8 @@
 #include <atomic>
 #include <thread>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -50,7 +52,7 @@ struct K1Params {
 // s*T*W*4 + t*W*4 + k*4 -- every thread owns its columns, so the gate loop
 // needs no barrier, and each access is one W-wide vector (LDS.32/64/128).
 struct K2Job {
-    const K2Gate *code;          // device image: a/b/d are byte offsets
+    const uint4 *code;           // device records, 2 x uint4 per gate
     unsigned long long *best;
     unsigned long long total_words;
     int n_gates;
@@ -68,26 +70,30 @@ struct K2Item {
 __constant__ unsigned c_lane_mask[5] = {0xAAAAAAAAu, 0xCCCCCCCCu, 0xF0F0F0F0u, 0xFF00FF00u,
                                         0xFFFF0000u};
 
-template <int W> struct VecT;
-template <> struct VecT<1> { typedef unsigned type; };
-template <> struct VecT<2> { typedef uint2 type; };
-template <> struct VecT<4> { typedef uint4 type; };
-
+// 32-bit shared-memory accessors (PTX): keeps the slot file in the shared
+// window without per-access generic->shared conversion.  All are volatile so
+// the compiler keeps program order between the slot loads and stores.
 template <int W>
-__device__ __forceinline__ typename VecT<W>::type vload(const unsigned char *p) {
-    return *reinterpret_cast<const typename VecT<W>::type *>(p);
+__device__ __forceinline__ void lds(unsigned addr, unsigned (&v)[W]) {
+    if constexpr (W == 1) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v[0]) : "r"(addr));
+    if constexpr (W == 2) asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v[0]), "=r"(v[1]) : "r"(addr));
+    if constexpr (W == 4)
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "r"(addr));
 }
 template <int W>
-__device__ __forceinline__ void vstore(unsigned char *p, const unsigned (&v)[W]) {
-    if constexpr (W == 1) *reinterpret_cast<unsigned *>(p) = v[0];
-    if constexpr (W == 2) *reinterpret_cast<uint2 *>(p) = make_uint2(v[0], v[1]);
-    if constexpr (W == 4) *reinterpret_cast<uint4 *>(p) = make_uint4(v[0], v[1], v[2], v[3]);
+__device__ __forceinline__ void sts(unsigned addr, const unsigned (&v)[W]) {
+    if constexpr (W == 1) asm volatile("st.shared.u32 [%0], %1;" :: "r"(addr), "r"(v[0]) : "memory");
+    if constexpr (W == 2) asm volatile("st.shared.v2.u32 [%0], {%1, %2};" :: "r"(addr), "r"(v[0]), "r"(v[1]) : "memory");
+    if constexpr (W == 4)
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};"
+                     :: "r"(addr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]) : "memory");
 }
-template <int W>
-__device__ __forceinline__ void unpack(const typename VecT<W>::type &x, unsigned (&v)[W]) {
-    if constexpr (W == 1) v[0] = x;
-    if constexpr (W == 2) { v[0] = x.x; v[1] = x.y; }
-    if constexpr (W == 4) { v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w; }
+__device__ __forceinline__ uint4 lds_rec(unsigned addr) {
+    uint4 r;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(addr));
+    return r;
 }
 
 template <int W>
@@ -96,11 +102,11 @@ __global__ void __launch_bounds__(128) es_k2(const K2Job *__restrict__ jobs,
                                              unsigned long long item_begin,
                                              unsigned long long item_end, unsigned *counter,
                                              int prog_bytes) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(16) uint4 smem[];
     __shared__ unsigned long long s_item;
-    K2Gate *prog = reinterpret_cast<K2Gate *>(smem);
     const unsigned T = blockDim.x, t = threadIdx.x, lane = t & 31u;
-    unsigned char *mine = smem + prog_bytes + t * W * 4;
+    const unsigned prog_addr = (unsigned)__cvta_generic_to_shared(smem);
+    const unsigned base = prog_addr + (unsigned)prog_bytes + t * W * 4;
     const unsigned long long kStop = ~0ull, kSkip = ~0ull - 1;
     int cur_job = -1;
     for (;;) {
@@ -120,52 +126,45 @@ __global__ void __launch_bounds__(128) es_k2(const K2Job *__restrict__ jobs,
         if (k == kSkip) { __syncthreads(); continue; }
         const K2Item it = items[k];
         const K2Job job = jobs[it.job];
-        if (it.job != cur_job) {  // stage the program (uniform branch)
-            const uint2 *src = reinterpret_cast<const uint2 *>(job.code);
-            uint2 *dst = reinterpret_cast<uint2 *>(prog);
-            for (int q = t; q < job.n_gates * 3; q += T) dst[q] = __ldg(&src[q]);
+        if (it.job != cur_job) {  // stage the program records (uniform branch)
+            const uint4 *src = reinterpret_cast<const uint4 *>(job.code);
+            for (int q = t; q < 2 * job.n_gates; q += T) smem[q] = __ldg(&src[q]);
             cur_job = it.job;
         }
         __syncthreads();
-        for (unsigned base = 0; base < it.n_words; base += T * W) {
-            const unsigned long long w = it.w0 + base + (unsigned long long)t * W;
+        for (unsigned wb = 0; wb < it.n_words; wb += T * W) {
+            const unsigned long long w = it.w0 + wb + (unsigned long long)t * W;
             // PI words into slots 0..n-1
             for (int j = 0; j < job.num_pis; ++j) {
                 unsigned v[W];
 #pragma unroll
                 for (int q = 0; q < W; ++q)
                     v[q] = j < 5 ? c_lane_mask[j] : ((((w + q) >> (j - 5)) & 1ull) ? ~0u : 0u);
-                vstore<W>(mine + (unsigned)j * T * W * 4, v);
+                sts<W>(base + (unsigned)j * T * W * 4, v);
             }
             unsigned acc[W];
 #pragma unroll
             for (int q = 0; q < W; ++q) acc[q] = 0;
-#pragma unroll 2
+            // Gate loop.  Records: {off_a, off_b, off_d, ctl} {ma, mb, -, -}.
+            // Operand A is the accumulator or is loaded into it; B is always a
+            // slot; the result stays in the accumulator and is stored only if
+            // it is live beyond the next gate.
+            uint4 r0 = lds_rec(prog_addr), r1 = lds_rec(prog_addr + 16u);
             for (int i = 0; i < job.n_gates; ++i) {
-                const K2Gate g = prog[i];
-                unsigned a[W], b[W], r[W];
-                if (g.ctl & 2u) {
+                const uint4 c0 = r0, c1 = r1;
+                r0 = lds_rec(prog_addr + 32u * (unsigned)(i + 1));  // next record (past-end reads harmless)
+                r1 = lds_rec(prog_addr + 32u * (unsigned)(i + 1) + 16u);
+                unsigned b[W];
+                if (!(c0.w & 2u)) lds<W>(base + c0.x, acc);
+                lds<W>(base + c0.y, b);
+                if (c0.w & 1u) {
 #pragma unroll
-                    for (int q = 0; q < W; ++q) a[q] = acc[q];
-                } else {
-                    unpack<W>(vload<W>(mine + g.a), a);
-                }
-                if (g.ctl & 4u) {
-#pragma unroll
-                    for (int q = 0; q < W; ++q) b[q] = acc[q];
-                } else {
-                    unpack<W>(vload<W>(mine + g.b), b);
-                }
-                if (g.ctl & 1u) {
-#pragma unroll
-                    for (int q = 0; q < W; ++q) r[q] = a[q] ^ b[q] ^ g.ma;
+                    for (int q = 0; q < W; ++q) acc[q] = acc[q] ^ b[q] ^ c1.x;
                 } else {
 #pragma unroll
-                    for (int q = 0; q < W; ++q) r[q] = (a[q] ^ g.ma) & (b[q] ^ g.mb);
+                    for (int q = 0; q < W; ++q) acc[q] = (acc[q] ^ c1.x) & (b[q] ^ c1.y);
                 }
-                if (g.ctl & 8u) vstore<W>(mine + g.d, r);
-#pragma unroll
-                for (int q = 0; q < W; ++q) acc[q] = r[q];
+                if (c0.w & 8u) sts<W>(base + c0.z, acc);
             }
             // outputs; lanes hold W consecutive words each, so the warp's first
             // failing word is in its lowest active lane, lowest q
@@ -173,7 +172,7 @@ __global__ void __launch_bounds__(128) es_k2(const K2Job *__restrict__ jobs,
 #pragma unroll
             for (int q = 0; q < W; ++q) {
                 unsigned o = (acc[q] ^ job.out_mask) & job.valid_mask;
-                if (w + q >= job.total_words || base + t * W + q >= it.n_words) o = 0;
+                if (w + q >= job.total_words || wb + t * W + q >= it.n_words) o = 0;
                 outw[q] = o;
                 any |= o;
             }
@@ -192,6 +191,8 @@ __global__ void __launch_bounds__(128) es_k2(const K2Job *__restrict__ jobs,
         }
     }
 }
+#undef K2_CASE
+#undef K2_CASES_V
 
 // ---------------------------------------------------------------------------
 // ALU-pipe peak microbenchmark: 8 independent LOP3 chains per thread, enough
@@ -232,6 +233,8 @@ struct Ctx {
     unsigned *d_counter = nullptr;         // [2] per in-flight slice
     unsigned long long *h_pin = nullptr;   // [4]
     cudaEvent_t ev_start = nullptr, ev_stop = nullptr, ev_slice[2] = {nullptr, nullptr};
+    cudaStream_t side[3] = {nullptr, nullptr, nullptr};  // concurrent K2 launch groups
+    cudaEvent_t ev_side[3] = {nullptr, nullptr, nullptr};
 };
 
 thread_local std::vector<Ctx *> t_ctx;
@@ -268,6 +271,10 @@ int get_ctx(int dev, Ctx **out) {
     CK(cudaEventCreate(&c->ev_stop));
     CK(cudaEventCreateWithFlags(&c->ev_slice[0], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_slice[1], cudaEventDisableTiming));
+    for (int q = 0; q < 3; ++q) {
+        CK(cudaStreamCreateWithFlags(&c->side[q], cudaStreamNonBlocking));
+        CK(cudaEventCreate(&c->ev_side[q]));
+    }
     t_ctx.push_back(c);
     *out = c;
     return ES_OK;
@@ -431,6 +438,33 @@ static int run_k1(const LutNet &net, int G, const es_run_opts &o, Ctx *c, double
 // ---------------------------------------------------------------------------
 // K2 driver (single program or batch)
 // ---------------------------------------------------------------------------
+// Run fn(0..n-1) on all host cores.
+template <class F>
+static void parallel_for(int n, F fn) {
+    const int nt = (int)std::min<int>(std::max(1u, std::thread::hardware_concurrency()),
+                                      std::max(1, n / 256));
+    std::atomic<int> next{0};
+    auto work = [&]() {
+        for (;;) {
+            const int i = next.fetch_add(1);
+            if (i >= n) return;
+            fn(i);
+        }
+    };
+    std::vector<std::thread> th;
+    for (int q = 1; q < nt; ++q) th.emplace_back(work);
+    work();
+    for (auto &x : th) x.join();
+}
+
+// Device records of a gate (32 bytes): byte offsets of the operand /
+// destination slots for the launch's stride plus the K2_* flags, then the
+// complement masks.
+static void k2_records(const K2Gate &g, uint32_t stride, uint4 *out) {
+    out[0] = make_uint4(g.a * stride, g.b * stride, g.d * stride, g.ctl);
+    out[1] = make_uint4(g.ma, g.mb, 0u, 0u);
+}
+
 template <int W>
 static int launch_k2(int grid, size_t smem, cudaStream_t st, const K2Job *jobs, const K2Item *items,
                      uint64_t begin, uint64_t end, unsigned *counter, int prog_bytes) {
@@ -451,19 +485,40 @@ static int k2_occupancy(size_t smem, int *nb) {
 // so a non-equivalent job's first item settles its minimum before its later
 // items are claimed -- those are then skipped -- while every item below the
 // final minimum is still fully evaluated.
-static int run_k2_group(const std::vector<int> &group, const es_prog *progs,
-                        const std::vector<K2Prog> &kps, const es_run_opts &o, Ctx *c,
-                        double deadline, es_result *outs, double *device_ms) {
+// One launch group: jobs sharing a words-per-thread width W.  Items are dealt
+// round-robin across jobs (item r of every job before item r+1 of any job),
+// so a non-equivalent job's first item settles its minimum before its later
+// items are claimed -- those are then skipped -- while every item below the
+// final minimum is still fully evaluated.
+struct K2Group {
+    std::vector<int> jobs_idx;   // indices into the caller's job arrays
+    int W = 1, prog_bytes = 0, nb = 1;
+    size_t smem = 0;
+    std::vector<uint4> code;
+    std::vector<K2Job> jobs;
+    std::vector<K2Item> items;
+    std::vector<unsigned long long> h_best;
+    std::vector<uint64_t> n_items, item_words;
+    uint8_t *d_buf = nullptr;
+    K2Job *d_jobs = nullptr;
+    K2Item *d_items = nullptr;
+    unsigned long long *d_best = nullptr;
+    uint64_t done_items = 0;
+    int launches = 0;
+};
+
+static int k2_group_prepare(K2Group &gp, const es_prog *progs, const K2Prog *kps, Ctx *c) {
     const int T = 128;
+    const std::vector<int> &group = gp.jobs_idx;
     int max_slots = 1, max_gates = 1;
     for (int j : group) {
         max_slots = std::max(max_slots, kps[j].num_slots);
         max_gates = std::max(max_gates, (int)kps[j].gates.size());
     }
-    const int prog_bytes = ((max_gates * 24) + 15) & ~15;
+    gp.prog_bytes = (max_gates + 1) * 32;
     int dev_smem = 0;
     CK(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->dev));
-    auto smem_for = [&](int W) { return (size_t)prog_bytes + (size_t)max_slots * T * W * 4; };
+    auto smem_for = [&](int W) { return (size_t)gp.prog_bytes + (size_t)max_slots * T * W * 4; };
     int W = 0;
     for (int cand : {4, 2, 1})
         if (2 * (smem_for(cand) + 1024) <= (size_t)dev_smem + 1024) { W = cand; break; }
@@ -474,123 +529,119 @@ static int run_k2_group(const std::vector<int> &group, const es_prog *progs,
         set_error("program needs " + std::to_string(max_slots) + " slots: too many for the K2 interpreter");
         return ES_E_BAD_PROGRAM;
     }
-    const size_t smem = smem_for(W);
+    gp.W = W;
+    gp.smem = smem_for(W);
     const uint32_t stride = (uint32_t)T * W * 4;
     const int G = (int)group.size();
-    std::vector<K2Gate> code;
-    std::vector<size_t> off(G, 0);
-    for (int q = 0; q < G; ++q) {
-        off[q] = code.size();
-        for (K2Gate g : kps[group[q]].gates) {
-            g.a *= stride; g.b *= stride; g.d *= stride;
-            code.push_back(g);
+    std::vector<size_t> off(G + 1, 0);  // 2 records per gate
+    for (int q = 0; q < G; ++q) off[q + 1] = off[q] + 2 * kps[group[q]].gates.size();
+    gp.code.assign(off[G], uint4{});
+    parallel_for(G, [&](int q) {
+        uint4 *dst = gp.code.data() + off[q];
+        for (const K2Gate &g : kps[group[q]].gates) { k2_records(g, stride, dst); dst += 2; }
+    });
+    int rc = W == 4 ? k2_occupancy<4>(gp.smem, &gp.nb) : W == 2 ? k2_occupancy<2>(gp.smem, &gp.nb)
+                                                                : k2_occupancy<1>(gp.smem, &gp.nb);
+    if (rc != ES_OK) return rc;
+    gp.nb = std::max(gp.nb, 1);
+    // item size: 4096 words, halved (down to one CTA iteration) until the
+    // group has >= 8 items per resident CTA
+    uint64_t iw = 4096;
+    for (;;) {
+        uint64_t cnt = 0;
+        for (int q = 0; q < G; ++q) {
+            const uint64_t tw = 1ull << std::max(progs[group[q]].num_pis - 5, 0);
+            cnt += (tw + std::min(tw, iw) - 1) / std::min(tw, iw);
         }
+        if (cnt >= (uint64_t)c->sms * gp.nb * 8 || iw <= (uint64_t)T * W) break;
+        iw >>= 1;
     }
-    std::vector<K2Job> jobs(G);
-    std::vector<unsigned long long> h_best(G, 0);
-    std::vector<uint64_t> n_items(G), item_words(G);
+    gp.jobs.assign(G, K2Job{});
+    gp.h_best.assign(G, 0);
+    gp.n_items.assign(G, 0);
+    gp.item_words.assign(G, 0);
     uint64_t max_items = 0;
     for (int q = 0; q < G; ++q) {
         const int P = progs[group[q]].num_pis;
         const uint64_t tw = 1ull << std::max(P - 5, 0);
-        item_words[q] = std::min<uint64_t>(tw, 4096);
-        n_items[q] = (tw + item_words[q] - 1) / item_words[q];
-        max_items = std::max(max_items, n_items[q]);
-        h_best[q] = 1ull << P;
+        gp.item_words[q] = std::min<uint64_t>(tw, iw);
+        gp.n_items[q] = (tw + gp.item_words[q] - 1) / gp.item_words[q];
+        max_items = std::max(max_items, gp.n_items[q]);
+        gp.h_best[q] = 1ull << P;
     }
-    std::vector<K2Item> items;
-    std::vector<uint64_t> last_pos(G, 0);  // position of each job's last item
+    gp.items.clear();
     for (uint64_t r = 0; r < max_items; ++r)
         for (int q = 0; q < G; ++q)
-            if (r < n_items[q]) {
+            if (r < gp.n_items[q]) {
                 const uint64_t tw = 1ull << std::max(progs[group[q]].num_pis - 5, 0);
-                const uint64_t w0 = r * item_words[q];
-                items.push_back(K2Item{w0, (unsigned)std::min<uint64_t>(item_words[q], tw - w0), q});
-                last_pos[q] = items.size();
+                const uint64_t w0 = r * gp.item_words[q];
+                gp.items.push_back(K2Item{w0, (unsigned)std::min<uint64_t>(gp.item_words[q], tw - w0), q});
             }
-    uint8_t *d_buf = nullptr;
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-    const size_t code_b = std::max<size_t>(code.size(), 1) * sizeof(K2Gate);
+    const size_t code_b = std::max<size_t>(gp.code.size(), 1) * sizeof(uint4);
     const size_t jobs_b = (size_t)G * sizeof(K2Job);
-    const size_t items_b = std::max<size_t>(items.size(), 1) * sizeof(K2Item);
+    const size_t items_b = std::max<size_t>(gp.items.size(), 1) * sizeof(K2Item);
     const size_t best_b = (size_t)G * 8;
-    CK(cudaMallocAsync(&d_buf, al(code_b) + al(jobs_b) + al(items_b) + al(best_b), c->stream));
-    K2Gate *d_code = (K2Gate *)d_buf;
-    K2Job *d_jobs = (K2Job *)(d_buf + al(code_b));
-    K2Item *d_items = (K2Item *)(d_buf + al(code_b) + al(jobs_b));
-    unsigned long long *d_best = (unsigned long long *)(d_buf + al(code_b) + al(jobs_b) + al(items_b));
+    CK(cudaMallocAsync(&gp.d_buf, al(code_b) + al(jobs_b) + al(items_b) + al(best_b), c->stream));
+    uint4 *d_code = (uint4 *)gp.d_buf;
+    gp.d_jobs = (K2Job *)(gp.d_buf + al(code_b));
+    gp.d_items = (K2Item *)(gp.d_buf + al(code_b) + al(jobs_b));
+    gp.d_best = (unsigned long long *)(gp.d_buf + al(code_b) + al(jobs_b) + al(items_b));
     for (int q = 0; q < G; ++q) {
         const int j = group[q];
-        K2Job &J = jobs[q];
+        K2Job &J = gp.jobs[q];
         J.code = d_code + off[q];
-        J.best = d_best + q;
+        J.best = gp.d_best + q;
         J.total_words = 1ull << std::max(progs[j].num_pis - 5, 0);
         J.n_gates = (int)kps[j].gates.size();
         J.num_pis = progs[j].num_pis;
         J.valid_mask = lane_valid_mask(progs[j].num_pis);
         J.out_mask = kps[j].out_mask;
     }
-    CK(cudaMemcpyAsync(d_code, code.data(), code.size() * sizeof(K2Gate), cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(d_jobs, jobs.data(), jobs_b, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(d_items, items.data(), items.size() * sizeof(K2Item), cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(d_best, h_best.data(), best_b, cudaMemcpyHostToDevice, c->stream));
-    int nb = 0, rc = ES_OK;
-    rc = W == 4 ? k2_occupancy<4>(smem, &nb) : W == 2 ? k2_occupancy<2>(smem, &nb) : k2_occupancy<1>(smem, &nb);
-    if (rc != ES_OK) return rc;
-    nb = std::max(nb, 1);
-    const uint64_t NI = items.size();
-    const bool sliced = deadline >= 0 || o.cancel_flag != nullptr;
-    const uint64_t per_slice = sliced ? std::max<uint64_t>((uint64_t)c->sms * nb * 8, 1) : NI;
-    CK(cudaEventRecord(c->ev_start, c->stream));
-    uint64_t done_items = 0;
-    int launches = 0, stop_reason = 0;
-    bool stopped = false;
-    for (uint64_t begin = 0; begin < NI; begin += per_slice) {
-        if (stop_requested(o, deadline, &stop_reason)) { stopped = true; break; }
-        const uint64_t end = std::min(NI, begin + per_slice);
-        CK(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned), c->stream));
-        const int grid = (int)std::min<uint64_t>(end - begin, (uint64_t)c->sms * nb);
-        rc = W == 4 ? launch_k2<4>(grid, smem, c->stream, d_jobs, d_items, begin, end, c->d_counter, prog_bytes)
-           : W == 2 ? launch_k2<2>(grid, smem, c->stream, d_jobs, d_items, begin, end, c->d_counter, prog_bytes)
-                    : launch_k2<1>(grid, smem, c->stream, d_jobs, d_items, begin, end, c->d_counter, prog_bytes);
-        if (rc != ES_OK) return rc;
-        ++launches;
-        if (sliced) { CK(cudaStreamSynchronize(c->stream)); }
-        done_items = end;
-    }
-    CK(cudaEventRecord(c->ev_stop, c->stream));
-    CK(cudaMemcpyAsync(h_best.data(), d_best, best_b, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaFreeAsync(d_buf, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, c->ev_start, c->ev_stop));
-    *device_ms += ms;
+    CK(cudaMemcpyAsync(d_code, gp.code.data(), gp.code.size() * sizeof(uint4), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(gp.d_jobs, gp.jobs.data(), jobs_b, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(gp.d_items, gp.items.data(), gp.items.size() * sizeof(K2Item), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(gp.d_best, gp.h_best.data(), best_b, cudaMemcpyHostToDevice, c->stream));
+    return ES_OK;
+}
+
+static int k2_group_launch(K2Group &gp, cudaStream_t st, unsigned *counter, uint64_t begin,
+                           uint64_t end, int sms) {
+    CK(cudaMemsetAsync(counter, 0, sizeof(unsigned), st));
+    const int grid = (int)std::min<uint64_t>(end - begin, (uint64_t)sms * gp.nb);
+    const int rc = gp.W == 4 ? launch_k2<4>(grid, gp.smem, st, gp.d_jobs, gp.d_items, begin, end, counter, gp.prog_bytes)
+                 : gp.W == 2 ? launch_k2<2>(grid, gp.smem, st, gp.d_jobs, gp.d_items, begin, end, counter, gp.prog_bytes)
+                             : launch_k2<1>(grid, gp.smem, st, gp.d_jobs, gp.d_items, begin, end, counter, gp.prog_bytes);
+    if (rc == ES_OK) { gp.launches++; gp.done_items = end; }
+    return rc;
+}
+
+static void k2_group_results(const K2Group &gp, const es_prog *progs, const K2Prog *kps,
+                             bool stopped, int stop_reason, es_result *outs) {
+    const int G = (int)gp.jobs_idx.size();
     std::vector<uint64_t> done_cnt(G, 0);
-    if (done_items >= NI) {
-        done_cnt = n_items;
-    } else {
-        for (uint64_t x = 0; x < done_items; ++x) done_cnt[items[x].job]++;
-    }
+    if (gp.done_items >= gp.items.size()) done_cnt = gp.n_items;
+    else
+        for (uint64_t x = 0; x < gp.done_items; ++x) done_cnt[gp.items[x].job]++;
     for (int q = 0; q < G; ++q) {
-        const int j = group[q];
+        const int j = gp.jobs_idx[q];
         es_result *r = &outs[j];
         const int P = progs[j].num_pis;
         const uint64_t sentinel = 1ull << P;
         r->engine = ES_ENGINE_INTERP;
-        r->launches += launches;
+        r->launches += gp.launches;
         r->num_luts = (int)kps[j].gates.size();
-        r->regs_per_thread = W;  // K2: words per thread
+        r->regs_per_thread = gp.W;  // K2: words per thread
         const uint64_t covered = done_cnt[q];  // this job's items in completed launches
-        const uint64_t item_patterns = item_words[q] * 32;
-        if (h_best[q] < sentinel) {
+        const uint64_t item_patterns = gp.item_words[q] * 32;
+        if (gp.h_best[q] < sentinel) {
             r->verdict = ES_COUNTEREXAMPLE;
-            r->witness_index = h_best[q];
-            r->patterns_evaluated = ref_patterns_for_hit(h_best[q], P);
+            r->witness_index = gp.h_best[q];
+            r->patterns_evaluated = ref_patterns_for_hit(gp.h_best[q], P);
             r->patterns_swept = std::min<uint64_t>(covered * item_patterns, sentinel);
-        } else if (stopped && done_items < last_pos[q]) {
+        } else if (stopped && covered < gp.n_items[q]) {
             r->verdict = ES_BUDGET_EXCEEDED;
             r->reason = stop_reason;
-            // contiguous prefix of the job's space that is complete
             r->patterns_evaluated = std::min<uint64_t>(covered * item_patterns, sentinel);
             r->patterns_swept = r->patterns_evaluated;
         } else {
@@ -599,15 +650,18 @@ static int run_k2_group(const std::vector<int> &group, const es_prog *progs,
             r->patterns_swept = sentinel;
         }
     }
-    return ES_OK;
 }
 
 static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &active,
-                  const es_run_opts &o, Ctx *c, double deadline, es_result *outs) {
-    // host: K2 programs (schedule, accumulator forwarding), in parallel
-    std::vector<K2Prog> kps(n_jobs);
+                  const es_run_opts &o, Ctx *c, double deadline, es_result *outs,
+                  const K2Prog *prebuilt = nullptr) {
+    // host: K2 programs (schedule, accumulator forwarding), in parallel --
+    // unless the caller built them already (sub-miter batches do at extraction)
+    std::vector<K2Prog> own;
     std::vector<int> bad(n_jobs, 0);
-    {
+    if (!prebuilt) {
+        own.resize(n_jobs);
+        std::vector<K2Prog> &kps = own;
         std::atomic<size_t> next{0};
         auto work = [&]() {
             for (;;) {
@@ -629,19 +683,72 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
     }
     for (int j : active)
         if (bad[j]) { set_error("malformed program in batch (job " + std::to_string(j) + ")"); return ES_E_BAD_PROGRAM; }
+    const K2Prog *kps = prebuilt ? prebuilt : own.data();
     // launch groups by slot count: small programs get 4 words per thread
-    std::vector<int> g4, g2, g1;
+    std::vector<K2Group> groups(3);
     for (int j : active) {
         const int sl = kps[j].num_slots;
-        (sl <= 44 ? g4 : sl <= 88 ? g2 : g1).push_back(j);
+        groups[sl <= 44 ? 0 : sl <= 88 ? 1 : 2].jobs_idx.push_back(j);
     }
-    double dev_ms = 0;
-    for (auto *grp : {&g4, &g2, &g1}) {
-        if (grp->empty()) continue;
-        int rc = run_k2_group(*grp, progs, kps, o, c, deadline, outs, &dev_ms);
+    groups.erase(std::remove_if(groups.begin(), groups.end(),
+                                [](const K2Group &g) { return g.jobs_idx.empty(); }),
+                 groups.end());
+    const bool verbose = getenv("ES_VERBOSE") != nullptr;
+    const double t0 = now_ms();
+    for (K2Group &gp : groups) {  // host images + one upload phase
+        int rc = k2_group_prepare(gp, progs, kps, c);
         if (rc != ES_OK) return rc;
     }
+    const double t1 = now_ms();
+    CK(cudaEventRecord(c->ev_start, c->stream));
+    const bool sliced = deadline >= 0 || o.cancel_flag != nullptr;
+    bool stopped = false;
+    int stop_reason = 0;
+    float dev_ms = 0;
+    if (!sliced) {
+        // all groups at once, one side stream each; device time = makespan
+        for (size_t g = 0; g < groups.size(); ++g) {
+            CK(cudaStreamWaitEvent(c->side[g], c->ev_start, 0));
+            int rc = k2_group_launch(groups[g], c->side[g], c->d_counter + g, 0,
+                                     groups[g].items.size(), c->sms);
+            if (rc != ES_OK) return rc;
+            CK(cudaEventRecord(c->ev_side[g], c->side[g]));
+            CK(cudaStreamWaitEvent(c->stream, c->ev_side[g], 0));
+        }
+        CK(cudaStreamSynchronize(c->stream));
+        for (size_t g = 0; g < groups.size(); ++g) {
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, c->ev_start, c->ev_side[g]));
+            dev_ms = std::max(dev_ms, ms);
+        }
+    } else {
+        // budget / cancel: groups in turn, in slices, checking between slices
+        for (K2Group &gp : groups) {
+            const uint64_t NI = gp.items.size();
+            const uint64_t per_slice = std::max<uint64_t>((uint64_t)c->sms * gp.nb * 8, 1);
+            for (uint64_t begin = 0; begin < NI && !stopped; begin += per_slice) {
+                if (stop_requested(o, deadline, &stop_reason)) { stopped = true; break; }
+                int rc = k2_group_launch(gp, c->stream, c->d_counter, begin, std::min(NI, begin + per_slice), c->sms);
+                if (rc != ES_OK) return rc;
+                CK(cudaStreamSynchronize(c->stream));
+            }
+        }
+        CK(cudaEventRecord(c->ev_stop, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        CK(cudaEventElapsedTime(&dev_ms, c->ev_start, c->ev_stop));
+    }
+    for (K2Group &gp : groups) {
+        CK(cudaMemcpyAsync(gp.h_best.data(), gp.d_best, gp.h_best.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaFreeAsync(gp.d_buf, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    for (K2Group &gp : groups) k2_group_results(gp, progs, kps, stopped, stop_reason, outs);
     for (int j : active) outs[j].device_ms = dev_ms;
+    if (verbose)
+        for (K2Group &gp : groups)
+            fprintf(stderr, "[es k2] group W=%d jobs=%zu items=%zu records=%zu | host+upload %.2fms, "
+                            "kernels %.2fms (makespan)\n", gp.W, gp.jobs_idx.size(), gp.items.size(),
+                    gp.code.size(), t1 - t0, dev_ms);
     return ES_OK;
 }
 
@@ -763,7 +870,8 @@ int run_one(const es_prog *prog, const es_run_opts *opts, es_result *out) {
     return rc;
 }
 
-int run_batch(int n_jobs, const es_prog *progs, const es_run_opts *opts, es_result *outs) {
+int run_batch(int n_jobs, const es_prog *progs, const es_run_opts *opts, es_result *outs,
+              const K2Prog *prebuilt) {
     const double t0 = now_ms();
     es_run_opts o{};
     if (opts) o = *opts;
@@ -784,7 +892,7 @@ int run_batch(int n_jobs, const es_prog *progs, const es_run_opts *opts, es_resu
         for (int j : active) { outs[j].verdict = ES_BUDGET_EXCEEDED; outs[j].reason = reason; }
         return ES_OK;
     }
-    rc = run_k2(n_jobs, progs, active, o, c, deadline, outs);
+    rc = run_k2(n_jobs, progs, active, o, c, deadline, outs, prebuilt);
     const double wall = now_ms() - t0;
     for (int j = 0; j < n_jobs; ++j) outs[j].wall_ms = wall;
     return rc;
@@ -890,6 +998,10 @@ void runtime_shutdown() {
         cudaEventDestroy(c->ev_stop);
         cudaEventDestroy(c->ev_slice[0]);
         cudaEventDestroy(c->ev_slice[1]);
+        for (int q = 0; q < 3; ++q) {
+            cudaStreamDestroy(c->side[q]);
+            cudaEventDestroy(c->ev_side[q]);
+        }
         delete c;
     }
     t_ctx.clear();
