@@ -84,8 +84,12 @@ typedef struct es_run_opts {
     const volatile int32_t *cancel_flag; /* host flag polled between slices; may be NULL */
     double slice_ms;        /* target device time per launch slice (budget/cancel granularity) */
     int32_t block_threads;  /* 0: default */
-    int32_t flags;          /* bit0: skip witness re-check on host; bit1: verbose */
+    int32_t flags;          /* ES_FLAG_* */
 } es_run_opts;
+
+/* es_run_opts.flags: K1 skeleton variants (default: K1) */
+#define ES_FLAG_K1T 4 /* word-uniform sub-network transposed across iterations */
+#define ES_FLAG_K1U 8 /* warp-uniform super-words, 32-thread CTAs (experimental) */
 
 /* EsResult (es.py:76-84) plus engine statistics. */
 typedef struct es_result {
@@ -196,7 +200,8 @@ int32_t es_k2_stats(const es_prog *prog, int32_t *num_gates, int32_t *num_slots,
                     int32_t *stores, int32_t *acc_reads);
 /* CPU model of the K2 program over words [w0, w0+nw) (bit-exact with K2). */
 int32_t es_k2_eval(const es_prog *prog, uint64_t w0, uint64_t nw, uint32_t *out_words);
-/* The PTX the JIT path would compile for `prog` (buf NULL -> returns size). */
+/* The PTX the JIT path would compile for `prog` (buf NULL -> returns size).
+ * block_threads: 128/256/512 -> K1; 32 -> K1U; -128 -> K1T. */
 int64_t es_emit_ptx(const es_prog *prog, int32_t block_threads, char *buf, int64_t cap);
 /* Compile PTX to SASS without a GPU (build-time check); returns cubin bytes or < 0. */
 int64_t es_jit_check(const es_prog *prog, int32_t block_threads, int32_t *regs_per_thread,

@@ -146,7 +146,7 @@ int64_t es_emit_ptx(const es_prog *prog, int32_t block_threads, char *buf, int64
     int rc = map_prog(prog, &net);
     if (rc != ES_OK) return rc;
     std::string ptx, err;
-    if (!splice_body(net, block_threads > 0 ? block_threads : 256, &ptx, &err)) {
+    if (!splice_body(net, block_threads != 0 ? block_threads : 256, &ptx, &err)) {
         set_error(err);
         return ES_E_BAD_ARG;
     }
@@ -164,13 +164,16 @@ int64_t es_jit_check(const es_prog *prog, int32_t block_threads, int32_t *regs_p
     int rc = map_prog(prog, &net);
     if (rc != ES_OK) return rc;
     std::string ptx, err, info;
-    if (!splice_body(net, block_threads > 0 ? block_threads : 256, &ptx, &err)) {
+    if (!splice_body(net, block_threads != 0 ? block_threads : 256, &ptx, &err)) {
         set_error(err);
         return ES_E_BAD_ARG;
     }
     std::vector<char> cubin;
     rc = ptx_to_cubin(ptx, &cubin, &info, &err);
     if (rc != ES_OK) { set_error(err); return rc; }
+    if (const char *dump = getenv("ES_DUMP_CUBIN")) {  // for cuobjdump -sass
+        if (FILE *f = fopen(dump, "wb")) { fwrite(cubin.data(), 1, cubin.size(), f); fclose(f); }
+    }
     int regs = -1, spill = 0;
     parse_ptxas_info(info, &regs, &spill);
     if (regs_per_thread) *regs_per_thread = regs;

@@ -18,8 +18,11 @@
 //                  es.py:9-10; here the register file is the SM's).
 //  * emit_body_ptx / eval_lutnet : the kernel body and its CPU model.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <map>
+#include <tuple>
 #include <sstream>
 #include <unordered_map>
 
@@ -457,15 +460,62 @@ void eval_lutnet(const LutNet &net, uint64_t w0, uint64_t nw, uint32_t *out) {
 // ---------------------------------------------------------------------------
 // PTX body for the K1 skeleton
 // ---------------------------------------------------------------------------
+// A LUT that is a 2-input function of a word-uniform PI u (0 or ~0 for the
+// whole word) and one other value x is, for each value of u, one of
+// {0, ~0, x, ~x} = x*S + T with S in {0, 1, -1} and T in {0, -1}.  So it is
+// one IMAD -- on the FMA pipe, idle in this kernel -- with S and T per-word
+// values derived from u's bit (shared by every LUT with the same (u, S/T)
+// pattern).  The ALU pipe, the kernel's bound, loses those LOP3s.
+namespace {
+struct ImadPlan {
+    int x = -1, u = -1;  // node ids
+    int s0, s1, t0, t1;  // x*S+T coefficients for u = 0 / u = 1
+};
+
+bool plan_imad(const LutNet &net, const Lut &L, ImadPlan *pl) {
+    const int P = net.num_pis;
+    auto word_pi = [&](int v) { return v >= 6 && v <= P && !net.is_const[v]; };
+    int vars[3], nv = 0;
+    for (int k = 0; k < 3; ++k) {
+        bool dep = false;
+        for (int i = 0; i < 8; ++i)
+            if (((L.tt >> i) & 1) != ((L.tt >> (i ^ (1 << k))) & 1)) dep = true;
+        if (dep) vars[nv++] = k;
+    }
+    if (nv != 2 || L.leaf[vars[0]] == L.leaf[vars[1]]) return false;
+    int ku = -1, kx = -1;
+    if (word_pi(L.leaf[vars[1]])) { ku = vars[1]; kx = vars[0]; }
+    else if (word_pi(L.leaf[vars[0]])) { ku = vars[0]; kx = vars[1]; }
+    else return false;
+    auto f = [&](int xv, int uv) { return (L.tt >> ((xv << kx) | (uv << ku))) & 1; };
+    auto st = [&](int uv, int *sv, int *tv) {
+        const int a = f(0, uv), b = f(1, uv);  // value at x = 0 / x = 1
+        if (!a && !b) { *sv = 0; *tv = 0; }
+        else if (a && b) { *sv = 0; *tv = -1; }
+        else if (!a && b) { *sv = 1; *tv = 0; }
+        else { *sv = -1; *tv = -1; }
+    };
+    st(0, &pl->s0, &pl->t0);
+    st(1, &pl->s1, &pl->t1);
+    pl->x = L.leaf[kx];
+    pl->u = L.leaf[ku];
+    return true;
+}
+}  // namespace
+
 std::string emit_body_ptx(const LutNet &net, const std::string &out,
-                          const std::string &wlo, const std::string &whi) {
+                          const std::string &wlo, const std::string &whi,
+                          const std::string &one) {
     const int N = (int)net.is_const.size();
+    const int P = net.num_pis;
+    const bool imad = !one.empty() && getenv("ES_NO_IMAD") == nullptr;
     std::ostringstream s;
     // register names per node
     std::vector<int> lut_idx(N, -1);
     for (size_t i = 0; i < net.luts.size(); ++i) lut_idx[net.luts[i].node] = (int)i;
     std::unordered_map<uint32_t, int> cidx;
     std::vector<uint32_t> consts;
+    std::vector<uint8_t> pi_mask(P + 1, 0), pi_bit(P + 1, 0);
     auto name = [&](int v) -> std::string {
         if (lut_idx[v] >= 0) return "%esq" + std::to_string(lut_idx[v]);
         if (net.is_const[v]) {
@@ -476,10 +526,36 @@ std::string emit_body_ptx(const LutNet &net, const std::string &out,
             else k = it->second;
             return "%esk" + std::to_string(k);
         }
+        pi_mask[v] = 1;
         return "%esm" + std::to_string(v);  // PI mask
     };
+    // per-word coefficient registers, keyed by (PI, a, b) = value a at u=0, b at u=1
+    std::map<std::tuple<int, int, int>, std::string> coef;
+    std::ostringstream coefs;
+    auto coef_reg = [&](int u, int a, int b) -> std::string {
+        if (a == b) return std::to_string(a);  // immediate
+        auto key = std::make_tuple(u, a, b);
+        auto it = coef.find(key);
+        if (it != coef.end()) return it->second;
+        const std::string r = "%esc" + std::to_string(coef.size());
+        coef[key] = r;
+        pi_bit[u] = 1;
+        const std::string m = name(u), bit = "%esb" + std::to_string(u);
+        if (a == 0 && b == -1) coefs << "mov.b32 " << r << ", " << m << ";\n";                      // -bit = mask
+        else if (a == 0 && b == 1) coefs << "mov.b32 " << r << ", " << bit << ";\n";
+        else coefs << "mad.lo.s32 " << r << ", " << bit << ", " << (b - a) << ", " << a << ";\n";
+        return r;
+    };
     std::ostringstream body;
+    int n_imad = 0;
     for (const Lut &L : net.luts) {
+        ImadPlan pl;
+        if (imad && plan_imad(net, L, &pl)) {
+            const std::string S = coef_reg(pl.u, pl.s0, pl.s1), T = coef_reg(pl.u, pl.t0, pl.t1);
+            body << "mad.lo.s32 " << name(L.node) << ", " << name(pl.x) << ", " << S << ", " << T << ";\n";
+            ++n_imad;
+            continue;
+        }
         body << "lop3.b32 " << name(L.node) << ", " << name(L.leaf[2]) << ", " << name(L.leaf[1])
              << ", " << name(L.leaf[0]) << ", " << (int)L.tt << ";\n";
     }
@@ -487,14 +563,127 @@ std::string emit_body_ptx(const LutNet &net, const std::string &out,
     s << "{\n";
     if (!net.luts.empty()) s << ".reg .b32 %esq<" << net.luts.size() << ">;\n";
     if (!consts.empty()) s << ".reg .b32 %esk<" << consts.size() << ">;\n";
-    if (!net.pis_used.empty()) s << ".reg .b32 %esm<" << (net.num_pis + 1) << ">;\n";
+    s << ".reg .b32 %esm<" << (P + 1) << ">;\n.reg .b32 %esb<" << (P + 1) << ">;\n";
+    if (!coef.empty()) s << ".reg .b32 %esc<" << coef.size() << ">;\n";
     for (size_t k = 0; k < consts.size(); ++k) s << "mov.b32 %esk" << k << ", " << consts[k] << ";\n";
-    for (int j : net.pis_used) {
+    if (imad) s << ".reg .b32 %esneg1;\nneg.s32 %esneg1, " << one << ";\n";
+    for (int j = 6; j <= P; ++j) {
+        if (!pi_mask[j] && !pi_bit[j]) continue;
         const int bit = j - 6;
         const std::string &src = bit < 32 ? wlo : whi;
         s << "shl.b32 %esm" << j << ", " << src << ", " << (31 - (bit & 31)) << ";\n";
         s << "shr.s32 %esm" << j << ", %esm" << j << ", 31;\n";
+        // bit = -mask, as an IMAD by an opaque one (FMA pipe, not folded into the ALU)
+        if (pi_bit[j]) s << "mul.lo.s32 %esb" << j << ", %esm" << j << ", %esneg1;\n";
     }
+    s << coefs.str() << body.str();
+    if (net.out_neg) s << "not.b32 " << out << ", " << oname << ";\n";
+    else s << "mov.b32 " << out << ", " << oname << ";\n";
+    s << "}\n";
+    (void)n_imad;
+    return s.str();
+}
+
+// ---------------------------------------------------------------------------
+// PTX body for the K1U skeleton (warp-uniform super-word section)
+// ---------------------------------------------------------------------------
+// A node is warp-uniform when its support avoids PIs 1..10 (bits of the
+// 32-bit word and of the lane index).  Such nodes are evaluated once per warp
+// as a super-word whose bit L is lane L's value: PIs 6..10 become the lane-mask
+// constants, PIs 11.. are uniform masks of the word-block index, so every
+// operand is uniform.  Where a uniform node feeds a per-lane LUT, each lane
+// extracts its bit as a full-word mask with two FMA-pipe multiplies:
+// (S * 2^(31-L)) moves bit L to the sign, mul.hi.s32 by an opaque 1 spreads it.
+std::string emit_body_ptx_u(const LutNet &net, const std::string &out, const std::string &wblo,
+                            const std::string &wbhi, const std::string &lane,
+                            const std::string &pow2, const std::string &one, int *n_uniform) {
+    const int N = (int)net.is_const.size();
+    const int P = net.num_pis;
+    std::vector<int> lut_idx(N, -1);
+    for (size_t i = 0; i < net.luts.size(); ++i) lut_idx[net.luts[i].node] = (int)i;
+    auto is_pi = [&](int v) { return v >= 1 && v <= P; };
+    std::vector<uint8_t> uni(N, 0), used_lane(N, 0);
+    for (int v = 0; v < N; ++v) {
+        if (is_pi(v) && v >= 11) uni[v] = 1;
+        else if (net.is_const[v] && (net.const_val[v] == 0u || net.const_val[v] == ~0u)) uni[v] = 1;
+    }
+    // PIs 6..10 are uniform in super-word form (lane-pattern constants)
+    auto super_ok = [&](int v) { return uni[v] || (is_pi(v) && v >= 6 && v <= 10); };
+    int nu = 0;
+    for (const Lut &L : net.luts) {
+        bool u = true;
+        for (int q = 0; q < 3; ++q) u = u && super_ok(L.leaf[q]);
+        uni[L.node] = u;
+        nu += u;
+    }
+    if (n_uniform) *n_uniform = nu;
+    // which uniform LUTs need a per-lane copy
+    std::vector<uint8_t> need_x(N, 0);
+    for (const Lut &L : net.luts)
+        if (!uni[L.node])
+            for (int q = 0; q < 3; ++q)
+                if (lut_idx[L.leaf[q]] >= 0 && uni[L.leaf[q]]) need_x[L.leaf[q]] = 1;
+    if (lut_idx[net.out_node] >= 0 && uni[net.out_node]) need_x[net.out_node] = 1;
+
+    std::unordered_map<uint32_t, int> cidx;
+    std::vector<uint32_t> consts;
+    std::vector<uint8_t> pi_lane(P + 1, 0), pi_uni(P + 1, 0);
+    auto konst = [&](uint32_t c) {
+        auto it = cidx.find(c);
+        int k;
+        if (it == cidx.end()) { k = (int)consts.size(); cidx[c] = k; consts.push_back(c); }
+        else k = it->second;
+        return "%esk" + std::to_string(k);
+    };
+    auto super_name = [&](int v) -> std::string {
+        if (lut_idx[v] >= 0) return "%esq" + std::to_string(lut_idx[v]);
+        if (is_pi(v) && v >= 6 && v <= 10) return konst(kLaneMask[v - 6]);
+        if (is_pi(v)) { pi_uni[v] = 1; return "%esm" + std::to_string(v); }
+        return konst(net.const_val[v]);
+    };
+    auto lane_name = [&](int v) -> std::string {
+        if (lut_idx[v] >= 0) return (uni[v] ? "%esx" : "%esq") + std::to_string(lut_idx[v]);
+        if (net.is_const[v]) return konst(net.const_val[v]);
+        if (is_pi(v) && v <= 10) { pi_lane[v] = 1; return "%esl" + std::to_string(v); }
+        pi_uni[v] = 1;
+        return "%esm" + std::to_string(v);
+    };
+    std::ostringstream body;
+    for (const Lut &L : net.luts) {
+        const int i = lut_idx[L.node];
+        if (uni[L.node]) {
+            body << "lop3.b32 %esq" << i << ", " << super_name(L.leaf[2]) << ", " << super_name(L.leaf[1])
+                 << ", " << super_name(L.leaf[0]) << ", " << (int)L.tt << ";\n";
+            if (need_x[L.node])
+                body << "mul.lo.u32 %esx" << i << ", %esq" << i << ", " << pow2 << ";\n"
+                     << "mul.hi.s32 %esx" << i << ", %esx" << i << ", " << one << ";\n";
+        } else {
+            body << "lop3.b32 %esq" << i << ", " << lane_name(L.leaf[2]) << ", " << lane_name(L.leaf[1])
+                 << ", " << lane_name(L.leaf[0]) << ", " << (int)L.tt << ";\n";
+        }
+    }
+    const std::string oname = lane_name(net.out_node);
+    std::ostringstream s;
+    s << "{\n";
+    if (!net.luts.empty()) {
+        s << ".reg .b32 %esq<" << net.luts.size() << ">;\n";
+        s << ".reg .b32 %esx<" << net.luts.size() << ">;\n";
+    }
+    if (!consts.empty()) s << ".reg .b32 %esk<" << consts.size() << ">;\n";
+    s << ".reg .b32 %esm<" << (P + 1) << ">;\n.reg .b32 %esl<" << (P + 1) << ">;\n";
+    for (size_t k = 0; k < consts.size(); ++k) s << "mov.b32 %esk" << k << ", " << consts[k] << ";\n";
+    for (int j = 6; j <= std::min(P, 10); ++j)
+        if (pi_lane[j]) {
+            s << "shl.b32 %esl" << j << ", " << lane << ", " << (31 - (j - 6)) << ";\n";
+            s << "shr.s32 %esl" << j << ", %esl" << j << ", 31;\n";
+        }
+    for (int j = 11; j <= P; ++j)
+        if (pi_uni[j]) {
+            const int bit = j - 11;
+            const std::string &src = bit < 32 ? wblo : wbhi;
+            s << "shl.b32 %esm" << j << ", " << src << ", " << (31 - (bit & 31)) << ";\n";
+            s << "shr.s32 %esm" << j << ", %esm" << j << ", 31;\n";
+        }
     s << body.str();
     if (net.out_neg) s << "not.b32 " << out << ", " << oname << ";\n";
     else s << "mov.b32 " << out << ", " << oname << ";\n";

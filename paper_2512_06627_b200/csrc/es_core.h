@@ -80,8 +80,17 @@ void eval_lutnet(const LutNet &net, uint64_t w0, uint64_t nw, uint32_t *out);
 
 // PTX body for the K1 skeleton: reads the word index from (wlo, whi) and
 // writes the output word to `out` (register names from the skeleton).
+// `one` names a register holding 1 that ptxas cannot constant-fold; with it,
+// LUTs of the form f(x, word PI) become FMA-pipe IMADs (empty: LOP3 only).
 std::string emit_body_ptx(const LutNet &net, const std::string &out,
-                          const std::string &wlo, const std::string &whi);
+                          const std::string &wlo, const std::string &whi,
+                          const std::string &one = "");
+
+// PTX body for the K1U skeleton (k1u_skeleton.cu): warp-uniform nodes as
+// super-words.  Operands: word-block index halves, lane, 2^(31-lane), opaque 1.
+std::string emit_body_ptx_u(const LutNet &net, const std::string &out, const std::string &wblo,
+                            const std::string &wbhi, const std::string &lane,
+                            const std::string &pow2, const std::string &one, int *n_uniform);
 
 uint32_t lane_valid_mask(int num_pis);
 

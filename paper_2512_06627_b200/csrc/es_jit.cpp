@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <sstream>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -13,11 +14,12 @@
 #include <cuda_runtime.h>
 #include <nvPTXCompiler.h>
 
+#include "es_codegen_t.h"
 #include "es_jit.h"
 
 namespace es {
 
-#include "k1_skeleton_ptx.inc"  // const char *kK1Ptx128, *kK1Ptx256, *kK1Ptx512
+#include "k1_skeleton_ptx.inc"  // kK1Ptx128/256/512 (K1), kK1UPtx32 (K1U)
 
 static const char *skeleton_for(int threads) {
     switch (threads) {
@@ -28,7 +30,60 @@ static const char *skeleton_for(int threads) {
     }
 }
 
-bool splice_body(const LutNet &net, int threads, std::string *ptx, std::string *err) {
+static bool splice_body_u(const LutNet &net, std::string *ptx, std::string *err) {
+    std::string s(kK1UPtx32);
+    const std::string marker = "// ES_BODY_U ";
+    size_t at = s.find(marker);
+    if (at == std::string::npos || s.find(marker, at + 1) != std::string::npos) {
+        *err = "K1U skeleton must contain exactly one ES_BODY_U marker";
+        return false;
+    }
+    size_t eol = s.find('\n', at);
+    std::string args = s.substr(at + marker.size(), eol - at - marker.size());
+    char o[64], a[64], b[64], l[64], p2[64], one[64];
+    if (sscanf(args.c_str(), "%63s %63s %63s %63s %63s %63s", o, a, b, l, p2, one) != 6) {
+        *err = "cannot parse ES_BODY_U operands: " + args;
+        return false;
+    }
+    int nu = 0;
+    s.replace(at, eol - at, emit_body_ptx_u(net, o, a, b, l, p2, one, &nu));
+    *ptx = std::move(s);
+    return true;
+}
+
+static bool marker_args(const std::string &s, const std::string &marker, size_t *at, size_t *eol,
+                        std::vector<std::string> *args, std::string *err) {
+    *at = s.find(marker);
+    if (*at == std::string::npos || s.find(marker, *at + 1) != std::string::npos) {
+        *err = "skeleton must contain exactly one " + marker;
+        return false;
+    }
+    *eol = s.find('\n', *at);
+    std::istringstream in(s.substr(*at + marker.size(), *eol - *at - marker.size()));
+    std::string a;
+    while (in >> a) args->push_back(a);
+    return true;
+}
+
+static bool splice_body_t(const LutNet &net, std::string *ptx, std::string *err, int *region_bytes) {
+    std::string s(kK1TPtx128);
+    const TSplit t = split_uniform(net);
+    size_t at, eol;
+    std::vector<std::string> a1, a2;
+    if (!marker_args(s, "// ES_BODY_T1 ", &at, &eol, &a1, err) || a1.size() != 3) return false;
+    s.replace(at, eol - at, emit_body_t1(net, t, a1[0], a1[1], a1[2], kK1TBlock));
+    if (!marker_args(s, "// ES_BODY_T2 ", &at, &eol, &a2, err) || a2.size() != 7) return false;
+    s.replace(at, eol - at, emit_body_t2(net, t, a2[0], a2[1], a2[2], a2[3], a2[4], a2[5], a2[6], kK1TBlock));
+    if (region_bytes) *region_bytes = std::max<int>(1, (int)t.boundary.size()) * kK1TBlock * 4;
+    *ptx = std::move(s);
+    return true;
+}
+
+bool splice_body(const LutNet &net, int threads, std::string *ptx, std::string *err,
+                 int *region_bytes) {
+    if (region_bytes) *region_bytes = 0;
+    if (threads == kK1UThreads) return splice_body_u(net, ptx, err);
+    if (threads == kK1TThreads) return splice_body_t(net, ptx, err, region_bytes);
     const char *sk = skeleton_for(threads);
     if (!sk) { *err = "unsupported K1 block size " + std::to_string(threads); return false; }
     std::string s(sk);
@@ -40,12 +95,12 @@ bool splice_body(const LutNet &net, int threads, std::string *ptx, std::string *
     }
     size_t eol = s.find('\n', at);
     std::string args = s.substr(at + marker.size(), eol - at - marker.size());
-    char out[64], wlo[64], whi[64];
-    if (sscanf(args.c_str(), "%63s %63s %63s", out, wlo, whi) != 3) {
+    char out[64], wlo[64], whi[64], one[64];
+    if (sscanf(args.c_str(), "%63s %63s %63s %63s", out, wlo, whi, one) != 4) {
         *err = "cannot parse ES_BODY operands: " + args;
         return false;
     }
-    std::string body = emit_body_ptx(net, out, wlo, whi);
+    std::string body = emit_body_ptx(net, out, wlo, whi, one);
     s.replace(at, eol - at, body);
     *ptx = std::move(s);
     return true;
@@ -114,8 +169,9 @@ std::unordered_map<uint64_t, JitKernel *> g_cache;
 
 int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std::string *err) {
     std::string ptx;
-    if (!splice_body(net, threads, &ptx, err)) return ES_E_BAD_PROGRAM;
-    const uint64_t key = fnv1a(ptx) ^ (uint64_t)threads;
+    int region = 0;
+    if (!splice_body(net, threads, &ptx, err, &region)) return ES_E_BAD_PROGRAM;
+    const uint64_t key = fnv1a(ptx) ^ (uint64_t)(uint32_t)threads;
     std::lock_guard<std::mutex> lk(g_jit_mu);
     auto it = g_cache.find(key);
     if (it != g_cache.end()) { *out = it->second; *jit_ms = 0.0; return ES_OK; }
@@ -126,6 +182,8 @@ int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std
     if (rc != ES_OK) return rc;
     JitKernel *k = new JitKernel();
     k->threads = threads;
+    k->block = threads == kK1TThreads ? 128 : threads;
+    k->region_bytes = region;
     parse_ptxas_info(info, &k->regs, &k->spill_bytes);
     cudaError_t e = cudaLibraryLoadData(&k->lib, cubin.data(), nullptr, nullptr, 0, nullptr,
                                         nullptr, 0);
@@ -134,7 +192,8 @@ int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std
         delete k;
         return ES_E_CUDA;
     }
-    e = cudaLibraryGetKernel(&k->kernel, k->lib, "es_k1");
+    e = cudaLibraryGetKernel(&k->kernel, k->lib,
+                             threads == kK1UThreads ? "es_k1u" : threads == kK1TThreads ? "es_k1t" : "es_k1");
     if (e != cudaSuccess) {
         *err = std::string("cudaLibraryGetKernel: ") + cudaGetErrorString(e);
         cudaLibraryUnload(k->lib);

@@ -14,7 +14,9 @@ namespace es {
 struct JitKernel {
     cudaLibrary_t lib = nullptr;
     cudaKernel_t kernel = nullptr;
-    int threads = 0;
+    int threads = 0;        // variant selector (see below)
+    int block = 0;          // CTA size of the launch
+    int region_bytes = 0;   // K1T: shared bytes per warp
     int regs = -1;
     int spill_bytes = 0;
     double jit_ms = 0;
@@ -25,8 +27,15 @@ inline double now_ms() {
     return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
 }
 
-// The complete PTX for `net` at a block size of 128/256/512 threads.
-bool splice_body(const LutNet &net, int threads, std::string *ptx, std::string *err);
+// "threads" selects the skeleton: 128/256/512 -> K1 at that CTA size;
+// kK1UThreads -> K1U (warp-uniform super-words, 32-thread CTAs);
+// kK1TThreads -> K1T (transposed word-uniform phase, 128-thread CTAs).
+constexpr int kK1UThreads = 32;
+constexpr int kK1TThreads = -128;
+
+// The complete PTX for `net` at a block size of 128/256/512 threads, or K1U.
+bool splice_body(const LutNet &net, int threads, std::string *ptx, std::string *err,
+                 int *region_bytes = nullptr);
 // PTX -> sm_100a cubin in process; `info` receives ptxas's verbose log.
 int ptx_to_cubin(const std::string &ptx, std::vector<char> *cubin, std::string *info,
                  std::string *err);

@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include "es_core.h"
+#include "es_codegen_t.h"
 #include "es_jit.h"
 #include "es_k2prog.h"
 
@@ -42,6 +43,8 @@ struct K1Params {
     unsigned long long total_words;
     unsigned int chunk_log2;
     unsigned int valid_mask;
+    unsigned int one;
+    unsigned int region_bytes;
 };
 
 // ---------------------------------------------------------------------------
@@ -310,7 +313,8 @@ int pick_chunk_log2(uint64_t total_words, int threads, int resident_ctas) {
 // ---------------------------------------------------------------------------
 struct K1Plan {
     JitKernel *jk = nullptr;
-    int threads = 256;
+    int threads = 256;     // CTA size
+    size_t smem = 0;       // dynamic shared bytes (K1T)
     int chunk_log2 = 8;
     uint64_t total_words = 1;
     uint64_t n_chunks = 1;
@@ -328,13 +332,18 @@ int k1_prepare(const LutNet &net, int threads, int sms, K1Plan *pl, double *jit_
         int rc = jit_get(net, threads, &pl->jk, jit_ms, &err);
         if (rc != ES_OK) { set_error(err); return rc; }
     }
-    pl->threads = threads;
+    pl->threads = pl->jk->block;
+    pl->smem = threads == kK1TThreads ? (size_t)pl->jk->region_bytes * (pl->jk->block / 32) : 0;
     const int P = net.num_pis;
     pl->total_words = 1ull << std::max(P - 5, 0);
     int nb = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)pl->jk->kernel, threads, 0));
+    if (pl->smem > 48 * 1024)
+        CK(cudaFuncSetAttribute((const void *)pl->jk->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)pl->jk->kernel, pl->threads, pl->smem));
     nb = std::max(nb, 1);
-    pl->chunk_log2 = pick_chunk_log2(pl->total_words, threads, sms * nb);
+    // K1T: a chunk holds whole phase blocks of every warp (32 words x 16 x warps)
+    const int min_words = threads == kK1TThreads ? 32 * kK1TBlock * (pl->threads / 32) : pl->threads;
+    pl->chunk_log2 = pick_chunk_log2(pl->total_words, min_words, sms * nb);
     pl->n_chunks = std::max<uint64_t>(1, pl->total_words >> pl->chunk_log2);
     pl->grid = (int)std::min<uint64_t>(pl->n_chunks, (uint64_t)sms * nb);
     pl->valid = lane_valid_mask(P);
@@ -352,16 +361,26 @@ int k1_launch(const K1Plan &pl, cudaStream_t st, unsigned long long *best, unsig
     kp.total_words = pl.total_words;
     kp.chunk_log2 = (unsigned)pl.chunk_log2;
     kp.valid_mask = pl.valid;
+    kp.one = 1u;
+    kp.region_bytes = (unsigned)pl.jk->region_bytes;
     CK(cudaMemsetAsync(counter, 0, sizeof(unsigned), st));
     void *args[] = {&kp};
     const int grid = (int)std::min<uint64_t>((uint64_t)pl.grid, std::max<uint64_t>(n_slots, 1));
-    CK(cudaLaunchKernel((const void *)pl.jk->kernel, dim3(grid), dim3(pl.threads), args, 0, st));
+    CK(cudaLaunchKernel((const void *)pl.jk->kernel, dim3(grid), dim3(pl.threads), args, pl.smem, st));
     return ES_OK;
+}
+
+// K1 skeleton choice: opts.flags bit 2 -> K1T, bit 3 -> K1U, else K1 at
+// opts.block_threads (default 128).
+static int k1_threads(const es_run_opts &o) {
+    if (o.flags & ES_FLAG_K1T) return kK1TThreads;
+    if (o.flags & ES_FLAG_K1U) return kK1UThreads;
+    return o.block_threads > 0 ? o.block_threads : 128;
 }
 
 static int run_k1(const LutNet &net, int G, const es_run_opts &o, Ctx *c, double deadline,
                   es_result *r, JitKernel **jk_cache) {
-    const int threads = o.block_threads > 0 ? o.block_threads : 128;
+    const int threads = k1_threads(o);
     K1Plan pl;
     double jit_ms = 0;
     int rc = k1_prepare(net, threads, c->sms, &pl, &jit_ms, *jk_cache);
@@ -760,7 +779,7 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
 struct MappedProg {
     LutNet net;
     int G = 0;
-    JitKernel *jk[3] = {nullptr, nullptr, nullptr};  // per block size 128/256/512
+    JitKernel *jk[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // K1 128/256/512, K1U, K1T
     std::mutex mu;
 };
 
@@ -861,8 +880,9 @@ int run_one(const es_prog *prog, const es_run_opts *opts, es_result *out) {
         std::vector<int> act{0};
         rc = run_k2(1, prog, act, o, c, deadline, out);
     } else {
-        const int threads = o.block_threads > 0 ? o.block_threads : 128;
-        const int slot = threads == 128 ? 0 : threads == 256 ? 1 : 2;
+        const int threads = k1_threads(o);
+        const int slot = threads == 128 ? 0 : threads == 256 ? 1 : threads == 512 ? 2
+                       : threads == kK1UThreads ? 3 : 4;
         std::lock_guard<std::mutex> lk(mp->mu);
         rc = run_k1(net, G, o, c, deadline, out, &mp->jk[slot]);
     }
@@ -927,7 +947,7 @@ int session_open(const es_prog *prog, const es_run_opts *opts, void **out) {
     s->num_pis = prog->num_pis;
     map_luts(dag, &s->net);
     double jit_ms = 0;
-    rc = k1_prepare(s->net, o.block_threads > 0 ? o.block_threads : 128, c->sms, &s->plan, &jit_ms);
+    rc = k1_prepare(s->net, k1_threads(o), c->sms, &s->plan, &jit_ms);
     if (rc != ES_OK) { delete s; return rc; }
     if (cudaMalloc(&s->d_counter, 64) != cudaSuccess) { delete s; set_error("cudaMalloc"); return ES_E_CUDA; }
     *out = s;

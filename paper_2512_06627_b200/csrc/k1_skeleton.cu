@@ -31,6 +31,8 @@ struct K1Params {
     unsigned long long total_words;
     unsigned int chunk_log2;       // words per chunk = 2^chunk_log2 (>= blockDim)
     unsigned int valid_mask;       // pattern bits of a word that exist (n < 5)
+    unsigned int one;              // == 1, opaque to ptxas (IMAD coefficients)
+    unsigned int region_bytes;     // K1T: shared bytes per warp (boundary super-words)
 };
 
 extern "C" __global__ void __launch_bounds__(ES_THREADS)
@@ -59,7 +61,8 @@ es_k1(const K1Params p)
         for (unsigned it = 0; it < words; it += ES_THREADS) {
             const unsigned long long w = w0 + it + threadIdx.x;
             unsigned out;
-            asm volatile("// ES_BODY %0 %1 %2" : "=r"(out) : "r"((unsigned)w), "r"((unsigned)(w >> 32)));
+            asm volatile("// ES_BODY %0 %1 %2 %3"
+                         : "=r"(out) : "r"((unsigned)w), "r"((unsigned)(w >> 32)), "r"(p.one));
             out &= p.valid_mask;
             if (w >= p.total_words) out = 0u;
             const unsigned hit = __ballot_sync(0xffffffffu, out != 0u);

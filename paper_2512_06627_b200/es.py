@@ -230,8 +230,11 @@ class _CancelWatcher:
         return ctypes.addressof(self.flag) if self.cancel is not None else None
 
 
+KERNEL_VARIANTS = {"k1": 0, "k1t": 4, "k1u": 8}  # es_run_opts.flags (ES_FLAG_K1T / _K1U)
+
+
 def _opts(device: int, engine: str, budget: float | None, cancel_addr, slice_ms: float,
-          block_threads: int) -> N.EsRunOpts:
+          block_threads: int, variant: str = "k1") -> N.EsRunOpts:
     o = N.EsRunOpts()
     o.device = device
     o.engine = N.ENGINES[engine]
@@ -239,7 +242,7 @@ def _opts(device: int, engine: str, budget: float | None, cancel_addr, slice_ms:
     o.cancel_flag = cancel_addr
     o.slice_ms = slice_ms
     o.block_threads = block_threads
-    o.flags = 0
+    o.flags = KERNEL_VARIANTS[variant]
     return o
 
 
@@ -262,7 +265,7 @@ def _to_esresult(r: N.EsResult, num_pis: int) -> EsResult:
 
 def run_exhaustive(p, workers: int = 1, budget: float | None = None, cancel=None, *,
                    device: int = 0, engine: str = "auto", slice_ms: float = 20.0,
-                   block_threads: int = 0) -> EsResult:
+                   block_threads: int = 0, variant: str = "k1") -> EsResult:
     """Sweep all 2^num_pis assignments on the GPU (es.py:252-339).
 
     Returns the minimum-index counterexample (the reference's workers=1
@@ -278,7 +281,7 @@ def run_exhaustive(p, workers: int = 1, budget: float | None = None, cancel=None
         return EsResult(BUDGET_EXCEEDED, patterns_evaluated=0)
     res = N.EsResult()
     with _CancelWatcher(cancel) as cw:
-        opts = _opts(device, engine, budget, cw.address, slice_ms, block_threads)
+        opts = _opts(device, engine, budget, cw.address, slice_ms, block_threads, variant)
         N.check(N.lib().es_run(ctypes.byref(prog.as_struct()), ctypes.byref(opts),
                                ctypes.byref(res)))
     return _to_esresult(res, prog.num_pis)

@@ -25,10 +25,11 @@ from .es import (BUDGET_EXCEEDED, ES_COUNTEREXAMPLE, EXHAUSTED_ZERO, EsResult, a
 class Session:
     """A program JIT-compiled for one device, launchable on any stream."""
 
-    def __init__(self, prog, device: int = 0, block_threads: int = 0):
+    def __init__(self, prog, device: int = 0, block_threads: int = 0, variant: str = "k1"):
         self.prog = as_program(prog)
         self.device = device
-        opts = _opts(device, "jit", None, None, 20.0, block_threads)
+        self.variant = variant
+        opts = _opts(device, "jit", None, None, 20.0, block_threads, variant)
         h = ctypes.c_void_p()
         N.check(N.lib().es_session_open(ctypes.byref(self.prog.as_struct()), ctypes.byref(opts),
                                         ctypes.byref(h)))

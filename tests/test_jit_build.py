@@ -23,7 +23,10 @@ def test_ptx_has_one_body_and_lop3():
     p = es.compile_program(M.gen_multiplier_miter(6, "array", "booth"))
     ptx = es.emit_ptx(p, 256)
     assert ".entry es_k1" in ptx and ".target sm_100a" in ptx
-    assert ptx.count("lop3.b32") == es.map_stats(p)["luts"]
+    # every LUT is one LOP3 (ALU pipe) or one IMAD (FMA pipe, f(x, word PI))
+    luts = es.map_stats(p)["luts"]
+    n_mad = sum(1 for ln in ptx.splitlines() if ln.startswith("mad.lo.s32 %esq"))
+    assert ptx.count("lop3.b32") + n_mad == luts and n_mad > 0
     assert "ES_BODY" not in ptx
     assert "atom.global.min.u64" in ptx
 
@@ -32,3 +35,11 @@ def test_unsupported_block_size():
     p = es.compile_program(M.gen_multiplier_miter(3, "array", "diagonal"))
     with pytest.raises(Exception):
         es.emit_ptx(p, 96)
+
+
+@pytest.mark.parametrize("variant", [32, -128])
+def test_experimental_variants_compile(variant):
+    """K1U (32) and K1T (-128) skeletons: PTX splices and compiles, no spills."""
+    p = es.compile_program(M.gen_multiplier_miter(12, "array", "wallace"))
+    j = es.jit_check(p, block_threads=variant)
+    assert j["cubin_bytes"] > 0 and j["spill_bytes"] == 0
