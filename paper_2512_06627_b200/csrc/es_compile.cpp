@@ -472,9 +472,9 @@ struct ImadPlan {
     int s0, s1, t0, t1;  // x*S+T coefficients for u = 0 / u = 1
 };
 
-bool plan_imad(const LutNet &net, const Lut &L, ImadPlan *pl) {
-    const int P = net.num_pis;
-    auto word_pi = [&](int v) { return v >= 6 && v <= P && !net.is_const[v]; };
+// `sel[v]`: v is word-uniform (0 or ~0 across the word) and not a constant --
+// a PI >= 6 or a LUT over such nodes -- so it can act as the IMAD selector.
+bool plan_imad(const Lut &L, const std::vector<uint8_t> &sel, ImadPlan *pl) {
     int vars[3], nv = 0;
     for (int k = 0; k < 3; ++k) {
         bool dep = false;
@@ -484,8 +484,8 @@ bool plan_imad(const LutNet &net, const Lut &L, ImadPlan *pl) {
     }
     if (nv != 2 || L.leaf[vars[0]] == L.leaf[vars[1]]) return false;
     int ku = -1, kx = -1;
-    if (word_pi(L.leaf[vars[1]])) { ku = vars[1]; kx = vars[0]; }
-    else if (word_pi(L.leaf[vars[0]])) { ku = vars[0]; kx = vars[1]; }
+    if (sel[L.leaf[vars[1]]]) { ku = vars[1]; kx = vars[0]; }
+    else if (sel[L.leaf[vars[0]]]) { ku = vars[0]; kx = vars[1]; }
     else return false;
     auto f = [&](int xv, int uv) { return (L.tt >> ((xv << kx) | (uv << ku))) & 1; };
     auto st = [&](int uv, int *sv, int *tv) {
@@ -515,7 +515,13 @@ std::string emit_body_ptx(const LutNet &net, const std::string &out,
     for (size_t i = 0; i < net.luts.size(); ++i) lut_idx[net.luts[i].node] = (int)i;
     std::unordered_map<uint32_t, int> cidx;
     std::vector<uint32_t> consts;
-    std::vector<uint8_t> pi_mask(P + 1, 0), pi_bit(P + 1, 0);
+    std::vector<uint8_t> pi_mask(P + 1, 0), sel(N, 0), have_bit(N, 0);
+    for (int j = 6; j <= P; ++j) sel[j] = !net.is_const[j];
+    for (const Lut &L : net.luts) {
+        bool u = true;
+        for (int q = 0; q < 3; ++q) u = u && sel[L.leaf[q]];
+        sel[L.node] = u;
+    }
     auto name = [&](int v) -> std::string {
         if (lut_idx[v] >= 0) return "%esq" + std::to_string(lut_idx[v]);
         if (net.is_const[v]) {
@@ -529,9 +535,18 @@ std::string emit_body_ptx(const LutNet &net, const std::string &out,
         pi_mask[v] = 1;
         return "%esm" + std::to_string(v);  // PI mask
     };
-    // per-word coefficient registers, keyed by (PI, a, b) = value a at u=0, b at u=1
+    std::ostringstream body;
+    // per-word coefficient registers keyed by (selector, a, b) = value a at
+    // u = 0, b at u = 1; emitted at first use (selectors precede their users)
     std::map<std::tuple<int, int, int>, std::string> coef;
-    std::ostringstream coefs;
+    auto bit_of = [&](int u) {  // bit = -mask, as an IMAD by an opaque -1 (FMA pipe)
+        const std::string b = "%esb" + std::to_string(u);
+        if (!have_bit[u]) {
+            have_bit[u] = 1;
+            body << "mul.lo.s32 " << b << ", " << name(u) << ", %esneg1;\n";
+        }
+        return b;
+    };
     auto coef_reg = [&](int u, int a, int b) -> std::string {
         if (a == b) return std::to_string(a);  // immediate
         auto key = std::make_tuple(u, a, b);
@@ -539,21 +554,21 @@ std::string emit_body_ptx(const LutNet &net, const std::string &out,
         if (it != coef.end()) return it->second;
         const std::string r = "%esc" + std::to_string(coef.size());
         coef[key] = r;
-        pi_bit[u] = 1;
-        const std::string m = name(u), bit = "%esb" + std::to_string(u);
-        if (a == 0 && b == -1) coefs << "mov.b32 " << r << ", " << m << ";\n";                      // -bit = mask
-        else if (a == 0 && b == 1) coefs << "mov.b32 " << r << ", " << bit << ";\n";
-        else coefs << "mad.lo.s32 " << r << ", " << bit << ", " << (b - a) << ", " << a << ";\n";
+        if (a == 0 && b == -1) {  // -bit = mask
+            const std::string m = name(u);
+            body << "mov.b32 " << r << ", " << m << ";\n";
+        } else {
+            const std::string bt = bit_of(u);  // may emit; keep it out of the line below
+            if (a == 0 && b == 1) body << "mov.b32 " << r << ", " << bt << ";\n";
+            else body << "mad.lo.s32 " << r << ", " << bt << ", " << (b - a) << ", " << a << ";\n";
+        }
         return r;
     };
-    std::ostringstream body;
-    int n_imad = 0;
     for (const Lut &L : net.luts) {
         ImadPlan pl;
-        if (imad && plan_imad(net, L, &pl)) {
+        if (imad && plan_imad(L, sel, &pl)) {
             const std::string S = coef_reg(pl.u, pl.s0, pl.s1), T = coef_reg(pl.u, pl.t0, pl.t1);
             body << "mad.lo.s32 " << name(L.node) << ", " << name(pl.x) << ", " << S << ", " << T << ";\n";
-            ++n_imad;
             continue;
         }
         body << "lop3.b32 " << name(L.node) << ", " << name(L.leaf[2]) << ", " << name(L.leaf[1])
@@ -563,24 +578,26 @@ std::string emit_body_ptx(const LutNet &net, const std::string &out,
     s << "{\n";
     if (!net.luts.empty()) s << ".reg .b32 %esq<" << net.luts.size() << ">;\n";
     if (!consts.empty()) s << ".reg .b32 %esk<" << consts.size() << ">;\n";
-    s << ".reg .b32 %esm<" << (P + 1) << ">;\n.reg .b32 %esb<" << (P + 1) << ">;\n";
+    s << ".reg .b32 %esm<" << (P + 1) << ">;\n.reg .b32 %esb<" << N << ">;\n";
     if (!coef.empty()) s << ".reg .b32 %esc<" << coef.size() << ">;\n";
     for (size_t k = 0; k < consts.size(); ++k) s << "mov.b32 %esk" << k << ", " << consts[k] << ";\n";
     if (imad) s << ".reg .b32 %esneg1;\nneg.s32 %esneg1, " << one << ";\n";
     for (int j = 6; j <= P; ++j) {
-        if (!pi_mask[j] && !pi_bit[j]) continue;
+        if (!pi_mask[j]) continue;
         const int bit = j - 6;
         const std::string &src = bit < 32 ? wlo : whi;
-        s << "shl.b32 %esm" << j << ", " << src << ", " << (31 - (bit & 31)) << ";\n";
-        s << "shr.s32 %esm" << j << ", %esm" << j << ", 31;\n";
-        // bit = -mask, as an IMAD by an opaque one (FMA pipe, not folded into the ALU)
-        if (pi_bit[j]) s << "mul.lo.s32 %esb" << j << ", %esm" << j << ", %esneg1;\n";
+        if (imad) {  // mask on the FMA pipe: bit to the sign by a multiply, spread by mul.hi
+            s << "mul.lo.u32 %esm" << j << ", " << src << ", " << (1u << (31 - (bit & 31))) << ";\n";
+            s << "mul.hi.s32 %esm" << j << ", %esm" << j << ", " << one << ";\n";
+        } else {
+            s << "shl.b32 %esm" << j << ", " << src << ", " << (31 - (bit & 31)) << ";\n";
+            s << "shr.s32 %esm" << j << ", %esm" << j << ", 31;\n";
+        }
     }
-    s << coefs.str() << body.str();
+    s << body.str();
     if (net.out_neg) s << "not.b32 " << out << ", " << oname << ";\n";
     else s << "mov.b32 " << out << ", " << oname << ";\n";
     s << "}\n";
-    (void)n_imad;
     return s.str();
 }
 

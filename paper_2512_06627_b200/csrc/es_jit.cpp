@@ -102,6 +102,10 @@ bool splice_body(const LutNet &net, int threads, std::string *ptx, std::string *
     }
     std::string body = emit_body_ptx(net, out, wlo, whi, one);
     s.replace(at, eol - at, body);
+    if (const char *m = getenv("ES_MAXNREG")) {  // experiment: register cap for occupancy
+        const size_t mt = s.find(".maxntid");
+        if (mt != std::string::npos) s.insert(s.find('\n', mt) + 1, std::string(".maxnreg ") + m + "\n");
+    }
     *ptx = std::move(s);
     return true;
 }
@@ -119,8 +123,13 @@ int ptx_to_cubin(const std::string &ptx, std::vector<char> *cubin, std::string *
         *err = "nvPTXCompilerCreate failed";
         return ES_E_CUDA;
     }
-    const char *opts[] = {"--gpu-name=sm_100a", "--verbose", "-O3"};
-    nvPTXCompileResult r = nvPTXCompilerCompile(h, 3, opts);
+    std::vector<const char *> opts = {"--gpu-name=sm_100a", "--verbose", "-O3"};
+    std::string maxr;
+    if (const char *m = getenv("ES_MAXRREG")) {  // experiment: cap registers for occupancy
+        maxr = std::string("--maxrregcount=") + m;
+        opts.push_back(maxr.c_str());
+    }
+    nvPTXCompileResult r = nvPTXCompilerCompile(h, (int)opts.size(), opts.data());
     size_t n = 0;
     if (r != NVPTXCOMPILE_SUCCESS) {
         nvPTXCompilerGetErrorLogSize(h, &n);
