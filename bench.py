@@ -369,7 +369,8 @@ def run_b200(args) -> None:
         launch_patterns = min(launch_patterns, r.patterns_evaluated // world + sess.patterns_per_chunk)
     lane_peak, _ = shard.alu_peak(local)
     achieved = G * launch_patterns / (k_ms * 1e-3)
-    lop3_rate = sess.num_luts * (launch_patterns / 32) / (k_ms * 1e-3)
+    pipes = es.map_pipes(prog)
+    lop3_rate = pipes["lop3"] * (launch_patterns / 32) / (k_ms * 1e-3)
 
     # e2e through the public API, host circuit in, host verdict out
     def e2e_step():
@@ -424,10 +425,14 @@ def run_b200(args) -> None:
                          "kernel": "es_k1", "kernel_ms": k_ms,
                          "peak_source": "measured: es_alu_peak LOP3 microbenchmark on this GPU "
                                         "(lane-LOP3/s x 32 patterns, 1 gate per LOP3)",
-                         "issue": {"lop3_per_word": sess.num_luts,
+                         "issue": {"luts_per_word": sess.num_luts,
+                                   "lop3_per_word": pipes["lop3"],
+                                   "imad_per_word": pipes["imad"],
                                    "achieved_lane_lop3_per_s": lop3_rate,
                                    "peak_lane_lop3_per_s": lane_peak,
-                                   "frac": lop3_rate / lane_peak}},
+                                   "frac": lop3_rate / lane_peak,
+                                   "note": "LUT-level ops only; ncu pipe utilisation in "
+                                           "profiles/ covers PI/loop overhead"}},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 56 * S + 8,
                     "d2h_bytes_per_step": 8,
                     "path": "es.es_check(sub-miter) -> compile_program -> C ABI es_run "

@@ -190,6 +190,9 @@ void es_batch_free(es_batch *b);
 /* LUT-3 mapping statistics of a program: LOP3s per word, schedule peak live. */
 int32_t es_map_stats(const es_prog *prog, int32_t *num_luts, int32_t *peak_live,
                      int32_t *num_gates);
+/* Per-word ops of the K1 body by pipe: LUTs issued as LOP3 (ALU pipe) and
+ * as IMAD (FMA pipe, f(x, word-uniform selector)); lop3 + imad = num_luts. */
+int32_t es_map_pipes(const es_prog *prog, int32_t *lop3, int32_t *imad);
 /* Evaluate the mapped+scheduled LUT program on the CPU for words [w0, w0+nw)
  * (32 patterns per word, the kernel's layout): writes the output words.
  * Lets GPU-less CI check the mapper bit-exactly. */

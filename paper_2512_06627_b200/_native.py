@@ -28,7 +28,7 @@ ENGINES = {"auto": ENGINE_AUTO, "jit": ENGINE_JIT, "interp": ENGINE_INTERP}
 
 # every symbol include/es_b200.h declares
 EXPORTS = ("es_compile", "es_run", "es_run_batch", "es_session_open", "es_session_geometry",
-           "es_session_launch", "es_session_close", "es_map_stats", "es_map_eval", "es_k2_stats", "es_k2_eval",
+           "es_session_launch", "es_session_close", "es_map_stats", "es_map_pipes", "es_map_eval", "es_k2_stats", "es_k2_eval",
            "es_emit_ptx", "es_jit_check", "es_alu_peak", "es_batch_extract", "es_batch_size",
            "es_batch_info", "es_batch_table", "es_batch_xag", "es_batch_select", "es_batch_run", "es_batch_merge", "es_batch_free",
            "es_last_error", "es_version", "es_shutdown")
@@ -106,6 +106,9 @@ def lib():
         L.es_map_stats.argtypes = [ctypes.POINTER(EsProg), ctypes.POINTER(ctypes.c_int32),
                                    ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
         L.es_map_stats.restype = ctypes.c_int32
+        L.es_map_pipes.argtypes = [ctypes.POINTER(EsProg), ctypes.POINTER(ctypes.c_int32),
+                                   ctypes.POINTER(ctypes.c_int32)]
+        L.es_map_pipes.restype = ctypes.c_int32
         L.es_map_eval.argtypes = [ctypes.POINTER(EsProg), ctypes.c_uint64, ctypes.c_uint64, _P]
         L.es_map_eval.restype = ctypes.c_int32
         L.es_k2_stats.argtypes = [ctypes.POINTER(EsProg), _P, _P, _P, _P]

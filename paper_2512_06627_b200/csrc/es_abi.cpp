@@ -100,6 +100,19 @@ int32_t es_map_stats(const es_prog *prog, int32_t *num_luts, int32_t *peak_live,
     return ES_OK;
 }
 
+int32_t es_map_pipes(const es_prog *prog, int32_t *lop3, int32_t *imad) {
+    LutNet net;
+    int rc = map_prog(prog, &net);
+    if (rc != ES_OK) return rc;
+    const std::string body = emit_body_ptx(net, "%o", "%lo", "%hi", "%one");
+    int nl = 0, ni = 0;
+    for (size_t p = 0; (p = body.find("lop3.b32 %esq", p)) != std::string::npos; ++p) ++nl;
+    for (size_t p = 0; (p = body.find("mad.lo.s32 %esq", p)) != std::string::npos; ++p) ++ni;
+    if (lop3) *lop3 = nl;
+    if (imad) *imad = ni;
+    return ES_OK;
+}
+
 int32_t es_map_eval(const es_prog *prog, uint64_t w0, uint64_t nw, uint32_t *out_words) {
     LutNet net;
     int rc = map_prog(prog, &net);

@@ -366,6 +366,14 @@ def map_stats(p) -> dict:
     return {"luts": luts.value, "peak_live": live.value, "gates": gates.value}
 
 
+def map_pipes(p) -> dict:
+    """K1 body ops per 32-pattern word: LOP3 (ALU pipe) and IMAD (FMA pipe)."""
+    prog = as_program(p)
+    l, i = ctypes.c_int32(), ctypes.c_int32()
+    N.check(N.lib().es_map_pipes(ctypes.byref(prog.as_struct()), ctypes.byref(l), ctypes.byref(i)))
+    return {"lop3": l.value, "imad": i.value}
+
+
 def map_eval(p, w0: int, nw: int) -> np.ndarray:
     """CPU model of the mapped kernel body: output words [w0, w0+nw)."""
     prog = as_program(p)
