@@ -284,11 +284,16 @@ def run_b200(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % max(torch.cuda.device_count(), 1) if args.backend != "nccl" else local
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     group = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        # --backend gloo lets several ranks share one GPU (NCCL needs one GPU per rank)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.backend)
 
     from paper_2512_06627_b200 import es, shard
 
@@ -310,14 +315,25 @@ def run_b200(args) -> None:
     sess = shard.session_for(prog, local)
     best = torch.empty(1, dtype=torch.int64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    S = args.slices or (1 if world == 1 else 8)
+    S = args.slices or (1 if world == 1 else 4)
+    peer = None
+    collective = args.collective if world > 1 else "none"
+    if collective == "p2p":
+        try:
+            peer = shard.PeerBest(group, local)
+        except Exception as exc:  # no IPC / peer access: fall back to NCCL MIN
+            print(f"[bench] peer word unavailable ({exc}); using NCCL all-reduce", file=sys.stderr)
+            collective = "nccl"
 
     def barrier():
         if world > 1:
             dist.barrier()
 
     def step():
-        r = shard.sweep_sharded(prog, group, local, slices=S, best=best)
+        if peer is not None:
+            r = shard.sweep_peer(prog, peer, group, local)
+        else:
+            r = shard.sweep_sharded(prog, group, local, slices=S, best=best)
         if r.verdict != expected or r.witness_index != cold.witness_index:
             raise RuntimeError(f"verdict drift: {r.verdict} {r.witness_index} vs "
                                f"{expected} {cold.witness_index}")
@@ -376,6 +392,8 @@ def run_b200(args) -> None:
     def e2e_step():
         if world == 1:
             res = es.es_check(sm, engine="jit")
+        elif peer is not None:
+            res = shard.es_check_peer(sm, peer, group, local)
         else:
             res = shard.es_check_sharded(sm, group, local, slices=S)
         return res
@@ -413,8 +431,12 @@ def run_b200(args) -> None:
             "config": {"workload": desc, "num_pis": P, "G": G,
                        "patterns_per_step": patterns_per_step, "verdict": r.verdict,
                        "witness_index": r.witness_index,
-                       "parallelism": f"pattern-space shards x{world}, NCCL MIN all-reduce "
-                                      f"after each of {S} launch slice(s)" if world > 1 else
+                       "parallelism": (f"pattern-space shards x{world}; one shared minimum word "
+                                       "in rank 0's HBM mapped into every rank (CUDA IPC, NVLink "
+                                       "peer memory): kernel atomicMin + early exit, 2 barriers "
+                                       "per verdict" if collective == "p2p" else
+                                       f"pattern-space shards x{world}, NCCL MIN all-reduce "
+                                       f"after each of {S} launch slice(s)") if world > 1 else
                                       "1 GPU, 1 launch per verdict",
                        "l2": "flushed between steps (256 MiB write, outside the step events); "
                              "the kernel reads no HBM inputs",
@@ -443,7 +465,7 @@ def run_b200(args) -> None:
                                 "host_compile_ms": cold.stats.get("compile_ms"),
                                 "device_ms": cold.stats.get("device_ms"),
                                 "warm_device_ms": total_s * 1e3 / args.steps},
-            "gpu_launches": args.steps * S * world,
+            "gpu_launches": args.steps * (1 if collective == "p2p" else S) * world,
             "clocks": clk.summary(),
         }
         if cpu is not None:
@@ -455,6 +477,9 @@ def run_b200(args) -> None:
                                **measure_cones(5, 2)}
             line["other_configs"] = extras
         print(json.dumps(line), flush=True)
+    if peer is not None:
+        barrier()
+        peer.close()
     if world > 1:
         dist.destroy_process_group()
 
@@ -505,6 +530,9 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--backend", default="nccl", help="torch.distributed backend for N>1")
+    ap.add_argument("--collective", choices=("p2p", "nccl"), default="p2p",
+                    help="N>1 exchange: shared peer word (p2p) or NCCL MIN per slice")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -186,6 +186,20 @@ int32_t es_batch_run(es_batch *b, const es_run_opts *opts, es_result *outs);
 int32_t es_batch_merge(es_batch *dst, es_batch *src);
 void es_batch_free(es_batch *b);
 
+/*
+ * Shared minimum word for the NVLink peer path: rank 0 allocates a
+ * device word and exports a 64-byte CUDA IPC handle; every other rank opens it
+ * (peer access is enabled lazily, so on an NVSwitch box the word is a peer
+ * GPU's memory reached over NVLink).  Pass the opened pointer as `best_dev` to
+ * es_session_launch: every rank's kernel then atomicMin's (system scope) into
+ * and early-exits on the one word, with no per-slice collective.
+ */
+int32_t es_ipc_alloc(int32_t device, void **dev_ptr, uint8_t *handle64);
+int32_t es_ipc_open(int32_t device, const uint8_t *handle64, void **dev_ptr);
+int32_t es_ipc_close(int32_t device, void *dev_ptr, int32_t owner);
+int32_t es_word_write(int32_t device, void *dev_ptr, uint64_t value);
+int32_t es_word_read(int32_t device, void *dev_ptr, uint64_t *value);
+
 /* Engine-internal views for tests and profiling. */
 /* LUT-3 mapping statistics of a program: LOP3s per word, schedule peak live. */
 int32_t es_map_stats(const es_prog *prog, int32_t *num_luts, int32_t *peak_live,

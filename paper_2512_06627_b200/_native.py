@@ -31,6 +31,7 @@ EXPORTS = ("es_compile", "es_run", "es_run_batch", "es_session_open", "es_sessio
            "es_session_launch", "es_session_close", "es_map_stats", "es_map_pipes", "es_map_eval", "es_k2_stats", "es_k2_eval",
            "es_emit_ptx", "es_jit_check", "es_alu_peak", "es_batch_extract", "es_batch_size",
            "es_batch_info", "es_batch_table", "es_batch_xag", "es_batch_select", "es_batch_run", "es_batch_merge", "es_batch_free",
+           "es_ipc_alloc", "es_ipc_open", "es_ipc_close", "es_word_write", "es_word_read",
            "es_last_error", "es_version", "es_shutdown")
 
 _P = ctypes.c_void_p
@@ -145,6 +146,16 @@ def lib():
         L.es_batch_merge.restype = ctypes.c_int32
         L.es_batch_free.argtypes = [_P]
         L.es_batch_free.restype = None
+        L.es_ipc_alloc.argtypes = [ctypes.c_int32, ctypes.POINTER(_P), _P]
+        L.es_ipc_alloc.restype = ctypes.c_int32
+        L.es_ipc_open.argtypes = [ctypes.c_int32, _P, ctypes.POINTER(_P)]
+        L.es_ipc_open.restype = ctypes.c_int32
+        L.es_ipc_close.argtypes = [ctypes.c_int32, _P, ctypes.c_int32]
+        L.es_ipc_close.restype = ctypes.c_int32
+        L.es_word_write.argtypes = [ctypes.c_int32, _P, ctypes.c_uint64]
+        L.es_word_write.restype = ctypes.c_int32
+        L.es_word_read.argtypes = [ctypes.c_int32, _P, ctypes.POINTER(ctypes.c_uint64)]
+        L.es_word_read.restype = ctypes.c_int32
         L.es_last_error.argtypes = []
         L.es_last_error.restype = ctypes.c_char_p
         L.es_version.argtypes = []

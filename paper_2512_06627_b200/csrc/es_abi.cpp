@@ -25,6 +25,10 @@ int session_launch(void *s, void *stream, uint64_t *best_dev, uint64_t chunk_beg
 void session_close(void *s);
 void runtime_shutdown();
 int alu_peak(int dev, double *lane_ops_per_s, double *ms_out);
+int ipc_alloc(int dev, void **ptr, unsigned char *handle);
+int ipc_open(int dev, const unsigned char *handle, void **ptr);
+int ipc_close(int dev, void *ptr, int owner);
+int word_io(int dev, void *ptr, uint64_t *value, int write);
 
 static int map_prog(const es_prog *prog, LutNet *net) {
     if (!prog || prog->num_instrs < 1) { set_error("empty program"); return ES_E_BAD_PROGRAM; }
@@ -325,6 +329,29 @@ int32_t es_batch_merge(es_batch *dst, es_batch *src) {
 }
 
 void es_batch_free(es_batch *bp) { delete (Batch *)bp; }
+
+int32_t es_ipc_alloc(int32_t device, void **dev_ptr, uint8_t *handle64) {
+    if (!dev_ptr || !handle64) return ES_E_BAD_ARG;
+    return ipc_alloc(device, dev_ptr, handle64);
+}
+
+int32_t es_ipc_open(int32_t device, const uint8_t *handle64, void **dev_ptr) {
+    if (!dev_ptr || !handle64) return ES_E_BAD_ARG;
+    return ipc_open(device, handle64, dev_ptr);
+}
+
+int32_t es_ipc_close(int32_t device, void *dev_ptr, int32_t owner) {
+    return ipc_close(device, dev_ptr, owner);
+}
+
+int32_t es_word_write(int32_t device, void *dev_ptr, uint64_t value) {
+    return word_io(device, dev_ptr, &value, 1);
+}
+
+int32_t es_word_read(int32_t device, void *dev_ptr, uint64_t *value) {
+    if (!value) return ES_E_BAD_ARG;
+    return word_io(device, dev_ptr, value, 0);
+}
 
 const char *es_last_error(void) { return t_err.c_str(); }
 

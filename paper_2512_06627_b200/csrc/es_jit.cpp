@@ -123,7 +123,9 @@ int ptx_to_cubin(const std::string &ptx, std::vector<char> *cubin, std::string *
         *err = "nvPTXCompilerCreate failed";
         return ES_E_CUDA;
     }
-    std::vector<const char *> opts = {"--gpu-name=sm_100a", "--verbose", "-O3"};
+    std::vector<const char *> opts = {"--gpu-name=sm_100a", "--verbose"};
+    std::string olev = std::string("-O") + (getenv("ES_PTXAS_O") ? getenv("ES_PTXAS_O") : "3");
+    opts.push_back(olev.c_str());
     std::string maxr;
     if (const char *m = getenv("ES_MAXRREG")) {  // experiment: cap registers for occupancy
         maxr = std::string("--maxrregcount=") + m;

@@ -1007,6 +1007,41 @@ int alu_peak(int dev, double *lane_ops_per_s, double *ms_out) {
     return ES_OK;
 }
 
+// ---------------------------------------------------------------------------
+// cross-process shared minimum word (CUDA IPC; NVLink peer memory across GPUs)
+// ---------------------------------------------------------------------------
+int ipc_alloc(int dev, void **ptr, unsigned char *handle) {
+    CK(cudaSetDevice(dev));
+    CK(cudaMalloc(ptr, 256));
+    CK(cudaMemset(*ptr, 0, 256));
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, *ptr));
+    memcpy(handle, &h, sizeof(h));
+    return ES_OK;
+}
+
+int ipc_open(int dev, const unsigned char *handle, void **ptr) {
+    CK(cudaSetDevice(dev));
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    CK(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return ES_OK;
+}
+
+int ipc_close(int dev, void *ptr, int owner) {
+    CK(cudaSetDevice(dev));
+    if (owner) { CK(cudaFree(ptr)); }
+    else { CK(cudaIpcCloseMemHandle(ptr)); }
+    return ES_OK;
+}
+
+int word_io(int dev, void *ptr, uint64_t *value, int write) {
+    CK(cudaSetDevice(dev));
+    if (write) { CK(cudaMemcpy(ptr, value, 8, cudaMemcpyHostToDevice)); }
+    else { CK(cudaMemcpy(value, ptr, 8, cudaMemcpyDeviceToHost)); }
+    return ES_OK;
+}
+
 void runtime_shutdown() {
     for (Ctx *c : t_ctx) {
         cudaSetDevice(c->dev);

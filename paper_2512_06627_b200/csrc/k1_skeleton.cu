@@ -70,7 +70,8 @@ es_k1(const K1Params p)
                 const int l = __ffs(hit) - 1;
                 const unsigned o = __shfl_sync(0xffffffffu, out, l);
                 const unsigned long long wl = __shfl_sync(0xffffffffu, w, l);
-                if (lane == 0) atomicMin(p.best, (wl << 5) | (unsigned long long)(__ffs(o) - 1));
+                // system scope: `best` may be a peer GPU's word mapped over NVLink (CUDA IPC)
+                if (lane == 0) atomicMin_system(p.best, (wl << 5) | (unsigned long long)(__ffs(o) - 1));
             }
         }
     }

@@ -51,7 +51,7 @@ es_k1u(const K1Params p)
             if (hit) {
                 const int l = __ffs(hit) - 1;
                 const unsigned o = __shfl_sync(0xffffffffu, out, l);
-                if (lane == 0) atomicMin(p.best, (((wb << 5) | (unsigned)l) << 5) | (unsigned long long)(__ffs(o) - 1));
+                if (lane == 0) atomicMin_system(p.best, (((wb << 5) | (unsigned)l) << 5) | (unsigned long long)(__ffs(o) - 1));
             }
         }
     }

@@ -171,3 +171,112 @@ def es_check_sharded(sm, group=None, device: int | None = None,
     if evaluate(sm.circuit, r.witness) != 1:
         raise AssertionError("exhaustive-simulation witness failed re-check")
     return CheckResult(COUNTEREXAMPLE, witness=r.witness, engine="es", stats=stats)
+
+
+class PeerBest:
+    """The NVLink-native exchange: ONE minimum word in rank 0's
+    device memory, mapped into every rank through CUDA IPC.  Every rank's
+    kernel atomicMin's (system scope) into it and reads it at each chunk
+    claim, so a counterexample found on any GPU stops every GPU at its next
+    chunk -- no per-slice collective on the data path.  Two words alternate
+    between verdicts so rank 0 can re-arm one while the other is being read.
+    Collective constructor (every rank of ``group``)."""
+
+    def __init__(self, group=None, device: int | None = None):
+        import torch
+        import torch.distributed as dist
+
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if self.world > 1 else 0
+        self.device = torch.cuda.current_device() if device is None else device
+        self.ptrs = []
+        self._step = 0
+        L = N.lib()
+        for _ in range(2):
+            ptr = ctypes.c_void_p()
+            handle = (ctypes.c_uint8 * 64)()
+            if self.rank == 0:
+                N.check(L.es_ipc_alloc(self.device, ctypes.byref(ptr), handle))
+            box = [bytes(handle)]
+            if self.world > 1:
+                dist.broadcast_object_list(box, src=0, group=group)
+            if self.rank != 0:
+                h = (ctypes.c_uint8 * 64).from_buffer_copy(box[0])
+                N.check(L.es_ipc_open(self.device, h, ctypes.byref(ptr)))
+            self.ptrs.append(ptr)
+
+    def write(self, k: int, value: int) -> None:
+        N.check(N.lib().es_word_write(self.device, self.ptrs[k], value))
+
+    def read(self, k: int) -> int:
+        v = ctypes.c_uint64()
+        N.check(N.lib().es_word_read(self.device, self.ptrs[k], ctypes.byref(v)))
+        return v.value
+
+    def close(self) -> None:
+        for p in self.ptrs:
+            if p:
+                N.lib().es_ipc_close(self.device, p, 1 if self.rank == 0 else 0)
+        self.ptrs = []
+
+
+def sweep_peer(prog, peer: PeerBest, group=None, device: int | None = None) -> EsResult:
+    """run_exhaustive sharded over ``group`` with the shared peer word
+    (collective call; same program on every rank).  One launch per rank over
+    its residue class of chunks; two barriers per verdict, no all-reduce."""
+    import torch
+    import torch.distributed as dist
+
+    p = as_program(prog)
+    world, rank = peer.world, peer.rank
+    dev = peer.device if device is None else device
+    last = len(p) - 1
+    if p.src0[last] < 0:  # constant rail, es.py:265-270
+        if p.neg0[last]:
+            return EsResult(ES_COUNTEREXAMPLE, (0,) * p.num_pis, 0, 0)
+        return EsResult(EXHAUSTED_ZERO, None, 1 << p.num_pis)
+    sess = session_for(p, dev)
+    sentinel = 1 << p.num_pis
+    k = peer._step & 1
+    peer._step += 1
+    if peer._step == 1 and rank == 0:
+        peer.write(k, sentinel)
+    if world > 1:
+        dist.barrier(group=group)      # word k armed; everyone has read word k^1
+    if rank == 0:
+        peer.write(k ^ 1, sentinel)  # re-arm the other word for the next verdict
+    stream = torch.cuda.current_stream(dev)
+    sess.launch(stream.cuda_stream, peer.ptrs[k].value, 0, sess.n_chunks, rank, world)
+    stream.synchronize()
+    if world > 1:
+        dist.barrier(group=group)      # every rank's chunks are done
+    b = peer.read(k)
+    if b < sentinel:
+        lo = min(p.num_pis, 14)
+        return EsResult(ES_COUNTEREXAMPLE, tuple((b >> i) & 1 for i in range(p.num_pis)),
+                        ((b >> lo) + 1) << lo, b)
+    return EsResult(EXHAUSTED_ZERO, None, sentinel)
+
+
+def es_check_peer(sm, peer: PeerBest, group=None, device: int | None = None):
+    """``es_check`` (es.py:342-365) sharded with the shared peer word."""
+    import time
+
+    from .es import TooManyInputs, compile_program
+    from .miter import evaluate
+    from .verdict import COUNTEREXAMPLE, EQUIVALENT, UNKNOWN, CheckResult
+
+    t0 = time.monotonic()
+    try:
+        prog = compile_program(sm.circuit)
+    except TooManyInputs:
+        return CheckResult(UNKNOWN, reason="ineligible", engine="es")
+    r = sweep_peer(prog, peer, group, device)
+    stats = {"patterns": r.patterns_evaluated, "registers": prog.num_registers,
+             "wall_time": time.monotonic() - t0}
+    if r.verdict == EXHAUSTED_ZERO:
+        return CheckResult(EQUIVALENT, engine="es", stats=stats)
+    if evaluate(sm.circuit, r.witness) != 1:
+        raise AssertionError("exhaustive-simulation witness failed re-check")
+    return CheckResult(COUNTEREXAMPLE, witness=r.witness, engine="es", stats=stats)

@@ -28,7 +28,7 @@ def test_ptx_has_one_body_and_lop3():
     n_mad = sum(1 for ln in ptx.splitlines() if ln.startswith("mad.lo.s32 %esq"))
     assert ptx.count("lop3.b32") + n_mad == luts and n_mad > 0
     assert "ES_BODY" not in ptx
-    assert "atom.global.min.u64" in ptx
+    assert "atom.sys.global.min.u64" in ptx or "atom.global.sys.min.u64" in ptx
 
 
 def test_unsupported_block_size():
