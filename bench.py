@@ -297,6 +297,8 @@ def run_b200(args) -> None:
 
     from paper_2512_06627_b200 import es, shard
 
+    if args.cofactor.isdigit():
+        args.cofactor = int(args.cofactor)
     if args.config == "cones":
         run_cones(args, rank, world, local, dev)
         return
@@ -304,15 +306,23 @@ def run_b200(args) -> None:
     sm = _Sub(x)
     P = x.num_pis
 
-    # cold time-to-verdict: compile + map + JIT + sweep, first call in process
+    # cold time-to-verdict: compile + map + JIT + sweep, first call in process,
+    # once in the default latency mode (cofactor="auto") and once in the mode
+    # this bench runs (--cofactor, default "throughput": deepest profitable
+    # cofactor expansion, larger JIT)
     t = time.perf_counter()
     prog = es.compile_program(x)
-    cold = es.run_exhaustive(prog, engine="jit")
+    cold = es.run_exhaustive(prog, engine="jit", cofactor="auto")
     cold_ms = 1e3 * (time.perf_counter() - t)
+    t = time.perf_counter()
+    cold_t = es.run_exhaustive(es.compile_program(x), engine="jit", cofactor=args.cofactor)
+    cold_t_ms = 1e3 * (time.perf_counter() - t)
     G = prog.num_gates
     expected = cold.verdict
+    if (cold_t.verdict, cold_t.witness_index) != (cold.verdict, cold.witness_index):
+        raise RuntimeError("cofactor modes disagree")
 
-    sess = shard.session_for(prog, local)
+    sess = shard.session_for(prog, local, args.cofactor)
     best = torch.empty(1, dtype=torch.int64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     S = args.slices or (1 if world == 1 else 4)
@@ -331,9 +341,9 @@ def run_b200(args) -> None:
 
     def step():
         if peer is not None:
-            r = shard.sweep_peer(prog, peer, group, local)
+            r = shard.sweep_peer(prog, peer, group, local, cofactor=args.cofactor)
         else:
-            r = shard.sweep_sharded(prog, group, local, slices=S, best=best)
+            r = shard.sweep_sharded(prog, group, local, slices=S, best=best, cofactor=args.cofactor)
         if r.verdict != expected or r.witness_index != cold.witness_index:
             raise RuntimeError(f"verdict drift: {r.verdict} {r.witness_index} vs "
                                f"{expected} {cold.witness_index}")
@@ -385,17 +395,19 @@ def run_b200(args) -> None:
         launch_patterns = min(launch_patterns, r.patterns_evaluated // world + sess.patterns_per_chunk)
     lane_peak, _ = shard.alu_peak(local)
     achieved = G * launch_patterns / (k_ms * 1e-3)
-    pipes = es.map_pipes(prog)
-    lop3_rate = pipes["lop3"] * (launch_patterns / 32) / (k_ms * 1e-3)
+    kcof = cold_t.stats.get("cofactor_pis", 0)  # same program, same mode as the session
+    pipes = es.map_pipes(prog, kcof)
+    # per kernel iteration = 2^k words (one per cofactor copy)
+    lop3_rate = pipes["lop3"] * (launch_patterns / 32 / 2 ** kcof) / (k_ms * 1e-3)
 
     # e2e through the public API, host circuit in, host verdict out
     def e2e_step():
         if world == 1:
-            res = es.es_check(sm, engine="jit")
+            res = es.es_check(sm, engine="jit", cofactor=args.cofactor)
         elif peer is not None:
-            res = shard.es_check_peer(sm, peer, group, local)
+            res = shard.es_check_peer(sm, peer, group, local, cofactor=args.cofactor)
         else:
-            res = shard.es_check_sharded(sm, group, local, slices=S)
+            res = shard.es_check_sharded(sm, group, local, slices=S, cofactor=args.cofactor)
         return res
     for _ in range(max(1, args.warmup)):
         e2e_step()
@@ -440,16 +452,20 @@ def run_b200(args) -> None:
                                       "1 GPU, 1 launch per verdict",
                        "l2": "flushed between steps (256 MiB write, outside the step events); "
                              "the kernel reads no HBM inputs",
-                       "luts_per_word": sess.num_luts, "regs_per_thread": sess.regs_per_thread},
+                       "cofactor_pis": kcof, "words_per_iteration": 2 ** kcof,
+                       "luts_per_iteration": sess.num_luts,
+                       "luts_per_word": sess.num_luts / 2 ** kcof,
+                       "regs_per_thread": sess.regs_per_thread},
             "roofline": {"bound": "alu", "achieved": achieved,
                          "peak": lane_peak * 32, "unit": UNIT,
                          "frac": achieved / (lane_peak * 32), "traffic": traffic,
                          "kernel": "es_k1", "kernel_ms": k_ms,
                          "peak_source": "measured: es_alu_peak LOP3 microbenchmark on this GPU "
                                         "(lane-LOP3/s x 32 patterns, 1 gate per LOP3)",
-                         "issue": {"luts_per_word": sess.num_luts,
-                                   "lop3_per_word": pipes["lop3"],
-                                   "imad_per_word": pipes["imad"],
+                         "issue": {"luts_per_iteration": sess.num_luts,
+                                   "lop3_per_iteration": pipes["lop3"],
+                                   "imad_per_iteration": pipes["imad"],
+                                   "words_per_iteration": 2 ** kcof,
                                    "achieved_lane_lop3_per_s": lop3_rate,
                                    "peak_lane_lop3_per_s": lane_peak,
                                    "frac": lop3_rate / lane_peak,
@@ -464,6 +480,11 @@ def run_b200(args) -> None:
             "time_to_verdict": {"cold_ms": cold_ms, "jit_ms": cold.stats.get("jit_ms"),
                                 "host_compile_ms": cold.stats.get("compile_ms"),
                                 "device_ms": cold.stats.get("device_ms"),
+                                "mode": "cofactor=auto (latency: JIT + sweep estimate), "
+                                        f"k={cold.stats.get('cofactor_pis')}",
+                                f"cold_ms_{args.cofactor}": cold_t_ms,
+                                f"jit_ms_{args.cofactor}": cold_t.stats.get("jit_ms"),
+                                f"device_ms_{args.cofactor}": cold_t.stats.get("device_ms"),
                                 "warm_device_ms": total_s * 1e3 / args.steps},
             "gpu_launches": args.steps * (1 if collective == "p2p" else S) * world,
             "clocks": clk.summary(),
@@ -527,6 +548,8 @@ def main() -> None:
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--config", default="mult16")
     ap.add_argument("--slices", type=int, default=0)
+    ap.add_argument("--cofactor", default="throughput",
+                    help="K1 cofactor mode: throughput (default), auto, none, or 1..4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-extras", action="store_true")

@@ -85,7 +85,19 @@ typedef struct es_run_opts {
     double slice_ms;        /* target device time per launch slice (budget/cancel granularity) */
     int32_t block_threads;  /* 0: default */
     int32_t flags;          /* ES_FLAG_* */
+    int32_t cofactor_pis;   /* ES_COFACTOR_* or k = 1..4 (K1 only) */
 } es_run_opts;
+
+/*
+ * es_run_opts.cofactor_pis -- K1 cofactor copies.  k word PIs (PI >= 6, chosen
+ * by smallest transitive fanout) are fixed per copy instead of per word, so
+ * one kernel iteration evaluates 2^k words: the logic outside their fanout
+ * once, the folded logic inside it once per copy.  Verdict and witness are
+ * unchanged (minimum index); only the speed and the JIT cost differ.
+ */
+#define ES_COFACTOR_AUTO 0         /* minimise estimated JIT + sweep time (tiers up on reuse) */
+#define ES_COFACTOR_NONE (-1)      /* one word per iteration */
+#define ES_COFACTOR_THROUGHPUT (-2) /* maximise sweep rate; JIT cost ignored */
 
 /* es_run_opts.flags: K1 skeleton variants (default: K1) */
 #define ES_FLAG_K1T 4 /* word-uniform sub-network transposed across iterations */
@@ -106,6 +118,7 @@ typedef struct es_result {
     double wall_ms;             /* whole call */
     int32_t launches;           /* kernel launches issued */
     int32_t regs_per_thread;    /* JIT kernel register count */
+    int32_t cofactor_pis;       /* K1 cofactor PIs used (0: none) */
 } es_result;
 
 /*
@@ -217,6 +230,17 @@ int32_t es_k2_stats(const es_prog *prog, int32_t *num_gates, int32_t *num_slots,
                     int32_t *stores, int32_t *acc_reads);
 /* CPU model of the K2 program over words [w0, w0+nw) (bit-exact with K2). */
 int32_t es_k2_eval(const es_prog *prog, uint64_t w0, uint64_t nw, uint32_t *out_words);
+/* The same views for the K1 variant with k cofactor PIs (0..4, chosen as
+ * es_run does: the k word PIs of smallest transitive fanout).  es_map_eval_k
+ * takes FULL word indices (cofactor PIs included) and returns the output of
+ * the copy each word belongs to, so it is comparable with es_map_eval. */
+int32_t es_map_stats_k(const es_prog *prog, int32_t k, int32_t *num_luts, int32_t *peak_live,
+                       int32_t *num_gates, int32_t *cof_pis /* k entries, may be NULL */);
+int32_t es_map_pipes_k(const es_prog *prog, int32_t k, int32_t *lop3, int32_t *imad);
+int32_t es_map_eval_k(const es_prog *prog, int32_t k, uint64_t w0, uint64_t nw, uint32_t *out_words);
+int64_t es_emit_ptx_k(const es_prog *prog, int32_t k, int32_t block_threads, char *buf, int64_t cap);
+int64_t es_jit_check_k(const es_prog *prog, int32_t k, int32_t block_threads, int32_t *regs_per_thread,
+                       int32_t *spill_bytes, char *log, int64_t log_cap);
 /* The PTX the JIT path would compile for `prog` (buf NULL -> returns size).
  * block_threads: 128/256/512 -> K1; 32 -> K1U; -128 -> K1T. */
 int64_t es_emit_ptx(const es_prog *prog, int32_t block_threads, char *buf, int64_t cap);

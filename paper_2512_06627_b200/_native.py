@@ -24,6 +24,9 @@ ES_E_NO_DEVICE = -5
 ES_E_WITNESS = -6
 
 ENGINE_AUTO, ENGINE_JIT, ENGINE_INTERP = 0, 1, 2
+# es_run_opts.cofactor_pis (include/es_b200.h)
+COFACTOR_AUTO, COFACTOR_NONE, COFACTOR_THROUGHPUT = 0, -1, -2
+COFACTOR_MODES = {"auto": COFACTOR_AUTO, "none": COFACTOR_NONE, "throughput": COFACTOR_THROUGHPUT}
 ENGINES = {"auto": ENGINE_AUTO, "jit": ENGINE_JIT, "interp": ENGINE_INTERP}
 
 # every symbol include/es_b200.h declares
@@ -32,6 +35,7 @@ EXPORTS = ("es_compile", "es_run", "es_run_batch", "es_session_open", "es_sessio
            "es_emit_ptx", "es_jit_check", "es_alu_peak", "es_batch_extract", "es_batch_size",
            "es_batch_info", "es_batch_table", "es_batch_xag", "es_batch_select", "es_batch_run", "es_batch_merge", "es_batch_free",
            "es_ipc_alloc", "es_ipc_open", "es_ipc_close", "es_word_write", "es_word_read",
+           "es_map_stats_k", "es_map_pipes_k", "es_map_eval_k", "es_emit_ptx_k", "es_jit_check_k",
            "es_last_error", "es_version", "es_shutdown")
 
 _P = ctypes.c_void_p
@@ -47,7 +51,7 @@ class EsRunOpts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("engine", ctypes.c_int32),
                 ("budget_s", ctypes.c_double), ("cancel_flag", _P),
                 ("slice_ms", ctypes.c_double), ("block_threads", ctypes.c_int32),
-                ("flags", ctypes.c_int32)]
+                ("flags", ctypes.c_int32), ("cofactor_pis", ctypes.c_int32)]
 
 
 class EsResult(ctypes.Structure):
@@ -57,7 +61,7 @@ class EsResult(ctypes.Structure):
                 ("patterns_swept", ctypes.c_uint64), ("compile_ms", ctypes.c_double),
                 ("jit_ms", ctypes.c_double), ("device_ms", ctypes.c_double),
                 ("wall_ms", ctypes.c_double), ("launches", ctypes.c_int32),
-                ("regs_per_thread", ctypes.c_int32)]
+                ("regs_per_thread", ctypes.c_int32), ("cofactor_pis", ctypes.c_int32)]
 
 
 class NativeError(RuntimeError):
@@ -123,6 +127,18 @@ def lib():
                                    ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
                                    ctypes.c_char_p, ctypes.c_int64]
         L.es_jit_check.restype = ctypes.c_int64
+        _I = ctypes.c_int32
+        L.es_map_stats_k.argtypes = [ctypes.POINTER(EsProg), _I, _P, _P, _P, _P]
+        L.es_map_stats_k.restype = _I
+        L.es_map_pipes_k.argtypes = [ctypes.POINTER(EsProg), _I, _P, _P]
+        L.es_map_pipes_k.restype = _I
+        L.es_map_eval_k.argtypes = [ctypes.POINTER(EsProg), _I, ctypes.c_uint64, ctypes.c_uint64, _P]
+        L.es_map_eval_k.restype = _I
+        L.es_emit_ptx_k.argtypes = [ctypes.POINTER(EsProg), _I, _I, ctypes.c_char_p, ctypes.c_int64]
+        L.es_emit_ptx_k.restype = ctypes.c_int64
+        L.es_jit_check_k.argtypes = [ctypes.POINTER(EsProg), _I, _I, _P, _P, ctypes.c_char_p,
+                                     ctypes.c_int64]
+        L.es_jit_check_k.restype = ctypes.c_int64
         L.es_alu_peak.argtypes = [ctypes.c_int32, ctypes.POINTER(ctypes.c_double),
                                   ctypes.POINTER(ctypes.c_double)]
         L.es_alu_peak.restype = ctypes.c_int32

@@ -1,4 +1,5 @@
 // es_abi.cpp -- extern "C" entry points declared in include/es_b200.h.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -30,13 +31,19 @@ int ipc_open(int dev, const unsigned char *handle, void **ptr);
 int ipc_close(int dev, void *ptr, int owner);
 int word_io(int dev, void *ptr, uint64_t *value, int write);
 
-static int map_prog(const es_prog *prog, LutNet *net) {
+// k = cofactor PIs (0: none), chosen as the runtime does (rank_cofactor_pis)
+static int map_prog(const es_prog *prog, LutNet *net, int k = 0) {
     if (!prog || prog->num_instrs < 1) { set_error("empty program"); return ES_E_BAD_PROGRAM; }
+    if (k < 0 || k > kMaxCofactorPis) { set_error("cofactor PIs must be 0..4"); return ES_E_BAD_ARG; }
     Dag dag;
     std::string err;
     int rc = build_dag(*prog, &dag, &err);
     if (rc != ES_OK) { set_error(err); return rc; }
-    map_luts(dag, net);
+    if (k == 0) { map_luts(dag, net); return ES_OK; }
+    std::vector<int32_t> pis = rank_cofactor_pis(dag, k);
+    std::sort(pis.begin(), pis.end());
+    if ((int)pis.size() != k) { set_error("fewer word PIs than cofactor PIs"); return ES_E_BAD_ARG; }
+    map_cofactored(dag, pis, net);
     return ES_OK;
 }
 
@@ -95,20 +102,31 @@ void es_session_close(es_session *s) { session_close(s); }
 
 int32_t es_map_stats(const es_prog *prog, int32_t *num_luts, int32_t *peak_live,
                      int32_t *num_gates) {
+    return es_map_stats_k(prog, 0, num_luts, peak_live, num_gates, nullptr);
+}
+
+int32_t es_map_stats_k(const es_prog *prog, int32_t k, int32_t *num_luts, int32_t *peak_live,
+                       int32_t *num_gates, int32_t *cof_pis) {
     LutNet net;
-    int rc = map_prog(prog, &net);
+    int rc = map_prog(prog, &net, k);
     if (rc != ES_OK) return rc;
     if (num_luts) *num_luts = (int32_t)net.luts.size();
     if (peak_live) *peak_live = net.peak_live;
     if (num_gates) *num_gates = net.num_gates;
+    if (cof_pis)
+        for (int i = 0; i < k; ++i) cof_pis[i] = net.cof_pis[i];
     return ES_OK;
 }
 
 int32_t es_map_pipes(const es_prog *prog, int32_t *lop3, int32_t *imad) {
+    return es_map_pipes_k(prog, 0, lop3, imad);
+}
+
+int32_t es_map_pipes_k(const es_prog *prog, int32_t k, int32_t *lop3, int32_t *imad) {
     LutNet net;
-    int rc = map_prog(prog, &net);
+    int rc = map_prog(prog, &net, k);
     if (rc != ES_OK) return rc;
-    const std::string body = emit_body_ptx(net, "%o", "%lo", "%hi", "%one");
+    const std::string body = emit_body_ptx(net, {"%o", "%c"}, "%lo", "%hi", "%one");
     int nl = 0, ni = 0;
     for (size_t p = 0; (p = body.find("lop3.b32 %esq", p)) != std::string::npos; ++p) ++nl;
     for (size_t p = 0; (p = body.find("mad.lo.s32 %esq", p)) != std::string::npos; ++p) ++ni;
@@ -118,8 +136,12 @@ int32_t es_map_pipes(const es_prog *prog, int32_t *lop3, int32_t *imad) {
 }
 
 int32_t es_map_eval(const es_prog *prog, uint64_t w0, uint64_t nw, uint32_t *out_words) {
+    return es_map_eval_k(prog, 0, w0, nw, out_words);
+}
+
+int32_t es_map_eval_k(const es_prog *prog, int32_t k, uint64_t w0, uint64_t nw, uint32_t *out_words) {
     LutNet net;
-    int rc = map_prog(prog, &net);
+    int rc = map_prog(prog, &net, k);
     if (rc != ES_OK) return rc;
     eval_lutnet(net, w0, nw, out_words);
     return ES_OK;
@@ -159,8 +181,12 @@ int32_t es_k2_eval(const es_prog *prog, uint64_t w0, uint64_t nw, uint32_t *out_
 }
 
 int64_t es_emit_ptx(const es_prog *prog, int32_t block_threads, char *buf, int64_t cap) {
+    return es_emit_ptx_k(prog, 0, block_threads, buf, cap);
+}
+
+int64_t es_emit_ptx_k(const es_prog *prog, int32_t k, int32_t block_threads, char *buf, int64_t cap) {
     LutNet net;
-    int rc = map_prog(prog, &net);
+    int rc = map_prog(prog, &net, k);
     if (rc != ES_OK) return rc;
     std::string ptx, err;
     if (!splice_body(net, block_threads != 0 ? block_threads : 256, &ptx, &err)) {
@@ -177,8 +203,13 @@ int64_t es_emit_ptx(const es_prog *prog, int32_t block_threads, char *buf, int64
 
 int64_t es_jit_check(const es_prog *prog, int32_t block_threads, int32_t *regs_per_thread,
                      int32_t *spill_bytes, char *log, int64_t log_cap) {
+    return es_jit_check_k(prog, 0, block_threads, regs_per_thread, spill_bytes, log, log_cap);
+}
+
+int64_t es_jit_check_k(const es_prog *prog, int32_t k, int32_t block_threads, int32_t *regs_per_thread,
+                       int32_t *spill_bytes, char *log, int64_t log_cap) {
     LutNet net;
-    int rc = map_prog(prog, &net);
+    int rc = map_prog(prog, &net, k);
     if (rc != ES_OK) return rc;
     std::string ptx, err, info;
     if (!splice_body(net, block_threads != 0 ? block_threads : 256, &ptx, &err)) {

@@ -214,13 +214,17 @@ void map_luts(const Dag &dag, LutNet *net) {
     net->pis_used.clear();
     net->is_const.assign(N, 0);
     net->const_val.assign(N, 0);
-    net->out_node = dag.out_node;
-    net->out_neg = dag.out_neg;
     net->num_gates = 0;
     net->peak_live = 0;
+    net->cof_pis.clear();
+    net->pi_bit.assign(P + 1, -1);
+    for (int j = kLanePis + 1; j <= P; ++j) net->pi_bit[j] = (int8_t)(j - kLanePis - 1);
+    std::vector<int32_t> outs = dag.outs;
+    std::vector<uint8_t> outs_neg = dag.outs_neg;
+    if (outs.empty()) { outs.push_back(dag.out_node); outs_neg.push_back(dag.out_neg); }
 
     std::vector<uint8_t> cone(N, 0);
-    cone[dag.out_node] = 1;
+    for (int32_t o : outs) cone[o] = 1;
     for (int v = N - 1; v >= FG; --v) {
         if (!cone[v]) continue;
         const int g = v - FG;
@@ -232,7 +236,7 @@ void map_luts(const Dag &dag, LutNet *net) {
     isc[0] = 1; cv[0] = 0;
     for (int j = 1; j <= std::min(P, kLanePis); ++j) { isc[j] = 1; cv[j] = kLaneMask[j - 1]; }
     std::vector<int32_t> fo(N, 0);
-    fo[dag.out_node] += 1;
+    for (int32_t o : outs) fo[o] += 1;
     for (int v = FG; v < N; ++v) {
         if (!cone[v]) continue;
         const int g = v - FG;
@@ -344,10 +348,13 @@ void map_luts(const Dag &dag, LutNet *net) {
         }
         return area;
     };
-    const int out = dag.out_node;
-    if (is_gate_lut(out)) {
-        mref[out] = 1;
-        ref_cut(out, cuts[out][best[out]]);
+    bool any_gate_out = false;
+    for (int32_t o : outs) {
+        if (!is_gate_lut(o)) continue;
+        any_gate_out = true;
+        if (mref[o]++ == 0) ref_cut(o, cuts[o][best[o]]);
+    }
+    if (any_gate_out) {
         for (int pass = 0; pass < 3; ++pass) {
             for (int v = FG; v < N; ++v) {
                 if (!is_gate_lut(v) || mref[v] == 0) continue;
@@ -378,11 +385,11 @@ void map_luts(const Dag &dag, LutNet *net) {
             else if (l >= 1 && l <= P && !isc[l]) pi_used[l] = 1;
         }
     }
-    if (out >= 1 && out <= P && !isc[out]) pi_used[out] = 1;
+    for (int32_t o : outs)
+        if (o >= 1 && o <= P && !isc[o]) pi_used[o] = 1;
     for (int j = 1; j <= P; ++j) if (pi_used[j]) net->pis_used.push_back(j);
-    std::vector<uint8_t> done(N, 0);
     std::vector<int> order;
-    if (is_gate_lut(out)) {
+    if (any_gate_out) {
         // need() bottom-up in topological order
         for (int v = FG; v < N; ++v) {
             if (!is_gate_lut(v) || mref[v] == 0) continue;
@@ -394,26 +401,80 @@ void map_luts(const Dag &dag, LutNet *net) {
             for (int q = 0; q < k; ++q) nd = std::max(nd, kn[q] + q);
             need[v] = nd;
         }
-        // iterative DFS
-        std::vector<int> st{out};
-        while (!st.empty()) {
-            const int v = st.back();
-            if (done[v]) { st.pop_back(); continue; }
-            const Cut &c = cuts[v][best[v]];
-            int pick = -1;
-            for (int q = 0; q < c.n; ++q) {  // highest-need pending child first
-                int l = c.leaf[q];
-                if (is_gate_lut(l) && !done[l] && (pick < 0 || need[l] > need[pick])) pick = l;
+    }
+    // iterative DFS from each output in turn, highest-need pending child first
+    auto dfs = [&](const std::vector<int32_t> &roots) {
+        std::vector<uint8_t> dn(N, 0);
+        std::vector<int> ord, st;
+        for (int32_t o : roots) {
+            if (!is_gate_lut(o) || dn[o]) continue;
+            st.push_back(o);
+            while (!st.empty()) {
+                const int v = st.back();
+                if (dn[v]) { st.pop_back(); continue; }
+                const Cut &c = cuts[v][best[v]];
+                int pick = -1;
+                for (int q = 0; q < c.n; ++q) {
+                    int l = c.leaf[q];
+                    if (is_gate_lut(l) && !dn[l] && (pick < 0 || need[l] > need[pick])) pick = l;
+                }
+                if (pick >= 0) { st.push_back(pick); continue; }
+                dn[v] = 1;
+                ord.push_back(v);
+                st.pop_back();
             }
-            if (pick >= 0) { st.push_back(pick); continue; }
-            done[v] = 1;
-            order.push_back(v);
-            st.pop_back();
+        }
+        return ord;
+    };
+    // peak simultaneously-live LUT values of an order
+    auto peak_of = [&](const std::vector<int> &ord) {
+        std::vector<int> rem = users;
+        for (int32_t o : outs)
+            if (is_gate_lut(o)) rem[o] += 1;
+        int live = 0, peak = 0;
+        for (int v : ord) {
+            const Cut &c = cuts[v][best[v]];
+            int freed = 0;
+            for (int q = 0; q < c.n; ++q) {
+                int l = c.leaf[q];
+                bool seen = false;
+                for (int r = 0; r < q; ++r) seen |= c.leaf[r] == l;
+                if (seen || !is_gate_lut(l)) continue;
+                if (--rem[l] == 0) ++freed;
+            }
+            live = live - freed + 1;
+            peak = std::max(peak, live);
+        }
+        return peak;
+    };
+    if (any_gate_out) {
+        order = dfs(outs);
+        if (outs.size() > 1) {
+            // cofactor copies: also try the most demanding copies first and keep
+            // the order with the smaller live set (fewer spills at 255 registers)
+            std::vector<int32_t> by_need = outs;
+            std::stable_sort(by_need.begin(), by_need.end(), [&](int a, int b) {
+                const int na = is_gate_lut(a) ? need[a] : 0, nb = is_gate_lut(b) ? need[b] : 0;
+                return na > nb;
+            });
+            std::vector<int> alt = dfs(by_need);
+            if (peak_of(alt) < peak_of(order)) order.swap(alt);
+        }
+    }
+    // an output's inversion folds into its root LUT when nothing else reads it
+    std::vector<uint8_t> out_count(N, 0), fold(N, 0);
+    for (int32_t o : outs) out_count[o] = (uint8_t)std::min(2, out_count[o] + 1);
+    for (size_t c = 0; c < outs.size(); ++c) {
+        const int o = outs[c];
+        if (is_gate_lut(o) && users[o] == 0 && out_count[o] == 1 && outs_neg[c]) {
+            fold[o] = 1;
+            outs_neg[c] = 0;
         }
     }
     // emit LUTs and measure the live set
     std::vector<int> remaining = users;
-    if (is_gate_lut(out)) remaining[out] += 1;
+    for (int32_t o : outs)
+        if (is_gate_lut(o)) remaining[o] += 1;
     int live = 0;
     for (int v : order) {
         const Cut &c = cuts[v][best[v]];
@@ -422,7 +483,7 @@ void map_luts(const Dag &dag, LutNet *net) {
         L.nleaves = c.n;
         for (int q = 0; q < 3; ++q) L.leaf[q] = q < c.n ? c.leaf[q] : c.leaf[0];
         L.tt = c.tt;
-        if (v == out && dag.out_neg) L.tt = (uint8_t)~L.tt;
+        if (fold[v]) L.tt = (uint8_t)~L.tt;
         net->luts.push_back(L);
         int freed = 0;
         for (int q = 0; q < c.n; ++q) {
@@ -435,7 +496,10 @@ void map_luts(const Dag &dag, LutNet *net) {
         live = live - freed + 1;
         net->peak_live = std::max(net->peak_live, live);
     }
-    if (is_gate_lut(out)) net->out_neg = false;  // folded into the root LUT
+    net->outs = outs;
+    net->outs_neg = outs_neg;
+    net->out_node = outs[0];
+    net->out_neg = outs_neg[0];
 }
 
 // ---------------------------------------------------------------------------
@@ -448,11 +512,15 @@ void eval_lutnet(const LutNet &net, uint64_t w0, uint64_t nw, uint32_t *out) {
     const uint32_t valid = lane_valid_mask(net.num_pis);
     for (uint64_t k = 0; k < nw; ++k) {
         const uint64_t w = w0 + k;
+        // w is the full word index: PI j >= 6 is bit j-6 of it, cofactor PIs
+        // included -- their bits select the copy whose output is this word's
         for (int j : net.pis_used) val[j] = ((w >> (j - 6)) & 1) ? ~0u : 0u;
         for (const Lut &L : net.luts)
             val[L.node] = lut3(L.tt, val[L.leaf[2]], val[L.leaf[1]], val[L.leaf[0]]);
-        uint32_t o = val[net.out_node];
-        if (net.out_neg) o = ~o;
+        size_t c = 0;
+        for (size_t b = 0; b < net.cof_pis.size(); ++b) c |= (size_t)((w >> (net.cof_pis[b] - 6)) & 1) << b;
+        uint32_t o = val[net.outs[c]];
+        if (net.outs_neg[c]) o = ~o;
         out[k] = o & valid;
     }
 }
@@ -503,7 +571,7 @@ bool plan_imad(const Lut &L, const std::vector<uint8_t> &sel, ImadPlan *pl) {
 }
 }  // namespace
 
-std::string emit_body_ptx(const LutNet &net, const std::string &out,
+std::string emit_body_ptx(const LutNet &net, const std::vector<std::string> &outs,
                           const std::string &wlo, const std::string &whi,
                           const std::string &one) {
     const int N = (int)net.is_const.size();
@@ -564,17 +632,38 @@ std::string emit_body_ptx(const LutNet &net, const std::string &out,
         }
         return r;
     };
+    // Cofactor copies: fold each copy's output into (first failing word, its
+    // copy number) as soon as it exists -- 3 ops per copy, 2 live registers.
+    const bool multi = net.outs.size() > 1;
+    std::vector<uint8_t> emitted(N, 0);
+    size_t next_copy = 0;
+    auto flush_outputs = [&]() {
+        while (multi && next_copy < net.outs.size()) {
+            const int o = net.outs[next_copy];
+            if (lut_idx[o] >= 0 && !emitted[o]) break;
+            std::string v = name(o);
+            if (net.outs_neg[next_copy]) { body << "not.b32 %est, " << v << ";\n"; v = "%est"; }
+            body << "setp.eq.b32 %espz, " << outs[0] << ", 0;\n"
+                 << "selp.b32 " << outs[0] << ", " << v << ", " << outs[0] << ", %espz;\n"
+                 << "selp.b32 " << outs[1] << ", " << next_copy << ", " << outs[1] << ", %espz;\n";
+            ++next_copy;
+        }
+    };
+    flush_outputs();
     for (const Lut &L : net.luts) {
         ImadPlan pl;
         if (imad && plan_imad(L, sel, &pl)) {
             const std::string S = coef_reg(pl.u, pl.s0, pl.s1), T = coef_reg(pl.u, pl.t0, pl.t1);
             body << "mad.lo.s32 " << name(L.node) << ", " << name(pl.x) << ", " << S << ", " << T << ";\n";
-            continue;
+        } else {
+            body << "lop3.b32 " << name(L.node) << ", " << name(L.leaf[2]) << ", " << name(L.leaf[1])
+                 << ", " << name(L.leaf[0]) << ", " << (int)L.tt << ";\n";
         }
-        body << "lop3.b32 " << name(L.node) << ", " << name(L.leaf[2]) << ", " << name(L.leaf[1])
-             << ", " << name(L.leaf[0]) << ", " << (int)L.tt << ";\n";
+        emitted[L.node] = 1;
+        flush_outputs();
     }
-    const std::string oname = name(net.out_node);
+    std::vector<std::string> onames;
+    if (!multi) onames.push_back(name(net.outs[0]));
     s << "{\n";
     if (!net.luts.empty()) s << ".reg .b32 %esq<" << net.luts.size() << ">;\n";
     if (!consts.empty()) s << ".reg .b32 %esk<" << consts.size() << ">;\n";
@@ -582,9 +671,11 @@ std::string emit_body_ptx(const LutNet &net, const std::string &out,
     if (!coef.empty()) s << ".reg .b32 %esc<" << coef.size() << ">;\n";
     for (size_t k = 0; k < consts.size(); ++k) s << "mov.b32 %esk" << k << ", " << consts[k] << ";\n";
     if (imad) s << ".reg .b32 %esneg1;\nneg.s32 %esneg1, " << one << ";\n";
+    if (multi)
+        s << ".reg .pred %espz;\n.reg .b32 %est;\nmov.b32 " << outs[0] << ", 0;\nmov.b32 " << outs[1] << ", 0;\n";
     for (int j = 6; j <= P; ++j) {
         if (!pi_mask[j]) continue;
-        const int bit = j - 6;
+        const int bit = net.pi_bit[j];  // bit of the kernel's word index
         const std::string &src = bit < 32 ? wlo : whi;
         if (imad) {  // mask on the FMA pipe: bit to the sign by a multiply, spread by mul.hi
             s << "mul.lo.u32 %esm" << j << ", " << src << ", " << (1u << (31 - (bit & 31))) << ";\n";
@@ -595,8 +686,8 @@ std::string emit_body_ptx(const LutNet &net, const std::string &out,
         }
     }
     s << body.str();
-    if (net.out_neg) s << "not.b32 " << out << ", " << oname << ";\n";
-    else s << "mov.b32 " << out << ", " << oname << ";\n";
+    if (!multi)
+        s << (net.outs_neg[0] ? "not.b32 " : "mov.b32 ") << outs[0] << ", " << onames[0] << ";\n";
     s << "}\n";
     return s.str();
 }

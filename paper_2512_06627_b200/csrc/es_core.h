@@ -33,6 +33,11 @@ struct Dag {
     std::vector<uint8_t> n0, n1;     // fanin complement flags, per gate
     int32_t out_node = 0;
     bool out_neg = false;
+    // Multi-output graphs (cofactor expansion, es_cofactor.cpp): when `outs`
+    // is non-empty it replaces (out_node, out_neg); output c is the miter
+    // output under cofactor assignment c.
+    std::vector<int32_t> outs;
+    std::vector<uint8_t> outs_neg;
     int num_nodes() const { return 1 + num_pis + (int)is_xor.size(); }
     int first_gate() const { return 1 + num_pis; }
     bool is_pi(int v) const { return v >= 1 && v <= num_pis; }
@@ -60,6 +65,14 @@ struct LutNet {
     // output: either a LUT/PI/constant node with optional inversion folded in
     int32_t out_node = 0;
     bool out_neg = false;                 // inversion still to apply (only when out is a leaf)
+    // all outputs, one per cofactor copy (outs[0] == out_node); 1 without cofactoring
+    std::vector<int32_t> outs;
+    std::vector<uint8_t> outs_neg;
+    // Cofactor PIs (ascending, all >= 6): their values are fixed per copy, not
+    // per word, so the kernel's word index w' enumerates the other PIs only.
+    // pi_bit[j] = bit of w' carrying PI j (-1 for lane PIs 1..5 and cofactor PIs).
+    std::vector<int32_t> cof_pis;
+    std::vector<int8_t> pi_bit;
     int num_gates = 0;                    // AND+XOR gates in the output cone
     int peak_live = 0;                    // max simultaneously live LUT values in the schedule
     std::vector<int32_t> pis_used;        // PIs >= 6 referenced as leaves
@@ -67,7 +80,24 @@ struct LutNet {
 
 // LUT-3 technology mapping (priority cuts + area flow + exact-area recovery)
 // followed by a live-range-minimising schedule.
+// Multi-output graphs map every output; cof_pis/pi_bit are left for the
+// caller (default: no cofactors, pi_bit[j] = j - 6).
 void map_luts(const Dag &dag, LutNet *net);
+
+// Cofactor expansion (es_cofactor.cpp).  A PI that is fixed per copy is a
+// constant inside each copy, so the logic in its transitive fanout folds;
+// logic outside it is shared by all copies (structural hashing).  One kernel
+// iteration then evaluates 2^k words -- one per assignment of the k cofactor
+// PIs -- for the price of the shared logic once plus the folded copies.
+constexpr int kMaxCofactorPis = 4;
+// Rank word PIs (>= 6) by transitive-fanout size (cheapest first) and return
+// the first `k` of that order (rank order: sort before cofactor_expand).
+std::vector<int32_t> rank_cofactor_pis(const Dag &dag, int k);
+// dag with the PIs in `pis` (ascending) cofactored: 2^k outputs, output c
+// under PI pis[b] = bit b of c.  Constant propagation + structural hashing.
+void cofactor_expand(const Dag &dag, const std::vector<int32_t> &pis, Dag *out);
+// map_luts of the expansion, with cof_pis / pi_bit filled in.
+void map_cofactored(const Dag &dag, const std::vector<int32_t> &pis, LutNet *net);
 
 // Reference compile_program (es.py:87-163), exact.
 int32_t ref_compile(int32_t num_pis, int32_t num_gates, const uint8_t *kind,
@@ -82,7 +112,9 @@ void eval_lutnet(const LutNet &net, uint64_t w0, uint64_t nw, uint32_t *out);
 // writes the output word to `out` (register names from the skeleton).
 // `one` names a register holding 1 that ptxas cannot constant-fold; with it,
 // LUTs of the form f(x, word PI) become FMA-pipe IMADs (empty: LOP3 only).
-std::string emit_body_ptx(const LutNet &net, const std::string &out,
+// Without cofactors `outs` = {output word}; with them {first failing copy's
+// word (0: none), that copy's number} -- the K1 multi skeleton's operands.
+std::string emit_body_ptx(const LutNet &net, const std::vector<std::string> &outs,
                           const std::string &wlo, const std::string &whi,
                           const std::string &one = "");
 

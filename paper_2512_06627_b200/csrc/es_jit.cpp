@@ -19,13 +19,14 @@
 
 namespace es {
 
-#include "k1_skeleton_ptx.inc"  // kK1Ptx128/256/512 (K1), kK1UPtx32 (K1U)
+#include "k1_skeleton_ptx.inc"  // kK1Ptx<threads>_<copies> (K1), kK1UPtx32 (K1U), kK1TPtx128 (K1T)
 
-static const char *skeleton_for(int threads) {
+static const char *skeleton_for(int threads, int copies) {
+    const bool multi = copies > 1;
     switch (threads) {
-        case 128: return kK1Ptx128;
-        case 256: return kK1Ptx256;
-        case 512: return kK1Ptx512;
+        case 128: return multi ? kK1Ptx128_1 : kK1Ptx128_0;
+        case 256: return multi ? kK1Ptx256_1 : kK1Ptx256_0;
+        case 512: return multi ? nullptr : kK1Ptx512_0;
         default: return nullptr;
     }
 }
@@ -82,10 +83,19 @@ static bool splice_body_t(const LutNet &net, std::string *ptx, std::string *err,
 bool splice_body(const LutNet &net, int threads, std::string *ptx, std::string *err,
                  int *region_bytes) {
     if (region_bytes) *region_bytes = 0;
+    const int copies = (int)net.outs.size();
+    if ((threads == kK1UThreads || threads == kK1TThreads) && copies != 1) {
+        *err = "K1U/K1T take no cofactor copies";
+        return false;
+    }
     if (threads == kK1UThreads) return splice_body_u(net, ptx, err);
     if (threads == kK1TThreads) return splice_body_t(net, ptx, err, region_bytes);
-    const char *sk = skeleton_for(threads);
-    if (!sk) { *err = "unsupported K1 block size " + std::to_string(threads); return false; }
+    const char *sk = skeleton_for(threads, copies);
+    if (!sk) {
+        *err = "unsupported K1 variant: " + std::to_string(threads) + " threads x " +
+               std::to_string(copies) + " copies";
+        return false;
+    }
     std::string s(sk);
     const std::string marker = "// ES_BODY ";
     size_t at = s.find(marker);
@@ -94,13 +104,16 @@ bool splice_body(const LutNet &net, int threads, std::string *ptx, std::string *
         return false;
     }
     size_t eol = s.find('\n', at);
-    std::string args = s.substr(at + marker.size(), eol - at - marker.size());
-    char out[64], wlo[64], whi[64], one[64];
-    if (sscanf(args.c_str(), "%63s %63s %63s %63s", out, wlo, whi, one) != 4) {
-        *err = "cannot parse ES_BODY operands: " + args;
+    std::istringstream in(s.substr(at + marker.size(), eol - at - marker.size()));
+    std::vector<std::string> a;
+    for (std::string t; in >> t;) a.push_back(t);
+    const int nout = copies > 1 ? 2 : 1;  // (first failing word, its copy) or the output word
+    if ((int)a.size() != nout + 3) {
+        *err = "cannot parse ES_BODY operands (" + std::to_string(a.size()) + ")";
         return false;
     }
-    std::string body = emit_body_ptx(net, out, wlo, whi, one);
+    const std::vector<std::string> outs(a.begin(), a.begin() + nout);
+    std::string body = emit_body_ptx(net, outs, a[nout], a[nout + 1], a[nout + 2]);
     s.replace(at, eol - at, body);
     if (const char *m = getenv("ES_MAXNREG")) {  // experiment: register cap for occupancy
         const size_t mt = s.find(".maxntid");

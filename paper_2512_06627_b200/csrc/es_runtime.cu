@@ -45,6 +45,8 @@ struct K1Params {
     unsigned int valid_mask;
     unsigned int one;
     unsigned int region_bytes;
+    unsigned int cof_n;
+    unsigned int cof_pos[4];
 };
 
 // ---------------------------------------------------------------------------
@@ -316,10 +318,23 @@ struct K1Plan {
     int threads = 256;     // CTA size
     size_t smem = 0;       // dynamic shared bytes (K1T)
     int chunk_log2 = 8;
-    uint64_t total_words = 1;
+    uint64_t total_words = 1;  // of the kernel's word index (cofactor PIs excluded)
     uint64_t n_chunks = 1;
     int grid = 1;
     uint32_t valid = 0;
+    int cof_n = 0;             // cofactor PIs: 2^cof_n words per iteration
+    unsigned cof_pos[4] = {0, 0, 0, 0};
+    // pattern index of the first pattern of chunk c (copy 0): the kernel's
+    // es_expand on the host; monotone in c
+    uint64_t first_pattern(uint64_t c) const {
+        uint64_t x = (c << chunk_log2) << 5;
+        for (int i = 0; i < cof_n; ++i) {
+            const unsigned sh = cof_pos[i];
+            x = ((x >> sh) << (sh + 1)) | (x & ((1ull << sh) - 1ull));
+        }
+        return x;
+    }
+    uint64_t patterns_per_chunk() const { return 1ull << (chunk_log2 + 5 + cof_n); }
 };
 
 int k1_prepare(const LutNet &net, int threads, int sms, K1Plan *pl, double *jit_ms,
@@ -335,7 +350,10 @@ int k1_prepare(const LutNet &net, int threads, int sms, K1Plan *pl, double *jit_
     pl->threads = pl->jk->block;
     pl->smem = threads == kK1TThreads ? (size_t)pl->jk->region_bytes * (pl->jk->block / 32) : 0;
     const int P = net.num_pis;
-    pl->total_words = 1ull << std::max(P - 5, 0);
+    pl->cof_n = (int)net.cof_pis.size();
+    if (pl->cof_n > 4 || (pl->cof_n > 0 && P - 5 - pl->cof_n < 0)) { set_error("bad cofactor set"); return ES_E_BAD_ARG; }
+    for (int i = 0; i < pl->cof_n; ++i) pl->cof_pos[i] = (unsigned)(net.cof_pis[i] - 1);
+    pl->total_words = 1ull << std::max(P - 5 - pl->cof_n, 0);
     int nb = 0;
     if (pl->smem > 48 * 1024)
         CK(cudaFuncSetAttribute((const void *)pl->jk->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->smem));
@@ -363,6 +381,8 @@ int k1_launch(const K1Plan &pl, cudaStream_t st, unsigned long long *best, unsig
     kp.valid_mask = pl.valid;
     kp.one = 1u;
     kp.region_bytes = (unsigned)pl.jk->region_bytes;
+    kp.cof_n = (unsigned)pl.cof_n;
+    for (int i = 0; i < 4; ++i) kp.cof_pos[i] = pl.cof_pos[i];
     CK(cudaMemsetAsync(counter, 0, sizeof(unsigned), st));
     void *args[] = {&kp};
     const int grid = (int)std::min<uint64_t>((uint64_t)pl.grid, std::max<uint64_t>(n_slots, 1));
@@ -372,15 +392,20 @@ int k1_launch(const K1Plan &pl, cudaStream_t st, unsigned long long *best, unsig
 
 // K1 skeleton choice: opts.flags bit 2 -> K1T, bit 3 -> K1U, else K1 at
 // opts.block_threads (default 128).
-static int k1_threads(const es_run_opts &o) {
+// Default CTA size: 128 for one word per iteration (165 registers: 3 CTAs
+// per SM), 256 with cofactor copies (255 registers; measured 10-15% faster).
+static int k1_threads(const es_run_opts &o, int cofactor_pis = 0) {
     if (o.flags & ES_FLAG_K1T) return kK1TThreads;
     if (o.flags & ES_FLAG_K1U) return kK1UThreads;
-    return o.block_threads > 0 ? o.block_threads : 128;
+    return o.block_threads > 0 ? o.block_threads : cofactor_pis > 0 ? 256 : 128;
+}
+static int k1_slot(int threads) {
+    return threads == 128 ? 0 : threads == 256 ? 1 : threads == 512 ? 2 : threads == kK1UThreads ? 3 : 4;
 }
 
 static int run_k1(const LutNet &net, int G, const es_run_opts &o, Ctx *c, double deadline,
                   es_result *r, JitKernel **jk_cache) {
-    const int threads = k1_threads(o);
+    const int threads = k1_threads(o, (int)net.cof_pis.size());
     K1Plan pl;
     double jit_ms = 0;
     int rc = k1_prepare(net, threads, c->sms, &pl, &jit_ms, *jk_cache);
@@ -389,9 +414,10 @@ static int run_k1(const LutNet &net, int G, const es_run_opts &o, Ctx *c, double
     r->engine = ES_ENGINE_JIT;
     r->jit_ms = jit_ms;
     r->regs_per_thread = pl.jk->regs;
+    r->cofactor_pis = pl.cof_n;
     const int P = net.num_pis;
     const uint64_t sentinel = 1ull << P;
-    const uint64_t chunk_patterns = 1ull << (pl.chunk_log2 + 5);
+    const uint64_t chunk_patterns = pl.patterns_per_chunk();
     // slice size from a conservative throughput estimate
     const bool sliced = deadline >= 0 || o.cancel_flag != nullptr;
     const double slice_ms = o.slice_ms > 0 ? o.slice_ms : 20.0;
@@ -423,7 +449,8 @@ static int run_k1(const LutNet &net, int G, const es_run_opts &o, Ctx *c, double
             CK(cudaEventSynchronize(c->ev_slice[q]));
             completed_chunks = slice_end[launches - 2];
             best = c->h_pin[1 + q];
-            if (best < sentinel && best < completed_chunks * chunk_patterns) found = true;
+            // every chunk below `completed_chunks` is swept: nothing smaller can appear
+            if (best < sentinel && best < pl.first_pattern(completed_chunks)) found = true;
         }
     }
     CK(cudaEventRecord(c->ev_stop, c->stream));
@@ -777,10 +804,27 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
 // Mapped programs cached by a hash of the program arrays: a warm call skips
 // graph rebuild, mapping, PTX emission and the JIT-cache lookup.
 struct MappedProg {
-    LutNet net;
+    Dag dag;
+    LutNet net;                      // no cofactors
     int G = 0;
-    JitKernel *jk[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // K1 128/256/512, K1U, K1T
+    // cofactor variants k = 1..kMaxCofactorPis, mapped on demand
+    std::vector<int32_t> cof_rank;   // the kMaxCofactorPis cheapest word PIs, by fanout
+    std::unique_ptr<LutNet> cof[kMaxCofactorPis + 1];
+    // K1 kernels per (k, skeleton): 128/256/512, K1U, K1T
+    JitKernel *jk[kMaxCofactorPis + 1][5] = {};
+    int runs = 0;                    // K1 runs so far (the reuse estimate of the auto policy)
     std::mutex mu;
+    const LutNet &variant(int k) {   // caller holds mu
+        if (k == 0) return net;
+        if (!cof[k]) {
+            if (cof_rank.empty()) cof_rank = rank_cofactor_pis(dag, kMaxCofactorPis);
+            std::vector<int32_t> pis(cof_rank.begin(), cof_rank.begin() + std::min<size_t>(k, cof_rank.size()));
+            std::sort(pis.begin(), pis.end());
+            cof[k].reset(new LutNet());
+            map_cofactored(dag, pis, cof[k].get());
+        }
+        return *cof[k];
+    }
 };
 
 static uint64_t prog_hash(const es_prog &p) {
@@ -812,6 +856,7 @@ static int get_mapped(const es_prog &p, std::shared_ptr<MappedProg> *out) {
     if (rc != ES_OK) { set_error(err); return rc; }
     auto mp = std::make_shared<MappedProg>();
     map_luts(dag, &mp->net);
+    mp->dag = std::move(dag);
     for (int i = 0; i < p.num_instrs; ++i) mp->G += (p.op[i] == ES_OP_AND || p.op[i] == ES_OP_XOR);
     std::lock_guard<std::mutex> lk(g_mapped_mu);
     if (g_mapped.size() >= 4096) g_mapped.clear();  // bound host memory for long sweeps
@@ -842,6 +887,48 @@ static int validate(const es_prog &p) {
         return ES_E_BAD_PROGRAM;
     }
     return ES_OK;
+}
+
+// K1 cofactor depth (es_cofactor.cpp).  Estimates from round-1 B200
+// measurements: ~1.9e13 LUT-words/s per 148 SMs for the sweep, ~0.1 ms of
+// PTX->SASS per LUT for the JIT (mult16: 1,549 LUTs in 140 ms).
+static double est_sweep_ms(const LutNet &n, int P, int sms) {
+    const int k = (int)n.cof_pis.size();
+    // beyond ~330 live values the kernel spills (255-register cap): ~10% at 358
+    const double spill = std::max(1.0, n.peak_live / 330.0);
+    return 1e3 * spill * (double)n.luts.size() * std::ldexp(1.0, std::max(P - 5 - k, 0)) /
+           (1.9e13 * sms / 148.0);
+}
+static double est_jit_ms(const LutNet &n) { return 0.1 * (double)n.luts.size(); }
+
+static int choose_cofactors(MappedProg &mp, const es_run_opts &o, int sms) {
+    const int P = mp.dag.num_pis;
+    if (o.flags & (ES_FLAG_K1T | ES_FLAG_K1U)) return 0;
+    if (o.cofactor_pis == ES_COFACTOR_NONE) return 0;
+    if (o.cofactor_pis > 0) {  // forced: any k the word PIs allow
+        if (P - 5 < 1) return 0;
+        const LutNet &n = mp.variant(std::min(o.cofactor_pis, std::min(kMaxCofactorPis, P - 5)));
+        return (int)n.cof_pis.size();
+    }
+    // keep >= 2^14 kernel words so the grid still fills the GPU
+    const int kmax = std::max(0, std::min(kMaxCofactorPis, P - 5 - 14));
+    if (kmax == 0) return 0;
+    const bool tput = o.cofactor_pis == ES_COFACTOR_THROUGHPUT;
+    const double sweep0 = est_sweep_ms(mp.net, P, sms);
+    // latency mode: a short sweep is JIT-bound; don't even map the variants
+    if (!tput && sweep0 * (1 + mp.runs) < 0.1 * est_jit_ms(mp.net)) return 0;
+    const double reuse = 1.0 + mp.runs;  // doubling rule: expect as many more runs as so far
+    int best = 0;
+    double best_cost = 1e300;
+    for (int k = 0; k <= kmax; ++k) {
+        const LutNet &n = mp.variant(k);
+        if ((int)n.cof_pis.size() != k) break;  // fewer candidate PIs than k
+        const double sweep = est_sweep_ms(n, P, sms);
+        const int slot = k1_slot(k1_threads(o, k));
+        const double cost = tput ? sweep : (mp.jk[k][slot] ? 0.0 : est_jit_ms(n)) + sweep * reuse;
+        if (cost < best_cost) { best_cost = cost; best = k; }
+    }
+    return best;
 }
 
 int run_one(const es_prog *prog, const es_run_opts *opts, es_result *out) {
@@ -880,11 +967,15 @@ int run_one(const es_prog *prog, const es_run_opts *opts, es_result *out) {
         std::vector<int> act{0};
         rc = run_k2(1, prog, act, o, c, deadline, out);
     } else {
-        const int threads = k1_threads(o);
-        const int slot = threads == 128 ? 0 : threads == 256 ? 1 : threads == 512 ? 2
-                       : threads == kK1UThreads ? 3 : 4;
         std::lock_guard<std::mutex> lk(mp->mu);
-        rc = run_k1(net, G, o, c, deadline, out, &mp->jk[slot]);
+        const double tc = now_ms();
+        const int k = choose_cofactors(*mp, o, c->sms);
+        const int slot = k1_slot(k1_threads(o, k));
+        const LutNet &kn = mp->variant(k);
+        out->compile_ms += now_ms() - tc;
+        out->num_luts = (int)kn.luts.size();
+        rc = run_k1(kn, G, o, c, deadline, out, &mp->jk[k][slot]);
+        mp->runs++;
     }
     out->wall_ms = now_ms() - t0;
     return rc;
@@ -945,9 +1036,15 @@ int session_open(const es_prog *prog, const es_run_opts *opts, void **out) {
     Session *s = new Session();
     s->dev = o.device;
     s->num_pis = prog->num_pis;
-    map_luts(dag, &s->net);
+    {
+        std::shared_ptr<MappedProg> mp;
+        rc = get_mapped(*prog, &mp);
+        if (rc != ES_OK) { delete s; return rc; }
+        std::lock_guard<std::mutex> lk(mp->mu);
+        s->net = mp->variant(choose_cofactors(*mp, o, c->sms));
+    }
     double jit_ms = 0;
-    rc = k1_prepare(s->net, k1_threads(o), c->sms, &s->plan, &jit_ms);
+    rc = k1_prepare(s->net, k1_threads(o, (int)s->net.cof_pis.size()), c->sms, &s->plan, &jit_ms);
     if (rc != ES_OK) { delete s; return rc; }
     if (cudaMalloc(&s->d_counter, 64) != cudaSuccess) { delete s; set_error("cudaMalloc"); return ES_E_CUDA; }
     *out = s;
@@ -957,7 +1054,7 @@ int session_open(const es_prog *prog, const es_run_opts *opts, void **out) {
 int session_geometry(const void *sp, uint64_t *n_chunks, uint64_t *ppc, int32_t *luts, int32_t *regs) {
     const Session *s = (const Session *)sp;
     if (n_chunks) *n_chunks = s->plan.n_chunks;
-    if (ppc) *ppc = 1ull << (s->plan.chunk_log2 + 5);
+    if (ppc) *ppc = s->plan.patterns_per_chunk();
     if (luts) *luts = (int32_t)s->net.luts.size();
     if (regs) *regs = s->plan.jk->regs;
     return ES_OK;

@@ -233,8 +233,17 @@ class _CancelWatcher:
 KERNEL_VARIANTS = {"k1": 0, "k1t": 4, "k1u": 8}  # es_run_opts.flags (ES_FLAG_K1T / _K1U)
 
 
+def _cofactor_code(cofactor) -> int:
+    if isinstance(cofactor, str):
+        return N.COFACTOR_MODES[cofactor]
+    k = int(cofactor)
+    if not 0 <= k <= 4:
+        raise ValueError("cofactor must be 'auto', 'none', 'throughput' or 0..4")
+    return N.COFACTOR_NONE if k == 0 else k
+
+
 def _opts(device: int, engine: str, budget: float | None, cancel_addr, slice_ms: float,
-          block_threads: int, variant: str = "k1") -> N.EsRunOpts:
+          block_threads: int, variant: str = "k1", cofactor="auto") -> N.EsRunOpts:
     o = N.EsRunOpts()
     o.device = device
     o.engine = N.ENGINES[engine]
@@ -243,6 +252,7 @@ def _opts(device: int, engine: str, budget: float | None, cancel_addr, slice_ms:
     o.slice_ms = slice_ms
     o.block_threads = block_threads
     o.flags = KERNEL_VARIANTS[variant]
+    o.cofactor_pis = _cofactor_code(cofactor)
     return o
 
 
@@ -251,7 +261,7 @@ def _stats_of(r: N.EsResult) -> dict:
             "luts": int(r.num_luts), "patterns_swept": int(r.patterns_swept),
             "compile_ms": r.compile_ms, "jit_ms": r.jit_ms, "device_ms": r.device_ms,
             "engine_wall_ms": r.wall_ms, "launches": int(r.launches),
-            "regs_per_thread": int(r.regs_per_thread)}
+            "regs_per_thread": int(r.regs_per_thread), "cofactor_pis": int(r.cofactor_pis)}
 
 
 def _to_esresult(r: N.EsResult, num_pis: int) -> EsResult:
@@ -265,12 +275,17 @@ def _to_esresult(r: N.EsResult, num_pis: int) -> EsResult:
 
 def run_exhaustive(p, workers: int = 1, budget: float | None = None, cancel=None, *,
                    device: int = 0, engine: str = "auto", slice_ms: float = 20.0,
-                   block_threads: int = 0, variant: str = "k1") -> EsResult:
+                   block_threads: int = 0, variant: str = "k1", cofactor="auto") -> EsResult:
     """Sweep all 2^num_pis assignments on the GPU (es.py:252-339).
 
     Returns the minimum-index counterexample (the reference's workers=1
     witness), EXHAUSTED_ZERO, or BUDGET_EXCEEDED when ``budget`` seconds
     elapse or ``cancel()`` turns true first.
+
+    ``cofactor`` (JIT engine): "auto" weighs JIT latency against sweep time
+    (and tiers up when a program is re-run), "throughput" picks the fastest
+    sweep, "none" or 0 disables, 1..4 forces that many cofactor PIs.  The
+    result is the same for every setting.
     """
     if workers < 1:
         raise ValueError("workers must be >= 1")
@@ -281,14 +296,14 @@ def run_exhaustive(p, workers: int = 1, budget: float | None = None, cancel=None
         return EsResult(BUDGET_EXCEEDED, patterns_evaluated=0)
     res = N.EsResult()
     with _CancelWatcher(cancel) as cw:
-        opts = _opts(device, engine, budget, cw.address, slice_ms, block_threads, variant)
+        opts = _opts(device, engine, budget, cw.address, slice_ms, block_threads, variant, cofactor)
         N.check(N.lib().es_run(ctypes.byref(prog.as_struct()), ctypes.byref(opts),
                                ctypes.byref(res)))
     return _to_esresult(res, prog.num_pis)
 
 
 def es_check(sm, workers: int = 1, budget: float | None = None, cancel=None, *,
-             device: int = 0, engine: str = "auto") -> CheckResult:
+             device: int = 0, engine: str = "auto", cofactor="auto") -> CheckResult:
     """Compile and sweep a sub-miter (es.py:342-365); witnesses are re-checked
     by direct evaluation and a mismatch raises AssertionError."""
     t0 = time.monotonic()
@@ -297,7 +312,7 @@ def es_check(sm, workers: int = 1, budget: float | None = None, cancel=None, *,
     except TooManyInputs:
         return CheckResult(UNKNOWN, reason="ineligible", engine="es")
     r = run_exhaustive(prog, workers=workers, budget=budget, cancel=cancel, device=device,
-                       engine=engine)
+                       engine=engine, cofactor=cofactor)
     stats = {"patterns": r.patterns_evaluated, "registers": prog.num_registers,
              "wall_time": time.monotonic() - t0, **r.stats}
     if r.verdict == EXHAUSTED_ZERO:
@@ -358,27 +373,33 @@ def es_check_batch(sms: Iterable, budget: float | None = None, cancel=None, *,
 
 # --- engine introspection (tests, profiling) --------------------------------
 
-def map_stats(p) -> dict:
+def map_stats(p, k: int = 0) -> dict:
+    """K1 mapping of ``p`` with ``k`` cofactor PIs: LUTs per iteration (2^k
+    words), schedule peak live set, cone gates, the cofactor PIs."""
     prog = as_program(p)
     luts, live, gates = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
-    N.check(N.lib().es_map_stats(ctypes.byref(prog.as_struct()), ctypes.byref(luts),
-                                 ctypes.byref(live), ctypes.byref(gates)))
-    return {"luts": luts.value, "peak_live": live.value, "gates": gates.value}
+    pis = (ctypes.c_int32 * 4)()
+    N.check(N.lib().es_map_stats_k(ctypes.byref(prog.as_struct()), k, ctypes.byref(luts),
+                                   ctypes.byref(live), ctypes.byref(gates), pis))
+    return {"luts": luts.value, "peak_live": live.value, "gates": gates.value,
+            "cofactor_pis": list(pis[:k])}
 
 
-def map_pipes(p) -> dict:
-    """K1 body ops per 32-pattern word: LOP3 (ALU pipe) and IMAD (FMA pipe)."""
+def map_pipes(p, k: int = 0) -> dict:
+    """K1 body ops per iteration: LOP3 (ALU pipe) and IMAD (FMA pipe)."""
     prog = as_program(p)
     l, i = ctypes.c_int32(), ctypes.c_int32()
-    N.check(N.lib().es_map_pipes(ctypes.byref(prog.as_struct()), ctypes.byref(l), ctypes.byref(i)))
+    N.check(N.lib().es_map_pipes_k(ctypes.byref(prog.as_struct()), k, ctypes.byref(l),
+                                   ctypes.byref(i)))
     return {"lop3": l.value, "imad": i.value}
 
 
-def map_eval(p, w0: int, nw: int) -> np.ndarray:
-    """CPU model of the mapped kernel body: output words [w0, w0+nw)."""
+def map_eval(p, w0: int, nw: int, k: int = 0) -> np.ndarray:
+    """CPU model of the mapped kernel body: output words [w0, w0+nw) (full
+    word indices; with k cofactor PIs each word comes from its copy)."""
     prog = as_program(p)
     out = np.zeros(nw, dtype=np.uint32)
-    N.check(N.lib().es_map_eval(ctypes.byref(prog.as_struct()), w0, nw, out.ctypes.data))
+    N.check(N.lib().es_map_eval_k(ctypes.byref(prog.as_struct()), k, w0, nw, out.ctypes.data))
     return out
 
 
@@ -399,21 +420,21 @@ def k2_eval(p, w0: int, nw: int) -> np.ndarray:
     return out
 
 
-def emit_ptx(p, block_threads: int = 256) -> str:
+def emit_ptx(p, block_threads: int = 256, k: int = 0) -> str:
     prog = as_program(p)
     L = N.lib()
-    n = N.check(L.es_emit_ptx(ctypes.byref(prog.as_struct()), block_threads, None, 0))
+    n = N.check(L.es_emit_ptx_k(ctypes.byref(prog.as_struct()), k, block_threads, None, 0))
     buf = ctypes.create_string_buffer(n)
-    N.check(L.es_emit_ptx(ctypes.byref(prog.as_struct()), block_threads, buf, n))
+    N.check(L.es_emit_ptx_k(ctypes.byref(prog.as_struct()), k, block_threads, buf, n))
     return buf.value.decode()
 
 
-def jit_check(p, block_threads: int = 256) -> dict:
+def jit_check(p, block_threads: int = 256, k: int = 0) -> dict:
     """PTX -> SASS for ``p`` without a GPU: cubin size, registers, spills."""
     prog = as_program(p)
     regs, spill = ctypes.c_int32(), ctypes.c_int32()
     log = ctypes.create_string_buffer(1 << 16)
-    n = N.check(N.lib().es_jit_check(ctypes.byref(prog.as_struct()), block_threads,
-                                     ctypes.byref(regs), ctypes.byref(spill), log, 1 << 16))
+    n = N.check(N.lib().es_jit_check_k(ctypes.byref(prog.as_struct()), k, block_threads,
+                                       ctypes.byref(regs), ctypes.byref(spill), log, 1 << 16))
     return {"cubin_bytes": n, "regs": regs.value, "spill_bytes": spill.value,
             "log": log.value.decode(errors="replace")}

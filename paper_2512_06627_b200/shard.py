@@ -25,11 +25,14 @@ from .es import (BUDGET_EXCEEDED, ES_COUNTEREXAMPLE, EXHAUSTED_ZERO, EsResult, a
 class Session:
     """A program JIT-compiled for one device, launchable on any stream."""
 
-    def __init__(self, prog, device: int = 0, block_threads: int = 0, variant: str = "k1"):
+    def __init__(self, prog, device: int = 0, block_threads: int = 0, variant: str = "k1",
+                 cofactor="throughput"):
         self.prog = as_program(prog)
         self.device = device
         self.variant = variant
-        opts = _opts(device, "jit", None, None, 20.0, block_threads, variant)
+        # sessions serve repeated / long sharded sweeps: default to the fastest
+        # K1 variant (es_run_opts.cofactor_pis); the JIT is paid once per session
+        opts = _opts(device, "jit", None, None, 20.0, block_threads, variant, cofactor)
         h = ctypes.c_void_p()
         N.check(N.lib().es_session_open(ctypes.byref(self.prog.as_struct()), ctypes.byref(opts),
                                         ctypes.byref(h)))
@@ -88,18 +91,18 @@ def sharded_loop(n_chunks: int, slices: int, launch, reduce) -> int:
 _sessions: dict[tuple[int, int], Session] = {}
 
 
-def session_for(prog, device: int) -> Session:
+def session_for(prog, device: int, cofactor="throughput") -> Session:
     p = as_program(prog)
     key = (hash(bytes(p.op) + bytes(p.dst) + bytes(p.src0) + bytes(p.src1) + bytes(p.neg0)
-                + bytes(p.neg1) + bytes(p.pi)) ^ p.num_pis, device)
+                + bytes(p.neg1) + bytes(p.pi)) ^ p.num_pis, device, str(cofactor))
     s = _sessions.get(key)
     if s is None:
-        s = _sessions[key] = Session(p, device)
+        s = _sessions[key] = Session(p, device, cofactor=cofactor)
     return s
 
 
 def sweep_sharded(prog, group=None, device: int | None = None, slices: int | None = None,
-                  best=None) -> EsResult:
+                  best=None, cofactor="throughput") -> EsResult:
     """run_exhaustive sharded over the ranks of ``group`` (collective call).
 
     Every rank must call it with the same program.  ``slices`` launch slices
@@ -118,7 +121,7 @@ def sweep_sharded(prog, group=None, device: int | None = None, slices: int | Non
         if p.neg0[last]:
             return EsResult(ES_COUNTEREXAMPLE, (0,) * p.num_pis, 0, 0)
         return EsResult(EXHAUSTED_ZERO, None, 1 << p.num_pis)
-    sess = session_for(p, dev)
+    sess = session_for(p, dev, cofactor)
     sentinel = 1 << p.num_pis
     if best is None:
         best = torch.empty(1, dtype=torch.int64, device=f"cuda:{dev}")
@@ -150,7 +153,7 @@ def alu_peak(device: int = 0) -> tuple[float, float]:
 
 
 def es_check_sharded(sm, group=None, device: int | None = None,
-                     slices: int | None = None):
+                     slices: int | None = None, cofactor="throughput"):
     """``es_check`` (es.py:342-365) with the sweep sharded over ``group``."""
     import time
 
@@ -163,7 +166,7 @@ def es_check_sharded(sm, group=None, device: int | None = None,
         prog = compile_program(sm.circuit)
     except TooManyInputs:
         return CheckResult(UNKNOWN, reason="ineligible", engine="es")
-    r = sweep_sharded(prog, group, device, slices)
+    r = sweep_sharded(prog, group, device, slices, cofactor=cofactor)
     stats = {"patterns": r.patterns_evaluated, "registers": prog.num_registers,
              "wall_time": time.monotonic() - t0}
     if r.verdict == EXHAUSTED_ZERO:
@@ -221,7 +224,8 @@ class PeerBest:
         self.ptrs = []
 
 
-def sweep_peer(prog, peer: PeerBest, group=None, device: int | None = None) -> EsResult:
+def sweep_peer(prog, peer: PeerBest, group=None, device: int | None = None,
+               cofactor="throughput") -> EsResult:
     """run_exhaustive sharded over ``group`` with the shared peer word
     (collective call; same program on every rank).  One launch per rank over
     its residue class of chunks; two barriers per verdict, no all-reduce."""
@@ -236,7 +240,7 @@ def sweep_peer(prog, peer: PeerBest, group=None, device: int | None = None) -> E
         if p.neg0[last]:
             return EsResult(ES_COUNTEREXAMPLE, (0,) * p.num_pis, 0, 0)
         return EsResult(EXHAUSTED_ZERO, None, 1 << p.num_pis)
-    sess = session_for(p, dev)
+    sess = session_for(p, dev, cofactor)
     sentinel = 1 << p.num_pis
     k = peer._step & 1
     peer._step += 1
@@ -259,7 +263,8 @@ def sweep_peer(prog, peer: PeerBest, group=None, device: int | None = None) -> E
     return EsResult(EXHAUSTED_ZERO, None, sentinel)
 
 
-def es_check_peer(sm, peer: PeerBest, group=None, device: int | None = None):
+def es_check_peer(sm, peer: PeerBest, group=None, device: int | None = None,
+                  cofactor="throughput"):
     """``es_check`` (es.py:342-365) sharded with the shared peer word."""
     import time
 
@@ -272,7 +277,7 @@ def es_check_peer(sm, peer: PeerBest, group=None, device: int | None = None):
         prog = compile_program(sm.circuit)
     except TooManyInputs:
         return CheckResult(UNKNOWN, reason="ineligible", engine="es")
-    r = sweep_peer(prog, peer, group, device)
+    r = sweep_peer(prog, peer, group, device, cofactor=cofactor)
     stats = {"patterns": r.patterns_evaluated, "registers": prog.num_registers,
              "wall_time": time.monotonic() - t0}
     if r.verdict == EXHAUSTED_ZERO:

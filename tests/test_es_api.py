@@ -95,11 +95,13 @@ def test_oracle_agreement_500(gpu, golden):  # test_acceptance.py:82-101 (ES col
 def test_budget_timeout_midway(gpu):
     m = M.gen_multiplier_miter(16, "array", "booth")
     p = es.compile_program(m)
-    es.run_exhaustive(p, engine="jit")  # warm the JIT cache
-    r = es.run_exhaustive(p, engine="jit", budget=0.004, slice_ms=1.0)
+    # one word per iteration (no cofactor copies): a ~10 ms sweep, so a 4 ms
+    # budget must stop it midway
+    es.run_exhaustive(p, engine="jit", cofactor="none")  # warm the JIT cache
+    r = es.run_exhaustive(p, engine="jit", budget=0.004, slice_ms=1.0, cofactor="none")
     assert r.verdict == es.BUDGET_EXCEEDED
     assert 0 < r.patterns_evaluated < 1 << 32
-    c = es.es_check(SM(m), budget=0.004)
+    c = es.es_check(SM(m), budget=0.004, cofactor="none")
     assert c.verdict == UNKNOWN and c.reason == "timeout"
 
 
