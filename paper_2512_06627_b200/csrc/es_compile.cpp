@@ -18,6 +18,7 @@
 //                  es.py:9-10; here the register file is the SM's).
 //  * emit_body_ptx / eval_lutnet : the kernel body and its CPU model.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
@@ -459,6 +460,66 @@ void map_luts(const Dag &dag, LutNet *net) {
             });
             std::vector<int> alt = dfs(by_need);
             if (peak_of(alt) < peak_of(order)) order.swap(alt);
+        }
+        if (getenv("ES_LIST_SCHED")) {
+            // experiment: greedy list scheduling, prefer the ready node that frees most
+            std::vector<int> pos(N, -1);
+            for (size_t i = 0; i < order.size(); ++i) pos[order[i]] = (int)i;
+            std::vector<int> pend(N, 0), rem = users;
+            for (int32_t o : outs) if (is_gate_lut(o)) rem[o] += 1;
+            std::vector<std::vector<int>> parents(N);
+            for (int v : order) {
+                const Cut &c = cuts[v][best[v]];
+                for (int q = 0; q < c.n; ++q) {
+                    int l = c.leaf[q];
+                    bool seen = false;
+                    for (int r = 0; r < q; ++r) seen |= c.leaf[r] == l;
+                    if (seen || !is_gate_lut(l)) continue;
+                    pend[v]++;
+                    parents[l].push_back(v);
+                }
+            }
+            std::vector<int> ready, out2;
+            for (int v : order) if (pend[v] == 0) ready.push_back(v);
+            const int window = atoi(getenv("ES_LIST_SCHED"));
+            while (!ready.empty()) {
+                int bi = -1, bs = 1 << 30, bp = 1 << 30;
+                for (int i = 0; i < (int)ready.size(); ++i) {
+                    const int v = ready[i];
+                    const Cut &c = cuts[v][best[v]];
+                    int fr = 0;
+                    for (int q = 0; q < c.n; ++q) {
+                        int l = c.leaf[q];
+                        bool seen = false;
+                        for (int r = 0; r < q; ++r) seen |= c.leaf[r] == l;
+                        if (seen || !is_gate_lut(l)) continue;
+                        if (rem[l] == 1) ++fr;
+                    }
+                    const int sc = 1 - fr;
+                    // only look `window` positions ahead of the DFS order
+                    if (pos[v] > (out2.empty() ? 0 : pos[out2.back()]) + window && sc >= 0) continue;
+                    if (sc < bs || (sc == bs && pos[v] < bp)) { bs = sc; bp = pos[v]; bi = i; }
+                }
+                if (bi < 0) {  // fall back to earliest in DFS order
+                    for (int i = 0; i < (int)ready.size(); ++i)
+                        if (bi < 0 || pos[ready[i]] < pos[ready[bi]]) bi = i;
+                }
+                const int v = ready[bi];
+                ready[bi] = ready.back();
+                ready.pop_back();
+                out2.push_back(v);
+                const Cut &c = cuts[v][best[v]];
+                for (int q = 0; q < c.n; ++q) {
+                    int l = c.leaf[q];
+                    bool seen = false;
+                    for (int r = 0; r < q; ++r) seen |= c.leaf[r] == l;
+                    if (seen || !is_gate_lut(l)) continue;
+                    rem[l]--;
+                }
+                for (int pa : parents[v]) if (--pend[pa] == 0) ready.push_back(pa);
+            }
+            if (getenv("ES_SCHED_DEBUG")) fprintf(stderr, "dfs peak %d list peak %d\n", peak_of(order), peak_of(out2));
+            if (peak_of(out2) < peak_of(order)) order.swap(out2);
         }
     }
     // an output's inversion folds into its root LUT when nothing else reads it
