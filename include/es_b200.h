@@ -185,6 +185,9 @@ int32_t es_batch_extract(int32_t num_pis, int32_t num_gates, const uint8_t *kind
                          const int32_t *merge_node, const uint32_t *merge_lit, int32_t n_pairs,
                          const int32_t *a, const int32_t *b, const uint8_t *polarity,
                          int32_t n_threads, es_batch **out);
+/* Build the interpreter programs (cofactor depth, schedule) of every job that
+ * lacks one; es_batch_run does it on demand, this lets callers time it. */
+int32_t es_batch_prepare(es_batch *b, int32_t n_threads);
 int32_t es_batch_size(const es_batch *b);
 int32_t es_batch_info(const es_batch *b, int32_t i, int32_t *num_pis, int32_t *num_gates,
                       uint64_t *hash, int32_t *num_instrs, int32_t *num_registers, int32_t *G);
@@ -230,6 +233,10 @@ int32_t es_k2_stats(const es_prog *prog, int32_t *num_gates, int32_t *num_slots,
                     int32_t *stores, int32_t *acc_reads);
 /* CPU model of the K2 program over words [w0, w0+nw) (bit-exact with K2). */
 int32_t es_k2_eval(const es_prog *prog, uint64_t w0, uint64_t nw, uint32_t *out_words);
+/* K2 with k forced cofactor PIs (0..6), and the depth K2 picks by itself
+ * (the fewest shared-memory wavefronts per word, <= 88 slots). */
+int32_t es_k2_eval_k(const es_prog *prog, int32_t k, uint64_t w0, uint64_t nw, uint32_t *out_words);
+int32_t es_k2_cofactor_pis(const es_prog *prog);
 /* The same views for the K1 variant with k cofactor PIs (0..4, chosen as
  * es_run does: the k word PIs of smallest transitive fanout).  es_map_eval_k
  * takes FULL word indices (cofactor PIs included) and returns the output of

@@ -36,6 +36,7 @@ EXPORTS = ("es_compile", "es_run", "es_run_batch", "es_session_open", "es_sessio
            "es_batch_info", "es_batch_table", "es_batch_xag", "es_batch_select", "es_batch_run", "es_batch_merge", "es_batch_free",
            "es_ipc_alloc", "es_ipc_open", "es_ipc_close", "es_word_write", "es_word_read",
            "es_map_stats_k", "es_map_pipes_k", "es_map_eval_k", "es_emit_ptx_k", "es_jit_check_k",
+           "es_k2_eval_k", "es_k2_cofactor_pis", "es_batch_prepare",
            "es_last_error", "es_version", "es_shutdown")
 
 _P = ctypes.c_void_p
@@ -139,6 +140,10 @@ def lib():
         L.es_jit_check_k.argtypes = [ctypes.POINTER(EsProg), _I, _I, _P, _P, ctypes.c_char_p,
                                      ctypes.c_int64]
         L.es_jit_check_k.restype = ctypes.c_int64
+        L.es_k2_eval_k.argtypes = [ctypes.POINTER(EsProg), _I, ctypes.c_uint64, ctypes.c_uint64, _P]
+        L.es_k2_eval_k.restype = _I
+        L.es_k2_cofactor_pis.argtypes = [ctypes.POINTER(EsProg)]
+        L.es_k2_cofactor_pis.restype = _I
         L.es_alu_peak.argtypes = [ctypes.c_int32, ctypes.POINTER(ctypes.c_double),
                                   ctypes.POINTER(ctypes.c_double)]
         L.es_alu_peak.restype = ctypes.c_int32
@@ -146,6 +151,8 @@ def lib():
                                        _P, _P, ctypes.c_int32, _P, _P, _P, ctypes.c_int32,
                                        ctypes.POINTER(_P)]
         L.es_batch_extract.restype = ctypes.c_int32
+        L.es_batch_prepare.argtypes = [_P, ctypes.c_int32]
+        L.es_batch_prepare.restype = ctypes.c_int32
         L.es_batch_size.argtypes = [_P]
         L.es_batch_size.restype = ctypes.c_int32
         L.es_batch_info.argtypes = [_P, ctypes.c_int32, _P, _P, _P, _P, _P, _P]

@@ -211,6 +211,11 @@ class NativeBatch:
         return SubMiter(Xag(n, gates, (Lit.unpack(out.value),)), self.origins[i] if
                         i < len(self.origins) else (0, 0), {}, tuple(int(q) for q in pm), i)
 
+    def prepare(self, threads: int = 0) -> None:
+        """Build every job's interpreter program now (cofactor depth, schedule);
+        run_arrays would do it on its first call."""
+        N.check(N.lib().es_batch_prepare(self._h, threads))
+
     def select(self, idx) -> None:
         idx = np.ascontiguousarray(idx, dtype=np.int32)
         N.check(N.lib().es_batch_select(self._h, len(idx), idx.ctypes.data))
@@ -273,10 +278,13 @@ def config4_pairs(lo: int = 14, hi: int = 24, seed: int = 0, sim_words: int = 1,
     archs = [("array", "booth"), ("array", "wallace"), ("array", "diagonal"),
              ("diagonal", "booth"), ("wallace", "booth"), ("diagonal", "wallace")]
     rng = random.Random(seed)
+    built: dict = {}
     for round_ in range(rounds):
         a_arch, b_arch = archs[round_ % len(archs)]
-        m = M.gen_multiplier_miter(16, a_arch, b_arch)
-        sup = support_masks(m)
+        if (a_arch, b_arch) not in built:  # deterministic: build each parent once
+            mm = M.gen_multiplier_miter(16, a_arch, b_arch)
+            built[(a_arch, b_arch)] = (mm, support_masks(mm))
+        m, sup = built[(a_arch, b_arch)]
         pairs = []
         for cls in candidate_classes(m, sim_words, seed + round_ // len(archs)):
             nodes = [n for n, _ in cls if sup[n].bit_count() <= hi]
@@ -328,6 +336,7 @@ def config4_batch(count: int = 10_000, lo: int = 14, hi: int = 24, seed: int = 0
     head = bs[0]
     for b in bs[1:]:
         head.extend(b)
+    head.prepare(threads)
     return head
 
 

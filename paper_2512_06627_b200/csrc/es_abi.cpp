@@ -18,7 +18,7 @@ void set_error(const std::string &m) { t_err = m; }
 
 int run_one(const es_prog *prog, const es_run_opts *opts, es_result *out);
 int run_batch(int n_jobs, const es_prog *progs, const es_run_opts *opts, es_result *outs,
-              const K2Prog *prebuilt = nullptr);
+              const K2Prog *const *prebuilt = nullptr);
 int session_open(const es_prog *prog, const es_run_opts *opts, void **out);
 int session_geometry(const void *s, uint64_t *n_chunks, uint64_t *ppc, int32_t *luts, int32_t *regs);
 int session_launch(void *s, void *stream, uint64_t *best_dev, uint64_t chunk_begin,
@@ -155,13 +155,13 @@ int32_t es_k2_stats(const es_prog *prog, int32_t *num_gates, int32_t *num_slots,
     int rc = build_dag(*prog, &dag, &err);
     if (rc != ES_OK) { set_error(err); return rc; }
     K2Prog kp;
-    build_k2prog(dag, &kp);
+    build_k2prog_auto(dag, &kp);
     int st = 0, acc = 0;
     for (const K2Gate &g : kp.gates) {
         st += (g.ctl & K2_STORE) != 0;
-        acc += ((g.ctl & K2_A_ACC) != 0) + ((g.ctl & K2_B_ACC) != 0);
+        acc += (g.ctl & K2_A_ACC) != 0;
     }
-    if (num_gates) *num_gates = (int32_t)kp.gates.size();
+    if (num_gates) *num_gates = kp.n_gates;
     if (num_slots) *num_slots = kp.num_slots;
     if (stores) *stores = st;
     if (acc_reads) *acc_reads = acc;
@@ -175,9 +175,34 @@ int32_t es_k2_eval(const es_prog *prog, uint64_t w0, uint64_t nw, uint32_t *out_
     int rc = build_dag(*prog, &dag, &err);
     if (rc != ES_OK) { set_error(err); return rc; }
     K2Prog kp;
-    build_k2prog(dag, &kp);
+    build_k2prog_auto(dag, &kp);
     eval_k2prog(kp, w0, nw, out_words);
     return ES_OK;
+}
+
+int32_t es_k2_eval_k(const es_prog *prog, int32_t k, uint64_t w0, uint64_t nw, uint32_t *out_words) {
+    if (!prog || prog->num_instrs < 1) { set_error("empty program"); return ES_E_BAD_PROGRAM; }
+    if (k < 0 || k > kK2MaxCofactorPis) { set_error("cofactor PIs must be 0..6"); return ES_E_BAD_ARG; }
+    Dag dag;
+    std::string err;
+    int rc = build_dag(*prog, &dag, &err);
+    if (rc != ES_OK) { set_error(err); return rc; }
+    K2Prog kp;
+    build_k2prog_k(dag, k, &kp);
+    if ((int)kp.cof_pis.size() != k) { set_error("fewer word PIs than cofactor PIs"); return ES_E_BAD_ARG; }
+    eval_k2prog(kp, w0, nw, out_words);
+    return ES_OK;
+}
+
+int32_t es_k2_cofactor_pis(const es_prog *prog) {
+    if (!prog || prog->num_instrs < 1) { set_error("empty program"); return ES_E_BAD_PROGRAM; }
+    Dag dag;
+    std::string err;
+    int rc = build_dag(*prog, &dag, &err);
+    if (rc != ES_OK) { set_error(err); return rc; }
+    K2Prog kp;
+    build_k2prog_auto(dag, &kp);
+    return (int32_t)kp.cof_pis.size();
 }
 
 int64_t es_emit_ptx(const es_prog *prog, int32_t block_threads, char *buf, int64_t cap) {
@@ -254,6 +279,14 @@ int32_t es_batch_extract(int32_t num_pis, int32_t num_gates, const uint8_t *kind
     return ES_OK;
 }
 
+int32_t es_batch_prepare(es_batch *bp, int32_t n_threads) {
+    Batch *bt = (Batch *)bp;
+    if (!bt) { set_error("bad argument"); return ES_E_BAD_ARG; }
+    const int rc = prepare_k2(bt->subs, n_threads);
+    if (rc != ES_OK) set_error("malformed sub-miter program");
+    return rc;
+}
+
 int32_t es_batch_size(const es_batch *bp) { return bp ? (int32_t)((const Batch *)bp)->subs.size() : ES_E_BAD_ARG; }
 
 int32_t es_batch_info(const es_batch *bp, int32_t i, int32_t *num_pis, int32_t *num_gates,
@@ -323,7 +356,7 @@ int32_t es_batch_run(es_batch *bp, const es_run_opts *opts, es_result *outs) {
     if (!bt || !outs) { set_error("bad argument"); return ES_E_BAD_ARG; }
     const int n = (int)bt->subs.size();
     std::vector<es_prog> progs;
-    std::vector<K2Prog> kps;
+    std::vector<const K2Prog *> kps;
     std::vector<int> where;
     for (int i = 0; i < n; ++i) {
         std::memset(&outs[i], 0, sizeof(es_result));
@@ -332,8 +365,10 @@ int32_t es_batch_run(es_batch *bp, const es_run_opts *opts, es_result *outs) {
         where.push_back(i);
     }
     const double t0 = now_ms();
+    int prc = prepare_k2(bt->subs, 0);  // no-op once es_batch_prepare ran
+    if (prc != ES_OK) { set_error("malformed sub-miter program"); return prc; }
     kps.reserve(where.size());
-    for (int i : where) kps.push_back(bt->subs[i].k2);  // built at extraction
+    for (int i : where) kps.push_back(&bt->subs[i].k2);
     std::vector<es_result> rs(progs.size());
     const double t1 = now_ms();
     int rc = run_batch((int)progs.size(), progs.data(), opts, rs.data(), kps.data());

@@ -108,18 +108,27 @@ void cofactor_expand(const Dag &dag, const std::vector<int32_t> &pis, Dag *out) 
     *out = Dag();
     out->num_pis = P;
     Strash sh(out);
-    sh.table.reserve((size_t)N * 2);
+    sh.table.reserve((size_t)N * 4);
     const int k = (int)pis.size();
+    // gates in the transitive fanout of the cofactor PIs: the only ones that
+    // differ between copies; the rest keep copy 0's literal
+    std::vector<uint8_t> tfo(N, 0);
+    for (int32_t j : pis) tfo[j] = 1;
+    std::vector<int32_t> tgates, all;
+    for (int v = FG; v < N; ++v) {
+        if (!cone[v]) continue;
+        all.push_back(v);
+        const int g = v - FG;
+        if (tfo[dag.f0[g]] || tfo[dag.f1[g]]) { tfo[v] = 1; tgates.push_back(v); }
+    }
     std::vector<uint32_t> lit(N, 0);
     std::vector<int32_t> src_outs = dag.outs;
     std::vector<uint8_t> src_neg = dag.outs_neg;
     if (src_outs.empty()) { src_outs.push_back(dag.out_node); src_neg.push_back(dag.out_neg); }
+    for (int j = 1; j <= P; ++j) lit[j] = (uint32_t)j * 2;
     for (int c = 0; c < (1 << k); ++c) {
-        lit[0] = 0;
-        for (int j = 1; j <= P; ++j) lit[j] = (uint32_t)j * 2;
         for (int b = 0; b < k; ++b) lit[pis[b]] = (uint32_t)((c >> b) & 1);
-        for (int v = FG; v < N; ++v) {
-            if (!cone[v]) continue;
+        for (int v : (c == 0 ? all : tgates)) {
             const int g = v - FG;
             const uint32_t a = lit[dag.f0[g]] ^ dag.n0[g], b = lit[dag.f1[g]] ^ dag.n1[g];
             lit[v] = dag.is_xor[g] ? sh.mk_xor(a, b) : sh.mk_and(a, b);

@@ -214,7 +214,6 @@ int extract_compile(int32_t num_pis, int32_t num_gates, const uint8_t *kind, con
             Dag dag;
             std::string e2;
             if (build_dag(s.view(), &dag, &e2) != ES_OK) { bad.fetch_add(1); continue; }
-            build_k2prog(dag, &s.k2);
         }
     };
     int T = n_threads > 0 ? n_threads : (int)std::max(1u, std::thread::hardware_concurrency());
@@ -250,6 +249,33 @@ int evaluate_sub(const SubMiterC &s, uint64_t pattern) {  // eval.py:22-36 on th
         v[1 + s.num_pis + g] = s.kind[g] == 0 ? (x & y) : (x ^ y);
     }
     return v[s.out_lit >> 1] ^ (s.out_lit & 1);
+}
+
+int prepare_k2(std::vector<SubMiterC> &subs, int n_threads) {
+    std::vector<int> todo;
+    for (int i = 0; i < (int)subs.size(); ++i)
+        if (!subs[i].k2_ready && !subs[i].too_many_inputs) todo.push_back(i);
+    if (todo.empty()) return ES_OK;
+    std::atomic<int> next{0}, bad{0};
+    auto work = [&]() {
+        for (;;) {
+            const int q = next.fetch_add(1);
+            if (q >= (int)todo.size()) return;
+            SubMiterC &s = subs[todo[q]];
+            Dag dag;
+            std::string err;
+            if (build_dag(s.view(), &dag, &err) != ES_OK) { bad.fetch_add(1); continue; }
+            build_k2prog_auto(dag, &s.k2);
+            s.k2_ready = true;
+        }
+    };
+    int T = n_threads > 0 ? n_threads : (int)std::max(1u, std::thread::hardware_concurrency());
+    T = std::min<int>(T, std::max<int>(1, (int)todo.size() / 8));
+    std::vector<std::thread> th;
+    for (int t = 1; t < T; ++t) th.emplace_back(work);
+    work();
+    for (auto &t : th) t.join();
+    return bad.load() ? ES_E_BAD_PROGRAM : ES_OK;
 }
 
 }  // namespace es

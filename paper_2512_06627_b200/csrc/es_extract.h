@@ -24,7 +24,8 @@ struct SubMiterC {
     std::vector<int32_t> dst, src0, src1, pi;
     std::vector<uint8_t> neg0, neg1;
     int32_t num_registers = 0;
-    K2Prog k2;  // interpreter program, built with the extraction
+    K2Prog k2;  // interpreter program (with cofactor copies), built by prepare_k2
+    bool k2_ready = false;
     es_prog view() const;
 };
 
@@ -35,5 +36,8 @@ int extract_compile(int32_t num_pis, int32_t num_gates, const uint8_t *kind, con
                     std::vector<SubMiterC> *out, std::string *err);
 
 int evaluate_sub(const SubMiterC &s, uint64_t pattern);
+// Build the K2 programs of the sub-miters that lack one, on n_threads host
+// threads (0 = all).  Done once per batch, after any selection.
+int prepare_k2(std::vector<SubMiterC> &subs, int n_threads);
 
 }  // namespace es

@@ -8,41 +8,148 @@
 //     most gates consume the previous gate's result;
 //   * that operand (always operand A) is read from an accumulator register
 //     (no LDS; a non-accumulator A is loaded straight into it), and a result
-//     whose only consumer is the next gate is never stored (no STS);
+//     whose only consumers are the next gate's operand A and the outputs
+//     folded right after it is never stored (no STS);
 //   * the remaining live values get LIFO-recycled slots after the PI slots
 //     (fanins are freed before the destination is allocated, as es.py:151-156);
-//   * complement flags become full-word masks; XOR folds both into one mask.
+//   * complement flags become record bits; XOR folds both into operand A's.
+// Cofactor copies (es_cofactor.cpp): the graph may have 2^k outputs, one per
+// assignment of k word PIs that are then fixed per copy instead of per word;
+// OUT records fold each copy's output into (first failing word, copy number)
+// in copy order, so the kernel's rare path can rebuild the minimum index.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <functional>
+#include <queue>
+#include <tuple>
 
 #include "es_k2prog.h"
 
 namespace es {
 
-static void emit_k2(const Dag &dag, const std::vector<int> &order, const std::vector<uint8_t> &cone,
-                    std::vector<int> refs, K2Prog *kp);
+namespace {
+
+struct Outs {
+    std::vector<int32_t> node;
+    std::vector<uint8_t> neg;
+};
+
+Outs outputs_of(const Dag &dag) {
+    Outs o;
+    if (dag.outs.empty()) { o.node.push_back(dag.out_node); o.neg.push_back(dag.out_neg); }
+    else { o.node = dag.outs; o.neg = dag.outs_neg; }
+    return o;
+}
+
+void emit_k2(const Dag &dag, const Outs &outs, const std::vector<int> &order,
+             const std::vector<uint8_t> &cone, std::vector<int> refs, K2Prog *kp) {
+    const int N = dag.num_nodes(), FG = dag.first_gate(), P = dag.num_pis;
+    auto is_gate = [&](int v) { return v >= FG && cone[v]; };
+    kp->num_pis = P;
+    kp->gates.clear();
+    kp->n_gates = 0;
+    kp->loads = kp->stores = 0;
+    // slots: 0..P-1 hold the PI words (filled once per word batch); gates
+    // above, LIFO-recycled
+    std::vector<int> slot(N, -1), pool, pos(N, -1);
+    for (int j = 1; j <= P; ++j) slot[j] = j - 1;
+    for (size_t i = 0; i < order.size(); ++i) pos[order[i]] = (int)i;
+    int top = P;
+    auto alloc = [&]() {
+        if (!pool.empty()) { int s = pool.back(); pool.pop_back(); return s; }
+        return top++;
+    };
+    // each copy's output is folded as soon as it exists and after the previous
+    // copy's: flush position = max(previous, position of its node)
+    const int C = (int)outs.node.size();
+    std::vector<int> flush(C, -1);
+    for (int c = 0; c < C; ++c) {
+        const int o = outs.node[c];
+        flush[c] = std::max(c ? flush[c - 1] : -1, is_gate(o) ? pos[o] : -1);
+    }
+    int next_copy = 0;
+    int last_gate = -1;  // node in the accumulator
+    auto emit_outs = [&](int upto) {
+        for (; next_copy < C && flush[next_copy] <= upto; ++next_copy) {
+            const int o = outs.node[next_copy];
+            const bool neg = outs.neg[next_copy];
+            K2Gate g{};
+            uint32_t ctl = K2_OUT | ((uint32_t)next_copy << 16) | (neg ? K2_NEG_A : 0u);
+            if (o == 0) {
+                if (!neg) continue;  // constant 0: this copy never fails
+                ctl |= K2_CONST;
+            } else if (o == last_gate) {
+                ctl |= K2_A_ACC;
+            } else {
+                g.a = (uint32_t)slot[o];
+                kp->loads++;
+            }
+            g.ctl = ctl;
+            kp->gates.push_back(g);
+            if (is_gate(o) && --refs[o] == 0 && slot[o] >= P) pool.push_back(slot[o]);
+        }
+    };
+    emit_outs(-1);
+    for (size_t i = 0; i < order.size(); ++i) {
+        const int v = order[i], gi = v - FG;
+        int fa = dag.f0[gi], fb = dag.f1[gi];
+        uint32_t na = dag.n0[gi], nb = dag.n1[gi];
+        // only operand A may come from the accumulator: swap the previous
+        // gate's result into A (AND and XOR are symmetric)
+        if (fb == last_gate && fa != last_gate) { std::swap(fa, fb); std::swap(na, nb); }
+        K2Gate g{};
+        uint32_t ctl = dag.is_xor[gi] ? K2_XOR : 0u;
+        if (fa == last_gate) ctl |= K2_A_ACC;
+        else { g.a = (uint32_t)slot[fa]; kp->loads++; }
+        g.b = (uint32_t)slot[fb];  // == last_gate only for AND(x, x): then x was stored
+        kp->loads++;
+        if (dag.is_xor[gi]) { if (na ^ nb) ctl |= K2_NEG_A; }
+        else { if (na) ctl |= K2_NEG_A; if (nb) ctl |= K2_NEG_B; }
+        // consume fanins; a slot frees when its last reader has read it
+        for (int f : {fa, fb}) {
+            if (!is_gate(f)) continue;
+            if (--refs[f] == 0 && slot[f] >= 0) pool.push_back(slot[f]);
+        }
+        // readers served by the accumulator: outputs folded right after this
+        // gate, and operand A of the next gate
+        int acc_uses = 0;
+        for (int c = next_copy; c < C && flush[c] == (int)i; ++c) acc_uses += outs.node[c] == v;
+        if (i + 1 < order.size()) {
+            const int nx = order[i + 1] - FG;
+            const bool a_ = dag.f0[nx] == v, b_ = dag.f1[nx] == v;
+            acc_uses += (a_ != b_) ? 1 : 0;
+        }
+        if (refs[v] > acc_uses) {
+            ctl |= K2_STORE;
+            slot[v] = alloc();
+            g.d = (uint32_t)slot[v];
+            kp->stores++;
+        }
+        g.ctl = ctl;
+        kp->gates.push_back(g);
+        kp->n_gates++;
+        last_gate = v;
+        emit_outs((int)i);
+    }
+    kp->num_slots = top;
+}
+
+}  // namespace
 
 void build_k2prog(const Dag &dag, K2Prog *kp) {
     const int N = dag.num_nodes(), FG = dag.first_gate(), P = dag.num_pis;
-    kp->num_pis = P;
-    kp->gates.clear();
-    kp->out_mask = dag.out_neg ? ~0u : 0u;
-    kp->const_out = false;
-    if (dag.out_node == 0) {  // constant output (callers normally short-cut it)
-        kp->const_out = true;
-        kp->num_slots = P;
-        return;
-    }
+    const Outs outs = outputs_of(dag);
     std::vector<uint8_t> cone(N, 0);
-    cone[dag.out_node] = 1;
+    for (int32_t o : outs.node) cone[o] = 1;
     for (int v = N - 1; v >= FG; --v) {
         if (!cone[v]) continue;
         cone[dag.f0[v - FG]] = cone[dag.f1[v - FG]] = 1;
     }
     auto is_gate = [&](int v) { return v >= FG && cone[v]; };
-    // register need, bottom-up
+    // register need, bottom-up; references (outputs count once per copy)
     std::vector<int> need(N, 0), refs(N, 0);
-    refs[dag.out_node] += 1;
+    for (int32_t o : outs.node) refs[o] += 1;
     for (int v = FG; v < N; ++v) {
         if (!cone[v]) continue;
         const int g = v - FG, a = dag.f0[g], b = dag.f1[g];
@@ -51,116 +158,167 @@ void build_k2prog(const Dag &dag, K2Prog *kp) {
         if (na < nb) std::swap(na, nb);
         need[v] = std::max({1, na, nb + 1});
     }
-    // DFS post-order from the output, highest-need child first
+    // candidate 1: DFS post-order from each output in copy order, highest-need child first
     std::vector<int> order;
-    if (is_gate(dag.out_node)) {
+    {
         std::vector<uint8_t> done(N, 0);
-        std::vector<int> st{dag.out_node};
-        while (!st.empty()) {
-            const int v = st.back();
-            if (done[v]) { st.pop_back(); continue; }
-            const int g = v - FG;
-            int pick = -1;
-            for (int l : {dag.f0[g], dag.f1[g]})
-                if (is_gate(l) && !done[l] && (pick < 0 || need[l] > need[pick])) pick = l;
-            if (pick >= 0) { st.push_back(pick); continue; }
-            done[v] = 1;
-            order.push_back(v);
-            st.pop_back();
+        std::vector<int> st;
+        for (int32_t o : outs.node) {
+            if (!is_gate(o) || done[o]) continue;
+            st.push_back(o);
+            while (!st.empty()) {
+                const int v = st.back();
+                if (done[v]) { st.pop_back(); continue; }
+                const int g = v - FG;
+                int pick = -1;
+                for (int l : {dag.f0[g], dag.f1[g]})
+                    if (is_gate(l) && !done[l] && (pick < 0 || need[l] > need[pick])) pick = l;
+                if (pick >= 0) { st.push_back(pick); continue; }
+                done[v] = 1;
+                order.push_back(v);
+                st.pop_back();
+            }
         }
     }
-    // candidate 2: the reference's topological order (node index order)
+    // candidate 2: topological (node index) order -- the reference's
     std::vector<int> topo;
     for (int v = FG; v < N; ++v)
         if (cone[v]) topo.push_back(v);
-    K2Prog a, b;
-    a.num_pis = b.num_pis = P;
-    a.out_mask = b.out_mask = kp->out_mask;
-    emit_k2(dag, order, cone, refs, &a);
-    emit_k2(dag, topo, cone, refs, &b);
-    auto cost = [](const K2Prog &q) {
-        int st = 0, acc = 0;
-        for (const K2Gate &g : q.gates) { st += (g.ctl & K2_STORE) != 0; acc += ((g.ctl & K2_A_ACC) != 0) + ((g.ctl & K2_B_ACC) != 0); }
-        return std::make_pair(q.num_slots, st - acc);
-    };
-    *kp = cost(a) <= cost(b) ? std::move(a) : std::move(b);
+    // candidate 3: greedy list schedule -- among the ready gates, the one that
+    // frees the most live values (ties: earliest in the DFS order); on wide
+    // cofactored graphs it needs far fewer slots than the DFS
+    std::vector<int> lsched;
+    {
+        std::vector<int> dpos(N, 0), pend(N, 0), rem = refs;
+        for (size_t i = 0; i < order.size(); ++i) dpos[order[i]] = (int)i;
+        std::vector<std::vector<int>> users(N);
+        for (int v : order) {
+            const int g = v - FG;
+            for (int l : {dag.f0[g], dag.f1[g]}) {
+                if (!is_gate(l)) continue;
+                if (dag.f0[g] == dag.f1[g] && l == dag.f1[g] && pend[v]) continue;
+                pend[v]++;
+                users[l].push_back(v);
+            }
+        }
+        // lazy min-heap of (score, DFS position, gate); scores only improve
+        // as fanins lose readers, so stale entries are skipped on pop
+        auto score = [&](int v) {
+            const int g = v - FG, a0 = dag.f0[g], a1 = dag.f1[g];
+            int fr = 0;
+            if (is_gate(a0) && rem[a0] == (a0 == a1 ? 2 : 1)) ++fr;
+            if (a1 != a0 && is_gate(a1) && rem[a1] == 1) ++fr;
+            return 1 - fr;
+        };
+        using E = std::tuple<int, int, int>;
+        std::priority_queue<E, std::vector<E>, std::greater<E>> heap;
+        std::vector<uint8_t> in_ready(N, 0), done(N, 0);
+        for (int v : order)
+            if (pend[v] == 0) { in_ready[v] = 1; heap.emplace(score(v), dpos[v], v); }
+        while (!heap.empty()) {
+            const auto [sc, dp, v] = heap.top();
+            heap.pop();
+            if (done[v] || sc != score(v)) continue;
+            done[v] = 1;
+            lsched.push_back(v);
+            const int g = v - FG;
+            for (int l : {dag.f0[g], dag.f1[g]}) {
+                if (!is_gate(l)) continue;
+                rem[l]--;
+                if (rem[l] <= 2)  // a remaining ready reader may now free l
+                    for (int u : users[l])
+                        if (in_ready[u] && !done[u]) heap.emplace(score(u), dpos[u], u);
+            }
+            for (int u : users[v])
+                if (--pend[u] == 0) { in_ready[u] = 1; heap.emplace(score(u), dpos[u], u); }
+        }
+    }
+    // the list schedule needs about half the slots of the DFS on cofactored
+    // graphs (and wins on ~98 % of the config-4 cones); the reference order
+    // still wins now and then on single-output programs
+    emit_k2(dag, outs, lsched, cone, refs, kp);
+    if (outs.node.size() == 1) {
+        K2Prog b;
+        emit_k2(dag, outs, topo, cone, refs, &b);
+        auto cost = [](const K2Prog &q) { return std::make_pair(q.num_slots, q.loads + q.stores); };
+        if (cost(b) < cost(*kp)) *kp = std::move(b);
+    }
 }
 
-static void emit_k2(const Dag &dag, const std::vector<int> &order, const std::vector<uint8_t> &cone,
-                    std::vector<int> refs, K2Prog *kp) {
-    const int N = dag.num_nodes(), FG = dag.first_gate(), P = dag.num_pis;
-    auto is_gate = [&](int v) { return v >= FG && cone[v]; };
-    // slots: 0..P-1 hold the PI words (filled once per word batch); gates
-    // above, LIFO-recycled
-    std::vector<int> slot(N, -1), pool;
-    for (int j = 1; j <= P; ++j) slot[j] = j - 1;
-    int top = P;
-    auto alloc = [&]() {
-        if (!pool.empty()) { int s = pool.back(); pool.pop_back(); return s; }
-        return top++;
-    };
-    if (order.empty()) {  // output is a PI: out = AND(pi, pi)
-        K2Gate g{};
-        g.a = g.b = (uint32_t)slot[dag.out_node];
-        g.ma = g.mb = 0;
-        g.ctl = 0;
-        kp->gates.push_back(g);
-        kp->num_slots = P;
+void build_k2prog_k(const Dag &dag, int k, K2Prog *kp) {
+    if (k <= 0) { build_k2prog(dag, kp); kp->cof_pis.clear(); return; }
+    std::vector<int32_t> pis = rank_cofactor_pis(dag, k);
+    std::sort(pis.begin(), pis.end());
+    Dag x;
+    cofactor_expand(dag, pis, &x);
+    build_k2prog(x, kp);
+    kp->cof_pis = pis;
+}
+
+void build_k2prog_auto(const Dag &dag, K2Prog *kp, int min_words_log2, int max_slots) {
+    if (const char *e = getenv("ES_K2_MAXSLOTS")) max_slots = atoi(e);
+    const int P = dag.num_pis;
+    const int kmax = std::min(kK2MaxCofactorPis, P - 5 - min_words_log2);
+    std::vector<int32_t> rank;
+    if (kmax >= 1) rank = rank_cofactor_pis(dag, kmax);
+    // gates per word of each depth (the interpreter's cost is ~linear in the
+    // gate count); the expansions share copy 0's literals outside the
+    // cofactor PIs' fanout, so they are cheap.  Build the best depth, and
+    // step down while its program needs more slots than the budget.
+    std::vector<Dag> xs(rank.size() + 1);
+    std::vector<double> per_word(rank.size() + 1, 0.0);
+    int gates0 = 0;
+    for (int v = 0; v < (int)dag.is_xor.size(); ++v) gates0++;
+    per_word[0] = (double)gates0;
+    for (int k = 1; k <= (int)rank.size(); ++k) {
+        std::vector<int32_t> pis(rank.begin(), rank.begin() + k);
+        std::sort(pis.begin(), pis.end());
+        cofactor_expand(dag, pis, &xs[k]);
+        per_word[k] = (double)xs[k].is_xor.size() / (double)(1u << k) + 0.25;  // + OUT records
+    }
+    std::vector<int> order(per_word.size());
+    for (size_t k = 0; k < order.size(); ++k) order[k] = (int)k;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return per_word[a] < per_word[b]; });
+    for (int k : order) {
+        if (k == 0) { build_k2prog(dag, kp); kp->cof_pis.clear(); return; }
+        K2Prog q;
+        build_k2prog(xs[k], &q);
+        if (q.num_slots > max_slots) continue;
+        q.cof_pis.assign(rank.begin(), rank.begin() + k);
+        std::sort(q.cof_pis.begin(), q.cof_pis.end());
+        *kp = std::move(q);
         return;
     }
-    for (size_t i = 0; i < order.size(); ++i) {
-        const int v = order[i], gi = v - FG;
-        const int prev = i > 0 ? order[i - 1] : -1;
-        int fa = dag.f0[gi], fb = dag.f1[gi];
-        uint32_t na = dag.n0[gi], nb = dag.n1[gi];
-        // only operand A may come from the accumulator: swap a previous-gate
-        // operand into A (AND and XOR are symmetric)
-        if (fb == prev && fa != prev) { std::swap(fa, fb); std::swap(na, nb); }
-        K2Gate g{};
-        uint32_t ctl = dag.is_xor[gi] ? K2_XOR : 0u;
-        if (fa == prev) ctl |= K2_A_ACC; else g.a = (uint32_t)slot[fa];
-        g.b = (uint32_t)slot[fb];  // == prev only for AND(x, x): then x was stored
-        const uint32_t ma = na ? ~0u : 0u, mb = nb ? ~0u : 0u;
-        if (dag.is_xor[gi]) { g.ma = ma ^ mb; g.mb = 0; }
-        else { g.ma = ma; g.mb = mb; }
-        // consume fanins; a slot frees when its last reader has read it
-        for (int f : {fa, fb}) {
-            if (!is_gate(f)) continue;
-            if (--refs[f] == 0 && slot[f] >= 0) pool.push_back(slot[f]);
-        }
-        // store unless the only remaining use is operand A of the next gate
-        // (or the output, which reads the accumulator after the last gate)
-        const int next = i + 1 < order.size() ? order[i + 1] : -1;
-        const int next_uses = next < 0 ? 1 : ((dag.f0[next - FG] == v || dag.f1[next - FG] == v) ? 1 : 0);
-        if (refs[v] > next_uses) {
-            ctl |= K2_STORE;
-            slot[v] = alloc();
-            g.d = (uint32_t)slot[v];
-        }
-        g.ctl = ctl;
-        kp->gates.push_back(g);
-    }
-    kp->num_slots = top;
 }
 
 void eval_k2prog(const K2Prog &kp, uint64_t w0, uint64_t nw, uint32_t *out) {
     static const uint32_t lane[5] = {0xAAAAAAAAu, 0xCCCCCCCCu, 0xF0F0F0F0u, 0xFF00FF00u, 0xFFFF0000u};
     std::vector<uint32_t> s(std::max(kp.num_slots, 1), 0);
+    const int C = 1 << kp.cof_pis.size();
+    std::vector<uint32_t> val(C, 0);
     const uint32_t valid = lane_valid_mask(kp.num_pis);
     for (uint64_t k = 0; k < nw; ++k) {
         const uint64_t w = w0 + k;
-        if (kp.const_out) { out[k] = kp.out_mask & valid; continue; }
         for (int j = 0; j < kp.num_pis; ++j)
             s[j] = j < 5 ? lane[j] : (((w >> (j - 5)) & 1) ? ~0u : 0u);
+        std::fill(val.begin(), val.end(), 0u);
         uint32_t acc = 0;
         for (const K2Gate &g : kp.gates) {
+            const uint32_t ma = (g.ctl & K2_NEG_A) ? ~0u : 0u, mb = (g.ctl & K2_NEG_B) ? ~0u : 0u;
+            if (g.ctl & K2_OUT) {
+                const uint32_t v = (g.ctl & K2_CONST) ? 0u : (g.ctl & K2_A_ACC) ? acc : s[g.a];
+                val[g.ctl >> 16] = v ^ ma;
+                continue;
+            }
             const uint32_t a = (g.ctl & K2_A_ACC) ? acc : s[g.a];
             const uint32_t b = s[g.b];
-            const uint32_t r = (g.ctl & K2_XOR) ? (a ^ b ^ g.ma) : ((a ^ g.ma) & (b ^ g.mb));
+            const uint32_t r = (g.ctl & K2_XOR) ? (a ^ b ^ ma) : ((a ^ ma) & (b ^ mb));
             if (g.ctl & K2_STORE) s[g.d] = r;
             acc = r;
         }
-        out[k] = (acc ^ kp.out_mask) & valid;
+        size_t c = 0;
+        for (size_t b = 0; b < kp.cof_pis.size(); ++b) c |= (size_t)((w >> (kp.cof_pis[b] - 6)) & 1) << b;
+        out[k] = val[c] & valid;
     }
 }
 

@@ -8,26 +8,48 @@
 
 namespace es {
 
-enum : uint32_t { K2_XOR = 1u, K2_A_ACC = 2u, K2_B_ACC = 4u, K2_STORE = 8u };
+// Record flags (K2Gate::ctl, low byte) and the copy number of an OUT record
+// (ctl >> 16).
+enum : uint32_t {
+    K2_XOR = 1u,      // gate: A ^ B ^ ma (else (A ^ ma) & (B ^ mb))
+    K2_A_ACC = 2u,    // operand A (gate) / the output value (OUT) is the accumulator
+    K2_STORE = 8u,    // gate: store the result into slot d
+    K2_OUT = 16u,     // output record: fold (A ^ ma) into (first failing word, copy)
+    K2_NEG_A = 32u,   // ma = ~0
+    K2_NEG_B = 64u,   // mb = ~0
+    K2_CONST = 128u,  // OUT: the value is the constant 0 (then NEG_A makes it ~0)
+};
+constexpr int kK2MaxCofactorPis = 6;
 
-// One gate of a K2 program: slots (host) or byte offsets (device image).
+// One 16-byte record: a gate or an output.  Slots on the host, byte offsets
+// in the device image.
 struct K2Gate {
     uint32_t a, b, d;  // operand / destination slot
-    uint32_t ma, mb;   // complement masks (XOR: ma = both, mb = 0)
-    uint32_t ctl;      // K2_* flags
+    uint32_t ctl;      // K2_* flags | copy << 16
 };
-static_assert(sizeof(K2Gate) == 24, "K2Gate is the 24-byte device record");
+static_assert(sizeof(K2Gate) == 16, "K2Gate is the 16-byte device record");
 
 struct K2Prog {
     int num_pis = 0;
-    int num_slots = 0;  // PI slots + gate slots
-    uint32_t out_mask = 0;
-    bool const_out = false;
-    std::vector<K2Gate> gates;
+    int num_slots = 0;              // PI slots + gate slots
+    std::vector<K2Gate> gates;      // gates and OUT records, in execution order
+    std::vector<int32_t> cof_pis;   // cofactor PIs (ascending); copies = 2^size
+    int n_gates = 0;                // gate records (excluding OUT)
+    int loads = 0, stores = 0;      // slot loads / stores per pass (cost model)
 };
 
+// K2 program of a (possibly multi-output) graph: DFS schedule with
+// accumulator forwarding, LIFO slot reuse, OUT records in copy order.
 void build_k2prog(const Dag &dag, K2Prog *kp);
-// CPU model of the interpreter over words [w0, w0+nw) (kernel word layout).
+// Pick the cofactor depth k (0..kK2MaxCofactorPis) that minimises the
+// shared-memory traffic per word, keeping >= 2^min_words_log2 kernel words
+// per job and <= max_slots slots (the interpreter's shared-memory limit at
+// one word per thread); then build that program.
+void build_k2prog_auto(const Dag &dag, K2Prog *kp, int min_words_log2 = 9, int max_slots = 176);
+// Forced depth k (tests): the k word PIs of smallest fanout.
+void build_k2prog_k(const Dag &dag, int k, K2Prog *kp);
+// CPU model of the interpreter over FULL word indices [w0, w0+nw) (cofactor
+// PIs included): each word's output is its copy's.
 void eval_k2prog(const K2Prog &kp, uint64_t w0, uint64_t nw, uint32_t *out);
 
 }  // namespace es

@@ -52,18 +52,23 @@ struct K1Params {
 // ---------------------------------------------------------------------------
 // K2: shared-memory interpreter (es_k2prog.cpp builds its programs)
 // ---------------------------------------------------------------------------
-// Per CTA: the current job's program staged in shared memory (24-byte
+// Per CTA: the current job's program staged in shared memory (16-byte
 // records), then the slot file: slot s of thread t, word k at byte
 // s*T*W*4 + t*W*4 + k*4 -- every thread owns its columns, so the gate loop
 // needs no barrier, and each access is one W-wide vector (LDS.32/64/128).
+// With cofactor copies (es_cofactor.cpp) a job's word index w enumerates the
+// non-cofactor PIs only and OUT records fold each copy's output into (first
+// failing word, copy); the pattern index inserts the cofactor bits.
 struct K2Job {
-    const uint4 *code;           // device records, 2 x uint4 per gate
+    const uint4 *code;           // device records, one uint4 per gate / output
     unsigned long long *best;
-    unsigned long long total_words;
-    int n_gates;
+    unsigned long long total_words;  // kernel words (cofactor PIs excluded)
+    unsigned long long cof_mask;     // bit j: PI j is a cofactor PI
+    int n_recs;
     int num_pis;
     unsigned valid_mask;
-    unsigned out_mask;
+    int cof_n;
+    unsigned char cof_pos[8];        // cofactor pattern bits (PI - 1), ascending
 };
 
 struct K2Item {
@@ -101,6 +106,15 @@ __device__ __forceinline__ uint4 lds_rec(unsigned addr) {
     return r;
 }
 
+// pattern index of kernel word bits x with zero bits inserted at cof_pos[]
+__device__ __forceinline__ unsigned long long k2_expand(unsigned long long x, const K2Job &job) {
+    for (int i = 0; i < job.cof_n; ++i) {
+        const unsigned s = job.cof_pos[i];
+        x = ((x >> s) << (s + 1)) | (x & ((1ull << s) - 1ull));
+    }
+    return x;
+}
+
 template <int W>
 __global__ void __launch_bounds__(128) es_k2(const K2Job *__restrict__ jobs,
                                              const K2Item *__restrict__ items,
@@ -121,7 +135,8 @@ __global__ void __launch_bounds__(128) es_k2(const K2Job *__restrict__ jobs,
                 k = kStop;
             } else {
                 const K2Item it = items[k];
-                if ((it.w0 << 5) > *(volatile unsigned long long *)jobs[it.job].best) k = kSkip;
+                const K2Job &jb = jobs[it.job];
+                if (k2_expand(it.w0 << 5, jb) > *(volatile unsigned long long *)jb.best) k = kSkip;
             }
             s_item = k;
         }
@@ -133,65 +148,97 @@ __global__ void __launch_bounds__(128) es_k2(const K2Job *__restrict__ jobs,
         const K2Job job = jobs[it.job];
         if (it.job != cur_job) {  // stage the program records (uniform branch)
             const uint4 *src = reinterpret_cast<const uint4 *>(job.code);
-            for (int q = t; q < 2 * job.n_gates; q += T) smem[q] = __ldg(&src[q]);
+            for (int q = t; q < job.n_recs; q += T) smem[q] = __ldg(&src[q]);
             cur_job = it.job;
         }
         __syncthreads();
         for (unsigned wb = 0; wb < it.n_words; wb += T * W) {
             const unsigned long long w = it.w0 + wb + (unsigned long long)t * W;
-            // PI words into slots 0..n-1
-            for (int j = 0; j < job.num_pis; ++j) {
-                unsigned v[W];
+            // PI words into slots 0..n-1: lane PIs are constants, cofactor PIs
+            // are folded into the program, the rest are bits of w
+            {
+                int bit = 0;
+                for (int j = 0; j < job.num_pis; ++j) {
+                    if (j >= 5 && ((job.cof_mask >> (j + 1)) & 1ull)) continue;
+                    unsigned v[W];
 #pragma unroll
-                for (int q = 0; q < W; ++q)
-                    v[q] = j < 5 ? c_lane_mask[j] : ((((w + q) >> (j - 5)) & 1ull) ? ~0u : 0u);
-                sts<W>(base + (unsigned)j * T * W * 4, v);
-            }
-            unsigned acc[W];
-#pragma unroll
-            for (int q = 0; q < W; ++q) acc[q] = 0;
-            // Gate loop.  Records: {off_a, off_b, off_d, ctl} {ma, mb, -, -}.
-            // Operand A is the accumulator or is loaded into it; B is always a
-            // slot; the result stays in the accumulator and is stored only if
-            // it is live beyond the next gate.
-            uint4 r0 = lds_rec(prog_addr), r1 = lds_rec(prog_addr + 16u);
-            for (int i = 0; i < job.n_gates; ++i) {
-                const uint4 c0 = r0, c1 = r1;
-                r0 = lds_rec(prog_addr + 32u * (unsigned)(i + 1));  // next record (past-end reads harmless)
-                r1 = lds_rec(prog_addr + 32u * (unsigned)(i + 1) + 16u);
-                unsigned b[W];
-                if (!(c0.w & 2u)) lds<W>(base + c0.x, acc);
-                lds<W>(base + c0.y, b);
-                if (c0.w & 1u) {
-#pragma unroll
-                    for (int q = 0; q < W; ++q) acc[q] = acc[q] ^ b[q] ^ c1.x;
-                } else {
-#pragma unroll
-                    for (int q = 0; q < W; ++q) acc[q] = (acc[q] ^ c1.x) & (b[q] ^ c1.y);
+                    for (int q = 0; q < W; ++q)
+                        v[q] = j < 5 ? c_lane_mask[j] : ((((w + q) >> bit) & 1ull) ? ~0u : 0u);
+                    if (j >= 5) ++bit;
+                    sts<W>(base + (unsigned)j * T * W * 4, v);
                 }
-                if (c0.w & 8u) sts<W>(base + c0.z, acc);
             }
-            // outputs; lanes hold W consecutive words each, so the warp's first
-            // failing word is in its lowest active lane, lowest q
-            unsigned any = 0, outw[W];
+            unsigned acc[W], fw[W], fc[W];
+#pragma unroll
+            for (int q = 0; q < W; ++q) { acc[q] = 0; fw[q] = 0; fc[q] = 0; }
+            // Records {off_a, off_b, off_d, ctl}.  Gates: operand A is the
+            // accumulator or is loaded into it, B is a slot, the result stays
+            // in the accumulator and is stored only if read later.  OUT: fold
+            // the copy's output into (first failing word, copy) per word.
+            uint4 r0 = lds_rec(prog_addr);
+            for (int i = 0; i < job.n_recs; ++i) {
+                const uint4 c0 = r0;
+                r0 = lds_rec(prog_addr + 16u * (unsigned)(i + 1));  // next record (past-end reads harmless)
+                const unsigned ma = (c0.w & K2_NEG_A) ? ~0u : 0u;
+                if (c0.w & K2_OUT) {
+                    unsigned v[W];
+                    if (c0.w & K2_A_ACC) {
+#pragma unroll
+                        for (int q = 0; q < W; ++q) v[q] = acc[q];
+                    } else if (c0.w & K2_CONST) {
+#pragma unroll
+                        for (int q = 0; q < W; ++q) v[q] = 0u;
+                    } else {
+                        lds<W>(base + c0.x, v);
+                    }
+                    const unsigned copy = c0.w >> 16;
+#pragma unroll
+                    for (int q = 0; q < W; ++q) {
+                        const bool first = fw[q] == 0u;
+                        fw[q] = first ? (v[q] ^ ma) : fw[q];
+                        fc[q] = first ? copy : fc[q];
+                    }
+                    continue;
+                }
+                unsigned b[W];
+                if (!(c0.w & K2_A_ACC)) lds<W>(base + c0.x, acc);
+                lds<W>(base + c0.y, b);
+                if (c0.w & K2_XOR) {
+#pragma unroll
+                    for (int q = 0; q < W; ++q) acc[q] = acc[q] ^ b[q] ^ ma;
+                } else {
+                    const unsigned mb = (c0.w & K2_NEG_B) ? ~0u : 0u;
+#pragma unroll
+                    for (int q = 0; q < W; ++q) acc[q] = (acc[q] ^ ma) & (b[q] ^ mb);
+                }
+                if (c0.w & K2_STORE) sts<W>(base + c0.z, acc);
+            }
+            unsigned any = 0;
 #pragma unroll
             for (int q = 0; q < W; ++q) {
-                unsigned o = (acc[q] ^ job.out_mask) & job.valid_mask;
+                unsigned o = fw[q] & job.valid_mask;
                 if (w + q >= job.total_words || wb + t * W + q >= it.n_words) o = 0;
-                outw[q] = o;
+                fw[q] = o;
                 any |= o;
             }
-            const unsigned hit = __ballot_sync(0xffffffffu, any != 0u);
-            if (hit) {
-                const int l = __ffs(hit) - 1;
-                if ((int)lane == l) {
-                    int q = 0;
-                    unsigned v = 0;
+            if (__ballot_sync(0xffffffffu, any != 0u)) {
+                // rare path: each lane's minimum pattern (cofactor bits
+                // interleave words and copies), then the warp minimum
+                unsigned long long cand = ~0ull;
 #pragma unroll
-                    for (int z = W - 1; z >= 0; --z)
-                        if (outw[z]) { q = z; v = outw[z]; }
-                    atomicMin(job.best, ((w + q) << 5) | (unsigned long long)(__ffs(v) - 1));
+                for (int q = 0; q < W; ++q) {
+                    if (!fw[q]) continue;
+                    unsigned long long pat = k2_expand(((w + q) << 5) | (unsigned long long)(__ffs(fw[q]) - 1), job);
+                    for (int b2 = 0; b2 < job.cof_n; ++b2)
+                        if ((fc[q] >> b2) & 1u) pat |= 1ull << job.cof_pos[b2];
+                    cand = pat < cand ? pat : cand;
                 }
+#pragma unroll
+                for (int off = 16; off; off >>= 1) {
+                    const unsigned long long o2 = __shfl_xor_sync(0xffffffffu, cand, off);
+                    cand = o2 < cand ? o2 : cand;
+                }
+                if (lane == 0) atomicMin(job.best, cand);
             }
         }
     }
@@ -240,6 +287,8 @@ struct Ctx {
     cudaEvent_t ev_start = nullptr, ev_stop = nullptr, ev_slice[2] = {nullptr, nullptr};
     cudaStream_t side[3] = {nullptr, nullptr, nullptr};  // concurrent K2 launch groups
     cudaEvent_t ev_side[3] = {nullptr, nullptr, nullptr};
+    uint4 *h_stage = nullptr;  // pinned staging of K2 program records (grown on demand)
+    size_t stage_cap = 0;      // in records
 };
 
 thread_local std::vector<Ctx *> t_ctx;
@@ -503,12 +552,10 @@ static void parallel_for(int n, F fn) {
     for (auto &x : th) x.join();
 }
 
-// Device records of a gate (32 bytes): byte offsets of the operand /
-// destination slots for the launch's stride plus the K2_* flags, then the
-// complement masks.
-static void k2_records(const K2Gate &g, uint32_t stride, uint4 *out) {
-    out[0] = make_uint4(g.a * stride, g.b * stride, g.d * stride, g.ctl);
-    out[1] = make_uint4(g.ma, g.mb, 0u, 0u);
+// Device record of a gate / output (16 bytes): byte offsets of the operand /
+// destination slots for the launch's stride, then the K2_* flags.
+static uint4 k2_record(const K2Gate &g, uint32_t stride) {
+    return make_uint4(g.a * stride, g.b * stride, g.d * stride, g.ctl);
 }
 
 template <int W>
@@ -540,7 +587,8 @@ struct K2Group {
     std::vector<int> jobs_idx;   // indices into the caller's job arrays
     int W = 1, prog_bytes = 0, nb = 1;
     size_t smem = 0;
-    std::vector<uint4> code;
+    uint4 *code = nullptr;       // device-image records, in the pinned stage
+    size_t n_code = 0;
     std::vector<K2Job> jobs;
     std::vector<K2Item> items;
     std::vector<unsigned long long> h_best;
@@ -553,24 +601,30 @@ struct K2Group {
     int launches = 0;
 };
 
-static int k2_group_prepare(K2Group &gp, const es_prog *progs, const K2Prog *kps, Ctx *c) {
+static int k2_target_ctas() {
+    const char *e = getenv("ES_K2_CTAS");
+    return e ? std::max(1, atoi(e)) : 2;
+}
+
+static int k2_group_prepare(K2Group &gp, const es_prog *progs, const K2Prog *const *kps, Ctx *c,
+                            uint4 *stage) {
     const int T = 128;
     const std::vector<int> &group = gp.jobs_idx;
-    int max_slots = 1, max_gates = 1;
+    int max_slots = 1, max_recs = 1;
     for (int j : group) {
-        max_slots = std::max(max_slots, kps[j].num_slots);
-        max_gates = std::max(max_gates, (int)kps[j].gates.size());
+        max_slots = std::max(max_slots, kps[j]->num_slots);
+        max_recs = std::max(max_recs, (int)kps[j]->gates.size());
     }
-    gp.prog_bytes = (max_gates + 1) * 32;
+    gp.prog_bytes = (max_recs + 1) * 16;
     int dev_smem = 0;
     CK(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->dev));
     auto smem_for = [&](int W) { return (size_t)gp.prog_bytes + (size_t)max_slots * T * W * 4; };
+    // widest W that keeps the target number of resident CTAs per SM, else
+    // fewer CTAs (the interpreter is latency-bound: warps matter more than W)
     int W = 0;
-    for (int cand : {4, 2, 1})
-        if (2 * (smem_for(cand) + 1024) <= (size_t)dev_smem + 1024) { W = cand; break; }
-    if (!W)
-        for (int cand : {2, 1})
-            if (smem_for(cand) <= (size_t)dev_smem) { W = cand; break; }
+    for (int ctas = k2_target_ctas(); ctas >= 1 && !W; --ctas)
+        for (int cand : {4, 2, 1})
+            if ((size_t)ctas * (smem_for(cand) + 1024) <= (size_t)dev_smem + 1024) { W = cand; break; }
     if (!W) {
         set_error("program needs " + std::to_string(max_slots) + " slots: too many for the K2 interpreter");
         return ES_E_BAD_PROGRAM;
@@ -579,13 +633,18 @@ static int k2_group_prepare(K2Group &gp, const es_prog *progs, const K2Prog *kps
     gp.smem = smem_for(W);
     const uint32_t stride = (uint32_t)T * W * 4;
     const int G = (int)group.size();
-    std::vector<size_t> off(G + 1, 0);  // 2 records per gate
-    for (int q = 0; q < G; ++q) off[q + 1] = off[q] + 2 * kps[group[q]].gates.size();
-    gp.code.assign(off[G], uint4{});
+    std::vector<size_t> off(G + 1, 0);  // one record per gate / output
+    for (int q = 0; q < G; ++q) off[q + 1] = off[q] + kps[group[q]]->gates.size();
+    gp.code = stage;  // records built straight into pinned memory: one DMA, no bounce copy
+    gp.n_code = off[G];
     parallel_for(G, [&](int q) {
-        uint4 *dst = gp.code.data() + off[q];
-        for (const K2Gate &g : kps[group[q]].gates) { k2_records(g, stride, dst); dst += 2; }
+        uint4 *dst = gp.code + off[q];
+        for (const K2Gate &g : kps[group[q]]->gates) *dst++ = k2_record(g, stride);
     });
+    auto kwords = [&](int q) {  // kernel words of job q (cofactor PIs excluded)
+        const int j = group[q];
+        return 1ull << std::max(progs[j].num_pis - 5 - (int)kps[j]->cof_pis.size(), 0);
+    };
     int rc = W == 4 ? k2_occupancy<4>(gp.smem, &gp.nb) : W == 2 ? k2_occupancy<2>(gp.smem, &gp.nb)
                                                                 : k2_occupancy<1>(gp.smem, &gp.nb);
     if (rc != ES_OK) return rc;
@@ -596,7 +655,7 @@ static int k2_group_prepare(K2Group &gp, const es_prog *progs, const K2Prog *kps
     for (;;) {
         uint64_t cnt = 0;
         for (int q = 0; q < G; ++q) {
-            const uint64_t tw = 1ull << std::max(progs[group[q]].num_pis - 5, 0);
+            const uint64_t tw = kwords(q);
             cnt += (tw + std::min(tw, iw) - 1) / std::min(tw, iw);
         }
         if (cnt >= (uint64_t)c->sms * gp.nb * 8 || iw <= (uint64_t)T * W) break;
@@ -609,7 +668,7 @@ static int k2_group_prepare(K2Group &gp, const es_prog *progs, const K2Prog *kps
     uint64_t max_items = 0;
     for (int q = 0; q < G; ++q) {
         const int P = progs[group[q]].num_pis;
-        const uint64_t tw = 1ull << std::max(P - 5, 0);
+        const uint64_t tw = kwords(q);
         gp.item_words[q] = std::min<uint64_t>(tw, iw);
         gp.n_items[q] = (tw + gp.item_words[q] - 1) / gp.item_words[q];
         max_items = std::max(max_items, gp.n_items[q]);
@@ -619,12 +678,12 @@ static int k2_group_prepare(K2Group &gp, const es_prog *progs, const K2Prog *kps
     for (uint64_t r = 0; r < max_items; ++r)
         for (int q = 0; q < G; ++q)
             if (r < gp.n_items[q]) {
-                const uint64_t tw = 1ull << std::max(progs[group[q]].num_pis - 5, 0);
+                const uint64_t tw = kwords(q);
                 const uint64_t w0 = r * gp.item_words[q];
                 gp.items.push_back(K2Item{w0, (unsigned)std::min<uint64_t>(gp.item_words[q], tw - w0), q});
             }
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-    const size_t code_b = std::max<size_t>(gp.code.size(), 1) * sizeof(uint4);
+    const size_t code_b = std::max<size_t>(gp.n_code, 1) * sizeof(uint4);
     const size_t jobs_b = (size_t)G * sizeof(K2Job);
     const size_t items_b = std::max<size_t>(gp.items.size(), 1) * sizeof(K2Item);
     const size_t best_b = (size_t)G * 8;
@@ -638,13 +697,18 @@ static int k2_group_prepare(K2Group &gp, const es_prog *progs, const K2Prog *kps
         K2Job &J = gp.jobs[q];
         J.code = d_code + off[q];
         J.best = gp.d_best + q;
-        J.total_words = 1ull << std::max(progs[j].num_pis - 5, 0);
-        J.n_gates = (int)kps[j].gates.size();
+        J.total_words = kwords(q);
+        J.n_recs = (int)kps[j]->gates.size();
         J.num_pis = progs[j].num_pis;
         J.valid_mask = lane_valid_mask(progs[j].num_pis);
-        J.out_mask = kps[j].out_mask;
+        J.cof_n = (int)kps[j]->cof_pis.size();
+        J.cof_mask = 0;
+        for (int b = 0; b < J.cof_n; ++b) {
+            J.cof_pos[b] = (unsigned char)(kps[j]->cof_pis[b] - 1);
+            J.cof_mask |= 1ull << kps[j]->cof_pis[b];
+        }
     }
-    CK(cudaMemcpyAsync(d_code, gp.code.data(), gp.code.size() * sizeof(uint4), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(d_code, gp.code, gp.n_code * sizeof(uint4), cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(gp.d_jobs, gp.jobs.data(), jobs_b, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(gp.d_items, gp.items.data(), gp.items.size() * sizeof(K2Item), cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(gp.d_best, gp.h_best.data(), best_b, cudaMemcpyHostToDevice, c->stream));
@@ -662,7 +726,7 @@ static int k2_group_launch(K2Group &gp, cudaStream_t st, unsigned *counter, uint
     return rc;
 }
 
-static void k2_group_results(const K2Group &gp, const es_prog *progs, const K2Prog *kps,
+static void k2_group_results(const K2Group &gp, const es_prog *progs, const K2Prog *const *kps,
                              bool stopped, int stop_reason, es_result *outs) {
     const int G = (int)gp.jobs_idx.size();
     std::vector<uint64_t> done_cnt(G, 0);
@@ -676,10 +740,10 @@ static void k2_group_results(const K2Group &gp, const es_prog *progs, const K2Pr
         const uint64_t sentinel = 1ull << P;
         r->engine = ES_ENGINE_INTERP;
         r->launches += gp.launches;
-        r->num_luts = (int)kps[j].gates.size();
+        r->num_luts = (int)kps[j]->gates.size();
         r->regs_per_thread = gp.W;  // K2: words per thread
         const uint64_t covered = done_cnt[q];  // this job's items in completed launches
-        const uint64_t item_patterns = gp.item_words[q] * 32;
+        const uint64_t item_patterns = (gp.item_words[q] * 32) << kps[j]->cof_pis.size();
         if (gp.h_best[q] < sentinel) {
             r->verdict = ES_COUNTEREXAMPLE;
             r->witness_index = gp.h_best[q];
@@ -700,7 +764,7 @@ static void k2_group_results(const K2Group &gp, const es_prog *progs, const K2Pr
 
 static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &active,
                   const es_run_opts &o, Ctx *c, double deadline, es_result *outs,
-                  const K2Prog *prebuilt = nullptr) {
+                  const K2Prog *const *prebuilt = nullptr) {
     // host: K2 programs (schedule, accumulator forwarding), in parallel --
     // unless the caller built them already (sub-miter batches do at extraction)
     std::vector<K2Prog> own;
@@ -717,7 +781,7 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
                 Dag dag;
                 std::string err;
                 if (build_dag(progs[j], &dag, &err) != ES_OK) { bad[j] = 1; continue; }
-                build_k2prog(dag, &kps[j]);
+                build_k2prog_auto(dag, &kps[j]);
             }
         };
         const int nt = (int)std::min<size_t>(std::max(1u, std::thread::hardware_concurrency()),
@@ -729,11 +793,16 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
     }
     for (int j : active)
         if (bad[j]) { set_error("malformed program in batch (job " + std::to_string(j) + ")"); return ES_E_BAD_PROGRAM; }
-    const K2Prog *kps = prebuilt ? prebuilt : own.data();
+    std::vector<const K2Prog *> own_ptr;
+    if (!prebuilt) {
+        own_ptr.resize(n_jobs, nullptr);
+        for (int j : active) own_ptr[j] = &own[j];
+    }
+    const K2Prog *const *kps = prebuilt ? prebuilt : own_ptr.data();
     // launch groups by slot count: small programs get 4 words per thread
     std::vector<K2Group> groups(3);
     for (int j : active) {
-        const int sl = kps[j].num_slots;
+        const int sl = kps[j]->num_slots;
         groups[sl <= 44 ? 0 : sl <= 88 ? 1 : 2].jobs_idx.push_back(j);
     }
     groups.erase(std::remove_if(groups.begin(), groups.end(),
@@ -741,9 +810,21 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
                  groups.end());
     const bool verbose = getenv("ES_VERBOSE") != nullptr;
     const double t0 = now_ms();
+    size_t total_recs = 0;
+    for (const K2Group &gp : groups)
+        for (int j : gp.jobs_idx) total_recs += kps[j]->gates.size();
+    if (total_recs > c->stage_cap) {
+        if (c->h_stage) CK(cudaFreeHost(c->h_stage));
+        c->h_stage = nullptr;
+        const size_t cap = std::max(total_recs, c->stage_cap + c->stage_cap / 2);
+        CK(cudaMallocHost(&c->h_stage, cap * sizeof(uint4)));
+        c->stage_cap = cap;
+    }
+    size_t stage_off = 0;
     for (K2Group &gp : groups) {  // host images + one upload phase
-        int rc = k2_group_prepare(gp, progs, kps, c);
+        int rc = k2_group_prepare(gp, progs, kps, c, c->h_stage + stage_off);
         if (rc != ES_OK) return rc;
+        stage_off += gp.n_code;
     }
     const double t1 = now_ms();
     CK(cudaEventRecord(c->ev_start, c->stream));
@@ -791,10 +872,17 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
     for (K2Group &gp : groups) k2_group_results(gp, progs, kps, stopped, stop_reason, outs);
     for (int j : active) outs[j].device_ms = dev_ms;
     if (verbose)
-        for (K2Group &gp : groups)
-            fprintf(stderr, "[es k2] group W=%d jobs=%zu items=%zu records=%zu | host+upload %.2fms, "
-                            "kernels %.2fms (makespan)\n", gp.W, gp.jobs_idx.size(), gp.items.size(),
-                    gp.code.size(), t1 - t0, dev_ms);
+        for (size_t g = 0; g < groups.size(); ++g) {
+            const K2Group &gp = groups[g];
+            float gms = -1;
+            if (!sliced) cudaEventElapsedTime(&gms, c->ev_start, c->ev_side[g]);
+            int cof = 0;
+            for (int j : gp.jobs_idx) cof += (int)kps[j]->cof_pis.size();
+            fprintf(stderr, "[es k2] group W=%d jobs=%zu items=%zu records=%zu mean-k=%.2f | host+upload "
+                            "%.2fms, this group %.2fms, makespan %.2fms\n", gp.W, gp.jobs_idx.size(),
+                    gp.items.size(), gp.n_code, (double)cof / std::max<size_t>(1, gp.jobs_idx.size()),
+                    t1 - t0, gms, dev_ms);
+        }
     return ES_OK;
 }
 
@@ -982,7 +1070,7 @@ int run_one(const es_prog *prog, const es_run_opts *opts, es_result *out) {
 }
 
 int run_batch(int n_jobs, const es_prog *progs, const es_run_opts *opts, es_result *outs,
-              const K2Prog *prebuilt) {
+              const K2Prog *const *prebuilt) {
     const double t0 = now_ms();
     es_run_opts o{};
     if (opts) o = *opts;
@@ -1146,6 +1234,7 @@ void runtime_shutdown() {
         cudaFree(c->d_best);
         cudaFree(c->d_counter);
         cudaFreeHost(c->h_pin);
+        if (c->h_stage) cudaFreeHost(c->h_stage);
         cudaEventDestroy(c->ev_start);
         cudaEventDestroy(c->ev_stop);
         cudaEventDestroy(c->ev_slice[0]);

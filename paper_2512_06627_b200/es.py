@@ -412,12 +412,21 @@ def k2_stats(p) -> dict:
             "acc_reads": v[3].value}
 
 
-def k2_eval(p, w0: int, nw: int) -> np.ndarray:
-    """CPU model of the K2 interpreter: output words [w0, w0+nw)."""
+def k2_eval(p, w0: int, nw: int, k: int | None = None) -> np.ndarray:
+    """CPU model of the K2 interpreter: output words [w0, w0+nw) (full word
+    indices).  ``k``: forced cofactor PIs; None = the depth K2 picks."""
     prog = as_program(p)
     out = np.zeros(nw, dtype=np.uint32)
-    N.check(N.lib().es_k2_eval(ctypes.byref(prog.as_struct()), w0, nw, out.ctypes.data))
+    if k is None:
+        N.check(N.lib().es_k2_eval(ctypes.byref(prog.as_struct()), w0, nw, out.ctypes.data))
+    else:
+        N.check(N.lib().es_k2_eval_k(ctypes.byref(prog.as_struct()), k, w0, nw, out.ctypes.data))
     return out
+
+
+def k2_cofactor_pis(p) -> int:
+    """Cofactor depth the K2 interpreter picks for ``p``."""
+    return N.check(N.lib().es_k2_cofactor_pis(ctypes.byref(as_program(p).as_struct())))
 
 
 def emit_ptx(p, block_threads: int = 256, k: int = 0) -> str:
