@@ -216,6 +216,35 @@ int32_t es_ipc_close(int32_t device, void *dev_ptr, int32_t owner);
 int32_t es_word_write(int32_t device, void *dev_ptr, uint64_t value);
 int32_t es_word_read(int32_t device, void *dev_ptr, uint64_t *value);
 
+/*
+ * K3: word-parallel random simulation (the sweep's
+ * candidate-class discovery and refinement).  simulate (sim.py:21-38): the
+ * XAG as packed gates (as es_compile), pi_words = num_pis x words uint64
+ * (row i drives PI i+1, bit b of word w = pattern 64w+b), node_words =
+ * (1+num_pis+num_gates) x words, row-major, the reference's array exactly.
+ * device_ms (may be NULL) = the simulation kernels' CUDA-event time.
+ */
+int32_t es_sim(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+               const uint32_t *in1, const uint64_t *pi_words, int64_t words, int32_t device,
+               uint64_t *node_words, double *device_ms);
+/* The same on device buffers, enqueued on `stream` (a cudaStream_t) without
+ * host synchronisation.  *prog_cache (may be NULL) keeps the compiled gate
+ * program between calls on the same XAG; free it with es_sim_prog_free. */
+int32_t es_sim_device(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+                      const uint32_t *in1, const uint64_t *d_pi_words, int64_t words, void *stream,
+                      uint64_t *d_node_words, void **prog_cache);
+void es_sim_prog_free(void *prog_cache);
+/* Host only: logic levels of the simulation program (batches never span one). */
+int32_t es_sim_levels(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+                     const uint32_t *in1);
+/* random_simulate + build_pe_classes (sweep.py:54-81) under the given drive:
+ * class_id[node] = class index in representative (smallest member) order,
+ * -1 for a singleton; polarity[node] = the canonical polarity (the
+ * complemented row's bytes compare smaller).  Arrays have num_nodes entries. */
+int32_t es_sim_classes(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+                       const uint32_t *in1, const uint64_t *pi_words, int64_t words, int32_t device,
+                       int32_t *class_id, uint8_t *polarity, int32_t *n_classes, double *device_ms);
+
 /* Engine-internal views for tests and profiling. */
 /* LUT-3 mapping statistics of a program: LOP3s per word, schedule peak live. */
 int32_t es_map_stats(const es_prog *prog, int32_t *num_luts, int32_t *peak_live,

@@ -37,6 +37,7 @@ EXPORTS = ("es_compile", "es_run", "es_run_batch", "es_session_open", "es_sessio
            "es_ipc_alloc", "es_ipc_open", "es_ipc_close", "es_word_write", "es_word_read",
            "es_map_stats_k", "es_map_pipes_k", "es_map_eval_k", "es_emit_ptx_k", "es_jit_check_k",
            "es_k2_eval_k", "es_k2_cofactor_pis", "es_batch_prepare",
+           "es_sim", "es_sim_device", "es_sim_prog_free", "es_sim_classes", "es_sim_levels",
            "es_last_error", "es_version", "es_shutdown")
 
 _P = ctypes.c_void_p
@@ -151,6 +152,16 @@ def lib():
                                        _P, _P, ctypes.c_int32, _P, _P, _P, ctypes.c_int32,
                                        ctypes.POINTER(_P)]
         L.es_batch_extract.restype = ctypes.c_int32
+        L.es_sim.argtypes = [_I, _I, _P, _P, _P, _P, ctypes.c_int64, _I, _P, _P]
+        L.es_sim.restype = _I
+        L.es_sim_device.argtypes = [_I, _I, _P, _P, _P, _P, ctypes.c_int64, _P, _P, _P]
+        L.es_sim_device.restype = _I
+        L.es_sim_prog_free.argtypes = [_P]
+        L.es_sim_prog_free.restype = None
+        L.es_sim_classes.argtypes = [_I, _I, _P, _P, _P, _P, ctypes.c_int64, _I, _P, _P, _P, _P]
+        L.es_sim_classes.restype = _I
+        L.es_sim_levels.argtypes = [_I, _I, _P, _P, _P]
+        L.es_sim_levels.restype = _I
         L.es_batch_prepare.argtypes = [_P, ctypes.c_int32]
         L.es_batch_prepare.restype = ctypes.c_int32
         L.es_batch_size.argtypes = [_P]

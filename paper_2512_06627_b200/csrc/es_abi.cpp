@@ -30,6 +30,18 @@ int ipc_alloc(int dev, void **ptr, unsigned char *handle);
 int ipc_open(int dev, const unsigned char *handle, void **ptr);
 int ipc_close(int dev, void *ptr, int owner);
 int word_io(int dev, void *ptr, uint64_t *value, int write);
+int sim_run(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+            const uint32_t *in1, const uint64_t *pi_words, int64_t words, int32_t device,
+            uint64_t *node_words, double *device_ms);
+int sim_run_device(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+                   const uint32_t *in1, const uint64_t *d_pi_words, int64_t words, void *stream,
+                   uint64_t *d_node_words, void **prog_cache);
+void sim_prog_free(void *prog_cache);
+int sim_levels(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+              const uint32_t *in1);
+int sim_classes(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+                const uint32_t *in1, const uint64_t *pi_words, int64_t words, int32_t device,
+                int32_t *class_id, uint8_t *polarity, int32_t *n_classes, double *device_ms);
 
 // k = cofactor PIs (0: none), chosen as the runtime does (rank_cofactor_pis)
 static int map_prog(const es_prog *prog, LutNet *net, int k = 0) {
@@ -257,6 +269,43 @@ int64_t es_jit_check_k(const es_prog *prog, int32_t k, int32_t block_threads, in
         log[n] = '\0';
     }
     return (int64_t)cubin.size();
+}
+
+int32_t es_sim(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+               const uint32_t *in1, const uint64_t *pi_words, int64_t words, int32_t device,
+               uint64_t *node_words, double *device_ms) {
+    if ((num_gates > 0 && (!kind || !in0 || !in1)) || (num_pis > 0 && !pi_words) || !node_words) {
+        set_error("null argument");
+        return ES_E_BAD_ARG;
+    }
+    return sim_run(num_pis, num_gates, kind, in0, in1, pi_words, words, device, node_words, device_ms);
+}
+
+int32_t es_sim_device(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+                      const uint32_t *in1, const uint64_t *d_pi_words, int64_t words, void *stream,
+                      uint64_t *d_node_words, void **prog_cache) {
+    if ((num_gates > 0 && (!kind || !in0 || !in1)) || !d_node_words) { set_error("null argument"); return ES_E_BAD_ARG; }
+    return sim_run_device(num_pis, num_gates, kind, in0, in1, d_pi_words, words, stream, d_node_words,
+                          prog_cache);
+}
+
+void es_sim_prog_free(void *prog_cache) { sim_prog_free(prog_cache); }
+
+int32_t es_sim_levels(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+                     const uint32_t *in1) {
+    if (num_gates > 0 && (!kind || !in0 || !in1)) { set_error("null argument"); return ES_E_BAD_ARG; }
+    return sim_levels(num_pis, num_gates, kind, in0, in1);
+}
+
+int32_t es_sim_classes(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+                       const uint32_t *in1, const uint64_t *pi_words, int64_t words, int32_t device,
+                       int32_t *class_id, uint8_t *polarity, int32_t *n_classes, double *device_ms) {
+    if ((num_gates > 0 && (!kind || !in0 || !in1)) || (num_pis > 0 && !pi_words)) {
+        set_error("null argument");
+        return ES_E_BAD_ARG;
+    }
+    return sim_classes(num_pis, num_gates, kind, in0, in1, pi_words, words, device, class_id, polarity,
+                       n_classes, device_ms);
 }
 
 int32_t es_alu_peak(int32_t device, double *lane_ops_per_s, double *ms) {

@@ -1,0 +1,437 @@
+// es_sim.cu -- K3: word-parallel random simulation of a whole XAG (sm_100a).
+//
+// Reference: cecprove/sim.py:21-38 (simulate) -- every node gets a row of
+// 64-bit words, bit b of word w = the node's value under pattern 64*w+b --
+// and sweep.py:54-81 (_signatures / build_pe_classes): nodes grouped by their
+// polarity-canonical row.  SURVEY 8(f) next-3: the sweep's random simulation,
+// candidate-class discovery and counterexample refinement.
+//
+// Layout in HBM is the reference's array: vals[node][word] (uint64,
+// row-major), PI rows = the caller's pi_words, node 0 = 0.  One thread per
+// 64-bit word walks the gates level by level, in batches of up to kSimU
+// gates of one level: it issues all 2*kSimU fanin loads of a batch (rows of
+// earlier levels, L2-resident: the kernel sweeps the word space in tiles so
+// the live rows of a tile fit in L2), then computes and stores the batch --
+// loads and stores coalesced across the warp.  Every node row is written
+// exactly once, so the kernel is bound by HBM writes: 8 bytes per gate per
+// word (the drive and the fanin re-reads come from L2).
+//
+// Classes: one warp per node hashes its polarity-canonical row (polarity =
+// bit 7 of word 0: the reference compares the rows' little-endian bytes, and
+// the first byte of a row and of its complement always differ); the host
+// groups nodes by hash, the device then checks every member's row against its
+// group leader word by word, and only a failed check (a 64-bit collision)
+// falls back to comparing downloaded rows on the host.  Classes are therefore
+// exactly the reference's.
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <numeric>
+#include <queue>
+#include <tuple>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/es_b200.h"
+
+namespace es {
+
+void set_error(const std::string &m);
+
+namespace {
+
+#define SCK(call)                                                                   \
+    do {                                                                            \
+        cudaError_t e_ = (call);                                                    \
+        if (e_ != cudaSuccess) {                                                    \
+            set_error(std::string(#call) + ": " + cudaGetErrorString(e_));          \
+            return ES_E_CUDA;                                                       \
+        }                                                                           \
+    } while (0)
+
+// record: {fanin node a, fanin node b, output node, flags}; flags bit 0 XOR,
+// 1 NEG_A, 2 NEG_B.  Gates are sorted by level and cut into batches of
+// kSimU gates of one level (padded with flags bit 3: no-op).
+struct SimRec {
+    uint32_t a, b, d, f;
+};
+constexpr int kSimU = 8;
+
+__global__ void __launch_bounds__(256) es_sim_kernel(const SimRec *__restrict__ recs, int n_batches,
+                                                     long long w_begin, long long w_end,
+                                                     long long words,
+                                                     unsigned long long *__restrict__ vals) {
+    const long long w = w_begin + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= w_end) return;
+    for (int bt = 0; bt < n_batches; ++bt) {
+        const SimRec *rb = recs + bt * kSimU;
+        unsigned long long x[kSimU], y[kSimU];
+        SimRec r[kSimU];
+#pragma unroll
+        for (int u = 0; u < kSimU; ++u) r[u] = rb[u];  // uniform: one broadcast per record
+#pragma unroll
+        for (int u = 0; u < kSimU; ++u) {
+            x[u] = vals[(long long)r[u].a * words + w];
+            y[u] = vals[(long long)r[u].b * words + w];
+        }
+#pragma unroll
+        for (int u = 0; u < kSimU; ++u) {
+            if (r[u].f & 8u) continue;
+            const unsigned long long xa = (r[u].f & 2u) ? ~x[u] : x[u];
+            const unsigned long long yb = (r[u].f & 4u) ? ~y[u] : y[u];
+            vals[(long long)r[u].d * words + w] = (r[u].f & 1u) ? (xa ^ yb) : (xa & yb);
+        }
+    }
+}
+
+// per node: polarity (bit 7 of word 0) and a 64-bit hash of the canonical row
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+    x ^= x >> 33; x *= 0xff51afd7ed558ccdull;
+    x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ull;
+    x ^= x >> 33;
+    return x;
+}
+
+__global__ void es_sig_kernel(const unsigned long long *__restrict__ vals, int n_nodes, long long words,
+                              unsigned long long *__restrict__ hash, unsigned char *__restrict__ pol) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= n_nodes) return;
+    const unsigned long long *row = vals + (long long)warp * words;
+    const unsigned long long inv = (row[0] >> 7) & 1ull ? ~0ull : 0ull;
+    unsigned long long h = 0;
+    for (long long q = lane; q < words; q += 32)
+        h += mix64((row[q] ^ inv) + 0x9e3779b97f4a7c15ull * (unsigned long long)(q + 1));
+#pragma unroll
+    for (int off = 16; off; off >>= 1) h += __shfl_xor_sync(0xffffffffu, h, off);
+    if (lane == 0) {
+        hash[warp] = mix64(h ^ (unsigned long long)words);
+        pol[warp] = (unsigned char)(inv & 1ull);
+    }
+}
+
+// members[i] vs leader[i]: canonical rows equal?  one warp per pair
+__global__ void es_verify_kernel(const unsigned long long *__restrict__ vals, long long words,
+                                 const int *__restrict__ member, const int *__restrict__ leader, int n,
+                                 const unsigned char *__restrict__ pol, int *__restrict__ bad) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= n) return;
+    const int m = member[warp], l = leader[warp];
+    const unsigned long long im = pol[m] ? ~0ull : 0ull, il = pol[l] ? ~0ull : 0ull;
+    const unsigned long long *rm = vals + (long long)m * words, *rl = vals + (long long)l * words;
+    int diff = 0;
+    for (long long q = lane; q < words; q += 32) diff |= (rm[q] ^ im) != (rl[q] ^ il);
+    diff = __any_sync(0xffffffffu, diff);
+    if (lane == 0) bad[warp] = diff;
+}
+
+struct SimProg {
+    std::vector<SimRec> recs;  // whole batches
+    int levels = 0;
+};
+
+// Levelised gate list: level(v) = 1 + max level of its gate fanins; gates
+// sorted by (level, node), each level cut into batches of kSimU (the last
+// batch of a level padded with no-ops), so a batch never reads a row it
+// writes.
+int build_sim_prog(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+                   const uint32_t *in1, SimProg *sp) {
+    const int FG = 1 + num_pis, NN = FG + num_gates;
+    std::vector<int> lvl(NN, 0);
+    int max_lvl = 0;
+    for (int g = 0; g < num_gates; ++g) {
+        const int v = FG + g, a = (int)(in0[g] >> 1), b = (int)(in1[g] >> 1);
+        if (a >= v || b >= v) { set_error("simulation: XAG not topological"); return ES_E_BAD_PROGRAM; }
+        lvl[v] = 1 + std::max(lvl[a], lvl[b]);
+        max_lvl = std::max(max_lvl, lvl[v]);
+    }
+    std::vector<int> start(max_lvl + 2, 0), order(num_gates);
+    for (int g = 0; g < num_gates; ++g) start[lvl[FG + g] + 1]++;
+    for (int l = 0; l <= max_lvl; ++l) start[l + 1] += start[l];
+    {
+        std::vector<int> fill(start.begin(), start.end() - 1);
+        for (int g = 0; g < num_gates; ++g) order[fill[lvl[FG + g]]++] = g;
+    }
+    sp->recs.clear();
+    sp->levels = max_lvl;
+    for (int l = 1; l <= max_lvl; ++l) {
+        for (int q = start[l]; q < start[l + 1]; ++q) {
+            const int g = order[q];
+            SimRec r{};
+            r.a = in0[g] >> 1;
+            r.b = in1[g] >> 1;
+            r.d = (uint32_t)(FG + g);
+            r.f = (kind[g] ? 1u : 0u) | ((in0[g] & 1) ? 2u : 0u) | ((in1[g] & 1) ? 4u : 0u);
+            sp->recs.push_back(r);
+        }
+        while (sp->recs.size() % kSimU) sp->recs.push_back(SimRec{0, 0, 0, 8u});
+    }
+    return ES_OK;
+}
+
+struct SimDev {
+    int dev = -1;
+    cudaStream_t st = nullptr;
+};
+
+int sim_device(int dev, SimDev **out) {
+    static thread_local std::vector<SimDev *> ctx;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) { set_error("no CUDA device visible"); return ES_E_NO_DEVICE; }
+    if (dev < 0 || dev >= n) { set_error("device ordinal out of range"); return ES_E_BAD_ARG; }
+    SCK(cudaSetDevice(dev));
+    for (SimDev *c : ctx)
+        if (c->dev == dev) { *out = c; return ES_OK; }
+    SimDev *c = new SimDev();
+    c->dev = dev;
+    SCK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    ctx.push_back(c);
+    *out = c;
+    return ES_OK;
+}
+
+// Enqueue the simulation on `st` with device buffers (vals: num_nodes x words).
+// The word space is swept in tiles whose live rows fit in L2 (the fanin
+// re-reads then never reach HBM).
+int sim_enqueue(const SimProg &sp, const SimRec *d_recs, int num_pis, long long words,
+                const unsigned long long *d_pi, unsigned long long *d_vals, cudaStream_t st,
+                long long num_nodes) {
+    SCK(cudaMemsetAsync(d_vals, 0, (size_t)words * 8, st));  // node 0 = 0
+    if (num_pis > 0)
+        SCK(cudaMemcpyAsync(d_vals + words, d_pi, (size_t)num_pis * words * 8, cudaMemcpyDeviceToDevice, st));
+    if (sp.recs.empty()) return ES_OK;
+    const int T = 256;
+    // tile: all rows of the tile <= ~48 MB (a third of L2), >= 2 waves of CTAs
+    long long tile = std::max<long long>(T * 148 * 2, (48ll << 20) / (8 * std::max<long long>(num_nodes, 1)));
+    tile = (tile + T - 1) / T * T;
+    for (long long w0 = 0; w0 < words; w0 += tile) {
+        const long long w1 = std::min(words, w0 + tile);
+        const long long grid = (w1 - w0 + T - 1) / T;
+        es_sim_kernel<<<(unsigned)grid, T, 0, st>>>(d_recs, (int)(sp.recs.size() / kSimU), w0, w1, words, d_vals);
+        SCK(cudaGetLastError());
+    }
+    return ES_OK;
+}
+
+}  // namespace
+
+int sim_levels(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+              const uint32_t *in1) {
+    SimProg sp;
+    const int rc = build_sim_prog(num_pis, num_gates, kind, in0, in1, &sp);
+    return rc == ES_OK ? sp.levels : rc;
+}
+
+// simulate() with host buffers (sim.py:21-38): node_words = num_nodes x words
+int sim_run(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+            const uint32_t *in1, const uint64_t *pi_words, int64_t words, int32_t device,
+            uint64_t *node_words, double *device_ms) {
+    if (words < 1 || num_pis < 0 || num_gates < 0) { set_error("bad argument"); return ES_E_BAD_ARG; }
+    SimProg sp;
+    int rc = build_sim_prog(num_pis, num_gates, kind, in0, in1, &sp);
+    if (rc != ES_OK) return rc;
+    SimDev *c = nullptr;
+    rc = sim_device(device, &c);
+    if (rc != ES_OK) return rc;
+    const long long NN = 1 + num_pis + num_gates;
+    SimRec *d_recs = nullptr;
+    unsigned long long *d_pi = nullptr, *d_vals = nullptr;
+    SCK(cudaMallocAsync(&d_recs, std::max<size_t>(sp.recs.size(), 1) * sizeof(SimRec), c->st));
+    SCK(cudaMallocAsync(&d_pi, std::max<size_t>((size_t)num_pis * words, 1) * 8, c->st));
+    SCK(cudaMallocAsync(&d_vals, (size_t)NN * words * 8, c->st));
+    if (!sp.recs.empty())
+        SCK(cudaMemcpyAsync(d_recs, sp.recs.data(), sp.recs.size() * sizeof(SimRec), cudaMemcpyHostToDevice, c->st));
+    if (num_pis > 0)
+        SCK(cudaMemcpyAsync(d_pi, pi_words, (size_t)num_pis * words * 8, cudaMemcpyHostToDevice, c->st));
+    cudaEvent_t e0, e1;
+    SCK(cudaEventCreate(&e0));
+    SCK(cudaEventCreate(&e1));
+    SCK(cudaEventRecord(e0, c->st));
+    rc = sim_enqueue(sp, d_recs, num_pis, words, d_pi, d_vals, c->st, NN);
+    SCK(cudaEventRecord(e1, c->st));
+    if (rc == ES_OK)
+        SCK(cudaMemcpyAsync(node_words, d_vals, (size_t)NN * words * 8, cudaMemcpyDeviceToHost, c->st));
+    SCK(cudaStreamSynchronize(c->st));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (device_ms) *device_ms = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFreeAsync(d_recs, c->st);
+    cudaFreeAsync(d_pi, c->st);
+    cudaFreeAsync(d_vals, c->st);
+    SCK(cudaStreamSynchronize(c->st));
+    return rc;
+}
+
+// Device-resident variant for callers that own the buffers (torch tensors):
+// enqueued on `stream`, no host synchronisation.
+int sim_run_device(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+                   const uint32_t *in1, const uint64_t *d_pi_words, int64_t words, void *stream,
+                   uint64_t *d_node_words, void **prog_cache) {
+    if (words < 1 || num_pis < 0 || num_gates < 0) { set_error("bad argument"); return ES_E_BAD_ARG; }
+    struct Cached { SimProg sp; SimRec *d_recs = nullptr; };
+    Cached *cp = prog_cache ? (Cached *)*prog_cache : nullptr;
+    if (!cp) {
+        cp = new Cached();
+        int rc = build_sim_prog(num_pis, num_gates, kind, in0, in1, &cp->sp);
+        if (rc != ES_OK) { delete cp; return rc; }
+        SCK(cudaMalloc(&cp->d_recs, std::max<size_t>(cp->sp.recs.size(), 1) * sizeof(SimRec)));
+        if (!cp->sp.recs.empty())
+            SCK(cudaMemcpy(cp->d_recs, cp->sp.recs.data(), cp->sp.recs.size() * sizeof(SimRec), cudaMemcpyHostToDevice));
+        if (prog_cache) *prog_cache = cp;
+    }
+    int rc = sim_enqueue(cp->sp, cp->d_recs, num_pis, words, (const unsigned long long *)d_pi_words,
+                         (unsigned long long *)d_node_words, (cudaStream_t)stream,
+                         1ll + num_pis + num_gates);
+    if (!prog_cache) {
+        cudaStreamSynchronize((cudaStream_t)stream);
+        cudaFree(cp->d_recs);
+        delete cp;
+    }
+    return rc;
+}
+
+void sim_prog_free(void *prog_cache) {
+    struct Cached { SimProg sp; SimRec *d_recs = nullptr; };
+    Cached *cp = (Cached *)prog_cache;
+    if (!cp) return;
+    cudaFree(cp->d_recs);
+    delete cp;
+}
+
+// random_simulate + build_pe_classes (sweep.py:66-81) from a PI drive:
+// class_id[node] = index of its class in representative order, -1 for a
+// singleton; polarity[node] = canonical polarity (inv < raw).
+int sim_classes(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+                const uint32_t *in1, const uint64_t *pi_words, int64_t words, int32_t device,
+                int32_t *class_id, uint8_t *polarity, int32_t *n_classes, double *device_ms) {
+    if (words < 1 || num_pis < 0 || num_gates < 0 || !class_id || !polarity || !n_classes) {
+        set_error("bad argument");
+        return ES_E_BAD_ARG;
+    }
+    SimProg sp;
+    int rc = build_sim_prog(num_pis, num_gates, kind, in0, in1, &sp);
+    if (rc != ES_OK) return rc;
+    SimDev *c = nullptr;
+    rc = sim_device(device, &c);
+    if (rc != ES_OK) return rc;
+    const int NN = 1 + num_pis + num_gates;
+    SimRec *d_recs = nullptr;
+    unsigned long long *d_pi = nullptr, *d_vals = nullptr, *d_hash = nullptr;
+    unsigned char *d_pol = nullptr;
+    SCK(cudaMallocAsync(&d_recs, std::max<size_t>(sp.recs.size(), 1) * sizeof(SimRec), c->st));
+    SCK(cudaMallocAsync(&d_pi, std::max<size_t>((size_t)num_pis * words, 1) * 8, c->st));
+    SCK(cudaMallocAsync(&d_vals, (size_t)NN * words * 8, c->st));
+    SCK(cudaMallocAsync(&d_hash, (size_t)NN * 8, c->st));
+    SCK(cudaMallocAsync(&d_pol, (size_t)NN, c->st));
+    if (!sp.recs.empty())
+        SCK(cudaMemcpyAsync(d_recs, sp.recs.data(), sp.recs.size() * sizeof(SimRec), cudaMemcpyHostToDevice, c->st));
+    if (num_pis > 0)
+        SCK(cudaMemcpyAsync(d_pi, pi_words, (size_t)num_pis * words * 8, cudaMemcpyHostToDevice, c->st));
+    cudaEvent_t e0, e1;
+    SCK(cudaEventCreate(&e0));
+    SCK(cudaEventCreate(&e1));
+    SCK(cudaEventRecord(e0, c->st));
+    rc = sim_enqueue(sp, d_recs, num_pis, words, d_pi, d_vals, c->st, NN);
+    if (rc != ES_OK) return rc;
+    es_sig_kernel<<<(NN * 32 + 255) / 256, 256, 0, c->st>>>(d_vals, NN, words, d_hash, d_pol);
+    SCK(cudaGetLastError());
+    std::vector<unsigned long long> h(NN);
+    std::vector<unsigned char> pol(NN);
+    SCK(cudaMemcpyAsync(h.data(), d_hash, (size_t)NN * 8, cudaMemcpyDeviceToHost, c->st));
+    SCK(cudaMemcpyAsync(pol.data(), d_pol, (size_t)NN, cudaMemcpyDeviceToHost, c->st));
+    SCK(cudaStreamSynchronize(c->st));
+    // group by hash; groups in first-member order = representative order
+    std::unordered_map<unsigned long long, int> gid;
+    gid.reserve((size_t)NN * 2);
+    std::vector<int> group(NN), gsize, gleader;
+    for (int v = 0; v < NN; ++v) {
+        auto it = gid.find(h[v]);
+        int g;
+        if (it == gid.end()) { g = (int)gsize.size(); gid.emplace(h[v], g); gsize.push_back(0); gleader.push_back(v); }
+        else g = it->second;
+        group[v] = g;
+        gsize[g]++;
+    }
+    // verify every non-leader member of a multi-node group on the device
+    std::vector<int> mem, lead;
+    for (int v = 0; v < NN; ++v)
+        if (gsize[group[v]] >= 2 && gleader[group[v]] != v) { mem.push_back(v); lead.push_back(gleader[group[v]]); }
+    std::vector<int> bad(mem.size(), 0);
+    if (!mem.empty()) {
+        int *d_m = nullptr, *d_l = nullptr, *d_bad = nullptr;
+        const size_t nb = mem.size() * sizeof(int);
+        SCK(cudaMallocAsync(&d_m, nb, c->st));
+        SCK(cudaMallocAsync(&d_l, nb, c->st));
+        SCK(cudaMallocAsync(&d_bad, nb, c->st));
+        SCK(cudaMemcpyAsync(d_m, mem.data(), nb, cudaMemcpyHostToDevice, c->st));
+        SCK(cudaMemcpyAsync(d_l, lead.data(), nb, cudaMemcpyHostToDevice, c->st));
+        es_verify_kernel<<<(unsigned)((mem.size() * 32 + 255) / 256), 256, 0, c->st>>>(
+            d_vals, words, d_m, d_l, (int)mem.size(), d_pol, d_bad);
+        SCK(cudaGetLastError());
+        SCK(cudaMemcpyAsync(bad.data(), d_bad, nb, cudaMemcpyDeviceToHost, c->st));
+        SCK(cudaEventRecord(e1, c->st));
+        SCK(cudaStreamSynchronize(c->st));
+        cudaFreeAsync(d_m, c->st);
+        cudaFreeAsync(d_l, c->st);
+        cudaFreeAsync(d_bad, c->st);
+    } else {
+        SCK(cudaEventRecord(e1, c->st));
+        SCK(cudaStreamSynchronize(c->st));
+    }
+    // a 64-bit collision: regroup that hash group exactly from downloaded rows
+    std::vector<int> sub(NN, 0);  // sub-group within a hash group (0 = leader's)
+    std::vector<char> split(gsize.size(), 0);
+    for (size_t q = 0; q < mem.size(); ++q)
+        if (bad[q]) split[group[mem[q]]] = 1;
+    for (size_t g = 0; g < gsize.size(); ++g) {
+        if (!split[g]) continue;
+        std::vector<int> nodes;
+        for (int v = 0; v < NN; ++v) if (group[v] == (int)g) nodes.push_back(v);
+        std::vector<std::vector<unsigned long long>> rows(nodes.size(), std::vector<unsigned long long>(words));
+        for (size_t q = 0; q < nodes.size(); ++q) {
+            SCK(cudaMemcpy(rows[q].data(), d_vals + (long long)nodes[q] * words, words * 8, cudaMemcpyDeviceToHost));
+            if (pol[nodes[q]]) for (auto &x : rows[q]) x = ~x;
+        }
+        int next = 0;
+        std::vector<int> lab(nodes.size(), -1);
+        for (size_t q = 0; q < nodes.size(); ++q) {
+            if (lab[q] >= 0) continue;
+            lab[q] = next++;
+            for (size_t r = q + 1; r < nodes.size(); ++r)
+                if (lab[r] < 0 && rows[r] == rows[q]) lab[r] = lab[q];
+        }
+        for (size_t q = 0; q < nodes.size(); ++q) sub[nodes[q]] = lab[q];
+    }
+    // class ids in representative (= first member) order, singletons -1
+    std::unordered_map<long long, int> cid;
+    std::unordered_map<long long, int> csize;
+    for (int v = 0; v < NN; ++v) csize[(long long)group[v] * NN + sub[v]]++;
+    int nc = 0;
+    for (int v = 0; v < NN; ++v) {
+        const long long key = (long long)group[v] * NN + sub[v];
+        polarity[v] = pol[v];
+        if (csize[key] < 2) { class_id[v] = -1; continue; }
+        auto it = cid.find(key);
+        if (it == cid.end()) { cid.emplace(key, nc); class_id[v] = nc++; }
+        else class_id[v] = it->second;
+    }
+    *n_classes = nc;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (device_ms) *device_ms = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFreeAsync(d_recs, c->st);
+    cudaFreeAsync(d_pi, c->st);
+    cudaFreeAsync(d_vals, c->st);
+    cudaFreeAsync(d_hash, c->st);
+    cudaFreeAsync(d_pol, c->st);
+    SCK(cudaStreamSynchronize(c->st));
+    return ES_OK;
+}
+
+}  // namespace es

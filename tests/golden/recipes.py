@@ -128,3 +128,29 @@ def build_with_reference(spec: dict, ref_miter, ref_xag):
     if "flip_gate" in spec:
         return None
     return x
+
+
+# --- random-simulation population (make_golden_sim.py, tests/test_sim*.py) ---
+
+def sim_population() -> list[dict]:
+    """Circuits x drives: random XAGs, multiplier/adder miters, the config
+    miters at the sweep's 64-word default (sweep.py:313)."""
+    specs = []
+    rng = random.Random(77)
+    for k in range(40):
+        specs.append({"kind": "random", "n_pis": rng.randint(1, 20), "n_gates": rng.randint(0, 600),
+                      "seed": 7000 + k, "words": rng.choice([1, 2, 3, 17, 64, 100]), "sim_seed": k})
+    for w, a, b in [(4, "array", "diagonal"), (6, "array", "diagonal"), (8, "array", "diagonal"),
+                    (8, "array", "booth"), (12, "array", "wallace"), (16, "array", "booth")]:
+        for words, seed in [(1, 0), (64, 0), (64, 3), (257, 1)]:
+            specs.append({"kind": "mult", "width": w, "a": a, "b": b, "words": words, "sim_seed": seed})
+    specs.append({"kind": "adder", "width": 8, "words": 64, "sim_seed": 0})
+    return specs
+
+
+def build_sim(spec):
+    if spec["kind"] == "random":
+        return random_xag(spec["n_pis"], spec["n_gates"], spec["seed"])
+    if spec["kind"] == "mult":
+        return M.gen_multiplier_miter(spec["width"], spec["a"], spec["b"])
+    return M.gen_adder_miter(spec["width"])
