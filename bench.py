@@ -114,7 +114,68 @@ def measure_cones(steps: int, warmup: int, rank: int = 0, world: int = 1, count:
             "e2e_value": work / (statistics.mean(wall_ms) * 1e-3)}
 
 
-def measure_other_configs(local: int) -> dict:
+def measure_random_sim(local: int, words: int = 1 << 16, cpu: bool = True) -> dict:
+    """K3 random simulation of the mult16 miter (every node
+    row written to HBM: 8 bytes per node per 64-pattern word), drive and
+    output resident; plus the sweep's 64-word PE-class discovery end to end."""
+    import numpy as np
+    import torch
+
+    from paper_2512_06627_b200 import sim
+
+    x, _ = build_workload("mult16")
+    nn = 1 + x.num_pis + len(x.gates)
+    pw = sim.random_pi_words(x.num_pis, words, 1)
+    d_pi = torch.from_numpy(pw.view(np.int64)).to(f"cuda:{local}")
+    d_out = torch.empty((nn, words), dtype=torch.int64, device=f"cuda:{local}")
+    ds = sim.DeviceSim(x)
+    st = torch.cuda.current_stream(local)
+    for _ in range(3):
+        ds.run(d_pi.data_ptr(), words, d_out.data_ptr(), st.cuda_stream)
+    reps = 20
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        ds.run(d_pi.data_ptr(), words, d_out.data_ptr(), st.cuda_stream)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    ds.close()
+    peak = None
+    try:
+        peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except (OSError, ValueError, KeyError):
+        pass
+    written = nn * words * 8
+    gbs = written / (ms * 1e-3) / 1e9
+    sim.pe_classes(x, 64, 0, device=local)  # warm
+    walls = []
+    for s in range(5):
+        t = time.perf_counter()
+        n_cls = len(sim.pe_classes(x, 64, s, device=local))
+        walls.append(1e3 * (time.perf_counter() - t))
+    out = {"workload": f"random simulation of the 16x16 array-vs-Booth miter, {words} 64-bit words "
+                       "per node (sim.py:21-38), device-resident drive and node matrix",
+           "device_ms": ms, "gate_patterns_per_s": len(x.gates) * words * 64 / (ms * 1e-3),
+           "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",
+                        "frac": None if peak is None else gbs / peak,
+                        "algorithmic_bytes": written,
+                        "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"},
+           "pe_classes_64_words_e2e_ms": statistics.median(walls), "pe_classes": n_cls}
+    if cpu:  # the reference algorithm restated in numpy (oracle/), same drive
+        from oracle import oracle as O
+        pw64 = sim.random_pi_words(x.num_pis, 64, 0)
+        t = time.perf_counter()
+        O.pe_classes(O.simulate(x, pw64))
+        out["cpu_pe_classes_64_words_ms"] = 1e3 * (time.perf_counter() - t)
+        small = sim.random_pi_words(x.num_pis, 4096, 1)
+        t = time.perf_counter()
+        O.simulate(x, small)
+        out["cpu_simulate_4096_words_ms"] = 1e3 * (time.perf_counter() - t)
+    return out
+
+
+def measure_other_configs(local: int, cofactor="throughput") -> dict:
     """Short warm measurements of the other BASELINE.json configs on 1 GPU."""
     from paper_2512_06627_b200 import es
 
@@ -123,12 +184,12 @@ def measure_other_configs(local: int) -> dict:
         x, desc = build_workload(name)
         t = time.perf_counter()
         p = es.compile_program(x)
-        cold = es.run_exhaustive(p, engine="auto", device=local)
+        cold = es.run_exhaustive(p, engine="auto", device=local, cofactor=cofactor)
         cold_ms = 1e3 * (time.perf_counter() - t)
         devs, walls = [], []
         for _ in range(10):
             t = time.perf_counter()
-            r = es.es_check(_Sub(x), engine="auto", device=local)
+            r = es.es_check(_Sub(x), engine="auto", device=local, cofactor=cofactor)
             walls.append(1e3 * (time.perf_counter() - t))
             devs.append(r.stats["device_ms"])
         pats = (1 << x.num_pis) if r.verdict == "EQUIVALENT" else r.stats["patterns"]
@@ -501,7 +562,8 @@ def run_b200(args) -> None:
         if cpu is not None:
             line["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
         if world == 1 and not args.no_extras:
-            extras = measure_other_configs(local)
+            extras = measure_other_configs(local, args.cofactor)
+            extras["random_sim"] = measure_random_sim(local, cpu=not args.no_cpu_baseline)
             extras["cones"] = {"workload": "config 4: ~10k candidate-pair cones (14-24 PIs) of "
                                            "16x16 multiplier miters, one batched launch",
                                **measure_cones(5, 2)}

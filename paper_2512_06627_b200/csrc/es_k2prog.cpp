@@ -18,6 +18,7 @@
 // OUT records fold each copy's output into (first failing word, copy number)
 // in copy order, so the kernel's rare path can rebuild the minimum index.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <functional>
@@ -255,10 +256,12 @@ void build_k2prog_k(const Dag &dag, int k, K2Prog *kp) {
     kp->cof_pis = pis;
 }
 
-void build_k2prog_auto(const Dag &dag, K2Prog *kp, int min_words_log2, int max_slots) {
+void build_k2prog_auto(const Dag &dag, K2Prog *kp, int min_words_log2, int max_slots,
+                       double min_work) {
     if (const char *e = getenv("ES_K2_MAXSLOTS")) max_slots = atoi(e);
     const int P = dag.num_pis;
-    const int kmax = std::min(kK2MaxCofactorPis, P - 5 - min_words_log2);
+    int kmax = std::min(kK2MaxCofactorPis, P - 5 - min_words_log2);
+    if ((double)dag.is_xor.size() * std::ldexp(1.0, P) < min_work) kmax = 0;
     std::vector<int32_t> rank;
     if (kmax >= 1) rank = rank_cofactor_pis(dag, kmax);
     // gates per word of each depth (the interpreter's cost is ~linear in the

@@ -44,8 +44,10 @@ void build_k2prog(const Dag &dag, K2Prog *kp);
 // Pick the cofactor depth k (0..kK2MaxCofactorPis) that minimises the
 // shared-memory traffic per word, keeping >= 2^min_words_log2 kernel words
 // per job and <= max_slots slots (the interpreter's shared-memory limit at
-// one word per thread); then build that program.
-void build_k2prog_auto(const Dag &dag, K2Prog *kp, int min_words_log2 = 9, int max_slots = 176);
+// one word per thread); then build that program.  A sweep of fewer than
+// min_work gate-patterns is not worth the host time of the search (k = 0).
+void build_k2prog_auto(const Dag &dag, K2Prog *kp, int min_words_log2 = 9, int max_slots = 176,
+                       double min_work = 0.0);
 // Forced depth k (tests): the k word PIs of smallest fanout.
 void build_k2prog_k(const Dag &dag, int k, K2Prog *kp);
 // CPU model of the interpreter over FULL word indices [w0, w0+nw) (cofactor

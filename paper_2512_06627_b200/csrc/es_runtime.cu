@@ -893,7 +893,8 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
 // graph rebuild, mapping, PTX emission and the JIT-cache lookup.
 struct MappedProg {
     Dag dag;
-    LutNet net;                      // no cofactors
+    LutNet net;                      // no cofactors (mapped on demand: variant(0))
+    bool net_ready = false;
     int G = 0;
     // cofactor variants k = 1..kMaxCofactorPis, mapped on demand
     std::vector<int32_t> cof_rank;   // the kMaxCofactorPis cheapest word PIs, by fanout
@@ -901,9 +902,15 @@ struct MappedProg {
     // K1 kernels per (k, skeleton): 128/256/512, K1U, K1T
     JitKernel *jk[kMaxCofactorPis + 1][5] = {};
     int runs = 0;                    // K1 runs so far (the reuse estimate of the auto policy)
+    std::shared_ptr<K2Prog> k2;      // interpreter program (its own cofactor depth), on demand
+    bool k2_searched = false;        // built with the cofactor-depth search
+    int k2_runs = 0;
     std::mutex mu;
     const LutNet &variant(int k) {   // caller holds mu
-        if (k == 0) return net;
+        if (k == 0) {
+            if (!net_ready) { map_luts(dag, &net); net_ready = true; }
+            return net;
+        }
         if (!cof[k]) {
             if (cof_rank.empty()) cof_rank = rank_cofactor_pis(dag, kMaxCofactorPis);
             std::vector<int32_t> pis(cof_rank.begin(), cof_rank.begin() + std::min<size_t>(k, cof_rank.size()));
@@ -943,7 +950,6 @@ static int get_mapped(const es_prog &p, std::shared_ptr<MappedProg> *out) {
     int rc = build_dag(p, &dag, &err);
     if (rc != ES_OK) { set_error(err); return rc; }
     auto mp = std::make_shared<MappedProg>();
-    map_luts(dag, &mp->net);
     mp->dag = std::move(dag);
     for (int i = 0; i < p.num_instrs; ++i) mp->G += (p.op[i] == ES_OP_AND || p.op[i] == ES_OP_XOR);
     std::lock_guard<std::mutex> lk(g_mapped_mu);
@@ -1002,9 +1008,10 @@ static int choose_cofactors(MappedProg &mp, const es_run_opts &o, int sms) {
     const int kmax = std::max(0, std::min(kMaxCofactorPis, P - 5 - 14));
     if (kmax == 0) return 0;
     const bool tput = o.cofactor_pis == ES_COFACTOR_THROUGHPUT;
-    const double sweep0 = est_sweep_ms(mp.net, P, sms);
+    const LutNet &net0 = mp.variant(0);
+    const double sweep0 = est_sweep_ms(net0, P, sms);
     // latency mode: a short sweep is JIT-bound; don't even map the variants
-    if (!tput && sweep0 * (1 + mp.runs) < 0.1 * est_jit_ms(mp.net)) return 0;
+    if (!tput && sweep0 * (1 + mp.runs) < 0.1 * est_jit_ms(net0)) return 0;
     const double reuse = 1.0 + mp.runs;  // doubling rule: expect as many more runs as so far
     int best = 0;
     double best_cost = 1e300;
@@ -1038,9 +1045,7 @@ int run_one(const es_prog *prog, const es_run_opts *opts, es_result *out) {
     std::shared_ptr<MappedProg> mp;
     rc = get_mapped(*prog, &mp);
     if (rc != ES_OK) return rc;
-    const LutNet &net = mp->net;
     const int G = mp->G;
-    out->num_luts = (int)net.luts.size();
     out->compile_ms = now_ms() - t0;
     Ctx *c = nullptr;
     rc = get_ctx(o.device, &c);
@@ -1053,7 +1058,30 @@ int run_one(const es_prog *prog, const es_run_opts *opts, es_result *out) {
     }
     if (engine == ES_ENGINE_INTERP) {
         std::vector<int> act{0};
-        rc = run_k2(1, prog, act, o, c, deadline, out);
+        const K2Prog *kp;
+        std::shared_ptr<K2Prog> hold;  // a concurrent tier-up may replace mp->k2
+        {
+            std::lock_guard<std::mutex> lk(mp->mu);
+            const double tc = now_ms();
+            // one program: search cofactor depths when the sweep (~4 ms of
+            // interpreter time and up) outweighs the host search, when the
+            // caller asks for throughput, or once re-runs have paid for it
+            const bool tput = o.cofactor_pis == ES_COFACTOR_THROUGHPUT;
+            const double work = (double)G * std::ldexp(1.0, prog->num_pis);
+            const bool tier_up = mp->k2 && !mp->k2_searched && (tput || work * (1 + mp->k2_runs) >= 2e11);
+            if (!mp->k2 || tier_up) {
+                const bool search = tput || work * (1 + mp->k2_runs) >= 2e11;
+                auto fresh = std::make_shared<K2Prog>();
+                build_k2prog_auto(mp->dag, fresh.get(), 9, 176, search ? 0.0 : 1e300);
+                mp->k2 = fresh;
+                mp->k2_searched = search;
+            }
+            mp->k2_runs++;
+            hold = mp->k2;
+            kp = hold.get();
+            out->compile_ms += now_ms() - tc;
+        }
+        rc = run_k2(1, prog, act, o, c, deadline, out, &kp);
     } else {
         std::lock_guard<std::mutex> lk(mp->mu);
         const double tc = now_ms();
