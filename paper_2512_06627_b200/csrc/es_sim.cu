@@ -25,6 +25,7 @@
 // exactly the reference's.
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <queue>
