@@ -42,6 +42,10 @@ extern "C" {
 #define ES_E_BAD_ARG (-4)         /* e.g. workers < 1 (es.py:260-261) */
 #define ES_E_NO_DEVICE (-5)       /* no CUDA device visible */
 #define ES_E_WITNESS (-6)         /* witness failed re-check (es.py:360-361 AssertionError) */
+#define ES_E_AIGER (-7)           /* AigerError: cyclic AND definitions (aiger.py:81-90) */
+#define ES_E_AIGER_HEADER (-8)    /* MalformedHeader (aiger.py:17, 29-41, 114-189) */
+#define ES_E_AIGER_LATCHES (-9)   /* LatchesUnsupported (aiger.py:21, 52-53) */
+#define ES_E_AIGER_DANGLING (-10) /* DanglingLiteral (aiger.py:25, 86, 97, 110, 190) */
 
 /* EsResult.verdict (es.py:34-36) */
 #define ES_EXHAUSTED_ZERO 0
@@ -244,6 +248,28 @@ int32_t es_sim_levels(int32_t num_pis, int32_t num_gates, const uint8_t *kind, c
 int32_t es_sim_classes(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
                        const uint32_t *in1, const uint64_t *pi_words, int64_t words, int32_t device,
                        int32_t *class_id, uint8_t *polarity, int32_t *n_classes, double *device_ms);
+
+/*
+ * AIGER ingest.  es_aiger_parse = parse_aiger
+ * (aiger.py:44-194) of ASCII "aag" or binary "aig" bytes, optionally followed
+ * by detect_xors (transform.py:79-119) -- the CLI's _load_circuit
+ * (cli.py:63-76).  The circuit is built with the reference's structural
+ * hashing, so it is gate-for-gate the reference's Xag; read it back with
+ * es_xag_size / es_xag_read (packed literals node*2+neg, kind 0 AND 1 XOR).
+ */
+typedef struct es_xag es_xag;
+int32_t es_aiger_parse(const uint8_t *data, int64_t len, int32_t detect_xors, es_xag **out);
+int32_t es_detect_xors(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+                       const uint32_t *in1, int32_t num_outputs, const uint32_t *out_lits,
+                       es_xag **out);
+int32_t es_xag_size(const es_xag *x, int32_t *num_pis, int32_t *num_gates, int32_t *num_outputs);
+int32_t es_xag_read(const es_xag *x, uint8_t *kind, uint32_t *in0, uint32_t *in1, uint32_t *out_lits);
+void es_xag_free(es_xag *x);
+/* write_aiger (aiger.py:197-225): ASCII AIGER, XOR as three ANDs; returns
+ * the byte count (buf may be NULL to size it). */
+int64_t es_aiger_write(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+                       const uint32_t *in1, int32_t num_outputs, const uint32_t *out_lits, char *buf,
+                       int64_t cap);
 
 /* Engine-internal views for tests and profiling. */
 /* LUT-3 mapping statistics of a program: LOP3s per word, schedule peak live. */

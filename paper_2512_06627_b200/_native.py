@@ -22,6 +22,7 @@ ES_E_BAD_PROGRAM = -3
 ES_E_BAD_ARG = -4
 ES_E_NO_DEVICE = -5
 ES_E_WITNESS = -6
+ES_E_AIGER, ES_E_AIGER_HEADER, ES_E_AIGER_LATCHES, ES_E_AIGER_DANGLING = -7, -8, -9, -10
 
 ENGINE_AUTO, ENGINE_JIT, ENGINE_INTERP = 0, 1, 2
 # es_run_opts.cofactor_pis (include/es_b200.h)
@@ -38,6 +39,8 @@ EXPORTS = ("es_compile", "es_run", "es_run_batch", "es_session_open", "es_sessio
            "es_map_stats_k", "es_map_pipes_k", "es_map_eval_k", "es_emit_ptx_k", "es_jit_check_k",
            "es_k2_eval_k", "es_k2_cofactor_pis", "es_batch_prepare",
            "es_sim", "es_sim_device", "es_sim_prog_free", "es_sim_classes", "es_sim_levels",
+           "es_aiger_parse", "es_detect_xors", "es_xag_size", "es_xag_read", "es_xag_free",
+           "es_aiger_write",
            "es_last_error", "es_version", "es_shutdown")
 
 _P = ctypes.c_void_p
@@ -162,6 +165,18 @@ def lib():
         L.es_sim_classes.restype = _I
         L.es_sim_levels.argtypes = [_I, _I, _P, _P, _P]
         L.es_sim_levels.restype = _I
+        L.es_aiger_parse.argtypes = [_P, ctypes.c_int64, _I, ctypes.POINTER(_P)]
+        L.es_aiger_parse.restype = _I
+        L.es_detect_xors.argtypes = [_I, _I, _P, _P, _P, _I, _P, ctypes.POINTER(_P)]
+        L.es_detect_xors.restype = _I
+        L.es_xag_size.argtypes = [_P, _P, _P, _P]
+        L.es_xag_size.restype = _I
+        L.es_xag_read.argtypes = [_P, _P, _P, _P, _P]
+        L.es_xag_read.restype = _I
+        L.es_xag_free.argtypes = [_P]
+        L.es_xag_free.restype = None
+        L.es_aiger_write.argtypes = [_I, _I, _P, _P, _P, _I, _P, ctypes.c_char_p, ctypes.c_int64]
+        L.es_aiger_write.restype = ctypes.c_int64
         L.es_batch_prepare.argtypes = [_P, ctypes.c_int32]
         L.es_batch_prepare.restype = ctypes.c_int32
         L.es_batch_size.argtypes = [_P]

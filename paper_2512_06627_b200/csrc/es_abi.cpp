@@ -10,6 +10,7 @@
 #include "es_extract.h"
 #include "es_jit.h"
 #include "es_k2prog.h"
+#include "es_xag.h"
 
 namespace es {
 
@@ -37,6 +38,12 @@ int sim_run_device(int32_t num_pis, int32_t num_gates, const uint8_t *kind, cons
                    const uint32_t *in1, const uint64_t *d_pi_words, int64_t words, void *stream,
                    uint64_t *d_node_words, void **prog_cache);
 void sim_prog_free(void *prog_cache);
+int aiger_parse(const uint8_t *data, int64_t len, int32_t xors, XagC **out);
+int xag_detect_xors(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+                    const uint32_t *in1, int32_t num_outputs, const uint32_t *out_lits, XagC **out);
+int64_t aiger_write(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+                    const uint32_t *in1, int32_t num_outputs, const uint32_t *out_lits, char *buf,
+                    int64_t cap);
 int sim_levels(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
               const uint32_t *in1);
 int sim_classes(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
@@ -306,6 +313,61 @@ int32_t es_sim_classes(int32_t num_pis, int32_t num_gates, const uint8_t *kind, 
     }
     return sim_classes(num_pis, num_gates, kind, in0, in1, pi_words, words, device, class_id, polarity,
                        n_classes, device_ms);
+}
+
+int32_t es_aiger_parse(const uint8_t *data, int64_t len, int32_t detect_xors, es_xag **out) {
+    if ((!data && len > 0) || len < 0 || !out) { set_error("bad argument"); return ES_E_BAD_ARG; }
+    XagC *x = nullptr;
+    static const uint8_t kEmpty = 0;
+    const int rc = aiger_parse(data ? data : &kEmpty, len, detect_xors, &x);
+    *out = (es_xag *)x;
+    return rc;
+}
+
+int32_t es_detect_xors(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+                       const uint32_t *in1, int32_t num_outputs, const uint32_t *out_lits,
+                       es_xag **out) {
+    if (!out || num_pis < 0 || num_gates < 0 || num_outputs < 0 ||
+        (num_gates > 0 && (!kind || !in0 || !in1)) || (num_outputs > 0 && !out_lits)) {
+        set_error("bad argument");
+        return ES_E_BAD_ARG;
+    }
+    XagC *x = nullptr;
+    const int rc = xag_detect_xors(num_pis, num_gates, kind, in0, in1, num_outputs, out_lits, &x);
+    *out = (es_xag *)x;
+    return rc;
+}
+
+int32_t es_xag_size(const es_xag *xp, int32_t *num_pis, int32_t *num_gates, int32_t *num_outputs) {
+    const XagC *x = (const XagC *)xp;
+    if (!x) { set_error("null xag"); return ES_E_BAD_ARG; }
+    if (num_pis) *num_pis = x->num_pis;
+    if (num_gates) *num_gates = (int32_t)x->kind.size();
+    if (num_outputs) *num_outputs = (int32_t)x->outs.size();
+    return ES_OK;
+}
+
+int32_t es_xag_read(const es_xag *xp, uint8_t *kind, uint32_t *in0, uint32_t *in1, uint32_t *out_lits) {
+    const XagC *x = (const XagC *)xp;
+    if (!x) { set_error("null xag"); return ES_E_BAD_ARG; }
+    if (kind) std::memcpy(kind, x->kind.data(), x->kind.size());
+    if (in0) std::memcpy(in0, x->in0.data(), 4 * x->in0.size());
+    if (in1) std::memcpy(in1, x->in1.data(), 4 * x->in1.size());
+    if (out_lits) std::memcpy(out_lits, x->outs.data(), 4 * x->outs.size());
+    return ES_OK;
+}
+
+void es_xag_free(es_xag *xp) { delete (XagC *)xp; }
+
+int64_t es_aiger_write(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+                       const uint32_t *in1, int32_t num_outputs, const uint32_t *out_lits, char *buf,
+                       int64_t cap) {
+    if (num_pis < 0 || num_gates < 0 || num_outputs < 0 || (num_gates > 0 && (!kind || !in0 || !in1)) ||
+        (num_outputs > 0 && !out_lits)) {
+        set_error("bad argument");
+        return ES_E_BAD_ARG;
+    }
+    return aiger_write(num_pis, num_gates, kind, in0, in1, num_outputs, out_lits, buf, cap);
 }
 
 int32_t es_alu_peak(int32_t device, double *lane_ops_per_s, double *ms) {

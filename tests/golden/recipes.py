@@ -154,3 +154,84 @@ def build_sim(spec):
     if spec["kind"] == "mult":
         return M.gen_multiplier_miter(spec["width"], spec["a"], spec["b"])
     return M.gen_adder_miter(spec["width"])
+
+
+# --- AIGER population (make_golden_aiger.py, tests/test_aiger.py) -------------
+
+def aiger_population() -> list[dict]:
+    specs = []
+    rng = random.Random(91)
+    for k in range(30):
+        specs.append({"kind": "random", "n_pis": rng.randint(1, 16), "n_gates": rng.randint(0, 400),
+                      "seed": 4000 + k, "shuffle": k % 3 == 0})
+    for w, a, b in [(3, "array", "diagonal"), (4, "array", "booth"), (6, "array", "wallace"),
+                    (8, "array", "booth"), (12, "array", "wallace"), (16, "array", "booth")]:
+        specs.append({"kind": "mult", "width": w, "a": a, "b": b, "shuffle": w == 6})
+    specs.append({"kind": "adder", "width": 8, "shuffle": True})
+    return specs
+
+
+def build_aiger_circuit(spec):
+    return build_sim(spec)
+
+
+def to_binary_aiger(ascii_bytes: bytes) -> bytes:
+    """Binary AIGER of an ASCII file whose ANDs are numbered consecutively
+    after the inputs with lhs > rhs0 >= rhs1 (write_aiger's form)."""
+    lines = ascii_bytes.decode().strip().split("\n")
+    m, i, l, o, a = (int(t) for t in lines[0].split()[1:6])
+    outs = lines[1 + i:1 + i + o]
+    ands = [tuple(int(t) for t in ln.split()) for ln in lines[1 + i + o:1 + i + o + a]]
+    out = bytearray(f"aig {m} {i} {l} {o} {a}\n".encode())
+    for ln in outs:
+        out += (ln + "\n").encode()
+
+    def varint(x):
+        while True:
+            byte = x & 0x7F
+            x >>= 7
+            if x:
+                out.append(byte | 0x80)
+            else:
+                out.append(byte)
+                return
+
+    for lhs, r0, r1 in ands:
+        varint(lhs - r0)
+        varint(r0 - r1)
+    return bytes(out)
+
+
+def shuffled_ascii(ascii_bytes: bytes, seed: int) -> bytes:
+    """Same ASCII file with the AND lines in a seeded random order (the
+    reader must DFS out-of-order definitions, aiger.py:63-92)."""
+    lines = ascii_bytes.decode().strip().split("\n")
+    i, o, a = (int(t) for t in lines[0].split()[2:3] + lines[0].split()[4:6])
+    head, body = lines[:1 + i + o], lines[1 + i + o:]
+    random.Random(seed).shuffle(body)
+    return ("\n".join(head + body) + "\n").encode()
+
+
+AIGER_ERROR_CASES = [
+    b"",
+    b"aag 1 1 0 1 0",
+    b"xyz 1 1 0 1 0\n2\n2\n",
+    b"aag 1 1 0\n",
+    b"aag a 1 0 1 0\n2\n2\n",
+    b"aag 3 1 1 1 1\n2\n4 2\n6\n6 2 4\n",
+    b"aag 1 2 0 1 0\n2\n4\n2\n",
+    b"aag 2 1 0 1 1\n2\n4\n4 2 8\n",
+    b"aag 3 1 0 1 2\n2\n4\n4 6 2\n6 4 2\n",
+    b"aag 2 1 0 1 1\n2\n4\n4 2\n",
+    b"aag 2 1 0 1 1\n3\n4\n4 2 2\n",
+    b"aag 2 1 0 1 1\n2\n9\n4 2 2\n",
+    b"aag 2 1 0 1 1 1\n2\n4\n4 2 2\n",
+    b"aag 2 1 0 1 1\n2\n4\n",
+    b"aig 2 1 0 1 1\n4\n",
+    b"aig 2 1 0 1 1\n4\n\x05\x00",
+    b"aag 2 1 0 1 1\n2\n4\n2 2 2\n",
+    b"aag 2 1 0 1 1\n2\n4\n4 2 x\n",
+    b"aag 3 1 0 1 1\n2\n6\n4 2 2\n",
+    b"aag 1 1 0 1 0\n2\n1\n",
+    b"aag 1 1 0 1 0 0 0\n2\n3\n",
+]
