@@ -28,6 +28,7 @@ import argparse
 import json
 import os
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -347,9 +348,37 @@ def run_reference(args) -> None:
 
 # --- the B200 arm ----------------------------------------------------------
 
+def disk_cache_ttv(config: str, cofactor) -> dict:
+    """Cold time-to-verdict in a fresh process with the on-disk cubin cache
+    (es_jit.cpp) populated by a previous process: compile + map + load + sweep,
+    no ptxas.  Two child processes on a private cache directory."""
+    import tempfile
+    code = ("import sys, time, json; sys.path.insert(0, %r)\n"
+            "from bench import build_workload\n"
+            "from paper_2512_06627_b200 import es\n"
+            "x, _ = build_workload(%r)\n"
+            "t = time.perf_counter(); r = es.run_exhaustive(es.compile_program(x), engine='jit', cofactor=%r)\n"
+            "print(json.dumps({'ms': 1e3 * (time.perf_counter() - t), 'jit_ms': r.stats['jit_ms']}))\n"
+            % (ROOT, config, cofactor))
+    out = {}
+    with tempfile.TemporaryDirectory() as d:
+        env = dict(os.environ, ES_JIT_CACHE="1", ES_JIT_CACHE_DIR=d)
+        for tag in ("populate", "warm_disk"):
+            r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                               timeout=600)
+            if r.returncode != 0:
+                return {"error": r.stderr[-300:]}
+            out[tag] = json.loads(r.stdout.strip().splitlines()[-1])
+    return {"cold_ms_disk_cache": out["warm_disk"]["ms"], "jit_ms_disk_cache": out["warm_disk"]["jit_ms"],
+            "cold_ms_first_process": out["populate"]["ms"]}
+
+
 def run_b200(args) -> None:
     import torch
     import torch.distributed as dist
+
+    # cold numbers below are true cold: no on-disk cubin cache in this process
+    os.environ["ES_JIT_CACHE"] = "0"
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -555,13 +584,19 @@ def run_b200(args) -> None:
                                 f"cold_ms_{args.cofactor}": cold_t_ms,
                                 f"jit_ms_{args.cofactor}": cold_t.stats.get("jit_ms"),
                                 f"device_ms_{args.cofactor}": cold_t.stats.get("device_ms"),
-                                "warm_device_ms": total_s * 1e3 / args.steps},
+                                "warm_device_ms": total_s * 1e3 / args.steps,
+                                "note": "cold = first call in a process, JIT included, on-disk "
+                                        "cubin cache off; disk_cache = a later process whose "
+                                        "cubins were compiled by an earlier one (the reference's "
+                                        "numba cache=True analogue)"},
             "gpu_launches": args.steps * (1 if collective == "p2p" else S) * world,
             "clocks": clk.summary(),
         }
         if cpu is not None:
             line["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
         if world == 1 and not args.no_extras:
+            for mode in ("auto", args.cofactor):
+                line["time_to_verdict"][f"disk_cache_{mode}"] = disk_cache_ttv(args.config, mode)
             extras = measure_other_configs(local, args.cofactor)
             extras["random_sim"] = measure_random_sim(local, cpu=not args.no_cpu_baseline)
             extras["cones"] = {"workload": "config 4: ~10k candidate-pair cones (14-24 PIs) of "

@@ -4,7 +4,11 @@
 // GPU needed), load it with cudaLibraryLoadData.  Modules are cached by a
 // hash of the final PTX, so a program is compiled once per process.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+
+#include <sys/stat.h>
+#include <unistd.h>
 #include <mutex>
 #include <sstream>
 #include <string>
@@ -189,6 +193,88 @@ void parse_ptxas_info(const std::string &info, int *regs, int *spill_bytes) {
 namespace {
 std::mutex g_jit_mu;
 std::unordered_map<uint64_t, JitKernel *> g_cache;
+
+// On-disk cubin cache (the analogue of the reference's numba cache=True,
+// es.py:175): a program compiled by one process is loaded by the next
+// without running ptxas.  ES_JIT_CACHE=0 disables it; ES_JIT_CACHE_DIR
+// overrides the directory (default $HOME/.cache/es_b200).  Entries are keyed
+// by a hash of the final PTX and the PTX compiler version, and verified by a
+// second hash and the PTX length on load.
+std::string disk_cache_dir() {
+    const char *off = getenv("ES_JIT_CACHE");
+    if (off && std::string(off) == "0") return "";
+    if (const char *d = getenv("ES_JIT_CACHE_DIR")) return d;
+    const char *home = getenv("HOME");
+    return home ? std::string(home) + "/.cache/es_b200" : "";
+}
+
+uint64_t second_hash(const std::string &s) {
+    uint64_t h = 0x9e3779b97f4a7c15ull;
+    for (unsigned char c : s) h = (h ^ c) * 0x100000001b3ull + (h >> 27);
+    return h;
+}
+
+std::string ptxc_version() {
+    unsigned major = 0, minor = 0;
+    nvPTXCompilerGetVersion(&major, &minor);
+    return std::to_string(major) + "." + std::to_string(minor);
+}
+
+std::string entry_path(const std::string &dir, uint64_t key) {
+    char name[64];
+    snprintf(name, sizeof name, "/%016llx.esbin", (unsigned long long)key);
+    return dir + name;
+}
+
+struct DiskHeader {
+    char magic[8];
+    uint64_t h2;
+    uint64_t ptx_len;
+    uint32_t info_len;
+    uint32_t cubin_len;
+};
+
+bool disk_load(const std::string &dir, uint64_t key, const std::string &ptx, std::vector<char> *cubin,
+               std::string *info) {
+    if (dir.empty()) return false;
+    FILE *f = fopen(entry_path(dir, key).c_str(), "rb");
+    if (!f) return false;
+    DiskHeader h{};
+    bool ok = fread(&h, sizeof h, 1, f) == 1 && memcmp(h.magic, "ESBIN01", 8) == 0 &&
+              h.h2 == second_hash(ptx) && h.ptx_len == ptx.size() && h.cubin_len > 0 &&
+              h.cubin_len < (1u << 30) && h.info_len < (1u << 20);
+    if (ok) {
+        info->resize(h.info_len);
+        cubin->resize(h.cubin_len);
+        ok = (h.info_len == 0 || fread(&(*info)[0], 1, h.info_len, f) == h.info_len) &&
+             fread(cubin->data(), 1, h.cubin_len, f) == h.cubin_len;
+    }
+    fclose(f);
+    return ok;
+}
+
+void disk_store(const std::string &dir, uint64_t key, const std::string &ptx, const std::vector<char> &cubin,
+                const std::string &info) {
+    if (dir.empty()) return;
+    std::string cmd = dir;  // mkdir -p
+    for (size_t i = 1; i <= cmd.size(); ++i)
+        if (i == cmd.size() || cmd[i] == '/') mkdir(cmd.substr(0, i).c_str(), 0755);
+    const std::string path = entry_path(dir, key);
+    const std::string tmp = path + ".tmp" + std::to_string((unsigned long long)getpid());
+    FILE *f = fopen(tmp.c_str(), "wb");
+    if (!f) return;
+    DiskHeader h{};
+    memcpy(h.magic, "ESBIN01", 8);
+    h.h2 = second_hash(ptx);
+    h.ptx_len = ptx.size();
+    h.info_len = (uint32_t)info.size();
+    h.cubin_len = (uint32_t)cubin.size();
+    const bool ok = fwrite(&h, sizeof h, 1, f) == 1 && fwrite(info.data(), 1, info.size(), f) == info.size() &&
+                    fwrite(cubin.data(), 1, cubin.size(), f) == cubin.size();
+    fclose(f);
+    if (ok) rename(tmp.c_str(), path.c_str());  // atomic publish
+    else remove(tmp.c_str());
+}
 }  // namespace
 
 int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std::string *err) {
@@ -202,8 +288,14 @@ int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std
     auto t0 = now_ms();
     std::vector<char> cubin;
     std::string info;
-    int rc = ptx_to_cubin(ptx, &cubin, &info, err);
-    if (rc != ES_OK) return rc;
+    static const std::string version = ptxc_version();
+    const uint64_t dkey = key ^ fnv1a(version) * 31u;
+    const std::string dir = disk_cache_dir();
+    if (!disk_load(dir, dkey, ptx, &cubin, &info)) {
+        int rc = ptx_to_cubin(ptx, &cubin, &info, err);
+        if (rc != ES_OK) return rc;
+        disk_store(dir, dkey, ptx, cubin, info);
+    }
     JitKernel *k = new JitKernel();
     k->threads = threads;
     k->block = threads == kK1TThreads ? 128 : threads;
