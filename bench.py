@@ -357,6 +357,8 @@ def disk_cache_ttv(config: str, cofactor) -> dict:
             "from bench import build_workload\n"
             "from paper_2512_06627_b200 import es\n"
             "x, _ = build_workload(%r)\n"
+            "from paper_2512_06627_b200 import miter as M\n"
+            "es.run_exhaustive(es.compile_program(M.gen_adder_miter(4)), engine='interp')  # CUDA context\n"
             "t = time.perf_counter(); r = es.run_exhaustive(es.compile_program(x), engine='jit', cofactor=%r)\n"
             "print(json.dumps({'ms': 1e3 * (time.perf_counter() - t), 'jit_ms': r.stats['jit_ms']}))\n"
             % (ROOT, config, cofactor))
