@@ -138,7 +138,7 @@ int extract_compile(int32_t num_pis, int32_t num_gates, const uint8_t *kind, con
         if ((int)(in0[i] >> 1) >= v || (int)(in1[i] >> 1) >= v) { *err = "parent XAG not topological"; return ES_E_BAD_PROGRAM; }
     }
     for (int i = 0; i < n_pairs; ++i)
-        if (a[i] <= 0 || a[i] >= nn || b[i] <= 0 || b[i] >= nn) { *err = "pair node out of range"; return ES_E_BAD_ARG; }
+        if (a[i] < 0 || a[i] >= nn || b[i] < 0 || b[i] >= nn) { *err = "pair node out of range"; return ES_E_BAD_ARG; }
     out->assign(n_pairs, SubMiterC());
     std::atomic<int> next{0};
     std::atomic<int> bad{0};

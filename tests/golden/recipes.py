@@ -235,3 +235,44 @@ AIGER_ERROR_CASES = [
     b"aag 1 1 0 1 0\n2\n1\n",
     b"aag 1 1 0 1 0 0 0\n2\n3\n",
 ]
+
+
+# --- sweep population (make_golden_sweep.py, tests/test_sweep_gpu.py) ---------
+
+def sweep_population() -> list[dict]:
+    specs = []
+    for w in (4, 6, 8):
+        specs.append({"kind": "adder", "width": w})
+    for w, a, b in [(4, "array", "diagonal"), (6, "array", "wallace"), (6, "array", "booth"),
+                    (8, "array", "diagonal"), (8, "array", "booth"), (10, "array", "wallace")]:
+        specs.append({"kind": "mult", "width": w, "a": a, "b": b})
+        for s in range(3):
+            specs.append({"kind": "mult", "width": w, "a": a, "b": b, "mutate": s})
+    # deep single-gate faults the 4,096 random patterns miss: refuted by ES
+    for flip in (1108, 1210, 941):
+        specs.append({"kind": "mult", "width": 12, "a": "array", "b": "wallace", "flip": flip})
+    specs.append({"kind": "mult", "width": 12, "a": "array", "b": "wallace"})
+    # a single failing pattern (random simulation cannot see it): the final
+    # ES obligation must find exactly that witness
+    for w, a, b, needle in [(8, "array", "booth", 0xBEEF), (10, "array", "wallace", 0x5A5A5),
+                            (12, "array", "wallace", 0xC0FFEE)]:
+        specs.append({"kind": "mult", "width": w, "a": a, "b": b, "needle": needle})
+    return specs
+
+
+def build_sweep_circuit(spec):
+    x = build_sim(spec)
+    if "mutate" in spec:
+        x = M.mutate(x, spec["mutate"], check_pis=0)
+    if "flip" in spec:
+        x = M.flip_gate(x, spec["flip"])
+    if "needle" in spec:  # OR a single minterm into the output: one failing pattern
+        from paper_2512_06627_b200.xag import XagBuilder
+        bld = XagBuilder(x.num_pis)
+        (o,) = M.copy_into(bld, x)
+        t = None
+        for i in range(x.num_pis):
+            lit = bld.pi(i + 1) if (spec["needle"] >> i) & 1 else ~bld.pi(i + 1)
+            t = lit if t is None else bld.add_and(t, lit)
+        x = bld.finish([bld.add_or(o, t)])
+    return x
