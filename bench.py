@@ -176,6 +176,29 @@ def measure_random_sim(local: int, words: int = 1 << 16, cpu: bool = True) -> di
     return out
 
 
+def measure_sweep(local: int) -> dict:
+    """the whole sweep with the ES engine (sweep.py:292-409)
+    on the config-2/3 multiplier miters -- K3 simulation and classes, C++
+    extraction, batched K2 / parallel-JIT K1 pair checks, final obligation.
+    Cold = first sweep of the miter in this process (JIT included)."""
+    from paper_2512_06627_b200 import miter as M
+    from paper_2512_06627_b200.sweep import SweepConfig, sweep
+
+    out = {}
+    for name, (w, a, b) in {"mult12": (12, "array", "wallace"), "mult16": (16, "array", "booth")}.items():
+        x = M.gen_multiplier_miter(w, a, b)
+        t = time.perf_counter()
+        r = sweep(x, SweepConfig(device=local))
+        cold = 1e3 * (time.perf_counter() - t)
+        t = time.perf_counter()
+        sweep(x, SweepConfig(device=local))
+        warm = 1e3 * (time.perf_counter() - t)
+        out[name] = {"verdict": r.verdict, "cold_ms": cold, "warm_ms": warm,
+                     "pairs_checked": r.stats["engine_calls"], "merges": r.stats["merges"],
+                     "reference_sweep_s_1_thread_build_container": {"mult12": 6.78, "mult16": 376.89}[name]}
+    return out
+
+
 def measure_other_configs(local: int, cofactor="throughput") -> dict:
     """Short warm measurements of the other BASELINE.json configs on 1 GPU."""
     from paper_2512_06627_b200 import es
@@ -601,6 +624,7 @@ def run_b200(args) -> None:
                 line["time_to_verdict"][f"disk_cache_{mode}"] = disk_cache_ttv(args.config, mode)
             extras = measure_other_configs(local, args.cofactor)
             extras["random_sim"] = measure_random_sim(local, cpu=not args.no_cpu_baseline)
+            extras["sweep_es"] = measure_sweep(local)
             extras["cones"] = {"workload": "config 4: ~10k candidate-pair cones (14-24 PIs) of "
                                            "16x16 multiplier miters, one batched launch",
                                **measure_cones(5, 2)}

@@ -221,10 +221,13 @@ class NativeBatch:
         N.check(N.lib().es_batch_select(self._h, len(idx), idx.ctypes.data))
         self.origins = [self.origins[i] for i in idx]
 
-    def run_arrays(self, budget: float | None = None, cancel=None, device: int = 0) -> np.ndarray:
+    def run_arrays(self, budget: float | None = None, cancel=None, device: int = 0,
+                   engine: str = "auto") -> np.ndarray:
         """Batched run_exhaustive over every sub-miter (witnesses re-checked on
         the sub-miter by the library); the raw es_result records as a numpy
-        structured array (fields of include/es_b200.h es_result)."""
+        structured array (fields of include/es_b200.h es_result).  engine
+        "auto": jobs of >= 2e12 gate-patterns get their own K1 kernel (JIT on
+        parallel host threads), the rest share one K2 launch; "interp": all K2."""
         from .es import _CancelWatcher, _opts
 
         n = len(self)
@@ -235,15 +238,15 @@ class NativeBatch:
                 outs[i].reason = 1
             return np.ctypeslib.as_array(outs)
         with _CancelWatcher(cancel) as cw:
-            opts = _opts(device, "interp", budget, cw.address, 20.0, 0)
+            opts = _opts(device, engine, budget, cw.address, 20.0, 0)
             N.check(N.lib().es_batch_run(self._h, ctypes.byref(opts), outs))
         return np.ctypeslib.as_array(outs)
 
-    def run(self, budget: float | None = None, cancel=None, device: int = 0):
+    def run(self, budget: float | None = None, cancel=None, device: int = 0, engine: str = "auto"):
         """As run_arrays, as a list of EsResult (None for ineligible jobs)."""
         from .es import _to_esresult
 
-        outs = self.run_arrays(budget, cancel, device)
+        outs = self.run_arrays(budget, cancel, device, engine)
         pis = self.table()["num_pis"]
         res = []
         for i in range(len(outs)):

@@ -1,5 +1,6 @@
 // es_abi.cpp -- extern "C" entry points declared in include/es_b200.h.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -18,6 +19,7 @@ thread_local std::string t_err;
 void set_error(const std::string &m) { t_err = m; }
 
 int run_one(const es_prog *prog, const es_run_opts *opts, es_result *out);
+int run_batch_jit(int n_jobs, const es_prog *progs, const es_run_opts *opts, es_result *outs);
 int run_batch(int n_jobs, const es_prog *progs, const es_run_opts *opts, es_result *outs,
               const K2Prog *const *prebuilt = nullptr);
 int session_open(const es_prog *prog, const es_run_opts *opts, void **out);
@@ -466,26 +468,52 @@ int32_t es_batch_run(es_batch *bp, const es_run_opts *opts, es_result *outs) {
     Batch *bt = (Batch *)bp;
     if (!bt || !outs) { set_error("bad argument"); return ES_E_BAD_ARG; }
     const int n = (int)bt->subs.size();
-    std::vector<es_prog> progs;
+    // jobs worth a JIT kernel of their own (>= kBatchJitWork gate-patterns,
+    // ~20 ms and up in the interpreter) run through K1, the rest through one
+    // batched K2 launch
+    constexpr double kBatchJitWork = 2e12;
+    std::vector<es_prog> progs, big_progs;
     std::vector<const K2Prog *> kps;
-    std::vector<int> where;
+    std::vector<int> where, big_where;
+    bool force_interp = opts && opts->engine == ES_ENGINE_INTERP;
     for (int i = 0; i < n; ++i) {
         std::memset(&outs[i], 0, sizeof(es_result));
         if (bt->subs[i].too_many_inputs) { outs[i].verdict = ES_BUDGET_EXCEEDED; outs[i].reason = -1; continue; }
-        progs.push_back(bt->subs[i].view());
+        const es_prog v = bt->subs[i].view();
+        int G = 0;
+        for (int q = 0; q < v.num_instrs; ++q) G += v.op[q] == ES_OP_AND || v.op[q] == ES_OP_XOR;
+        if (!force_interp && (double)G * std::ldexp(1.0, v.num_pis) >= kBatchJitWork) {
+            big_progs.push_back(v);
+            big_where.push_back(i);
+            continue;
+        }
+        progs.push_back(v);
         where.push_back(i);
     }
     const double t0 = now_ms();
-    int prc = prepare_k2(bt->subs, 0);  // no-op once es_batch_prepare ran
+    int prc = prepare_k2(bt->subs, 0, &where);  // no-op once es_batch_prepare ran
     if (prc != ES_OK) { set_error("malformed sub-miter program"); return prc; }
     kps.reserve(where.size());
     for (int i : where) kps.push_back(&bt->subs[i].k2);
-    std::vector<es_result> rs(progs.size());
+    std::vector<es_result> rs(progs.size()), big_rs(big_progs.size());
     const double t1 = now_ms();
-    int rc = run_batch((int)progs.size(), progs.data(), opts, rs.data(), kps.data());
-    if (getenv("ES_VERBOSE"))
-        fprintf(stderr, "[es batch] jobs=%d prep=%.2fms run_batch=%.2fms\n", n, t1 - t0, now_ms() - t1);
+    int rc = progs.empty() ? ES_OK : run_batch((int)progs.size(), progs.data(), opts, rs.data(), kps.data());
     if (rc != ES_OK) return rc;
+    const double t2 = now_ms();
+    if (!big_progs.empty()) {
+        es_run_opts ob{};
+        if (opts) ob = *opts;
+        if (ob.budget_s >= 0 && opts) ob.budget_s = std::max(0.0, ob.budget_s - 1e-3 * (t2 - t0));
+        rc = run_batch_jit((int)big_progs.size(), big_progs.data(), &ob, big_rs.data());
+        if (rc != ES_OK) return rc;
+    }
+    if (getenv("ES_VERBOSE"))
+        fprintf(stderr, "[es batch] jobs=%d (K1 %zu) prep=%.2fms K2=%.2fms K1=%.2fms\n", n, big_progs.size(),
+                t1 - t0, t2 - t1, now_ms() - t2);
+    for (size_t k = 0; k < big_where.size(); ++k) {
+        where.push_back(big_where[k]);
+        rs.push_back(big_rs[k]);
+    }
     for (size_t k = 0; k < where.size(); ++k) {
         outs[where[k]] = rs[k];
         if (rs[k].verdict == ES_COUNTEREXAMPLE &&

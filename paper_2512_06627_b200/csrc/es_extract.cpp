@@ -204,10 +204,15 @@ int evaluate_sub(const SubMiterC &s, uint64_t pattern) {  // eval.py:22-36 on th
     return v[s.out_lit >> 1] ^ (s.out_lit & 1);
 }
 
-int prepare_k2(std::vector<SubMiterC> &subs, int n_threads) {
+int prepare_k2(std::vector<SubMiterC> &subs, int n_threads, const std::vector<int> *only) {
     std::vector<int> todo;
-    for (int i = 0; i < (int)subs.size(); ++i)
-        if (!subs[i].k2_ready && !subs[i].too_many_inputs) todo.push_back(i);
+    if (only) {
+        for (int i : *only)
+            if (!subs[i].k2_ready && !subs[i].too_many_inputs) todo.push_back(i);
+    } else {
+        for (int i = 0; i < (int)subs.size(); ++i)
+            if (!subs[i].k2_ready && !subs[i].too_many_inputs) todo.push_back(i);
+    }
     if (todo.empty()) return ES_OK;
     std::atomic<int> next{0}, bad{0};
     auto work = [&]() {

@@ -282,9 +282,12 @@ int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std
     int region = 0;
     if (!splice_body(net, threads, &ptx, err, &region)) return ES_E_BAD_PROGRAM;
     const uint64_t key = fnv1a(ptx) ^ (uint64_t)(uint32_t)threads;
-    std::lock_guard<std::mutex> lk(g_jit_mu);
-    auto it = g_cache.find(key);
-    if (it != g_cache.end()) { *out = it->second; *jit_ms = 0.0; return ES_OK; }
+    {
+        std::lock_guard<std::mutex> lk(g_jit_mu);
+        auto it = g_cache.find(key);
+        if (it != g_cache.end()) { *out = it->second; *jit_ms = 0.0; return ES_OK; }
+    }
+    // compile outside the lock: batches JIT many programs on parallel threads
     auto t0 = now_ms();
     std::vector<char> cubin;
     std::string info;
@@ -318,6 +321,14 @@ int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std
     }
     *jit_ms = now_ms() - t0;
     k->jit_ms = *jit_ms;
+    std::lock_guard<std::mutex> lk(g_jit_mu);
+    auto it = g_cache.find(key);
+    if (it != g_cache.end()) {  // another thread won the race: keep its module
+        cudaLibraryUnload(k->lib);
+        delete k;
+        *out = it->second;
+        return ES_OK;
+    }
     g_cache[key] = k;
     *out = k;
     return ES_OK;

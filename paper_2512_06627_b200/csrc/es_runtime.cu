@@ -1097,6 +1097,53 @@ int run_one(const es_prog *prog, const es_run_opts *opts, es_result *out) {
     return rc;
 }
 
+// Sub-miters as large as whole miters (a sweep's late-column pairs of a 16x16
+// multiplier are 32-PI cones of ~2,800 gates) are K1 work: compile all their
+// kernels on parallel host threads first (each is its own program), then run
+// them one after another on the device.
+int run_batch_jit(int n_jobs, const es_prog *progs, const es_run_opts *opts, es_result *outs) {
+    es_run_opts o{};
+    if (opts) o = *opts;
+    o.engine = ES_ENGINE_JIT;
+    const double t0 = now_ms();
+    const double deadline = o.budget_s >= 0 && opts ? t0 + 1e3 * o.budget_s : -1.0;
+    int sms = 0;
+    if (cudaGetDeviceCount(&sms) != cudaSuccess || sms == 0) { set_error("no CUDA device visible"); return ES_E_NO_DEVICE; }
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, o.device));
+    std::atomic<int> next{0};
+    auto warm = [&]() {
+        if (cudaSetDevice(o.device) != cudaSuccess) return;
+        for (;;) {
+            const int i = next.fetch_add(1);
+            if (i >= n_jobs) return;
+            if (validate(progs[i]) != ES_OK || progs[i].src0[progs[i].num_instrs - 1] < 0) continue;
+            std::shared_ptr<MappedProg> mp;
+            if (get_mapped(progs[i], &mp) != ES_OK) continue;
+            std::lock_guard<std::mutex> lk(mp->mu);
+            const int k = choose_cofactors(*mp, o, sms);
+            const LutNet &net = mp->variant(k);
+            const int threads = k1_threads(o, k), slot = k1_slot(threads);
+            if (mp->jk[k][slot]) continue;
+            JitKernel *jk = nullptr;
+            double ms = 0;
+            std::string err;
+            if (jit_get(net, threads, &jk, &ms, &err) == ES_OK) mp->jk[k][slot] = jk;
+        }
+    };
+    const int nt = (int)std::min<unsigned>(std::max(1u, std::thread::hardware_concurrency()), (unsigned)n_jobs);
+    std::vector<std::thread> th;
+    for (int q = 1; q < nt; ++q) th.emplace_back(warm);
+    warm();
+    for (auto &x : th) x.join();
+    for (int i = 0; i < n_jobs; ++i) {
+        es_run_opts oi = o;
+        if (deadline >= 0) oi.budget_s = std::max(0.0, (deadline - now_ms()) * 1e-3);
+        const int rc = run_one(&progs[i], &oi, &outs[i]);
+        if (rc != ES_OK) return rc;
+    }
+    return ES_OK;
+}
+
 int run_batch(int n_jobs, const es_prog *progs, const es_run_opts *opts, es_result *outs,
               const K2Prog *const *prebuilt) {
     const double t0 = now_ms();

@@ -43,7 +43,7 @@ class SweepConfig:
 
     engine: str = "es"
     budget: float | None = None  # global wall budget
-    pair_budget: float = 5.0  # per round of sub-miters; final obligation gets the rest
+    pair_budget: float = 5.0  # per sub-miter (a round of n gets n x); final obligation gets the rest
     seed: int = 0
     sim_words: int = 64
     device: int = 0
@@ -126,7 +126,9 @@ def sweep(miter, config: SweepConfig = SweepConfig()) -> CheckResult:
         if not run_idx:
             continue
         batch.select(run_idx)
-        budget = config.pair_budget if rem is None else min(config.pair_budget, rem)
+        # the reference gives each sub-miter pair_budget (sweep.py:355-356)
+        budget = config.pair_budget * len(run_idx)
+        budget = budget if rem is None else min(budget, rem)
         results = batch.run(budget=budget, device=dev)
         stats["engine_calls"] += len(run_idx)
         cexes = []
