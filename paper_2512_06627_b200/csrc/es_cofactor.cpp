@@ -15,6 +15,7 @@
 // top bits, smallest fanout) give 8 copies for 3,163 LUTs: 395 LUTs per word
 // instead of 1,549.
 #include <algorithm>
+#include <cstdlib>
 #include <unordered_map>
 
 #include "es_core.h"
@@ -99,6 +100,15 @@ std::vector<int32_t> rank_cofactor_pis(const Dag &dag, int k) {
         return a > b;  // ties: the higher PI (later in the pattern order)
     });
     if ((int)cand.size() > k) cand.resize(k);
+    if (const char *e = getenv("ES_COF_PIS")) {  // experiment: explicit cofactor PIs
+        std::vector<int32_t> forced;
+        for (const char *q = e; *q;) {
+            forced.push_back(atoi(q));
+            while (*q && *q != ',') ++q;
+            if (*q == ',') ++q;
+        }
+        if ((int)forced.size() >= k) { forced.resize(k); return forced; }
+    }
     return cand;
 }
 
