@@ -351,8 +351,11 @@ int pick_chunk_log2(uint64_t total_words, int threads, int resident_ctas) {
     const int tw = total_words ? 63 - __builtin_clzll(total_words) : 0;
     int lg = 0;
     while ((1 << lg) < threads) ++lg;
-    // aim for >= 16 chunks per resident CTA, cap at 2^13 words (2^18 patterns)
-    int want = tw - (int)std::ceil(std::log2(std::max(1, resident_ctas * 16)));
+    // aim for >= 32 chunks per resident CTA over the whole space (a rank of
+    // an 8-GPU shard still gets ~4: a small tail), cap at 2^13 words
+    int per_cta = 32;  // measured: full mult16 +0.5 %, its 1/8 shard -11 % vs 16
+    if (const char *e = getenv("ES_CHUNKS_PER_CTA")) per_cta = std::max(1, atoi(e));
+    int want = tw - (int)std::ceil(std::log2(std::max(1, resident_ctas * per_cta)));
     want = std::min(want, 13);
     return std::max(lg, want);
 }
