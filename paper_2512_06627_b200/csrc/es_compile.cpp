@@ -518,7 +518,6 @@ void map_luts(const Dag &dag, LutNet *net) {
                 }
                 for (int pa : parents[v]) if (--pend[pa] == 0) ready.push_back(pa);
             }
-            if (getenv("ES_SCHED_DEBUG")) fprintf(stderr, "dfs peak %d list peak %d\n", peak_of(order), peak_of(out2));
             if (peak_of(out2) < peak_of(order)) order.swap(out2);
         }
     }

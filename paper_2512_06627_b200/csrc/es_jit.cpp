@@ -143,11 +143,6 @@ int ptx_to_cubin(const std::string &ptx, std::vector<char> *cubin, std::string *
     std::vector<const char *> opts = {"--gpu-name=sm_100a", "--verbose"};
     std::string olev = std::string("-O") + (getenv("ES_PTXAS_O") ? getenv("ES_PTXAS_O") : "3");
     opts.push_back(olev.c_str());
-    std::string maxr;
-    if (const char *m = getenv("ES_MAXRREG")) {  // experiment: cap registers for occupancy
-        maxr = std::string("--maxrregcount=") + m;
-        opts.push_back(maxr.c_str());
-    }
     nvPTXCompileResult r = nvPTXCompilerCompile(h, (int)opts.size(), opts.data());
     size_t n = 0;
     if (r != NVPTXCOMPILE_SUCCESS) {
