@@ -282,15 +282,33 @@ void build_k2prog_auto(const Dag &dag, K2Prog *kp, int min_words_log2, int max_s
     std::vector<int> order(per_word.size());
     for (size_t k = 0; k < order.size(); ++k) order[k] = (int)k;
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return per_word[a] < per_word[b]; });
+    // The cheapest depth by gates may need > 88 slots, which the runtime runs
+    // at one CTA per SM (ncu, config 4: 23 % issue vs 42 % at two CTAs), so
+    // weigh occupancy: also try the next depths until one fits 88 slots and
+    // keep the lower effective cost.  Penalty 3.5 measured best on config 4
+    // (1.0: 28.7 ms, 1.8: 26.6, 2.5: 25.1, 3.5: 24.8, 6.0: 25.1).
+    static const double big_pen = getenv("ES_K2_BIGPEN") ? atof(getenv("ES_K2_BIGPEN")) : 3.5;
+    auto occupancy_cost = [](const K2Prog &q, double pw) {
+        return pw * (q.num_slots > 88 ? big_pen : q.num_slots > 44 ? 1.1 : 1.0);
+    };
+    bool have = false;
+    double best = 0;
+    int builds = 0;
     for (int k : order) {
-        if (k == 0) { build_k2prog(dag, kp); kp->cof_pis.clear(); return; }
         K2Prog q;
-        build_k2prog(xs[k], &q);
-        if (q.num_slots > max_slots) continue;
-        q.cof_pis.assign(rank.begin(), rank.begin() + k);
-        std::sort(q.cof_pis.begin(), q.cof_pis.end());
-        *kp = std::move(q);
-        return;
+        if (k == 0) build_k2prog(dag, &q);
+        else build_k2prog(xs[k], &q);
+        ++builds;
+        if (q.num_slots > max_slots && k != 0) continue;
+        const double c = occupancy_cost(q, per_word[k]);
+        if (!have || c < best) {
+            q.cof_pis.assign(rank.begin(), rank.begin() + k);
+            std::sort(q.cof_pis.begin(), q.cof_pis.end());
+            *kp = std::move(q);
+            best = c;
+            have = true;
+        }
+        if (kp->num_slots <= 88 || builds >= 4 || k == 0) break;
     }
 }
 
