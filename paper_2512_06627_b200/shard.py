@@ -181,9 +181,15 @@ class PeerBest:
     device memory, mapped into every rank through CUDA IPC.  Every rank's
     kernel atomicMin's (system scope) into it and reads it at each chunk
     claim, so a counterexample found on any GPU stops every GPU at its next
-    chunk -- no per-slice collective on the data path.  Two words alternate
-    between verdicts so rank 0 can re-arm one while the other is being read.
-    Collective constructor (every rank of ``group``)."""
+    chunk -- no per-slice collective on the data path.  Three words rotate
+    between verdicts: rank 0 re-arms the word of verdict s+1 while verdict s
+    runs, and that word was last read at verdict s-2, before the barrier that
+    closed verdict s-1 -- so one barrier per verdict suffices.  Words are
+    armed with all-ones (no pattern index reaches it), so one PeerBest serves
+    programs of any PI count.  Collective constructor (every rank of ``group``)."""
+
+    NONE = 0xFFFFFFFFFFFFFFFF  # "no counterexample yet"
+    WORDS = 3
 
     def __init__(self, group=None, device: int | None = None):
         import torch
@@ -196,11 +202,12 @@ class PeerBest:
         self.ptrs = []
         self._step = 0
         L = N.lib()
-        for _ in range(2):
+        for _ in range(self.WORDS):
             ptr = ctypes.c_void_p()
             handle = (ctypes.c_uint8 * 64)()
             if self.rank == 0:
                 N.check(L.es_ipc_alloc(self.device, ctypes.byref(ptr), handle))
+                N.check(L.es_word_write(self.device, ptr, self.NONE))  # armed before it is shared
             box = [bytes(handle)]
             if self.world > 1:
                 dist.broadcast_object_list(box, src=0, group=group)
@@ -228,7 +235,7 @@ def sweep_peer(prog, peer: PeerBest, group=None, device: int | None = None,
                cofactor="throughput") -> EsResult:
     """run_exhaustive sharded over ``group`` with the shared peer word
     (collective call; same program on every rank).  One launch per rank over
-    its residue class of chunks; two barriers per verdict, no all-reduce."""
+    its residue class of chunks; one barrier per verdict, no all-reduce."""
     import torch
     import torch.distributed as dist
 
@@ -242,14 +249,10 @@ def sweep_peer(prog, peer: PeerBest, group=None, device: int | None = None,
         return EsResult(EXHAUSTED_ZERO, None, 1 << p.num_pis)
     sess = session_for(p, dev, cofactor)
     sentinel = 1 << p.num_pis
-    k = peer._step & 1
+    k = peer._step % peer.WORDS
     peer._step += 1
-    if peer._step == 1 and rank == 0:
-        peer.write(k, sentinel)
-    if world > 1:
-        dist.barrier(group=group)      # word k armed; everyone has read word k^1
-    if rank == 0:
-        peer.write(k ^ 1, sentinel)  # re-arm the other word for the next verdict
+    if rank == 0:  # the next verdict's word: last read two verdicts ago
+        peer.write((k + 1) % peer.WORDS, peer.NONE)
     stream = torch.cuda.current_stream(dev)
     sess.launch(stream.cuda_stream, peer.ptrs[k].value, 0, sess.n_chunks, rank, world)
     stream.synchronize()
