@@ -569,7 +569,7 @@ def run_b200(args) -> None:
                        "witness_index": r.witness_index,
                        "parallelism": (f"pattern-space shards x{world}; one shared minimum word "
                                        "in rank 0's HBM mapped into every rank (CUDA IPC, NVLink "
-                                       "peer memory): kernel atomicMin + early exit, 2 barriers "
+                                       "peer memory): kernel atomicMin + early exit, 1 barrier "
                                        "per verdict" if collective == "p2p" else
                                        f"pattern-space shards x{world}, NCCL MIN all-reduce "
                                        f"after each of {S} launch slice(s)") if world > 1 else
@@ -599,7 +599,9 @@ def run_b200(args) -> None:
                     "d2h_bytes_per_step": 8,
                     "path": "es.es_check(sub-miter) -> compile_program -> C ABI es_run "
                             "(JIT module cached by program hash)" if world == 1 else
-                            "shard.es_check_sharded -> compile_program -> session launches + NCCL",
+                            ("shard.es_check_peer -> compile_program -> one session launch per rank "
+                             "on the shared peer word + 1 barrier" if collective == "p2p" else
+                             "shard.es_check_sharded -> compile_program -> session launches + NCCL MIN"),
                     "ms_per_step": float(e_total.item()) / args.steps},
             "time_to_verdict": {"cold_ms": cold_ms, "jit_ms": cold.stats.get("jit_ms"),
                                 "host_compile_ms": cold.stats.get("compile_ms"),
