@@ -16,7 +16,7 @@ import ctypes
 import numpy as np
 
 from . import _native as N
-from .xag import Gate, GateKind, Lit, Xag
+from .xag import Gate, GateKind, Lit, Xag, packed_gates
 
 
 class AigerError(ValueError):
@@ -76,9 +76,7 @@ def parse_aiger(data) -> Xag:
 
 def _arrays(xag):
     g = len(xag.gates)
-    kind = np.fromiter((int(q.kind) for q in xag.gates), np.uint8, g)
-    in0 = np.fromiter((q.in0.node * 2 + int(q.in0.neg) for q in xag.gates), np.uint32, g)
-    in1 = np.fromiter((q.in1.node * 2 + int(q.in1.neg) for q in xag.gates), np.uint32, g)
+    kind, in0, in1 = packed_gates(xag)
     outs = np.fromiter((o.node * 2 + int(o.neg) for o in xag.outputs), np.uint32, len(xag.outputs))
     return xag.num_pis, g, kind, in0, in1, len(xag.outputs), outs
 

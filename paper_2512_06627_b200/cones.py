@@ -22,7 +22,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as N
-from .xag import FALSE, Gate, GateKind, Lit, Xag, XagBuilder
+from .xag import FALSE, Gate, GateKind, Lit, Xag, XagBuilder, packed_gates
 
 _ONES = np.uint64(0xFFFFFFFFFFFFFFFF)
 
@@ -153,9 +153,7 @@ class NativeBatch:
     def __init__(self, parent, pairs, merges: dict[int, Lit] | None = None, threads: int = 0):
         pairs = list(pairs)
         n, g = parent.num_pis, len(parent.gates)
-        kind = np.fromiter((int(q.kind) for q in parent.gates), np.uint8, g)
-        in0 = np.fromiter((q.in0.node * 2 + int(q.in0.neg) for q in parent.gates), np.uint32, g)
-        in1 = np.fromiter((q.in1.node * 2 + int(q.in1.neg) for q in parent.gates), np.uint32, g)
+        kind, in0, in1 = packed_gates(parent)
         merges = merges or {}
         mn = np.array(list(merges.keys()), np.int32)
         ml = np.array([l.node * 2 + int(l.neg) for l in merges.values()], np.uint32)

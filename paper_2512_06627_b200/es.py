@@ -30,6 +30,7 @@ import numpy as np
 from . import _native as N
 from .miter import evaluate
 from .verdict import COUNTEREXAMPLE, EQUIVALENT, UNKNOWN, CheckResult
+from .xag import packed_gates
 
 MAX_ES_PIS = 40
 
@@ -173,9 +174,7 @@ def compile_program(xag) -> InstrProgram:
     n, g = xag.num_pis, len(xag.gates)
     if n > MAX_ES_PIS:
         raise TooManyInputs(f"{n} PIs exceeds the {MAX_ES_PIS} ceiling")
-    kinds = np.fromiter((int(q.kind) for q in xag.gates), dtype=np.uint8, count=g)
-    in0 = np.fromiter((q.in0.node * 2 + int(q.in0.neg) for q in xag.gates), dtype=np.uint32, count=g)
-    in1 = np.fromiter((q.in1.node * 2 + int(q.in1.neg) for q in xag.gates), dtype=np.uint32, count=g)
+    kinds, in0, in1 = packed_gates(xag)
     o = xag.outputs[0]
     cap = n + g + 1
     op = np.zeros(cap, np.int8)
