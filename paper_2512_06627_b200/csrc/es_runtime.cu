@@ -317,6 +317,17 @@ int get_ctx(int dev, Ctx **out) {
     Ctx *c = new Ctx();
     c->dev = dev;
     CK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, dev));
+    {
+        // keep freed stream-ordered allocations in the pool: the K2 / K3 drivers
+        // allocate per call, and a pool that trims at every synchronize goes
+        // back to the driver each time (measured: 0.5 -> 11 ms per small K2 run
+        // once another process had used the GPU)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    }
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CK(cudaMalloc(&c->d_best, 64));
     CK(cudaMalloc(&c->d_counter, 64));

@@ -188,6 +188,11 @@ int sim_device(int dev, SimDev **out) {
     SimDev *c = new SimDev();
     c->dev = dev;
     SCK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    cudaMemPool_t pool;  // keep freed per-call buffers cached (see es_runtime.cu:get_ctx)
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
     ctx.push_back(c);
     *out = c;
     return ES_OK;
