@@ -17,6 +17,12 @@ GRID = list(itertools.product([1, 2, 3, 8, 32], [0.01, 0.5, 10.0, 900.0], [0.02,
 
 
 def test_cpu_rules_match_reference():
+    import os
+    import sys
+    src = "/root/reference/pkg/src"  # the build container only (never on the GPU box)
+    if os.path.isdir(src) and src not in sys.path:
+        os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+        sys.path.append(src)
     ref = pytest.importorskip("cecprove.sched", reason="reference not importable here")
     for n, ts, tb, te, cutoff in GRID:
         p = O.Predictions(ts, tb, te)
