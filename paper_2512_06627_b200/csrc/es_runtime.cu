@@ -243,8 +243,6 @@ __global__ void __launch_bounds__(128) es_k2(const K2Job *__restrict__ jobs,
         }
     }
 }
-#undef K2_CASE
-#undef K2_CASES_V
 
 // ---------------------------------------------------------------------------
 // ALU-pipe peak microbenchmark: 8 independent LOP3 chains per thread, enough
@@ -587,11 +585,6 @@ static int k2_occupancy(size_t smem, int *nb) {
     return ES_OK;
 }
 
-// One launch group: jobs sharing a words-per-thread width W.  Items are dealt
-// round-robin across jobs (item r of every job before item r+1 of any job),
-// so a non-equivalent job's first item settles its minimum before its later
-// items are claimed -- those are then skipped -- while every item below the
-// final minimum is still fully evaluated.
 // One launch group: jobs sharing a words-per-thread width W.  Items are dealt
 // round-robin across jobs (item r of every job before item r+1 of any job),
 // so a non-equivalent job's first item settles its minimum before its later
