@@ -559,6 +559,21 @@ def run_b200(args) -> None:
                 traffic = json.load(open(prof)).get(args.config)
             except (OSError, ValueError):
                 traffic = None
+        # hardware pipe utilisation of the same kernel from the committed ncu
+        # summary (the bench itself never runs under a profiler)
+        hw = None
+        ncu_file = {4: "r01_k1_cof4_mult16_ncu_full.json", 3: "r01_k1_cof3_mult16_ncu_full.json",
+                    0: "r01_k1_mult16_ncu_full.json"}.get(kcof)
+        if args.config == "mult16" and ncu_file and os.path.exists(os.path.join(ROOT, "profiles", ncu_file)):
+            try:
+                d = json.load(open(os.path.join(ROOT, "profiles", ncu_file)))
+                pct = lambda k: float(d[k].split()[0])  # noqa: E731
+                hw = {"alu_pipe_pct": pct("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+                      "fma_pipe_pct": pct("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
+                      "issue_active_pct": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                      "source": f"profiles/{ncu_file} (ncu --set full, same kernel)"}
+            except (OSError, ValueError, KeyError):
+                hw = None
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_s * 1e3 / args.steps,
@@ -583,6 +598,7 @@ def run_b200(args) -> None:
             "roofline": {"bound": "alu", "achieved": achieved,
                          "peak": lane_peak * 32, "unit": UNIT,
                          "frac": achieved / (lane_peak * 32), "traffic": traffic,
+                         "hardware": hw,
                          "kernel": "es_k1", "kernel_ms": k_ms,
                          "peak_source": "measured: es_alu_peak LOP3 microbenchmark on this GPU "
                                         "(lane-LOP3/s x 32 patterns, 1 gate per LOP3)",
