@@ -220,12 +220,14 @@ class NativeBatch:
         self.origins = [self.origins[i] for i in idx]
 
     def run_arrays(self, budget: float | None = None, cancel=None, device: int = 0,
-                   engine: str = "auto") -> np.ndarray:
+                   engine: str = "auto", cofactor="auto") -> np.ndarray:
         """Batched run_exhaustive over every sub-miter (witnesses re-checked on
         the sub-miter by the library); the raw es_result records as a numpy
         structured array (fields of include/es_b200.h es_result).  engine
         "auto": jobs of >= 2e12 gate-patterns get their own K1 kernel (JIT on
-        parallel host threads), the rest share one K2 launch; "interp": all K2."""
+        parallel host threads), the rest share one K2 launch; "interp": all K2.
+        cofactor "none": interpreter programs without the cofactor-depth search
+        (cheaper on the host for batches with little device work)."""
         from .es import _CancelWatcher, _opts
 
         n = len(self)
@@ -236,15 +238,16 @@ class NativeBatch:
                 outs[i].reason = 1
             return np.ctypeslib.as_array(outs)
         with _CancelWatcher(cancel) as cw:
-            opts = _opts(device, engine, budget, cw.address, 20.0, 0)
+            opts = _opts(device, engine, budget, cw.address, 20.0, 0, cofactor=cofactor)
             N.check(N.lib().es_batch_run(self._h, ctypes.byref(opts), outs))
         return np.ctypeslib.as_array(outs)
 
-    def run(self, budget: float | None = None, cancel=None, device: int = 0, engine: str = "auto"):
+    def run(self, budget: float | None = None, cancel=None, device: int = 0, engine: str = "auto",
+            cofactor="auto"):
         """As run_arrays, as a list of EsResult (None for ineligible jobs)."""
         from .es import _to_esresult
 
-        outs = self.run_arrays(budget, cancel, device, engine)
+        outs = self.run_arrays(budget, cancel, device, engine, cofactor)
         pis = self.table()["num_pis"]
         res = []
         for i in range(len(outs)):

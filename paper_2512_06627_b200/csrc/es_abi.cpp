@@ -491,7 +491,9 @@ int32_t es_batch_run(es_batch *bp, const es_run_opts *opts, es_result *outs) {
         where.push_back(i);
     }
     const double t0 = now_ms();
-    int prc = prepare_k2(bt->subs, 0, &where);  // no-op once es_batch_prepare ran
+    // no-op once es_batch_prepare ran; cofactor_pis NONE skips the depth search
+    const bool search = !(opts && opts->cofactor_pis == ES_COFACTOR_NONE);
+    int prc = prepare_k2(bt->subs, 0, &where, search);
     if (prc != ES_OK) { set_error("malformed sub-miter program"); return prc; }
     kps.reserve(where.size());
     for (int i : where) kps.push_back(&bt->subs[i].k2);

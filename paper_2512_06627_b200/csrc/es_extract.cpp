@@ -204,7 +204,7 @@ int evaluate_sub(const SubMiterC &s, uint64_t pattern) {  // eval.py:22-36 on th
     return v[s.out_lit >> 1] ^ (s.out_lit & 1);
 }
 
-int prepare_k2(std::vector<SubMiterC> &subs, int n_threads, const std::vector<int> *only) {
+int prepare_k2(std::vector<SubMiterC> &subs, int n_threads, const std::vector<int> *only, bool search) {
     std::vector<int> todo;
     if (only) {
         for (int i : *only)
@@ -223,7 +223,8 @@ int prepare_k2(std::vector<SubMiterC> &subs, int n_threads, const std::vector<in
             Dag dag;
             std::string err;
             if (build_dag(s.view(), &dag, &err) != ES_OK) { bad.fetch_add(1); continue; }
-            build_k2prog_auto(dag, &s.k2);
+            if (search) build_k2prog_auto(dag, &s.k2);
+            else build_k2prog(dag, &s.k2);
             s.k2_ready = true;
         }
     };

@@ -38,6 +38,9 @@ int extract_compile(int32_t num_pis, int32_t num_gates, const uint8_t *kind, con
 int evaluate_sub(const SubMiterC &s, uint64_t pattern);
 // Build the K2 programs of the sub-miters that lack one, on n_threads host
 // threads (0 = all).  Done once per batch, after any selection.
-int prepare_k2(std::vector<SubMiterC> &subs, int n_threads, const std::vector<int> *only = nullptr);
+// search = false: plain programs (no cofactor-depth search) -- cheaper on the
+// host when the batch's device work is small (a sweep round).
+int prepare_k2(std::vector<SubMiterC> &subs, int n_threads, const std::vector<int> *only = nullptr,
+               bool search = true);
 
 }  // namespace es

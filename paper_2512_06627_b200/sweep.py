@@ -129,7 +129,11 @@ def sweep(miter, config: SweepConfig = SweepConfig()) -> CheckResult:
         # the reference gives each sub-miter pair_budget (sweep.py:355-356)
         budget = config.pair_budget * len(run_idx)
         budget = budget if rem is None else min(budget, rem)
-        results = batch.run(budget=budget, device=dev)
+        # the interpreter's cofactor-depth search costs more host time than it
+        # saves on a round's few dozen cones: plain programs, unless the round
+        # is heavy (its big jobs go through K1 either way)
+        work = float((tab["G"].astype(np.float64)[run_idx] * np.exp2(tab["num_pis"][run_idx])).sum())
+        results = batch.run(budget=budget, device=dev, cofactor="auto" if work > 1e13 else "none")
         stats["engine_calls"] += len(run_idx)
         cexes = []
         for j, (k, r) in enumerate(zip(run_idx, results)):
