@@ -20,6 +20,7 @@
 
 #include "es_codegen_t.h"
 #include "es_jit.h"
+#include "es_nvtx.h"
 
 namespace es {
 
@@ -283,6 +284,7 @@ int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std
         if (it != g_cache.end()) { *out = it->second; *jit_ms = 0.0; return ES_OK; }
     }
     // compile outside the lock: batches JIT many programs on parallel threads
+    NvtxRange nvtx("es_jit");
     auto t0 = now_ms();
     std::vector<char> cubin;
     std::string info;

@@ -28,6 +28,7 @@
 #include "es_codegen_t.h"
 #include "es_jit.h"
 #include "es_k2prog.h"
+#include "es_nvtx.h"
 
 namespace es {
 
@@ -466,6 +467,7 @@ static int k1_slot(int threads) {
 
 static int run_k1(const LutNet &net, int G, const es_run_opts &o, Ctx *c, double deadline,
                   es_result *r, JitKernel **jk_cache) {
+    NvtxRange nvtx("es_k1");
     const int threads = k1_threads(o, (int)net.cof_pis.size());
     K1Plan pl;
     double jit_ms = 0;
@@ -772,6 +774,7 @@ static void k2_group_results(const K2Group &gp, const es_prog *progs, const K2Pr
 static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &active,
                   const es_run_opts &o, Ctx *c, double deadline, es_result *outs,
                   const K2Prog *const *prebuilt = nullptr) {
+    NvtxRange nvtx("es_k2");
     // host: K2 programs (schedule, accumulator forwarding), in parallel --
     // unless the caller built them already (sub-miter batches do at extraction)
     std::vector<K2Prog> own;
@@ -914,6 +917,7 @@ struct MappedProg {
     int k2_runs = 0;
     std::mutex mu;
     const LutNet &variant(int k) {   // caller holds mu
+        NvtxRange nvtx("es_map");
         if (k == 0) {
             if (!net_ready) { map_luts(dag, &net); net_ready = true; }
             return net;
@@ -1034,6 +1038,7 @@ static int choose_cofactors(MappedProg &mp, const es_run_opts &o, int sms) {
 }
 
 int run_one(const es_prog *prog, const es_run_opts *opts, es_result *out) {
+    NvtxRange nvtx("es_run");
     const double t0 = now_ms();
     std::memset(out, 0, sizeof(*out));
     es_run_opts o{};
@@ -1109,6 +1114,7 @@ int run_one(const es_prog *prog, const es_run_opts *opts, es_result *out) {
 // kernels on parallel host threads first (each is its own program), then run
 // them one after another on the device.
 int run_batch_jit(int n_jobs, const es_prog *progs, const es_run_opts *opts, es_result *outs) {
+    NvtxRange nvtx("es_batch_k1");
     es_run_opts o{};
     if (opts) o = *opts;
     o.engine = ES_ENGINE_JIT;

@@ -37,6 +37,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/es_b200.h"
+#include "es_nvtx.h"
 
 namespace es {
 
@@ -234,6 +235,7 @@ int sim_levels(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const ui
 int sim_run(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
             const uint32_t *in1, const uint64_t *pi_words, int64_t words, int32_t device,
             uint64_t *node_words, double *device_ms) {
+    NvtxRange nvtx("es_sim");
     if (words < 1 || num_pis < 0 || num_gates < 0) { set_error("bad argument"); return ES_E_BAD_ARG; }
     SimProg sp;
     int rc = build_sim_prog(num_pis, num_gates, kind, in0, in1, &sp);
@@ -314,6 +316,7 @@ void sim_prog_free(void *prog_cache) {
 int sim_classes(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
                 const uint32_t *in1, const uint64_t *pi_words, int64_t words, int32_t device,
                 int32_t *class_id, uint8_t *polarity, int32_t *n_classes, double *device_ms) {
+    NvtxRange nvtx("es_sim_classes");
     if (words < 1 || num_pis < 0 || num_gates < 0 || !class_id || !polarity || !n_classes) {
         set_error("bad argument");
         return ES_E_BAD_ARG;
