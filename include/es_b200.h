@@ -192,6 +192,11 @@ int32_t es_batch_extract(int32_t num_pis, int32_t num_gates, const uint8_t *kind
 /* Build the interpreter programs (cofactor depth, schedule) of every job that
  * lacks one; es_batch_run does it on demand, this lets callers time it. */
 int32_t es_batch_prepare(es_batch *b, int32_t n_threads);
+/* Per-job interpreter program shape after es_batch_prepare: slot-file rows,
+ * records (gates + OUT records) and cofactor depth; -1 for unprepared jobs.
+ * The runtime groups launches by slots (<=44: 4 words/thread, <=88: 2, else). */
+int32_t es_batch_k2_stats(const es_batch *b, int32_t *num_slots, int32_t *num_records,
+                          int32_t *cofactor_pis);
 int32_t es_batch_size(const es_batch *b);
 int32_t es_batch_info(const es_batch *b, int32_t i, int32_t *num_pis, int32_t *num_gates,
                       uint64_t *hash, int32_t *num_instrs, int32_t *num_registers, int32_t *G);
@@ -231,6 +236,13 @@ int32_t es_word_read(int32_t device, void *dev_ptr, uint64_t *value);
 int32_t es_sim(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
                const uint32_t *in1, const uint64_t *pi_words, int64_t words, int32_t device,
                uint64_t *node_words, double *device_ms);
+/* ones_fraction(simulate(...)) numerators (sim.py:45-48; the stability /
+ * entropy features, features.py:165-180): ones[v] = number of 1-bits of node
+ * v over all words*64 patterns, num_nodes int64.  The node matrix stays on
+ * the device. */
+int32_t es_sim_ones(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+                    const uint32_t *in1, const uint64_t *pi_words, int64_t words, int32_t device,
+                    int64_t *ones, double *device_ms);
 /* The same on device buffers, enqueued on `stream` (a cudaStream_t) without
  * host synchronisation.  *prog_cache (may be NULL) keeps the compiled gate
  * program between calls on the same XAG; free it with es_sim_prog_free. */

@@ -34,11 +34,11 @@ ENGINES = {"auto": ENGINE_AUTO, "jit": ENGINE_JIT, "interp": ENGINE_INTERP}
 EXPORTS = ("es_compile", "es_run", "es_run_batch", "es_session_open", "es_session_geometry",
            "es_session_launch", "es_session_close", "es_map_stats", "es_map_pipes", "es_map_eval", "es_k2_stats", "es_k2_eval",
            "es_emit_ptx", "es_jit_check", "es_alu_peak", "es_batch_extract", "es_batch_size",
-           "es_batch_info", "es_batch_table", "es_batch_xag", "es_batch_select", "es_batch_run", "es_batch_merge", "es_batch_free",
+           "es_batch_info", "es_batch_table", "es_batch_k2_stats", "es_batch_xag", "es_batch_select", "es_batch_run", "es_batch_merge", "es_batch_free",
            "es_ipc_alloc", "es_ipc_open", "es_ipc_close", "es_word_write", "es_word_read",
            "es_map_stats_k", "es_map_pipes_k", "es_map_eval_k", "es_emit_ptx_k", "es_jit_check_k",
            "es_k2_eval_k", "es_k2_cofactor_pis", "es_batch_prepare",
-           "es_sim", "es_sim_device", "es_sim_prog_free", "es_sim_classes", "es_sim_levels",
+           "es_sim", "es_sim_ones", "es_sim_device", "es_sim_prog_free", "es_sim_classes", "es_sim_levels",
            "es_aiger_parse", "es_detect_xors", "es_xag_size", "es_xag_read", "es_xag_free",
            "es_aiger_write",
            "es_last_error", "es_version", "es_shutdown")
@@ -157,6 +157,8 @@ def lib():
         L.es_batch_extract.restype = ctypes.c_int32
         L.es_sim.argtypes = [_I, _I, _P, _P, _P, _P, ctypes.c_int64, _I, _P, _P]
         L.es_sim.restype = _I
+        L.es_sim_ones.argtypes = [_I, _I, _P, _P, _P, _P, ctypes.c_int64, _I, _P, _P]
+        L.es_sim_ones.restype = _I
         L.es_sim_device.argtypes = [_I, _I, _P, _P, _P, _P, ctypes.c_int64, _P, _P, _P]
         L.es_sim_device.restype = _I
         L.es_sim_prog_free.argtypes = [_P]
@@ -183,6 +185,8 @@ def lib():
         L.es_batch_size.restype = ctypes.c_int32
         L.es_batch_info.argtypes = [_P, ctypes.c_int32, _P, _P, _P, _P, _P, _P]
         L.es_batch_info.restype = ctypes.c_int32
+        L.es_batch_k2_stats.argtypes = [_P, _P, _P, _P]
+        L.es_batch_k2_stats.restype = ctypes.c_int32
         L.es_batch_table.argtypes = [_P, _P, _P, _P, _P]
         L.es_batch_table.restype = ctypes.c_int32
         L.es_batch_xag.argtypes = [_P, ctypes.c_int32, _P, _P, _P, _P, _P]

@@ -194,6 +194,16 @@ class NativeBatch:
                                        out["hash"].ctypes.data))
         return out
 
+    def k2_stats(self) -> dict:
+        """Per-job interpreter program shape (after prepare): num_slots,
+        num_records, cofactor_pis; -1 where no program was built yet."""
+        n = len(self)
+        out = {k: np.zeros(n, np.int32) for k in ("num_slots", "num_records", "cofactor_pis")}
+        N.check(N.lib().es_batch_k2_stats(self._h, out["num_slots"].ctypes.data,
+                                          out["num_records"].ctypes.data,
+                                          out["cofactor_pis"].ctypes.data))
+        return out
+
     def submiter(self, i: int) -> SubMiter:
         inf = self.info(i)
         ng, n = inf["num_gates"], inf["num_pis"]

@@ -36,6 +36,9 @@ int word_io(int dev, void *ptr, uint64_t *value, int write);
 int sim_run(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
             const uint32_t *in1, const uint64_t *pi_words, int64_t words, int32_t device,
             uint64_t *node_words, double *device_ms);
+int sim_ones(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+             const uint32_t *in1, const uint64_t *pi_words, int64_t words, int32_t device,
+             int64_t *ones, double *device_ms);
 int sim_run_device(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
                    const uint32_t *in1, const uint64_t *d_pi_words, int64_t words, void *stream,
                    uint64_t *d_node_words, void **prog_cache);
@@ -290,6 +293,16 @@ int32_t es_sim(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const ui
     return sim_run(num_pis, num_gates, kind, in0, in1, pi_words, words, device, node_words, device_ms);
 }
 
+int32_t es_sim_ones(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+                    const uint32_t *in1, const uint64_t *pi_words, int64_t words, int32_t device,
+                    int64_t *ones, double *device_ms) {
+    if ((num_gates > 0 && (!kind || !in0 || !in1)) || (num_pis > 0 && !pi_words) || !ones) {
+        set_error("null argument");
+        return ES_E_BAD_ARG;
+    }
+    return sim_ones(num_pis, num_gates, kind, in0, in1, pi_words, words, device, ones, device_ms);
+}
+
 int32_t es_sim_device(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
                       const uint32_t *in1, const uint64_t *d_pi_words, int64_t words, void *stream,
                       uint64_t *d_node_words, void **prog_cache) {
@@ -400,6 +413,20 @@ int32_t es_batch_prepare(es_batch *bp, int32_t n_threads) {
     return rc;
 }
 
+int32_t es_batch_k2_stats(const es_batch *bp, int32_t *num_slots, int32_t *num_records,
+                          int32_t *cofactor_pis) {
+    const Batch *bt = (const Batch *)bp;
+    if (!bt) { set_error("bad argument"); return ES_E_BAD_ARG; }
+    for (size_t i = 0; i < bt->subs.size(); ++i) {
+        const SubMiterC &s = bt->subs[i];
+        const bool ok = s.k2_ready;
+        if (num_slots) num_slots[i] = ok ? s.k2.num_slots : -1;
+        if (num_records) num_records[i] = ok ? (int32_t)s.k2.gates.size() : -1;
+        if (cofactor_pis) cofactor_pis[i] = ok ? (int32_t)s.k2.cof_pis.size() : -1;
+    }
+    return ES_OK;
+}
+
 int32_t es_batch_size(const es_batch *bp) { return bp ? (int32_t)((const Batch *)bp)->subs.size() : ES_E_BAD_ARG; }
 
 int32_t es_batch_info(const es_batch *bp, int32_t i, int32_t *num_pis, int32_t *num_gates,
@@ -412,11 +439,7 @@ int32_t es_batch_info(const es_batch *bp, int32_t i, int32_t *num_pis, int32_t *
     if (hash) *hash = s.hash;
     if (num_instrs) *num_instrs = s.too_many_inputs ? 0 : (int32_t)s.op.size();
     if (num_registers) *num_registers = s.num_registers;
-    if (G) {
-        int g = 0;
-        for (int8_t o : s.op) g += (o == ES_OP_AND || o == ES_OP_XOR);
-        *G = g;
-    }
+    if (G) *G = s.G;
     return s.too_many_inputs ? ES_E_TOO_MANY_INPUTS : ES_OK;
 }
 
@@ -428,11 +451,7 @@ int32_t es_batch_table(const es_batch *bp, int32_t *num_pis, int32_t *num_gates,
         const SubMiterC &s = bt->subs[i];
         if (num_pis) num_pis[i] = s.num_pis;
         if (num_gates) num_gates[i] = (int32_t)s.kind.size();
-        if (G) {
-            int g = 0;
-            for (int8_t o : s.op) g += (o == ES_OP_AND || o == ES_OP_XOR);
-            G[i] = g;
-        }
+        if (G) G[i] = s.G;
         if (hash) hash[i] = s.hash;
     }
     return ES_OK;
@@ -468,6 +487,7 @@ int32_t es_batch_run(es_batch *bp, const es_run_opts *opts, es_result *outs) {
     Batch *bt = (Batch *)bp;
     if (!bt || !outs) { set_error("bad argument"); return ES_E_BAD_ARG; }
     const int n = (int)bt->subs.size();
+    const double t_in = now_ms();
     // jobs worth a JIT kernel of their own (>= kBatchJitWork gate-patterns,
     // ~20 ms and up in the interpreter) run through K1, the rest through one
     // batched K2 launch
@@ -480,9 +500,7 @@ int32_t es_batch_run(es_batch *bp, const es_run_opts *opts, es_result *outs) {
         std::memset(&outs[i], 0, sizeof(es_result));
         if (bt->subs[i].too_many_inputs) { outs[i].verdict = ES_BUDGET_EXCEEDED; outs[i].reason = -1; continue; }
         const es_prog v = bt->subs[i].view();
-        int G = 0;
-        for (int q = 0; q < v.num_instrs; ++q) G += v.op[q] == ES_OP_AND || v.op[q] == ES_OP_XOR;
-        if (!force_interp && (double)G * std::ldexp(1.0, v.num_pis) >= kBatchJitWork) {
+        if (!force_interp && (double)bt->subs[i].G * std::ldexp(1.0, v.num_pis) >= kBatchJitWork) {
             big_progs.push_back(v);
             big_where.push_back(i);
             continue;
@@ -510,20 +528,26 @@ int32_t es_batch_run(es_batch *bp, const es_run_opts *opts, es_result *outs) {
         if (rc != ES_OK) return rc;
     }
     if (getenv("ES_VERBOSE"))
-        fprintf(stderr, "[es batch] jobs=%d (K1 %zu) prep=%.2fms K2=%.2fms K1=%.2fms\n", n, big_progs.size(),
-                t1 - t0, t2 - t1, now_ms() - t2);
+        fprintf(stderr, "[es batch] jobs=%d (K1 %zu) split=%.2fms prep=%.2fms K2=%.2fms K1=%.2fms\n", n,
+                big_progs.size(), t0 - t_in, t1 - t0, t2 - t1, now_ms() - t2);
     for (size_t k = 0; k < big_where.size(); ++k) {
         where.push_back(big_where[k]);
         rs.push_back(big_rs[k]);
     }
-    for (size_t k = 0; k < where.size(); ++k) {
+    // re-check every witness on its sub-miter (es.py:360), on all host cores
+    std::atomic<int> bad_job{-1};
+    parallel_for((int)where.size(), [&](int k) {
         outs[where[k]] = rs[k];
-        if (rs[k].verdict == ES_COUNTEREXAMPLE &&
-            evaluate_sub(bt->subs[where[k]], rs[k].witness_index) != 1) {
-            set_error("exhaustive-simulation witness failed re-check (job " + std::to_string(where[k]) + ")");
-            return ES_E_WITNESS;
+        if (rs[k].verdict == ES_COUNTEREXAMPLE && evaluate_sub(bt->subs[where[k]], rs[k].witness_index) != 1) {
+            int none = -1;
+            bad_job.compare_exchange_strong(none, where[k]);
         }
+    });
+    if (bad_job.load() >= 0) {
+        set_error("exhaustive-simulation witness failed re-check (job " + std::to_string(bad_job.load()) + ")");
+        return ES_E_WITNESS;
     }
+    if (getenv("ES_VERBOSE")) fprintf(stderr, "[es batch] total %.2fms\n", now_ms() - t_in);
     return ES_OK;
 }
 

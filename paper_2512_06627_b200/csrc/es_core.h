@@ -8,13 +8,35 @@
 //     -> PTX body   spliced into the hand-written K1 skeleton (k1_skeleton.cu)
 #pragma once
 
+#include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/es_b200.h"
 
 namespace es {
+
+// Run fn(0..n-1) on all host cores (one thread per 256 items at most).
+template <class F>
+inline void parallel_for(int n, F fn) {
+    const int nt = (int)std::min<int>(std::max(1u, std::thread::hardware_concurrency()),
+                                      std::max(1, n / 256));
+    std::atomic<int> next{0};
+    auto work = [&]() {
+        for (;;) {
+            const int i = next.fetch_add(1);
+            if (i >= n) return;
+            fn(i);
+        }
+    };
+    std::vector<std::thread> th;
+    for (int q = 1; q < nt; ++q) th.emplace_back(work);
+    work();
+    for (auto &x : th) x.join();
+}
 
 // Pattern layout shared by every engine (kernel, CPU model, witness decode):
 // pattern p = 32*w + b.  Bit b of a 32-bit word carries PIs 1..5

@@ -164,6 +164,7 @@ int extract_compile(int32_t num_pis, int32_t num_gates, const uint8_t *kind, con
             if (n < 0) { bad.fetch_add(1); continue; }
             s.op.resize(n); s.dst.resize(n); s.src0.resize(n); s.neg0.resize(n);
             s.src1.resize(n); s.neg1.resize(n); s.pi.resize(n);
+            for (int8_t o : s.op) s.G += o == ES_OP_AND || o == ES_OP_XOR;
             Dag dag;
             std::string e2;
             if (build_dag(s.view(), &dag, &e2) != ES_OK) { bad.fetch_add(1); continue; }

@@ -24,6 +24,7 @@ struct SubMiterC {
     std::vector<int32_t> dst, src0, src1, pi;
     std::vector<uint8_t> neg0, neg1;
     int32_t num_registers = 0;
+    int32_t G = 0;  // AND + XOR instructions (the credited gate count)
     K2Prog k2;  // interpreter program (with cofactor copies), built by prepare_k2
     bool k2_ready = false;
     es_prog view() const;

@@ -299,7 +299,13 @@ void build_k2prog_auto(const Dag &dag, K2Prog *kp, int min_words_log2, int max_s
         if (k == 0) build_k2prog(dag, &q);
         else build_k2prog(xs[k], &q);
         ++builds;
-        if (q.num_slots > max_slots && k != 0) continue;
+        // over 88 slots the runtime runs one word per thread at two CTAs per SM
+        // only if slots + staged records fit half an SM's shared memory
+        // (2 x (smem + 1 KB reserve + statics) <= 228 KB); otherwise one 4-warp CTA, which
+        // measured 12 % slower on config 4 than capping the depth
+        const size_t w1_smem = (size_t)q.num_slots * 128 * 4 + (q.gates.size() + 1) * 16;
+        const bool fits = q.num_slots <= max_slots && (q.num_slots <= 88 || w1_smem <= 115600);
+        if (!fits && k != 0) continue;
         const double c = occupancy_cost(q, per_word[k]);
         if (!have || c < best) {
             q.cof_pis.assign(rank.begin(), rank.begin() + k);

@@ -121,12 +121,17 @@ __global__ void __launch_bounds__(128) es_k2(const K2Job *__restrict__ jobs,
                                              const K2Item *__restrict__ items,
                                              unsigned long long item_begin,
                                              unsigned long long item_end, unsigned *counter,
-                                             int prog_bytes) {
+                                             int smem_bytes) {
+    // dynamic shared memory: the slot file from the bottom, the current job's
+    // records (plus one past-end record for the prefetch) at the top, so a job
+    // needs slots * 512 * W + (records + 1) * 16 bytes of its own, not the
+    // group's largest slot file plus its longest program
     extern __shared__ __align__(16) uint4 smem[];
     __shared__ unsigned long long s_item;
     const unsigned T = blockDim.x, t = threadIdx.x, lane = t & 31u;
-    const unsigned prog_addr = (unsigned)__cvta_generic_to_shared(smem);
-    const unsigned base = prog_addr + (unsigned)prog_bytes + t * W * 4;
+    const unsigned smem_addr = (unsigned)__cvta_generic_to_shared(smem);
+    const unsigned base = smem_addr + t * W * 4;
+    unsigned prog_addr = smem_addr;
     const unsigned long long kStop = ~0ull, kSkip = ~0ull - 1;
     int cur_job = -1;
     for (;;) {
@@ -147,9 +152,11 @@ __global__ void __launch_bounds__(128) es_k2(const K2Job *__restrict__ jobs,
         if (k == kSkip) { __syncthreads(); continue; }
         const K2Item it = items[k];
         const K2Job job = jobs[it.job];
+        const int rec0 = smem_bytes / 16 - (job.n_recs + 1);
+        prog_addr = smem_addr + 16u * (unsigned)rec0;
         if (it.job != cur_job) {  // stage the program records (uniform branch)
             const uint4 *src = reinterpret_cast<const uint4 *>(job.code);
-            for (int q = t; q < job.n_recs; q += T) smem[q] = __ldg(&src[q]);
+            for (int q = t; q < job.n_recs; q += T) smem[rec0 + q] = __ldg(&src[q]);
             cur_job = it.job;
         }
         __syncthreads();
@@ -547,24 +554,6 @@ static int run_k1(const LutNet &net, int G, const es_run_opts &o, Ctx *c, double
 // ---------------------------------------------------------------------------
 // K2 driver (single program or batch)
 // ---------------------------------------------------------------------------
-// Run fn(0..n-1) on all host cores.
-template <class F>
-static void parallel_for(int n, F fn) {
-    const int nt = (int)std::min<int>(std::max(1u, std::thread::hardware_concurrency()),
-                                      std::max(1, n / 256));
-    std::atomic<int> next{0};
-    auto work = [&]() {
-        for (;;) {
-            const int i = next.fetch_add(1);
-            if (i >= n) return;
-            fn(i);
-        }
-    };
-    std::vector<std::thread> th;
-    for (int q = 1; q < nt; ++q) th.emplace_back(work);
-    work();
-    for (auto &x : th) x.join();
-}
 
 // Device record of a gate / output (16 bytes): byte offsets of the operand /
 // destination slots for the launch's stride, then the K2_* flags.
@@ -574,8 +563,8 @@ static uint4 k2_record(const K2Gate &g, uint32_t stride) {
 
 template <int W>
 static int launch_k2(int grid, size_t smem, cudaStream_t st, const K2Job *jobs, const K2Item *items,
-                     uint64_t begin, uint64_t end, unsigned *counter, int prog_bytes) {
-    es_k2<W><<<grid, 128, smem, st>>>(jobs, items, begin, end, counter, prog_bytes);
+                     uint64_t begin, uint64_t end, unsigned *counter, int smem_bytes) {
+    es_k2<W><<<grid, 128, smem, st>>>(jobs, items, begin, end, counter, smem_bytes);
     CK(cudaGetLastError());
     return ES_OK;
 }
@@ -594,7 +583,7 @@ static int k2_occupancy(size_t smem, int *nb) {
 // final minimum is still fully evaluated.
 struct K2Group {
     std::vector<int> jobs_idx;   // indices into the caller's job arrays
-    int W = 1, prog_bytes = 0, nb = 1;
+    int W = 1, smem_bytes = 0, nb = 1;
     size_t smem = 0;
     uint4 *code = nullptr;       // device-image records, in the pinned stage
     size_t n_code = 0;
@@ -619,15 +608,16 @@ static int k2_group_prepare(K2Group &gp, const es_prog *progs, const K2Prog *con
                             uint4 *stage) {
     const int T = 128;
     const std::vector<int> &group = gp.jobs_idx;
-    int max_slots = 1, max_recs = 1;
-    for (int j : group) {
-        max_slots = std::max(max_slots, kps[j]->num_slots);
-        max_recs = std::max(max_recs, (int)kps[j]->gates.size());
-    }
-    gp.prog_bytes = (max_recs + 1) * 16;
+    int max_slots = 1;
+    for (int j : group) max_slots = std::max(max_slots, kps[j]->num_slots);
     int dev_smem = 0;
     CK(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->dev));
-    auto smem_for = [&](int W) { return (size_t)gp.prog_bytes + (size_t)max_slots * T * W * 4; };
+    auto smem_for = [&](int W) {  // the largest job's slot file + records (kernel layout)
+        size_t m = 16;
+        for (int j : group)
+            m = std::max(m, (size_t)std::max(kps[j]->num_slots, 1) * T * W * 4 + (kps[j]->gates.size() + 1) * 16);
+        return m;
+    };
     // widest W that keeps the target number of resident CTAs per SM, else
     // fewer CTAs (the interpreter is latency-bound: warps matter more than W)
     int W = 0;
@@ -640,6 +630,7 @@ static int k2_group_prepare(K2Group &gp, const es_prog *progs, const K2Prog *con
     }
     gp.W = W;
     gp.smem = smem_for(W);
+    gp.smem_bytes = (int)gp.smem;
     const uint32_t stride = (uint32_t)T * W * 4;
     const int G = (int)group.size();
     std::vector<size_t> off(G + 1, 0);  // one record per gate / output
@@ -728,9 +719,9 @@ static int k2_group_launch(K2Group &gp, cudaStream_t st, unsigned *counter, uint
                            uint64_t end, int sms) {
     CK(cudaMemsetAsync(counter, 0, sizeof(unsigned), st));
     const int grid = (int)std::min<uint64_t>(end - begin, (uint64_t)sms * gp.nb);
-    const int rc = gp.W == 4 ? launch_k2<4>(grid, gp.smem, st, gp.d_jobs, gp.d_items, begin, end, counter, gp.prog_bytes)
-                 : gp.W == 2 ? launch_k2<2>(grid, gp.smem, st, gp.d_jobs, gp.d_items, begin, end, counter, gp.prog_bytes)
-                             : launch_k2<1>(grid, gp.smem, st, gp.d_jobs, gp.d_items, begin, end, counter, gp.prog_bytes);
+    const int rc = gp.W == 4 ? launch_k2<4>(grid, gp.smem, st, gp.d_jobs, gp.d_items, begin, end, counter, gp.smem_bytes)
+                 : gp.W == 2 ? launch_k2<2>(grid, gp.smem, st, gp.d_jobs, gp.d_items, begin, end, counter, gp.smem_bytes)
+                             : launch_k2<1>(grid, gp.smem, st, gp.d_jobs, gp.d_items, begin, end, counter, gp.smem_bytes);
     if (rc == ES_OK) { gp.launches++; gp.done_items = end; }
     return rc;
 }
@@ -1166,7 +1157,8 @@ int run_batch(int n_jobs, const es_prog *progs, const es_run_opts *opts, es_resu
     std::vector<int> active;
     for (int j = 0; j < n_jobs; ++j) {
         std::memset(&outs[j], 0, sizeof(es_result));
-        int rc = validate(progs[j]);
+        // batch sub-miters were compiled and checked (build_dag) at extraction
+        int rc = prebuilt ? ES_OK : validate(progs[j]);
         if (rc != ES_OK) return rc;
         if (!constant_rail(progs[j], &outs[j])) active.push_back(j);
     }

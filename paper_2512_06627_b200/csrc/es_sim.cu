@@ -114,6 +114,20 @@ __global__ void es_sig_kernel(const unsigned long long *__restrict__ vals, int n
     }
 }
 
+// per-node count of 1-bits over all simulated patterns (ones_fraction,
+// sim.py:45-48), one warp per node row: only the counts leave the device
+__global__ void es_ones_kernel(const unsigned long long *__restrict__ vals, int n_nodes, long long words,
+                               long long *__restrict__ counts) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= n_nodes) return;
+    const unsigned long long *row = vals + (long long)warp * words;
+    long long c = 0;
+    for (long long q = lane; q < words; q += 32) c += __popcll(row[q]);
+#pragma unroll
+    for (int off = 16; off; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
+    if (lane == 0) counts[warp] = c;
+}
+
 // members[i] vs leader[i]: canonical rows equal?  one warp per pair
 __global__ void es_verify_kernel(const unsigned long long *__restrict__ vals, long long words,
                                  const int *__restrict__ member, const int *__restrict__ leader, int n,
@@ -231,10 +245,11 @@ int sim_levels(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const ui
     return rc == ES_OK ? sp.levels : rc;
 }
 
-// simulate() with host buffers (sim.py:21-38): node_words = num_nodes x words
-int sim_run(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
-            const uint32_t *in1, const uint64_t *pi_words, int64_t words, int32_t device,
-            uint64_t *node_words, double *device_ms) {
+// simulate() with host buffers (sim.py:21-38): node_words = num_nodes x words,
+// and/or ones = per-node 1-bit counts (num_nodes int64)
+static int sim_run_host(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+                        const uint32_t *in1, const uint64_t *pi_words, int64_t words, int32_t device,
+                        uint64_t *node_words, int64_t *ones, double *device_ms) {
     NvtxRange nvtx("es_sim");
     if (words < 1 || num_pis < 0 || num_gates < 0) { set_error("bad argument"); return ES_E_BAD_ARG; }
     SimProg sp;
@@ -248,7 +263,9 @@ int sim_run(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint3
     unsigned long long *d_pi = nullptr, *d_vals = nullptr;
     SCK(cudaMallocAsync(&d_recs, std::max<size_t>(sp.recs.size(), 1) * sizeof(SimRec), c->st));
     SCK(cudaMallocAsync(&d_pi, std::max<size_t>((size_t)num_pis * words, 1) * 8, c->st));
+    long long *d_ones = nullptr;
     SCK(cudaMallocAsync(&d_vals, (size_t)NN * words * 8, c->st));
+    if (ones) SCK(cudaMallocAsync(&d_ones, (size_t)NN * 8, c->st));
     if (!sp.recs.empty())
         SCK(cudaMemcpyAsync(d_recs, sp.recs.data(), sp.recs.size() * sizeof(SimRec), cudaMemcpyHostToDevice, c->st));
     if (num_pis > 0)
@@ -258,10 +275,17 @@ int sim_run(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint3
     SCK(cudaEventCreate(&e1));
     SCK(cudaEventRecord(e0, c->st));
     rc = sim_enqueue(sp, d_recs, num_pis, words, d_pi, d_vals, c->st, NN);
+    if (rc == ES_OK && ones) {
+        es_ones_kernel<<<(unsigned)((NN * 32 + 255) / 256), 256, 0, c->st>>>(d_vals, (int)NN, words, d_ones);
+        SCK(cudaGetLastError());
+    }
     SCK(cudaEventRecord(e1, c->st));
-    if (rc == ES_OK)
+    if (rc == ES_OK && node_words)
         SCK(cudaMemcpyAsync(node_words, d_vals, (size_t)NN * words * 8, cudaMemcpyDeviceToHost, c->st));
+    if (rc == ES_OK && ones)
+        SCK(cudaMemcpyAsync(ones, d_ones, (size_t)NN * 8, cudaMemcpyDeviceToHost, c->st));
     SCK(cudaStreamSynchronize(c->st));
+    if (d_ones) cudaFreeAsync(d_ones, c->st);
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
     if (device_ms) *device_ms = ms;
@@ -272,6 +296,21 @@ int sim_run(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint3
     cudaFreeAsync(d_vals, c->st);
     SCK(cudaStreamSynchronize(c->st));
     return rc;
+}
+
+int sim_run(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+            const uint32_t *in1, const uint64_t *pi_words, int64_t words, int32_t device,
+            uint64_t *node_words, double *device_ms) {
+    return sim_run_host(num_pis, num_gates, kind, in0, in1, pi_words, words, device, node_words, nullptr,
+                        device_ms);
+}
+
+int sim_ones(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+             const uint32_t *in1, const uint64_t *pi_words, int64_t words, int32_t device,
+             int64_t *ones, double *device_ms) {
+    if (!ones) { set_error("bad argument"); return ES_E_BAD_ARG; }
+    return sim_run_host(num_pis, num_gates, kind, in0, in1, pi_words, words, device, nullptr, ones,
+                        device_ms);
 }
 
 // Device-resident variant for callers that own the buffers (torch tensors):

@@ -54,6 +54,28 @@ def test_config4_workload_shape():
     assert len(hs) == 1500
 
 
+def test_k2_program_shapes(round0):
+    """es_batch_k2_stats: -1 before prepare; afterwards every interpreter
+    program fits the launch-group rule of the runtime (<= 176 slots; over 88
+    slots, slot file + staged records fit two CTAs per SM at one word per
+    thread, unless uncofactored) and the table's gate counts match G."""
+    m, pairs = round0
+    nb = cones.NativeBatch(m, pairs[:300])
+    st = nb.k2_stats()
+    assert (st["num_slots"] == -1).all() and (st["num_records"] == -1).all()
+    nb.prepare()
+    st = nb.k2_stats()
+    tab = nb.table()
+    for i in range(len(nb)):
+        slots, recs, k = int(st["num_slots"][i]), int(st["num_records"][i]), int(st["cofactor_pis"][i])
+        assert slots >= tab["num_pis"][i] and 0 <= k <= 6
+        assert recs >= (tab["G"][i] > 0)  # gates + one OUT record per copy
+        if k > 0:
+            assert slots <= 176
+            assert slots <= 88 or slots * 512 + (recs + 1) * 16 <= 115600
+        assert tab["G"][i] == nb.info(i)["G"]
+
+
 def test_merges_collapse_nodes(round0):
     """A merge map (proven node -> earlier representative) is honoured like
     sweep.py:84-89: extracting (a, b) with the later node merged onto the

@@ -32,6 +32,22 @@ def test_simulate_golden(rows, gpu):
         assert round(float(sim.ones_fraction(vals).sum()), 9) == r["ones_sum"]
 
 
+def test_ones_and_features_golden(rows, gpu):
+    """es_sim_ones (popcount on the device) and stability_entropy vs the
+    reference's features.py:165-180 sums; per-node equality with the oracle."""
+    for r in rows:
+        x = recipes.build_sim(r)
+        pw = sim.random_pi_words(x.num_pis, r["words"], r["sim_seed"])
+        cnt = sim.ones_counts(x, pw)
+        assert cnt.dtype == np.int64 and sha(cnt.tobytes()) == r["ones_counts_sha"], r
+        stab, ent = sim.stability_entropy(x, r["words"], r["sim_seed"])
+        assert round(sum(stab), 9) == r["stability_sum"], r
+        assert round(sum(ent), 9) == r["entropy_sum"], r
+        if r["words"] <= 64:
+            ostab, oent = O.stability_entropy(x, pw)
+            assert stab == ostab and ent == oent
+
+
 def test_classes_golden(rows, gpu):
     for r in rows:
         x = recipes.build_sim(r)
