@@ -605,7 +605,7 @@ static int k2_target_ctas() {
 }
 
 static int k2_group_prepare(K2Group &gp, const es_prog *progs, const K2Prog *const *kps, Ctx *c,
-                            uint4 *stage) {
+                            uint4 *stage, cudaStream_t st) {
     const int T = 128;
     const std::vector<int> &group = gp.jobs_idx;
     int max_slots = 1;
@@ -687,7 +687,7 @@ static int k2_group_prepare(K2Group &gp, const es_prog *progs, const K2Prog *con
     const size_t jobs_b = (size_t)G * sizeof(K2Job);
     const size_t items_b = std::max<size_t>(gp.items.size(), 1) * sizeof(K2Item);
     const size_t best_b = (size_t)G * 8;
-    CK(cudaMallocAsync(&gp.d_buf, al(code_b) + al(jobs_b) + al(items_b) + al(best_b), c->stream));
+    CK(cudaMallocAsync(&gp.d_buf, al(code_b) + al(jobs_b) + al(items_b) + al(best_b), st));
     uint4 *d_code = (uint4 *)gp.d_buf;
     gp.d_jobs = (K2Job *)(gp.d_buf + al(code_b));
     gp.d_items = (K2Item *)(gp.d_buf + al(code_b) + al(jobs_b));
@@ -708,10 +708,15 @@ static int k2_group_prepare(K2Group &gp, const es_prog *progs, const K2Prog *con
             J.cof_mask |= 1ull << kps[j]->cof_pis[b];
         }
     }
-    CK(cudaMemcpyAsync(d_code, gp.code, gp.n_code * sizeof(uint4), cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(gp.d_jobs, gp.jobs.data(), jobs_b, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(gp.d_items, gp.items.data(), gp.items.size() * sizeof(K2Item), cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(gp.d_best, gp.h_best.data(), best_b, cudaMemcpyHostToDevice, c->stream));
+    return ES_OK;
+}
+
+// the group's image to the device (after k2_group_prepare, same stream)
+static int k2_group_upload(K2Group &gp, cudaStream_t st) {
+    CK(cudaMemcpyAsync((uint4 *)gp.d_buf, gp.code, gp.n_code * sizeof(uint4), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(gp.d_jobs, gp.jobs.data(), gp.jobs.size() * sizeof(K2Job), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(gp.d_items, gp.items.data(), gp.items.size() * sizeof(K2Item), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(gp.d_best, gp.h_best.data(), gp.h_best.size() * 8, cudaMemcpyHostToDevice, st));
     return ES_OK;
 }
 
@@ -821,28 +826,51 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
         CK(cudaMallocHost(&c->h_stage, cap * sizeof(uint4)));
         c->stage_cap = cap;
     }
-    size_t stage_off = 0;
-    for (K2Group &gp : groups) {  // host images + one upload phase
-        int rc = k2_group_prepare(gp, progs, kps, c, c->h_stage + stage_off);
-        if (rc != ES_OK) return rc;
-        stage_off += gp.n_code;
-    }
-    const double t1 = now_ms();
-    CK(cudaEventRecord(c->ev_start, c->stream));
     const bool sliced = deadline >= 0 || o.cancel_flag != nullptr;
     bool stopped = false;
     int stop_reason = 0;
     float dev_ms = 0;
-    if (!sliced) {
-        // all groups at once, one side stream each; device time = makespan
+    std::vector<size_t> stage_off(groups.size() + 1, 0);
+    for (size_t g = 0; g < groups.size(); ++g) {  // records of each group straight into pinned memory
+        size_t n = 0;
+        for (int j : groups[g].jobs_idx) n += kps[j]->gates.size();
+        stage_off[g + 1] = stage_off[g] + n;
+    }
+    double t1 = now_ms();
+    if (sliced) {  // host images + one upload phase, then slices
         for (size_t g = 0; g < groups.size(); ++g) {
-            CK(cudaStreamWaitEvent(c->side[g], c->ev_start, 0));
-            int rc = k2_group_launch(groups[g], c->side[g], c->d_counter + g, 0,
+            int rc = k2_group_prepare(groups[g], progs, kps, c, c->h_stage + stage_off[g], c->stream);
+            if (rc == ES_OK) rc = k2_group_upload(groups[g], c->stream);
+            if (rc != ES_OK) return rc;
+        }
+        t1 = now_ms();
+        CK(cudaEventRecord(c->ev_start, c->stream));
+    }
+    if (!sliced) {
+        // all groups at once, one side stream each, each launched as soon as
+        // its host image is ready, the largest programs first (their group is
+        // the long pole; the smaller groups' host work overlaps it); device
+        // time = makespan from the first upload
+        for (size_t gi = 0; gi < groups.size(); ++gi) {
+            const size_t g = groups.size() - 1 - gi;
+            int rc = k2_group_prepare(groups[g], progs, kps, c, c->h_stage + stage_off[g], c->stream);
+            if (rc != ES_OK) return rc;
+            if (gi == 0) {
+                t1 = now_ms();
+                CK(cudaEventRecord(c->ev_start, c->stream));
+            }
+            CK(cudaEventRecord(c->ev_side[g], c->stream));  // after the group's allocation
+            CK(cudaStreamWaitEvent(c->side[g], c->ev_side[g], 0));
+            rc = k2_group_upload(groups[g], c->side[g]);
+            if (rc != ES_OK) return rc;
+            rc = k2_group_launch(groups[g], c->side[g], c->d_counter + g, 0,
                                      groups[g].items.size(), c->sms);
             if (rc != ES_OK) return rc;
             CK(cudaEventRecord(c->ev_side[g], c->side[g]));
-            CK(cudaStreamWaitEvent(c->stream, c->ev_side[g], 0));
         }
+        // join only now: a join inside the loop would order the next group's
+        // allocation (on the main stream) after this group's kernel
+        for (size_t g = 0; g < groups.size(); ++g) CK(cudaStreamWaitEvent(c->stream, c->ev_side[g], 0));
         CK(cudaStreamSynchronize(c->stream));
         for (size_t g = 0; g < groups.size(); ++g) {
             float ms = 0;
