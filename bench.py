@@ -109,7 +109,30 @@ def measure_cones(steps: int, warmup: int, rank: int = 0, world: int = 1, count:
         wall_ms.append(1e3 * (time.perf_counter() - t))
         dev_ms.append(float(res["device_ms"].max()))
     work, eq, neq = cones_work(batch, res)
-    return {"jobs": len(batch), "eq": eq, "neq": neq, "gate_patterns": work,
+    # shared-memory roofline of the K2 interpreter (12 B per
+    # gate-word -- two operand loads and one store of a 32-pattern word):
+    # credited = the reference's gate-words, executed = the records the
+    # interpreter ran (cofactor copies, early exits), against the measured
+    # shared-memory load bandwidth
+    import numpy as np
+    from paper_2512_06627_b200 import shard
+
+    st = batch.k2_stats()
+    tab = batch.table()
+    ran = (res["reason"] != -1) & (res["engine"] == 2) & (st["num_records"] > 0)
+    kw = np.exp2(np.maximum(tab["num_pis"] - 5 - st["cofactor_pis"], 0).astype(np.float64))
+    frac_swept = res["patterns_swept"].astype(np.float64) / np.exp2(tab["num_pis"].astype(np.float64))
+    rec_words = float((st["num_records"] * kw * frac_swept)[ran].sum())
+    smem_bps, _ = shard.smem_peak(0)
+    dev_s = statistics.mean(dev_ms) * 1e-3
+    roof = {"bound": "smem", "unit": "GB/s", "peak": smem_bps / 1e9,
+            "peak_source": "measured: es_smem_peak (conflict-free 16-byte shared loads, all SMs)",
+            "achieved": work / 32 * 12 / dev_s / 1e9,
+            "executed": rec_words * 12 / dev_s / 1e9,
+            "bytes_per_gate_word": 12, "executed_record_words": rec_words}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["executed_frac"] = roof["executed"] / roof["peak"]
+    return {"jobs": len(batch), "eq": eq, "neq": neq, "gate_patterns": work, "roofline": roof,
             "device_ms": statistics.mean(dev_ms), "e2e_ms": statistics.mean(wall_ms),
             "extract_compile_ms": host_ms, "value": work / (statistics.mean(dev_ms) * 1e-3),
             "e2e_value": work / (statistics.mean(wall_ms) * 1e-3)}

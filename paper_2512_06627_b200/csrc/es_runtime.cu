@@ -278,6 +278,27 @@ __global__ void __launch_bounds__(256) es_alu_peak_kernel(unsigned *sink, int it
 
 int alu_peak(int dev, double *lane_ops_per_s, double *ms_out);
 
+// Shared-memory load bandwidth microbenchmark (the K2 interpreter's slot file
+// is a shared-memory bound): conflict-free 16-byte loads, 8
+// independent per thread per iteration, over a 16 KB tile per CTA.
+__global__ void __launch_bounds__(256) es_smem_peak_kernel(unsigned *sink, int iters) {
+    __shared__ __align__(16) uint4 tile[1024];
+    for (int q = threadIdx.x; q < 1024; q += blockDim.x) tile[q] = make_uint4(q, q * 3u, q * 5u, q * 7u);
+    __syncthreads();
+    const unsigned base = (unsigned)__cvta_generic_to_shared(tile);
+    unsigned x = 0, y = 0, z = 0, w = 0;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const unsigned addr = base + 16u * ((threadIdx.x + 128u * k + (unsigned)i) & 1023u);
+            unsigned a, b, c, d;
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(addr));
+            x ^= a; y ^= b; z ^= c; w ^= d;
+        }
+    }
+    if ((x ^ y ^ z ^ w) == 0x9E3779B9u) sink[0] = x;
+}
+
 // ---------------------------------------------------------------------------
 // per-thread, per-device context
 // ---------------------------------------------------------------------------
@@ -1296,6 +1317,26 @@ int alu_peak(int dev, double *lane_ops_per_s, double *ms_out) {
     CK(cudaEventElapsedTime(&ms, c->ev_start, c->ev_stop));
     const double ops = (double)grid * threads * (double)iters * 64.0;
     *lane_ops_per_s = ops / (ms * 1e-3);
+    if (ms_out) *ms_out = ms;
+    return ES_OK;
+}
+
+int smem_peak(int dev, double *bytes_per_s, double *ms_out) {
+    Ctx *c = nullptr;
+    int rc = get_ctx(dev, &c);
+    if (rc != ES_OK) return rc;
+    const int threads = 256, iters = 2048;
+    const int grid = c->sms * 8;
+    unsigned *sink = c->d_counter + 8;
+    es_smem_peak_kernel<<<grid, threads, 0, c->stream>>>(sink, 32);  // warm-up
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(c->ev_start, c->stream));
+    es_smem_peak_kernel<<<grid, threads, 0, c->stream>>>(sink, iters);
+    CK(cudaEventRecord(c->ev_stop, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, c->ev_start, c->ev_stop));
+    *bytes_per_s = (double)grid * threads * (double)iters * 8.0 * 16.0 / (ms * 1e-3);
     if (ms_out) *ms_out = ms;
     return ES_OK;
 }

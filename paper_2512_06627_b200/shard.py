@@ -152,6 +152,13 @@ def alu_peak(device: int = 0) -> tuple[float, float]:
     return v.value, ms.value
 
 
+def smem_peak(device: int = 0) -> tuple[float, float]:
+    """Measured shared-memory load bytes/s of the device (and the ms)."""
+    v, ms = ctypes.c_double(), ctypes.c_double()
+    N.check(N.lib().es_smem_peak(device, ctypes.byref(v), ctypes.byref(ms)))
+    return v.value, ms.value
+
+
 def es_check_sharded(sm, group=None, device: int | None = None,
                      slices: int | None = None, cofactor="throughput"):
     """``es_check`` (es.py:342-365) with the sweep sharded over ``group``."""
