@@ -123,6 +123,7 @@ typedef struct es_result {
     int32_t launches;           /* kernel launches issued */
     int32_t regs_per_thread;    /* JIT kernel register count */
     int32_t cofactor_pis;       /* K1 cofactor PIs used (0: none) */
+    int32_t jit_opt;            /* ptxas -O level of the K1 kernel (1: cold runs, 3: throughput) */
 } es_result;
 
 /*

@@ -66,7 +66,8 @@ class EsResult(ctypes.Structure):
                 ("patterns_swept", ctypes.c_uint64), ("compile_ms", ctypes.c_double),
                 ("jit_ms", ctypes.c_double), ("device_ms", ctypes.c_double),
                 ("wall_ms", ctypes.c_double), ("launches", ctypes.c_int32),
-                ("regs_per_thread", ctypes.c_int32), ("cofactor_pis", ctypes.c_int32)]
+                ("regs_per_thread", ctypes.c_int32), ("cofactor_pis", ctypes.c_int32),
+                ("jit_opt", ctypes.c_int32)]
 
 
 class NativeError(RuntimeError):

@@ -134,15 +134,20 @@ static uint64_t fnv1a(const std::string &s) {
     return h;
 }
 
+static int effective_opt(int opt) {
+    const char *e = getenv("ES_PTXAS_O");
+    return e ? atoi(e) : opt;
+}
+
 int ptx_to_cubin(const std::string &ptx, std::vector<char> *cubin, std::string *info,
-                 std::string *err) {
+                 std::string *err, int opt) {
     nvPTXCompilerHandle h = nullptr;
     if (nvPTXCompilerCreate(&h, ptx.size(), ptx.c_str()) != NVPTXCOMPILE_SUCCESS) {
         *err = "nvPTXCompilerCreate failed";
         return ES_E_CUDA;
     }
     std::vector<const char *> opts = {"--gpu-name=sm_100a", "--verbose"};
-    std::string olev = std::string("-O") + (getenv("ES_PTXAS_O") ? getenv("ES_PTXAS_O") : "3");
+    std::string olev = "-O" + std::to_string(effective_opt(opt));
     opts.push_back(olev.c_str());
     nvPTXCompileResult r = nvPTXCompilerCompile(h, (int)opts.size(), opts.data());
     size_t n = 0;
@@ -273,11 +278,13 @@ void disk_store(const std::string &dir, uint64_t key, const std::string &ptx, co
 }
 }  // namespace
 
-int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std::string *err) {
+int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std::string *err,
+            int opt) {
     std::string ptx;
     int region = 0;
     if (!splice_body(net, threads, &ptx, err, &region)) return ES_E_BAD_PROGRAM;
-    const uint64_t key = fnv1a(ptx) ^ (uint64_t)(uint32_t)threads;
+    opt = effective_opt(opt);
+    const uint64_t key = fnv1a(ptx) ^ (uint64_t)(uint32_t)threads ^ ((uint64_t)(opt & 7) << 56);
     {
         std::lock_guard<std::mutex> lk(g_jit_mu);
         auto it = g_cache.find(key);
@@ -292,7 +299,7 @@ int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std
     const uint64_t dkey = key ^ fnv1a(version) * 31u;
     const std::string dir = disk_cache_dir();
     if (!disk_load(dir, dkey, ptx, &cubin, &info)) {
-        int rc = ptx_to_cubin(ptx, &cubin, &info, err);
+        int rc = ptx_to_cubin(ptx, &cubin, &info, err, opt);
         if (rc != ES_OK) return rc;
         disk_store(dir, dkey, ptx, cubin, info);
     }
@@ -300,6 +307,7 @@ int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std
     k->threads = threads;
     k->block = threads == kK1TThreads ? 128 : threads;
     k->region_bytes = region;
+    k->opt = opt;
     parse_ptxas_info(info, &k->regs, &k->spill_bytes);
     cudaError_t e = cudaLibraryLoadData(&k->lib, cubin.data(), nullptr, nullptr, 0, nullptr,
                                         nullptr, 0);

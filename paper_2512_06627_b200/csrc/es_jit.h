@@ -19,6 +19,7 @@ struct JitKernel {
     int region_bytes = 0;   // K1T: shared bytes per warp
     int regs = -1;
     int spill_bytes = 0;
+    int opt = 3;            // ptxas optimisation level it was compiled at
     double jit_ms = 0;
 };
 
@@ -36,12 +37,15 @@ constexpr int kK1TThreads = -128;
 // The complete PTX for `net` at a block size of 128/256/512 threads, or K1U.
 bool splice_body(const LutNet &net, int threads, std::string *ptx, std::string *err,
                  int *region_bytes = nullptr);
-// PTX -> sm_100a cubin in process; `info` receives ptxas's verbose log.
+// PTX -> sm_100a cubin in process at ptxas -O<opt> (ES_PTXAS_O overrides);
+// `info` receives ptxas's verbose log.
 int ptx_to_cubin(const std::string &ptx, std::vector<char> *cubin, std::string *info,
-                 std::string *err);
+                 std::string *err, int opt = 3);
 void parse_ptxas_info(const std::string &info, int *regs, int *spill_bytes);
-// Cached compile + load.  Thread-safe.
-int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std::string *err);
+// Cached compile + load at ptxas -O<opt> (1: ~40 % less compile time, a few
+// % slower kernels -- for cold single runs; 3: default).  Thread-safe.
+int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std::string *err,
+            int opt = 3);
 void jit_clear();
 
 }  // namespace es

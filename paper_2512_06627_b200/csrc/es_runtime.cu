@@ -428,13 +428,13 @@ struct K1Plan {
 };
 
 int k1_prepare(const LutNet &net, int threads, int sms, K1Plan *pl, double *jit_ms,
-               JitKernel *cached = nullptr) {
+               JitKernel *cached = nullptr, int opt = 3) {
     std::string err;
     if (cached) {
         pl->jk = cached;
         *jit_ms = 0.0;
     } else {
-        int rc = jit_get(net, threads, &pl->jk, jit_ms, &err);
+        int rc = jit_get(net, threads, &pl->jk, jit_ms, &err, opt);
         if (rc != ES_OK) { set_error(err); return rc; }
     }
     pl->threads = pl->jk->block;
@@ -494,18 +494,19 @@ static int k1_slot(int threads) {
 }
 
 static int run_k1(const LutNet &net, int G, const es_run_opts &o, Ctx *c, double deadline,
-                  es_result *r, JitKernel **jk_cache) {
+                  es_result *r, JitKernel **jk_cache, int opt = 3) {
     NvtxRange nvtx("es_k1");
     const int threads = k1_threads(o, (int)net.cof_pis.size());
     K1Plan pl;
     double jit_ms = 0;
-    int rc = k1_prepare(net, threads, c->sms, &pl, &jit_ms, *jk_cache);
+    int rc = k1_prepare(net, threads, c->sms, &pl, &jit_ms, *jk_cache, opt);
     if (rc != ES_OK) return rc;
     *jk_cache = pl.jk;
     r->engine = ES_ENGINE_JIT;
     r->jit_ms = jit_ms;
     r->regs_per_thread = pl.jk->regs;
     r->cofactor_pis = pl.cof_n;
+    r->jit_opt = pl.jk->opt;
     const int P = net.num_pis;
     const uint64_t sentinel = 1ull << P;
     const uint64_t chunk_patterns = pl.patterns_per_chunk();
@@ -1044,35 +1045,63 @@ static double est_sweep_ms(const LutNet &n, int P, int sms) {
     return 1e3 * spill * (double)n.luts.size() * std::ldexp(1.0, std::max(P - 5 - k, 0)) /
            (1.9e13 * sms / 148.0);
 }
-static double est_jit_ms(const LutNet &n) { return 0.1 * (double)n.luts.size(); }
+// ptxas -O3 vs -O1 (mult16, round 1): compile 140 / 95 ms at k=0, 1,056 /
+// 578 ms at k=4; the -O1 kernels run 0.6-9 % slower
+static double est_jit_ms(const LutNet &n, int opt = 3) {
+    return (opt >= 3 ? 0.1 : 0.062) * (double)n.luts.size();
+}
+constexpr double kO1Slowdown = 1.07;
 
-static int choose_cofactors(MappedProg &mp, const es_run_opts &o, int sms) {
+// ptxas level for variant k: throughput mode always -O3; otherwise the level
+// with the smaller compile + expected sweep time (a kernel already compiled
+// at that level or higher costs nothing), so a cold single run compiles at
+// -O1 and a program that keeps being re-run tiers up to -O3.
+static int k1_opt(const MappedProg &mp, const LutNet &n, int k, int slot, int P, int sms, bool tput,
+                  double *cost) {
+    const double sweep = est_sweep_ms(n, P, sms);
+    if (tput) { *cost = sweep; return 3; }
+    const double reuse = 1.0 + mp.runs;  // doubling rule: expect as many more runs as so far
+    const JitKernel *have = mp.jk[k][slot];
+    int best = 3;
+    *cost = 1e300;
+    for (int opt : {3, 1}) {
+        const double jit = (have && have->opt >= opt) ? 0.0 : est_jit_ms(n, opt);
+        const double c = jit + sweep * reuse * (opt < 3 ? kO1Slowdown : 1.0);
+        if (c < *cost) { *cost = c; best = opt; }
+    }
+    return best;
+}
+
+static int choose_cofactors(MappedProg &mp, const es_run_opts &o, int sms, int *opt) {
     const int P = mp.dag.num_pis;
-    if (o.flags & (ES_FLAG_K1T | ES_FLAG_K1U)) return 0;
-    if (o.cofactor_pis == ES_COFACTOR_NONE) return 0;
+    const bool tput = o.cofactor_pis == ES_COFACTOR_THROUGHPUT;
+    double cost = 0;
+    auto fixed = [&](int k) {
+        const LutNet &n = mp.variant(k);
+        *opt = k1_opt(mp, n, k, k1_slot(k1_threads(o, k)), P, sms, tput, &cost);
+        return k;
+    };
+    if (o.flags & (ES_FLAG_K1T | ES_FLAG_K1U)) return fixed(0);
+    if (o.cofactor_pis == ES_COFACTOR_NONE) return fixed(0);
     if (o.cofactor_pis > 0) {  // forced: any k the word PIs allow
-        if (P - 5 < 1) return 0;
+        if (P - 5 < 1) return fixed(0);
         const LutNet &n = mp.variant(std::min(o.cofactor_pis, std::min(kMaxCofactorPis, P - 5)));
-        return (int)n.cof_pis.size();
+        return fixed((int)n.cof_pis.size());
     }
     // keep >= 2^14 kernel words so the grid still fills the GPU
     const int kmax = std::max(0, std::min(kMaxCofactorPis, P - 5 - 14));
-    if (kmax == 0) return 0;
-    const bool tput = o.cofactor_pis == ES_COFACTOR_THROUGHPUT;
+    if (kmax == 0) return fixed(0);
     const LutNet &net0 = mp.variant(0);
     const double sweep0 = est_sweep_ms(net0, P, sms);
     // latency mode: a short sweep is JIT-bound; don't even map the variants
-    if (!tput && sweep0 * (1 + mp.runs) < 0.1 * est_jit_ms(net0)) return 0;
-    const double reuse = 1.0 + mp.runs;  // doubling rule: expect as many more runs as so far
+    if (!tput && sweep0 * (1 + mp.runs) < 0.1 * est_jit_ms(net0)) return fixed(0);
     int best = 0;
     double best_cost = 1e300;
     for (int k = 0; k <= kmax; ++k) {
         const LutNet &n = mp.variant(k);
         if ((int)n.cof_pis.size() != k) break;  // fewer candidate PIs than k
-        const double sweep = est_sweep_ms(n, P, sms);
-        const int slot = k1_slot(k1_threads(o, k));
-        const double cost = tput ? sweep : (mp.jk[k][slot] ? 0.0 : est_jit_ms(n)) + sweep * reuse;
-        if (cost < best_cost) { best_cost = cost; best = k; }
+        const int ok = k1_opt(mp, n, k, k1_slot(k1_threads(o, k)), P, sms, tput, &cost);
+        if (cost < best_cost) { best_cost = cost; best = k; *opt = ok; }
     }
     return best;
 }
@@ -1137,12 +1166,15 @@ int run_one(const es_prog *prog, const es_run_opts *opts, es_result *out) {
     } else {
         std::lock_guard<std::mutex> lk(mp->mu);
         const double tc = now_ms();
-        const int k = choose_cofactors(*mp, o, c->sms);
+        int opt = 3;
+        const int k = choose_cofactors(*mp, o, c->sms, &opt);
         const int slot = k1_slot(k1_threads(o, k));
         const LutNet &kn = mp->variant(k);
         out->compile_ms += now_ms() - tc;
         out->num_luts = (int)kn.luts.size();
-        rc = run_k1(kn, G, o, c, deadline, out, &mp->jk[k][slot]);
+        // tier-up: recompile at the higher level (the old module stays in the JIT cache)
+        if (mp->jk[k][slot] && mp->jk[k][slot]->opt < opt) mp->jk[k][slot] = nullptr;
+        rc = run_k1(kn, G, o, c, deadline, out, &mp->jk[k][slot], opt);
         mp->runs++;
     }
     out->wall_ms = now_ms() - t0;
@@ -1173,14 +1205,15 @@ int run_batch_jit(int n_jobs, const es_prog *progs, const es_run_opts *opts, es_
             std::shared_ptr<MappedProg> mp;
             if (get_mapped(progs[i], &mp) != ES_OK) continue;
             std::lock_guard<std::mutex> lk(mp->mu);
-            const int k = choose_cofactors(*mp, o, sms);
+            int opt = 3;
+            const int k = choose_cofactors(*mp, o, sms, &opt);
             const LutNet &net = mp->variant(k);
             const int threads = k1_threads(o, k), slot = k1_slot(threads);
-            if (mp->jk[k][slot]) continue;
+            if (mp->jk[k][slot] && mp->jk[k][slot]->opt >= opt) continue;
             JitKernel *jk = nullptr;
             double ms = 0;
             std::string err;
-            if (jit_get(net, threads, &jk, &ms, &err) == ES_OK) mp->jk[k][slot] = jk;
+            if (jit_get(net, threads, &jk, &ms, &err, opt) == ES_OK) mp->jk[k][slot] = jk;
         }
     };
     const int nt = (int)std::min<unsigned>(std::max(1u, std::thread::hardware_concurrency()), (unsigned)n_jobs);
@@ -1253,15 +1286,17 @@ int session_open(const es_prog *prog, const es_run_opts *opts, void **out) {
     Session *s = new Session();
     s->dev = o.device;
     s->num_pis = prog->num_pis;
+    int opt = 3;
     {
         std::shared_ptr<MappedProg> mp;
         rc = get_mapped(*prog, &mp);
         if (rc != ES_OK) { delete s; return rc; }
         std::lock_guard<std::mutex> lk(mp->mu);
-        s->net = mp->variant(choose_cofactors(*mp, o, c->sms));
+        s->net = mp->variant(choose_cofactors(*mp, o, c->sms, &opt));
     }
     double jit_ms = 0;
-    rc = k1_prepare(s->net, k1_threads(o, (int)s->net.cof_pis.size()), c->sms, &s->plan, &jit_ms);
+    rc = k1_prepare(s->net, k1_threads(o, (int)s->net.cof_pis.size()), c->sms, &s->plan, &jit_ms,
+                    nullptr, opt);
     if (rc != ES_OK) { delete s; return rc; }
     if (cudaMalloc(&s->d_counter, 64) != cudaSuccess) { delete s; set_error("cudaMalloc"); return ES_E_CUDA; }
     *out = s;

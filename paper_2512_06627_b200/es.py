@@ -260,7 +260,8 @@ def _stats_of(r: N.EsResult) -> dict:
             "luts": int(r.num_luts), "patterns_swept": int(r.patterns_swept),
             "compile_ms": r.compile_ms, "jit_ms": r.jit_ms, "device_ms": r.device_ms,
             "engine_wall_ms": r.wall_ms, "launches": int(r.launches),
-            "regs_per_thread": int(r.regs_per_thread), "cofactor_pis": int(r.cofactor_pis)}
+            "regs_per_thread": int(r.regs_per_thread), "cofactor_pis": int(r.cofactor_pis),
+            "jit_opt": int(r.jit_opt)}
 
 
 def _to_esresult(r: N.EsResult, num_pis: int) -> EsResult:

@@ -46,3 +46,31 @@ def test_cache_off_and_corrupt_entries(tmp_path, gpu):
     assert r.returncode == 0, r.stderr[-2000:]
     got = json.loads(r.stdout.strip().splitlines()[-1])
     assert (got["verdict"], got["w"]) == (ref["verdict"], ref["w"])
+
+
+LEVELS = """
+import sys, json; sys.path.insert(0, %r)
+from paper_2512_06627_b200 import es, miter as M
+m = M.flip_gate(M.gen_multiplier_miter(10, "array", "booth"), 400)
+p = es.compile_program(m)
+out = []
+for cof in ("auto", "throughput", "none"):
+    r = es.run_exhaustive(p, engine="jit", cofactor=cof)
+    out.append([cof, r.stats["jit_opt"], r.verdict, r.witness_index])
+print(json.dumps(out))
+""" % ROOT
+
+
+@pytest.mark.gpu
+def test_cold_runs_compile_at_o1_throughput_at_o3(gpu):
+    """A cold latency-mode run is JIT-bound: ptxas -O1 (about 40 % less
+    compile time); throughput mode compiles at -O3.  Same verdict and
+    minimum-index witness either way."""
+    env = dict(os.environ, ES_JIT_CACHE="0")
+    env.pop("ES_PTXAS_O", None)
+    r = subprocess.run([sys.executable, "-c", LEVELS], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    runs = json.loads(r.stdout.strip().splitlines()[-1])
+    levels = {cof: opt for cof, opt, _, _ in runs}
+    assert levels["auto"] == 1 and levels["throughput"] == 3
+    assert len({(v, w) for _, _, v, w in runs}) == 1 and runs[0][2] == "COUNTEREXAMPLE"
