@@ -62,30 +62,41 @@ struct SimRec {
 };
 constexpr int kSimU = 16;  // measured (mult16, 65,536 words): 8 -> 0.57 ms, 16 -> 0.54, 32 -> 0.78
 
+// G threads per word (lanes of one warp): thread g of a word evaluates gates
+// g, g+G, ... of each batch, so G x more warps hide the latency of the
+// sequential level chain; __syncwarp orders a batch's row stores before the
+// next batch's loads (rows of one word are only touched by its G lanes).
+template <int G>
 __global__ void __launch_bounds__(256) es_sim_kernel(const SimRec *__restrict__ recs, int n_batches,
                                                      long long w_begin, long long w_end,
                                                      long long words,
                                                      unsigned long long *__restrict__ vals) {
-    const long long w = w_begin + (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (w >= w_end) return;
+    constexpr int U = kSimU / G;
+    const int gi = threadIdx.x % G;
+    const long long w = w_begin + ((long long)blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const bool active = w < w_end;
+    if (__all_sync(0xffffffffu, !active)) return;
     for (int bt = 0; bt < n_batches; ++bt) {
-        const SimRec *rb = recs + bt * kSimU;
-        unsigned long long x[kSimU], y[kSimU];
-        SimRec r[kSimU];
+        const SimRec *rb = recs + bt * kSimU + gi;
+        unsigned long long x[U], y[U];
+        SimRec r[U];
 #pragma unroll
-        for (int u = 0; u < kSimU; ++u) r[u] = rb[u];  // uniform: one broadcast per record
+        for (int u = 0; u < U; ++u) r[u] = rb[u * G];
+        if (active) {
 #pragma unroll
-        for (int u = 0; u < kSimU; ++u) {
-            x[u] = vals[(long long)r[u].a * words + w];
-            y[u] = vals[(long long)r[u].b * words + w];
+            for (int u = 0; u < U; ++u) {
+                x[u] = vals[(long long)r[u].a * words + w];
+                y[u] = vals[(long long)r[u].b * words + w];
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (r[u].f & 8u) continue;
+                const unsigned long long xa = (r[u].f & 2u) ? ~x[u] : x[u];
+                const unsigned long long yb = (r[u].f & 4u) ? ~y[u] : y[u];
+                vals[(long long)r[u].d * words + w] = (r[u].f & 1u) ? (xa ^ yb) : (xa & yb);
+            }
         }
-#pragma unroll
-        for (int u = 0; u < kSimU; ++u) {
-            if (r[u].f & 8u) continue;
-            const unsigned long long xa = (r[u].f & 2u) ? ~x[u] : x[u];
-            const unsigned long long yb = (r[u].f & 4u) ? ~y[u] : y[u];
-            vals[(long long)r[u].d * words + w] = (r[u].f & 1u) ? (xa ^ yb) : (xa & yb);
-        }
+        if (G > 1) __syncwarp();
     }
 }
 
@@ -229,8 +240,19 @@ int sim_enqueue(const SimProg &sp, const SimRec *d_recs, int num_pis, long long 
     tile = (tile + T - 1) / T * T;
     for (long long w0 = 0; w0 < words; w0 += tile) {
         const long long w1 = std::min(words, w0 + tile);
-        const long long grid = (w1 - w0 + T - 1) / T;
-        es_sim_kernel<<<(unsigned)grid, T, 0, st>>>(d_recs, (int)(sp.recs.size() / kSimU), w0, w1, words, d_vals);
+        // threads per word: the level chain is latency-bound, so small drives
+        // (the sweep's 64 words) take more lanes per word.  mult16, us, for
+        // G = 1/2/4/8: 64 words ~300/166/138/113; 8,192: -/-/202/182;
+        // 16,384: 375/272/227/309; 32,768: 390/317/372/-; 65,536: 535/584/720/-
+        const long long nw = w1 - w0;
+        int G = nw <= 8192 ? 8 : nw <= 16384 ? 4 : nw <= 32768 ? 2 : 1;
+        if (const char *e = getenv("ES_SIM_G")) G = atoi(e);
+        const long long grid = (nw * G + T - 1) / T;
+        const int nb = (int)(sp.recs.size() / kSimU);
+        if (G == 8) es_sim_kernel<8><<<(unsigned)grid, T, 0, st>>>(d_recs, nb, w0, w1, words, d_vals);
+        else if (G == 4) es_sim_kernel<4><<<(unsigned)grid, T, 0, st>>>(d_recs, nb, w0, w1, words, d_vals);
+        else if (G == 2) es_sim_kernel<2><<<(unsigned)grid, T, 0, st>>>(d_recs, nb, w0, w1, words, d_vals);
+        else es_sim_kernel<1><<<(unsigned)grid, T, 0, st>>>(d_recs, nb, w0, w1, words, d_vals);
         SCK(cudaGetLastError());
     }
     return ES_OK;

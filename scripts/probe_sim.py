@@ -4,7 +4,7 @@ sys.path.insert(0, '.')
 import numpy as np
 import torch
 from paper_2512_06627_b200 import miter as M, sim
-for words in (64, 4096, 1 << 16):
+for words in [int(a) for a in sys.argv[1:]] or (64, 4096, 1 << 16):
     m = M.gen_multiplier_miter(16, "array", "booth")
     nn = 1 + m.num_pis + len(m.gates)
     pw = sim.random_pi_words(m.num_pis, words, 1)
