@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <condition_variable>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -1195,39 +1196,58 @@ int run_batch_jit(int n_jobs, const es_prog *progs, const es_run_opts *opts, es_
     int sms = 0;
     if (cudaGetDeviceCount(&sms) != cudaSuccess || sms == 0) { set_error("no CUDA device visible"); return ES_E_NO_DEVICE; }
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, o.device));
+    // compile on worker threads; run each job on this thread as soon as its
+    // kernel is ready (in job order), so device sweeps overlap later compiles
     std::atomic<int> next{0};
+    std::vector<uint8_t> ready(n_jobs, 0);
+    std::mutex rmu;
+    std::condition_variable rcv;
+    auto mark = [&](int i) {
+        { std::lock_guard<std::mutex> lk(rmu); ready[i] = 1; }
+        rcv.notify_all();
+    };
     auto warm = [&]() {
-        if (cudaSetDevice(o.device) != cudaSuccess) return;
+        const bool dev_ok = cudaSetDevice(o.device) == cudaSuccess;
         for (;;) {
             const int i = next.fetch_add(1);
             if (i >= n_jobs) return;
-            if (validate(progs[i]) != ES_OK || progs[i].src0[progs[i].num_instrs - 1] < 0) continue;
-            std::shared_ptr<MappedProg> mp;
-            if (get_mapped(progs[i], &mp) != ES_OK) continue;
-            std::lock_guard<std::mutex> lk(mp->mu);
-            int opt = 3;
-            const int k = choose_cofactors(*mp, o, sms, &opt);
-            const LutNet &net = mp->variant(k);
-            const int threads = k1_threads(o, k), slot = k1_slot(threads);
-            if (mp->jk[k][slot] && mp->jk[k][slot]->opt >= opt) continue;
-            JitKernel *jk = nullptr;
-            double ms = 0;
-            std::string err;
-            if (jit_get(net, threads, &jk, &ms, &err, opt) == ES_OK) mp->jk[k][slot] = jk;
+            if (dev_ok && validate(progs[i]) == ES_OK && progs[i].src0[progs[i].num_instrs - 1] >= 0) {
+                std::shared_ptr<MappedProg> mp;
+                if (get_mapped(progs[i], &mp) == ES_OK) {
+                    std::lock_guard<std::mutex> lk(mp->mu);
+                    int opt = 3;
+                    const int k = choose_cofactors(*mp, o, sms, &opt);
+                    const LutNet &net = mp->variant(k);
+                    const int threads = k1_threads(o, k), slot = k1_slot(threads);
+                    if (!(mp->jk[k][slot] && mp->jk[k][slot]->opt >= opt)) {
+                        JitKernel *jk = nullptr;
+                        double ms = 0;
+                        std::string err;
+                        if (jit_get(net, threads, &jk, &ms, &err, opt) == ES_OK) mp->jk[k][slot] = jk;
+                    }
+                }
+            }
+            mark(i);  // failures surface in run_one
         }
     };
     const int nt = (int)std::min<unsigned>(std::max(1u, std::thread::hardware_concurrency()), (unsigned)n_jobs);
     std::vector<std::thread> th;
-    for (int q = 1; q < nt; ++q) th.emplace_back(warm);
-    warm();
-    for (auto &x : th) x.join();
-    for (int i = 0; i < n_jobs; ++i) {
+    for (int q = 0; q < nt; ++q) th.emplace_back(warm);
+    int rc = ES_OK;
+    for (int i = 0; i < n_jobs && rc == ES_OK; ++i) {
+        {
+            std::unique_lock<std::mutex> lk(rmu);
+            rcv.wait(lk, [&] { return ready[i] != 0; });
+        }
         es_run_opts oi = o;
         if (deadline >= 0) oi.budget_s = std::max(0.0, (deadline - now_ms()) * 1e-3);
-        const int rc = run_one(&progs[i], &oi, &outs[i]);
-        if (rc != ES_OK) return rc;
+        rc = run_one(&progs[i], &oi, &outs[i]);
     }
-    return ES_OK;
+    next.store(n_jobs);  // on an error, stop compiling what will not run
+    for (auto &x : th) x.join();
+    if (getenv("ES_VERBOSE"))
+        fprintf(stderr, "[es batch k1] jobs=%d compile threads=%d wall=%.2fms\n", n_jobs, nt, now_ms() - t0);
+    return rc;
 }
 
 int run_batch(int n_jobs, const es_prog *progs, const es_run_opts *opts, es_result *outs,
