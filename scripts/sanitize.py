@@ -17,3 +17,7 @@ print("batch", len(res), int((res["verdict"] == 1).sum()))
 pw = sim.random_pi_words(m.num_pis, 100, 0)
 assert sim.simulate(m, pw).shape[1] == 100
 print("classes", len(sim.pe_classes(m, pi_words=pw)))
+for words in (20_000, 40_000):  # K3 at 4 and 1 lanes per word (100 words: 8)
+    pw = sim.random_pi_words(m.num_pis, words, 1)
+    assert sim.simulate(m, pw).shape[1] == words
+print("ones", int(sim.ones_counts(m, pw).sum()))
