@@ -193,6 +193,11 @@ int32_t es_batch_extract(int32_t num_pis, int32_t num_gates, const uint8_t *kind
 /* Build the interpreter programs (cofactor depth, schedule) of every job that
  * lacks one; es_batch_run does it on demand, this lets callers time it. */
 int32_t es_batch_prepare(es_batch *b, int32_t n_threads);
+/* evaluate (eval.py:22-36): the single output of a packed XAG (as es_compile)
+ * on pattern `pattern` (PI i+1 = bit i, <= 64 PIs): returns 0 or 1, or an
+ * error code.  es_check's witness re-check (es.py:360-361). */
+int32_t es_xag_eval(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+                    const uint32_t *in1, uint32_t out_lit, uint64_t pattern);
 /* Per-job interpreter program shape after es_batch_prepare: slot-file rows,
  * records (gates + OUT records) and cofactor depth; -1 for unprepared jobs.
  * The runtime groups launches by slots (<=44: 4 words/thread, <=88: 2, else). */

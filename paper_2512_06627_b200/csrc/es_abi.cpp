@@ -419,6 +419,25 @@ int32_t es_batch_prepare(es_batch *bp, int32_t n_threads) {
     return rc;
 }
 
+int32_t es_xag_eval(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+                    const uint32_t *in1, uint32_t out_lit, uint64_t pattern) {
+    if (num_pis < 0 || num_pis > 64 || num_gates < 0 || (num_gates > 0 && (!kind || !in0 || !in1))) {
+        set_error("bad argument");
+        return ES_E_BAD_ARG;
+    }
+    const uint32_t nn = 1u + (uint32_t)num_pis + (uint32_t)num_gates;
+    std::vector<uint8_t> v(nn, 0);
+    for (int i = 0; i < num_pis; ++i) v[1 + i] = (pattern >> i) & 1;
+    for (int g = 0; g < num_gates; ++g) {
+        const uint32_t a = in0[g] >> 1, b = in1[g] >> 1;
+        if (a >= 1u + num_pis + g || b >= 1u + num_pis + g) { set_error("XAG not topological"); return ES_E_BAD_PROGRAM; }
+        const uint8_t x = v[a] ^ (in0[g] & 1), y = v[b] ^ (in1[g] & 1);
+        v[1 + num_pis + g] = kind[g] ? (x ^ y) : (x & y);
+    }
+    if ((out_lit >> 1) >= nn) { set_error("output literal out of range"); return ES_E_BAD_ARG; }
+    return v[out_lit >> 1] ^ (out_lit & 1);
+}
+
 int32_t es_batch_k2_stats(const es_batch *bp, int32_t *num_slots, int32_t *num_records,
                           int32_t *cofactor_pis) {
     const Batch *bt = (const Batch *)bp;

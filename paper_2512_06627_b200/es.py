@@ -302,6 +302,18 @@ def run_exhaustive(p, workers: int = 1, budget: float | None = None, cancel=None
     return _to_esresult(res, prog.num_pis)
 
 
+def _recheck(xag, witness) -> int:
+    """The witness re-check (es.py:360-361) natively (es_xag_eval); XAGs over
+    64 PIs (never ES-eligible) fall back to the direct evaluation."""
+    if xag.num_pis > 64 or len(xag.outputs) != 1:
+        return evaluate(xag, witness)
+    kind, in0, in1 = packed_gates(xag)
+    o = xag.outputs[0]
+    idx = sum(int(b) << i for i, b in enumerate(witness))
+    return N.check(N.lib().es_xag_eval(xag.num_pis, len(xag.gates), kind.ctypes.data, in0.ctypes.data,
+                                       in1.ctypes.data, o.node * 2 + int(o.neg), idx))
+
+
 def es_check(sm, workers: int = 1, budget: float | None = None, cancel=None, *,
              device: int = 0, engine: str = "auto", cofactor="auto") -> CheckResult:
     """Compile and sweep a sub-miter (es.py:342-365); witnesses are re-checked
@@ -318,7 +330,7 @@ def es_check(sm, workers: int = 1, budget: float | None = None, cancel=None, *,
     if r.verdict == EXHAUSTED_ZERO:
         return CheckResult(EQUIVALENT, engine="es", stats=stats)
     if r.verdict == ES_COUNTEREXAMPLE:
-        if evaluate(sm.circuit, r.witness) != 1:
+        if _recheck(sm.circuit, r.witness) != 1:
             raise AssertionError("exhaustive-simulation witness failed re-check")
         return CheckResult(COUNTEREXAMPLE, witness=r.witness, engine="es", stats=stats)
     reason = "cancelled" if (cancel is not None and cancel()) else "timeout"
@@ -362,7 +374,7 @@ def es_check_batch(sms: Iterable, budget: float | None = None, cancel=None, *,
         if r.verdict == EXHAUSTED_ZERO:
             results[i] = CheckResult(EQUIVALENT, engine="es", stats=stats)
         elif r.verdict == ES_COUNTEREXAMPLE:
-            if evaluate(sms[i].circuit, r.witness) != 1:
+            if _recheck(sms[i].circuit, r.witness) != 1:
                 raise AssertionError("exhaustive-simulation witness failed re-check")
             results[i] = CheckResult(COUNTEREXAMPLE, witness=r.witness, engine="es", stats=stats)
         else:

@@ -104,3 +104,20 @@ def test_programs_from_reference_objects_are_accepted():
         num_registers = p.num_registers
         num_pis = p.num_pis
     assert es.as_program(RefLike()) == p
+
+
+def test_native_witness_recheck_matches_evaluate():
+    """es_xag_eval (the es_check witness re-check, es.py:360-361) equals the
+    direct evaluation (eval.py:22-36) on random XAGs and patterns."""
+    import random as _r
+
+    from paper_2512_06627_b200 import es as _es
+    from paper_2512_06627_b200.miter import evaluate as _ev
+    from paper_2512_06627_b200.xag import random_xag as _rx
+
+    rng = _r.Random(7)
+    for k in range(60):
+        x = _rx(rng.randint(1, 40), rng.randint(0, 300), seed=k)
+        for _ in range(8):
+            bits = tuple(rng.randint(0, 1) for _ in range(x.num_pis))
+            assert _es._recheck(x, bits) == _ev(x, bits)
