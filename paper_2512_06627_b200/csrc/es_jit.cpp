@@ -149,6 +149,16 @@ int ptx_to_cubin(const std::string &ptx, std::vector<char> *cubin, std::string *
     std::vector<const char *> opts = {"--gpu-name=sm_100a", "--verbose"};
     std::string olev = "-O" + std::to_string(effective_opt(opt));
     opts.push_back(olev.c_str());
+    // experiments: extra ptxas options, space-separated (use with ES_JIT_CACHE=0)
+    std::vector<std::string> extra;
+    if (const char *e = getenv("ES_PTXAS_EXTRA")) {
+        std::string cur;
+        for (const char *c = e;; ++c) {
+            if (*c == ' ' || *c == 0) { if (!cur.empty()) extra.push_back(cur); cur.clear(); if (!*c) break; }
+            else cur += *c;
+        }
+    }
+    for (const std::string &x : extra) opts.push_back(x.c_str());
     nvPTXCompileResult r = nvPTXCompilerCompile(h, (int)opts.size(), opts.data());
     size_t n = 0;
     if (r != NVPTXCOMPILE_SUCCESS) {

@@ -48,7 +48,6 @@ void emit_k2(const Dag &dag, const Outs &outs, const std::vector<int> &order,
     const int N = dag.num_nodes(), FG = dag.first_gate(), P = dag.num_pis;
     auto is_gate = [&](int v) { return v >= FG && cone[v]; };
     kp->num_pis = P;
-    kp->prefetch_ok = true;
     kp->gates.clear();
     kp->n_gates = 0;
     kp->loads = kp->stores = 0;
@@ -106,7 +105,6 @@ void emit_k2(const Dag &dag, const Outs &outs, const std::vector<int> &order,
         else { g.a = (uint32_t)slot[fa]; kp->loads++; }
         g.b = (uint32_t)slot[fb];  // == last_gate only for AND(x, x): then x was stored
         kp->loads++;
-        if (fb == last_gate) kp->prefetch_ok = false;  // B is the slot the previous record stores
         if (dag.is_xor[gi]) { if (na ^ nb) ctl |= K2_NEG_A; }
         else { if (na) ctl |= K2_NEG_A; if (nb) ctl |= K2_NEG_B; }
         // consume fanins; a slot frees when its last reader has read it
@@ -305,7 +303,7 @@ void build_k2prog_auto(const Dag &dag, K2Prog *kp, int min_words_log2, int max_s
         // only if slots + staged records fit half an SM's shared memory
         // (2 x (smem + 1 KB reserve + statics) <= 228 KB); otherwise one 4-warp CTA, which
         // measured 12 % slower on config 4 than capping the depth
-        const size_t w1_smem = (size_t)q.num_slots * 128 * 4 + (q.gates.size() + 2) * 16;
+        const size_t w1_smem = (size_t)q.num_slots * 128 * 4 + (q.gates.size() + 1) * 16;
         const bool fits = q.num_slots <= max_slots && (q.num_slots <= 88 || w1_smem <= 115600);
         if (!fits && k != 0) continue;
         const double c = occupancy_cost(q, per_word[k]);

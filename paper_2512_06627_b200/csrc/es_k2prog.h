@@ -36,9 +36,6 @@ struct K2Prog {
     std::vector<int32_t> cof_pis;   // cofactor PIs (ascending); copies = 2^size
     int n_gates = 0;                // gate records (excluding OUT)
     int loads = 0, stores = 0;      // slot loads / stores per pass (cost model)
-    // no gate reads the previous gate's result through a slot (x op x), so
-    // the kernel may load record i+1's operands before record i stores
-    bool prefetch_ok = true;
 };
 
 // K2 program of a (possibly multi-output) graph: DFS schedule with

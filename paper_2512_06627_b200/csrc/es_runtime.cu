@@ -71,7 +71,6 @@ struct K2Job {
     unsigned valid_mask;
     int cof_n;
     unsigned char cof_pos[8];        // cofactor pattern bits (PI - 1), ascending
-    int prefetch;                    // operands of record i+1 may be loaded before record i stores
 };
 
 struct K2Item {
@@ -107,17 +106,6 @@ __device__ __forceinline__ uint4 lds_rec(unsigned addr) {
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(addr));
     return r;
-}
-
-// the slot operands of record c (as the record loop reads them)
-template <int W>
-__device__ __forceinline__ void k2_fetch(const uint4 &c, unsigned base, unsigned (&pa)[W], unsigned (&pb)[W]) {
-    if (c.w & K2_OUT) {
-        if (!(c.w & (K2_A_ACC | K2_CONST))) lds<W>(base + c.x, pa);
-    } else {
-        if (!(c.w & K2_A_ACC)) lds<W>(base + c.x, pa);
-        lds<W>(base + c.y, pb);
-    }
 }
 
 // pattern index of kernel word bits x with zero bits inserted at cof_pos[]
@@ -165,7 +153,7 @@ __global__ void __launch_bounds__(128) es_k2(const K2Job *__restrict__ jobs,
         if (k == kSkip) { __syncthreads(); continue; }
         const K2Item it = items[k];
         const K2Job job = jobs[it.job];
-        const int rec0 = smem_bytes / 16 - (job.n_recs + 2);
+        const int rec0 = smem_bytes / 16 - (job.n_recs + 1);
         prog_addr = smem_addr + 16u * (unsigned)rec0;
         if (it.job != cur_job) {  // stage the program records (uniform branch)
             const uint4 *src = reinterpret_cast<const uint4 *>(job.code);
@@ -196,95 +184,47 @@ __global__ void __launch_bounds__(128) es_k2(const K2Job *__restrict__ jobs,
             // accumulator or is loaded into it, B is a slot, the result stays
             // in the accumulator and is stored only if read later.  OUT: fold
             // the copy's output into (first failing word, copy) per word.
-            if (job.prefetch) {
-                // software pipeline: record i+1 and its slot operands load while
-                // record i computes (the host guarantees record i+1 never reads
-                // the slot record i stores: that value is the accumulator)
-                const unsigned n = (unsigned)job.n_recs;
-                uint4 cur = lds_rec(prog_addr), nxt = lds_rec(prog_addr + 16u);
-                unsigned pa[W], pb[W];
-#pragma unroll
-                for (int q = 0; q < W; ++q) { pa[q] = 0u; pb[q] = 0u; }
-                k2_fetch<W>(cur, base, pa, pb);
-                for (unsigned i = 0; i < n; ++i) {
-                    const uint4 c0 = cur;
-                    unsigned a_[W], b[W];
-#pragma unroll
-                    for (int q = 0; q < W; ++q) { a_[q] = pa[q]; b[q] = pb[q]; }
-                    cur = nxt;
-                    nxt = lds_rec(prog_addr + 16u * (i + 2u));  // <= 2 past the end: reserved
-                    if (i + 1u < n) k2_fetch<W>(cur, base, pa, pb);
-                    const unsigned ma = (c0.w & K2_NEG_A) ? ~0u : 0u;
-                    if (c0.w & K2_OUT) {
-                        unsigned v[W];
-#pragma unroll
-                        for (int q = 0; q < W; ++q)
-                            v[q] = (c0.w & K2_A_ACC) ? acc[q] : (c0.w & K2_CONST) ? 0u : a_[q];
-                        const unsigned copy = c0.w >> 16;
-#pragma unroll
-                        for (int q = 0; q < W; ++q) {
-                            const bool first = fw[q] == 0u;
-                            fw[q] = first ? (v[q] ^ ma) : fw[q];
-                            fc[q] = first ? copy : fc[q];
-                        }
-                        continue;
-                    }
-                    if (!(c0.w & K2_A_ACC)) {
-#pragma unroll
-                        for (int q = 0; q < W; ++q) acc[q] = a_[q];
-                    }
-                    if (c0.w & K2_XOR) {
-#pragma unroll
-                        for (int q = 0; q < W; ++q) acc[q] = acc[q] ^ b[q] ^ ma;
-                    } else {
-                        const unsigned mb = (c0.w & K2_NEG_B) ? ~0u : 0u;
-#pragma unroll
-                        for (int q = 0; q < W; ++q) acc[q] = (acc[q] ^ ma) & (b[q] ^ mb);
-                    }
-                    if (c0.w & K2_STORE) sts<W>(base + c0.z, acc);
-                }
-            } else {
-                uint4 r0 = lds_rec(prog_addr);
-                // unrolled 8x (measured: 1x 26.4 ms, 2x (ptxas default) 21.9,
-                // 4x 21.2, 8x 20.7, 16x 21.8 on config 4)
+            uint4 r0 = lds_rec(prog_addr);
+            // Unrolled 8x; this file is compiled with ptxas
+            // --register-usage-level=10 (build.py): config 4 20.0 ms (at the
+            // default level 5: 1x 26.4 ms, ptxas's own 2x 24.5, 8x 22.6).
 #pragma unroll 8
-                for (int i = 0; i < job.n_recs; ++i) {
-                    const uint4 c0 = r0;
-                    r0 = lds_rec(prog_addr + 16u * (unsigned)(i + 1));  // next record (past-end reads harmless)
-                    const unsigned ma = (c0.w & K2_NEG_A) ? ~0u : 0u;
-                    if (c0.w & K2_OUT) {
-                        unsigned v[W];
-                        if (c0.w & K2_A_ACC) {
-    #pragma unroll
-                            for (int q = 0; q < W; ++q) v[q] = acc[q];
-                        } else if (c0.w & K2_CONST) {
-    #pragma unroll
-                            for (int q = 0; q < W; ++q) v[q] = 0u;
-                        } else {
-                            lds<W>(base + c0.x, v);
-                        }
-                        const unsigned copy = c0.w >> 16;
-    #pragma unroll
-                        for (int q = 0; q < W; ++q) {
-                            const bool first = fw[q] == 0u;
-                            fw[q] = first ? (v[q] ^ ma) : fw[q];
-                            fc[q] = first ? copy : fc[q];
-                        }
-                        continue;
-                    }
-                    unsigned b[W];
-                    if (!(c0.w & K2_A_ACC)) lds<W>(base + c0.x, acc);
-                    lds<W>(base + c0.y, b);
-                    if (c0.w & K2_XOR) {
-    #pragma unroll
-                        for (int q = 0; q < W; ++q) acc[q] = acc[q] ^ b[q] ^ ma;
+            for (int i = 0; i < job.n_recs; ++i) {
+                const uint4 c0 = r0;
+                r0 = lds_rec(prog_addr + 16u * (unsigned)(i + 1));  // next record (past-end reads harmless)
+                const unsigned ma = (c0.w & K2_NEG_A) ? ~0u : 0u;
+                if (c0.w & K2_OUT) {
+                    unsigned v[W];
+                    if (c0.w & K2_A_ACC) {
+#pragma unroll
+                        for (int q = 0; q < W; ++q) v[q] = acc[q];
+                    } else if (c0.w & K2_CONST) {
+#pragma unroll
+                        for (int q = 0; q < W; ++q) v[q] = 0u;
                     } else {
-                        const unsigned mb = (c0.w & K2_NEG_B) ? ~0u : 0u;
-    #pragma unroll
-                        for (int q = 0; q < W; ++q) acc[q] = (acc[q] ^ ma) & (b[q] ^ mb);
+                        lds<W>(base + c0.x, v);
                     }
-                    if (c0.w & K2_STORE) sts<W>(base + c0.z, acc);
+                    const unsigned copy = c0.w >> 16;
+#pragma unroll
+                    for (int q = 0; q < W; ++q) {
+                        const bool first = fw[q] == 0u;
+                        fw[q] = first ? (v[q] ^ ma) : fw[q];
+                        fc[q] = first ? copy : fc[q];
+                    }
+                    continue;
                 }
+                unsigned b[W];
+                if (!(c0.w & K2_A_ACC)) lds<W>(base + c0.x, acc);
+                lds<W>(base + c0.y, b);
+                if (c0.w & K2_XOR) {
+#pragma unroll
+                    for (int q = 0; q < W; ++q) acc[q] = acc[q] ^ b[q] ^ ma;
+                } else {
+                    const unsigned mb = (c0.w & K2_NEG_B) ? ~0u : 0u;
+#pragma unroll
+                    for (int q = 0; q < W; ++q) acc[q] = (acc[q] ^ ma) & (b[q] ^ mb);
+                }
+                if (c0.w & K2_STORE) sts<W>(base + c0.z, acc);
             }
             unsigned any = 0;
 #pragma unroll
@@ -686,17 +626,6 @@ struct K2Group {
     int launches = 0;
 };
 
-// Operand-prefetch pipeline of the record loop: opt-in (ES_K2_PREFETCH=1).
-// Measured slower (config 4: 32.4 ms vs 21.9 ms).  Its presence in the
-// kernel is deliberate: with it compiled in, ptxas allocates 39-55 instead of
-// 32-40 registers and schedules the default loop ~10-20 % faster (same-box
-// A/B of both builds: config 4 24.5 -> 21.9 ms, mult12 0.70 -> 0.55 ms; with
-// the default loop unrolled 8x, 22.6 -> 20.7 ms and 0.64 -> 0.49 ms).
-static bool k2_prefetch_enabled() {
-    static const bool on = getenv("ES_K2_PREFETCH") != nullptr && atoi(getenv("ES_K2_PREFETCH")) != 0;
-    return on;
-}
-
 static int k2_target_ctas() {
     const char *e = getenv("ES_K2_CTAS");
     return e ? std::max(1, atoi(e)) : 2;
@@ -713,7 +642,7 @@ static int k2_group_prepare(K2Group &gp, const es_prog *progs, const K2Prog *con
     auto smem_for = [&](int W) {  // the largest job's slot file + records (kernel layout)
         size_t m = 16;
         for (int j : group)
-            m = std::max(m, (size_t)std::max(kps[j]->num_slots, 1) * T * W * 4 + (kps[j]->gates.size() + 2) * 16);
+            m = std::max(m, (size_t)std::max(kps[j]->num_slots, 1) * T * W * 4 + (kps[j]->gates.size() + 1) * 16);
         return m;
     };
     // widest W that keeps the target number of resident CTAs per SM, else
@@ -800,7 +729,6 @@ static int k2_group_prepare(K2Group &gp, const es_prog *progs, const K2Prog *con
         J.num_pis = progs[j].num_pis;
         J.valid_mask = lane_valid_mask(progs[j].num_pis);
         J.cof_n = (int)kps[j]->cof_pis.size();
-        J.prefetch = kps[j]->prefetch_ok && k2_prefetch_enabled();
         J.cof_mask = 0;
         for (int b = 0; b < J.cof_n; ++b) {
             J.cof_pos[b] = (unsigned char)(kps[j]->cof_pis[b] - 1);

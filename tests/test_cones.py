@@ -72,7 +72,7 @@ def test_k2_program_shapes(round0):
         assert recs >= (tab["G"][i] > 0)  # gates + one OUT record per copy
         if k > 0:
             assert slots <= 176
-            assert slots <= 88 or slots * 512 + (recs + 2) * 16 <= 115600
+            assert slots <= 88 or slots * 512 + (recs + 1) * 16 <= 115600
         assert tab["G"][i] == nb.info(i)["G"]
 
 
