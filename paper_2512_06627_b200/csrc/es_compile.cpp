@@ -460,6 +460,23 @@ void map_luts(const Dag &dag, LutNet *net) {
             });
             std::vector<int> alt = dfs(by_need);
             if (peak_of(alt) < peak_of(order)) order.swap(alt);
+            // visit the copies in bit-reversed order: logic shared by the copies
+            // that agree on a cofactor PI is then used by consecutive copies
+            // and dies early (mult16, k=4: peak live 358 -> 212 values, kernel
+            // 2.58 -> 2.32 ms, JIT 1.03 -> 0.74 s).  The OUT fold still runs in
+            // copy order (flush_outputs waits for copy 0).
+            const int C = (int)outs.size();
+            if ((C & (C - 1)) == 0) {
+                const int kb = __builtin_ctz((unsigned)C);
+                std::vector<int32_t> rev(C);
+                for (int c = 0; c < C; ++c) {
+                    int r = 0;
+                    for (int b = 0; b < kb; ++b) r |= ((c >> b) & 1) << (kb - 1 - b);
+                    rev[c] = outs[r];
+                }
+                std::vector<int> o2 = dfs(rev);
+                if (peak_of(o2) < peak_of(order)) order.swap(o2);
+            }
         }
         if (getenv("ES_LIST_SCHED")) {
             // experiment: greedy list scheduling, prefer the ready node that frees most
