@@ -89,7 +89,7 @@ typedef struct es_run_opts {
     double slice_ms;        /* target device time per launch slice (budget/cancel granularity) */
     int32_t block_threads;  /* 0: default */
     int32_t flags;          /* ES_FLAG_* */
-    int32_t cofactor_pis;   /* ES_COFACTOR_* or k = 1..4 (K1 only) */
+    int32_t cofactor_pis;   /* ES_COFACTOR_* or k = 1..5 (K1 only) */
 } es_run_opts;
 
 /*
@@ -310,7 +310,7 @@ int32_t es_k2_eval(const es_prog *prog, uint64_t w0, uint64_t nw, uint32_t *out_
  * (the fewest shared-memory wavefronts per word, <= 88 slots). */
 int32_t es_k2_eval_k(const es_prog *prog, int32_t k, uint64_t w0, uint64_t nw, uint32_t *out_words);
 int32_t es_k2_cofactor_pis(const es_prog *prog);
-/* The same views for the K1 variant with k cofactor PIs (0..4, chosen as
+/* The same views for the K1 variant with k cofactor PIs (0..5, chosen as
  * es_run does: the k word PIs of smallest transitive fanout).  es_map_eval_k
  * takes FULL word indices (cofactor PIs included) and returns the output of
  * the copy each word belongs to, so it is comparable with es_map_eval. */

@@ -59,7 +59,7 @@ int sim_classes(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const u
 // k = cofactor PIs (0: none), chosen as the runtime does (rank_cofactor_pis)
 static int map_prog(const es_prog *prog, LutNet *net, int k = 0) {
     if (!prog || prog->num_instrs < 1) { set_error("empty program"); return ES_E_BAD_PROGRAM; }
-    if (k < 0 || k > kMaxCofactorPis) { set_error("cofactor PIs must be 0..4"); return ES_E_BAD_ARG; }
+    if (k < 0 || k > kMaxCofactorPis) { set_error("cofactor PIs must be 0.." + std::to_string(kMaxCofactorPis)); return ES_E_BAD_ARG; }
     Dag dag;
     std::string err;
     int rc = build_dag(*prog, &dag, &err);
@@ -139,7 +139,7 @@ int32_t es_map_stats_k(const es_prog *prog, int32_t k, int32_t *num_luts, int32_
     if (peak_live) *peak_live = net.peak_live;
     if (num_gates) *num_gates = net.num_gates;
     if (cof_pis)
-        for (int i = 0; i < k; ++i) cof_pis[i] = net.cof_pis[i];
+        for (int i = 0; i < (int)net.cof_pis.size() && i < k; ++i) cof_pis[i] = net.cof_pis[i];
     return ES_OK;
 }
 

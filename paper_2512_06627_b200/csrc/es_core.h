@@ -111,7 +111,7 @@ void map_luts(const Dag &dag, LutNet *net);
 // logic outside it is shared by all copies (structural hashing).  One kernel
 // iteration then evaluates 2^k words -- one per assignment of the k cofactor
 // PIs -- for the price of the shared logic once plus the folded copies.
-constexpr int kMaxCofactorPis = 4;
+constexpr int kMaxCofactorPis = 5;
 // Rank word PIs (>= 6) by transitive-fanout size (cheapest first) and return
 // the first `k` of that order (rank order: sort before cofactor_expand).
 std::vector<int32_t> rank_cofactor_pis(const Dag &dag, int k);

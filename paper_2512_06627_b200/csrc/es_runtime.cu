@@ -48,7 +48,7 @@ struct K1Params {
     unsigned int one;
     unsigned int region_bytes;
     unsigned int cof_n;
-    unsigned int cof_pos[4];
+    unsigned int cof_pos[8];
 };
 
 // ---------------------------------------------------------------------------
@@ -418,7 +418,7 @@ struct K1Plan {
     int grid = 1;
     uint32_t valid = 0;
     int cof_n = 0;             // cofactor PIs: 2^cof_n words per iteration
-    unsigned cof_pos[4] = {0, 0, 0, 0};
+    unsigned cof_pos[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     // pattern index of the first pattern of chunk c (copy 0): the kernel's
     // es_expand on the host; monotone in c
     uint64_t first_pattern(uint64_t c) const {
@@ -446,7 +446,7 @@ int k1_prepare(const LutNet &net, int threads, int sms, K1Plan *pl, double *jit_
     pl->smem = threads == kK1TThreads ? (size_t)pl->jk->region_bytes * (pl->jk->block / 32) : 0;
     const int P = net.num_pis;
     pl->cof_n = (int)net.cof_pis.size();
-    if (pl->cof_n > 4 || (pl->cof_n > 0 && P - 5 - pl->cof_n < 0)) { set_error("bad cofactor set"); return ES_E_BAD_ARG; }
+    if (pl->cof_n > kMaxCofactorPis || (pl->cof_n > 0 && P - 5 - pl->cof_n < 0)) { set_error("bad cofactor set"); return ES_E_BAD_ARG; }
     for (int i = 0; i < pl->cof_n; ++i) pl->cof_pos[i] = (unsigned)(net.cof_pis[i] - 1);
     pl->total_words = 1ull << std::max(P - 5 - pl->cof_n, 0);
     int nb = 0;
@@ -477,7 +477,7 @@ int k1_launch(const K1Plan &pl, cudaStream_t st, unsigned long long *best, unsig
     kp.one = 1u;
     kp.region_bytes = (unsigned)pl.jk->region_bytes;
     kp.cof_n = (unsigned)pl.cof_n;
-    for (int i = 0; i < 4; ++i) kp.cof_pos[i] = pl.cof_pos[i];
+    for (int i = 0; i < 8; ++i) kp.cof_pos[i] = pl.cof_pos[i];
     CK(cudaMemsetAsync(counter, 0, sizeof(unsigned), st));
     void *args[] = {&kp};
     const int grid = (int)std::min<uint64_t>((uint64_t)pl.grid, std::max<uint64_t>(n_slots, 1));
@@ -1045,15 +1045,19 @@ static int validate(const es_prog &p) {
 // PTX->SASS per LUT for the JIT (mult16: 1,549 LUTs in 140 ms).
 static double est_sweep_ms(const LutNet &n, int P, int sms) {
     const int k = (int)n.cof_pis.size();
-    // beyond ~330 live values the kernel spills (255-register cap): ~10% at 358
-    const double spill = std::max(1.0, n.peak_live / 330.0);
+    // beyond ~330 live values the kernel spills (255-register cap); fitted on
+    // mult16: 358 live -> x1.12, 446 live (5 cofactor PIs) -> x2.6
+    const double over = std::max(0.0, n.peak_live - 330.0);
+    const double spill = 1.0 + 1.5e-4 * over * over;
     return 1e3 * spill * (double)n.luts.size() * std::ldexp(1.0, std::max(P - 5 - k, 0)) /
            (1.9e13 * sms / 148.0);
 }
-// ptxas -O3 vs -O1 (mult16, round 1): compile 140 / 95 ms at k=0, 1,056 /
-// 578 ms at k=4; the -O1 kernels run 0.6-9 % slower
+// ptxas time per LUT grows with register pressure (mult16 -O3: 0.09 ms/LUT
+// at 143 live values, 0.15 at 212, 0.53 at 446); -O1 compiles in ~60 % of
+// that (k=0: 95 vs 140 ms) for kernels 0.6-9 % slower
 static double est_jit_ms(const LutNet &n, int opt = 3) {
-    return (opt >= 3 ? 0.1 : 0.062) * (double)n.luts.size();
+    const double p = n.peak_live / 200.0;
+    return (opt >= 3 ? 0.09 : 0.056) * std::max(1.0, p * p) * (double)n.luts.size();
 }
 constexpr double kO1Slowdown = 1.07;
 

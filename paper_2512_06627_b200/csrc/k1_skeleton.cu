@@ -42,7 +42,7 @@ struct K1Params {
     unsigned int one;              // == 1, opaque to ptxas (IMAD coefficients)
     unsigned int region_bytes;     // K1T: shared bytes per warp (boundary super-words)
     unsigned int cof_n;            // cofactor PIs (2^cof_n copies per iteration)
-    unsigned int cof_pos[4];       // their pattern-bit positions (PI - 1), ascending
+    unsigned int cof_pos[8];       // their pattern-bit positions (PI - 1), ascending
 };
 
 #ifndef ES_MULTI
@@ -59,7 +59,7 @@ __device__ __forceinline__ unsigned long long es_expand(unsigned long long x, co
 #pragma unroll 1
     for (unsigned i = 0; i < n; ++i) {
         unsigned s;
-        asm volatile("mov.b32 %0, %1;" : "=r"(s) : "r"(p.cof_pos[i & 3]));
+        asm volatile("mov.b32 %0, %1;" : "=r"(s) : "r"(p.cof_pos[i & 7]));
         x = ((x >> s) << (s + 1)) | (x & ((1ull << s) - 1ull));
     }
     return x;

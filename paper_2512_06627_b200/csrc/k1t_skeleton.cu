@@ -33,7 +33,7 @@ struct K1Params {
     unsigned int one;              // == 1; opaque to ptxas (keeps the FMA-pipe extraction)
     unsigned int region_bytes;     // K1T: shared bytes per warp (boundary super-words)
     unsigned int cof_n;            // unused here (no cofactor copies)
-    unsigned int cof_pos[4];
+    unsigned int cof_pos[8];
 };
 
 extern "C" __global__ void __launch_bounds__(ES_THREADS)

@@ -236,8 +236,8 @@ def _cofactor_code(cofactor) -> int:
     if isinstance(cofactor, str):
         return N.COFACTOR_MODES[cofactor]
     k = int(cofactor)
-    if not 0 <= k <= 4:
-        raise ValueError("cofactor must be 'auto', 'none', 'throughput' or 0..4")
+    if not 0 <= k <= 5:
+        raise ValueError("cofactor must be 'auto', 'none', 'throughput' or 0..5")
     return N.COFACTOR_NONE if k == 0 else k
 
 
@@ -284,7 +284,7 @@ def run_exhaustive(p, workers: int = 1, budget: float | None = None, cancel=None
 
     ``cofactor`` (JIT engine): "auto" weighs JIT latency against sweep time
     (and tiers up when a program is re-run), "throughput" picks the fastest
-    sweep, "none" or 0 disables, 1..4 forces that many cofactor PIs.  The
+    sweep, "none" or 0 disables, 1..5 forces that many cofactor PIs.  The
     result is the same for every setting.
     """
     if workers < 1:
@@ -390,7 +390,7 @@ def map_stats(p, k: int = 0) -> dict:
     words), schedule peak live set, cone gates, the cofactor PIs."""
     prog = as_program(p)
     luts, live, gates = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
-    pis = (ctypes.c_int32 * 4)()
+    pis = (ctypes.c_int32 * 8)()
     N.check(N.lib().es_map_stats_k(ctypes.byref(prog.as_struct()), k, ctypes.byref(luts),
                                    ctypes.byref(live), ctypes.byref(gates), pis))
     return {"luts": luts.value, "peak_live": live.value, "gates": gates.value,
