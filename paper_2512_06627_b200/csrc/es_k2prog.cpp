@@ -283,13 +283,15 @@ void build_k2prog_auto(const Dag &dag, K2Prog *kp, int min_words_log2, int max_s
     for (size_t k = 0; k < order.size(); ++k) order[k] = (int)k;
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return per_word[a] < per_word[b]; });
     // The cheapest depth by gates may need > 88 slots, which the runtime runs
-    // at one CTA per SM (ncu, config 4: 23 % issue vs 42 % at two CTAs), so
-    // weigh occupancy: also try the next depths until one fits 88 slots and
-    // keep the lower effective cost.  Penalty 3.5 measured best on config 4
-    // (1.0: 28.7 ms, 1.8: 26.6, 2.5: 25.1, 3.5: 24.8, 6.0: 25.1).
-    static const double big_pen = getenv("ES_K2_BIGPEN") ? atof(getenv("ES_K2_BIGPEN")) : 3.5;
+    // at one word per thread (W=1, two CTAs per SM when it fits), so weigh
+    // occupancy: also try the next depths until one fits 88 slots and keep
+    // the lower effective cost.  Penalties re-measured on config 4 after the
+    // K2 tuning (big 1.5: 22.4 ms, 2: 21.3, 2.5: 19.1, 3: 20.0, 3.5: 20.0;
+    // mid 1.1 vs 1.25-1.6 within noise or worse).
+    static const double big_pen = getenv("ES_K2_BIGPEN") ? atof(getenv("ES_K2_BIGPEN")) : 2.5;
+    static const double mid_pen = getenv("ES_K2_MIDPEN") ? atof(getenv("ES_K2_MIDPEN")) : 1.1;
     auto occupancy_cost = [](const K2Prog &q, double pw) {
-        return pw * (q.num_slots > 88 ? big_pen : q.num_slots > 44 ? 1.1 : 1.0);
+        return pw * (q.num_slots > 88 ? big_pen : q.num_slots > 44 ? mid_pen : 1.0);
     };
     bool have = false;
     double best = 0;
