@@ -291,7 +291,8 @@ void build_k2prog_auto(const Dag &dag, K2Prog *kp, int min_words_log2, int max_s
     static const double big_pen = getenv("ES_K2_BIGPEN") ? atof(getenv("ES_K2_BIGPEN")) : 2.5;
     static const double mid_pen = getenv("ES_K2_MIDPEN") ? atof(getenv("ES_K2_MIDPEN")) : 1.1;
     auto occupancy_cost = [](const K2Prog &q, double pw) {
-        return pw * (q.num_slots > 88 ? big_pen : q.num_slots > 44 ? mid_pen : 1.0);
+        const int g = k2_group_of(q.num_slots, q.gates.size());
+        return pw * (g == 2 ? big_pen : g == 1 ? mid_pen : 1.0);
     };
     bool have = false;
     double best = 0;
@@ -306,7 +307,8 @@ void build_k2prog_auto(const Dag &dag, K2Prog *kp, int min_words_log2, int max_s
         // (2 x (smem + 1 KB reserve + statics) <= 228 KB); otherwise one 4-warp CTA, which
         // measured 12 % slower on config 4 than capping the depth
         const size_t w1_smem = (size_t)q.num_slots * 128 * 4 + (q.gates.size() + 1) * 16;
-        const bool fits = q.num_slots <= max_slots && (q.num_slots <= 88 || w1_smem <= 115600);
+        const bool fits = q.num_slots <= max_slots && (k2_group_of(q.num_slots, q.gates.size()) < 2 ||
+                                                       w1_smem <= kK2TwoCtaBytes);
         if (!fits && k != 0) continue;
         const double c = occupancy_cost(q, per_word[k]);
         if (!have || c < best) {
@@ -316,7 +318,7 @@ void build_k2prog_auto(const Dag &dag, K2Prog *kp, int min_words_log2, int max_s
             best = c;
             have = true;
         }
-        if (kp->num_slots <= 88 || builds >= 4 || k == 0) break;
+        if (k2_group_of(kp->num_slots, kp->gates.size()) < 2 || builds >= 4 || k == 0) break;
     }
 }
 

@@ -38,6 +38,17 @@ struct K2Prog {
     int loads = 0, stores = 0;      // slot loads / stores per pass (cost model)
 };
 
+// Launch group of a program: the widest words-per-thread W (4, 2, 1) at which
+// its slot file (slots x 128 threads x W x 4 B) plus its staged records fit
+// two CTAs per SM (2 x (bytes + 1 KB) <= 228 KB); 0 = W4, 1 = W2, 2 = W1.
+constexpr size_t kK2TwoCtaBytes = 115600;
+inline int k2_group_of(int num_slots, size_t num_records) {
+    const size_t rec = (num_records + 1) * 16, s = (size_t)(num_slots > 0 ? num_slots : 1) * 512;
+    if (s * 4 + rec <= kK2TwoCtaBytes) return 0;
+    if (s * 2 + rec <= kK2TwoCtaBytes) return 1;
+    return 2;
+}
+
 // K2 program of a (possibly multi-output) graph: DFS schedule with
 // accumulator forwarding, LIFO slot reuse, OUT records in copy order.
 void build_k2prog(const Dag &dag, K2Prog *kp);

@@ -836,7 +836,7 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
     std::vector<K2Group> groups(3);
     for (int j : active) {
         const int sl = kps[j]->num_slots;
-        groups[sl <= 44 ? 0 : sl <= 88 ? 1 : 2].jobs_idx.push_back(j);
+        groups[k2_group_of(sl, kps[j]->gates.size())].jobs_idx.push_back(j);
     }
     groups.erase(std::remove_if(groups.begin(), groups.end(),
                                 [](const K2Group &g) { return g.jobs_idx.empty(); }),
