@@ -43,3 +43,16 @@ def test_experimental_variants_compile(variant):
     p = es.compile_program(M.gen_multiplier_miter(12, "array", "wallace"))
     j = es.jit_check(p, block_threads=variant)
     assert j["cubin_bytes"] > 0 and j["spill_bytes"] == 0
+
+
+def test_throughput_kernel_mult16_k4_has_no_spills():
+    """The bench's kernel (mult16, 4 cofactor PIs, 256-thread CTAs): with the
+    copies visited in bit-reversed order the schedule's live set is ~212
+    values and ptxas fits it in 255 registers without spilling (the index
+    order needed 358 values and spilled ~1 KB per thread)."""
+    from paper_2512_06627_b200 import miter as M
+
+    p = es.compile_program(M.gen_multiplier_miter(16, "array", "booth"))
+    assert es.map_stats(p, 4)["peak_live"] <= 230
+    j = es.jit_check(p, block_threads=256, k=4)
+    assert j["spill_bytes"] == 0, j["log"]
