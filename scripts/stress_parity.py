@@ -4,7 +4,7 @@ deep patterns) and multiplier faults, checked on every engine / policy of
 the product path against the oracle's canonical minimum-index witness
 (oracle/es_oracle.c, workers=1 semantics).
 
-    python scripts/stress_parity.py [n_cases] [seed]
+    python scripts/stress_parity.py [n_cases] [seed] [min_pis max_pis max_gates]
 """
 import json
 import random
@@ -20,7 +20,7 @@ MODES = [("interp", "none"), ("interp", "auto"), ("interp", "throughput"),
          ("jit", "none"), ("jit", "auto"), ("jit", "throughput"), ("jit", 2), ("jit", 4)]
 
 
-def cases(n, seed):
+def cases(n, seed, lo=12, hi=27, max_gates=500):
     rng = random.Random(seed)
     for k in range(n):
         if k % 5 == 4:
@@ -28,8 +28,8 @@ def cases(n, seed):
             m = M.gen_multiplier_miter(w, "array", rng.choice(["booth", "wallace", "diagonal"]))
             yield f"mult{w}-flip", M.flip_gate(m, rng.randrange(len(m.gates)))
             continue
-        n_pis = rng.randint(12, 27)
-        x = random_xag(n_pis, rng.randint(40, 500), seed=seed * 100003 + k)
+        n_pis = rng.randint(lo, hi)
+        x = random_xag(n_pis, rng.randint(40, max_gates), seed=seed * 100003 + k)
         if not x.gates:
             continue
         # fault a gate near the output (so it usually reaches it), then gate
@@ -46,10 +46,11 @@ def cases(n, seed):
 def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 60
     seed = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+    lo, hi, mg = (int(a) for a in sys.argv[3:6]) if len(sys.argv) > 5 else (12, 27, 500)
     t0 = time.time()
     stats = {"cases": 0, "runs": 0, "eq": 0, "neq": 0, "mismatches": []}
-    for name, x in cases(n, seed):
-        if x.num_pis > 30:
+    for name, x in cases(n, seed, lo, hi, mg):
+        if x.num_pis > 40:
             continue
         ref_v, ref_w, _ = O.min_witness(O.compile_program(x))
         p = es.compile_program(x)
