@@ -1104,13 +1104,16 @@ static int choose_cofactors(MappedProg &mp, const es_run_opts &o, int sms, int *
     const double sweep0 = est_sweep_ms(net0, P, sms);
     // latency mode: a short sweep is JIT-bound; don't even map the variants
     if (!tput && sweep0 * (1 + mp.runs) < 0.1 * est_jit_ms(net0)) return fixed(0);
-    int best = 0;
+    int best = 0, worse = 0;
     double best_cost = 1e300;
     for (int k = 0; k <= kmax; ++k) {
         const LutNet &n = mp.variant(k);
         if ((int)n.cof_pis.size() != k) break;  // fewer candidate PIs than k
         const int ok = k1_opt(mp, n, k, k1_slot(k1_threads(o, k)), P, sms, tput, &cost);
-        if (cost < best_cost) { best_cost = cost; best = k; *opt = ok; }
+        if (cost < best_cost) { best_cost = cost; best = k; *opt = ok; worse = 0; }
+        // latency mode: the JIT term grows with k, so two deeper variants that
+        // do not pay end the search (mapping k=3..5 costs ~40 ms on mult16)
+        else if (!tput && ++worse >= 2) break;
     }
     return best;
 }
