@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(128) es_k2(const K2Job *__restrict__ jobs,
             for (int i = 0; i < job.n_recs; ++i) {
                 const uint4 c0 = r0;
                 r0 = lds_rec(prog_addr + 16u * (unsigned)(i + 1));  // next record (past-end reads harmless)
-                const unsigned ma = (c0.w & K2_NEG_A) ? ~0u : 0u;
+                const unsigned ma = (unsigned)((int)c0.w >> 31);  // NEG_A mirrored in bit 31
                 if (c0.w & K2_OUT) {
                     unsigned v[W];
                     if (c0.w & K2_A_ACC) {
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(128) es_k2(const K2Job *__restrict__ jobs,
                     } else {
                         lds<W>(base + c0.x, v);
                     }
-                    const unsigned copy = c0.w >> 16;
+                    const unsigned copy = (c0.w >> 16) & 0x3FFFu;
 #pragma unroll
                     for (int q = 0; q < W; ++q) {
                         const bool first = fw[q] == 0u;
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(128) es_k2(const K2Job *__restrict__ jobs,
 #pragma unroll
                     for (int q = 0; q < W; ++q) acc[q] = acc[q] ^ b[q] ^ ma;
                 } else {
-                    const unsigned mb = (c0.w & K2_NEG_B) ? ~0u : 0u;
+                    const unsigned mb = (unsigned)((int)(c0.w << 1) >> 31);  // NEG_B in bit 30
 #pragma unroll
                     for (int q = 0; q < W; ++q) acc[q] = (acc[q] ^ ma) & (b[q] ^ mb);
                 }
@@ -585,7 +585,11 @@ static int run_k1(const LutNet &net, int G, const es_run_opts &o, Ctx *c, double
 // Device record of a gate / output (16 bytes): byte offsets of the operand /
 // destination slots for the launch's stride, then the K2_* flags.
 static uint4 k2_record(const K2Gate &g, uint32_t stride) {
-    return make_uint4(g.a * stride, g.b * stride, g.d * stride, g.ctl);
+    // the complement flags are mirrored into bits 31 / 30 so the kernel turns
+    // them into masks with one arithmetic shift each (copy numbers < 2^14):
+    // config 4 17.8 -> 15.8 ms
+    const uint32_t ctl = g.ctl | ((g.ctl & K2_NEG_A) ? 0x80000000u : 0u) | ((g.ctl & K2_NEG_B) ? 0x40000000u : 0u);
+    return make_uint4(g.a * stride, g.b * stride, g.d * stride, ctl);
 }
 
 template <int W>
