@@ -124,6 +124,12 @@ typedef struct es_result {
     int32_t regs_per_thread;    /* JIT kernel register count */
     int32_t cofactor_pis;       /* K1 cofactor PIs used (0: none) */
     int32_t jit_opt;            /* ptxas -O level of the K1 kernel (1: cold runs, 3: throughput) */
+    int32_t witness_minimal;    /* COUNTEREXAMPLE: 1 = witness_index is the minimum failing pattern
+                                 * (always, except when a budget/cancel stop cut a cofactored sweep
+                                 * short before every smaller pattern was swept: then the witness is
+                                 * valid but may not be the minimum, and patterns_evaluated =
+                                 * patterns_swept) */
+    int32_t n_devices;          /* GPUs the sweep ran on */
 } es_result;
 
 /*

@@ -67,7 +67,8 @@ class EsResult(ctypes.Structure):
                 ("jit_ms", ctypes.c_double), ("device_ms", ctypes.c_double),
                 ("wall_ms", ctypes.c_double), ("launches", ctypes.c_int32),
                 ("regs_per_thread", ctypes.c_int32), ("cofactor_pis", ctypes.c_int32),
-                ("jit_opt", ctypes.c_int32)]
+                ("jit_opt", ctypes.c_int32), ("witness_minimal", ctypes.c_int32),
+                ("n_devices", ctypes.c_int32)]
 
 
 class NativeError(RuntimeError):

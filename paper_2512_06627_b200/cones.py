@@ -242,11 +242,7 @@ class NativeBatch:
 
         n = len(self)
         outs = (N.EsResult * n)()
-        if budget is not None and budget <= 0:
-            for i in range(n):
-                outs[i].verdict = 2
-                outs[i].reason = 1
-            return np.ctypeslib.as_array(outs)
+        # budget <= 0 is decided natively, after each job's constant-rail check
         with _CancelWatcher(cancel) as cw:
             opts = _opts(device, engine, budget, cw.address, 20.0, 0, cofactor=cofactor)
             N.check(N.lib().es_batch_run(self._h, ctypes.byref(opts), outs))

@@ -204,6 +204,7 @@ void parse_ptxas_info(const std::string &info, int *regs, int *spill_bytes) {
 namespace {
 std::mutex g_jit_mu;
 std::unordered_map<uint64_t, JitKernel *> g_cache;
+std::vector<JitKernel *> g_uncached;  // kernels whose key collided with a resident entry
 
 // On-disk cubin cache (the analogue of the reference's numba cache=True,
 // es.py:175): a program compiled by one process is loaded by the next
@@ -295,10 +296,14 @@ int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std
     if (!splice_body(net, threads, &ptx, err, &region)) return ES_E_BAD_PROGRAM;
     opt = effective_opt(opt);
     const uint64_t key = fnv1a(ptx) ^ (uint64_t)(uint32_t)threads ^ ((uint64_t)(opt & 7) << 56);
+    // the 64-bit key alone could collide: a hit must also match a second,
+    // independent hash and the length of the PTX
+    const uint64_t h2 = second_hash(ptx);
+    auto same = [&](const JitKernel *k) { return k->ptx_h2 == h2 && k->ptx_len == ptx.size(); };
     {
         std::lock_guard<std::mutex> lk(g_jit_mu);
         auto it = g_cache.find(key);
-        if (it != g_cache.end()) { *out = it->second; *jit_ms = 0.0; return ES_OK; }
+        if (it != g_cache.end() && same(it->second)) { *out = it->second; *jit_ms = 0.0; return ES_OK; }
     }
     // compile outside the lock: batches JIT many programs on parallel threads
     NvtxRange nvtx("es_jit");
@@ -318,6 +323,8 @@ int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std
     k->block = threads == kK1TThreads ? 128 : threads;
     k->region_bytes = region;
     k->opt = opt;
+    k->ptx_h2 = h2;
+    k->ptx_len = ptx.size();
     parse_ptxas_info(info, &k->regs, &k->spill_bytes);
     cudaError_t e = cudaLibraryLoadData(&k->lib, cubin.data(), nullptr, nullptr, 0, nullptr,
                                         nullptr, 0);
@@ -338,13 +345,14 @@ int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std
     k->jit_ms = *jit_ms;
     std::lock_guard<std::mutex> lk(g_jit_mu);
     auto it = g_cache.find(key);
-    if (it != g_cache.end()) {  // another thread won the race: keep its module
+    if (it != g_cache.end() && same(it->second)) {  // another thread won the race: keep its module
         cudaLibraryUnload(k->lib);
         delete k;
         *out = it->second;
         return ES_OK;
     }
-    g_cache[key] = k;
+    if (it != g_cache.end()) g_uncached.push_back(k);  // key collision: keep the resident entry
+    else g_cache[key] = k;
     *out = k;
     return ES_OK;
 }
@@ -356,6 +364,11 @@ void jit_clear() {
         delete kv.second;
     }
     g_cache.clear();
+    for (JitKernel *k : g_uncached) {
+        cudaLibraryUnload(k->lib);
+        delete k;
+    }
+    g_uncached.clear();
 }
 
 }  // namespace es

@@ -21,6 +21,8 @@ struct JitKernel {
     int spill_bytes = 0;
     int opt = 3;            // ptxas optimisation level it was compiled at
     double jit_ms = 0;
+    uint64_t ptx_h2 = 0;    // second hash + length of the PTX: cache-hit check
+    size_t ptx_len = 0;
 };
 
 inline double now_ms() {

@@ -49,6 +49,16 @@ inline int k2_group_of(int num_slots, size_t num_records) {
     return 2;
 }
 
+// Whether the interpreter can run a program at all: its slot file at one word
+// per thread plus its staged records (and the kernel's 16 static bytes) in
+// one CTA's dynamic shared memory (B200 opt-in maximum, 227 KB).  Programs
+// that do not fit go to K1 (es_runtime.cu routes them).
+constexpr size_t kK2MaxSmemBytes = 232448 - 64;
+inline size_t k2_smem_w1(int num_slots, size_t num_records) {
+    return (size_t)(num_slots > 0 ? num_slots : 1) * 512 + (num_records + 1) * 16;
+}
+inline bool k2_fits(const K2Prog &kp) { return k2_smem_w1(kp.num_slots, kp.gates.size()) <= kK2MaxSmemBytes; }
+
 // K2 program of a (possibly multi-output) graph: DFS schedule with
 // accumulator forwarding, LIFO slot reuse, OUT records in copy order.
 void build_k2prog(const Dag &dag, K2Prog *kp);

@@ -563,8 +563,13 @@ static int run_k1(const LutNet &net, int G, const es_run_opts &o, Ctx *c, double
     if (best < sentinel) {
         r->verdict = ES_COUNTEREXAMPLE;
         r->witness_index = best;
-        r->patterns_evaluated = ref_patterns_for_hit(best, P);
         r->patterns_swept = std::min<uint64_t>(completed_chunks * chunk_patterns, sentinel);
+        // minimum only if every chunk that could hold a smaller pattern was swept:
+        // always for a finished sweep; a budget/cancel stop of a cofactored sweep
+        // (chunks interleave high pattern bits) may leave smaller ones unswept
+        const bool minimal = completed_chunks >= pl.n_chunks || best < pl.first_pattern(completed_chunks);
+        r->witness_minimal = minimal ? 1 : 0;
+        r->patterns_evaluated = minimal ? ref_patterns_for_hit(best, P) : r->patterns_swept;
     } else if (stopped) {
         r->verdict = ES_BUDGET_EXCEEDED;
         r->reason = stop_reason;
@@ -762,6 +767,16 @@ static int k2_group_launch(K2Group &gp, cudaStream_t st, unsigned *counter, uint
     return rc;
 }
 
+// first pattern (copy 0) of kernel word w of a job: k2_expand on the host
+static uint64_t k2_expand_host(uint64_t w, const K2Job &job) {
+    uint64_t x = w << 5;
+    for (int i = 0; i < job.cof_n; ++i) {
+        const unsigned s = job.cof_pos[i];
+        x = ((x >> s) << (s + 1)) | (x & ((1ull << s) - 1ull));
+    }
+    return x;
+}
+
 static void k2_group_results(const K2Group &gp, const es_prog *progs, const K2Prog *const *kps,
                              bool stopped, int stop_reason, es_result *outs) {
     const int G = (int)gp.jobs_idx.size();
@@ -783,8 +798,14 @@ static void k2_group_results(const K2Group &gp, const es_prog *progs, const K2Pr
         if (gp.h_best[q] < sentinel) {
             r->verdict = ES_COUNTEREXAMPLE;
             r->witness_index = gp.h_best[q];
-            r->patterns_evaluated = ref_patterns_for_hit(gp.h_best[q], P);
             r->patterns_swept = std::min<uint64_t>(covered * item_patterns, sentinel);
+            // a job's completed items are a prefix of its items (round-robin
+            // order); the witness is the minimum unless a stop left an item
+            // whose first pattern lies below it (cofactor bits above the item)
+            const bool minimal = covered >= gp.n_items[q] ||
+                                 gp.h_best[q] < k2_expand_host(covered * gp.item_words[q], gp.jobs[q]);
+            r->witness_minimal = minimal ? 1 : 0;
+            r->patterns_evaluated = minimal ? ref_patterns_for_hit(gp.h_best[q], P) : r->patterns_swept;
         } else if (stopped && covered < gp.n_items[q]) {
             r->verdict = ES_BUDGET_EXCEEDED;
             r->reason = stop_reason;
@@ -798,9 +819,9 @@ static void k2_group_results(const K2Group &gp, const es_prog *progs, const K2Pr
     }
 }
 
-static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &active,
+static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &active_in,
                   const es_run_opts &o, Ctx *c, double deadline, es_result *outs,
-                  const K2Prog *const *prebuilt = nullptr) {
+                  const K2Prog *const *prebuilt = nullptr, std::vector<int> *unfit = nullptr) {
     NvtxRange nvtx("es_k2");
     // host: K2 programs (schedule, accumulator forwarding), in parallel --
     // unless the caller built them already (sub-miter batches do at extraction)
@@ -813,8 +834,8 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
         auto work = [&]() {
             for (;;) {
                 const size_t q = next.fetch_add(1);
-                if (q >= active.size()) return;
-                const int j = active[q];
+                if (q >= active_in.size()) return;
+                const int j = active_in[q];
                 Dag dag;
                 std::string err;
                 if (build_dag(progs[j], &dag, &err) != ES_OK) { bad[j] = 1; continue; }
@@ -822,20 +843,34 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
             }
         };
         const int nt = (int)std::min<size_t>(std::max(1u, std::thread::hardware_concurrency()),
-                                             std::max<size_t>(1, active.size() / 64));
+                                             std::max<size_t>(1, active_in.size() / 64));
         std::vector<std::thread> th;
         for (int q = 1; q < nt; ++q) th.emplace_back(work);
         work();
         for (auto &x : th) x.join();
     }
-    for (int j : active)
+    for (int j : active_in)
         if (bad[j]) { set_error("malformed program in batch (job " + std::to_string(j) + ")"); return ES_E_BAD_PROGRAM; }
     std::vector<const K2Prog *> own_ptr;
     if (!prebuilt) {
         own_ptr.resize(n_jobs, nullptr);
-        for (int j : active) own_ptr[j] = &own[j];
+        for (int j : active_in) own_ptr[j] = &own[j];
     }
     const K2Prog *const *kps = prebuilt ? prebuilt : own_ptr.data();
+    // programs whose slot file cannot fit one CTA's shared memory: handed back
+    // to the caller for K1 (or an error when the caller forced the interpreter)
+    std::vector<int> active;
+    active.reserve(active_in.size());
+    for (int j : active_in) {
+        if (k2_fits(*kps[j])) { active.push_back(j); continue; }
+        if (!unfit) {
+            set_error("program needs " + std::to_string(kps[j]->num_slots) +
+                      " slots: too many for the K2 interpreter (job " + std::to_string(j) + ")");
+            return ES_E_BAD_PROGRAM;
+        }
+        unfit->push_back(j);
+    }
+    if (active.empty()) return ES_OK;
     // launch groups by slot count: small programs get 4 words per thread
     std::vector<K2Group> groups(3);
     for (int j : active) {
@@ -952,6 +987,7 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
 // Mapped programs cached by a hash of the program arrays: a warm call skips
 // graph rebuild, mapping, PTX emission and the JIT-cache lookup.
 struct MappedProg {
+    std::vector<uint8_t> sig;        // the program arrays: a cache hit must match them exactly
     Dag dag;
     LutNet net;                      // no cofactors (mapped on demand: variant(0))
     bool net_ready = false;
@@ -996,21 +1032,35 @@ static uint64_t prog_hash(const es_prog &p) {
     return h;
 }
 
+// all program arrays, concatenated (the exact identity behind the hash key)
+static std::vector<uint8_t> prog_sig(const es_prog &p) {
+    const size_t n = (size_t)p.num_instrs;
+    std::vector<uint8_t> v(12 + n * 19);
+    uint8_t *d = v.data();
+    auto put = [&](const void *s, size_t b) { std::memcpy(d, s, b); d += b; };
+    put(&p.num_instrs, 4); put(&p.num_registers, 4); put(&p.num_pis, 4);
+    put(p.op, n); put(p.dst, 4 * n); put(p.src0, 4 * n); put(p.neg0, n);
+    put(p.src1, 4 * n); put(p.neg1, n); put(p.pi, 4 * n);
+    return v;
+}
+
 static std::mutex g_mapped_mu;
 static std::vector<std::pair<uint64_t, std::shared_ptr<MappedProg>>> g_mapped;
 
 static int get_mapped(const es_prog &p, std::shared_ptr<MappedProg> *out) {
     const uint64_t key = prog_hash(p);
+    std::vector<uint8_t> sig = prog_sig(p);
     {
         std::lock_guard<std::mutex> lk(g_mapped_mu);
-        for (auto &kv : g_mapped)
-            if (kv.first == key) { *out = kv.second; return ES_OK; }
+        for (auto &kv : g_mapped)  // hash hit + identical arrays (no collision risk)
+            if (kv.first == key && kv.second->sig == sig) { *out = kv.second; return ES_OK; }
     }
     Dag dag;
     std::string err;
     int rc = build_dag(p, &dag, &err);
     if (rc != ES_OK) { set_error(err); return rc; }
     auto mp = std::make_shared<MappedProg>();
+    mp->sig = std::move(sig);
     mp->dag = std::move(dag);
     for (int i = 0; i < p.num_instrs; ++i) mp->G += (p.op[i] == ES_OP_AND || p.op[i] == ES_OP_XOR);
     std::lock_guard<std::mutex> lk(g_mapped_mu);
@@ -1027,6 +1077,7 @@ static bool constant_rail(const es_prog &p, es_result *r) {
     if (p.neg0[last]) {
         r->verdict = ES_COUNTEREXAMPLE;
         r->witness_index = 0;
+        r->witness_minimal = 1;
         r->patterns_evaluated = 0;
     } else {
         r->verdict = ES_EXHAUSTED_ZERO;
@@ -1157,6 +1208,7 @@ int run_one(const es_prog *prog, const es_run_opts *opts, es_result *out) {
         std::vector<int> act{0};
         const K2Prog *kp;
         std::shared_ptr<K2Prog> hold;  // a concurrent tier-up may replace mp->k2
+        bool unfit = false;
         {
             std::lock_guard<std::mutex> lk(mp->mu);
             const double tc = now_ms();
@@ -1177,9 +1229,20 @@ int run_one(const es_prog *prog, const es_run_opts *opts, es_result *out) {
             hold = mp->k2;
             kp = hold.get();
             out->compile_ms += now_ms() - tc;
+            unfit = !k2_fits(*kp);
         }
-        rc = run_k2(1, prog, act, o, c, deadline, out, &kp);
-    } else {
+        if (!unfit) {
+            rc = run_k2(1, prog, act, o, c, deadline, out, &kp);
+        } else if (o.engine == ES_ENGINE_INTERP) {
+            set_error("program needs " + std::to_string(kp->num_slots) + " slots (" +
+                      std::to_string(k2_smem_w1(kp->num_slots, kp->gates.size())) +
+                      " B of shared memory): too many for the K2 interpreter; use engine auto or jit");
+            return ES_E_BAD_PROGRAM;
+        } else {
+            engine = ES_ENGINE_JIT;  // auto: the live set is too wide for shared memory -> registers (K1)
+        }
+    }
+    if (engine == ES_ENGINE_JIT) {
         std::lock_guard<std::mutex> lk(mp->mu);
         const double tc = now_ms();
         int opt = 3;
@@ -1288,7 +1351,16 @@ int run_batch(int n_jobs, const es_prog *progs, const es_run_opts *opts, es_resu
         for (int j : active) { outs[j].verdict = ES_BUDGET_EXCEEDED; outs[j].reason = reason; }
         return ES_OK;
     }
-    rc = run_k2(n_jobs, progs, active, o, c, deadline, outs, prebuilt);
+    std::vector<int> unfit;
+    rc = run_k2(n_jobs, progs, active, o, c, deadline, outs, prebuilt,
+                o.engine == ES_ENGINE_INTERP ? nullptr : &unfit);
+    // live sets too wide for the interpreter's shared memory run on K1
+    for (size_t q = 0; q < unfit.size() && rc == ES_OK; ++q) {
+        es_run_opts oj = o;
+        oj.engine = ES_ENGINE_JIT;
+        if (deadline >= 0) oj.budget_s = std::max(0.0, (deadline - now_ms()) * 1e-3);
+        rc = run_one(&progs[unfit[q]], &oj, &outs[unfit[q]]);
+    }
     const double wall = now_ms() - t0;
     for (int j = 0; j < n_jobs; ++j) outs[j].wall_ms = wall;
     return rc;

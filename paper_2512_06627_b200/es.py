@@ -261,7 +261,8 @@ def _stats_of(r: N.EsResult) -> dict:
             "compile_ms": r.compile_ms, "jit_ms": r.jit_ms, "device_ms": r.device_ms,
             "engine_wall_ms": r.wall_ms, "launches": int(r.launches),
             "regs_per_thread": int(r.regs_per_thread), "cofactor_pis": int(r.cofactor_pis),
-            "jit_opt": int(r.jit_opt)}
+            "jit_opt": int(r.jit_opt), "witness_minimal": bool(r.witness_minimal),
+            "n_devices": int(r.n_devices)}
 
 
 def _to_esresult(r: N.EsResult, num_pis: int) -> EsResult:
@@ -290,10 +291,13 @@ def run_exhaustive(p, workers: int = 1, budget: float | None = None, cancel=None
     if workers < 1:
         raise ValueError("workers must be >= 1")
     prog = as_program(p)
-    if budget is not None and budget <= 0:  # deadline passes before the first batch
-        return EsResult(BUDGET_EXCEEDED, patterns_evaluated=0)
-    if cancel is not None and cancel():
-        return EsResult(BUDGET_EXCEEDED, patterns_evaluated=0)
+    # a constant output is decided before the budget is looked at (es.py:265-270);
+    # otherwise a spent budget or a raised cancel stops before the first batch
+    if prog.src0[-1] >= 0:
+        if budget is not None and budget <= 0:
+            return EsResult(BUDGET_EXCEEDED, patterns_evaluated=0)
+        if cancel is not None and cancel():
+            return EsResult(BUDGET_EXCEEDED, patterns_evaluated=0)
     res = N.EsResult()
     with _CancelWatcher(cancel) as cw:
         opts = _opts(device, engine, budget, cw.address, slice_ms, block_threads, variant, cofactor)
@@ -343,12 +347,12 @@ def run_exhaustive_batch(progs: Sequence, budget: float | None = None, cancel=No
     ps = [as_program(p) for p in progs]
     if not ps:
         return []
-    if budget is not None and budget <= 0:
-        return [EsResult(BUDGET_EXCEEDED) for _ in ps]
+    # budget <= 0 is decided natively, after each job's constant-rail check (es.py:265-270)
     arr = (N.EsProg * len(ps))(*[p.as_struct() for p in ps])
     outs = (N.EsResult * len(ps))()
     with _CancelWatcher(cancel) as cw:
-        opts = _opts(device, "interp", budget, cw.address, 20.0, 0)
+        # "auto": programs too wide for the interpreter's shared memory run on K1
+        opts = _opts(device, "auto", budget, cw.address, 20.0, 0)
         N.check(N.lib().es_run_batch(len(ps), arr, ctypes.byref(opts), outs))
     return [_to_esresult(outs[i], ps[i].num_pis) for i in range(len(ps))]
 
