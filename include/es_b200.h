@@ -82,7 +82,7 @@ typedef struct es_prog {
 
 /* Options of one run (run_exhaustive's workers/budget/cancel, es.py:252-253). */
 typedef struct es_run_opts {
-    int32_t device;         /* CUDA ordinal */
+    int32_t device;         /* CUDA ordinal (when n_devices == 0) */
     int32_t engine;         /* ES_ENGINE_* */
     double budget_s;        /* < 0: none; 0.0 -> BUDGET_EXCEEDED before any work */
     const volatile int32_t *cancel_flag; /* host flag polled between slices; may be NULL */
@@ -90,6 +90,9 @@ typedef struct es_run_opts {
     int32_t block_threads;  /* 0: default */
     int32_t flags;          /* ES_FLAG_* */
     int32_t cofactor_pis;   /* ES_COFACTOR_* or k = 1..5 (K1 only) */
+    int32_t n_devices;      /* > 0: sweep on devices[0..n_devices) (one host thread each; an
+                             * ordinal may repeat); 0: on `device` only */
+    const int32_t *devices;
 } es_run_opts;
 
 /*
@@ -103,9 +106,7 @@ typedef struct es_run_opts {
 #define ES_COFACTOR_NONE (-1)      /* one word per iteration */
 #define ES_COFACTOR_THROUGHPUT (-2) /* maximise sweep rate; JIT cost ignored */
 
-/* es_run_opts.flags: K1 skeleton variants (default: K1) */
-#define ES_FLAG_K1T 4 /* word-uniform sub-network transposed across iterations */
-#define ES_FLAG_K1U 8 /* warp-uniform super-words, 32-thread CTAs (experimental) */
+/* es_run_opts.flags: reserved (0) */
 
 /* EsResult (es.py:76-84) plus engine statistics. */
 typedef struct es_result {
@@ -130,6 +131,9 @@ typedef struct es_result {
                                  * valid but may not be the minimum, and patterns_evaluated =
                                  * patterns_swept) */
     int32_t n_devices;          /* GPUs the sweep ran on */
+    int32_t phases;             /* K1: 2 when a counterexample above a cofactored chunk's range
+                                 * needed a second sweep below it (non-contiguous chunks) */
+    int32_t phase2_cofactor_pis;/* cofactor PIs of the second phase's variant (phases == 2) */
 } es_result;
 
 /*
@@ -147,11 +151,18 @@ int32_t es_compile(int32_t num_pis, int32_t num_gates, const uint8_t *kind,
                    int32_t *num_registers);
 
 /*
- * run_exhaustive (es.py:252-339) on one GPU: sweep all 2^num_pis patterns and
- * return the MINIMUM-index pattern whose output is 1 (== the reference's
- * workers=1 witness), EXHAUSTED_ZERO, or BUDGET_EXCEEDED.
+ * run_exhaustive (es.py:252-339): sweep all 2^num_pis patterns and return the
+ * MINIMUM-index pattern whose output is 1 (== the reference's workers=1
+ * witness), EXHAUSTED_ZERO, or BUDGET_EXCEEDED.  One call may drive several
+ * GPUs (es_run_opts.devices; the reference's workers, es.py:272-331): the
+ * pattern space is dealt to them chunk by chunk and one minimum word in the
+ * first device's memory, shared as NVLink peer memory, gives every GPU the
+ * global early exit.
  */
 int32_t es_run(const es_prog *prog, const es_run_opts *opts, es_result *out);
+
+/* Visible CUDA devices (0 when there is no driver or GPU; never an error). */
+int32_t es_device_count(int32_t *n);
 
 /*
  * Batched run_exhaustive over many independent programs (the sweep's
@@ -328,7 +339,7 @@ int64_t es_emit_ptx_k(const es_prog *prog, int32_t k, int32_t block_threads, cha
 int64_t es_jit_check_k(const es_prog *prog, int32_t k, int32_t block_threads, int32_t *regs_per_thread,
                        int32_t *spill_bytes, char *log, int64_t log_cap);
 /* The PTX the JIT path would compile for `prog` (buf NULL -> returns size).
- * block_threads: 128/256/512 -> K1; 32 -> K1U; -128 -> K1T. */
+ * block_threads: 128/256/512. */
 int64_t es_emit_ptx(const es_prog *prog, int32_t block_threads, char *buf, int64_t cap);
 /* Compile PTX to SASS without a GPU (build-time check); returns cubin bytes or < 0. */
 int64_t es_jit_check(const es_prog *prog, int32_t block_threads, int32_t *regs_per_thread,

@@ -41,7 +41,7 @@ EXPORTS = ("es_compile", "es_run", "es_run_batch", "es_session_open", "es_sessio
            "es_sim", "es_sim_ones", "es_sim_device", "es_sim_prog_free", "es_sim_classes", "es_sim_levels",
            "es_aiger_parse", "es_detect_xors", "es_xag_size", "es_xag_read", "es_xag_free",
            "es_aiger_write",
-           "es_last_error", "es_version", "es_shutdown")
+           "es_device_count", "es_last_error", "es_version", "es_shutdown")
 
 _P = ctypes.c_void_p
 
@@ -56,7 +56,8 @@ class EsRunOpts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("engine", ctypes.c_int32),
                 ("budget_s", ctypes.c_double), ("cancel_flag", _P),
                 ("slice_ms", ctypes.c_double), ("block_threads", ctypes.c_int32),
-                ("flags", ctypes.c_int32), ("cofactor_pis", ctypes.c_int32)]
+                ("flags", ctypes.c_int32), ("cofactor_pis", ctypes.c_int32),
+                ("n_devices", ctypes.c_int32), ("devices", _P)]
 
 
 class EsResult(ctypes.Structure):
@@ -68,7 +69,8 @@ class EsResult(ctypes.Structure):
                 ("wall_ms", ctypes.c_double), ("launches", ctypes.c_int32),
                 ("regs_per_thread", ctypes.c_int32), ("cofactor_pis", ctypes.c_int32),
                 ("jit_opt", ctypes.c_int32), ("witness_minimal", ctypes.c_int32),
-                ("n_devices", ctypes.c_int32)]
+                ("n_devices", ctypes.c_int32), ("phases", ctypes.c_int32),
+                ("phase2_cofactor_pis", ctypes.c_int32)]
 
 
 class NativeError(RuntimeError):
@@ -102,6 +104,8 @@ def lib():
         L.es_run_batch.argtypes = [ctypes.c_int32, ctypes.POINTER(EsProg),
                                    ctypes.POINTER(EsRunOpts), ctypes.POINTER(EsResult)]
         L.es_run_batch.restype = ctypes.c_int32
+        L.es_device_count.argtypes = [ctypes.POINTER(ctypes.c_int32)]
+        L.es_device_count.restype = ctypes.c_int32
         L.es_session_open.argtypes = [ctypes.POINTER(EsProg), ctypes.POINTER(EsRunOpts),
                                       ctypes.POINTER(_P)]
         L.es_session_open.restype = ctypes.c_int32

@@ -4,6 +4,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+
+#include <cuda_runtime.h>
 #include <string>
 #include <vector>
 
@@ -96,6 +98,14 @@ int32_t es_compile(int32_t num_pis, int32_t num_gates, const uint8_t *kind, cons
 int32_t es_run(const es_prog *prog, const es_run_opts *opts, es_result *out) {
     if (!prog || !out) { set_error("null argument"); return ES_E_BAD_ARG; }
     return run_one(prog, opts, out);
+}
+
+int32_t es_device_count(int32_t *n) {
+    if (!n) { set_error("null argument"); return ES_E_BAD_ARG; }
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) { cudaGetLastError(); c = 0; }
+    *n = c;
+    return ES_OK;
 }
 
 int32_t es_run_batch(int32_t n_jobs, const es_prog *progs, const es_run_opts *opts,

@@ -78,7 +78,7 @@ std::vector<uint8_t> output_cone(const Dag &dag) {
 
 }  // namespace
 
-std::vector<int32_t> rank_cofactor_pis(const Dag &dag, int k) {
+std::vector<int32_t> rank_cofactor_pis(const Dag &dag, int k, int max_pi) {
     // cost of cofactoring PI j ~ the gates whose support contains j (they are
     // duplicated per copy; the rest is shared); PIs <= 40 fit one 64-bit mask
     const int N = dag.num_nodes(), FG = dag.first_gate(), P = dag.num_pis;
@@ -93,7 +93,7 @@ std::vector<int32_t> rank_cofactor_pis(const Dag &dag, int k) {
         for (uint64_t r = m; r; r &= r - 1) tfo[__builtin_ctzll(r)]++;
     }
     std::vector<int32_t> cand;
-    for (int j = kLanePis + 1; j <= P; ++j)
+    for (int j = kLanePis + 1; j <= std::min(P, max_pi); ++j)
         if (cone[j]) cand.push_back(j);
     std::stable_sort(cand.begin(), cand.end(), [&](int32_t a, int32_t b) {
         if (tfo[a] != tfo[b]) return tfo[a] < tfo[b];
@@ -107,7 +107,9 @@ std::vector<int32_t> rank_cofactor_pis(const Dag &dag, int k) {
             while (*q && *q != ',') ++q;
             if (*q == ',') ++q;
         }
-        if ((int)forced.size() >= k) { forced.resize(k); return forced; }
+        bool below = true;
+        for (int32_t j : forced) below = below && j <= max_pi;
+        if ((int)forced.size() >= k && below) { forced.resize(k); return forced; }
     }
     return cand;
 }

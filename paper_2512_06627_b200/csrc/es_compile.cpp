@@ -769,111 +769,5 @@ std::string emit_body_ptx(const LutNet &net, const std::vector<std::string> &out
     return s.str();
 }
 
-// ---------------------------------------------------------------------------
-// PTX body for the K1U skeleton (warp-uniform super-word section)
-// ---------------------------------------------------------------------------
-// A node is warp-uniform when its support avoids PIs 1..10 (bits of the
-// 32-bit word and of the lane index).  Such nodes are evaluated once per warp
-// as a super-word whose bit L is lane L's value: PIs 6..10 become the lane-mask
-// constants, PIs 11.. are uniform masks of the word-block index, so every
-// operand is uniform.  Where a uniform node feeds a per-lane LUT, each lane
-// extracts its bit as a full-word mask with two FMA-pipe multiplies:
-// (S * 2^(31-L)) moves bit L to the sign, mul.hi.s32 by an opaque 1 spreads it.
-std::string emit_body_ptx_u(const LutNet &net, const std::string &out, const std::string &wblo,
-                            const std::string &wbhi, const std::string &lane,
-                            const std::string &pow2, const std::string &one, int *n_uniform) {
-    const int N = (int)net.is_const.size();
-    const int P = net.num_pis;
-    std::vector<int> lut_idx(N, -1);
-    for (size_t i = 0; i < net.luts.size(); ++i) lut_idx[net.luts[i].node] = (int)i;
-    auto is_pi = [&](int v) { return v >= 1 && v <= P; };
-    std::vector<uint8_t> uni(N, 0), used_lane(N, 0);
-    for (int v = 0; v < N; ++v) {
-        if (is_pi(v) && v >= 11) uni[v] = 1;
-        else if (net.is_const[v] && (net.const_val[v] == 0u || net.const_val[v] == ~0u)) uni[v] = 1;
-    }
-    // PIs 6..10 are uniform in super-word form (lane-pattern constants)
-    auto super_ok = [&](int v) { return uni[v] || (is_pi(v) && v >= 6 && v <= 10); };
-    int nu = 0;
-    for (const Lut &L : net.luts) {
-        bool u = true;
-        for (int q = 0; q < 3; ++q) u = u && super_ok(L.leaf[q]);
-        uni[L.node] = u;
-        nu += u;
-    }
-    if (n_uniform) *n_uniform = nu;
-    // which uniform LUTs need a per-lane copy
-    std::vector<uint8_t> need_x(N, 0);
-    for (const Lut &L : net.luts)
-        if (!uni[L.node])
-            for (int q = 0; q < 3; ++q)
-                if (lut_idx[L.leaf[q]] >= 0 && uni[L.leaf[q]]) need_x[L.leaf[q]] = 1;
-    if (lut_idx[net.out_node] >= 0 && uni[net.out_node]) need_x[net.out_node] = 1;
-
-    std::unordered_map<uint32_t, int> cidx;
-    std::vector<uint32_t> consts;
-    std::vector<uint8_t> pi_lane(P + 1, 0), pi_uni(P + 1, 0);
-    auto konst = [&](uint32_t c) {
-        auto it = cidx.find(c);
-        int k;
-        if (it == cidx.end()) { k = (int)consts.size(); cidx[c] = k; consts.push_back(c); }
-        else k = it->second;
-        return "%esk" + std::to_string(k);
-    };
-    auto super_name = [&](int v) -> std::string {
-        if (lut_idx[v] >= 0) return "%esq" + std::to_string(lut_idx[v]);
-        if (is_pi(v) && v >= 6 && v <= 10) return konst(kLaneMask[v - 6]);
-        if (is_pi(v)) { pi_uni[v] = 1; return "%esm" + std::to_string(v); }
-        return konst(net.const_val[v]);
-    };
-    auto lane_name = [&](int v) -> std::string {
-        if (lut_idx[v] >= 0) return (uni[v] ? "%esx" : "%esq") + std::to_string(lut_idx[v]);
-        if (net.is_const[v]) return konst(net.const_val[v]);
-        if (is_pi(v) && v <= 10) { pi_lane[v] = 1; return "%esl" + std::to_string(v); }
-        pi_uni[v] = 1;
-        return "%esm" + std::to_string(v);
-    };
-    std::ostringstream body;
-    for (const Lut &L : net.luts) {
-        const int i = lut_idx[L.node];
-        if (uni[L.node]) {
-            body << "lop3.b32 %esq" << i << ", " << super_name(L.leaf[2]) << ", " << super_name(L.leaf[1])
-                 << ", " << super_name(L.leaf[0]) << ", " << (int)L.tt << ";\n";
-            if (need_x[L.node])
-                body << "mul.lo.u32 %esx" << i << ", %esq" << i << ", " << pow2 << ";\n"
-                     << "mul.hi.s32 %esx" << i << ", %esx" << i << ", " << one << ";\n";
-        } else {
-            body << "lop3.b32 %esq" << i << ", " << lane_name(L.leaf[2]) << ", " << lane_name(L.leaf[1])
-                 << ", " << lane_name(L.leaf[0]) << ", " << (int)L.tt << ";\n";
-        }
-    }
-    const std::string oname = lane_name(net.out_node);
-    std::ostringstream s;
-    s << "{\n";
-    if (!net.luts.empty()) {
-        s << ".reg .b32 %esq<" << net.luts.size() << ">;\n";
-        s << ".reg .b32 %esx<" << net.luts.size() << ">;\n";
-    }
-    if (!consts.empty()) s << ".reg .b32 %esk<" << consts.size() << ">;\n";
-    s << ".reg .b32 %esm<" << (P + 1) << ">;\n.reg .b32 %esl<" << (P + 1) << ">;\n";
-    for (size_t k = 0; k < consts.size(); ++k) s << "mov.b32 %esk" << k << ", " << consts[k] << ";\n";
-    for (int j = 6; j <= std::min(P, 10); ++j)
-        if (pi_lane[j]) {
-            s << "shl.b32 %esl" << j << ", " << lane << ", " << (31 - (j - 6)) << ";\n";
-            s << "shr.s32 %esl" << j << ", %esl" << j << ", 31;\n";
-        }
-    for (int j = 11; j <= P; ++j)
-        if (pi_uni[j]) {
-            const int bit = j - 11;
-            const std::string &src = bit < 32 ? wblo : wbhi;
-            s << "shl.b32 %esm" << j << ", " << src << ", " << (31 - (bit & 31)) << ";\n";
-            s << "shr.s32 %esm" << j << ", %esm" << j << ", 31;\n";
-        }
-    s << body.str();
-    if (net.out_neg) s << "not.b32 " << out << ", " << oname << ";\n";
-    else s << "mov.b32 " << out << ", " << oname << ";\n";
-    s << "}\n";
-    return s.str();
-}
 
 }  // namespace es

@@ -114,7 +114,9 @@ void map_luts(const Dag &dag, LutNet *net);
 constexpr int kMaxCofactorPis = 5;
 // Rank word PIs (>= 6) by transitive-fanout size (cheapest first) and return
 // the first `k` of that order (rank order: sort before cofactor_expand).
-std::vector<int32_t> rank_cofactor_pis(const Dag &dag, int k);
+// max_pi: only PIs <= max_pi are candidates (the second phase of a
+// non-equivalent sweep keeps its cofactor bits below the witness's top bit).
+std::vector<int32_t> rank_cofactor_pis(const Dag &dag, int k, int max_pi = 1 << 20);
 // dag with the PIs in `pis` (ascending) cofactored: 2^k outputs, output c
 // under PI pis[b] = bit b of c.  Constant propagation + structural hashing.
 void cofactor_expand(const Dag &dag, const std::vector<int32_t> &pis, Dag *out);
@@ -139,12 +141,6 @@ void eval_lutnet(const LutNet &net, uint64_t w0, uint64_t nw, uint32_t *out);
 std::string emit_body_ptx(const LutNet &net, const std::vector<std::string> &outs,
                           const std::string &wlo, const std::string &whi,
                           const std::string &one = "");
-
-// PTX body for the K1U skeleton (k1u_skeleton.cu): warp-uniform nodes as
-// super-words.  Operands: word-block index halves, lane, 2^(31-lane), opaque 1.
-std::string emit_body_ptx_u(const LutNet &net, const std::string &out, const std::string &wblo,
-                            const std::string &wbhi, const std::string &lane,
-                            const std::string &pow2, const std::string &one, int *n_uniform);
 
 uint32_t lane_valid_mask(int num_pis);
 

@@ -18,13 +18,12 @@
 #include <cuda_runtime.h>
 #include <nvPTXCompiler.h>
 
-#include "es_codegen_t.h"
 #include "es_jit.h"
 #include "es_nvtx.h"
 
 namespace es {
 
-#include "k1_skeleton_ptx.inc"  // kK1Ptx<threads>_<copies> (K1), kK1UPtx32 (K1U), kK1TPtx128 (K1T)
+#include "k1_skeleton_ptx.inc"  // kK1Ptx<threads>_<copies>
 
 static const char *skeleton_for(int threads, int copies) {
     const bool multi = copies > 1;
@@ -36,65 +35,10 @@ static const char *skeleton_for(int threads, int copies) {
     }
 }
 
-static bool splice_body_u(const LutNet &net, std::string *ptx, std::string *err) {
-    std::string s(kK1UPtx32);
-    const std::string marker = "// ES_BODY_U ";
-    size_t at = s.find(marker);
-    if (at == std::string::npos || s.find(marker, at + 1) != std::string::npos) {
-        *err = "K1U skeleton must contain exactly one ES_BODY_U marker";
-        return false;
-    }
-    size_t eol = s.find('\n', at);
-    std::string args = s.substr(at + marker.size(), eol - at - marker.size());
-    char o[64], a[64], b[64], l[64], p2[64], one[64];
-    if (sscanf(args.c_str(), "%63s %63s %63s %63s %63s %63s", o, a, b, l, p2, one) != 6) {
-        *err = "cannot parse ES_BODY_U operands: " + args;
-        return false;
-    }
-    int nu = 0;
-    s.replace(at, eol - at, emit_body_ptx_u(net, o, a, b, l, p2, one, &nu));
-    *ptx = std::move(s);
-    return true;
-}
-
-static bool marker_args(const std::string &s, const std::string &marker, size_t *at, size_t *eol,
-                        std::vector<std::string> *args, std::string *err) {
-    *at = s.find(marker);
-    if (*at == std::string::npos || s.find(marker, *at + 1) != std::string::npos) {
-        *err = "skeleton must contain exactly one " + marker;
-        return false;
-    }
-    *eol = s.find('\n', *at);
-    std::istringstream in(s.substr(*at + marker.size(), *eol - *at - marker.size()));
-    std::string a;
-    while (in >> a) args->push_back(a);
-    return true;
-}
-
-static bool splice_body_t(const LutNet &net, std::string *ptx, std::string *err, int *region_bytes) {
-    std::string s(kK1TPtx128);
-    const TSplit t = split_uniform(net);
-    size_t at, eol;
-    std::vector<std::string> a1, a2;
-    if (!marker_args(s, "// ES_BODY_T1 ", &at, &eol, &a1, err) || a1.size() != 3) return false;
-    s.replace(at, eol - at, emit_body_t1(net, t, a1[0], a1[1], a1[2], kK1TBlock));
-    if (!marker_args(s, "// ES_BODY_T2 ", &at, &eol, &a2, err) || a2.size() != 7) return false;
-    s.replace(at, eol - at, emit_body_t2(net, t, a2[0], a2[1], a2[2], a2[3], a2[4], a2[5], a2[6], kK1TBlock));
-    if (region_bytes) *region_bytes = std::max<int>(1, (int)t.boundary.size()) * kK1TBlock * 4;
-    *ptx = std::move(s);
-    return true;
-}
-
 bool splice_body(const LutNet &net, int threads, std::string *ptx, std::string *err,
                  int *region_bytes) {
     if (region_bytes) *region_bytes = 0;
     const int copies = (int)net.outs.size();
-    if ((threads == kK1UThreads || threads == kK1TThreads) && copies != 1) {
-        *err = "K1U/K1T take no cofactor copies";
-        return false;
-    }
-    if (threads == kK1UThreads) return splice_body_u(net, ptx, err);
-    if (threads == kK1TThreads) return splice_body_t(net, ptx, err, region_bytes);
     const char *sk = skeleton_for(threads, copies);
     if (!sk) {
         *err = "unsupported K1 variant: " + std::to_string(threads) + " threads x " +
@@ -320,7 +264,7 @@ int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std
     }
     JitKernel *k = new JitKernel();
     k->threads = threads;
-    k->block = threads == kK1TThreads ? 128 : threads;
+    k->block = threads;
     k->region_bytes = region;
     k->opt = opt;
     k->ptx_h2 = h2;
@@ -334,7 +278,7 @@ int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std
         return ES_E_CUDA;
     }
     e = cudaLibraryGetKernel(&k->kernel, k->lib,
-                             threads == kK1UThreads ? "es_k1u" : threads == kK1TThreads ? "es_k1t" : "es_k1");
+                             "es_k1");
     if (e != cudaSuccess) {
         *err = std::string("cudaLibraryGetKernel: ") + cudaGetErrorString(e);
         cudaLibraryUnload(k->lib);

@@ -16,7 +16,7 @@ struct JitKernel {
     cudaKernel_t kernel = nullptr;
     int threads = 0;        // variant selector (see below)
     int block = 0;          // CTA size of the launch
-    int region_bytes = 0;   // K1T: shared bytes per warp
+    int region_bytes = 0;   // (unused: 0)
     int regs = -1;
     int spill_bytes = 0;
     int opt = 3;            // ptxas optimisation level it was compiled at
@@ -30,13 +30,7 @@ inline double now_ms() {
     return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
 }
 
-// "threads" selects the skeleton: 128/256/512 -> K1 at that CTA size;
-// kK1UThreads -> K1U (warp-uniform super-words, 32-thread CTAs);
-// kK1TThreads -> K1T (transposed word-uniform phase, 128-thread CTAs).
-constexpr int kK1UThreads = 32;
-constexpr int kK1TThreads = -128;
-
-// The complete PTX for `net` at a block size of 128/256/512 threads, or K1U.
+// The complete PTX for `net` at a block size of 128/256/512 threads.
 bool splice_body(const LutNet &net, int threads, std::string *ptx, std::string *err,
                  int *region_bytes = nullptr);
 // PTX -> sm_100a cubin in process at ptxas -O<opt> (ES_PTXAS_O overrides);

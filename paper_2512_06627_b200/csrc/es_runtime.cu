@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <condition_variable>
 #include <mutex>
@@ -26,7 +27,6 @@
 #include <cuda_runtime.h>
 
 #include "es_core.h"
-#include "es_codegen_t.h"
 #include "es_jit.h"
 #include "es_k2prog.h"
 #include "es_nvtx.h"
@@ -42,11 +42,11 @@ struct K1Params {
     unsigned long long first_chunk;
     unsigned long long n_slots;
     unsigned long long world;
+    unsigned long long hit_stop;
     unsigned long long total_words;
     unsigned int chunk_log2;
     unsigned int valid_mask;
     unsigned int one;
-    unsigned int region_bytes;
     unsigned int cof_n;
     unsigned int cof_pos[8];
 };
@@ -283,6 +283,10 @@ __global__ void __launch_bounds__(256) es_alu_peak_kernel(unsigned *sink, int it
 
 int alu_peak(int dev, double *lane_ops_per_s, double *ms_out);
 
+// *w = min(*w, *v): folds the other devices' minimum into a device-local word
+// (multi-GPU sweep without peer access)
+__global__ void es_word_min_kernel(unsigned long long *w, const unsigned long long *v) { atomicMin(w, *v); }
+
 // Shared-memory load bandwidth microbenchmark (the K2 interpreter's slot file
 // is a shared-memory bound): conflict-free 16-byte loads, 8
 // independent per thread per iteration, over a 16 KB tile per CTA.
@@ -305,7 +309,7 @@ __global__ void __launch_bounds__(256) es_smem_peak_kernel(unsigned *sink, int i
 }
 
 // ---------------------------------------------------------------------------
-// per-thread, per-device context
+// per-device contexts, leased for the duration of one call
 // ---------------------------------------------------------------------------
 namespace {
 
@@ -323,7 +327,13 @@ struct Ctx {
     size_t stage_cap = 0;      // in records
 };
 
-thread_local std::vector<Ctx *> t_ctx;
+// Every call leases one context per device it runs on (a stream, the slice
+// words, events) and returns it when it ends, so concurrent callers (the
+// scheduler races ES against SAT/BDD on several host threads, and a
+// multi-GPU sweep drives each device from its own host thread) never share
+// a stream, while a context outlives the thread that made it.
+std::mutex g_ctx_mu;
+std::vector<Ctx *> g_ctx_all, g_ctx_free;
 
 int cuda_fail(cudaError_t e, const char *what) {
     set_error(std::string(what) + ": " + cudaGetErrorString(e));
@@ -336,17 +346,7 @@ int cuda_fail(cudaError_t e, const char *what) {
         if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
     } while (0)
 
-int get_ctx(int dev, Ctx **out) {
-    int n = 0;
-    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
-        set_error("no CUDA device visible");
-        return ES_E_NO_DEVICE;
-    }
-    if (dev < 0 || dev >= n) { set_error("device ordinal out of range"); return ES_E_BAD_ARG; }
-    CK(cudaSetDevice(dev));
-    for (Ctx *c : t_ctx)
-        if (c->dev == dev) { *out = c; return ES_OK; }
-    Ctx *c = new Ctx();
+int make_ctx(int dev, Ctx *c) {
     c->dev = dev;
     CK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, dev));
     {
@@ -372,10 +372,54 @@ int get_ctx(int dev, Ctx **out) {
         CK(cudaStreamCreateWithFlags(&c->side[q], cudaStreamNonBlocking));
         CK(cudaEventCreate(&c->ev_side[q]));
     }
-    t_ctx.push_back(c);
-    *out = c;
     return ES_OK;
 }
+
+int check_device(int dev) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        set_error("no CUDA device visible");
+        return ES_E_NO_DEVICE;
+    }
+    if (dev < 0 || dev >= n) {
+        set_error("device ordinal " + std::to_string(dev) + " out of range (" + std::to_string(n) + " visible)");
+        return ES_E_BAD_ARG;
+    }
+    return ES_OK;
+}
+
+struct CtxLease {
+    Ctx *c = nullptr;
+    CtxLease() = default;
+    CtxLease(const CtxLease &) = delete;
+    CtxLease &operator=(const CtxLease &) = delete;
+    int acquire(int dev) {
+        int rc = check_device(dev);
+        if (rc != ES_OK) return rc;
+        CK(cudaSetDevice(dev));
+        {
+            std::lock_guard<std::mutex> lk(g_ctx_mu);
+            for (size_t i = 0; i < g_ctx_free.size(); ++i)
+                if (g_ctx_free[i]->dev == dev) {
+                    c = g_ctx_free[i];
+                    g_ctx_free.erase(g_ctx_free.begin() + (long)i);
+                    return ES_OK;
+                }
+        }
+        Ctx *n = new Ctx();
+        rc = make_ctx(dev, n);
+        if (rc != ES_OK) { delete n; return rc; }  // (partially created CUDA objects leak; rare)
+        std::lock_guard<std::mutex> lk(g_ctx_mu);
+        g_ctx_all.push_back(n);
+        c = n;
+        return ES_OK;
+    }
+    ~CtxLease() {
+        if (!c) return;
+        std::lock_guard<std::mutex> lk(g_ctx_mu);
+        g_ctx_free.push_back(c);
+    }
+};
 
 inline uint64_t ref_patterns_for_hit(uint64_t idx, int P) {
     const int b = std::min(P, 14);  // reference batch = 2^min(n,14) patterns
@@ -433,7 +477,7 @@ struct K1Plan {
 };
 
 int k1_prepare(const LutNet &net, int threads, int sms, K1Plan *pl, double *jit_ms,
-               JitKernel *cached = nullptr, int opt = 3) {
+               JitKernel *cached = nullptr, int opt = 3, int n_dev = 1) {
     std::string err;
     if (cached) {
         pl->jk = cached;
@@ -443,7 +487,7 @@ int k1_prepare(const LutNet &net, int threads, int sms, K1Plan *pl, double *jit_
         if (rc != ES_OK) { set_error(err); return rc; }
     }
     pl->threads = pl->jk->block;
-    pl->smem = threads == kK1TThreads ? (size_t)pl->jk->region_bytes * (pl->jk->block / 32) : 0;
+    pl->smem = 0;
     const int P = net.num_pis;
     pl->cof_n = (int)net.cof_pis.size();
     if (pl->cof_n > kMaxCofactorPis || (pl->cof_n > 0 && P - 5 - pl->cof_n < 0)) { set_error("bad cofactor set"); return ES_E_BAD_ARG; }
@@ -454,133 +498,255 @@ int k1_prepare(const LutNet &net, int threads, int sms, K1Plan *pl, double *jit_
         CK(cudaFuncSetAttribute((const void *)pl->jk->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->smem));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)pl->jk->kernel, pl->threads, pl->smem));
     nb = std::max(nb, 1);
-    // K1T: a chunk holds whole phase blocks of every warp (32 words x 16 x warps)
-    const int min_words = threads == kK1TThreads ? 32 * kK1TBlock * (pl->threads / 32) : pl->threads;
-    pl->chunk_log2 = pick_chunk_log2(pl->total_words, min_words, sms * nb);
+    const int min_words = pl->threads;
+    // chunk size for the whole job: n_dev GPUs' resident CTAs share the chunks
+    pl->chunk_log2 = pick_chunk_log2(pl->total_words, min_words, sms * nb * std::max(1, n_dev));
     pl->n_chunks = std::max<uint64_t>(1, pl->total_words >> pl->chunk_log2);
     pl->grid = (int)std::min<uint64_t>(pl->n_chunks, (uint64_t)sms * nb);
     pl->valid = lane_valid_mask(P);
     return ES_OK;
 }
 
+// counter: two words, [0] claims and [1] chunks swept, zeroed here
 int k1_launch(const K1Plan &pl, cudaStream_t st, unsigned long long *best, unsigned *counter,
-              uint64_t first_chunk, uint64_t n_slots, uint64_t world) {
+              uint64_t first_chunk, uint64_t n_slots, uint64_t world, uint64_t hit_stop = 0) {
     K1Params kp;
     kp.best = best;
     kp.counter = counter;
     kp.first_chunk = first_chunk;
     kp.n_slots = n_slots;
     kp.world = world;
+    kp.hit_stop = hit_stop;
     kp.total_words = pl.total_words;
     kp.chunk_log2 = (unsigned)pl.chunk_log2;
     kp.valid_mask = pl.valid;
     kp.one = 1u;
-    kp.region_bytes = (unsigned)pl.jk->region_bytes;
     kp.cof_n = (unsigned)pl.cof_n;
     for (int i = 0; i < 8; ++i) kp.cof_pos[i] = pl.cof_pos[i];
-    CK(cudaMemsetAsync(counter, 0, sizeof(unsigned), st));
+    CK(cudaMemsetAsync(counter, 0, 2 * sizeof(unsigned), st));
     void *args[] = {&kp};
     const int grid = (int)std::min<uint64_t>((uint64_t)pl.grid, std::max<uint64_t>(n_slots, 1));
     CK(cudaLaunchKernel((const void *)pl.jk->kernel, dim3(grid), dim3(pl.threads), args, pl.smem, st));
     return ES_OK;
 }
 
-// K1 skeleton choice: opts.flags bit 2 -> K1T, bit 3 -> K1U, else K1 at
-// opts.block_threads (default 128).
 // Default CTA size: 128 for one word per iteration (165 registers: 3 CTAs
 // per SM), 256 with cofactor copies (255 registers; measured 10-15% faster).
 static int k1_threads(const es_run_opts &o, int cofactor_pis = 0) {
-    if (o.flags & ES_FLAG_K1T) return kK1TThreads;
-    if (o.flags & ES_FLAG_K1U) return kK1UThreads;
     return o.block_threads > 0 ? o.block_threads : cofactor_pis > 0 ? 256 : 128;
 }
-static int k1_slot(int threads) {
-    return threads == 128 ? 0 : threads == 256 ? 1 : threads == 512 ? 2 : threads == kK1UThreads ? 3 : 4;
+static int k1_slot(int threads) { return threads == 128 ? 0 : threads == 256 ? 1 : 2; }
+
+// The devices of one run: es_run_opts.devices[0..n_devices) when given (the
+// same ordinal may repeat: several host threads then share one GPU), else
+// es_run_opts.device.
+static std::vector<int> run_devices(const es_run_opts &o) {
+    std::vector<int> d;
+    if (o.n_devices > 0 && o.devices)
+        for (int i = 0; i < o.n_devices; ++i) d.push_back(o.devices[i]);
+    if (d.empty()) d.push_back(o.device);
+    return d;
 }
 
-static int run_k1(const LutNet &net, int G, const es_run_opts &o, Ctx *c, double deadline,
-                  es_result *r, JitKernel **jk_cache, int opt = 3) {
-    NvtxRange nvtx("es_k1");
-    const int threads = k1_threads(o, (int)net.cof_pis.size());
-    K1Plan pl;
-    double jit_ms = 0;
-    int rc = k1_prepare(net, threads, c->sms, &pl, &jit_ms, *jk_cache, opt);
-    if (rc != ES_OK) return rc;
-    *jk_cache = pl.jk;
-    r->engine = ES_ENGINE_JIT;
-    r->jit_ms = jit_ms;
-    r->regs_per_thread = pl.jk->regs;
-    r->cofactor_pis = pl.cof_n;
-    r->jit_opt = pl.jk->opt;
-    const int P = net.num_pis;
-    const uint64_t sentinel = 1ull << P;
-    const uint64_t chunk_patterns = pl.patterns_per_chunk();
-    // slice size from a conservative throughput estimate
+// ---------------------------------------------------------------------------
+// Multi-device K1 sweep.  Global chunks [begin, n_chunks) are
+// dealt round-robin: device d sweeps begin + d + k*n.  Every device is driven
+// by its own host thread in launch slices, and all kernels atomicMin into ONE
+// minimum word in device 0's HBM, reached by the other GPUs as peer memory
+// over NVLink/NVSwitch (system-scope atomics): a counterexample found on any
+// GPU stops every GPU at its next chunk claim, with no collective on the data
+// path.  Without peer access each device keeps its own word and the host
+// threads combine them between slices.  The swept prefix is tracked per
+// device, so the minimum-index proof (best below the first pattern of the
+// first unswept chunk) holds across devices.
+// ---------------------------------------------------------------------------
+struct SweepOut {
+    uint64_t best = 0;        // minimum failing pattern found (init_best if none)
+    uint64_t prefix = 0;      // global chunks [0, prefix) fully swept
+    uint64_t swept = 0;       // chunks swept (all devices, completed launches)
+    bool stopped = false;     // budget / cancel
+    int reason = 0;
+    double device_ms = 0;     // max over devices of the slices' CUDA-event time
+    int launches = 0;
+};
+
+static int sweep_k1(const K1Plan &pl, int G, const es_run_opts &o, const std::vector<Ctx *> &cs,
+                    double deadline, uint64_t begin, uint64_t init_best, uint64_t hit_stop,
+                    SweepOut *res) {
+    const int n = (int)cs.size();
+    const uint64_t N = pl.n_chunks;
+    // the shared word: device 0's, if every other device can reach it
+    bool shared = true;
+    for (int d = 1; d < n && shared; ++d) {
+        if (cs[d]->dev == cs[0]->dev) continue;
+        int can = 0;
+        if (cudaDeviceCanAccessPeer(&can, cs[d]->dev, cs[0]->dev) != cudaSuccess || !can) { shared = false; break; }
+        CK(cudaSetDevice(cs[d]->dev));
+        const cudaError_t e = cudaDeviceEnablePeerAccess(cs[0]->dev, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else if (e != cudaSuccess) { cudaGetLastError(); shared = false; }
+    }
+    std::vector<unsigned long long *> word(n);
+    for (int d = 0; d < n; ++d) word[d] = shared ? cs[0]->d_best : cs[d]->d_best;
+    for (int d = 0; d < n; ++d) {
+        if (d > 0 && shared) continue;
+        CK(cudaSetDevice(cs[d]->dev));
+        cs[d]->h_pin[0] = init_best;
+        CK(cudaMemcpyAsync(cs[d]->d_best, cs[d]->h_pin, 8, cudaMemcpyHostToDevice, cs[d]->stream));
+        CK(cudaStreamSynchronize(cs[d]->stream));  // armed before any device launches
+    }
+    // slice size (in this device's chunk slots) from a conservative rate estimate
     const bool sliced = deadline >= 0 || o.cancel_flag != nullptr;
     const double slice_ms = o.slice_ms > 0 ? o.slice_ms : 20.0;
-    const double est_rate = 2.0e14;  // gate-patterns/s, deliberately low
-    const double chunk_ms = 1e3 * (double)std::max(G, 1) * (double)chunk_patterns / est_rate;
-    uint64_t per_slice = sliced ? (uint64_t)std::max(1.0, slice_ms / chunk_ms) : pl.n_chunks;
-    per_slice = std::max<uint64_t>(per_slice, (uint64_t)pl.grid);
+    const double est_rate = 2.0e14;  // gate-patterns/s per GPU, deliberately low
+    const double chunk_ms = 1e3 * (double)std::max(G, 1) * (double)pl.patterns_per_chunk() / est_rate;
+    uint64_t per_slice_all = sliced ? (uint64_t)std::max(1.0, slice_ms / chunk_ms) : N;
+    per_slice_all = std::max<uint64_t>(per_slice_all, (uint64_t)pl.grid);
 
-    c->h_pin[0] = sentinel;
-    CK(cudaMemcpyAsync(c->d_best, c->h_pin, 8, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaEventRecord(c->ev_start, c->stream));
-    uint64_t completed_chunks = 0;
-    int launches = 0, stop_reason = 0;
-    bool stopped = false, found = false;
-    uint64_t best = sentinel;
-    std::vector<uint64_t> slice_end;
-    for (uint64_t begin = 0; begin < pl.n_chunks && !found; begin += per_slice) {
-        if (stop_requested(o, deadline, &stop_reason)) { stopped = true; break; }
-        const uint64_t n = std::min(per_slice, pl.n_chunks - begin);
-        const int s = launches & 1;
-        rc = k1_launch(pl, c->stream, c->d_best, c->d_counter + s, begin, n, 1);
-        if (rc != ES_OK) return rc;
-        CK(cudaMemcpyAsync(c->h_pin + 1 + s, c->d_best, 8, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaEventRecord(c->ev_slice[s], c->stream));
-        slice_end.push_back(begin + n);
-        ++launches;
-        if (launches >= 2) {  // keep two slices in flight; inspect the older one
-            const int q = (launches - 2) & 1;
-            CK(cudaEventSynchronize(c->ev_slice[q]));
-            completed_chunks = slice_end[launches - 2];
-            best = c->h_pin[1 + q];
-            // every chunk below `completed_chunks` is swept: nothing smaller can appear
-            if (best < sentinel && best < pl.first_pattern(completed_chunks)) found = true;
+    std::vector<std::atomic<uint64_t>> progress(n);  // per device: slots swept (prefix of its class)
+    std::vector<uint64_t> slots(n, 0);
+    for (int d = 0; d < n; ++d) {
+        slots[d] = N > begin + d ? (N - begin - d + n - 1) / n : 0;
+        progress[d].store(0);
+    }
+    std::atomic<uint64_t> best{init_best};
+    std::atomic<bool> done{false};
+    std::atomic<int> stop_reason{0}, err{ES_OK}, launches{0};
+    std::atomic<uint64_t> swept{0};
+    std::mutex err_mu;
+    std::string err_msg;
+    std::vector<double> dev_ms(n, 0.0);
+    auto prefix = [&]() {  // global chunks [0, p) all swept
+        uint64_t p = N;
+        for (int d = 0; d < n; ++d) {
+            const uint64_t pr = progress[d].load();
+            if (pr < slots[d]) p = std::min(p, begin + pr * n + d);
         }
+        return p;
+    };
+    auto lower = [&](uint64_t v) {
+        uint64_t cur = best.load();
+        while (v < cur && !best.compare_exchange_weak(cur, v)) {}
+    };
+    auto settled = [&]() {  // nothing below `best` is left unswept, or phase 1 saw a hit
+        const uint64_t b = best.load();
+        if (b < hit_stop) return true;
+        const uint64_t p = prefix();
+        return p >= N || b < pl.first_pattern(p);
+    };
+    auto worker = [&](int d) {
+        Ctx *c = cs[d];
+        auto fail = [&](int rc) {
+            std::lock_guard<std::mutex> lk(err_mu);
+            if (err.load() == ES_OK) { err.store(rc); err_msg = es_last_error(); }
+            done.store(true);
+        };
+        if (cudaSetDevice(c->dev) != cudaSuccess) { fail(cuda_fail(cudaGetLastError(), "cudaSetDevice")); return; }
+        const uint64_t per_slice = std::max<uint64_t>(1, per_slice_all);
+        std::vector<uint64_t> slice_end;
+        int my = 0;
+        if (cudaEventRecord(c->ev_start, c->stream) != cudaSuccess) { fail(cuda_fail(cudaGetLastError(), "event")); return; }
+        unsigned *h_swept = reinterpret_cast<unsigned *>(c->h_pin + 4);  // per slice: chunks swept
+        auto harvest = [&](int q, uint64_t end) {  // slice q's copies have landed
+            lower(c->h_pin[1 + q]);
+            swept.fetch_add(h_swept[q]);
+            progress[d].store(end);
+            if (settled()) done.store(true);
+        };
+        for (uint64_t b = 0; b < slots[d] && !done.load(); b += per_slice) {
+            int reason = 0;
+            if (stop_requested(o, deadline, &reason)) {
+                int z = 0;
+                stop_reason.compare_exchange_strong(z, reason);
+                done.store(true);
+                break;
+            }
+            const uint64_t ns = std::min(per_slice, slots[d] - b);
+            const int s = my & 1;
+            if (!shared) {  // fold the other devices' finds into this device's word first
+                const uint64_t g = best.load();
+                if (g < init_best) {
+                    c->h_pin[3] = g;
+                    if (cudaMemcpyAsync(c->d_best + 1, c->h_pin + 3, 8, cudaMemcpyHostToDevice, c->stream) != cudaSuccess) {
+                        fail(cuda_fail(cudaGetLastError(), "cudaMemcpyAsync")); return;
+                    }
+                    es_word_min_kernel<<<1, 1, 0, c->stream>>>(c->d_best, c->d_best + 1);
+                }
+            }
+            int rc = k1_launch(pl, c->stream, word[d], c->d_counter + 2 * s, begin + d + b * n, ns,
+                               (uint64_t)n, hit_stop);
+            if (rc != ES_OK) { fail(rc); return; }
+            if (cudaMemcpyAsync(c->h_pin + 1 + s, word[d], 8, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+                cudaMemcpyAsync(h_swept + s, c->d_counter + 2 * s + 1, 4, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+                cudaEventRecord(c->ev_slice[s], c->stream) != cudaSuccess) {
+                fail(cuda_fail(cudaGetLastError(), "slice bookkeeping")); return;
+            }
+            slice_end.push_back(b + ns);
+            ++my;
+            launches.fetch_add(1);
+            if (my >= 2) {  // two slices in flight; inspect the older one
+                const int q = (my - 2) & 1;
+                if (cudaEventSynchronize(c->ev_slice[q]) != cudaSuccess) { fail(cuda_fail(cudaGetLastError(), "sync")); return; }
+                harvest(q, slice_end[my - 2]);
+            }
+        }
+        if (cudaEventRecord(c->ev_stop, c->stream) != cudaSuccess || cudaStreamSynchronize(c->stream) != cudaSuccess) {
+            fail(cuda_fail(cudaGetLastError(), "cudaStreamSynchronize")); return;
+        }
+        if (my > 0) harvest((my - 1) & 1, slice_end[my - 1]);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, c->ev_start, c->ev_stop);
+        dev_ms[d] = ms;
+    };
+    if (n == 1) {
+        worker(0);
+    } else {
+        std::vector<std::thread> th;
+        for (int d = 1; d < n; ++d) th.emplace_back(worker, d);
+        worker(0);
+        for (auto &t : th) t.join();
     }
-    CK(cudaEventRecord(c->ev_stop, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    if (launches > 0) {
-        completed_chunks = slice_end[launches - 1];
-        best = c->h_pin[1 + ((launches - 1) & 1)];
+    if (err.load() != ES_OK) { set_error(err_msg); return err.load(); }
+    if (shared) {  // final value of the shared word (every device has synchronised)
+        CK(cudaSetDevice(cs[0]->dev));
+        CK(cudaMemcpy(cs[0]->h_pin, cs[0]->d_best, 8, cudaMemcpyDeviceToHost));
+        lower(cs[0]->h_pin[0]);
     }
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, c->ev_start, c->ev_stop));
-    r->device_ms = ms;
-    r->launches = launches;
-    if (best < sentinel) {
+    res->best = best.load();
+    res->prefix = prefix();
+    res->swept = swept.load();
+    res->reason = stop_reason.load();
+    res->stopped = res->reason != 0;
+    res->launches = launches.load();
+    res->device_ms = *std::max_element(dev_ms.begin(), dev_ms.end());
+    return ES_OK;
+}
+
+// The result of a finished or stopped K1 sweep over [0, n_chunks) of `pl`.
+static void k1_result(const K1Plan &pl, const SweepOut &sw, int P, es_result *r) {
+    const uint64_t sentinel = 1ull << P;
+    r->device_ms += sw.device_ms;
+    r->launches += sw.launches;
+    const uint64_t swept_patterns = std::min<uint64_t>(sw.swept * pl.patterns_per_chunk(), sentinel);
+    r->patterns_swept += swept_patterns;
+    r->patterns_swept = std::min(r->patterns_swept, sentinel);
+    if (sw.best < sentinel) {
         r->verdict = ES_COUNTEREXAMPLE;
-        r->witness_index = best;
-        r->patterns_swept = std::min<uint64_t>(completed_chunks * chunk_patterns, sentinel);
-        // minimum only if every chunk that could hold a smaller pattern was swept:
-        // always for a finished sweep; a budget/cancel stop of a cofactored sweep
-        // (chunks interleave high pattern bits) may leave smaller ones unswept
-        const bool minimal = completed_chunks >= pl.n_chunks || best < pl.first_pattern(completed_chunks);
+        r->witness_index = sw.best;
+        // the minimum, unless a stop left chunks below it unswept (cofactor
+        // bits above the chunk interleave high patterns into low chunks)
+        const bool minimal = sw.prefix >= pl.n_chunks || sw.best < pl.first_pattern(sw.prefix);
         r->witness_minimal = minimal ? 1 : 0;
-        r->patterns_evaluated = minimal ? ref_patterns_for_hit(best, P) : r->patterns_swept;
-    } else if (stopped) {
+        r->patterns_evaluated = minimal ? ref_patterns_for_hit(sw.best, P) : r->patterns_swept;
+    } else if (sw.stopped) {
         r->verdict = ES_BUDGET_EXCEEDED;
-        r->reason = stop_reason;
-        r->patterns_evaluated = std::min<uint64_t>(completed_chunks * chunk_patterns, sentinel);
-        r->patterns_swept = r->patterns_evaluated;
+        r->reason = sw.reason;
+        r->patterns_evaluated = r->patterns_swept;
     } else {
         r->verdict = ES_EXHAUSTED_ZERO;
         r->patterns_evaluated = sentinel;
         r->patterns_swept = sentinel;
     }
-    return ES_OK;
 }
 
 // ---------------------------------------------------------------------------
@@ -989,36 +1155,37 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
 struct MappedProg {
     std::vector<uint8_t> sig;        // the program arrays: a cache hit must match them exactly
     Dag dag;
-    LutNet net;                      // no cofactors (mapped on demand: variant(0))
-    bool net_ready = false;
     int G = 0;
-    // cofactor variants k = 1..kMaxCofactorPis, mapped on demand
-    std::vector<int32_t> cof_rank;   // the kMaxCofactorPis cheapest word PIs, by fanout
-    std::unique_ptr<LutNet> cof[kMaxCofactorPis + 1];
-    // K1 kernels per (k, skeleton): 128/256/512, K1U, K1T
-    JitKernel *jk[kMaxCofactorPis + 1][5] = {};
+    // K1 variants keyed by their cofactor PI set (ascending; empty = one word
+    // per iteration), mapped on demand; kernels per (set, CTA size)
+    std::map<std::vector<int32_t>, std::unique_ptr<LutNet>> nets;
+    std::map<std::pair<std::vector<int32_t>, int>, JitKernel *> jks;
+    std::map<int, std::vector<int32_t>> ranks;  // max_pi -> the cheapest word PIs (<= max_pi), by fanout
     int runs = 0;                    // K1 runs so far (the reuse estimate of the auto policy)
     std::shared_ptr<K2Prog> k2;      // interpreter program (its own cofactor depth), on demand
     bool k2_searched = false;        // built with the cofactor-depth search
     int k2_runs = 0;
     std::mutex mu;
-    const LutNet &variant(int k) {   // caller holds mu
-        NvtxRange nvtx("es_map");
-        if (k == 0) {
-            if (!net_ready) { map_luts(dag, &net); net_ready = true; }
-            return net;
-        }
-        if (!cof[k]) {
-            if (cof_rank.empty()) cof_rank = rank_cofactor_pis(dag, kMaxCofactorPis);
-            std::vector<int32_t> pis(cof_rank.begin(), cof_rank.begin() + std::min<size_t>(k, cof_rank.size()));
-            std::sort(pis.begin(), pis.end());
-            cof[k].reset(new LutNet());
-            map_cofactored(dag, pis, cof[k].get());
-        }
-        return *cof[k];
+    // the k word PIs of smallest transitive fanout among PIs <= max_pi, ascending
+    std::vector<int32_t> ranked(int k, int max_pi = 1 << 20) {  // caller holds mu
+        auto it = ranks.find(max_pi);
+        if (it == ranks.end()) it = ranks.emplace(max_pi, rank_cofactor_pis(dag, kMaxCofactorPis, max_pi)).first;
+        std::vector<int32_t> pis(it->second.begin(), it->second.begin() + std::min<size_t>(k, it->second.size()));
+        std::sort(pis.begin(), pis.end());
+        return pis;
     }
+    const LutNet &variant_set(const std::vector<int32_t> &pis) {  // caller holds mu
+        auto &slot = nets[pis];
+        if (!slot) {
+            NvtxRange nvtx("es_map");
+            slot.reset(new LutNet());
+            map_cofactored(dag, pis, slot.get());
+        }
+        return *slot;
+    }
+    const LutNet &variant(int k) { return variant_set(ranked(k)); }
+    JitKernel *&jk(const LutNet &n, int threads) { return jks[{n.cof_pis, k1_slot(threads)}]; }
 };
-
 static uint64_t prog_hash(const es_prog &p) {
     uint64_t h = 1469598103934665603ull;
     auto mix = [&](const void *d, size_t n) {
@@ -1120,12 +1287,11 @@ constexpr double kO1Slowdown = 1.07;
 // with the smaller compile + expected sweep time (a kernel already compiled
 // at that level or higher costs nothing), so a cold single run compiles at
 // -O1 and a program that keeps being re-run tiers up to -O3.
-static int k1_opt(const MappedProg &mp, const LutNet &n, int k, int slot, int P, int sms, bool tput,
+static int k1_opt(const MappedProg &mp, const LutNet &n, const JitKernel *have, int P, int sms, bool tput,
                   double *cost) {
     const double sweep = est_sweep_ms(n, P, sms);
     if (tput) { *cost = sweep; return 3; }
     const double reuse = 1.0 + mp.runs;  // doubling rule: expect as many more runs as so far
-    const JitKernel *have = mp.jk[k][slot];
     int best = 3;
     *cost = 1e300;
     for (int opt : {3, 1}) {
@@ -1142,10 +1308,9 @@ static int choose_cofactors(MappedProg &mp, const es_run_opts &o, int sms, int *
     double cost = 0;
     auto fixed = [&](int k) {
         const LutNet &n = mp.variant(k);
-        *opt = k1_opt(mp, n, k, k1_slot(k1_threads(o, k)), P, sms, tput, &cost);
+        *opt = k1_opt(mp, n, mp.jk(n, k1_threads(o, k)), P, sms, tput, &cost);
         return k;
     };
-    if (o.flags & (ES_FLAG_K1T | ES_FLAG_K1U)) return fixed(0);
     if (o.cofactor_pis == ES_COFACTOR_NONE) return fixed(0);
     if (o.cofactor_pis > 0) {  // forced: any k the word PIs allow
         if (P - 5 < 1) return fixed(0);
@@ -1164,13 +1329,126 @@ static int choose_cofactors(MappedProg &mp, const es_run_opts &o, int sms, int *
     for (int k = 0; k <= kmax; ++k) {
         const LutNet &n = mp.variant(k);
         if ((int)n.cof_pis.size() != k) break;  // fewer candidate PIs than k
-        const int ok = k1_opt(mp, n, k, k1_slot(k1_threads(o, k)), P, sms, tput, &cost);
+        const int ok = k1_opt(mp, n, mp.jk(n, k1_threads(o, k)), P, sms, tput, &cost);
         if (cost < best_cost) { best_cost = cost; best = k; *opt = ok; worse = 0; }
         // latency mode: the JIT term grows with k, so two deeper variants that
         // do not pay end the search (mapping k=3..5 costs ~40 ms on mult16)
         else if (!tput && ++worse >= 2) break;
     }
     return best;
+}
+
+// Compile-or-fetch the K1 kernel of variant `n` and plan its sweep over the
+// devices of `cs` (chunk size for all of them).
+static int k1_plan_for(MappedProg &mp, const LutNet &n, const es_run_opts &o, int sms, int n_dev, int opt,
+                       K1Plan *pl, double *jit_ms) {
+    const int threads = k1_threads(o, (int)n.cof_pis.size());
+    JitKernel *&slot = mp.jk(n, threads);
+    if (slot && slot->opt < opt) slot = nullptr;  // tier-up: recompile at the higher level (old module stays cached)
+    int rc = k1_prepare(n, threads, sms, pl, jit_ms, slot, opt, n_dev);
+    if (rc == ES_OK) slot = pl->jk;
+    return rc;
+}
+
+// Whether variant `pl`'s chunks are contiguous pattern intervals: its
+// cofactor bits all lie inside a chunk.  If not (the cheapest cofactor PIs
+// are usually the top ones, e.g. the multiplier's b12..b15 = pattern bits
+// 28..31), a chunk spans every value of those bits, and a counterexample
+// above 2^28 leaves every chunk's first pattern below it: the skip rule can
+// never fire (config 5 cost 1.03x the full EQ sweep).
+static bool chunks_contiguous(const K1Plan &pl) {
+    for (int i = 0; i < pl.cof_n; ++i)
+        if ((int)pl.cof_pos[i] >= pl.chunk_log2 + 5 + pl.cof_n) return false;
+    return true;
+}
+
+// K1 run of variant `net` on the devices `cs`, minimum-index witness for any
+// cofactor set.  Non-contiguous chunks run in two phases:
+//   1. the fast variant, stopping at the FIRST counterexample w1 (hit_stop);
+//      if w1 lies below every chunk not yet swept, it is the minimum;
+//   2. otherwise the cheaper of (a) finishing phase 1's sweep with w1 as the
+//      running minimum, or (b) a variant whose cofactor PIs all lie below
+//      w1's top bit, whose chunks are ordered like w1's high bits, so its
+//      sweep stops after the ~w1/2^n of the space below w1.
+// The minimum over both phases is the reference's workers=1 witness.
+static int run_k1_job(MappedProg &mp, const LutNet &net, const es_run_opts &o, const std::vector<Ctx *> &cs,
+                      double deadline, int opt, es_result *r) {
+    NvtxRange nvtx("es_k1");
+    const int n_dev = (int)cs.size();
+    const int sms = cs[0]->sms;
+    const int P = net.num_pis, G = mp.G;
+    const uint64_t sentinel = 1ull << P;
+    const bool tput = o.cofactor_pis == ES_COFACTOR_THROUGHPUT;
+    K1Plan pl;
+    double jit_ms = 0;
+    int rc = k1_plan_for(mp, net, o, sms, n_dev, opt, &pl, &jit_ms);
+    if (rc != ES_OK) return rc;
+    r->engine = ES_ENGINE_JIT;
+    r->jit_ms += jit_ms;
+    r->regs_per_thread = pl.jk->regs;
+    r->cofactor_pis = pl.cof_n;
+    r->jit_opt = pl.jk->opt;
+    r->num_luts = (int)net.luts.size();
+    r->n_devices = n_dev;
+    r->phases = 1;
+    const bool two_phase = !chunks_contiguous(pl);
+    SweepOut s1;
+    rc = sweep_k1(pl, G, o, cs, deadline, 0, sentinel, two_phase ? sentinel : 0, &s1);
+    if (rc != ES_OK) return rc;
+    const bool proven = s1.best < sentinel && (s1.prefix >= pl.n_chunks || s1.best < pl.first_pattern(s1.prefix));
+    if (!two_phase || s1.stopped || s1.best >= sentinel || proven) {
+        if (two_phase && s1.best >= sentinel && !s1.stopped && s1.prefix < pl.n_chunks) {
+            // cannot happen: phase 1 only stops early on a hit
+            set_error("internal: phase 1 ended early without a counterexample");
+            return ES_E_CUDA;
+        }
+        k1_result(pl, s1, P, r);
+        return ES_OK;
+    }
+    // phase 2
+    r->phases = 2;
+    const uint64_t w1 = s1.best;
+    const double frac_left = 1.0 - (double)s1.prefix / (double)pl.n_chunks;
+    const double cost_a = frac_left * est_sweep_ms(net, P, sms * n_dev);
+    const int hb = 63 - __builtin_clzll(w1);  // PIs 6..hb have pattern bits below w1's top bit
+    const LutNet *best_net = nullptr;
+    double best_cost = cost_a;
+    for (int k = (int)net.cof_pis.size(); k >= 0; --k) {
+        if (hb < kLanePis + 1 + k) continue;
+        std::vector<int32_t> pis = mp.ranked(k, hb);
+        if ((int)pis.size() != k) continue;
+        const LutNet &cand = mp.variant_set(pis);
+        const double frac = std::min(1.0, std::ldexp((double)w1 + 1.0, -P) * 1.02);
+        double c = frac * est_sweep_ms(cand, P, sms * n_dev);
+        const JitKernel *have = mp.jk(cand, k1_threads(o, k));
+        if (!tput && !(have && have->opt >= opt)) c += est_jit_ms(cand, opt);
+        if (c < best_cost) { best_cost = c; best_net = &cand; }
+    }
+    SweepOut s2;
+    if (!best_net) {  // (a): finish phase 1's sweep, skipping chunks above w1
+        rc = sweep_k1(pl, G, o, cs, deadline, s1.prefix, w1, 0, &s2);
+        if (rc != ES_OK) return rc;
+        s2.swept += s1.swept;
+        s2.device_ms += s1.device_ms;
+        s2.launches += s1.launches;
+        s2.prefix = s2.stopped ? std::min(s1.prefix, s2.prefix) : pl.n_chunks;
+        k1_result(pl, s2, P, r);
+        return ES_OK;
+    }
+    // (b): the low-cofactor variant over the space below w1
+    K1Plan pl2;
+    double jit2 = 0;
+    rc = k1_plan_for(mp, *best_net, o, sms, n_dev, opt, &pl2, &jit2);
+    if (rc != ES_OK) return rc;
+    r->jit_ms += jit2;
+    rc = sweep_k1(pl2, G, o, cs, deadline, 0, w1, 0, &s2);
+    if (rc != ES_OK) return rc;
+    r->device_ms += s1.device_ms;
+    r->launches += s1.launches;
+    r->patterns_swept += std::min<uint64_t>(s1.swept * pl.patterns_per_chunk(), sentinel);
+    r->phase2_cofactor_pis = pl2.cof_n;
+    k1_result(pl2, s2, P, r);
+    return ES_OK;
 }
 
 int run_one(const es_prog *prog, const es_run_opts *opts, es_result *out) {
@@ -1195,9 +1473,18 @@ int run_one(const es_prog *prog, const es_run_opts *opts, es_result *out) {
     if (rc != ES_OK) return rc;
     const int G = mp->G;
     out->compile_ms = now_ms() - t0;
-    Ctx *c = nullptr;
-    rc = get_ctx(o.device, &c);
-    if (rc != ES_OK) return rc;
+    // one leased context per device of the run (the same ordinal may repeat)
+    const std::vector<int> devs = run_devices(o);
+    std::vector<std::unique_ptr<CtxLease>> leases;
+    std::vector<Ctx *> cs;
+    for (int d : devs) {
+        leases.emplace_back(new CtxLease());
+        rc = leases.back()->acquire(d);
+        if (rc != ES_OK) return rc;
+        cs.push_back(leases.back()->c);
+    }
+    Ctx *c = cs[0];
+    out->n_devices = 1;
     int engine = o.engine;
     if (engine == ES_ENGINE_AUTO) {
         // the interpreter beats JIT compile latency on small sweeps
@@ -1246,14 +1533,10 @@ int run_one(const es_prog *prog, const es_run_opts *opts, es_result *out) {
         std::lock_guard<std::mutex> lk(mp->mu);
         const double tc = now_ms();
         int opt = 3;
-        const int k = choose_cofactors(*mp, o, c->sms, &opt);
-        const int slot = k1_slot(k1_threads(o, k));
+        const int k = choose_cofactors(*mp, o, c->sms * (int)cs.size(), &opt);
         const LutNet &kn = mp->variant(k);
         out->compile_ms += now_ms() - tc;
-        out->num_luts = (int)kn.luts.size();
-        // tier-up: recompile at the higher level (the old module stays in the JIT cache)
-        if (mp->jk[k][slot] && mp->jk[k][slot]->opt < opt) mp->jk[k][slot] = nullptr;
-        rc = run_k1(kn, G, o, c, deadline, out, &mp->jk[k][slot], opt);
+        rc = run_k1_job(*mp, kn, o, cs, deadline, opt, out);
         mp->runs++;
     }
     out->wall_ms = now_ms() - t0;
@@ -1294,14 +1577,15 @@ int run_batch_jit(int n_jobs, const es_prog *progs, const es_run_opts *opts, es_
                 if (get_mapped(progs[i], &mp) == ES_OK) {
                     std::lock_guard<std::mutex> lk(mp->mu);
                     int opt = 3;
-                    const int k = choose_cofactors(*mp, o, sms, &opt);
+                    const int k = choose_cofactors(*mp, o, sms * (int)run_devices(o).size(), &opt);
                     const LutNet &net = mp->variant(k);
-                    const int threads = k1_threads(o, k), slot = k1_slot(threads);
-                    if (!(mp->jk[k][slot] && mp->jk[k][slot]->opt >= opt)) {
+                    const int threads = k1_threads(o, k);
+                    JitKernel *&have = mp->jk(net, threads);
+                    if (!(have && have->opt >= opt)) {
                         JitKernel *jk = nullptr;
                         double ms = 0;
                         std::string err;
-                        if (jit_get(net, threads, &jk, &ms, &err, opt) == ES_OK) mp->jk[k][slot] = jk;
+                        if (jit_get(net, threads, &jk, &ms, &err, opt) == ES_OK) have = jk;
                     }
                 }
             }
@@ -1343,9 +1627,10 @@ int run_batch(int n_jobs, const es_prog *progs, const es_run_opts *opts, es_resu
         if (!constant_rail(progs[j], &outs[j])) active.push_back(j);
     }
     if (active.empty()) return ES_OK;
-    Ctx *c = nullptr;
-    int rc = get_ctx(o.device, &c);
+    CtxLease lease;
+    int rc = lease.acquire(o.device);
     if (rc != ES_OK) return rc;
+    Ctx *c = lease.c;
     int reason = 0;
     if (stop_requested(o, deadline, &reason)) {
         for (int j : active) { outs[j].verdict = ES_BUDGET_EXCEEDED; outs[j].reason = reason; }
@@ -1387,9 +1672,10 @@ int session_open(const es_prog *prog, const es_run_opts *opts, void **out) {
     std::string err;
     rc = build_dag(*prog, &dag, &err);
     if (rc != ES_OK) { set_error(err); return rc; }
-    Ctx *c = nullptr;
-    rc = get_ctx(o.device, &c);
+    CtxLease lease;
+    rc = lease.acquire(o.device);
     if (rc != ES_OK) return rc;
+    Ctx *c = lease.c;
     Session *s = new Session();
     s->dev = o.device;
     s->num_pis = prog->num_pis;
@@ -1443,9 +1729,10 @@ void session_close(void *sp) {
 }
 
 int alu_peak(int dev, double *lane_ops_per_s, double *ms_out) {
-    Ctx *c = nullptr;
-    int rc = get_ctx(dev, &c);
+    CtxLease lease;
+    int rc = lease.acquire(dev);
     if (rc != ES_OK) return rc;
+    Ctx *c = lease.c;
     const int threads = 256, iters = 4096;
     const int grid = c->sms * 8;
     unsigned *sink = c->d_counter + 8;
@@ -1464,9 +1751,10 @@ int alu_peak(int dev, double *lane_ops_per_s, double *ms_out) {
 }
 
 int smem_peak(int dev, double *bytes_per_s, double *ms_out) {
-    Ctx *c = nullptr;
-    int rc = get_ctx(dev, &c);
+    CtxLease lease;
+    int rc = lease.acquire(dev);
     if (rc != ES_OK) return rc;
+    Ctx *c = lease.c;
     const int threads = 256, iters = 2048;
     const int grid = c->sms * 8;
     unsigned *sink = c->d_counter + 8;
@@ -1519,7 +1807,8 @@ int word_io(int dev, void *ptr, uint64_t *value, int write) {
 }
 
 void runtime_shutdown() {
-    for (Ctx *c : t_ctx) {
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    for (Ctx *c : g_ctx_all) {
         cudaSetDevice(c->dev);
         cudaStreamDestroy(c->stream);
         cudaFree(c->d_best);
@@ -1536,7 +1825,8 @@ void runtime_shutdown() {
         }
         delete c;
     }
-    t_ctx.clear();
+    g_ctx_all.clear();
+    g_ctx_free.clear();
     {
         std::lock_guard<std::mutex> lk(g_mapped_mu);
         g_mapped.clear();

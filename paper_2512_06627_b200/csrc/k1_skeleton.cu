@@ -26,21 +26,22 @@
 // so the claim order and the skip rule keep the minimum-index guarantee.
 //
 // Multi-GPU: chunk ids of one launch are first_chunk + k*world, k < n_slots
-// (the host puts this rank's residue class in first_chunk).  `best` is the
-// rank-local copy of the global minimum, reduced across ranks between
-// launches.
+// (the host puts this device's residue class in first_chunk).  `best` is one
+// word in device 0's HBM that every GPU's kernels atomicMin into as peer
+// memory (system scope), or a device-local copy combined by the host between
+// launch slices when peer access is unavailable.
 
 struct K1Params {
     unsigned long long *best;      // min failing pattern, sentinel 2^n
-    unsigned int *counter;         // chunk claim counter, zeroed before launch
+    unsigned int *counter;         // [0] chunk claims, [1] chunks swept; zeroed before launch
     unsigned long long first_chunk;
     unsigned long long n_slots;    // chunks this launch may claim
     unsigned long long world;      // chunk stride between claims
+    unsigned long long hit_stop;   // stop claiming once *best < hit_stop (0: never)
     unsigned long long total_words;
     unsigned int chunk_log2;       // words per chunk = 2^chunk_log2 (>= blockDim)
     unsigned int valid_mask;       // pattern bits of a word that exist (n < 5)
     unsigned int one;              // == 1, opaque to ptxas (IMAD coefficients)
-    unsigned int region_bytes;     // K1T: shared bytes per warp (boundary super-words)
     unsigned int cof_n;            // cofactor PIs (2^cof_n copies per iteration)
     unsigned int cof_pos[8];       // their pattern-bit positions (PI - 1), ascending
 };
@@ -81,7 +82,12 @@ es_k1(const K1Params p)
 #else
                 const unsigned long long first_pattern = es_expand((c << p.chunk_log2) << 5, p);
 #endif
-                if (first_pattern > *(volatile unsigned long long *)p.best) c = ~0ull;
+                const unsigned long long b = *(volatile unsigned long long *)p.best;
+                // skip rule: every pattern of this chunk (and of every later
+                // one) lies above the minimum; phase 1 of a non-equivalent
+                // search (hit_stop) also stops at the first counterexample
+                if (first_pattern > b || b < p.hit_stop) c = ~0ull;
+                else atomicAdd(p.counter + 1, 1u);
             }
             s_chunk = c;
         }

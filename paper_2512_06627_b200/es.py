@@ -229,9 +229,6 @@ class _CancelWatcher:
         return ctypes.addressof(self.flag) if self.cancel is not None else None
 
 
-KERNEL_VARIANTS = {"k1": 0, "k1t": 4, "k1u": 8}  # es_run_opts.flags (ES_FLAG_K1T / _K1U)
-
-
 def _cofactor_code(cofactor) -> int:
     if isinstance(cofactor, str):
         return N.COFACTOR_MODES[cofactor]
@@ -242,7 +239,7 @@ def _cofactor_code(cofactor) -> int:
 
 
 def _opts(device: int, engine: str, budget: float | None, cancel_addr, slice_ms: float,
-          block_threads: int, variant: str = "k1", cofactor="auto") -> N.EsRunOpts:
+          block_threads: int, cofactor="auto", devices: Sequence[int] | None = None) -> N.EsRunOpts:
     o = N.EsRunOpts()
     o.device = device
     o.engine = N.ENGINES[engine]
@@ -250,8 +247,13 @@ def _opts(device: int, engine: str, budget: float | None, cancel_addr, slice_ms:
     o.cancel_flag = cancel_addr
     o.slice_ms = slice_ms
     o.block_threads = block_threads
-    o.flags = KERNEL_VARIANTS[variant]
+    o.flags = 0
     o.cofactor_pis = _cofactor_code(cofactor)
+    if devices:
+        arr = (ctypes.c_int32 * len(devices))(*[int(d) for d in devices])
+        o.n_devices = len(devices)
+        o.devices = ctypes.cast(arr, ctypes.c_void_p)
+        o._devices_keepalive = arr  # the array must outlive the call
     return o
 
 
@@ -262,7 +264,8 @@ def _stats_of(r: N.EsResult) -> dict:
             "engine_wall_ms": r.wall_ms, "launches": int(r.launches),
             "regs_per_thread": int(r.regs_per_thread), "cofactor_pis": int(r.cofactor_pis),
             "jit_opt": int(r.jit_opt), "witness_minimal": bool(r.witness_minimal),
-            "n_devices": int(r.n_devices)}
+            "n_devices": int(r.n_devices), "phases": int(r.phases),
+            "phase2_cofactor_pis": int(r.phase2_cofactor_pis) if r.phases == 2 else None}
 
 
 def _to_esresult(r: N.EsResult, num_pis: int) -> EsResult:
@@ -276,7 +279,8 @@ def _to_esresult(r: N.EsResult, num_pis: int) -> EsResult:
 
 def run_exhaustive(p, workers: int = 1, budget: float | None = None, cancel=None, *,
                    device: int = 0, engine: str = "auto", slice_ms: float = 20.0,
-                   block_threads: int = 0, variant: str = "k1", cofactor="auto") -> EsResult:
+                   block_threads: int = 0, cofactor="auto",
+                   devices: Sequence[int] | None = None) -> EsResult:
     """Sweep all 2^num_pis assignments on the GPU (es.py:252-339).
 
     Returns the minimum-index counterexample (the reference's workers=1
@@ -287,6 +291,12 @@ def run_exhaustive(p, workers: int = 1, budget: float | None = None, cancel=None
     (and tiers up when a program is re-run), "throughput" picks the fastest
     sweep, "none" or 0 disables, 1..5 forces that many cofactor PIs.  The
     result is the same for every setting.
+
+    ``devices``: sweep on these CUDA ordinals at once (the reference's
+    ``workers``, es.py:272-331, as GPUs): chunks of the pattern space are
+    dealt round-robin, one host thread drives each device, and one minimum
+    word shared over NVLink stops every GPU once a smaller pattern cannot
+    exist.  ``"all"`` = every visible GPU.  Default: ``device`` alone.
     """
     if workers < 1:
         raise ValueError("workers must be >= 1")
@@ -300,7 +310,8 @@ def run_exhaustive(p, workers: int = 1, budget: float | None = None, cancel=None
             return EsResult(BUDGET_EXCEEDED, patterns_evaluated=0)
     res = N.EsResult()
     with _CancelWatcher(cancel) as cw:
-        opts = _opts(device, engine, budget, cw.address, slice_ms, block_threads, variant, cofactor)
+        opts = _opts(device, engine, budget, cw.address, slice_ms, block_threads, cofactor,
+                     _devices(devices))
         N.check(N.lib().es_run(ctypes.byref(prog.as_struct()), ctypes.byref(opts),
                                ctypes.byref(res)))
     return _to_esresult(res, prog.num_pis)
@@ -318,8 +329,32 @@ def _recheck(xag, witness) -> int:
                                        in1.ctypes.data, o.node * 2 + int(o.neg), idx))
 
 
+def device_count() -> int:
+    """Visible CUDA devices (0 without a driver)."""
+    n = ctypes.c_int32()
+    N.check(N.lib().es_device_count(ctypes.byref(n)))
+    return n.value
+
+
+def _devices(devices) -> list[int] | None:
+    if devices is None:
+        return None
+    if isinstance(devices, str):
+        if devices != "all":
+            raise ValueError("devices must be a sequence of ordinals or 'all'")
+        n = device_count()
+        if n < 1:
+            raise N.NativeError(N.ES_E_NO_DEVICE, "no CUDA device visible")
+        return list(range(n))
+    d = [int(x) for x in devices]
+    if not d:
+        raise ValueError("devices must not be empty")
+    return d
+
+
 def es_check(sm, workers: int = 1, budget: float | None = None, cancel=None, *,
-             device: int = 0, engine: str = "auto", cofactor="auto") -> CheckResult:
+             device: int = 0, engine: str = "auto", cofactor="auto",
+             devices: Sequence[int] | str | None = None) -> CheckResult:
     """Compile and sweep a sub-miter (es.py:342-365); witnesses are re-checked
     by direct evaluation and a mismatch raises AssertionError."""
     t0 = time.monotonic()
@@ -328,7 +363,7 @@ def es_check(sm, workers: int = 1, budget: float | None = None, cancel=None, *,
     except TooManyInputs:
         return CheckResult(UNKNOWN, reason="ineligible", engine="es")
     r = run_exhaustive(prog, workers=workers, budget=budget, cancel=cancel, device=device,
-                       engine=engine, cofactor=cofactor)
+                       engine=engine, cofactor=cofactor, devices=devices)
     stats = {"patterns": r.patterns_evaluated, "registers": prog.num_registers,
              "wall_time": time.monotonic() - t0, **r.stats}
     if r.verdict == EXHAUSTED_ZERO:

@@ -25,14 +25,12 @@ from .es import (BUDGET_EXCEEDED, ES_COUNTEREXAMPLE, EXHAUSTED_ZERO, EsResult, a
 class Session:
     """A program JIT-compiled for one device, launchable on any stream."""
 
-    def __init__(self, prog, device: int = 0, block_threads: int = 0, variant: str = "k1",
-                 cofactor="throughput"):
+    def __init__(self, prog, device: int = 0, block_threads: int = 0, cofactor="throughput"):
         self.prog = as_program(prog)
         self.device = device
-        self.variant = variant
         # sessions serve repeated / long sharded sweeps: default to the fastest
         # K1 variant (es_run_opts.cofactor_pis); the JIT is paid once per session
-        opts = _opts(device, "jit", None, None, 20.0, block_threads, variant, cofactor)
+        opts = _opts(device, "jit", None, None, 20.0, block_threads, cofactor)
         h = ctypes.c_void_p()
         N.check(N.lib().es_session_open(ctypes.byref(self.prog.as_struct()), ctypes.byref(opts),
                                         ctypes.byref(h)))

@@ -61,22 +61,6 @@ def test_jit_block_sizes(golden, gpu, block):
         _check(r, g, (name, block))
 
 
-@pytest.mark.parametrize("variant", ["k1t", "k1u"])
-def test_experimental_k1_variants(golden, gpu, variant):
-    """K1T (transposed word-uniform phase) and K1U (warp-uniform super-words)
-    are bit-exact on the config miters and deep faults."""
-    specs = {s["name"]: s for s in recipes.miter_population()}
-    names = ["mult12_array_wallace", "mult12_array_wallace_flip1108", "mult10_array_booth",
-             "mult8_array_diagonal_mut3", "adder8_ripple_lookahead", "mult16_array_booth_flip1220",
-             "mult14_array_diagonal"]
-    for g in golden["miters"]:
-        if g["name"] not in names:
-            continue
-        x = recipes.build_miter_recipe(specs[g["name"]])
-        r = es.run_exhaustive(es.compile_program(x), engine="jit", variant=variant)
-        _check(r, g, (g["name"], variant))
-
-
 def test_imad_offload_random(golden, gpu):
     """IMAD-mapped LUTs (f(x, word PI)) on random XAGs with many word PIs."""
     for g in golden["random"]:

@@ -37,14 +37,6 @@ def test_unsupported_block_size():
         es.emit_ptx(p, 96)
 
 
-@pytest.mark.parametrize("variant", [32, -128])
-def test_experimental_variants_compile(variant):
-    """K1U (32) and K1T (-128) skeletons: PTX splices and compiles, no spills."""
-    p = es.compile_program(M.gen_multiplier_miter(12, "array", "wallace"))
-    j = es.jit_check(p, block_threads=variant)
-    assert j["cubin_bytes"] > 0 and j["spill_bytes"] == 0
-
-
 def test_throughput_kernel_mult16_k4_has_no_spills():
     """The bench's kernel (mult16, 4 cofactor PIs, 256-thread CTAs): with the
     copies visited in bit-reversed order the schedule's live set is ~212
