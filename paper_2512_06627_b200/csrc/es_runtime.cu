@@ -507,7 +507,8 @@ int k1_prepare(const LutNet &net, int threads, int sms, K1Plan *pl, double *jit_
     return ES_OK;
 }
 
-// counter: two words, [0] claims and [1] chunks swept, zeroed here
+// counter: three words, [0] claims, [1] chunks swept (zeroed here) and [2]
+// the lowest slot a hit_stop launch left unswept (set to ~0 here)
 int k1_launch(const K1Plan &pl, cudaStream_t st, unsigned long long *best, unsigned *counter,
               uint64_t first_chunk, uint64_t n_slots, uint64_t world, uint64_t hit_stop = 0) {
     K1Params kp;
@@ -524,6 +525,7 @@ int k1_launch(const K1Plan &pl, cudaStream_t st, unsigned long long *best, unsig
     kp.cof_n = (unsigned)pl.cof_n;
     for (int i = 0; i < 8; ++i) kp.cof_pos[i] = pl.cof_pos[i];
     CK(cudaMemsetAsync(counter, 0, 2 * sizeof(unsigned), st));
+    CK(cudaMemsetAsync(counter + 2, 0xFF, sizeof(unsigned), st));
     void *args[] = {&kp};
     const int grid = (int)std::min<uint64_t>((uint64_t)pl.grid, std::max<uint64_t>(n_slots, 1));
     CK(cudaLaunchKernel((const void *)pl.jk->kernel, dim3(grid), dim3(pl.threads), args, pl.smem, st));
@@ -646,11 +648,16 @@ static int sweep_k1(const K1Plan &pl, int G, const es_run_opts &o, const std::ve
         std::vector<uint64_t> slice_end;
         int my = 0;
         if (cudaEventRecord(c->ev_start, c->stream) != cudaSuccess) { fail(cuda_fail(cudaGetLastError(), "event")); return; }
-        unsigned *h_swept = reinterpret_cast<unsigned *>(c->h_pin + 4);  // per slice: chunks swept
-        auto harvest = [&](int q, uint64_t end) {  // slice q's copies have landed
+        // per slice q: h_cnt[4q + 1] chunks swept, h_cnt[4q + 2] first slot left by hit_stop
+        unsigned *h_cnt = reinterpret_cast<unsigned *>(c->h_pin + 4);
+        std::vector<uint64_t> slice_begin;
+        auto harvest = [&](int q, uint64_t b0, uint64_t end) {  // slice q's copies have landed
             lower(c->h_pin[1 + q]);
-            swept.fetch_add(h_swept[q]);
-            progress[d].store(end);
+            swept.fetch_add(h_cnt[4 * q + 1]);
+            // every slot below the first one hit_stop skipped was swept (the
+            // claims are in slot order); later ones only by chance
+            const uint64_t cut = h_cnt[4 * q + 2] == ~0u ? end : std::min<uint64_t>(end, b0 + h_cnt[4 * q + 2]);
+            if (cut > progress[d].load()) progress[d].store(cut);
             if (settled()) done.store(true);
         };
         for (uint64_t b = 0; b < slots[d] && !done.load(); b += per_slice) {
@@ -673,27 +680,28 @@ static int sweep_k1(const K1Plan &pl, int G, const es_run_opts &o, const std::ve
                     es_word_min_kernel<<<1, 1, 0, c->stream>>>(c->d_best, c->d_best + 1);
                 }
             }
-            int rc = k1_launch(pl, c->stream, word[d], c->d_counter + 2 * s, begin + d + b * n, ns,
+            int rc = k1_launch(pl, c->stream, word[d], c->d_counter + 4 * s, begin + d + b * n, ns,
                                (uint64_t)n, hit_stop);
             if (rc != ES_OK) { fail(rc); return; }
             if (cudaMemcpyAsync(c->h_pin + 1 + s, word[d], 8, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
-                cudaMemcpyAsync(h_swept + s, c->d_counter + 2 * s + 1, 4, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+                cudaMemcpyAsync(h_cnt + 4 * s, c->d_counter + 4 * s, 12, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
                 cudaEventRecord(c->ev_slice[s], c->stream) != cudaSuccess) {
                 fail(cuda_fail(cudaGetLastError(), "slice bookkeeping")); return;
             }
+            slice_begin.push_back(b);
             slice_end.push_back(b + ns);
             ++my;
             launches.fetch_add(1);
             if (my >= 2) {  // two slices in flight; inspect the older one
                 const int q = (my - 2) & 1;
                 if (cudaEventSynchronize(c->ev_slice[q]) != cudaSuccess) { fail(cuda_fail(cudaGetLastError(), "sync")); return; }
-                harvest(q, slice_end[my - 2]);
+                harvest(q, slice_begin[my - 2], slice_end[my - 2]);
             }
         }
         if (cudaEventRecord(c->ev_stop, c->stream) != cudaSuccess || cudaStreamSynchronize(c->stream) != cudaSuccess) {
             fail(cuda_fail(cudaGetLastError(), "cudaStreamSynchronize")); return;
         }
-        if (my > 0) harvest((my - 1) & 1, slice_end[my - 1]);
+        if (my > 0) harvest((my - 1) & 1, slice_begin[my - 1], slice_end[my - 1]);
         float ms = 0;
         cudaEventElapsedTime(&ms, c->ev_start, c->ev_stop);
         dev_ms[d] = ms;

@@ -33,7 +33,7 @@
 
 struct K1Params {
     unsigned long long *best;      // min failing pattern, sentinel 2^n
-    unsigned int *counter;         // [0] chunk claims, [1] chunks swept; zeroed before launch
+    unsigned int *counter;         // [0] claims, [1] chunks swept, [2] first slot hit_stop skipped
     unsigned long long first_chunk;
     unsigned long long n_slots;    // chunks this launch may claim
     unsigned long long world;      // chunk stride between claims
@@ -84,10 +84,18 @@ es_k1(const K1Params p)
 #endif
                 const unsigned long long b = *(volatile unsigned long long *)p.best;
                 // skip rule: every pattern of this chunk (and of every later
-                // one) lies above the minimum; phase 1 of a non-equivalent
-                // search (hit_stop) also stops at the first counterexample
-                if (first_pattern > b || b < p.hit_stop) c = ~0ull;
-                else atomicAdd(p.counter + 1, 1u);
+                // one) lies above the minimum.  Phase 1 of a non-equivalent
+                // search (hit_stop) also stops at the first counterexample and
+                // records the lowest slot it left unswept: the host's proof
+                // only counts the slots below it as swept
+                if (first_pattern > b) {
+                    c = ~0ull;
+                } else if (b < p.hit_stop) {
+                    atomicMin(p.counter + 2, (unsigned)k);
+                    c = ~0ull;
+                } else {
+                    atomicAdd(p.counter + 1, 1u);
+                }
             }
             s_chunk = c;
         }
