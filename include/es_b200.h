@@ -247,6 +247,16 @@ int32_t es_ipc_open(int32_t device, const uint8_t *handle64, void **dev_ptr);
 int32_t es_ipc_close(int32_t device, void *dev_ptr, int32_t owner);
 int32_t es_word_write(int32_t device, void *dev_ptr, uint64_t value);
 int32_t es_word_read(int32_t device, void *dev_ptr, uint64_t *value);
+/* Device-side verdict barrier on an exchange slot ([0] minimum word, [8]
+ * arrival counter; es_ipc_alloc'd): enqueued on `stream` after a rank's
+ * es_session_launch, es_peer_arrive_wait counts the rank in, waits on the
+ * device until all `world` ranks have, and writes the final minimum to
+ * out_dev (device or mapped memory) -- no host synchronisation, no
+ * collective.  es_peer_arm re-arms a slot (minimum all-ones, counter 0);
+ * rank 0 arms the slot of verdict s+1 while verdict s runs (three slots
+ * rotate: the armed one was last used at verdict s-2). */
+int32_t es_peer_arm(void *stream, void *word_dev);
+int32_t es_peer_arrive_wait(void *stream, void *word_dev, int32_t world, void *out_dev);
 
 /*
  * K3: word-parallel random simulation (the sweep's

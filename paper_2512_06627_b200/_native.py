@@ -41,7 +41,7 @@ EXPORTS = ("es_compile", "es_run", "es_run_batch", "es_session_open", "es_sessio
            "es_sim", "es_sim_ones", "es_sim_device", "es_sim_prog_free", "es_sim_classes", "es_sim_levels",
            "es_aiger_parse", "es_detect_xors", "es_xag_size", "es_xag_read", "es_xag_free",
            "es_aiger_write",
-           "es_device_count", "es_last_error", "es_version", "es_shutdown")
+           "es_peer_arm", "es_peer_arrive_wait", "es_device_count", "es_last_error", "es_version", "es_shutdown")
 
 _P = ctypes.c_void_p
 
@@ -104,6 +104,10 @@ def lib():
         L.es_run_batch.argtypes = [ctypes.c_int32, ctypes.POINTER(EsProg),
                                    ctypes.POINTER(EsRunOpts), ctypes.POINTER(EsResult)]
         L.es_run_batch.restype = ctypes.c_int32
+        L.es_peer_arm.argtypes = [_P, _P]
+        L.es_peer_arm.restype = ctypes.c_int32
+        L.es_peer_arrive_wait.argtypes = [_P, _P, ctypes.c_int32, _P]
+        L.es_peer_arrive_wait.restype = ctypes.c_int32
         L.es_device_count.argtypes = [ctypes.POINTER(ctypes.c_int32)]
         L.es_device_count.restype = ctypes.c_int32
         L.es_session_open.argtypes = [ctypes.POINTER(EsProg), ctypes.POINTER(EsRunOpts),

@@ -36,6 +36,8 @@ int ipc_alloc(int dev, void **ptr, unsigned char *handle);
 int ipc_open(int dev, const unsigned char *handle, void **ptr);
 int ipc_close(int dev, void *ptr, int owner);
 int word_io(int dev, void *ptr, uint64_t *value, int write);
+int peer_arm(void *stream, void *word);
+int peer_arrive_wait(void *stream, void *word, int world, void *out);
 int sim_run(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
             const uint32_t *in1, const uint64_t *pi_words, int64_t words, int32_t device,
             uint64_t *node_words, double *device_ms);
@@ -612,6 +614,16 @@ int32_t es_ipc_close(int32_t device, void *dev_ptr, int32_t owner) {
 
 int32_t es_word_write(int32_t device, void *dev_ptr, uint64_t value) {
     return word_io(device, dev_ptr, &value, 1);
+}
+
+int32_t es_peer_arm(void *stream, void *word_dev) {
+    if (!word_dev) { set_error("null word"); return ES_E_BAD_ARG; }
+    return peer_arm(stream, word_dev);
+}
+
+int32_t es_peer_arrive_wait(void *stream, void *word_dev, int32_t world, void *out_dev) {
+    if (!word_dev || !out_dev) { set_error("null argument"); return ES_E_BAD_ARG; }
+    return peer_arrive_wait(stream, word_dev, world, out_dev);
 }
 
 int32_t es_word_read(int32_t device, void *dev_ptr, uint64_t *value) {

@@ -1358,6 +1358,29 @@ static int k1_plan_for(MappedProg &mp, const LutNet &n, const es_run_opts &o, in
     return rc;
 }
 
+// Fraction of a variant's kernel words whose first pattern (cofactor bits
+// zero) is <= w: the part of the space a sweep with running minimum w must
+// visit (first patterns are monotone in the word index: binary search).
+static double frac_at_or_below(const std::vector<int32_t> &pis, int P, uint64_t w) {
+    const int k = (int)pis.size();
+    const int bits = std::max(P - 5 - k, 0);
+    auto first = [&](uint64_t x) {
+        x <<= 5;
+        for (int32_t j : pis) {  // ascending pattern bits j-1
+            const unsigned s = (unsigned)(j - 1);
+            x = ((x >> s) << (s + 1)) | (x & ((1ull << s) - 1ull));
+        }
+        return x;
+    };
+    uint64_t lo = 0, hi = 1ull << bits;  // count of x with first(x) <= w, in [lo, hi]
+    if (first(0) > w) return 0.0;
+    while (hi - lo > 1) {
+        const uint64_t mid = lo + (hi - lo) / 2;
+        if (first(mid) <= w) lo = mid; else hi = mid;
+    }
+    return std::ldexp((double)(lo + 1), -bits);
+}
+
 // Whether variant `pl`'s chunks are contiguous pattern intervals: its
 // cofactor bits all lie inside a chunk.  If not (the cheapest cofactor PIs
 // are usually the top ones, e.g. the multiplier's b12..b15 = pattern bits
@@ -1418,20 +1441,26 @@ static int run_k1_job(MappedProg &mp, const LutNet &net, const es_run_opts &o, c
     const uint64_t w1 = s1.best;
     const double frac_left = 1.0 - (double)s1.prefix / (double)pl.n_chunks;
     const double cost_a = frac_left * est_sweep_ms(net, P, sms * n_dev);
-    const int hb = 63 - __builtin_clzll(w1);  // PIs 6..hb have pattern bits below w1's top bit
+    // candidates: the cheapest PIs below one of w1's top set bits (PI j is
+    // pattern bit j-1, so "PIs <= b" keeps every cofactor bit below bit b),
+    // at the same depth or one less; cost = the exact fraction of the space
+    // whose chunks start at or below w1, times the variant's sweep estimate
+    std::vector<int> tops;
+    for (int b = 63 - __builtin_clzll(w1); b >= kLanePis + 1 && tops.size() < 3; --b)
+        if ((w1 >> b) & 1ull) tops.push_back(b);
     const LutNet *best_net = nullptr;
     double best_cost = cost_a;
-    for (int k = (int)net.cof_pis.size(); k >= 0; --k) {
-        if (hb < kLanePis + 1 + k) continue;
-        std::vector<int32_t> pis = mp.ranked(k, hb);
-        if ((int)pis.size() != k) continue;
-        const LutNet &cand = mp.variant_set(pis);
-        const double frac = std::min(1.0, std::ldexp((double)w1 + 1.0, -P) * 1.02);
-        double c = frac * est_sweep_ms(cand, P, sms * n_dev);
-        const JitKernel *have = mp.jk(cand, k1_threads(o, k));
-        if (!tput && !(have && have->opt >= opt)) c += est_jit_ms(cand, opt);
-        if (c < best_cost) { best_cost = c; best_net = &cand; }
-    }
+    const int k0 = (int)net.cof_pis.size();
+    for (int max_pi : tops)
+        for (int k = k0; k >= std::max(0, k0 - 1); --k) {
+            std::vector<int32_t> pis = mp.ranked(k, max_pi);
+            if ((int)pis.size() != k) continue;
+            const LutNet &cand = mp.variant_set(pis);
+            double c = frac_at_or_below(pis, P, w1) * est_sweep_ms(cand, P, sms * n_dev);
+            const JitKernel *have = mp.jk(cand, k1_threads(o, k));
+            if (!tput && !(have && have->opt >= opt)) c += est_jit_ms(cand, opt);
+            if (c < best_cost) { best_cost = c; best_net = &cand; }
+        }
     SweepOut s2;
     if (!best_net) {  // (a): finish phase 1's sweep, skipping chunks above w1
         rc = sweep_k1(pl, G, o, cs, deadline, s1.prefix, w1, 0, &s2);
@@ -1782,6 +1811,49 @@ int smem_peak(int dev, double *bytes_per_s, double *ms_out) {
 // ---------------------------------------------------------------------------
 // cross-process shared minimum word (CUDA IPC; NVLink peer memory across GPUs)
 // ---------------------------------------------------------------------------
+// Layout of one exchange slot: [0] the minimum word, [8] the arrival counter.
+// Device-side verdict barrier: after its sweep kernel (same stream), every
+// rank's es_peer_arrive adds one to the counter with system scope, waits
+// until all `world` ranks have arrived, then copies the final minimum to
+// `out` -- no host round trip and no collective between verdicts, so the
+// host can queue verdict after verdict.  Rank 0 re-arms the slot two
+// verdicts ahead (es_peer_arm): every rank has passed that slot's barrier
+// before rank 0 can pass the previous one.
+__global__ void es_peer_arm_kernel(unsigned long long *word) {
+    word[0] = ~0ull;
+    reinterpret_cast<unsigned *>(word + 1)[0] = 0u;
+    __threadfence_system();
+}
+
+__global__ void es_peer_arrive_kernel(unsigned long long *word, unsigned world, unsigned long long *out) {
+    unsigned *counter = reinterpret_cast<unsigned *>(word + 1);
+    __threadfence_system();  // this rank's sweep (stream-ordered before us) is complete
+    atomicAdd_system(counter, 1u);
+    unsigned v;
+    for (;;) {
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+        if (v >= world) break;
+        __nanosleep(100);
+    }
+    unsigned long long w;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(w) : "l"(word) : "memory");
+    *out = w;
+}
+
+int peer_arm(void *stream, void *word) {
+    es_peer_arm_kernel<<<1, 1, 0, (cudaStream_t)stream>>>((unsigned long long *)word);
+    CK(cudaGetLastError());
+    return ES_OK;
+}
+
+int peer_arrive_wait(void *stream, void *word, int world, void *out) {
+    if (world < 1) { set_error("bad world size"); return ES_E_BAD_ARG; }
+    es_peer_arrive_kernel<<<1, 1, 0, (cudaStream_t)stream>>>((unsigned long long *)word, (unsigned)world,
+                                                            (unsigned long long *)out);
+    CK(cudaGetLastError());
+    return ES_OK;
+}
+
 int ipc_alloc(int dev, void **ptr, unsigned char *handle) {
     CK(cudaSetDevice(dev));
     CK(cudaMalloc(ptr, 256));

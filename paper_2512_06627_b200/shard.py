@@ -182,16 +182,20 @@ def es_check_sharded(sm, group=None, device: int | None = None,
 
 
 class PeerBest:
-    """The NVLink-native exchange: ONE minimum word in rank 0's
+    """The NVLink-native exchange: minimum words in rank 0's
     device memory, mapped into every rank through CUDA IPC.  Every rank's
-    kernel atomicMin's (system scope) into it and reads it at each chunk
-    claim, so a counterexample found on any GPU stops every GPU at its next
-    chunk -- no per-slice collective on the data path.  Three words rotate
-    between verdicts: rank 0 re-arms the word of verdict s+1 while verdict s
-    runs, and that word was last read at verdict s-2, before the barrier that
-    closed verdict s-1 -- so one barrier per verdict suffices.  Words are
-    armed with all-ones (no pattern index reaches it), so one PeerBest serves
-    programs of any PI count.  Collective constructor (every rank of ``group``)."""
+    kernel atomicMin's (system scope) into the verdict's word and reads it at
+    each chunk claim, so a counterexample found on any GPU stops every GPU at
+    its next chunk -- no collective on the data path.  Each word carries an
+    arrival counter: after its sweep a rank's stream runs es_peer_arrive_wait
+    (a one-thread kernel: count in, wait on the device for all ranks, copy
+    the final minimum out), so a verdict needs no host barrier and the host
+    can queue verdicts back to back.  Three words rotate: rank 0 re-arms the
+    word of verdict s+1 on its stream while verdict s runs; that word was
+    last used by verdict s-2, whose device barrier every rank passed before
+    any rank could finish verdict s-1.  Words are armed with all-ones (no
+    pattern index reaches it), so one PeerBest serves programs of any PI
+    count.  Collective constructor (every rank of ``group``)."""
 
     NONE = 0xFFFFFFFFFFFFFFFF  # "no counterexample yet"
     WORDS = 3
@@ -211,8 +215,9 @@ class PeerBest:
             ptr = ctypes.c_void_p()
             handle = (ctypes.c_uint8 * 64)()
             if self.rank == 0:
+                # zero-filled: arrival counter 0; the word is armed before it is shared
                 N.check(L.es_ipc_alloc(self.device, ctypes.byref(ptr), handle))
-                N.check(L.es_word_write(self.device, ptr, self.NONE))  # armed before it is shared
+                N.check(L.es_word_write(self.device, ptr, self.NONE))
             box = [bytes(handle)]
             if self.world > 1:
                 dist.broadcast_object_list(box, src=0, group=group)
@@ -220,6 +225,8 @@ class PeerBest:
                 h = (ctypes.c_uint8 * 64).from_buffer_copy(box[0])
                 N.check(L.es_ipc_open(self.device, h, ctypes.byref(ptr)))
             self.ptrs.append(ptr)
+        if self.world > 1:
+            dist.barrier(group=group)  # every rank has mapped the words
 
     def write(self, k: int, value: int) -> None:
         N.check(N.lib().es_word_write(self.device, self.ptrs[k], value))
@@ -230,45 +237,77 @@ class PeerBest:
         return v.value
 
     def close(self) -> None:
+        """Collective: no rank may still be using rank 0's words."""
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.synchronize(self.device)
+        if self.world > 1:
+            dist.barrier(group=self.group)
         for p in self.ptrs:
             if p:
                 N.lib().es_ipc_close(self.device, p, 1 if self.rank == 0 else 0)
         self.ptrs = []
 
 
-def sweep_peer(prog, peer: PeerBest, group=None, device: int | None = None,
-               cofactor="throughput") -> EsResult:
-    """run_exhaustive sharded over ``group`` with the shared peer word
-    (collective call; same program on every rank).  One launch per rank over
-    its residue class of chunks; one barrier per verdict, no all-reduce."""
-    import torch
-    import torch.distributed as dist
-
-    p = as_program(prog)
-    world, rank = peer.world, peer.rank
-    dev = peer.device if device is None else device
+def _constant_rail(p) -> EsResult | None:
     last = len(p) - 1
     if p.src0[last] < 0:  # constant rail, es.py:265-270
         if p.neg0[last]:
             return EsResult(ES_COUNTEREXAMPLE, (0,) * p.num_pis, 0, 0)
         return EsResult(EXHAUSTED_ZERO, None, 1 << p.num_pis)
+    return None
+
+
+def sweep_peer_async(prog, peer: PeerBest, out_ptr: int, device: int | None = None,
+                     cofactor="throughput", stream: int | None = None) -> None:
+    """Queue one sharded verdict on ``stream`` (default: torch's current
+    stream) without host synchronisation: this rank's sweep over its residue
+    class of chunks, then the device-side barrier that writes the final
+    minimum (all-ones: none) to the 8-byte device buffer at ``out_ptr``.
+    Collective: every rank queues the same programs in the same order."""
+    import torch
+
+    p = as_program(prog)
+    dev = peer.device if device is None else device
     sess = session_for(p, dev, cofactor)
-    sentinel = 1 << p.num_pis
+    st = torch.cuda.current_stream(dev).cuda_stream if stream is None else stream
     k = peer._step % peer.WORDS
     peer._step += 1
-    if rank == 0:  # the next verdict's word: last read two verdicts ago
-        peer.write((k + 1) % peer.WORDS, peer.NONE)
-    stream = torch.cuda.current_stream(dev)
-    sess.launch(stream.cuda_stream, peer.ptrs[k].value, 0, sess.n_chunks, rank, world)
-    stream.synchronize()
-    if world > 1:
-        dist.barrier(group=group)      # every rank's chunks are done
-    b = peer.read(k)
+    L = N.lib()
+    if peer.rank == 0:  # the next verdict's word: last used two verdicts ago
+        N.check(L.es_peer_arm(ctypes.c_void_p(st), peer.ptrs[(k + 1) % peer.WORDS]))
+    sess.launch(st, peer.ptrs[k].value, 0, sess.n_chunks, peer.rank, peer.world)
+    N.check(L.es_peer_arrive_wait(ctypes.c_void_p(st), peer.ptrs[k], peer.world,
+                                  ctypes.c_void_p(out_ptr)))
+
+
+def peer_result(p, b: int) -> EsResult:
+    """EsResult of a verdict whose final minimum word is ``b``."""
+    p = as_program(p)
+    sentinel = 1 << p.num_pis
     if b < sentinel:
         lo = min(p.num_pis, 14)
         return EsResult(ES_COUNTEREXAMPLE, tuple((b >> i) & 1 for i in range(p.num_pis)),
                         ((b >> lo) + 1) << lo, b)
     return EsResult(EXHAUSTED_ZERO, None, sentinel)
+
+
+def sweep_peer(prog, peer: PeerBest, group=None, device: int | None = None,
+               cofactor="throughput") -> EsResult:
+    """run_exhaustive sharded over ``group`` with the shared peer word
+    (collective call; same program on every rank).  One launch per rank over
+    its residue class of chunks, the device-side barrier, one 8-byte read."""
+    import torch
+
+    p = as_program(prog)
+    rail = _constant_rail(p)
+    if rail is not None:
+        return rail
+    dev = peer.device if device is None else device
+    out = torch.empty(1, dtype=torch.int64, device=f"cuda:{dev}")
+    sweep_peer_async(p, peer, out.data_ptr(), dev, cofactor)
+    return peer_result(p, int(out.item()) & 0xFFFFFFFFFFFFFFFF)
 
 
 def es_check_peer(sm, peer: PeerBest, group=None, device: int | None = None,
