@@ -219,6 +219,18 @@ class NativeBatch:
         return SubMiter(Xag(n, gates, (Lit.unpack(out.value),)), self.origins[i] if
                         i < len(self.origins) else (0, 0), {}, tuple(int(q) for q in pm), i)
 
+    def packed(self, i: int):
+        """Sub-miter i as packed arrays: (num_pis, kind, in0, in1, out_lit)."""
+        inf = self.info(i)
+        ng, n = inf["num_gates"], inf["num_pis"]
+        kind = np.zeros(ng, np.uint8)
+        in0 = np.zeros(ng, np.uint32)
+        in1 = np.zeros(ng, np.uint32)
+        out = ctypes.c_uint32()
+        N.check(N.lib().es_batch_xag(self._h, i, kind.ctypes.data, in0.ctypes.data,
+                                     in1.ctypes.data, ctypes.byref(out), None))
+        return n, kind, in0, in1, out.value
+
     def prepare(self, threads: int = 0) -> None:
         """Build every job's interpreter program now (cofactor depth, schedule);
         run_arrays would do it on its first call."""
