@@ -134,6 +134,8 @@ typedef struct es_result {
     int32_t phases;             /* K1: 2 when a counterexample above a cofactored chunk's range
                                  * needed a second sweep below it (non-contiguous chunks) */
     int32_t phase2_cofactor_pis;/* cofactor PIs of the second phase's variant (phases == 2) */
+    int32_t phase2_copies;      /* > 0: the second phase ran the first phase's cofactor set
+                                 * restricted to copies 0..phase2_copies-1 */
 } es_result;
 
 /*
@@ -346,6 +348,13 @@ int32_t es_map_stats_k(const es_prog *prog, int32_t k, int32_t *num_luts, int32_
 int32_t es_map_pipes_k(const es_prog *prog, int32_t k, int32_t *lop3, int32_t *imad);
 int32_t es_map_eval_k(const es_prog *prog, int32_t k, uint64_t w0, uint64_t nw, uint32_t *out_words);
 int64_t es_emit_ptx_k(const es_prog *prog, int32_t k, int32_t block_threads, char *buf, int64_t cap);
+/* The restricted variant of the second phase of a non-equivalent search: the
+ * k-PI cofactor set evaluating only copies 0..copies-1 (0 = all).  eval gives
+ * 0 for words of the other copies. */
+int32_t es_map_stats_kc(const es_prog *prog, int32_t k, int32_t copies, int32_t *num_luts,
+                        int32_t *peak_live);
+int32_t es_map_eval_kc(const es_prog *prog, int32_t k, int32_t copies, uint64_t w0, uint64_t nw,
+                       uint32_t *out_words);
 int64_t es_jit_check_k(const es_prog *prog, int32_t k, int32_t block_threads, int32_t *regs_per_thread,
                        int32_t *spill_bytes, char *log, int64_t log_cap);
 /* The PTX the JIT path would compile for `prog` (buf NULL -> returns size).

@@ -36,7 +36,7 @@ EXPORTS = ("es_compile", "es_run", "es_run_batch", "es_session_open", "es_sessio
            "es_emit_ptx", "es_jit_check", "es_alu_peak", "es_smem_peak", "es_batch_extract", "es_batch_size",
            "es_batch_info", "es_batch_table", "es_batch_k2_stats", "es_xag_eval", "es_batch_xag", "es_batch_select", "es_batch_run", "es_batch_merge", "es_batch_free",
            "es_ipc_alloc", "es_ipc_open", "es_ipc_close", "es_word_write", "es_word_read",
-           "es_map_stats_k", "es_map_pipes_k", "es_map_eval_k", "es_emit_ptx_k", "es_jit_check_k",
+           "es_map_stats_k", "es_map_pipes_k", "es_map_eval_k", "es_map_stats_kc", "es_map_eval_kc", "es_emit_ptx_k", "es_jit_check_k",
            "es_k2_eval_k", "es_k2_cofactor_pis", "es_batch_prepare",
            "es_sim", "es_sim_ones", "es_sim_device", "es_sim_prog_free", "es_sim_classes", "es_sim_levels",
            "es_aiger_parse", "es_detect_xors", "es_xag_size", "es_xag_read", "es_xag_free",
@@ -70,7 +70,7 @@ class EsResult(ctypes.Structure):
                 ("regs_per_thread", ctypes.c_int32), ("cofactor_pis", ctypes.c_int32),
                 ("jit_opt", ctypes.c_int32), ("witness_minimal", ctypes.c_int32),
                 ("n_devices", ctypes.c_int32), ("phases", ctypes.c_int32),
-                ("phase2_cofactor_pis", ctypes.c_int32)]
+                ("phase2_cofactor_pis", ctypes.c_int32), ("phase2_copies", ctypes.c_int32)]
 
 
 class NativeError(RuntimeError):
@@ -108,6 +108,11 @@ def lib():
         L.es_peer_arm.restype = ctypes.c_int32
         L.es_peer_arrive_wait.argtypes = [_P, _P, ctypes.c_int32, _P]
         L.es_peer_arrive_wait.restype = ctypes.c_int32
+        L.es_map_stats_kc.argtypes = [ctypes.POINTER(EsProg), ctypes.c_int32, ctypes.c_int32, _P, _P]
+        L.es_map_stats_kc.restype = ctypes.c_int32
+        L.es_map_eval_kc.argtypes = [ctypes.POINTER(EsProg), ctypes.c_int32, ctypes.c_int32,
+                                     ctypes.c_uint64, ctypes.c_uint64, _P]
+        L.es_map_eval_kc.restype = ctypes.c_int32
         L.es_device_count.argtypes = [ctypes.POINTER(ctypes.c_int32)]
         L.es_device_count.restype = ctypes.c_int32
         L.es_session_open.argtypes = [ctypes.POINTER(EsProg), ctypes.POINTER(EsRunOpts),

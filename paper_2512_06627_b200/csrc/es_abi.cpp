@@ -61,7 +61,7 @@ int sim_classes(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const u
                 int32_t *class_id, uint8_t *polarity, int32_t *n_classes, double *device_ms);
 
 // k = cofactor PIs (0: none), chosen as the runtime does (rank_cofactor_pis)
-static int map_prog(const es_prog *prog, LutNet *net, int k = 0) {
+static int map_prog(const es_prog *prog, LutNet *net, int k = 0, int copies = 0) {
     if (!prog || prog->num_instrs < 1) { set_error("empty program"); return ES_E_BAD_PROGRAM; }
     if (k < 0 || k > kMaxCofactorPis) { set_error("cofactor PIs must be 0.." + std::to_string(kMaxCofactorPis)); return ES_E_BAD_ARG; }
     Dag dag;
@@ -72,7 +72,10 @@ static int map_prog(const es_prog *prog, LutNet *net, int k = 0) {
     std::vector<int32_t> pis = rank_cofactor_pis(dag, k);
     std::sort(pis.begin(), pis.end());
     if ((int)pis.size() != k) { set_error("fewer word PIs than cofactor PIs"); return ES_E_BAD_ARG; }
-    map_cofactored(dag, pis, net);
+    if (copies < 0 || copies > (1 << k)) { set_error("copies must be 0..2^k"); return ES_E_BAD_ARG; }
+    std::vector<int32_t> ids;
+    for (int c = 0; c < copies; ++c) ids.push_back(c);
+    map_cofactored(dag, pis, net, copies && copies < (1 << k) ? &ids : nullptr);
     return ES_OK;
 }
 
@@ -179,6 +182,25 @@ int32_t es_map_eval(const es_prog *prog, uint64_t w0, uint64_t nw, uint32_t *out
 int32_t es_map_eval_k(const es_prog *prog, int32_t k, uint64_t w0, uint64_t nw, uint32_t *out_words) {
     LutNet net;
     int rc = map_prog(prog, &net, k);
+    if (rc != ES_OK) return rc;
+    eval_lutnet(net, w0, nw, out_words);
+    return ES_OK;
+}
+
+int32_t es_map_stats_kc(const es_prog *prog, int32_t k, int32_t copies, int32_t *num_luts,
+                        int32_t *peak_live) {
+    LutNet net;
+    int rc = map_prog(prog, &net, k, copies);
+    if (rc != ES_OK) return rc;
+    if (num_luts) *num_luts = (int32_t)net.luts.size();
+    if (peak_live) *peak_live = net.peak_live;
+    return ES_OK;
+}
+
+int32_t es_map_eval_kc(const es_prog *prog, int32_t k, int32_t copies, uint64_t w0, uint64_t nw,
+                       uint32_t *out_words) {
+    LutNet net;
+    int rc = map_prog(prog, &net, k, copies);
     if (rc != ES_OK) return rc;
     eval_lutnet(net, w0, nw, out_words);
     return ES_OK;

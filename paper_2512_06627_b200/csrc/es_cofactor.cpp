@@ -114,7 +114,8 @@ std::vector<int32_t> rank_cofactor_pis(const Dag &dag, int k, int max_pi) {
     return cand;
 }
 
-void cofactor_expand(const Dag &dag, const std::vector<int32_t> &pis, Dag *out) {
+void cofactor_expand(const Dag &dag, const std::vector<int32_t> &pis, Dag *out,
+                     const std::vector<int32_t> *copies) {
     const int N = dag.num_nodes(), FG = dag.first_gate(), P = dag.num_pis;
     const std::vector<uint8_t> cone = output_cone(dag);
     *out = Dag();
@@ -138,13 +139,21 @@ void cofactor_expand(const Dag &dag, const std::vector<int32_t> &pis, Dag *out) 
     std::vector<uint8_t> src_neg = dag.outs_neg;
     if (src_outs.empty()) { src_outs.push_back(dag.out_node); src_neg.push_back(dag.out_neg); }
     for (int j = 1; j <= P; ++j) lit[j] = (uint32_t)j * 2;
-    for (int c = 0; c < (1 << k); ++c) {
+    std::vector<int32_t> every;
+    if (!copies) {
+        for (int c = 0; c < (1 << k); ++c) every.push_back(c);
+        copies = &every;
+    }
+    bool first = true;
+    for (int32_t c : *copies) {
         for (int b = 0; b < k; ++b) lit[pis[b]] = (uint32_t)((c >> b) & 1);
-        for (int v : (c == 0 ? all : tgates)) {
+        // the first copy builds the logic outside the cofactor PIs' fanout too
+        for (int v : (first ? all : tgates)) {
             const int g = v - FG;
             const uint32_t a = lit[dag.f0[g]] ^ dag.n0[g], b = lit[dag.f1[g]] ^ dag.n1[g];
             lit[v] = dag.is_xor[g] ? sh.mk_xor(a, b) : sh.mk_and(a, b);
         }
+        first = false;
         for (size_t q = 0; q < src_outs.size(); ++q) {
             const uint32_t o = lit[src_outs[q]] ^ src_neg[q];
             out->outs.push_back((int32_t)(o >> 1));
@@ -155,12 +164,14 @@ void cofactor_expand(const Dag &dag, const std::vector<int32_t> &pis, Dag *out) 
     out->out_neg = out->outs_neg[0];
 }
 
-void map_cofactored(const Dag &dag, const std::vector<int32_t> &pis, LutNet *net) {
+void map_cofactored(const Dag &dag, const std::vector<int32_t> &pis, LutNet *net,
+                    const std::vector<int32_t> *copies) {
     if (pis.empty()) { map_luts(dag, net); return; }
     Dag x;
-    cofactor_expand(dag, pis, &x);
+    cofactor_expand(dag, pis, &x, copies);
     map_luts(x, net);
     net->cof_pis = pis;
+    if (copies && (int)copies->size() != (1 << pis.size())) net->copy_ids = *copies;
     const int P = dag.num_pis;
     net->pi_bit.assign(P + 1, -1);
     int bit = 0;

@@ -465,18 +465,19 @@ void map_luts(const Dag &dag, LutNet *net) {
             // and dies early (mult16, k=4: peak live 358 -> 212 values, kernel
             // 2.58 -> 2.32 ms, JIT 1.03 -> 0.74 s).  The OUT fold still runs in
             // copy order (flush_outputs waits for copy 0).
+            // (a restricted variant's copies 0..C-1 with C not a power of two:
+            // the bit-reversed order of the enclosing power of two, truncated)
             const int C = (int)outs.size();
-            if ((C & (C - 1)) == 0) {
-                const int kb = __builtin_ctz((unsigned)C);
-                std::vector<int32_t> rev(C);
-                for (int c = 0; c < C; ++c) {
-                    int r = 0;
-                    for (int b = 0; b < kb; ++b) r |= ((c >> b) & 1) << (kb - 1 - b);
-                    rev[c] = outs[r];
-                }
-                std::vector<int> o2 = dfs(rev);
-                if (peak_of(o2) < peak_of(order)) order.swap(o2);
+            int kb = 0;
+            while ((1 << kb) < C) ++kb;
+            std::vector<int32_t> rev;
+            for (int c = 0; c < (1 << kb); ++c) {
+                int r = 0;
+                for (int b = 0; b < kb; ++b) r |= ((c >> b) & 1) << (kb - 1 - b);
+                if (r < C) rev.push_back(outs[r]);
             }
+            std::vector<int> o2 = dfs(rev);
+            if (peak_of(o2) < peak_of(order)) order.swap(o2);
         }
         if (getenv("ES_LIST_SCHED")) {
             // experiment: greedy list scheduling, prefer the ready node that frees most
@@ -594,10 +595,16 @@ void eval_lutnet(const LutNet &net, uint64_t w0, uint64_t nw, uint32_t *out) {
         for (int j : net.pis_used) val[j] = ((w >> (j - 6)) & 1) ? ~0u : 0u;
         for (const Lut &L : net.luts)
             val[L.node] = lut3(L.tt, val[L.leaf[2]], val[L.leaf[1]], val[L.leaf[0]]);
-        size_t c = 0;
-        for (size_t b = 0; b < net.cof_pis.size(); ++b) c |= (size_t)((w >> (net.cof_pis[b] - 6)) & 1) << b;
-        uint32_t o = val[net.outs[c]];
-        if (net.outs_neg[c]) o = ~o;
+        int32_t c = 0;
+        for (size_t b = 0; b < net.cof_pis.size(); ++b) c |= (int32_t)((w >> (net.cof_pis[b] - 6)) & 1) << b;
+        size_t i = (size_t)c;  // the output of copy c (a restricted variant lacks some: 0)
+        if (!net.copy_ids.empty()) {
+            auto it = std::find(net.copy_ids.begin(), net.copy_ids.end(), c);
+            if (it == net.copy_ids.end()) { out[k] = 0; continue; }
+            i = (size_t)(it - net.copy_ids.begin());
+        }
+        uint32_t o = val[net.outs[i]];
+        if (net.outs_neg[i]) o = ~o;
         out[k] = o & valid;
     }
 }
@@ -711,7 +718,7 @@ std::string emit_body_ptx(const LutNet &net, const std::vector<std::string> &out
     };
     // Cofactor copies: fold each copy's output into (first failing word, its
     // copy number) as soon as it exists -- 3 ops per copy, 2 live registers.
-    const bool multi = net.outs.size() > 1;
+    const bool multi = net.outs.size() > 1 || !net.cof_pis.empty();
     std::vector<uint8_t> emitted(N, 0);
     size_t next_copy = 0;
     auto flush_outputs = [&]() {
@@ -722,7 +729,7 @@ std::string emit_body_ptx(const LutNet &net, const std::vector<std::string> &out
             if (net.outs_neg[next_copy]) { body << "not.b32 %est, " << v << ";\n"; v = "%est"; }
             body << "setp.eq.b32 %espz, " << outs[0] << ", 0;\n"
                  << "selp.b32 " << outs[0] << ", " << v << ", " << outs[0] << ", %espz;\n"
-                 << "selp.b32 " << outs[1] << ", " << next_copy << ", " << outs[1] << ", %espz;\n";
+                 << "selp.b32 " << outs[1] << ", " << net.copy_id(next_copy) << ", " << outs[1] << ", %espz;\n";
             ++next_copy;
         }
     };

@@ -95,6 +95,12 @@ struct LutNet {
     // pi_bit[j] = bit of w' carrying PI j (-1 for lane PIs 1..5 and cofactor PIs).
     std::vector<int32_t> cof_pis;
     std::vector<int8_t> pi_bit;
+    // copy_ids[i] = the cofactor assignment of outs[i] (bit b = value of
+    // cof_pis[b]); empty = all 2^k copies in order.  A restricted variant
+    // evaluates only some copies (the second phase of a non-equivalent
+    // search needs only the copies below the first witness's).
+    std::vector<int32_t> copy_ids;
+    int copy_id(size_t i) const { return copy_ids.empty() ? (int)i : copy_ids[i]; }
     int num_gates = 0;                    // AND+XOR gates in the output cone
     int peak_live = 0;                    // max simultaneously live LUT values in the schedule
     std::vector<int32_t> pis_used;        // PIs >= 6 referenced as leaves
@@ -119,9 +125,12 @@ constexpr int kMaxCofactorPis = 5;
 std::vector<int32_t> rank_cofactor_pis(const Dag &dag, int k, int max_pi = 1 << 20);
 // dag with the PIs in `pis` (ascending) cofactored: 2^k outputs, output c
 // under PI pis[b] = bit b of c.  Constant propagation + structural hashing.
-void cofactor_expand(const Dag &dag, const std::vector<int32_t> &pis, Dag *out);
-// map_luts of the expansion, with cof_pis / pi_bit filled in.
-void map_cofactored(const Dag &dag, const std::vector<int32_t> &pis, LutNet *net);
+// copies: the assignments to expand (ascending; nullptr = all 2^k).
+void cofactor_expand(const Dag &dag, const std::vector<int32_t> &pis, Dag *out,
+                     const std::vector<int32_t> *copies = nullptr);
+// map_luts of the expansion, with cof_pis / pi_bit (and copy_ids) filled in.
+void map_cofactored(const Dag &dag, const std::vector<int32_t> &pis, LutNet *net,
+                    const std::vector<int32_t> *copies = nullptr);
 
 // Reference compile_program (es.py:87-163), exact.
 int32_t ref_compile(int32_t num_pis, int32_t num_gates, const uint8_t *kind,

@@ -38,7 +38,9 @@ static const char *skeleton_for(int threads, int copies) {
 bool splice_body(const LutNet &net, int threads, std::string *ptx, std::string *err,
                  int *region_bytes) {
     if (region_bytes) *region_bytes = 0;
-    const int copies = (int)net.outs.size();
+    // the multi-copy skeleton whenever there are cofactor PIs (it inserts
+    // their bits into pattern indices), even for a one-copy restricted variant
+    const int copies = net.cof_pis.empty() ? (int)net.outs.size() : std::max(2, (int)net.outs.size());
     const char *sk = skeleton_for(threads, copies);
     if (!sk) {
         *err = "unsupported K1 variant: " + std::to_string(threads) + " threads x " +

@@ -1166,8 +1166,10 @@ struct MappedProg {
     int G = 0;
     // K1 variants keyed by their cofactor PI set (ascending; empty = one word
     // per iteration), mapped on demand; kernels per (set, CTA size)
-    std::map<std::vector<int32_t>, std::unique_ptr<LutNet>> nets;
-    std::map<std::pair<std::vector<int32_t>, int>, JitKernel *> jks;
+    // (cofactor PIs, copies: 0 = all 2^k, t = the restricted variant of copies 0..t-1)
+    using VariantKey = std::pair<std::vector<int32_t>, int>;
+    std::map<VariantKey, std::unique_ptr<LutNet>> nets;
+    std::map<std::pair<VariantKey, int>, JitKernel *> jks;
     std::map<int, std::vector<int32_t>> ranks;  // max_pi -> the cheapest word PIs (<= max_pi), by fanout
     int runs = 0;                    // K1 runs so far (the reuse estimate of the auto policy)
     std::shared_ptr<K2Prog> k2;      // interpreter program (its own cofactor depth), on demand
@@ -1182,17 +1184,22 @@ struct MappedProg {
         std::sort(pis.begin(), pis.end());
         return pis;
     }
-    const LutNet &variant_set(const std::vector<int32_t> &pis) {  // caller holds mu
-        auto &slot = nets[pis];
+    const LutNet &variant_set(const std::vector<int32_t> &pis, int copies = 0) {  // caller holds mu
+        if (copies >= (1 << pis.size())) copies = 0;
+        auto &slot = nets[{pis, copies}];
         if (!slot) {
             NvtxRange nvtx("es_map");
             slot.reset(new LutNet());
-            map_cofactored(dag, pis, slot.get());
+            std::vector<int32_t> ids;
+            for (int c = 0; c < copies; ++c) ids.push_back(c);
+            map_cofactored(dag, pis, slot.get(), copies ? &ids : nullptr);
         }
         return *slot;
     }
     const LutNet &variant(int k) { return variant_set(ranked(k)); }
-    JitKernel *&jk(const LutNet &n, int threads) { return jks[{n.cof_pis, k1_slot(threads)}]; }
+    JitKernel *&jk(const LutNet &n, int threads) {
+        return jks[{{n.cof_pis, (int)n.copy_ids.size()}, k1_slot(threads)}];
+    }
 };
 static uint64_t prog_hash(const es_prog &p) {
     uint64_t h = 1469598103934665603ull;
@@ -1461,7 +1468,44 @@ static int run_k1_job(MappedProg &mp, const LutNet &net, const es_run_opts &o, c
             if (!tput && !(have && have->opt >= opt)) c += est_jit_ms(cand, opt);
             if (c < best_cost) { best_cost = c; best_net = &cand; }
         }
+    // (c): the phase-1 cofactor set restricted to the copies below w1's copy c1
+    // (a smaller body, same chunk order) over the chunks phase 1 left: every
+    // pattern below w1 is either in a swept chunk or in one of those copies
+    int c1 = 0;
+    for (int b = 0; b < pl.cof_n; ++b) c1 |= (int)((w1 >> pl.cof_pos[b]) & 1ull) << b;
+    const LutNet *restricted = nullptr;
+    if (c1 > 0 && c1 < (1 << pl.cof_n)) {
+        const LutNet &cand = mp.variant_set(net.cof_pis, c1);
+        double c = frac_left * est_sweep_ms(cand, P, sms * n_dev);
+        const JitKernel *have = mp.jk(cand, k1_threads(o, pl.cof_n));
+        if (!tput && !(have && have->opt >= opt)) c += est_jit_ms(cand, opt);
+        if (c < best_cost) { best_cost = c; best_net = nullptr; restricted = &cand; }
+    }
     SweepOut s2;
+    if (restricted) {
+        K1Plan pl2;
+        double jit2 = 0;
+        rc = k1_plan_for(mp, *restricted, o, sms, n_dev, opt, &pl2, &jit2);
+        if (rc != ES_OK) return rc;
+        r->jit_ms += jit2;
+        // phase 1's swept prefix in the restricted plan's chunk units (rounded down)
+        const uint64_t from = ((s1.prefix << pl.chunk_log2) >> pl2.chunk_log2);
+        rc = sweep_k1(pl2, G, o, cs, deadline, from, w1, 0, &s2);
+        if (rc != ES_OK) return rc;
+        r->device_ms += s1.device_ms;
+        r->launches += s1.launches;
+        r->patterns_swept += std::min<uint64_t>(s1.swept * pl.patterns_per_chunk(), sentinel);
+        r->phase2_cofactor_pis = pl2.cof_n;
+        r->phase2_copies = c1;
+        // the proof: phase 1 swept chunks [0, s1.prefix) of every copy, phase 2
+        // copies [0, c1) of the rest; a stop leaves the prefix of both
+        r->patterns_swept += (s2.swept << (pl2.chunk_log2 + 5)) * (uint64_t)c1;  // c1 copies per chunk word
+        SweepOut s3 = s2;
+        s3.swept = 0;
+        s3.prefix = s2.stopped ? std::min(s1.prefix, (s2.prefix << pl2.chunk_log2) >> pl.chunk_log2) : pl.n_chunks;
+        k1_result(pl, s3, P, r);
+        return ES_OK;
+    }
     if (!best_net) {  // (a): finish phase 1's sweep, skipping chunks above w1
         rc = sweep_k1(pl, G, o, cs, deadline, s1.prefix, w1, 0, &s2);
         if (rc != ES_OK) return rc;

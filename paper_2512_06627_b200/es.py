@@ -265,7 +265,8 @@ def _stats_of(r: N.EsResult) -> dict:
             "regs_per_thread": int(r.regs_per_thread), "cofactor_pis": int(r.cofactor_pis),
             "jit_opt": int(r.jit_opt), "witness_minimal": bool(r.witness_minimal),
             "n_devices": int(r.n_devices), "phases": int(r.phases),
-            "phase2_cofactor_pis": int(r.phase2_cofactor_pis) if r.phases == 2 else None}
+            "phase2_cofactor_pis": int(r.phase2_cofactor_pis) if r.phases == 2 else None,
+            "phase2_copies": int(r.phase2_copies) if r.phases == 2 else None}
 
 
 def _to_esresult(r: N.EsResult, num_pis: int) -> EsResult:
@@ -434,6 +435,25 @@ def map_stats(p, k: int = 0) -> dict:
                                    ctypes.byref(live), ctypes.byref(gates), pis))
     return {"luts": luts.value, "peak_live": live.value, "gates": gates.value,
             "cofactor_pis": list(pis[:k])}
+
+
+def map_stats_restricted(p, k: int, copies: int) -> dict:
+    """The k-PI cofactor variant restricted to copies 0..copies-1 (the second
+    phase of a non-equivalent search): LUTs per iteration, peak live set."""
+    prog = as_program(p)
+    luts, live = ctypes.c_int32(), ctypes.c_int32()
+    N.check(N.lib().es_map_stats_kc(ctypes.byref(prog.as_struct()), k, copies, ctypes.byref(luts),
+                                    ctypes.byref(live)))
+    return {"luts": luts.value, "peak_live": live.value}
+
+
+def map_eval_restricted(p, w0: int, nw: int, k: int, copies: int) -> np.ndarray:
+    """CPU model of the restricted variant (0 for words of other copies)."""
+    prog = as_program(p)
+    out = np.zeros(nw, dtype=np.uint32)
+    N.check(N.lib().es_map_eval_kc(ctypes.byref(prog.as_struct()), k, copies, w0, nw,
+                                   out.ctypes.data))
+    return out
 
 
 def map_pipes(p, k: int = 0) -> dict:

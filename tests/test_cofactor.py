@@ -76,3 +76,26 @@ def test_cofactor_ptx_compiles(k):
     m = M.gen_multiplier_miter(8, "array", "booth")
     r = es.jit_check(es.compile_program(m), 256, k=k)
     assert r["cubin_bytes"] > 0 and r["spill_bytes"] == 0
+
+
+@pytest.mark.parametrize("k,copies", [(2, 1), (2, 3), (3, 5), (4, 6), (4, 11)])
+def test_restricted_copies_model(k, copies):
+    """The second phase's restricted variant (copies 0..copies-1 of the same
+    cofactor set): words of those copies equal the full variant's, the other
+    copies' words are 0 (not evaluated), and the body is smaller."""
+    x = M.gen_multiplier_miter(6, "array", "booth")
+    bad = M.flip_gate(x, 40)
+    for c in (x, bad):
+        p = es.compile_program(c)
+        n = c.num_pis
+        full = es.map_eval(p, 0, 1 << (n - 5), k=k)
+        part = es.map_eval_restricted(p, 0, 1 << (n - 5), k, copies)
+        cof = es.map_stats(p, k)["cofactor_pis"]
+        w = np.arange(1 << (n - 5), dtype=np.uint64)
+        copy = np.zeros_like(w)
+        for b, j in enumerate(cof):
+            copy |= ((w >> np.uint64(j - 6)) & np.uint64(1)) << np.uint64(b)
+        keep = copy < copies
+        assert np.array_equal(part[keep], full[keep])
+        assert not part[~keep].any()
+    assert es.map_stats_restricted(p, k, copies)["luts"] < es.map_stats(p, k)["luts"]

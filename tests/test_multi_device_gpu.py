@@ -54,12 +54,28 @@ def test_neq_two_phase_sweeps_below_the_witness(gpu, miters):
         assert r.stats["patterns_swept"] < 0.5 * (1 << 32), r.stats
 
 
-def test_neq_shallow_witness_single_phase(gpu, miters):
-    """A witness below 2^28 (the cofactor bits' range) is proven by phase 1."""
-    p, g = miters["mult16_array_booth_flip1220"]
-    r = es.run_exhaustive(p, engine="jit", cofactor="throughput")
-    _check(r, g, "flip1220")
-    assert r.stats["phases"] == 1 and r.stats["patterns_swept"] < (1 << 30)
+def test_neq_shallow_witness_single_phase(gpu):
+    """A witness below 2^28 (its cofactor bits all 0) is proven by phase 1."""
+    needle = (1 << 24) + 5
+    x = recipes.build_sweep_circuit({"kind": "mult", "width": 16, "a": "array", "b": "booth",
+                                     "needle": needle})
+    r = es.run_exhaustive(es.compile_program(x), engine="jit", cofactor="throughput")
+    assert r.witness_index == needle and r.stats["phases"] == 1
+    assert r.stats["patterns_swept"] < (1 << 30)
+
+
+@pytest.mark.parametrize("needle", [(1 << 28) + 1, 3 << 29, (1 << 31) + 12345, (1 << 32) - 1])
+def test_neq_deep_needles(gpu, needle):
+    """A single failing pattern at any depth is found exactly, whichever
+    second phase the policy picks (restricted copies, low cofactor set, or
+    finishing the first sweep), on one device or two host threads."""
+    x = recipes.build_sweep_circuit({"kind": "mult", "width": 16, "a": "array", "b": "booth",
+                                     "needle": needle})
+    p = es.compile_program(x)
+    for devices in (None, [0, 0]):
+        r = es.run_exhaustive(p, engine="jit", cofactor="throughput", devices=devices)
+        assert (r.verdict, r.witness_index) == (es.ES_COUNTEREXAMPLE, needle), (devices, r.stats)
+        assert r.patterns_evaluated == ((needle >> 14) + 1) << 14
 
 
 def test_devices_all_and_es_check(gpu, miters):
