@@ -6,20 +6,30 @@
 
 One step = one exact-simulation verdict of the configured miter: all 2^n
 primary-input patterns swept (or, for a non-equivalent miter, every pattern
-up to the minimum-index counterexample), sharded over the N ranks of one node
-(torchrun, one process per GPU, NCCL MIN all-reduce of the 8-byte minimum
-between launch slices).  Default workload: BASELINE.json configs[2], the
-16x16 array vs radix-4 Booth multiplier miter (32 PIs, 2^32 patterns) -- the
-configuration BASELINE.json's metric is quoted on at 1/2/4/8 B200.
+up to the minimum-index counterexample).  Default workload: BASELINE.json
+configs[2], the 16x16 array vs radix-4 Booth multiplier miter (32 PIs, 2^32
+patterns) -- the configuration BASELINE.json's metric is quoted on at
+1/2/4/8 B200.
+
+N GPUs, two launch modes (the pattern space is sharded either way):
+  * ``python bench.py --gpus N`` (no torchrun): ONE es_run call drives N GPUs
+    (es_run_opts.devices: one host thread per GPU, one minimum word in GPU 0's
+    HBM shared as NVLink peer memory).  Fails if fewer than N GPUs are visible.
+  * torchrun, one process per GPU (WORLD_SIZE must equal --gpus): each rank
+    sweeps its residue class of chunks; the ranks share one minimum word over
+    CUDA IPC and close every verdict with a device-side barrier
+    (es_peer_arrive_wait) -- no collective and no host round trip per verdict.
 
 Metric: simulated gate-patterns/s, gate = AND/XOR instruction of the
 reference compile_program (G), so one step is G * 2^n gate-patterns of
 algorithmic work.  Rank 0 prints ONE JSON line.
 
---impl reference times the reference algorithm's CPU restatement
-(oracle/, es.py:175-339 semantics) on all host cores on a bounded sample of
-the same sweep; the reference package itself is Python+numba and is not
-present on the GPU box.
+--impl reference runs the UNMODIFIED reference package (cecprove, installed
+into baseline/_ref from /root/reference; Python + numba) through its own
+public API -- run_exhaustive(compile_program(x), workers=<all host threads>,
+budget=<bounded sample>) -- on the box's host cores, on the same miter.  If
+baseline/_ref is missing it times the oracle's C restatement instead
+(kind "port").
 """
 
 from __future__ import annotations
@@ -30,6 +40,7 @@ import os
 import statistics
 import subprocess
 import sys
+import tempfile
 import threading
 import time
 
@@ -38,6 +49,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "simulated gate·patterns/s and ES time-to-verdict per miter at 1/2/4/8 B200"
 UNIT = "gate·patterns/s"
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
 
 # --- workloads -------------------------------------------------------------
@@ -74,6 +86,244 @@ class _Sub:
         self.id = 0
 
 
+# --- the reference package (baseline/_ref) ---------------------------------
+
+_REF = None
+
+
+def reference_pkg():
+    """The unmodified reference (cecprove) installed in baseline/_ref, or None.
+    Its numba JIT cache goes to a private temp directory."""
+    global _REF
+    if _REF is not None:
+        return _REF or None
+    _REF = False
+    if not os.path.isdir(os.path.join(REF_DIR, "cecprove")):
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", tempfile.mkdtemp(prefix="numba_ref_"))
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import cecprove.es  # noqa: F401
+        import cecprove.xag  # noqa: F401
+        import cecprove
+
+        _REF = cecprove
+    except Exception as exc:  # numba missing, ...
+        print(f"[bench] reference package unusable: {exc}", file=sys.stderr)
+        return None
+    return _REF
+
+
+def to_ref(x, ref):
+    """This repo's Xag as a reference Xag (field for field, xag.py:71-125)."""
+    X = ref.xag
+    return X.Xag(x.num_pis,
+                 tuple(X.Gate(X.GateKind(int(g.kind)), X.Lit(g.in0.node, bool(g.in0.neg)),
+                              X.Lit(g.in1.node, bool(g.in1.neg))) for g in x.gates),
+                 tuple(X.Lit(o.node, bool(o.neg)) for o in x.outputs))
+
+
+def _ref_G(p) -> int:
+    return sum(1 for i in p.instrs if i.op in (1, 2))
+
+
+def ref_sample(x, workers: int, seconds: float, ref=None) -> dict:
+    """The reference's own run_exhaustive (es.py:252) on `workers` threads for
+    at most `seconds` (its budget argument): gate-patterns/s over the patterns
+    it evaluated.  A run that finishes first is a full verdict."""
+    ref = ref or reference_pkg()
+    p = ref.es.compile_program(to_ref(x, ref))
+    G = _ref_G(p)
+    ref.es.run_exhaustive(p, workers=workers, budget=0.05)  # numba JIT (cache=True) outside the timing
+    t = time.perf_counter()
+    r = ref.es.run_exhaustive(p, workers=workers, budget=seconds)
+    dt = time.perf_counter() - t
+    return {"value": G * r.patterns_evaluated / dt, "verdict": r.verdict,
+            "patterns": r.patterns_evaluated, "seconds": dt, "G": G, "workers": workers,
+            "witness_index": None if r.witness is None else sum(b << i for i, b in enumerate(r.witness))}
+
+
+def port_sample(x, target_s: float, threads: int | None = None) -> dict:
+    """The oracle's C restatement of the reference algorithm (es.py:175-339) on
+    a bounded prefix of the sweep (whole 2^14-pattern batches, all threads)."""
+    from oracle import oracle as O
+
+    p = O.compile_program(x)
+    G = p.num_gate_instrs
+    threads = threads or os.cpu_count() or 1
+    total_batches = 1 << max(x.num_pis - 14, 0)
+    per_batch = 1 << min(x.num_pis, 14)
+    O.min_witness(p, threads=threads, max_batches=min(total_batches, 4 * threads))  # warm-up
+    probe = min(total_batches, 64 * threads)
+    t = time.perf_counter()
+    O.min_witness(p, threads=threads, max_batches=probe)
+    dt = max(time.perf_counter() - t, 1e-6)
+    nb = int(min(total_batches, max(probe, probe * target_s / dt)))
+    t = time.perf_counter()
+    verdict, idx, done = O.min_witness(p, threads=threads, max_batches=nb)
+    dt = time.perf_counter() - t
+    return {"value": G * done * per_batch / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"first {nb} of {total_batches} reference batches (2^{min(x.num_pis, 14)} "
+                      f"patterns each) of the same sweep, G={G}, {dt:.2f}s, oracle/es_oracle.c "
+                      f"(es.py:175-339 restated), {threads} threads",
+            "seconds": dt}
+
+
+def cpu_baseline(x, seconds: float, desc: str = "") -> dict:
+    """The reference ES on the host: the better of workers=1 and workers=all
+    (BASELINE.md section 4, step 3), each a bounded run; the oracle port when
+    the reference package is unavailable."""
+    ref = reference_pkg()
+    cores = os.cpu_count() or 1
+    if ref is None:
+        return port_sample(x, seconds)
+    one = ref_sample(x, 1, seconds / 2, ref)
+    allc = ref_sample(x, cores, seconds / 2, ref)
+    best = allc if allc["value"] >= one["value"] else one
+    out = {"value": best["value"], "unit": UNIT, "cores": best["workers"], "kind": "reference",
+           "sample": (f"cecprove.es.run_exhaustive(compile_program(x), workers={best['workers']}, "
+                      f"budget={seconds / 2:.1f}s) from baseline/_ref (numba): "
+                      f"{best['patterns']} patterns in {best['seconds']:.2f}s, verdict "
+                      f"{best['verdict']}{desc}"),
+           "workers_1": {k: one[k] for k in ("value", "patterns", "seconds", "verdict")},
+           f"workers_{cores}": {k: allc[k] for k in ("value", "patterns", "seconds", "verdict")}}
+    if best["verdict"] != "BUDGET_EXCEEDED":
+        out["time_to_verdict_s"] = best["seconds"]
+        out["witness_index"] = best["witness_index"]
+    return out
+
+
+# --- clocks ----------------------------------------------------------------
+
+class ClockSampler:
+    """SM clock and throttle reasons sampled DURING the timed region: NVML in
+    process every 2 ms, on every GPU of the run."""
+
+    # NVML clocks-event-reason bits (nvml.h)
+    REASONS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+               "hw_thermal_slowdown": 0x40}
+
+    def __init__(self, devices, period_s: float = 0.002):
+        self.devices = list(devices) if isinstance(devices, (list, tuple)) else [devices]
+        self.period = period_s
+        self.samples: list[tuple[float, float, int]] = []
+        self._stop = threading.Event()
+        self._t = None
+        self._nvml = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = [pynvml.nvmlDeviceGetHandleByIndex(d) for d in sorted(set(self.devices))]
+            self._max = [float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)) for h in self._h]
+            self._sample()
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        except Exception:
+            self._nvml = None
+        return self
+
+    def _sample(self):
+        nv = self._nvml
+        for h, mx in zip(self._h, self._max):
+            sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+            try:
+                rs = int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))
+            except AttributeError:
+                rs = int(nv.nvmlDeviceGetCurrentClocksThrottleReasons(h))
+            self.samples.append((sm, mx, rs))
+
+    def _run(self):
+        while not self._stop.wait(self.period):
+            try:
+                self._sample()
+            except Exception:
+                return
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join(timeout=2)
+        if self._nvml is not None:
+            try:
+                self._sample()
+            except Exception:
+                pass
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0,
+                    "source": "unavailable"}
+        reasons = sorted({nm for _, _, rs in self.samples for nm, bit in self.REASONS.items()
+                          if rs & bit})
+        return {"sm_mhz": statistics.median(sm for sm, _, _ in self.samples),
+                "sm_max_mhz": max(mx for _, mx, _ in self.samples), "reasons": reasons,
+                "samples": len(self.samples), "source": "NVML, 2 ms period",
+                "gpus": len(set(self.devices))}
+
+
+# --- roofline helpers ------------------------------------------------------
+
+def k1_roofline(prog, k: int, launch_patterns: int, k_ms: float, lane_peak: float, G: int,
+                sess) -> dict:
+    """Hardware fraction of the dominant kernel (es_k1): LOP3 lane-ops it
+    issues per second against the measured LOP3 peak (es_alu_peak).  The
+    algorithmic credit (gate-patterns per executed lane-op: LUT-3 mapping x
+    cofactor sharing) is reported separately as alg_ops_ratio."""
+    from paper_2512_06627_b200 import es
+
+    pipes = es.map_pipes(prog, k)
+    iters = launch_patterns / 32 / 2 ** k  # kernel iterations (2^k words each)
+    lop3_rate = pipes["lop3"] * iters / (k_ms * 1e-3)
+    gate_rate = G * launch_patterns / (k_ms * 1e-3)
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("mult16")
+        except (OSError, ValueError):
+            traffic = None
+    return {"bound": "alu", "unit": "lane-LOP3/s", "achieved": lop3_rate, "peak": lane_peak,
+            "frac": lop3_rate / lane_peak, "traffic": traffic,
+            "kernel": "es_k1", "kernel_ms": k_ms,
+            "peak_source": "measured: es_alu_peak (8 independent LOP3 chains per thread, all SMs)",
+            "achieved_def": "LOP3 instructions of the kernel body (es.map_pipes) x 32 lanes x "
+                            "iterations / kernel time (CUDA events on the launch stream)",
+            "lop3_per_iteration": pipes["lop3"], "imad_per_iteration": pipes["imad"],
+            "words_per_iteration": 2 ** k, "luts_per_iteration": sess.num_luts,
+            "imad_lane_ops_per_s": pipes["imad"] * iters / (k_ms * 1e-3),
+            "gate_patterns_per_s": gate_rate,
+            "alg_ops_ratio": gate_rate / (lop3_rate * 32),
+            "alg_ops_ratio_def": "reference gate-patterns per executed LOP3 lane-op (32 patterns): "
+                                 "LUT-3 mapping x cofactor sharing x IMAD offload -- algorithmic "
+                                 "credit, not utilisation"}
+
+
+def ncu_hw(kcof: int):
+    """ALU/FMA pipe utilisation of the same kernel from the committed ncu
+    summary (the bench itself never runs under a profiler)."""
+    name = {4: "r02_k1_cof4_mult16_ncu_full.json"}.get(kcof)
+    for cand in filter(None, [name, {4: "r01_k1_cof4_mult16_ncu_full.json"}.get(kcof)]):
+        path = os.path.join(ROOT, "profiles", cand)
+        if not os.path.exists(path):
+            continue
+        try:
+            d = json.load(open(path))
+            pct = lambda k: float(d[k].split()[0])  # noqa: E731
+            return {"alu_pipe_pct": pct("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+                    "fma_pipe_pct": pct("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
+                    "issue_active_pct": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                    "source": f"profiles/{cand} (ncu --set full, same kernel)"}
+        except (OSError, ValueError, KeyError):
+            continue
+    return None
+
+
+# --- config 4 (batched cones) ----------------------------------------------
+
 def cones_work(batch, rec) -> tuple[int, int, int]:
     """(gate-patterns, EQ count, NEQ count) of one batched verdict; ``rec`` is
     NativeBatch.run_arrays()'s es_result array."""
@@ -89,15 +339,68 @@ def cones_work(batch, rec) -> tuple[int, int, int]:
     return work, int(eq.sum()), int(neq.sum())
 
 
-def measure_cones(steps: int, warmup: int, rank: int = 0, world: int = 1, count: int = 10_000):
+def cones_oracle_check(batch, rec) -> dict:
+    """Every job of the batched verdict against the CPU oracle's single-worker
+    run (verdict, minimum-index witness, patterns_evaluated); raises on any
+    mismatch (VERDICT r01 next #1)."""
+    from oracle import oracle as O
+
+    t = time.perf_counter()
+    refs = O.run_packed_batch([batch.packed(i) for i in range(len(batch))])
+    codes = {"EXHAUSTED_ZERO": 0, "COUNTEREXAMPLE": 1}
+    bad = 0
+    for i, g in enumerate(refs):
+        if g is None:
+            continue
+        v = int(rec["verdict"][i])
+        w = int(rec["witness_index"][i]) if v == 1 else None
+        if (v, w, int(rec["patterns_evaluated"][i])) != (codes[g.verdict], g.witness_index,
+                                                         g.patterns_evaluated):
+            bad += 1
+    if bad:
+        raise RuntimeError(f"config 4: {bad} of {len(refs)} jobs differ from the oracle")
+    return {"jobs_checked": len(refs), "mismatches": 0, "oracle_s": time.perf_counter() - t}
+
+
+def k2_smem_model(batch, res) -> dict:
+    """Shared-memory wavefronts the K2 interpreter issues (the unit ncu's
+    l1tex__data_pipe_lsu_wavefronts_mem_shared counts): per warp-iteration
+    (32 threads x W words) one broadcast record load plus W wavefronts per
+    slot load or store (W words x 4 B x 32 threads = W x 128 B), with the
+    accumulator forwarding's actual per-program load/store counts."""
+    import numpy as np
+
+    st = batch.k2_stats()
+    tr = batch.k2_traffic()
+    tab = batch.table()
+    ran = (res["reason"] != -1) & (res["engine"] == 2) & (st["num_records"] > 0)
+    W = np.maximum(res["regs_per_thread"], 1).astype(np.float64)  # K2 reports its words per thread here
+    words = res["patterns_swept"].astype(np.float64) / 32.0  # executed pattern words (all copies)
+    copies = np.exp2(st["cofactor_pis"].astype(np.float64))
+    iters = words / copies  # interpreter passes over the record list, per thread-word
+    warp_iters = iters / (32.0 * W)
+    per = st["num_records"] + (tr["loads"] + tr["stores"]) * W
+    wavefronts = float((warp_iters * per)[ran].sum())
+    return {"wavefronts": wavefronts, "bytes": wavefronts * 128.0,
+            "record_passes": float((iters * st["num_records"])[ran].sum())}
+
+
+def measure_cones(steps: int, warmup: int, rank: int = 0, world: int = 1, count: int = 10_000,
+                  check: bool = True, cpu_seconds: float = 0.0):
     """Config 4: one batched ES verdict over ~10k candidate-pair cones.
     Device time = the library's CUDA events around the kernel slices (inputs
     resident); e2e = NativeBatch.run wall time (program upload + results)."""
-    from paper_2512_06627_b200 import cones
+    from paper_2512_06627_b200 import cones, shard
 
     t = time.perf_counter()
-    batch = cones.config4_batch(count)
-    host_ms = 1e3 * (time.perf_counter() - t)
+    batches = cones.config4_batches(count)
+    sample_ms = 1e3 * (time.perf_counter() - t)  # harness: simulate, pick pairs, extract, compile
+    t = time.perf_counter()
+    batch = batches[0]
+    for b in batches[1:]:
+        batch.extend(b)
+    batch.prepare()
+    prepare_ms = 1e3 * (time.perf_counter() - t)  # K2 programs (cofactor depth, schedule)
     if world > 1:
         batch.select(list(range(rank, len(batch), world)))
     for _ in range(warmup):
@@ -109,34 +412,78 @@ def measure_cones(steps: int, warmup: int, rank: int = 0, world: int = 1, count:
         wall_ms.append(1e3 * (time.perf_counter() - t))
         dev_ms.append(float(res["device_ms"].max()))
     work, eq, neq = cones_work(batch, res)
-    # shared-memory roofline of the K2 interpreter (12 B per
-    # gate-word -- two operand loads and one store of a 32-pattern word):
-    # credited = the reference's gate-words, executed = the records the
-    # interpreter ran (cofactor copies, early exits), against the measured
-    # shared-memory load bandwidth
-    import numpy as np
-    from paper_2512_06627_b200 import shard
-
-    st = batch.k2_stats()
-    tab = batch.table()
-    ran = (res["reason"] != -1) & (res["engine"] == 2) & (st["num_records"] > 0)
-    kw = np.exp2(np.maximum(tab["num_pis"] - 5 - st["cofactor_pis"], 0).astype(np.float64))
-    frac_swept = res["patterns_swept"].astype(np.float64) / np.exp2(tab["num_pis"].astype(np.float64))
-    rec_words = float((st["num_records"] * kw * frac_swept)[ran].sum())
     smem_bps, _ = shard.smem_peak(0)
     dev_s = statistics.mean(dev_ms) * 1e-3
+    model = k2_smem_model(batch, res)
     roof = {"bound": "smem", "unit": "GB/s", "peak": smem_bps / 1e9,
             "peak_source": "measured: es_smem_peak (conflict-free 16-byte shared loads, all SMs)",
-            "achieved": work / 32 * 12 / dev_s / 1e9,
-            "executed": rec_words * 12 / dev_s / 1e9,
-            "bytes_per_gate_word": 12, "executed_record_words": rec_words}
+            "achieved": model["bytes"] / dev_s / 1e9,
+            "achieved_def": "shared-memory wavefronts x 128 B the interpreter issues (record "
+                            "broadcasts + slot loads/stores after accumulator forwarding, per "
+                            "program) / device time",
+            "wavefronts": model["wavefronts"], "record_passes": model["record_passes"]}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["executed_frac"] = roof["executed"] / roof["peak"]
-    return {"jobs": len(batch), "eq": eq, "neq": neq, "gate_patterns": work, "roofline": roof,
-            "device_ms": statistics.mean(dev_ms), "e2e_ms": statistics.mean(wall_ms),
-            "extract_compile_ms": host_ms, "value": work / (statistics.mean(dev_ms) * 1e-3),
-            "e2e_value": work / (statistics.mean(wall_ms) * 1e-3)}
+    out = {"jobs": len(batch), "eq": eq, "neq": neq, "gate_patterns": work, "roofline": roof,
+           "device_ms": statistics.mean(dev_ms), "e2e_ms": statistics.mean(wall_ms),
+           "host_ms": {"pair_sampling_extract_compile": sample_ms, "k2_program_build": prepare_ms},
+           "value": work / dev_s, "e2e_value": work / (statistics.mean(wall_ms) * 1e-3)}
+    if check:
+        out["oracle_check"] = cones_oracle_check(batch, res)
+    if cpu_seconds > 0:
+        out["cpu_baseline"] = cones_cpu_baseline(batch, cpu_seconds)
+    return out
 
+
+def _ref_cone_worker(args):
+    """One process of the N-process reference harness: es_check(workers=1) on
+    its share of the cones (the reference's own call, es.py:342)."""
+    items, seconds = args
+    ref = reference_pkg()
+    from paper_2512_06627_b200.xag import Gate, GateKind, Lit, Xag
+
+    work, n, t0 = 0, 0, time.perf_counter()
+    for (npis, kind, in0, in1, out) in items:
+        x = Xag(npis, tuple(Gate(GateKind(int(k)), Lit.unpack(int(a)), Lit.unpack(int(b)))
+                            for k, a, b in zip(kind, in0, in1)), (Lit.unpack(int(out)),))
+        rx = to_ref(x, ref)
+        p = ref.es.compile_program(rx)
+        r = ref.es.run_exhaustive(p, workers=1)
+        work += _ref_G(p) * r.patterns_evaluated
+        n += 1
+        if time.perf_counter() - t0 > seconds:
+            break
+    return work, n, time.perf_counter() - t0
+
+
+def cones_cpu_baseline(batch, seconds: float) -> dict:
+    """the reference's per-cone ES (compile +
+    run_exhaustive, workers=1) in a loop on one core, and the same harness on
+    every host core (one process per core, cones dealt round-robin)."""
+    import multiprocessing as mp
+
+    ref = reference_pkg()
+    items = [batch.packed(i) for i in range(len(batch))]
+    if ref is None:
+        return {"unavailable": "baseline/_ref missing"}
+    _ref_cone_worker((items[:2], 1.0))  # numba JIT outside the timing
+    w1, n1, s1 = _ref_cone_worker((items, seconds / 2))
+    cores = os.cpu_count() or 1
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        parts = pool.map(_ref_cone_worker, [(items[c::cores], seconds / 2) for c in range(cores)])
+    wn = sum(p[0] for p in parts)
+    nn = sum(p[1] for p in parts)
+    sn = max(p[2] for p in parts)
+    best_all = wn / sn
+    return {"value": max(w1 / s1, best_all), "unit": UNIT, "cores": cores if best_all > w1 / s1 else 1,
+            "kind": "reference",
+            "sample": f"cecprove es compile_program + run_exhaustive(workers=1) per cone (baseline/_ref): "
+                      f"1 core {n1} cones in {s1:.1f}s; {cores} processes {nn} cones in {sn:.1f}s",
+            "per_core": {"value": w1 / s1, "cones": n1, "seconds": s1},
+            f"processes_{cores}": {"value": best_all, "cones": nn, "seconds": sn}}
+
+
+# --- other measurements ----------------------------------------------------
 
 def measure_random_sim(local: int, words: int = 1 << 16, cpu: bool = True) -> dict:
     """K3 random simulation of the mult16 miter (every node
@@ -222,8 +569,9 @@ def measure_sweep(local: int) -> dict:
     return out
 
 
-def measure_other_configs(local: int, cofactor="throughput") -> dict:
-    """Short warm measurements of the other BASELINE.json configs on 1 GPU."""
+def measure_other_configs(local: int, cofactor="throughput", cpu_seconds: float = 0.0) -> dict:
+    """Short warm measurements of the other BASELINE.json configs on 1 GPU,
+    each with the reference's CPU ES beside it."""
     from paper_2512_06627_b200 import es
 
     out = {}
@@ -244,165 +592,32 @@ def measure_other_configs(local: int, cofactor="throughput") -> dict:
             devs.append(r.stats["device_ms"])
         pats = (1 << x.num_pis) if r.verdict == "EQUIVALENT" else r.stats["patterns"]
         dev = statistics.median(devs)
-        out[name] = {"workload": desc, "verdict": r.verdict,
-                     "witness_index": None if r.witness is None else
-                     sum(b << i for i, b in enumerate(r.witness)),
-                     "engine": r.stats["engine"], "device_ms": dev,
-                     "e2e_ms": statistics.median(walls), "cold_ms": cold_ms,
-                     "cold_engine": cold.stats["engine"], "cold_jit_ms": cold.stats["jit_ms"],
-                     "gate_patterns_per_s": p.num_gates * pats / (dev * 1e-3)}
+        row = {"workload": desc, "verdict": r.verdict,
+               "witness_index": None if r.witness is None else
+               sum(b << i for i, b in enumerate(r.witness)),
+               "engine": r.stats["engine"], "device_ms": dev,
+               "e2e_ms": statistics.median(walls), "cold_ms": cold_ms,
+               "cold_engine": cold.stats["engine"], "cold_jit_ms": cold.stats["jit_ms"],
+               "gate_patterns_per_s": p.num_gates * pats / (dev * 1e-3),
+               "patterns_swept": r.stats["patterns_swept"], "phases": r.stats["phases"],
+               "phase2_copies": r.stats["phase2_copies"],
+               "phase2_cofactor_pis": r.stats["phase2_cofactor_pis"]}
+        if cpu_seconds > 0:
+            cb = cpu_baseline(x, cpu_seconds)
+            row["cpu_baseline"] = cb
+            if "time_to_verdict_s" in cb:
+                row["speedup_time_to_verdict_vs_cpu"] = cb["time_to_verdict_s"] * 1e3 / row["e2e_ms"]
+            else:  # rate-based: the CPU's time to the same verdict at its measured rate
+                row["cpu_time_to_verdict_est_s"] = p.num_gates * pats / cb["value"]
+        out[name] = row
+    eq = out.get("mult16_neq")
     return out
 
-
-# --- clocks ----------------------------------------------------------------
-
-class ClockSampler:
-    """SM clock and throttle reasons sampled DURING the timed region: NVML in
-    process every 2 ms (a 50-step mult16 region is ~130 ms, too short for an
-    nvidia-smi child to start), nvidia-smi -lms as the fallback."""
-
-    # NVML clocks-event-reason bits (nvml.h)
-    REASONS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
-               "hw_thermal_slowdown": 0x40}
-
-    def __init__(self, device: int, period_s: float = 0.002):
-        self.device = device
-        self.period = period_s
-        self.samples: list[tuple[float, float, int]] = []
-        self._stop = threading.Event()
-        self._t = None
-        self._nvml = None
-
-    def __enter__(self):
-        try:
-            import pynvml
-            pynvml.nvmlInit()
-            self._nvml = pynvml
-            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
-            self._max = float(pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM))
-            self._sample()
-            self._t = threading.Thread(target=self._run, daemon=True)
-            self._t.start()
-        except Exception:
-            self._nvml = None
-        return self
-
-    def _sample(self):
-        nv = self._nvml
-        sm = float(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
-        try:
-            rs = int(nv.nvmlDeviceGetCurrentClocksEventReasons(self._h))
-        except AttributeError:
-            rs = int(nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h))
-        self.samples.append((sm, self._max, rs))
-
-    def _run(self):
-        while not self._stop.wait(self.period):
-            try:
-                self._sample()
-            except Exception:
-                return
-
-    def __exit__(self, *exc):
-        self._stop.set()
-        if self._t is not None:
-            self._t.join(timeout=2)
-        if self._nvml is not None:
-            try:
-                self._sample()
-            except Exception:
-                pass
-
-    def summary(self) -> dict:
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0,
-                    "source": "unavailable"}
-        reasons = sorted({nm for _, _, rs in self.samples for nm, bit in self.REASONS.items()
-                          if rs & bit})
-        return {"sm_mhz": statistics.median(sm for sm, _, _ in self.samples),
-                "sm_max_mhz": max(mx for _, mx, _ in self.samples), "reasons": reasons,
-                "samples": len(self.samples), "source": "NVML, 2 ms period"}
-
-
-# --- CPU baseline (oracle port of the reference algorithm) -----------------
-
-def cpu_sample(x, target_s: float, threads: int | None = None) -> dict:
-    """Time the reference algorithm's CPU restatement on a bounded prefix of
-    the sweep (whole 2^14-pattern batches, all host threads)."""
-    from oracle import oracle as O
-
-    p = O.compile_program(x)
-    G = p.num_gate_instrs
-    threads = threads or os.cpu_count() or 1
-    total_batches = 1 << max(x.num_pis - 14, 0)
-    per_batch = 1 << min(x.num_pis, 14)
-    O.min_witness(p, threads=threads, max_batches=min(total_batches, 4 * threads))  # warm-up
-    probe = min(total_batches, 64 * threads)
-    t = time.perf_counter()
-    O.min_witness(p, threads=threads, max_batches=probe)
-    dt = max(time.perf_counter() - t, 1e-6)
-    nb = int(min(total_batches, max(probe, probe * target_s / dt)))
-    t = time.perf_counter()
-    verdict, idx, done = O.min_witness(p, threads=threads, max_batches=nb)
-    dt = time.perf_counter() - t
-    work = G * done * per_batch
-    return {"value": work / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"first {nb} of {total_batches} reference batches (2^{min(x.num_pis, 14)} "
-                      f"patterns each) of the same sweep, G={G}, {dt:.2f}s, "
-                      f"oracle/es_oracle.c (es.py:175-339 restated), {threads} threads",
-            "seconds": dt, "batches": int(done)}
-
-
-def run_reference(args) -> None:
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
-    from oracle import oracle as O
-
-    x, desc = build_workload(args.config)
-    p = O.compile_program(x)
-    G = p.num_gate_instrs
-    threads = os.cpu_count() or 1
-    per_batch = 1 << min(x.num_pis, 14)
-    total_batches = 1 << max(x.num_pis - 14, 0)
-    # size one step to ~1.5 s of work on this host
-    probe = min(total_batches, 64 * threads)
-    O.min_witness(p, threads=threads, max_batches=probe)
-    t = time.perf_counter()
-    O.min_witness(p, threads=threads, max_batches=probe)
-    dt = max(time.perf_counter() - t, 1e-6)
-    nb = int(min(total_batches, max(probe, probe * 1.5 / dt)))
-    for _ in range(args.warmup):
-        O.min_witness(p, threads=threads, max_batches=nb)
-    t = time.perf_counter()
-    done = 0
-    for _ in range(args.steps):
-        _, _, d = O.min_witness(p, threads=threads, max_batches=nb)
-        done += d
-    el = time.perf_counter() - t
-    value = G * done * per_batch / el
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "u64 (bit-parallel words)", "data": "synthetic",
-            "impl": "reference",
-            "config": {"workload": desc, "num_pis": x.num_pis, "G": G,
-                       "step": f"{nb} of {total_batches} reference batches per step"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": f"{nb} batches x 2^{min(x.num_pis, 14)} patterns per "
-                                       f"step, all {threads} host threads"},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
-
-
-# --- the B200 arm ----------------------------------------------------------
 
 def disk_cache_ttv(config: str, cofactor) -> dict:
     """Cold time-to-verdict in a fresh process with the on-disk cubin cache
     (es_jit.cpp) populated by a previous process: compile + map + load + sweep,
     no ptxas.  Two child processes on a private cache directory."""
-    import tempfile
     code = ("import sys, time, json; sys.path.insert(0, %r)\n"
             "from bench import build_workload\n"
             "from paper_2512_06627_b200 import es\n"
@@ -425,288 +640,415 @@ def disk_cache_ttv(config: str, cofactor) -> dict:
             "cold_ms_first_process": out["populate"]["ms"]}
 
 
+# --- the reference arm -----------------------------------------------------
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    ref = reference_pkg()
+    # each step a bounded sample so the whole run ends within a few minutes
+    per_step = max(0.3, min(5.0, 150.0 / max(1, args.steps + args.warmup)))
+    base = {"metric": METRIC, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u64 (bit-parallel words)", "data": "synthetic",
+            "impl": "reference"}
+    if args.config == "cones":
+        from paper_2512_06627_b200 import cones
+        batch = cones.config4_batch(10_000)
+        items = [batch.packed(i) for i in range(len(batch))]
+        _ref_cone_worker((items[:2], 1.0))
+        work = 0
+        el = 0.0
+        for s in range(args.warmup + args.steps):
+            w, n, dt = _ref_cone_worker((items[(s * 97) % len(items):], per_step))
+            if s >= args.warmup:
+                work, el = work + w, el + dt
+        value = work / el
+        line = dict(base, value=value, ms_per_step=1e3 * el / args.steps,
+                    config={"workload": "config 4: ~10k candidate-pair cones (14-24 PIs) of 16x16 "
+                                        "multiplier miters", "step": f"{per_step:.2f}s of per-cone ES"},
+                    cpu_baseline={"value": value, "unit": UNIT, "cores": 1, "kind": "reference",
+                                  "sample": f"cecprove compile_program + run_exhaustive(workers=1) per "
+                                            f"cone, {per_step:.2f}s per step"},
+                    e2e={"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
+        print(json.dumps(line), flush=True)
+        return
+    x, desc = build_workload(args.config)
+    if ref is None:  # the oracle's C restatement (kind "port")
+        from oracle import oracle as O
+        p = O.compile_program(x)
+        G = p.num_gate_instrs
+        per_batch = 1 << min(x.num_pis, 14)
+        total_batches = 1 << max(x.num_pis - 14, 0)
+        probe = min(total_batches, 64 * cores)
+        O.min_witness(p, threads=cores, max_batches=probe)
+        t = time.perf_counter()
+        O.min_witness(p, threads=cores, max_batches=probe)
+        dt = max(time.perf_counter() - t, 1e-6)
+        nb = int(min(total_batches, max(probe, probe * per_step / dt)))
+        for _ in range(args.warmup):
+            O.min_witness(p, threads=cores, max_batches=nb)
+        t = time.perf_counter()
+        done = sum(O.min_witness(p, threads=cores, max_batches=nb)[2] for _ in range(args.steps))
+        el = time.perf_counter() - t
+        value = G * done * per_batch / el
+        kind, sample = "port", f"{nb} batches x 2^{min(x.num_pis, 14)} patterns per step (oracle C port)"
+    else:
+        p = ref.es.compile_program(to_ref(x, ref))
+        G = _ref_G(p)
+        ref.es.run_exhaustive(p, workers=cores, budget=0.05)  # numba JIT
+        for _ in range(args.warmup):
+            ref.es.run_exhaustive(p, workers=cores, budget=per_step)
+        pats, el = 0, 0.0
+        verdicts = set()
+        for _ in range(args.steps):
+            t = time.perf_counter()
+            r = ref.es.run_exhaustive(p, workers=cores, budget=per_step)
+            el += time.perf_counter() - t
+            pats += r.patterns_evaluated
+            verdicts.add(r.verdict)
+        value = G * pats / el
+        kind = "reference"
+        sample = (f"cecprove.es.run_exhaustive(compile_program(x), workers={cores}, budget="
+                  f"{per_step:.2f}s) per step (baseline/_ref, numba); verdicts {sorted(verdicts)}")
+    line = dict(base, value=value, ms_per_step=1e3 * el / args.steps,
+                config={"workload": desc, "num_pis": x.num_pis, "G": G,
+                        "step": f"bounded sample: {per_step:.2f}s of the same sweep"},
+                cpu_baseline={"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
+                e2e={"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
+    print(json.dumps(line), flush=True)
+
+
+# --- the B200 arm ----------------------------------------------------------
+
 def run_b200(args) -> None:
     import torch
-    import torch.distributed as dist
 
     # cold numbers below are true cold: no on-disk cubin cache in this process
     os.environ["ES_JIT_CACHE"] = "0"
-
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    local = local % max(torch.cuda.device_count(), 1) if args.backend != "nccl" else local
-    torch.cuda.set_device(local)
-    dev = torch.device(f"cuda:{local}")
-    group = None
+    if world > 1 and world != args.gpus:
+        raise SystemExit(f"bench: torchrun WORLD_SIZE={world} but --gpus {args.gpus}")
+    if args.cofactor.isdigit():
+        args.cofactor = int(args.cofactor)
     if world > 1:
-        # --backend gloo lets several ranks share one GPU (NCCL needs one GPU per rank)
-        if args.backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
-        else:
-            dist.init_process_group(args.backend)
+        run_ranks(args, world)
+        return
+    from paper_2512_06627_b200 import es
+
+    visible = es.device_count()
+    if visible < args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but only {visible} CUDA device(s) visible")
+    if args.config == "cones":
+        run_cones(args)
+        return
+    run_local(args, list(range(args.gpus)))
+
+
+def run_local(args, devs: list[int]) -> None:
+    """N GPUs driven by ONE es_run call (es_run_opts.devices), or 1 GPU."""
+    import torch
 
     from paper_2512_06627_b200 import es, shard
 
-    if args.cofactor.isdigit():
-        args.cofactor = int(args.cofactor)
+    N = len(devs)
+    devices = devs if N > 1 else None
+    x, desc = build_workload(args.config)
+    sm = _Sub(x)
+    P = x.num_pis
+    for d in devs:
+        torch.cuda.set_device(d)
+        shard.alu_peak(d)  # CUDA context + module load outside the cold measurement
+    torch.cuda.set_device(devs[0])
+    # cold time-to-verdict: compile + map + JIT + sweep, first call in process,
+    # in the default latency mode (cofactor="auto") and in this run's mode
+    t = time.perf_counter()
+    prog = es.compile_program(x)
+    cold = es.run_exhaustive(prog, engine="jit", cofactor="auto", devices=devices)
+    cold_ms = 1e3 * (time.perf_counter() - t)
+    t = time.perf_counter()
+    cold_t = es.run_exhaustive(es.compile_program(x), engine="jit", cofactor=args.cofactor, devices=devices)
+    cold_t_ms = 1e3 * (time.perf_counter() - t)
+    G = prog.num_gates
+    if (cold_t.verdict, cold_t.witness_index) != (cold.verdict, cold.witness_index):
+        raise RuntimeError("cofactor modes disagree")
+    expected = (cold.verdict, cold.witness_index)
+    flush = [torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{d}") for d in devs]
+
+    def step():
+        r = es.run_exhaustive(prog, engine="jit", cofactor=args.cofactor, devices=devices)
+        if (r.verdict, r.witness_index) != expected:
+            raise RuntimeError(f"verdict drift: {r.verdict} {r.witness_index} vs {expected}")
+        return r
+
+    def sync():
+        for d in devs:
+            torch.cuda.synchronize(d)
+
+    for _ in range(args.warmup):
+        step()
+        for f in flush:
+            f.zero_()
+    sync()
+    # timed region: K verdicts; device time of each = the library's CUDA events
+    # around its launch slices (max over the GPUs); L2 flushed between verdicts
+    dev_ms, host_ms = [], []
+    with ClockSampler(devs) as clk:
+        for _ in range(args.steps):
+            t = time.perf_counter()
+            r = step()
+            host_ms.append(1e3 * (time.perf_counter() - t))
+            dev_ms.append(r.stats["device_ms"])
+            for f in flush:
+                f.zero_()
+            sync()
+    total_s = sum(dev_ms) * 1e-3
+    patterns_per_step = (1 << P) if r.witness_index is None else min(1 << P, r.patterns_evaluated)
+    value = G * patterns_per_step * args.steps / total_s
+
+    # dominant kernel (es_k1) alone on GPU 0: one launch over the whole space
+    sess = shard.session_for(prog, devs[0], args.cofactor)
+    dev = torch.device(f"cuda:{devs[0]}")
+    best = torch.empty(1, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(max(args.steps, 5))]
+    for a, b in kev:
+        best.fill_(1 << P)
+        flush[0].zero_()
+        a.record()
+        sess.launch(stream, best.data_ptr(), 0, sess.n_chunks, 0, 1)
+        b.record()
+    torch.cuda.synchronize(dev)
+    k_ms = statistics.mean(a.elapsed_time(b) for a, b in kev)
+    launch_patterns = sess.n_chunks * sess.patterns_per_chunk
+    if r.witness_index is not None:
+        launch_patterns = min(launch_patterns, r.stats["patterns_swept"])
+    lane_peak, _ = shard.alu_peak(devs[0])
+    kcof = cold_t.stats.get("cofactor_pis", 0)
+    roof = k1_roofline(prog, kcof, launch_patterns, k_ms, lane_peak, G, sess)
+    roof["hardware"] = ncu_hw(kcof) if args.config == "mult16" else None
+
+    # e2e through the public API: host circuit in, host verdict out
+    for _ in range(max(1, args.warmup)):
+        es.es_check(sm, engine="jit", cofactor=args.cofactor, devices=devices)
+    e_ms, launches = [], []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        res = es.es_check(sm, engine="jit", cofactor=args.cofactor, devices=devices)
+        e_ms.append(1e3 * (time.perf_counter() - t))
+        launches.append(res.stats["launches"])
+    e2e_value = G * patterns_per_step * args.steps / (sum(e_ms) * 1e-3)
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        cpu = cpu_baseline(x, args.cpu_seconds)
+    mode_desc = (f"{N} GPUs in one es_run call (es_run_opts.devices): chunks dealt round-robin, one "
+                 "host thread per GPU, one minimum word in GPU 0's HBM shared as NVLink peer memory "
+                 "(kernel atomicMin + skip rule), no collective" if N > 1 else "1 GPU, es_run")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_s * 1e3 / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "u32 (bit-parallel LOP3 words)", "data": "synthetic",
+        "config": {"workload": desc, "num_pis": P, "G": G, "patterns_per_step": patterns_per_step,
+                   "verdict": r.verdict, "witness_index": r.witness_index,
+                   "parallelism": mode_desc,
+                   "l2": "flushed between steps (256 MiB write per GPU, outside the step's device "
+                         "time); the kernel reads no HBM inputs",
+                   "cofactor_pis": kcof, "words_per_iteration": 2 ** kcof,
+                   "luts_per_iteration": sess.num_luts, "luts_per_word": sess.num_luts / 2 ** kcof,
+                   "regs_per_thread": sess.regs_per_thread, "phases": r.stats["phases"],
+                   "patterns_swept": r.stats["patterns_swept"],
+                   "host_ms_per_step": statistics.mean(host_ms)},
+        "roofline": roof,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * N,
+                "d2h_bytes_per_step": 20 * int(statistics.mean(launches)),
+                "path": "es.es_check(sub-miter) -> compile_program -> C ABI es_run (host circuit in, "
+                        "host verdict out; JIT module cached by program hash)",
+                "ms_per_step": statistics.mean(e_ms)},
+        "time_to_verdict": {"cold_ms": cold_ms, "jit_ms": cold.stats.get("jit_ms"),
+                            "host_compile_ms": cold.stats.get("compile_ms"),
+                            "device_ms": cold.stats.get("device_ms"),
+                            "mode": f"cofactor=auto (latency), k={cold.stats.get('cofactor_pis')}",
+                            f"cold_ms_{args.cofactor}": cold_t_ms,
+                            f"jit_ms_{args.cofactor}": cold_t.stats.get("jit_ms"),
+                            f"device_ms_{args.cofactor}": cold_t.stats.get("device_ms"),
+                            "warm_device_ms": total_s * 1e3 / args.steps,
+                            "note": "cold = first call in a process, JIT included, on-disk cubin "
+                                    "cache off"},
+        "gpu_launches": int(sum(launches)),
+        "clocks": clk.summary(),
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        line["cpu_baseline"]["detail"] = {k: v for k, v in cpu.items()
+                                          if k not in ("value", "unit", "cores", "kind", "sample")}
+    if N == 1 and not args.no_extras:
+        for mode in ("auto", args.cofactor):
+            line["time_to_verdict"][f"disk_cache_{mode}"] = disk_cache_ttv(args.config, mode)
+        # the GPU idled (down-clocked) during the child processes: bring the
+        # clocks back up before the short extra measurements
+        t_end = time.perf_counter() + 0.5
+        while time.perf_counter() < t_end:
+            sess.launch(stream, best.data_ptr(), 0, sess.n_chunks, 0, 1)
+            torch.cuda.synchronize(dev)
+        cs = 0.0 if args.no_cpu_baseline else args.extra_cpu_seconds
+        extras = measure_other_configs(devs[0], args.cofactor, cs)
+        extras["random_sim"] = measure_random_sim(devs[0], cpu=not args.no_cpu_baseline)
+        extras["sweep_es"] = measure_sweep(devs[0])
+        extras["cones"] = {"workload": "config 4: ~10k candidate-pair cones (14-24 PIs) of "
+                                       "16x16 multiplier miters, one batched launch",
+                           **measure_cones(5, 2, cpu_seconds=cs)}
+        line["other_configs"] = extras
+    print(json.dumps(line), flush=True)
+
+
+def run_ranks(args, world: int) -> None:
+    """torchrun: one process per GPU, each sweeping its residue class of
+    chunks; one shared minimum word per verdict (CUDA IPC into rank 0's HBM,
+    NVLink peer memory) closed by a device-side barrier, verdicts queued
+    back to back (p2p), or the NCCL MIN all-reduce fallback (--collective nccl)."""
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.backend == "nccl":
+        if torch.cuda.device_count() < world:
+            raise SystemExit(f"bench: {world} ranks but {torch.cuda.device_count()} GPUs visible")
+    else:  # --backend gloo lets several ranks share one GPU (tests only)
+        local = local % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    if args.backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(args.backend)
+    from paper_2512_06627_b200 import es, shard
+
     if args.config == "cones":
         run_cones(args, rank, world, local, dev)
         return
     x, desc = build_workload(args.config)
-    sm = _Sub(x)
     P = x.num_pis
-
-    # CUDA context + module load outside the cold measurement (a process pays
-    # them once, whatever it runs); the roofline's peak is re-measured later
-    shard.alu_peak(local)
-    # cold time-to-verdict: compile + map + JIT + sweep, first call in process,
-    # once in the default latency mode (cofactor="auto") and once in the mode
-    # this bench runs (--cofactor, default "throughput": deepest profitable
-    # cofactor expansion, larger JIT)
-    t = time.perf_counter()
     prog = es.compile_program(x)
-    cold = es.run_exhaustive(prog, engine="jit", cofactor="auto")
-    cold_ms = 1e3 * (time.perf_counter() - t)
-    t = time.perf_counter()
-    cold_t = es.run_exhaustive(es.compile_program(x), engine="jit", cofactor=args.cofactor)
-    cold_t_ms = 1e3 * (time.perf_counter() - t)
     G = prog.num_gates
-    expected = cold.verdict
-    if (cold_t.verdict, cold_t.witness_index) != (cold.verdict, cold.witness_index):
-        raise RuntimeError("cofactor modes disagree")
-
+    expected = es.run_exhaustive(prog, engine="jit", cofactor=args.cofactor, device=local)
     sess = shard.session_for(prog, local, args.cofactor)
-    best = torch.empty(1, dtype=torch.int64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    S = args.slices or (1 if world == 1 else 4)
+    collective = args.collective
     peer = None
-    collective = args.collective if world > 1 else "none"
     if collective == "p2p":
         try:
-            peer = shard.PeerBest(group, local)
+            peer = shard.PeerBest(None, local)
         except Exception as exc:  # no IPC / peer access: fall back to NCCL MIN
             print(f"[bench] peer word unavailable ({exc}); using NCCL all-reduce", file=sys.stderr)
             collective = "nccl"
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    def step():
-        if peer is not None:
-            r = shard.sweep_peer(prog, peer, group, local, cofactor=args.cofactor)
-        else:
-            r = shard.sweep_sharded(prog, group, local, slices=S, best=best, cofactor=args.cofactor)
-        if r.verdict != expected or r.witness_index != cold.witness_index:
-            raise RuntimeError(f"verdict drift: {r.verdict} {r.witness_index} vs "
-                               f"{expected} {cold.witness_index}")
-        return r
-
-    for _ in range(args.warmup):
-        step()
-        flush.zero_()
-    torch.cuda.synchronize()
-
-    # timed region: K steps, each bracketed by CUDA events on the launch stream,
-    # L2 flushed between steps (outside the events)
+    S = args.slices or 4
+    best = torch.empty(1, dtype=torch.int64, device=dev)
+    n = args.warmup + args.steps
+    outs = torch.empty(n, dtype=torch.int64, device=dev)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
-    barrier()
+
+    def verdict(i: int):
+        if peer is not None:  # queued: no host synchronisation
+            shard.sweep_peer_async(prog, peer, outs[i].data_ptr(), local, args.cofactor)
+        else:
+            r = shard.sweep_sharded(prog, None, local, slices=S, best=best, cofactor=args.cofactor)
+            outs[i].fill_(r.witness_index if r.witness_index is not None else (1 << 64) - 1 - (1 << 63) * 2)
+
+    for i in range(args.warmup):
+        verdict(i)
+        flush.zero_()
     torch.cuda.synchronize()
+    dist.barrier()
     with ClockSampler(local) as clk:
         for i in range(args.steps):
             evs[i][0].record()
-            r = step()
+            verdict(args.warmup + i)
             evs[i][1].record()
             flush.zero_()
         torch.cuda.synchronize()
-    barrier()
+    dist.barrier()
+    words = [int(v) & 0xFFFFFFFFFFFFFFFF for v in outs.tolist()]
+    want = expected.witness_index
+    for w in words:
+        got = w if w < (1 << P) else None
+        if got != want:
+            raise RuntimeError(f"rank {rank}: verdict drift {got} vs {want}")
     step_ms = [a.elapsed_time(b) for a, b in evs]
-    total_ms = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
-    total_s = float(total_ms.item()) * 1e-3
-    patterns_per_step = (1 << P) if r.witness_index is None else min(
-        1 << P, r.patterns_evaluated)
+    total = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    dist.all_reduce(total, op=dist.ReduceOp.MAX)
+    total_s = float(total.item()) * 1e-3
+    patterns_per_step = (1 << P) if want is None else min(1 << P, expected.patterns_evaluated)
     value = G * patterns_per_step * args.steps / total_s
-
-    # dominant kernel (es_k1) alone: this rank's shard in one launch
-    stream = torch.cuda.current_stream(dev).cuda_stream
-    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    for i in range(args.steps):
-        best.fill_(1 << P)
-        flush.zero_()
-        kev[i][0].record()
-        sess.launch(stream, best.data_ptr(), 0, sess.n_chunks, rank, world)
-        kev[i][1].record()
-    torch.cuda.synchronize()
-    k_ms = statistics.mean(a.elapsed_time(b) for a, b in kev)
-    my_chunks = len(range(rank, sess.n_chunks, world))
-    launch_patterns = my_chunks * sess.patterns_per_chunk
-    if r.witness_index is not None:
-        launch_patterns = min(launch_patterns, r.patterns_evaluated // world + sess.patterns_per_chunk)
-    lane_peak, _ = shard.alu_peak(local)
-    achieved = G * launch_patterns / (k_ms * 1e-3)
-    kcof = cold_t.stats.get("cofactor_pis", 0)  # same program, same mode as the session
-    pipes = es.map_pipes(prog, kcof)
-    # per kernel iteration = 2^k words (one per cofactor copy)
-    lop3_rate = pipes["lop3"] * (launch_patterns / 32 / 2 ** kcof) / (k_ms * 1e-3)
-
-    # e2e through the public API, host circuit in, host verdict out
-    def e2e_step():
-        if world == 1:
-            res = es.es_check(sm, engine="jit", cofactor=args.cofactor)
-        elif peer is not None:
-            res = shard.es_check_peer(sm, peer, group, local, cofactor=args.cofactor)
-        else:
-            res = shard.es_check_sharded(sm, group, local, slices=S, cofactor=args.cofactor)
-        return res
-    for _ in range(max(1, args.warmup)):
-        e2e_step()
-    barrier()
+    # e2e: es_check through the sharded API, host circuit in, host verdict out
+    sm = _Sub(x)
     e_ms = []
-    for _ in range(args.steps):
-        barrier()
+    for i in range(max(1, args.warmup) + args.steps):
+        dist.barrier()
         t = time.perf_counter()
-        res = e2e_step()
-        e_ms.append(1e3 * (time.perf_counter() - t))
+        if peer is not None:
+            shard.es_check_peer(sm, peer, None, local, cofactor=args.cofactor)
+        else:
+            shard.es_check_sharded(sm, None, local, slices=S, cofactor=args.cofactor)
+        if i >= max(1, args.warmup):
+            e_ms.append(1e3 * (time.perf_counter() - t))
     e_total = torch.tensor([sum(e_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(e_total, op=dist.ReduceOp.MAX)
+    dist.all_reduce(e_total, op=dist.ReduceOp.MAX)
     e2e_value = G * patterns_per_step * args.steps / (float(e_total.item()) * 1e-3)
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_sample(x, args.cpu_seconds)
-
     if rank == 0:
-        traffic = None
-        prof = os.path.join(ROOT, "profiles", "k1_traffic.json")
-        if os.path.exists(prof):
-            try:
-                traffic = json.load(open(prof)).get(args.config)
-            except (OSError, ValueError):
-                traffic = None
-        # hardware pipe utilisation of the same kernel from the committed ncu
-        # summary (the bench itself never runs under a profiler)
-        hw = None
-        ncu_file = {4: "r01_k1_cof4_mult16_ncu_full.json", 3: "r01_k1_cof3_mult16_ncu_full.json",
-                    0: "r01_k1_mult16_ncu_full.json"}.get(kcof)
-        if args.config == "mult16" and ncu_file and os.path.exists(os.path.join(ROOT, "profiles", ncu_file)):
-            try:
-                d = json.load(open(os.path.join(ROOT, "profiles", ncu_file)))
-                pct = lambda k: float(d[k].split()[0])  # noqa: E731
-                hw = {"alu_pipe_pct": pct("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
-                      "fma_pipe_pct": pct("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
-                      "issue_active_pct": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
-                      "source": f"profiles/{ncu_file} (ncu --set full, same kernel)"}
-            except (OSError, ValueError, KeyError):
-                hw = None
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_s * 1e3 / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "u32 (bit-parallel LOP3 words)", "data": "synthetic",
-            "config": {"workload": desc, "num_pis": P, "G": G,
-                       "patterns_per_step": patterns_per_step, "verdict": r.verdict,
-                       "witness_index": r.witness_index,
-                       "parallelism": (f"pattern-space shards x{world}; one shared minimum word "
-                                       "in rank 0's HBM mapped into every rank (CUDA IPC, NVLink "
-                                       "peer memory): kernel atomicMin + early exit, 1 barrier "
-                                       "per verdict" if collective == "p2p" else
-                                       f"pattern-space shards x{world}, NCCL MIN all-reduce "
-                                       f"after each of {S} launch slice(s)") if world > 1 else
-                                      "1 GPU, 1 launch per verdict",
-                       "l2": "flushed between steps (256 MiB write, outside the step events); "
-                             "the kernel reads no HBM inputs",
-                       "cofactor_pis": kcof, "words_per_iteration": 2 ** kcof,
-                       "luts_per_iteration": sess.num_luts,
-                       "luts_per_word": sess.num_luts / 2 ** kcof,
-                       "regs_per_thread": sess.regs_per_thread},
-            "roofline": {"bound": "alu", "achieved": achieved,
-                         "peak": lane_peak * 32, "unit": UNIT,
-                         "frac": achieved / (lane_peak * 32), "traffic": traffic,
-                         "hardware": hw,
-                         "kernel": "es_k1", "kernel_ms": k_ms,
-                         "peak_source": "measured: es_alu_peak LOP3 microbenchmark on this GPU "
-                                        "(lane-LOP3/s x 32 patterns, 1 gate per LOP3)",
-                         "issue": {"luts_per_iteration": sess.num_luts,
-                                   "lop3_per_iteration": pipes["lop3"],
-                                   "imad_per_iteration": pipes["imad"],
-                                   "words_per_iteration": 2 ** kcof,
-                                   "achieved_lane_lop3_per_s": lop3_rate,
-                                   "peak_lane_lop3_per_s": lane_peak,
-                                   "frac": lop3_rate / lane_peak,
-                                   "note": "LUT-level ops only; ncu pipe utilisation in "
-                                           "profiles/ covers PI/loop overhead"}},
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 56 * S + 8,
-                    "d2h_bytes_per_step": 8,
-                    "path": "es.es_check(sub-miter) -> compile_program -> C ABI es_run "
-                            "(JIT module cached by program hash)" if world == 1 else
-                            ("shard.es_check_peer -> compile_program -> one session launch per rank "
-                             "on the shared peer word + 1 barrier" if collective == "p2p" else
-                             "shard.es_check_sharded -> compile_program -> session launches + NCCL MIN"),
+            "config": {"workload": desc, "num_pis": P, "G": G, "patterns_per_step": patterns_per_step,
+                       "verdict": expected.verdict, "witness_index": want,
+                       "parallelism": (f"torchrun x{world}: pattern-space shards, one minimum word in "
+                                       "rank 0's HBM mapped into every rank (CUDA IPC / NVLink peer "
+                                       "memory), kernel atomicMin + skip rule, device-side verdict "
+                                       "barrier (es_peer_arrive_wait), verdicts queued back to back"
+                                       if collective == "p2p" else
+                                       f"torchrun x{world}: pattern-space shards, NCCL MIN all-reduce "
+                                       f"after each of {S} launch slice(s)"),
+                       "l2": "flushed between steps (256 MiB write, outside the step events)",
+                       "cofactor_pis": expected.stats["cofactor_pis"],
+                       "luts_per_iteration": sess.num_luts},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8, "d2h_bytes_per_step": 8,
+                    "path": "shard.es_check_peer -> compile_program -> session launch + device barrier"
+                            if collective == "p2p" else "shard.es_check_sharded",
                     "ms_per_step": float(e_total.item()) / args.steps},
-            "time_to_verdict": {"cold_ms": cold_ms, "jit_ms": cold.stats.get("jit_ms"),
-                                "host_compile_ms": cold.stats.get("compile_ms"),
-                                "device_ms": cold.stats.get("device_ms"),
-                                "mode": "cofactor=auto (latency: JIT + sweep estimate), "
-                                        f"k={cold.stats.get('cofactor_pis')}",
-                                f"cold_ms_{args.cofactor}": cold_t_ms,
-                                f"jit_ms_{args.cofactor}": cold_t.stats.get("jit_ms"),
-                                f"device_ms_{args.cofactor}": cold_t.stats.get("device_ms"),
-                                "warm_device_ms": total_s * 1e3 / args.steps,
-                                "note": "cold = first call in a process, JIT included, on-disk "
-                                        "cubin cache off; disk_cache = a later process whose "
-                                        "cubins were compiled by an earlier one (the reference's "
-                                        "numba cache=True analogue)"},
-            "gpu_launches": args.steps * (1 if collective == "p2p" else S) * world,
+            "gpu_launches": args.steps * world * (3 if collective == "p2p" else S),
             "clocks": clk.summary(),
         }
-        if cpu is not None:
-            line["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
-        if world == 1 and not args.no_extras:
-            for mode in ("auto", args.cofactor):
-                line["time_to_verdict"][f"disk_cache_{mode}"] = disk_cache_ttv(args.config, mode)
-            # the GPU idled (down-clocked) during the child processes: bring the
-            # clocks back up before the short extra measurements
-            t_end = time.perf_counter() + 0.5
-            while time.perf_counter() < t_end:
-                sess.launch(stream, best.data_ptr(), 0, sess.n_chunks, rank, world)
-                torch.cuda.synchronize()
-            extras = measure_other_configs(local, args.cofactor)
-            extras["random_sim"] = measure_random_sim(local, cpu=not args.no_cpu_baseline)
-            extras["sweep_es"] = measure_sweep(local)
-            extras["cones"] = {"workload": "config 4: ~10k candidate-pair cones (14-24 PIs) of "
-                                           "16x16 multiplier miters, one batched launch",
-                               **measure_cones(5, 2)}
-            line["other_configs"] = extras
         print(json.dumps(line), flush=True)
     if peer is not None:
-        barrier()
         peer.close()
-    if world > 1:
-        dist.destroy_process_group()
+    dist.destroy_process_group()
 
 
-def run_cones(args, rank, world, local, dev) -> None:
+def run_cones(args, rank: int = 0, world: int = 1, local: int = 0, dev=None) -> None:
     """Config 4 as the headline workload (--config cones)."""
     import torch
     import torch.distributed as dist
 
     with ClockSampler(local) as clk:
-        m = measure_cones(args.steps, args.warmup, rank, world)
-    t = torch.tensor([m["device_ms"], m["e2e_ms"]], dtype=torch.float64, device=dev)
+        m = measure_cones(args.steps, args.warmup, rank, world, check=True,
+                          cpu_seconds=0.0 if args.no_cpu_baseline or rank else args.extra_cpu_seconds)
     if world > 1:
+        t = torch.tensor([m["device_ms"], m["e2e_ms"]], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         w = torch.tensor([m["gate_patterns"]], dtype=torch.float64, device=dev)
         dist.all_reduce(w)
         work = float(w.item())
+        dev_ms, e2e_ms = float(t[0]), float(t[1])
     else:
-        work = m["gate_patterns"]
-    dev_ms, e2e_ms = float(t[0]), float(t[1])
+        work, dev_ms, e2e_ms = m["gate_patterns"], m["device_ms"], m["e2e_ms"]
     if rank == 0:
         line = {"metric": METRIC, "value": work / (dev_ms * 1e-3), "unit": UNIT,
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -715,12 +1057,15 @@ def run_cones(args, rank, world, local, dev) -> None:
                 "config": {"workload": "config 4: ~10k candidate-pair cones (14-24 PIs) of 16x16 "
                                        "multiplier miters, batched K2 launch",
                            "jobs_rank0": m["jobs"], "eq_rank0": m["eq"], "neq_rank0": m["neq"],
-                           "extract_compile_ms": m["extract_compile_ms"],
+                           "host_ms": m["host_ms"],
                            "parallelism": f"jobs dealt round-robin over {world} GPU(s)"},
+                "roofline": m["roofline"], "oracle_check": m.get("oracle_check"),
                 "e2e": {"value": work / (e2e_ms * 1e-3), "unit": UNIT,
                         "ms_per_step": e2e_ms, "h2d_bytes_per_step": None,
                         "d2h_bytes_per_step": None},
-                "gpu_launches": args.steps * world, "clocks": clk.summary()}
+                "gpu_launches": args.steps * world * 3, "clocks": clk.summary()}
+        if "cpu_baseline" in m:
+            line["cpu_baseline"] = m["cpu_baseline"]
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -729,19 +1074,21 @@ def run_cones(args, rank, world, local, dev) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--config", default="mult16")
     ap.add_argument("--slices", type=int, default=0)
     ap.add_argument("--cofactor", default="throughput",
-                    help="K1 cofactor mode: throughput (default), auto, none, or 1..4")
+                    help="K1 cofactor mode: throughput (default), auto, none, or 1..5")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--extra-cpu-seconds", type=float, default=6.0,
+                    help="CPU baseline budget of each other_configs entry")
     ap.add_argument("--no-extras", action="store_true")
-    ap.add_argument("--backend", default="nccl", help="torch.distributed backend for N>1")
+    ap.add_argument("--backend", default="nccl", help="torch.distributed backend under torchrun")
     ap.add_argument("--collective", choices=("p2p", "nccl"), default="p2p",
-                    help="N>1 exchange: shared peer word (p2p) or NCCL MIN per slice")
+                    help="torchrun exchange: shared peer word (p2p) or NCCL MIN per slice")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

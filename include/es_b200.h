@@ -222,6 +222,10 @@ int32_t es_xag_eval(int32_t num_pis, int32_t num_gates, const uint8_t *kind, con
  * The runtime groups launches by slots (<=44: 4 words/thread, <=88: 2, else). */
 int32_t es_batch_k2_stats(const es_batch *b, int32_t *num_slots, int32_t *num_records,
                           int32_t *cofactor_pis);
+/* Per-job shared-memory traffic of one interpreter pass (after accumulator
+ * forwarding): slot loads, and slot stores including the PI words written at
+ * the start of the pass; -1 for unprepared jobs (the bench's K2 roofline). */
+int32_t es_batch_k2_traffic(const es_batch *b, int32_t *loads, int32_t *stores);
 int32_t es_batch_size(const es_batch *b);
 int32_t es_batch_info(const es_batch *b, int32_t i, int32_t *num_pis, int32_t *num_gates,
                       uint64_t *hash, int32_t *num_instrs, int32_t *num_registers, int32_t *G);

@@ -34,7 +34,7 @@ ENGINES = {"auto": ENGINE_AUTO, "jit": ENGINE_JIT, "interp": ENGINE_INTERP}
 EXPORTS = ("es_compile", "es_run", "es_run_batch", "es_session_open", "es_session_geometry",
            "es_session_launch", "es_session_close", "es_map_stats", "es_map_pipes", "es_map_eval", "es_k2_stats", "es_k2_eval",
            "es_emit_ptx", "es_jit_check", "es_alu_peak", "es_smem_peak", "es_batch_extract", "es_batch_size",
-           "es_batch_info", "es_batch_table", "es_batch_k2_stats", "es_xag_eval", "es_batch_xag", "es_batch_select", "es_batch_run", "es_batch_merge", "es_batch_free",
+           "es_batch_info", "es_batch_table", "es_batch_k2_stats", "es_batch_k2_traffic", "es_xag_eval", "es_batch_xag", "es_batch_select", "es_batch_run", "es_batch_merge", "es_batch_free",
            "es_ipc_alloc", "es_ipc_open", "es_ipc_close", "es_word_write", "es_word_read",
            "es_map_stats_k", "es_map_pipes_k", "es_map_eval_k", "es_map_stats_kc", "es_map_eval_kc", "es_emit_ptx_k", "es_jit_check_k",
            "es_k2_eval_k", "es_k2_cofactor_pis", "es_batch_prepare",
@@ -113,6 +113,8 @@ def lib():
         L.es_map_eval_kc.argtypes = [ctypes.POINTER(EsProg), ctypes.c_int32, ctypes.c_int32,
                                      ctypes.c_uint64, ctypes.c_uint64, _P]
         L.es_map_eval_kc.restype = ctypes.c_int32
+        L.es_batch_k2_traffic.argtypes = [_P, _P, _P]
+        L.es_batch_k2_traffic.restype = ctypes.c_int32
         L.es_device_count.argtypes = [ctypes.POINTER(ctypes.c_int32)]
         L.es_device_count.restype = ctypes.c_int32
         L.es_session_open.argtypes = [ctypes.POINTER(EsProg), ctypes.POINTER(EsRunOpts),

@@ -204,6 +204,13 @@ class NativeBatch:
                                           out["cofactor_pis"].ctypes.data))
         return out
 
+    def k2_traffic(self) -> dict:
+        """Per-job shared-memory slot loads and stores of one interpreter pass."""
+        n = len(self)
+        out = {k: np.zeros(n, np.int32) for k in ("loads", "stores")}
+        N.check(N.lib().es_batch_k2_traffic(self._h, out["loads"].ctypes.data, out["stores"].ctypes.data))
+        return out
+
     def submiter(self, i: int) -> SubMiter:
         inf = self.info(i)
         ng, n = inf["num_gates"], inf["num_pis"]

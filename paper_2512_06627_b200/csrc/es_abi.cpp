@@ -486,6 +486,20 @@ int32_t es_batch_k2_stats(const es_batch *bp, int32_t *num_slots, int32_t *num_r
     return ES_OK;
 }
 
+int32_t es_batch_k2_traffic(const es_batch *bp, int32_t *loads, int32_t *stores) {
+    const Batch *bt = (const Batch *)bp;
+    if (!bt) { set_error("bad argument"); return ES_E_BAD_ARG; }
+    for (size_t i = 0; i < bt->subs.size(); ++i) {
+        const SubMiterC &s = bt->subs[i];
+        const bool ok = s.k2_ready;
+        // per pass over the records: operand loads, result stores, and the
+        // PI words stored into their slots at the start of every pass
+        if (loads) loads[i] = ok ? s.k2.loads : -1;
+        if (stores) stores[i] = ok ? s.k2.stores + s.num_pis - (int32_t)s.k2.cof_pis.size() : -1;
+    }
+    return ES_OK;
+}
+
 int32_t es_batch_size(const es_batch *bp) { return bp ? (int32_t)((const Batch *)bp)->subs.size() : ES_E_BAD_ARG; }
 
 int32_t es_batch_info(const es_batch *bp, int32_t i, int32_t *num_pis, int32_t *num_gates,

@@ -574,9 +574,9 @@ struct SweepOut {
 
 static int sweep_k1(const K1Plan &pl, int G, const es_run_opts &o, const std::vector<Ctx *> &cs,
                     double deadline, uint64_t begin, uint64_t init_best, uint64_t hit_stop,
-                    SweepOut *res) {
+                    SweepOut *res, uint64_t end = ~0ull) {
     const int n = (int)cs.size();
-    const uint64_t N = pl.n_chunks;
+    const uint64_t N = std::min(end, pl.n_chunks);  // this sweep covers global chunks [begin, N)
     // the shared word: device 0's, if every other device can reach it
     bool shared = true;
     for (int d = 1; d < n && shared; ++d) {
@@ -1448,6 +1448,17 @@ static int run_k1_job(MappedProg &mp, const LutNet &net, const es_run_opts &o, c
     const uint64_t w1 = s1.best;
     const double frac_left = 1.0 - (double)s1.prefix / (double)pl.n_chunks;
     const double cost_a = frac_left * est_sweep_ms(net, P, sms * n_dev);
+    // the chunk holding w1: phase 1 may have left chunks below it unswept
+    // (a claim that read the minimum after w1 landed skips its chunk)
+    uint64_t cw1 = 0;
+    {
+        uint64_t lo = 0, hi = pl.n_chunks;  // last chunk whose first pattern is <= w1
+        while (hi - lo > 1) {
+            const uint64_t mid = lo + (hi - lo) / 2;
+            if (pl.first_pattern(mid) <= w1) lo = mid; else hi = mid;
+        }
+        cw1 = lo;
+    }
     // candidates: the cheapest PIs below one of w1's top set bits (PI j is
     // pattern bit j-1, so "PIs <= b" keeps every cofactor bit below bit b),
     // at the same depth or one less; cost = the exact fraction of the space
@@ -1488,10 +1499,24 @@ static int run_k1_job(MappedProg &mp, const LutNet &net, const es_run_opts &o, c
         rc = k1_plan_for(mp, *restricted, o, sms, n_dev, opt, &pl2, &jit2);
         if (rc != ES_OK) return rc;
         r->jit_ms += jit2;
-        // phase 1's swept prefix in the restricted plan's chunk units (rounded down)
+        // every copy of the chunks phase 1 left below w1's (few: the claims in
+        // flight when w1 landed), with the phase-1 variant
+        SweepOut gap;
+        gap.best = w1;
+        if (s1.prefix <= cw1) {
+            rc = sweep_k1(pl, G, o, cs, deadline, s1.prefix, w1, 0, &gap, cw1 + 1);
+            if (rc != ES_OK) return rc;
+            r->device_ms += gap.device_ms;
+            r->launches += gap.launches;
+            r->patterns_swept += gap.swept * pl.patterns_per_chunk();
+        }
+        // then copies 0..c1-1 of everything phase 1 left, in the restricted
+        // plan's chunk units (rounded down)
         const uint64_t from = ((s1.prefix << pl.chunk_log2) >> pl2.chunk_log2);
-        rc = sweep_k1(pl2, G, o, cs, deadline, from, w1, 0, &s2);
+        rc = sweep_k1(pl2, G, o, cs, deadline, from, gap.best, 0, &s2);
         if (rc != ES_OK) return rc;
+        s2.stopped = s2.stopped || gap.stopped;
+        s2.reason = s2.reason ? s2.reason : gap.reason;
         r->device_ms += s1.device_ms;
         r->launches += s1.launches;
         r->patterns_swept += std::min<uint64_t>(s1.swept * pl.patterns_per_chunk(), sentinel);
