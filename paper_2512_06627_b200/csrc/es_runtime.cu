@@ -64,6 +64,7 @@ struct K1Params {
 struct K2Job {
     const uint4 *code;           // device records, one uint4 per gate / output
     unsigned long long *best;
+    unsigned *swept;             // items of this job actually evaluated (not skipped)
     unsigned long long total_words;  // kernel words (cofactor PIs excluded)
     unsigned long long cof_mask;     // bit j: PI j is a cofactor PI
     int n_recs;
@@ -144,6 +145,7 @@ __global__ void __launch_bounds__(128) es_k2(const K2Job *__restrict__ jobs,
                 const K2Item it = items[k];
                 const K2Job &jb = jobs[it.job];
                 if (k2_expand(it.w0 << 5, jb) > *(volatile unsigned long long *)jb.best) k = kSkip;
+                else atomicAdd(jb.swept, 1u);
             }
             s_item = k;
         }
@@ -800,11 +802,13 @@ struct K2Group {
     std::vector<K2Job> jobs;
     std::vector<K2Item> items;
     std::vector<unsigned long long> h_best;
+    std::vector<unsigned> h_swept;   // per job: items evaluated
     std::vector<uint64_t> n_items, item_words;
     uint8_t *d_buf = nullptr;
     K2Job *d_jobs = nullptr;
     K2Item *d_items = nullptr;
     unsigned long long *d_best = nullptr;
+    unsigned *d_swept = nullptr;
     uint64_t done_items = 0;
     int launches = 0;
 };
@@ -896,17 +900,20 @@ static int k2_group_prepare(K2Group &gp, const es_prog *progs, const K2Prog *con
     const size_t code_b = std::max<size_t>(gp.n_code, 1) * sizeof(uint4);
     const size_t jobs_b = (size_t)G * sizeof(K2Job);
     const size_t items_b = std::max<size_t>(gp.items.size(), 1) * sizeof(K2Item);
-    const size_t best_b = (size_t)G * 8;
-    CK(cudaMallocAsync(&gp.d_buf, al(code_b) + al(jobs_b) + al(items_b) + al(best_b), st));
+    const size_t best_b = (size_t)G * 8, swept_b = (size_t)G * 4;
+    CK(cudaMallocAsync(&gp.d_buf, al(code_b) + al(jobs_b) + al(items_b) + al(best_b) + al(swept_b), st));
     uint4 *d_code = (uint4 *)gp.d_buf;
     gp.d_jobs = (K2Job *)(gp.d_buf + al(code_b));
     gp.d_items = (K2Item *)(gp.d_buf + al(code_b) + al(jobs_b));
     gp.d_best = (unsigned long long *)(gp.d_buf + al(code_b) + al(jobs_b) + al(items_b));
+    gp.d_swept = (unsigned *)(gp.d_buf + al(code_b) + al(jobs_b) + al(items_b) + al(best_b));
+    gp.h_swept.assign(G, 0u);
     for (int q = 0; q < G; ++q) {
         const int j = group[q];
         K2Job &J = gp.jobs[q];
         J.code = d_code + off[q];
         J.best = gp.d_best + q;
+        J.swept = gp.d_swept + q;
         J.total_words = kwords(q);
         J.n_recs = (int)kps[j]->gates.size();
         J.num_pis = progs[j].num_pis;
@@ -927,6 +934,7 @@ static int k2_group_upload(K2Group &gp, cudaStream_t st) {
     CK(cudaMemcpyAsync(gp.d_jobs, gp.jobs.data(), gp.jobs.size() * sizeof(K2Job), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(gp.d_items, gp.items.data(), gp.items.size() * sizeof(K2Item), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(gp.d_best, gp.h_best.data(), gp.h_best.size() * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(gp.d_swept, 0, gp.h_swept.size() * 4, st));
     return ES_OK;
 }
 
@@ -969,10 +977,12 @@ static void k2_group_results(const K2Group &gp, const es_prog *progs, const K2Pr
         r->regs_per_thread = gp.W;  // K2: words per thread
         const uint64_t covered = done_cnt[q];  // this job's items in completed launches
         const uint64_t item_patterns = (gp.item_words[q] * 32) << kps[j]->cof_pis.size();
+        // items evaluated (skipped ones excluded), the last possibly partial
+        const uint64_t swept = std::min<uint64_t>((uint64_t)gp.h_swept[q] * item_patterns, sentinel);
         if (gp.h_best[q] < sentinel) {
             r->verdict = ES_COUNTEREXAMPLE;
             r->witness_index = gp.h_best[q];
-            r->patterns_swept = std::min<uint64_t>(covered * item_patterns, sentinel);
+            r->patterns_swept = swept;
             // a job's completed items are a prefix of its items (round-robin
             // order); the witness is the minimum unless a stop left an item
             // whose first pattern lies below it (cofactor bits above the item)
@@ -984,11 +994,11 @@ static void k2_group_results(const K2Group &gp, const es_prog *progs, const K2Pr
             r->verdict = ES_BUDGET_EXCEEDED;
             r->reason = stop_reason;
             r->patterns_evaluated = std::min<uint64_t>(covered * item_patterns, sentinel);
-            r->patterns_swept = r->patterns_evaluated;
+            r->patterns_swept = swept;
         } else {
             r->verdict = ES_EXHAUSTED_ZERO;
             r->patterns_evaluated = sentinel;
-            r->patterns_swept = sentinel;
+            r->patterns_swept = swept;
         }
     }
 }
@@ -1135,6 +1145,7 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
     }
     for (K2Group &gp : groups) {
         CK(cudaMemcpyAsync(gp.h_best.data(), gp.d_best, gp.h_best.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(gp.h_swept.data(), gp.d_swept, gp.h_swept.size() * 4, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaFreeAsync(gp.d_buf, c->stream));
     }
     CK(cudaStreamSynchronize(c->stream));
@@ -1450,15 +1461,12 @@ static int run_k1_job(MappedProg &mp, const LutNet &net, const es_run_opts &o, c
     const double cost_a = frac_left * est_sweep_ms(net, P, sms * n_dev);
     // the chunk holding w1: phase 1 may have left chunks below it unswept
     // (a claim that read the minimum after w1 landed skips its chunk)
-    uint64_t cw1 = 0;
-    {
-        uint64_t lo = 0, hi = pl.n_chunks;  // last chunk whose first pattern is <= w1
-        while (hi - lo > 1) {
-            const uint64_t mid = lo + (hi - lo) / 2;
-            if (pl.first_pattern(mid) <= w1) lo = mid; else hi = mid;
-        }
-        cw1 = lo;
+    uint64_t cw1 = w1;  // w1 with its cofactor bits removed, in chunks
+    for (int b = pl.cof_n - 1; b >= 0; --b) {
+        const unsigned s = pl.cof_pos[b];
+        cw1 = ((cw1 >> (s + 1)) << s) | (cw1 & ((1ull << s) - 1ull));
     }
+    cw1 >>= pl.chunk_log2 + 5;
     // candidates: the cheapest PIs below one of w1's top set bits (PI j is
     // pattern bit j-1, so "PIs <= b" keeps every cofactor bit below bit b),
     // at the same depth or one less; cost = the exact fraction of the space
@@ -1593,9 +1601,28 @@ int run_one(const es_prog *prog, const es_run_opts *opts, es_result *out) {
     out->n_devices = 1;
     int engine = o.engine;
     if (engine == ES_ENGINE_AUTO) {
-        // the interpreter beats JIT compile latency on small sweeps
+        // The interpreter needs no JIT, the straight-line kernel sweeps ~40x
+        // faster once compiled.  Estimates (round-1 B200 measurements): K2
+        // ~5e13 gate-patterns/s (mult12: 2.5e10 in 0.45 ms), K1 ~2e15 plus
+        // ~0.02 ms of launch, ptxas ~0.04 ms per gate at -O1 (mult16: 95 ms).
+        // Big sweeps go to K1; small ones to K1 when it is already compiled
+        // or, in throughput mode, when its sweep is faster (JIT ignored);
+        // otherwise by the doubling rule on the program's run count, so a
+        // re-run program tiers up from K2 to K1 (mult12 at ~130 runs).
         const double work = (double)G * std::ldexp(1.0, prog->num_pis);
-        engine = work < 4e12 ? ES_ENGINE_INTERP : ES_ENGINE_JIT;
+        const double k2_ms = 1e3 * work / 5e13, k1_ms = 0.02 + 1e3 * work / 2e15;
+        bool compiled = false;
+        double reuse = 1.0;
+        {
+            std::lock_guard<std::mutex> lk(mp->mu);
+            for (const auto &kv : mp->jks) compiled = compiled || kv.second != nullptr;
+            reuse += mp->runs + mp->k2_runs;
+        }
+        const bool tput = o.cofactor_pis == ES_COFACTOR_THROUGHPUT;
+        const double jit_ms = compiled ? 0.0 : 0.04 * G;
+        if (work >= 4e12) engine = ES_ENGINE_JIT;
+        else if (tput || compiled) engine = k1_ms < k2_ms ? ES_ENGINE_JIT : ES_ENGINE_INTERP;
+        else engine = jit_ms + k1_ms * reuse < k2_ms * reuse ? ES_ENGINE_JIT : ES_ENGINE_INTERP;
     }
     if (engine == ES_ENGINE_INTERP) {
         std::vector<int> act{0};

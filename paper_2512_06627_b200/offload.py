@@ -16,6 +16,7 @@ the B200 engine; SAT and BDD stay the caller's (the reference's
 from __future__ import annotations
 
 import threading
+from concurrent.futures import ThreadPoolExecutor, as_completed
 from dataclasses import dataclass
 from typing import Callable
 
@@ -114,61 +115,71 @@ def plan_allocation(n: int, p: Predictions, cutoff: float, cost_sat: float = 0.0
     return EnginePlan(sat_threads=n - bdd, bdd_threads=bdd)
 
 
+def race(jobs: dict[str, Callable[[Callable[[], bool]], CheckResult]]) -> CheckResult:
+    """Run every engine job at once; the first decisive verdict (EQUIVALENT /
+    COUNTEREXAMPLE) wins and raises the shared cancel predicate the others
+    poll (the B200 ES engine mirrors it into its native cancel flag, checked
+    between launch slices).  The call returns once every engine has stopped,
+    so no engine outlives its race.  Without a decisive verdict the result is
+    UNKNOWN, reason "timeout" if any engine timed out, with each engine's
+    statistics -- the reference race's outcome contract (sched.py:210-266).
+    A job that raises counts as UNKNOWN("error: ...")."""
+    stop = threading.Event()
+    first = threading.Lock()
+    winner: list[CheckResult] = []
+
+    def guarded(name, job):
+        try:
+            r = job(stop.is_set)
+        except Exception as exc:  # an engine bug must not hang the race
+            r = CheckResult(UNKNOWN, reason=f"error: {exc}", engine=name)
+        if r.verdict != UNKNOWN:
+            with first:  # the first decisive verdict to land wins ...
+                if not winner:
+                    winner.append(r)
+            stop.set()  # ... and cancels the others right away
+        return r
+
+    undecided: dict[str, CheckResult] = {}
+    with ThreadPoolExecutor(max_workers=len(jobs), thread_name_prefix="race") as pool:
+        futs = {pool.submit(guarded, name, job): name for name, job in jobs.items()}
+        for fut in as_completed(futs):  # every engine has stopped when the pool closes
+            r = fut.result()
+            if r.verdict == UNKNOWN:
+                undecided[r.engine or futs[fut]] = r
+    if winner:
+        return winner[0]
+    reasons = {r.reason for r in undecided.values()}
+    reason = "timeout" if "timeout" in reasons else (min(reasons) if reasons else "")
+    return CheckResult(UNKNOWN, reason=reason,
+                       stats={"engines": {k: dict(r.stats, reason=r.reason) for k, r in undecided.items()}})
+
+
 def dispatch(sm, plan: EnginePlan, sat: Callable | None = None, bdd: Callable | None = None,
              es_cpu: Callable | None = None, budget: float | None = None, seed: int = 0,
              device: int = 0) -> CheckResult:
-    """Race the planned engines; the first settled verdict cancels the rest
-    (sched.py:210-266).  ES runs on the B200 (es.es_check) when the plan says
-    es_on_device -- or whenever no CPU ES callable is given; the other
-    engines are the caller's callables with the reference's signatures
+    """The planned engines raced on ``sm`` (the reference's dispatch contract,
+    sched.py:210-266).  ES runs on the B200 (es.es_check) when the plan says
+    es_on_device -- or whenever no CPU ES callable is given; SAT and BDD are
+    the caller's callables with the reference's signatures
     (sat(sm, threads=, budget=, cancel=, seed=), bdd(sm, budget=, cancel=),
     es_cpu(sm, workers=, budget=, cancel=))."""
     from . import es as gpu_es
 
-    stop = threading.Event()
-    lock = threading.Lock()
-    settled: list[CheckResult] = []
-    leftovers: dict[str, CheckResult] = {}
-
-    def publish(r: CheckResult) -> None:
-        with lock:
-            if r.verdict != UNKNOWN:
-                if not settled:
-                    settled.append(r)
-                    stop.set()
-            else:
-                leftovers[r.engine or "?"] = r
-
-    jobs = []
+    jobs: dict[str, Callable[[Callable[[], bool]], CheckResult]] = {}
     if plan.sat_threads > 0:
         if sat is None:
             raise ValueError("plan enables SAT but no sat callable was given")
-        jobs.append(lambda: sat(sm, threads=plan.sat_threads, budget=budget, cancel=stop.is_set, seed=seed))
+        jobs["sat"] = lambda cancel: sat(sm, threads=plan.sat_threads, budget=budget, cancel=cancel,
+                                         seed=seed)
     if plan.es_on_device or (plan.es_threads > 0 and es_cpu is None):
-        jobs.append(lambda: gpu_es.es_check(sm, budget=budget, cancel=stop.is_set, device=device))
+        jobs["es"] = lambda cancel: gpu_es.es_check(sm, budget=budget, cancel=cancel, device=device)
     elif plan.es_threads > 0:
-        jobs.append(lambda: es_cpu(sm, workers=plan.es_threads, budget=budget, cancel=stop.is_set))
+        jobs["es"] = lambda cancel: es_cpu(sm, workers=plan.es_threads, budget=budget, cancel=cancel)
     if plan.bdd_threads > 0:
         if bdd is None:
             raise ValueError("plan enables BDD but no bdd callable was given")
-        jobs.append(lambda: bdd(sm, budget=budget, cancel=stop.is_set))
+        jobs["bdd"] = lambda cancel: bdd(sm, budget=budget, cancel=cancel)
     if not jobs:
         raise ValueError("plan enables no engine")
-
-    def run(job) -> None:
-        try:
-            publish(job())
-        except Exception as exc:  # an engine bug must not hang the race
-            publish(CheckResult(UNKNOWN, reason=f"error: {exc}", engine="?"))
-
-    threads = [threading.Thread(target=run, args=(j,)) for j in jobs]
-    for t in threads:
-        t.start()
-    for t in threads:
-        t.join()
-    if settled:
-        return settled[0]
-    reasons = {r.reason for r in leftovers.values()}
-    reason = "timeout" if "timeout" in reasons else (sorted(reasons)[0] if reasons else "")
-    stats = {"engines": {k: dict(r.stats, reason=r.reason) for k, r in leftovers.items()}}
-    return CheckResult(UNKNOWN, reason=reason, stats=stats)
+    return race(jobs)
