@@ -423,9 +423,16 @@ def measure_cones(steps: int, warmup: int, rank: int = 0, world: int = 1, count:
                             "program) / device time",
             "wavefronts": model["wavefronts"], "record_passes": model["record_passes"]}
     roof["frac"] = roof["achieved"] / roof["peak"]
+    lt = cones.LAST_TIMING
     out = {"jobs": len(batch), "eq": eq, "neq": neq, "gate_patterns": work, "roofline": roof,
            "device_ms": statistics.mean(dev_ms), "e2e_ms": statistics.mean(wall_ms),
-           "host_ms": {"pair_sampling_extract_compile": sample_ms, "k2_program_build": prepare_ms},
+           "host_ms": {"pair_sampling": 1e3 * lt.get("pair_sampling_s", 0.0),
+                       "extract_compile": 1e3 * lt.get("extract_compile_s", 0.0),
+                       "pairs_extracted": lt.get("pairs_extracted"),
+                       "k2_program_build": prepare_ms, "batch_total": sample_ms + prepare_ms},
+           "e2e_with_build_ms": statistics.mean(wall_ms) + prepare_ms
+                                + 1e3 * lt.get("extract_compile_s", 0.0) * len(batch)
+                                / max(1, lt.get("pairs_extracted") or 1),
            "value": work / dev_s, "e2e_value": work / (statistics.mean(wall_ms) * 1e-3)}
     if check:
         out["oracle_check"] = cones_oracle_check(batch, res)

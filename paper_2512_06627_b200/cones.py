@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import ctypes
 import random
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -338,10 +339,20 @@ def config4_batches(count: int = 10_000, lo: int = 14, hi: int = 24, seed: int =
     out: list[NativeBatch] = []
     seen: set[int] = set()
     total = 0
-    for m, pairs in config4_pairs(lo, hi, seed):
-        if total >= count:
+    t_pairs = t_extract = 0.0
+    extracted = 0
+    gen = config4_pairs(lo, hi, seed)
+    while total < count:
+        t = time.perf_counter()
+        try:
+            m, pairs = next(gen)
+        except StopIteration:
             break
-        nb = NativeBatch(m, pairs, threads=threads)
+        t_pairs += time.perf_counter() - t
+        t = time.perf_counter()
+        nb = NativeBatch(m, pairs, threads=threads)  # C++ extract_submiter + compile_program
+        t_extract += time.perf_counter() - t
+        extracted += len(pairs)
         tab = nb.table()
         keep = []
         for i in range(len(nb)):
@@ -355,7 +366,16 @@ def config4_batches(count: int = 10_000, lo: int = 14, hi: int = 24, seed: int =
         nb.select(keep)
         total += len(keep)
         out.append(nb)
+    LAST_TIMING.clear()
+    LAST_TIMING.update(pair_sampling_s=t_pairs, extract_compile_s=t_extract, pairs_extracted=extracted,
+                       jobs=total)
     return out
+
+
+# host time of the last config4_batches call: pair sampling (random simulation
+# and candidate classes, the sweep's job; numpy here), and C++ extraction +
+# reference-schedule compilation of every candidate pair (kept or not)
+LAST_TIMING: dict = {}
 
 
 def config4_batch(count: int = 10_000, lo: int = 14, hi: int = 24, seed: int = 0,

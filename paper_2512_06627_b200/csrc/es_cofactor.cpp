@@ -25,21 +25,60 @@ namespace es {
 namespace {
 
 // Literal = node*2 + complement; 0 = FALSE, 1 = TRUE.
+// Open-addressing (linear probing) structural-hash table: the expansion runs
+// for every candidate depth of every config-4 cone (K2's cofactor search), so
+// it is a host hot spot (std::unordered_map measured ~5x slower).
 struct Strash {
     Dag *d;
-    std::unordered_map<uint64_t, int32_t> table;
+    std::vector<uint64_t> keys;  // 0 = empty (a real key always has b >= 2)
+    std::vector<int32_t> vals;
+    size_t used = 0, mask = 0;
     explicit Strash(Dag *dag) : d(dag) {}
+    void reserve(size_t n) {
+        size_t cap = 64;
+        while (cap < 2 * n) cap <<= 1;
+        keys.assign(cap, 0);
+        vals.assign(cap, 0);
+        mask = cap - 1;
+        used = 0;
+    }
+    static size_t hash(uint64_t k) {
+        k ^= k >> 33; k *= 0xff51afd7ed558ccdull; k ^= k >> 33;
+        return (size_t)k;
+    }
+    void grow() {
+        std::vector<uint64_t> ok;
+        std::vector<int32_t> ov;
+        ok.swap(keys);
+        ov.swap(vals);
+        keys.assign(ok.size() * 2, 0);
+        vals.assign(ok.size() * 2, 0);
+        mask = keys.size() - 1;
+        for (size_t i = 0; i < ok.size(); ++i) {
+            if (!ok[i]) continue;
+            size_t h = hash(ok[i]) & mask;
+            while (keys[h]) h = (h + 1) & mask;
+            keys[h] = ok[i];
+            vals[h] = ov[i];
+        }
+    }
     int32_t node(bool x, uint32_t a, uint32_t b) {
         const uint64_t key = ((uint64_t)x << 63) | ((uint64_t)a << 32) | b;
-        auto it = table.find(key);
-        if (it != table.end()) return it->second;
+        if (keys.empty()) reserve(1024);
+        size_t h = hash(key) & mask;
+        while (keys[h]) {
+            if (keys[h] == key) return vals[h];
+            h = (h + 1) & mask;
+        }
         const int32_t v = d->num_nodes();
         d->is_xor.push_back(x);
         d->f0.push_back((int32_t)(a >> 1));
         d->n0.push_back(a & 1);
         d->f1.push_back((int32_t)(b >> 1));
         d->n1.push_back(b & 1);
-        table.emplace(key, v);
+        keys[h] = key;
+        vals[h] = v;
+        if (++used * 2 > keys.size()) grow();
         return v;
     }
     uint32_t mk_and(uint32_t a, uint32_t b) {
@@ -121,7 +160,7 @@ void cofactor_expand(const Dag &dag, const std::vector<int32_t> &pis, Dag *out,
     *out = Dag();
     out->num_pis = P;
     Strash sh(out);
-    sh.table.reserve((size_t)N * 4);
+    sh.reserve((size_t)N * 2);
     const int k = (int)pis.size();
     // gates in the transitive fanout of the cofactor PIs: the only ones that
     // differ between copies; the rest keep copy 0's literal

@@ -192,16 +192,34 @@ void build_k2prog(const Dag &dag, K2Prog *kp) {
     {
         std::vector<int> dpos(N, 0), pend(N, 0), rem = refs;
         for (size_t i = 0; i < order.size(); ++i) dpos[order[i]] = (int)i;
-        std::vector<std::vector<int>> users(N);
+        // readers of each gate, CSR (ustart[l]..ustart[l+1]); a gate reading
+        // the same fanin twice is one reader
+        std::vector<int> ustart(N + 1, 0), uidx;
         for (int v : order) {
             const int g = v - FG;
-            for (int l : {dag.f0[g], dag.f1[g]}) {
-                if (!is_gate(l)) continue;
-                if (dag.f0[g] == dag.f1[g] && l == dag.f1[g] && pend[v]) continue;
-                pend[v]++;
-                users[l].push_back(v);
+            if (is_gate(dag.f0[g])) ustart[dag.f0[g] + 1]++;
+            if (dag.f1[g] != dag.f0[g] && is_gate(dag.f1[g])) ustart[dag.f1[g] + 1]++;
+        }
+        for (int v = 0; v < N; ++v) ustart[v + 1] += ustart[v];
+        uidx.resize(ustart[N]);
+        {
+            std::vector<int> fill(ustart.begin(), ustart.end() - 1);
+            for (int v : order) {
+                const int g = v - FG;
+                for (int l : {dag.f0[g], dag.f1[g]}) {
+                    if (!is_gate(l)) continue;
+                    if (dag.f0[g] == dag.f1[g] && l == dag.f1[g] && pend[v]) continue;
+                    pend[v]++;
+                    uidx[fill[l]++] = v;
+                }
             }
         }
+        struct Users {
+            const int *b, *e;
+            const int *begin() const { return b; }
+            const int *end() const { return e; }
+        };
+        auto users = [&](int l) { return Users{uidx.data() + ustart[l], uidx.data() + ustart[l + 1]}; };
         // lazy min-heap of (score, DFS position, gate); scores only improve
         // as fanins lose readers, so stale entries are skipped on pop
         auto score = [&](int v) {
@@ -227,10 +245,10 @@ void build_k2prog(const Dag &dag, K2Prog *kp) {
                 if (!is_gate(l)) continue;
                 rem[l]--;
                 if (rem[l] <= 2)  // a remaining ready reader may now free l
-                    for (int u : users[l])
+                    for (int u : users(l))
                         if (in_ready[u] && !done[u]) heap.emplace(score(u), dpos[u], u);
             }
-            for (int u : users[v])
+            for (int u : users(v))
                 if (--pend[u] == 0) { in_ready[u] = 1; heap.emplace(score(u), dpos[u], u); }
         }
     }
