@@ -363,11 +363,14 @@ def cones_oracle_check(batch, rec) -> dict:
 
 
 def k2_smem_model(batch, res) -> dict:
-    """Shared-memory wavefronts the K2 interpreter issues (the unit ncu's
-    l1tex__data_pipe_lsu_wavefronts_mem_shared counts): per warp-iteration
-    (32 threads x W words) one broadcast record load plus W wavefronts per
-    slot load or store (W words x 4 B x 32 threads = W x 128 B), with the
-    accumulator forwarding's actual per-program load/store counts."""
+    """Shared-memory wavefronts the K2 interpreter issues (ncu's
+    l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld + _op_st): per warp and
+    pass over a job's records, each 16-byte broadcast record load (records +
+    the one-past-end prefetch) costs 2 wavefronts, each slot load or store W
+    (W words x 4 B x 32 threads = W x 128 B), with the accumulator
+    forwarding's actual per-program load/store counts and the PI words
+    stored at the start of a pass.  Calibrated against ncu per launch group
+    (profiles/r02_k2_cones_W*_ncu_full.json: loads and stores within 0.5 %)."""
     import numpy as np
 
     st = batch.k2_stats()
@@ -379,10 +382,17 @@ def k2_smem_model(batch, res) -> dict:
     copies = np.exp2(st["cofactor_pis"].astype(np.float64))
     iters = words / copies  # interpreter passes over the record list, per thread-word
     warp_iters = iters / (32.0 * W)
-    per = st["num_records"] + (tr["loads"] + tr["stores"]) * W
+    per = 2.0 * (st["num_records"] + 1) + (tr["loads"] + tr["stores"]) * W
     wavefronts = float((warp_iters * per)[ran].sum())
+    groups = {}
+    for w in (1, 2, 4):
+        m = ran & (W == w)
+        groups[f"W{w}"] = {"jobs": int(m.sum()),
+                           "ld_wavefronts": float((warp_iters * (2.0 * (st["num_records"] + 1)
+                                                                 + tr["loads"] * W))[m].sum()),
+                           "st_wavefronts": float((warp_iters * tr["stores"] * W)[m].sum())}
     return {"wavefronts": wavefronts, "bytes": wavefronts * 128.0,
-            "record_passes": float((iters * st["num_records"])[ran].sum())}
+            "record_passes": float((iters * st["num_records"])[ran].sum()), "groups": groups}
 
 
 def measure_cones(steps: int, warmup: int, rank: int = 0, world: int = 1, count: int = 10_000,
@@ -421,7 +431,9 @@ def measure_cones(steps: int, warmup: int, rank: int = 0, world: int = 1, count:
             "achieved_def": "shared-memory wavefronts x 128 B the interpreter issues (record "
                             "broadcasts + slot loads/stores after accumulator forwarding, per "
                             "program) / device time",
-            "wavefronts": model["wavefronts"], "record_passes": model["record_passes"]}
+            "wavefronts": model["wavefronts"], "record_passes": model["record_passes"],
+            "groups": model["groups"],
+            "ncu_check": "profiles/r02_k2_cones_W*_ncu_full.json: ld/st wavefronts per group"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     lt = cones.LAST_TIMING
     out = {"jobs": len(batch), "eq": eq, "neq": neq, "gate_patterns": work, "roofline": roof,
