@@ -93,6 +93,9 @@ typedef struct es_run_opts {
     int32_t n_devices;      /* > 0: sweep on devices[0..n_devices) (one host thread each; an
                              * ordinal may repeat); 0: on `device` only */
     const int32_t *devices;
+    int32_t jit_parts;      /* K1 build: 0 = policy (cold runs split the body so ptxas compiles
+                             * its phases on parallel host threads), 1 = one straight-line body,
+                             * >= 2 = split into that many phases */
 } es_run_opts;
 
 /*
@@ -136,6 +139,7 @@ typedef struct es_result {
     int32_t phase2_cofactor_pis;/* cofactor PIs of the second phase's variant (phases == 2) */
     int32_t phase2_copies;      /* > 0: the second phase ran the first phase's cofactor set
                                  * restricted to copies 0..phase2_copies-1 */
+    int32_t jit_parts;          /* K1: phases of the kernel's split build (1: one body) */
 } es_result;
 
 /*
@@ -361,6 +365,13 @@ int32_t es_map_eval_kc(const es_prog *prog, int32_t k, int32_t copies, uint64_t 
                        uint32_t *out_words);
 int64_t es_jit_check_k(const es_prog *prog, int32_t k, int32_t block_threads, int32_t *regs_per_thread,
                        int32_t *spill_bytes, char *log, int64_t log_cap);
+/* Split build without a GPU: the k-cofactor body cut into `parts` phases,
+ * compiled on parallel host threads and linked (es_split.cpp).  Returns the
+ * linked cubin's bytes or < 0; smem_bytes = the slot file per CTA, slots =
+ * shared-memory slots per thread, loads = slot loads per iteration. */
+int64_t es_jit_check_split(const es_prog *prog, int32_t k, int32_t parts, int32_t block_threads,
+                           int32_t *regs_per_thread, int32_t *smem_bytes, int32_t *slots, int32_t *loads,
+                           double *ms);
 /* The PTX the JIT path would compile for `prog` (buf NULL -> returns size).
  * block_threads: 128/256/512. */
 int64_t es_emit_ptx(const es_prog *prog, int32_t block_threads, char *buf, int64_t cap);

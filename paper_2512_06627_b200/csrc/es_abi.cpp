@@ -318,6 +318,52 @@ int64_t es_jit_check_k(const es_prog *prog, int32_t k, int32_t block_threads, in
     return (int64_t)cubin.size();
 }
 
+int64_t es_jit_check_split(const es_prog *prog, int32_t k, int32_t parts, int32_t block_threads,
+                           int32_t *regs_per_thread, int32_t *smem_bytes, int32_t *slots, int32_t *loads,
+                           double *ms) {
+    LutNet net;
+    int rc = map_prog(prog, &net, k);
+    if (rc != ES_OK) return rc;
+    const int threads = block_threads != 0 ? block_threads : 128;
+    const double t0 = now_ms();
+    std::string skel, err, info;
+    std::vector<std::string> phases;
+    int smem = 0;
+    if (!splice_split(net, threads, parts, &skel, &phases, &err, &smem)) {
+        set_error(err);
+        return ES_E_BAD_ARG;
+    }
+    if (const char *dir = getenv("ES_DUMP_SPLIT")) {  // the modules, for ptxas / cuobjdump by hand
+        for (size_t m = 0; m <= phases.size(); ++m) {
+            const std::string path = std::string(dir) + "/mod" + std::to_string(m) + ".ptx";
+            if (FILE *f = fopen(path.c_str(), "w")) {
+                const std::string &txt = m == 0 ? skel : phases[m - 1];
+                fwrite(txt.data(), 1, txt.size(), f);
+                fclose(f);
+            }
+        }
+    }
+    std::vector<char> cubin;
+    rc = split_to_cubin(skel, phases, &cubin, &info, &err, 1);
+    if (rc != ES_OK) { set_error(err); return rc; }
+    if (ms) *ms = now_ms() - t0;
+    if (const char *dump = getenv("ES_DUMP_CUBIN")) {
+        if (FILE *f = fopen(dump, "wb")) { fwrite(cubin.data(), 1, cubin.size(), f); fclose(f); }
+    }
+    int regs = -1, spill = 0;
+    parse_ptxas_info(info, &regs, &spill);
+    if (regs_per_thread) *regs_per_thread = regs;
+    if (smem_bytes) *smem_bytes = smem;
+    if (slots) *slots = smem / (threads * 4);
+    if (loads) {  // slot loads per iteration: count them in the phase text
+        int nl = 0;
+        for (const std::string &ph : phases)
+            for (size_t p = ph.find("ld.shared.b32"); p != std::string::npos; p = ph.find("ld.shared.b32", p + 1)) ++nl;
+        *loads = nl;
+    }
+    return (int64_t)cubin.size();
+}
+
 int32_t es_sim(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
                const uint32_t *in1, const uint64_t *pi_words, int64_t words, int32_t device,
                uint64_t *node_words, double *device_ms) {

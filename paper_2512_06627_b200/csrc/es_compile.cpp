@@ -618,12 +618,6 @@ void eval_lutnet(const LutNet &net, uint64_t w0, uint64_t nw, uint32_t *out) {
 // one IMAD -- on the FMA pipe, idle in this kernel -- with S and T per-word
 // values derived from u's bit (shared by every LUT with the same (u, S/T)
 // pattern).  The ALU pipe, the kernel's bound, loses those LOP3s.
-namespace {
-struct ImadPlan {
-    int x = -1, u = -1;  // node ids
-    int s0, s1, t0, t1;  // x*S+T coefficients for u = 0 / u = 1
-};
-
 // `sel[v]`: v is word-uniform (0 or ~0 across the word) and not a constant --
 // a PI >= 6 or a LUT over such nodes -- so it can act as the IMAD selector.
 bool plan_imad(const Lut &L, const std::vector<uint8_t> &sel, ImadPlan *pl) {
@@ -653,7 +647,6 @@ bool plan_imad(const Lut &L, const std::vector<uint8_t> &sel, ImadPlan *pl) {
     pl->u = L.leaf[ku];
     return true;
 }
-}  // namespace
 
 std::string emit_body_ptx(const LutNet &net, const std::vector<std::string> &outs,
                           const std::string &wlo, const std::string &whi,

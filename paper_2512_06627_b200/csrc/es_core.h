@@ -151,6 +151,33 @@ std::string emit_body_ptx(const LutNet &net, const std::vector<std::string> &out
                           const std::string &wlo, const std::string &whi,
                           const std::string &one = "");
 
+// A LUT that is a 2-input function of a word-uniform selector u and one
+// other value x, as x*S + T (one FMA-pipe IMAD; es_compile.cpp).
+struct ImadPlan {
+    int x = -1, u = -1;  // node ids
+    int s0, s1, t0, t1;  // x*S+T coefficients for u = 0 / u = 1
+};
+// sel[v]: v is word-uniform (a PI >= 6 or a LUT over such nodes).
+bool plan_imad(const Lut &L, const std::vector<uint8_t> &sel, ImadPlan *pl);
+
+// Split build of the K1 body (es_split.cpp): the LUT sequence cut into
+// `parts` phases, each one a separately compiled PTX module holding one
+// device function, so ptxas runs on the phases in parallel and the linker
+// joins them.  Values live across a cut pass through per-thread shared-memory
+// slots (slot s of thread t at es_slots + (s*threads + t)*4).
+struct SplitPtx {
+    std::vector<std::string> phases;  // complete PTX modules, one .func each
+    std::string decls;                // module-scope .extern declarations for the caller
+    std::string call_body;            // replaces the K1 skeleton's ES_BODY line
+    int slots = 0;                    // shared-memory slots per thread
+    int crossings = 0;                // values stored to a slot (one store each)
+    int loads = 0;                    // slot loads over all phases (per iteration)
+    std::vector<int> cuts;            // first LUT of each phase
+};
+bool emit_split_ptx(const LutNet &net, int threads, int parts, const std::string &header,
+                    const std::vector<std::string> &outs, const std::string &wlo,
+                    const std::string &whi, const std::string &one, SplitPtx *out);
+
 uint32_t lane_valid_mask(int num_pis);
 
 }  // namespace es

@@ -9,6 +9,7 @@
 
 #include <sys/stat.h>
 #include <unistd.h>
+#include <atomic>
 #include <mutex>
 #include <sstream>
 #include <string>
@@ -16,7 +17,9 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <nvJitLink.h>
 #include <nvPTXCompiler.h>
+#include <thread>
 
 #include "es_jit.h"
 #include "es_nvtx.h"
@@ -74,6 +77,41 @@ bool splice_body(const LutNet &net, int threads, std::string *ptx, std::string *
     return true;
 }
 
+// Split build (es_split.cpp): the skeleton with its body replaced by calls
+// to `parts` phase functions, and the phase modules.  smem_bytes: the
+// dynamic shared memory of the slot file.
+bool splice_split(const LutNet &net, int threads, int parts, std::string *skel,
+                  std::vector<std::string> *phases, std::string *err, int *smem_bytes) {
+    const int copies = net.cof_pis.empty() ? (int)net.outs.size() : std::max(2, (int)net.outs.size());
+    const char *sk = skeleton_for(threads, copies);
+    if (!sk) { *err = "unsupported K1 variant"; return false; }
+    std::string s(sk);
+    const std::string marker = "// ES_BODY ";
+    const size_t at = s.find(marker);
+    const size_t hdr_end = s.find(".address_size 64");
+    if (at == std::string::npos || hdr_end == std::string::npos) { *err = "bad K1 skeleton"; return false; }
+    const size_t hdr_eol = s.find('\n', hdr_end);
+    size_t eol = s.find('\n', at);
+    std::istringstream in(s.substr(at + marker.size(), eol - at - marker.size()));
+    std::vector<std::string> a;
+    for (std::string t; in >> t;) a.push_back(t);
+    const int nout = copies > 1 ? 2 : 1;
+    if ((int)a.size() != nout + 3) { *err = "cannot parse ES_BODY operands"; return false; }
+    SplitPtx sp;
+    const std::string header = s.substr(0, hdr_eol + 1);
+    if (!emit_split_ptx(net, threads, parts, header, std::vector<std::string>(a.begin(), a.begin() + nout),
+                        a[nout], a[nout + 1], a[nout + 2], &sp)) {
+        *err = "program too small to split into " + std::to_string(parts) + " phases";
+        return false;
+    }
+    s.replace(at, eol - at, sp.call_body);
+    s.insert(hdr_eol + 1, sp.decls);
+    *skel = std::move(s);
+    *phases = std::move(sp.phases);
+    *smem_bytes = sp.slots * threads * 4;
+    return true;
+}
+
 static uint64_t fnv1a(const std::string &s) {
     uint64_t h = 1469598103934665603ull;
     for (unsigned char c : s) { h ^= c; h *= 1099511628211ull; }
@@ -86,7 +124,7 @@ static int effective_opt(int opt) {
 }
 
 int ptx_to_cubin(const std::string &ptx, std::vector<char> *cubin, std::string *info,
-                 std::string *err, int opt) {
+                 std::string *err, int opt, bool relocatable) {
     nvPTXCompilerHandle h = nullptr;
     if (nvPTXCompilerCreate(&h, ptx.size(), ptx.c_str()) != NVPTXCOMPILE_SUCCESS) {
         *err = "nvPTXCompilerCreate failed";
@@ -95,6 +133,7 @@ int ptx_to_cubin(const std::string &ptx, std::vector<char> *cubin, std::string *
     std::vector<const char *> opts = {"--gpu-name=sm_100a", "--verbose"};
     std::string olev = "-O" + std::to_string(effective_opt(opt));
     opts.push_back(olev.c_str());
+    if (relocatable) opts.push_back("-c");
     // experiments: extra ptxas options, space-separated (use with ES_JIT_CACHE=0)
     std::vector<std::string> extra;
     if (const char *e = getenv("ES_PTXAS_EXTRA")) {
@@ -235,13 +274,97 @@ void disk_store(const std::string &dir, uint64_t key, const std::string &ptx, co
 }
 }  // namespace
 
+// Split build: the skeleton and the phase modules compiled relocatable on
+// parallel host threads (largest first), then linked by nvJitLink.  `info`
+// gets a ptxas-style line with the largest register count and the summed
+// spill bytes of the modules.
+int split_to_cubin(const std::string &skel, const std::vector<std::string> &phases, std::vector<char> *cubin,
+                   std::string *info, std::string *err, int opt) {
+    const int M = 1 + (int)phases.size();
+    std::vector<std::vector<char>> objs(M);
+    std::vector<std::string> infos(M), errs(M);
+    std::vector<int> rcs(M, ES_OK);
+    std::atomic<int> next{0};
+    auto work = [&]() {
+        for (;;) {
+            const int i = next.fetch_add(1);
+            if (i >= M) return;
+            const int m = (i + 1) % M;  // phases first, the small skeleton last
+            const double t0 = now_ms();
+            rcs[m] = ptx_to_cubin(m == 0 ? skel : phases[m - 1], &objs[m], &infos[m], &errs[m], opt, true);
+            if (getenv("ES_VERBOSE"))
+                fprintf(stderr, "[es] split module %d: %.1f ms (%.1f .. %.1f)\n", m, now_ms() - t0, t0, now_ms());
+        }
+    };
+    const int nt = std::min<int>(M, std::max(1u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    for (int q = 1; q < nt; ++q) th.emplace_back(work);
+    work();
+    for (auto &x : th) x.join();
+    int regs = 0, spill = 0;
+    for (int m = 0; m < M; ++m) {
+        if (rcs[m] != ES_OK) { *err = "split module " + std::to_string(m) + ": " + errs[m]; return rcs[m]; }
+        int r = 0, sb = 0;
+        parse_ptxas_info(infos[m], &r, &sb);
+        regs = std::max(regs, r);
+        spill += sb;
+    }
+    const double tl = now_ms();
+    nvJitLinkHandle h = nullptr;
+    const char *lopts[] = {"-arch=sm_100a"};
+    if (nvJitLinkCreate(&h, 1, lopts) != NVJITLINK_SUCCESS) { *err = "nvJitLinkCreate failed"; return ES_E_CUDA; }
+    nvJitLinkResult lr = NVJITLINK_SUCCESS;
+    for (int m = 0; m < M && lr == NVJITLINK_SUCCESS; ++m) {
+        const std::string nm = "es_mod" + std::to_string(m);
+        lr = nvJitLinkAddData(h, NVJITLINK_INPUT_CUBIN, objs[m].data(), objs[m].size(), nm.c_str());
+    }
+    if (lr == NVJITLINK_SUCCESS) lr = nvJitLinkComplete(h);
+    if (lr != NVJITLINK_SUCCESS) {
+        size_t n = 0;
+        nvJitLinkGetErrorLogSize(h, &n);
+        std::string log(n, '\0');
+        if (n) nvJitLinkGetErrorLog(h, &log[0]);
+        *err = "nvJitLink failed (" + std::to_string((int)lr) + "): " + log;
+        nvJitLinkDestroy(&h);
+        return ES_E_CUDA;
+    }
+    size_t n = 0;
+    nvJitLinkGetLinkedCubinSize(h, &n);
+    cubin->resize(n);
+    nvJitLinkGetLinkedCubin(h, cubin->data());
+    nvJitLinkDestroy(&h);
+    if (getenv("ES_VERBOSE")) fprintf(stderr, "[es] split link: %.1f ms\n", now_ms() - tl);
+    *info = "ptxas info    : Used " + std::to_string(regs) + " registers, split build of " +
+            std::to_string(phases.size()) + " phases, " + std::to_string(spill) + " bytes spill stores, 0 bytes spill loads\n";
+    return ES_OK;
+}
+
 int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std::string *err,
-            int opt) {
+            int opt, int parts) {
     std::string ptx;
+    std::string skel;
+    std::vector<std::string> phases;
     int region = 0;
-    if (!splice_body(net, threads, &ptx, err, &region)) return ES_E_BAD_PROGRAM;
-    opt = effective_opt(opt);
-    const uint64_t key = fnv1a(ptx) ^ (uint64_t)(uint32_t)threads ^ ((uint64_t)(opt & 7) << 56);
+    if (opt < 0) parts = -opt;  // build level -P: split into P phases at ptxas -O1
+    // a program too small to cut, or whose slot file would not fit shared
+    // memory, gets the one-body build at -O1 instead
+    if (parts > 1 && (!splice_split(net, threads, parts, &skel, &phases, err, &region) || region > 200 * 1024)) {
+        parts = 1;
+        opt = 1;
+        region = 0;
+        err->clear();
+    }
+    if (parts > 1) {
+        ptx = skel;  // the cache key covers every module
+        for (const std::string &ph : phases) { ptx += "\n// ES_PHASE\n"; ptx += ph; }
+    } else {
+        parts = 1;
+        if (!splice_body(net, threads, &ptx, err, &region)) return ES_E_BAD_PROGRAM;
+    }
+    const int level = parts > 1 ? -parts : effective_opt(opt);  // what the kernel is cached as
+    opt = parts > 1 ? effective_opt(1) : level;                  // the ptxas level
+    const uint64_t key = fnv1a(ptx) ^ (uint64_t)(uint32_t)threads ^ ((uint64_t)(opt & 7) << 56) ^
+                         ((uint64_t)parts << 48);
     // the 64-bit key alone could collide: a hit must also match a second,
     // independent hash and the length of the PTX
     const uint64_t h2 = second_hash(ptx);
@@ -260,7 +383,8 @@ int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std
     const uint64_t dkey = key ^ fnv1a(version) * 31u;
     const std::string dir = disk_cache_dir();
     if (!disk_load(dir, dkey, ptx, &cubin, &info)) {
-        int rc = ptx_to_cubin(ptx, &cubin, &info, err, opt);
+        int rc = parts > 1 ? split_to_cubin(skel, phases, &cubin, &info, err, opt)
+                           : ptx_to_cubin(ptx, &cubin, &info, err, opt);
         if (rc != ES_OK) return rc;
         disk_store(dir, dkey, ptx, cubin, info);
     }
@@ -268,7 +392,8 @@ int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std
     k->threads = threads;
     k->block = threads;
     k->region_bytes = region;
-    k->opt = opt;
+    k->opt = level;
+    k->parts = parts;
     k->ptx_h2 = h2;
     k->ptx_len = ptx.size();
     parse_ptxas_info(info, &k->regs, &k->spill_bytes);
@@ -286,6 +411,10 @@ int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std
         cudaLibraryUnload(k->lib);
         delete k;
         return ES_E_CUDA;
+    }
+    if (parts > 1) {  // the linked kernel's register count (the phases' ABI calls included)
+        cudaFuncAttributes fa{};
+        if (cudaFuncGetAttributes(&fa, (const void *)k->kernel) == cudaSuccess) k->regs = fa.numRegs;
     }
     *jit_ms = now_ms() - t0;
     k->jit_ms = *jit_ms;

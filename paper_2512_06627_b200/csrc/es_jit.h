@@ -16,10 +16,12 @@ struct JitKernel {
     cudaKernel_t kernel = nullptr;
     int threads = 0;        // variant selector (see below)
     int block = 0;          // CTA size of the launch
-    int region_bytes = 0;   // (unused: 0)
+    int region_bytes = 0;   // dynamic shared memory of the launch (split build: its slot file)
+    int parts = 1;          // phases of a split build (1: one straight-line body)
     int regs = -1;
     int spill_bytes = 0;
-    int opt = 3;            // ptxas optimisation level it was compiled at
+    int opt = 3;            // build level: ptxas -O3 / -O1, or -P = split build of P phases at -O1
+                            // (ordered: a request for level L is met by a kernel of level >= L)
     double jit_ms = 0;
     uint64_t ptx_h2 = 0;    // second hash + length of the PTX: cache-hit check
     size_t ptx_len = 0;
@@ -36,12 +38,19 @@ bool splice_body(const LutNet &net, int threads, std::string *ptx, std::string *
 // PTX -> sm_100a cubin in process at ptxas -O<opt> (ES_PTXAS_O overrides);
 // `info` receives ptxas's verbose log.
 int ptx_to_cubin(const std::string &ptx, std::vector<char> *cubin, std::string *info,
-                 std::string *err, int opt = 3);
+                 std::string *err, int opt = 3, bool relocatable = false);
+// Split build (es_split.cpp): the skeleton calling `parts` phase functions,
+// and the phase modules; smem_bytes = the slot file per CTA.
+bool splice_split(const LutNet &net, int threads, int parts, std::string *skel,
+                  std::vector<std::string> *phases, std::string *err, int *smem_bytes);
+int split_to_cubin(const std::string &skel, const std::vector<std::string> &phases, std::vector<char> *cubin,
+                   std::string *info, std::string *err, int opt);
 void parse_ptxas_info(const std::string &info, int *regs, int *spill_bytes);
 // Cached compile + load at ptxas -O<opt> (1: ~40 % less compile time, a few
 // % slower kernels -- for cold single runs; 3: default).  Thread-safe.
+// parts > 1 (or opt = -parts): split build (cold runs: ptxas on the phases in parallel).
 int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std::string *err,
-            int opt = 3);
+            int opt = 3, int parts = 1);
 void jit_clear();
 
 }  // namespace es

@@ -489,14 +489,21 @@ int k1_prepare(const LutNet &net, int threads, int sms, K1Plan *pl, double *jit_
         if (rc != ES_OK) { set_error(err); return rc; }
     }
     pl->threads = pl->jk->block;
-    pl->smem = 0;
+    pl->smem = (size_t)pl->jk->region_bytes;  // split build: the slot file
     const int P = net.num_pis;
     pl->cof_n = (int)net.cof_pis.size();
     if (pl->cof_n > kMaxCofactorPis || (pl->cof_n > 0 && P - 5 - pl->cof_n < 0)) { set_error("bad cofactor set"); return ES_E_BAD_ARG; }
     for (int i = 0; i < pl->cof_n; ++i) pl->cof_pos[i] = (unsigned)(net.cof_pis[i] - 1);
     pl->total_words = 1ull << std::max(P - 5 - pl->cof_n, 0);
     int nb = 0;
-    if (pl->smem > 48 * 1024)
+    if (getenv("ES_VERBOSE")) {
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, (const void *)pl->jk->kernel);
+        fprintf(stderr, "[es] K1 kernel: regs %d local %zu B static smem %zu B max threads %d, dynamic smem %zu B, parts %d\n",
+                fa.numRegs, (size_t)fa.localSizeBytes, (size_t)fa.sharedSizeBytes, fa.maxThreadsPerBlock, pl->smem,
+                pl->jk->parts);
+    }
+    if (pl->smem > 0)  // the skeleton's static shared memory counts against the 48 KB default too
         CK(cudaFuncSetAttribute((const void *)pl->jk->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->smem));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)pl->jk->kernel, pl->threads, pl->smem));
     nb = std::max(nb, 1);
@@ -1309,20 +1316,46 @@ static double est_jit_ms(const LutNet &n, int opt = 3) {
 }
 constexpr double kO1Slowdown = 1.07;
 
+// Split build (es_split.cpp, build level -P): ptxas on P phase modules in
+// parallel host threads, then one nvJitLink.  Fitted on the B200 box (16
+// host threads; mult16 k=0 / k=2, ES_JIT_CACHE=0): JIT = 0.75 * J1 / P +
+// 40 ms + 0.4 ms * P (J1 = the one-body -O1 JIT; the constant is the link,
+// module load and per-module ptxas start-up), and the sweep runs 1 + 0.09 P
+// times the one-body kernel's time (shared-memory slot traffic at the cuts).
+// mult16 k=0: J1 95 ms -> P=8 50 ms, sweep 10.5 -> 18.0 ms.
+static int split_parts(const LutNet &n, const es_run_opts &o) {
+    int P = o.jit_parts >= 2 ? o.jit_parts : 0;
+    if (const char *e = getenv("ES_JIT_PARTS")) P = atoi(e);
+    if (P == 0) P = (int)std::min(8u, std::max(1u, std::thread::hardware_concurrency() / 2));
+    if (P < 2 || (int)n.luts.size() < 16 * P) return 0;
+    return P;
+}
+static double est_split_jit_ms(const LutNet &n, int P) {
+    return 0.75 * est_jit_ms(n, 1) / P + 40.0 + 0.4 * P;
+}
+static double split_slowdown(int P) { return 1.0 + 0.09 * P; }
+
 // ptxas level for variant k: throughput mode always -O3; otherwise the level
 // with the smaller compile + expected sweep time (a kernel already compiled
 // at that level or higher costs nothing), so a cold single run compiles at
 // -O1 and a program that keeps being re-run tiers up to -O3.
 static int k1_opt(const MappedProg &mp, const LutNet &n, const JitKernel *have, int P, int sms, bool tput,
-                  double *cost) {
+                  double *cost, const es_run_opts &o) {
     const double sweep = est_sweep_ms(n, P, sms);
+    const int parts = o.jit_parts == 1 ? 0 : split_parts(n, o);
+    if (o.jit_parts >= 2 && parts >= 2) {  // forced split build
+        *cost = (have && have->opt >= -parts ? 0.0 : est_split_jit_ms(n, parts)) + sweep * split_slowdown(parts);
+        return -parts;
+    }
     if (tput) { *cost = sweep; return 3; }
     const double reuse = 1.0 + mp.runs;  // doubling rule: expect as many more runs as so far
     int best = 3;
     *cost = 1e300;
-    for (int opt : {3, 1}) {
-        const double jit = (have && have->opt >= opt) ? 0.0 : est_jit_ms(n, opt);
-        const double c = jit + sweep * reuse * (opt < 3 ? kO1Slowdown : 1.0);
+    for (int opt : {3, 1, -parts}) {
+        if (opt == 0) continue;  // no split candidate
+        const double jit = (have && have->opt >= opt) ? 0.0 : opt < 0 ? est_split_jit_ms(n, parts) : est_jit_ms(n, opt);
+        const double slow = opt == 3 ? 1.0 : opt == 1 ? kO1Slowdown : kO1Slowdown * split_slowdown(parts);
+        const double c = jit + sweep * reuse * slow;
         if (c < *cost) { *cost = c; best = opt; }
     }
     return best;
@@ -1334,7 +1367,7 @@ static int choose_cofactors(MappedProg &mp, const es_run_opts &o, int sms, int *
     double cost = 0;
     auto fixed = [&](int k) {
         const LutNet &n = mp.variant(k);
-        *opt = k1_opt(mp, n, mp.jk(n, k1_threads(o, k)), P, sms, tput, &cost);
+        *opt = k1_opt(mp, n, mp.jk(n, k1_threads(o, k)), P, sms, tput, &cost, o);
         return k;
     };
     if (o.cofactor_pis == ES_COFACTOR_NONE) return fixed(0);
@@ -1355,7 +1388,7 @@ static int choose_cofactors(MappedProg &mp, const es_run_opts &o, int sms, int *
     for (int k = 0; k <= kmax; ++k) {
         const LutNet &n = mp.variant(k);
         if ((int)n.cof_pis.size() != k) break;  // fewer candidate PIs than k
-        const int ok = k1_opt(mp, n, mp.jk(n, k1_threads(o, k)), P, sms, tput, &cost);
+        const int ok = k1_opt(mp, n, mp.jk(n, k1_threads(o, k)), P, sms, tput, &cost, o);
         if (cost < best_cost) { best_cost = cost; best = k; *opt = ok; worse = 0; }
         // latency mode: the JIT term grows with k, so two deeper variants that
         // do not pay end the search (mapping k=3..5 costs ~40 ms on mult16)
@@ -1436,7 +1469,8 @@ static int run_k1_job(MappedProg &mp, const LutNet &net, const es_run_opts &o, c
     r->jit_ms += jit_ms;
     r->regs_per_thread = pl.jk->regs;
     r->cofactor_pis = pl.cof_n;
-    r->jit_opt = pl.jk->opt;
+    r->jit_opt = pl.jk->opt < 0 ? 1 : pl.jk->opt;
+    r->jit_parts = pl.jk->parts;
     r->num_luts = (int)net.luts.size();
     r->n_devices = n_dev;
     r->phases = 1;
@@ -1484,7 +1518,7 @@ static int run_k1_job(MappedProg &mp, const LutNet &net, const es_run_opts &o, c
             const LutNet &cand = mp.variant_set(pis);
             double c = frac_at_or_below(pis, P, w1) * est_sweep_ms(cand, P, sms * n_dev);
             const JitKernel *have = mp.jk(cand, k1_threads(o, k));
-            if (!tput && !(have && have->opt >= opt)) c += est_jit_ms(cand, opt);
+            if (!tput && !(have && have->opt >= opt)) c += opt < 0 ? est_split_jit_ms(cand, -opt) : est_jit_ms(cand, opt);
             if (c < best_cost) { best_cost = c; best_net = &cand; }
         }
     // (c): the phase-1 cofactor set restricted to the copies below w1's copy c1
@@ -1497,7 +1531,7 @@ static int run_k1_job(MappedProg &mp, const LutNet &net, const es_run_opts &o, c
         const LutNet &cand = mp.variant_set(net.cof_pis, c1);
         double c = frac_left * est_sweep_ms(cand, P, sms * n_dev);
         const JitKernel *have = mp.jk(cand, k1_threads(o, pl.cof_n));
-        if (!tput && !(have && have->opt >= opt)) c += est_jit_ms(cand, opt);
+        if (!tput && !(have && have->opt >= opt)) c += opt < 0 ? est_split_jit_ms(cand, -opt) : est_jit_ms(cand, opt);
         if (c < best_cost) { best_cost = c; best_net = nullptr; restricted = &cand; }
     }
     SweepOut s2;
@@ -1685,6 +1719,7 @@ int run_batch_jit(int n_jobs, const es_prog *progs, const es_run_opts *opts, es_
     es_run_opts o{};
     if (opts) o = *opts;
     o.engine = ES_ENGINE_JIT;
+    if (o.jit_parts == 0) o.jit_parts = 1;  // the jobs already compile on parallel host threads
     const double t0 = now_ms();
     const double deadline = o.budget_s >= 0 && opts ? t0 + 1e3 * o.budget_s : -1.0;
     int sms = 0;

@@ -239,7 +239,8 @@ def _cofactor_code(cofactor) -> int:
 
 
 def _opts(device: int, engine: str, budget: float | None, cancel_addr, slice_ms: float,
-          block_threads: int, cofactor="auto", devices: Sequence[int] | None = None) -> N.EsRunOpts:
+          block_threads: int, cofactor="auto", devices: Sequence[int] | None = None,
+          jit_parts: int = 0) -> N.EsRunOpts:
     o = N.EsRunOpts()
     o.device = device
     o.engine = N.ENGINES[engine]
@@ -249,6 +250,9 @@ def _opts(device: int, engine: str, budget: float | None, cancel_addr, slice_ms:
     o.block_threads = block_threads
     o.flags = 0
     o.cofactor_pis = _cofactor_code(cofactor)
+    if jit_parts < 0:
+        raise ValueError("jit_parts must be >= 0")
+    o.jit_parts = jit_parts
     if devices:
         arr = (ctypes.c_int32 * len(devices))(*[int(d) for d in devices])
         o.n_devices = len(devices)
@@ -266,7 +270,8 @@ def _stats_of(r: N.EsResult) -> dict:
             "jit_opt": int(r.jit_opt), "witness_minimal": bool(r.witness_minimal),
             "n_devices": int(r.n_devices), "phases": int(r.phases),
             "phase2_cofactor_pis": int(r.phase2_cofactor_pis) if r.phases == 2 else None,
-            "phase2_copies": int(r.phase2_copies) if r.phases == 2 else None}
+            "phase2_copies": int(r.phase2_copies) if r.phases == 2 else None,
+            "jit_parts": int(r.jit_parts)}
 
 
 def _to_esresult(r: N.EsResult, num_pis: int) -> EsResult:
@@ -281,7 +286,7 @@ def _to_esresult(r: N.EsResult, num_pis: int) -> EsResult:
 def run_exhaustive(p, workers: int = 1, budget: float | None = None, cancel=None, *,
                    device: int = 0, engine: str = "auto", slice_ms: float = 20.0,
                    block_threads: int = 0, cofactor="auto",
-                   devices: Sequence[int] | None = None) -> EsResult:
+                   devices: Sequence[int] | None = None, jit_parts: int = 0) -> EsResult:
     """Sweep all 2^num_pis assignments on the GPU (es.py:252-339).
 
     Returns the minimum-index counterexample (the reference's workers=1
@@ -298,6 +303,11 @@ def run_exhaustive(p, workers: int = 1, budget: float | None = None, cancel=None
     dealt round-robin, one host thread drives each device, and one minimum
     word shared over NVLink stops every GPU once a smaller pattern cannot
     exist.  ``"all"`` = every visible GPU.  Default: ``device`` alone.
+
+    ``jit_parts`` (JIT engine): 0 lets the policy split a cold program's
+    kernel body into phases that ptxas compiles on parallel host threads
+    (es_split.cpp), 1 keeps one straight-line body, >= 2 forces that many
+    phases.
     """
     if workers < 1:
         raise ValueError("workers must be >= 1")
@@ -312,7 +322,7 @@ def run_exhaustive(p, workers: int = 1, budget: float | None = None, cancel=None
     res = N.EsResult()
     with _CancelWatcher(cancel) as cw:
         opts = _opts(device, engine, budget, cw.address, slice_ms, block_threads, cofactor,
-                     _devices(devices))
+                     _devices(devices), jit_parts)
         N.check(N.lib().es_run(ctypes.byref(prog.as_struct()), ctypes.byref(opts),
                                ctypes.byref(res)))
     return _to_esresult(res, prog.num_pis)
@@ -355,7 +365,7 @@ def _devices(devices) -> list[int] | None:
 
 def es_check(sm, workers: int = 1, budget: float | None = None, cancel=None, *,
              device: int = 0, engine: str = "auto", cofactor="auto",
-             devices: Sequence[int] | str | None = None) -> CheckResult:
+             devices: Sequence[int] | str | None = None, jit_parts: int = 0) -> CheckResult:
     """Compile and sweep a sub-miter (es.py:342-365); witnesses are re-checked
     by direct evaluation and a mismatch raises AssertionError."""
     t0 = time.monotonic()
@@ -364,7 +374,7 @@ def es_check(sm, workers: int = 1, budget: float | None = None, cancel=None, *,
     except TooManyInputs:
         return CheckResult(UNKNOWN, reason="ineligible", engine="es")
     r = run_exhaustive(prog, workers=workers, budget=budget, cancel=cancel, device=device,
-                       engine=engine, cofactor=cofactor, devices=devices)
+                       engine=engine, cofactor=cofactor, devices=devices, jit_parts=jit_parts)
     stats = {"patterns": r.patterns_evaluated, "registers": prog.num_registers,
              "wall_time": time.monotonic() - t0, **r.stats}
     if r.verdict == EXHAUSTED_ZERO:

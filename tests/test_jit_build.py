@@ -48,3 +48,21 @@ def test_throughput_kernel_mult16_k4_has_no_spills():
     assert es.map_stats(p, 4)["peak_live"] <= 230
     j = es.jit_check(p, block_threads=256, k=4)
     assert j["spill_bytes"] == 0, j["log"]
+
+
+@pytest.mark.parametrize("k,parts", [(0, 2), (0, 6), (2, 4)])
+def test_split_build_compiles_and_links(k, parts):
+    """The split build (es_split.cpp): phase modules compile relocatable and
+    nvJitLink joins them with the skeleton, with no GPU."""
+    import ctypes
+
+    from paper_2512_06627_b200 import _native as N
+
+    p = es.compile_program(M.gen_multiplier_miter(12, "array", "wallace"))
+    regs, smem, slots, loads = (ctypes.c_int32() for _ in range(4))
+    ms = ctypes.c_double()
+    n = N.check(N.lib().es_jit_check_split(ctypes.byref(p.as_struct()), k, parts, 128, ctypes.byref(regs),
+                                           ctypes.byref(smem), ctypes.byref(slots), ctypes.byref(loads),
+                                           ctypes.byref(ms)))
+    assert n > 0
+    assert slots.value > 0 and smem.value == slots.value * 128 * 4 and loads.value >= slots.value - 2
