@@ -19,6 +19,8 @@ enum : uint32_t {
     K2_NEG_B = 64u,   // mb = ~0
     K2_CONST = 128u,  // OUT: the value is the constant 0 (then NEG_A makes it ~0)
 };
+// OUT with K2_A_ACC in a multi-lane program: the accumulator's lane (2 bits)
+constexpr unsigned K2_OUT_LANE_SHIFT = 8;
 constexpr int kK2MaxCofactorPis = 6;
 
 // One 16-byte record: a gate or an output.  Slots on the host, byte offsets
@@ -36,14 +38,22 @@ struct K2Prog {
     std::vector<int32_t> cof_pis;   // cofactor PIs (ascending); copies = 2^size
     int n_gates = 0;                // gate records (excluding OUT)
     int loads = 0, stores = 0;      // slot loads / stores per pass (cost model)
+    // Multi-lane program (lanes L = 2 or 4; kernel es_k2d): records come in
+    // steps of L -- L independent gates, one per lane, each lane with its own
+    // accumulator (a NOP lane is acc & ~0 over the zero slot num_pis), or up
+    // to L OUT records (the rest NOPs).  Every lane's operands are read
+    // before any result of the step is stored.
+    int lanes = 1;
 };
 
 // Launch group of a program: the widest words-per-thread W (4, 2, 1) at which
 // its slot file (slots x 128 threads x W x 4 B) plus its staged records fit
 // two CTAs per SM (2 x (bytes + 1 KB) <= 228 KB); 0 = W4, 1 = W2, 2 = W1.
 constexpr size_t kK2TwoCtaBytes = 115600;
+// records staged past a program's end (the kernels prefetch one step ahead)
+constexpr int kK2PadRecords = 4;
 inline int k2_group_of(int num_slots, size_t num_records) {
-    const size_t rec = (num_records + 1) * 16, s = (size_t)(num_slots > 0 ? num_slots : 1) * 512;
+    const size_t rec = (num_records + kK2PadRecords) * 16, s = (size_t)(num_slots > 0 ? num_slots : 1) * 512;
     if (s * 4 + rec <= kK2TwoCtaBytes) return 0;
     if (s * 2 + rec <= kK2TwoCtaBytes) return 1;
     return 2;
@@ -55,10 +65,14 @@ inline int k2_group_of(int num_slots, size_t num_records) {
 // that do not fit go to K1 (es_runtime.cu routes them).
 constexpr size_t kK2MaxSmemBytes = 232448 - 64;
 inline size_t k2_smem_w1(int num_slots, size_t num_records) {
-    return (size_t)(num_slots > 0 ? num_slots : 1) * 512 + (num_records + 1) * 16;
+    return (size_t)(num_slots > 0 ? num_slots : 1) * 512 + (num_records + kK2PadRecords) * 16;
 }
-inline bool k2_fits(const K2Prog &kp) { return k2_smem_w1(kp.num_slots, kp.gates.size()) <= kK2MaxSmemBytes; }
+// Device records of a program (one per record).
+inline size_t k2_device_records(const K2Prog &kp) { return kp.gates.size(); }
+inline bool k2_fits(const K2Prog &kp) { return k2_smem_w1(kp.num_slots, k2_device_records(kp)) <= kK2MaxSmemBytes; }
 
+// Lanes of the K2 programs build_k2prog emits (ES_K2_LANES: 1, 2 or 4).
+int k2_lanes();
 // K2 program of a (possibly multi-output) graph: DFS schedule with
 // accumulator forwarding, LIFO slot reuse, OUT records in copy order.
 void build_k2prog(const Dag &dag, K2Prog *kp);

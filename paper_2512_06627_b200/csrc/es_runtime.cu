@@ -259,6 +259,196 @@ __global__ void __launch_bounds__(128) es_k2(const K2Job *__restrict__ jobs,
     }
 }
 
+// K2, L lanes (multi-lane programs, es_k2prog.cpp emit_k2_lanes): every
+// step is L records -- L independent gates with one accumulator per lane,
+// or up to L OUT records -- so a warp has L dependency chains to issue from
+// (the one-lane kernel is latency-bound at 8 warps per SM: stall_wait 2.2
+// per issue).  Every lane's operands are loaded before any result of the step
+// is stored; slot num_pis holds zero (a NOP lane is acc & ~0 over it).
+#ifndef ES_K2D_UNROLL
+#define ES_K2D_UNROLL 2
+#endif
+template <int W, int L>
+__global__ void __launch_bounds__(128) es_k2d(const K2Job *__restrict__ jobs,
+                                              const K2Item *__restrict__ items,
+                                              unsigned long long item_begin,
+                                              unsigned long long item_end, unsigned *counter,
+                                              int smem_bytes) {
+    extern __shared__ __align__(16) uint4 smem[];
+    __shared__ unsigned long long s_item;
+    const unsigned T = blockDim.x, t = threadIdx.x, lane = t & 31u;
+    const unsigned smem_addr = (unsigned)__cvta_generic_to_shared(smem);
+    const unsigned base = smem_addr + t * W * 4;
+    unsigned prog_addr = smem_addr;
+    const unsigned long long kStop = ~0ull, kSkip = ~0ull - 1;
+    int cur_job = -1;
+    for (;;) {
+        if (t == 0) {
+            unsigned long long k = item_begin + atomicAdd(counter, 1u);
+            if (k >= item_end) {
+                k = kStop;
+            } else {
+                const K2Item it = items[k];
+                const K2Job &jb = jobs[it.job];
+                if (k2_expand(it.w0 << 5, jb) > *(volatile unsigned long long *)jb.best) k = kSkip;
+                else atomicAdd(jb.swept, 1u);
+            }
+            s_item = k;
+        }
+        __syncthreads();
+        const unsigned long long k = s_item;
+        if (k == kStop) break;
+        if (k == kSkip) { __syncthreads(); continue; }
+        const K2Item it = items[k];
+        const K2Job job = jobs[it.job];
+        // records, then room for one step's prefetch past the end
+        const int rec0 = smem_bytes / 16 - (job.n_recs + kK2PadRecords);
+        prog_addr = smem_addr + 16u * (unsigned)rec0;
+        if (it.job != cur_job) {
+            const uint4 *src = reinterpret_cast<const uint4 *>(job.code);
+            for (int q = t; q < job.n_recs; q += T) smem[rec0 + q] = __ldg(&src[q]);
+            cur_job = it.job;
+        }
+        __syncthreads();
+        const int n_steps = job.n_recs / L;
+        for (unsigned wb = 0; wb < it.n_words; wb += T * W) {
+            const unsigned long long w = it.w0 + wb + (unsigned long long)t * W;
+            {
+                int bit = 0;
+                for (int j = 0; j < job.num_pis; ++j) {
+                    if (j >= 5 && ((job.cof_mask >> (j + 1)) & 1ull)) continue;
+                    unsigned v[W];
+#pragma unroll
+                    for (int q = 0; q < W; ++q)
+                        v[q] = j < 5 ? c_lane_mask[j] : ((((w + q) >> bit) & 1ull) ? ~0u : 0u);
+                    if (j >= 5) ++bit;
+                    sts<W>(base + (unsigned)j * T * W * 4, v);
+                }
+                unsigned z[W];
+#pragma unroll
+                for (int q = 0; q < W; ++q) z[q] = 0u;
+                sts<W>(base + (unsigned)job.num_pis * T * W * 4, z);  // the NOP lanes' zero slot
+            }
+            unsigned acc[L][W], b[L][W], fw[W], fc[W];
+#pragma unroll
+            for (int h = 0; h < L; ++h)
+#pragma unroll
+                for (int q = 0; q < W; ++q) acc[h][q] = 0;
+#pragma unroll
+            for (int q = 0; q < W; ++q) { fw[q] = 0; fc[q] = 0; }
+            uint4 nx[L];
+#pragma unroll
+            for (int h = 0; h < L; ++h) nx[h] = lds_rec(prog_addr + 16u * h);
+#pragma unroll 2
+            for (int i = 0; i < n_steps; ++i) {
+                uint4 c[L];
+#pragma unroll
+                for (int h = 0; h < L; ++h) {
+                    c[h] = nx[h];
+                    nx[h] = lds_rec(prog_addr + 16u * (unsigned)(L * (i + 1) + h));  // next step (past-end reads harmless)
+                }
+                if (c[0].w & K2_OUT) {  // OUT step: fold in record (= copy) order
+#pragma unroll
+                    for (int h = 0; h < L; ++h) {
+                        if (!(c[h].w & K2_OUT)) continue;
+                        const unsigned m = (unsigned)((int)c[h].w >> 31);
+                        unsigned v[W];
+                        if (c[h].w & K2_A_ACC) {
+                            const unsigned ln = (c[h].w >> K2_OUT_LANE_SHIFT) & 3u;
+#pragma unroll
+                            for (int q = 0; q < W; ++q) {
+                                unsigned x = acc[0][q];
+#pragma unroll
+                                for (int g = 1; g < L; ++g) x = ln == (unsigned)g ? acc[g][q] : x;
+                                v[q] = x;
+                            }
+                        } else if (c[h].w & K2_CONST) {
+#pragma unroll
+                            for (int q = 0; q < W; ++q) v[q] = 0u;
+                        } else {
+                            lds<W>(base + c[h].x, v);
+                        }
+                        const unsigned copy = (c[h].w >> 16) & 0x3FFFu;
+#pragma unroll
+                        for (int q = 0; q < W; ++q) {
+                            const bool first = fw[q] == 0u;
+                            fw[q] = first ? (v[q] ^ m) : fw[q];
+                            fc[q] = first ? copy : fc[q];
+                        }
+                    }
+                    continue;
+                }
+                // every lane's loads first (A straight into its accumulator)
+#pragma unroll
+                for (int h = 0; h < L; ++h) {
+                    if (!(c[h].w & K2_A_ACC)) lds<W>(base + c[h].x, acc[h]);
+                    lds<W>(base + c[h].y, b[h]);
+                }
+                if constexpr (L >= 2) {
+                    // masks from the msb of ctl bytes 3 / 2 / 1 (NEG_A, NEG_B,
+                    // XOR; packed by k2_group_prepare), one PRMT each:
+                    // u = A ^ ma, t = B ^ mb, result = s ? u ^ t : u & t
+#pragma unroll
+                    for (int h = 0; h < L; ++h) {
+                        unsigned ma, mb, ms;
+                        asm("prmt.b32 %0, %1, 0, 0xBBBB;" : "=r"(ma) : "r"(c[h].w));
+                        asm("prmt.b32 %0, %1, 0, 0xAAAA;" : "=r"(mb) : "r"(c[h].w));
+                        asm("prmt.b32 %0, %1, 0, 0x9999;" : "=r"(ms) : "r"(c[h].w));
+#pragma unroll
+                        for (int q = 0; q < W; ++q) {
+                            const unsigned u = acc[h][q] ^ ma, tt = b[h][q] ^ mb;
+                            unsigned r;  // s ? u ^ t : u & t as one LOP3 (0x68 over u, t, s)
+                            asm("lop3.b32 %0, %1, %2, %3, 0x68;" : "=r"(r) : "r"(u), "r"(tt), "r"(ms));
+                            acc[h][q] = r;
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int h = 0; h < L; ++h) {
+                        const unsigned ma = (unsigned)((int)c[h].w >> 31);         // NEG_A mirrored in bit 31
+                        const unsigned mb = (unsigned)((int)(c[h].w << 1) >> 31);  // NEG_B in bit 30
+                        if (c[h].w & K2_XOR) {
+#pragma unroll
+                            for (int q = 0; q < W; ++q) acc[h][q] = acc[h][q] ^ b[h][q] ^ ma;
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < W; ++q) acc[h][q] = (acc[h][q] ^ ma) & (b[h][q] ^ mb);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int h = 0; h < L; ++h)
+                    if (c[h].w & K2_STORE) sts<W>(base + c[h].z, acc[h]);
+            }
+            unsigned any = 0;
+#pragma unroll
+            for (int q = 0; q < W; ++q) {
+                unsigned o = fw[q] & job.valid_mask;
+                if (w + q >= job.total_words || wb + t * W + q >= it.n_words) o = 0;
+                fw[q] = o;
+                any |= o;
+            }
+            if (__ballot_sync(0xffffffffu, any != 0u)) {
+                unsigned long long cand = ~0ull;
+#pragma unroll
+                for (int q = 0; q < W; ++q) {
+                    if (!fw[q]) continue;
+                    unsigned long long pat = k2_expand(((w + q) << 5) | (unsigned long long)(__ffs(fw[q]) - 1), job);
+                    for (int b2 = 0; b2 < job.cof_n; ++b2)
+                        if ((fc[q] >> b2) & 1u) pat |= 1ull << job.cof_pos[b2];
+                    cand = pat < cand ? pat : cand;
+                }
+#pragma unroll
+                for (int off = 16; off; off >>= 1) {
+                    const unsigned long long o2 = __shfl_xor_sync(0xffffffffu, cand, off);
+                    cand = o2 < cand ? o2 : cand;
+                }
+                if (lane == 0) atomicMin(job.best, cand);
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // ALU-pipe peak microbenchmark: 8 independent LOP3 chains per thread, enough
 // warps to saturate every SMSP.  Gives the measured roofline denominator for
@@ -782,17 +972,26 @@ static uint4 k2_record(const K2Gate &g, uint32_t stride) {
 
 template <int W>
 static int launch_k2(int grid, size_t smem, cudaStream_t st, const K2Job *jobs, const K2Item *items,
-                     uint64_t begin, uint64_t end, unsigned *counter, int smem_bytes) {
-    es_k2<W><<<grid, 128, smem, st>>>(jobs, items, begin, end, counter, smem_bytes);
+                     uint64_t begin, uint64_t end, unsigned *counter, int smem_bytes, int lanes) {
+    if (lanes == 4) es_k2d<W, 4><<<grid, 128, smem, st>>>(jobs, items, begin, end, counter, smem_bytes);
+    else if (lanes == 2) es_k2d<W, 2><<<grid, 128, smem, st>>>(jobs, items, begin, end, counter, smem_bytes);
+    else es_k2<W><<<grid, 128, smem, st>>>(jobs, items, begin, end, counter, smem_bytes);
     CK(cudaGetLastError());
     return ES_OK;
 }
 
-template <int W>
-static int k2_occupancy(size_t smem, int *nb) {
-    CK(cudaFuncSetAttribute(es_k2<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(nb, es_k2<W>, 128, smem));
+template <class K>
+static int k2_occ(K kern, size_t smem, int *nb) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(nb, kern, 128, smem));
     return ES_OK;
+}
+
+template <int W>
+static int k2_occupancy(size_t smem, int *nb, int lanes) {
+    if (lanes == 4) return k2_occ(es_k2d<W, 4>, smem, nb);
+    if (lanes == 2) return k2_occ(es_k2d<W, 2>, smem, nb);
+    return k2_occ(es_k2<W>, smem, nb);
 }
 
 // One launch group: jobs sharing a words-per-thread width W.  Items are dealt
@@ -803,6 +1002,7 @@ static int k2_occupancy(size_t smem, int *nb) {
 struct K2Group {
     std::vector<int> jobs_idx;   // indices into the caller's job arrays
     int W = 1, smem_bytes = 0, nb = 1;
+    int lanes = 1;               // multi-lane programs (es_k2d) when > 1
     size_t smem = 0;
     uint4 *code = nullptr;       // device-image records, in the pinned stage
     size_t n_code = 0;
@@ -836,7 +1036,7 @@ static int k2_group_prepare(K2Group &gp, const es_prog *progs, const K2Prog *con
     auto smem_for = [&](int W) {  // the largest job's slot file + records (kernel layout)
         size_t m = 16;
         for (int j : group)
-            m = std::max(m, (size_t)std::max(kps[j]->num_slots, 1) * T * W * 4 + (kps[j]->gates.size() + 1) * 16);
+            m = std::max(m, (size_t)std::max(kps[j]->num_slots, 1) * T * W * 4 + (k2_device_records(*kps[j]) + kK2PadRecords) * 16);
         return m;
     };
     // widest W that keeps the target number of resident CTAs per SM, else
@@ -855,19 +1055,32 @@ static int k2_group_prepare(K2Group &gp, const es_prog *progs, const K2Prog *con
     const uint32_t stride = (uint32_t)T * W * 4;
     const int G = (int)group.size();
     std::vector<size_t> off(G + 1, 0);  // one record per gate / output
-    for (int q = 0; q < G; ++q) off[q + 1] = off[q] + kps[group[q]]->gates.size();
+    for (int q = 0; q < G; ++q) off[q + 1] = off[q] + k2_device_records(*kps[group[q]]);
     gp.code = stage;  // records built straight into pinned memory: one DMA, no bounce copy
     gp.n_code = off[G];
     parallel_for(G, [&](int q) {
         uint4 *dst = gp.code + off[q];
-        for (const K2Gate &g : kps[group[q]]->gates) *dst++ = k2_record(g, stride);
+        const K2Prog &kp = *kps[group[q]];
+        for (const K2Gate &g : kp.gates) {
+            uint4 r = k2_record(g, stride);
+            // two-lane gate records: the byte-msb masks es_k2d<W, 2> PRMTs out
+            // -- NEG_A in bit 31 (k2_record), NEG_B in bit 23, XOR in bit 15
+            // (for XOR the combined inversion is NEG_A and mb = 0)
+            if (kp.lanes >= 2 && !(g.ctl & K2_OUT))
+                r.w = (r.w & ~0x00808000u) | ((g.ctl & K2_XOR) ? 0x8000u : ((g.ctl & K2_NEG_B) ? 0x800000u : 0u));
+            *dst++ = r;
+        }
     });
     auto kwords = [&](int q) {  // kernel words of job q (cofactor PIs excluded)
         const int j = group[q];
         return 1ull << std::max(progs[j].num_pis - 5 - (int)kps[j]->cof_pis.size(), 0);
     };
-    int rc = W == 4 ? k2_occupancy<4>(gp.smem, &gp.nb) : W == 2 ? k2_occupancy<2>(gp.smem, &gp.nb)
-                                                                : k2_occupancy<1>(gp.smem, &gp.nb);
+    // the group's lane count is its programs' (build_k2prog: ES_K2_LANES)
+    gp.lanes = group.empty() ? 1 : kps[group[0]]->lanes;
+    for (int j : group)
+        if (kps[j]->lanes != gp.lanes) { set_error("internal: K2 programs of different lane counts in one group"); return ES_E_BAD_PROGRAM; }
+    int rc = W == 4 ? k2_occupancy<4>(gp.smem, &gp.nb, gp.lanes) : W == 2 ? k2_occupancy<2>(gp.smem, &gp.nb, gp.lanes)
+                                                                : k2_occupancy<1>(gp.smem, &gp.nb, gp.lanes);
     if (rc != ES_OK) return rc;
     gp.nb = std::max(gp.nb, 1);
     // item size: 4096 words, halved (down to one CTA iteration) until the
@@ -922,7 +1135,7 @@ static int k2_group_prepare(K2Group &gp, const es_prog *progs, const K2Prog *con
         J.best = gp.d_best + q;
         J.swept = gp.d_swept + q;
         J.total_words = kwords(q);
-        J.n_recs = (int)kps[j]->gates.size();
+        J.n_recs = (int)k2_device_records(*kps[j]);
         J.num_pis = progs[j].num_pis;
         J.valid_mask = lane_valid_mask(progs[j].num_pis);
         J.cof_n = (int)kps[j]->cof_pis.size();
@@ -949,9 +1162,9 @@ static int k2_group_launch(K2Group &gp, cudaStream_t st, unsigned *counter, uint
                            uint64_t end, int sms) {
     CK(cudaMemsetAsync(counter, 0, sizeof(unsigned), st));
     const int grid = (int)std::min<uint64_t>(end - begin, (uint64_t)sms * gp.nb);
-    const int rc = gp.W == 4 ? launch_k2<4>(grid, gp.smem, st, gp.d_jobs, gp.d_items, begin, end, counter, gp.smem_bytes)
-                 : gp.W == 2 ? launch_k2<2>(grid, gp.smem, st, gp.d_jobs, gp.d_items, begin, end, counter, gp.smem_bytes)
-                             : launch_k2<1>(grid, gp.smem, st, gp.d_jobs, gp.d_items, begin, end, counter, gp.smem_bytes);
+    const int rc = gp.W == 4 ? launch_k2<4>(grid, gp.smem, st, gp.d_jobs, gp.d_items, begin, end, counter, gp.smem_bytes, gp.lanes)
+                 : gp.W == 2 ? launch_k2<2>(grid, gp.smem, st, gp.d_jobs, gp.d_items, begin, end, counter, gp.smem_bytes, gp.lanes)
+                             : launch_k2<1>(grid, gp.smem, st, gp.d_jobs, gp.d_items, begin, end, counter, gp.smem_bytes, gp.lanes);
     if (rc == ES_OK) { gp.launches++; gp.done_items = end; }
     return rc;
 }
@@ -1066,7 +1279,7 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
     std::vector<K2Group> groups(3);
     for (int j : active) {
         const int sl = kps[j]->num_slots;
-        groups[k2_group_of(sl, kps[j]->gates.size())].jobs_idx.push_back(j);
+        groups[k2_group_of(sl, k2_device_records(*kps[j]))].jobs_idx.push_back(j);
     }
     groups.erase(std::remove_if(groups.begin(), groups.end(),
                                 [](const K2Group &g) { return g.jobs_idx.empty(); }),
@@ -1075,7 +1288,7 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
     const double t0 = now_ms();
     size_t total_recs = 0;
     for (const K2Group &gp : groups)
-        for (int j : gp.jobs_idx) total_recs += kps[j]->gates.size();
+        for (int j : gp.jobs_idx) total_recs += k2_device_records(*kps[j]);
     if (total_recs > c->stage_cap) {
         if (c->h_stage) CK(cudaFreeHost(c->h_stage));
         c->h_stage = nullptr;
@@ -1090,7 +1303,7 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
     std::vector<size_t> stage_off(groups.size() + 1, 0);
     for (size_t g = 0; g < groups.size(); ++g) {  // records of each group straight into pinned memory
         size_t n = 0;
-        for (int j : groups[g].jobs_idx) n += kps[j]->gates.size();
+        for (int j : groups[g].jobs_idx) n += k2_device_records(*kps[j]);
         stage_off[g + 1] = stage_off[g] + n;
     }
     double t1 = now_ms();
@@ -1689,7 +1902,7 @@ int run_one(const es_prog *prog, const es_run_opts *opts, es_result *out) {
             rc = run_k2(1, prog, act, o, c, deadline, out, &kp);
         } else if (o.engine == ES_ENGINE_INTERP) {
             set_error("program needs " + std::to_string(kp->num_slots) + " slots (" +
-                      std::to_string(k2_smem_w1(kp->num_slots, kp->gates.size())) +
+                      std::to_string(k2_smem_w1(kp->num_slots, k2_device_records(*kp))) +
                       " B of shared memory): too many for the K2 interpreter; use engine auto or jit");
             return ES_E_BAD_PROGRAM;
         } else {
