@@ -366,11 +366,11 @@ def k2_smem_model(batch, res) -> dict:
     """Shared-memory wavefronts the K2 interpreter issues (ncu's
     l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld + _op_st): per warp and
     pass over a job's records, each 16-byte broadcast record load (records +
-    the one-past-end prefetch) costs 2 wavefronts, each slot load or store W
-    (W words x 4 B x 32 threads = W x 128 B), with the accumulator
-    forwarding's actual per-program load/store counts and the PI words
-    stored at the start of a pass.  Calibrated against ncu per launch group
-    (profiles/r02_k2_cones_W*_ncu_full.json: loads and stores within 0.5 %)."""
+    the two-step prefetch of the two-lane kernel, 4 records) costs 2
+    wavefronts, each slot load or store W (W words x 4 B x 32 threads = W x
+    128 B), with the per-program load/store counts of the two-lane schedule
+    (accumulator forwarding per lane; a NOP lane loads the zero slot).
+    Calibrated against ncu per launch group (profiles/r02_k2l_*)."""
     import numpy as np
 
     st = batch.k2_stats()
@@ -382,13 +382,13 @@ def k2_smem_model(batch, res) -> dict:
     copies = np.exp2(st["cofactor_pis"].astype(np.float64))
     iters = words / copies  # interpreter passes over the record list, per thread-word
     warp_iters = iters / (32.0 * W)
-    per = 2.0 * (st["num_records"] + 1) + (tr["loads"] + tr["stores"]) * W
+    per = 2.0 * (st["num_records"] + 4) + (tr["loads"] + tr["stores"]) * W
     wavefronts = float((warp_iters * per)[ran].sum())
     groups = {}
     for w in (1, 2, 4):
         m = ran & (W == w)
         groups[f"W{w}"] = {"jobs": int(m.sum()),
-                           "ld_wavefronts": float((warp_iters * (2.0 * (st["num_records"] + 1)
+                           "ld_wavefronts": float((warp_iters * (2.0 * (st["num_records"] + 4)
                                                                  + tr["loads"] * W))[m].sum()),
                            "st_wavefronts": float((warp_iters * tr["stores"] * W)[m].sum())}
     return {"wavefronts": wavefronts, "bytes": wavefronts * 128.0,
@@ -433,7 +433,7 @@ def measure_cones(steps: int, warmup: int, rank: int = 0, world: int = 1, count:
                             "program) / device time",
             "wavefronts": model["wavefronts"], "record_passes": model["record_passes"],
             "groups": model["groups"],
-            "ncu_check": "profiles/r02_k2_cones_W*_ncu_full.json: ld/st wavefronts per group"}
+            "ncu_check": "profiles/r02_k2l_cones_W*_ncu_full.json: ld/st wavefronts per group"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     lt = cones.LAST_TIMING
     out = {"jobs": len(batch), "eq": eq, "neq": neq, "gate_patterns": work, "roofline": roof,

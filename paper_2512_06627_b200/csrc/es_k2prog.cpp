@@ -354,7 +354,10 @@ void emit_k2_lanes(const Dag &dag, const Outs &outs, const std::vector<int> &ord
             rec[h].ctl |= K2_STORE;
             kp->stores++;
         }
-        for (int h = 0; h < L; ++h) kp->gates.push_back(rec[h]);
+        for (int h = 0; h < L; ++h) {
+            if (st.g[h] < 0) kp->loads++;  // a NOP lane still loads the zero slot
+            kp->gates.push_back(rec[h]);
+        }
     }
     kp->num_slots = top;
 }

@@ -51,7 +51,7 @@ struct K2Prog {
 // two CTAs per SM (2 x (bytes + 1 KB) <= 228 KB); 0 = W4, 1 = W2, 2 = W1.
 constexpr size_t kK2TwoCtaBytes = 115600;
 // records staged past a program's end (the kernels prefetch one step ahead)
-constexpr int kK2PadRecords = 4;
+constexpr int kK2PadRecords = 8;  // two steps of up to four lanes
 inline int k2_group_of(int num_slots, size_t num_records) {
     const size_t rec = (num_records + kK2PadRecords) * 16, s = (size_t)(num_slots > 0 ? num_slots : 1) * 512;
     if (s * 4 + rec <= kK2TwoCtaBytes) return 0;

@@ -336,22 +336,46 @@ __global__ void __launch_bounds__(128) es_k2d(const K2Job *__restrict__ jobs,
                 for (int q = 0; q < W; ++q) acc[h][q] = 0;
 #pragma unroll
             for (int q = 0; q < W; ++q) { fw[q] = 0; fc[q] = 0; }
-            uint4 nx[L];
+            // the current step's records c[], the next step's nx[], and c's
+            // decoded operand addresses and masks; each step ends by decoding
+            // the next one inside its own basic block, so the decode overlaps
+            // the step's logic instead of heading the next block
+            uint4 c[L], nx[L];
+            unsigned pa[L], pb[L], pd[L], ma[L], mb[L], ms[L];
 #pragma unroll
-            for (int h = 0; h < L; ++h) nx[h] = lds_rec(prog_addr + 16u * h);
-#pragma unroll 2
-            for (int i = 0; i < n_steps; ++i) {
-                uint4 c[L];
+            for (int h = 0; h < L; ++h) {
+                c[h] = lds_rec(prog_addr + 16u * h);
+                nx[h] = lds_rec(prog_addr + 16u * (L + h));
+            }
+            // masks from the msb of ctl bytes 3 / 2 / 1 (NEG_A, NEG_B, XOR;
+            // packed by k2_group_prepare), one PRMT each
+            auto decode = [&]() {
 #pragma unroll
                 for (int h = 0; h < L; ++h) {
-                    c[h] = nx[h];
-                    nx[h] = lds_rec(prog_addr + 16u * (unsigned)(L * (i + 1) + h));  // next step (past-end reads harmless)
+                    pa[h] = base + c[h].x;
+                    pb[h] = base + c[h].y;
+                    pd[h] = base + c[h].z;
+                    asm("prmt.b32 %0, %1, 0, 0xBBBB;" : "=r"(ma[h]) : "r"(c[h].w));
+                    asm("prmt.b32 %0, %1, 0, 0xAAAA;" : "=r"(mb[h]) : "r"(c[h].w));
+                    asm("prmt.b32 %0, %1, 0, 0x9999;" : "=r"(ms[h]) : "r"(c[h].w));
                 }
+            };
+            decode();
+#pragma unroll 2
+            for (int i = 0; i < n_steps; ++i) {
+                // step i+2's records (past-end reads harmless: kK2PadRecords)
+                auto advance = [&]() {
+#pragma unroll
+                    for (int h = 0; h < L; ++h) {
+                        c[h] = nx[h];
+                        nx[h] = lds_rec(prog_addr + 16u * (unsigned)(L * (i + 2) + h));
+                    }
+                    decode();
+                };
                 if (c[0].w & K2_OUT) {  // OUT step: fold in record (= copy) order
 #pragma unroll
                     for (int h = 0; h < L; ++h) {
                         if (!(c[h].w & K2_OUT)) continue;
-                        const unsigned m = (unsigned)((int)c[h].w >> 31);
                         unsigned v[W];
                         if (c[h].w & K2_A_ACC) {
                             const unsigned ln = (c[h].w >> K2_OUT_LANE_SHIFT) & 3u;
@@ -366,59 +390,39 @@ __global__ void __launch_bounds__(128) es_k2d(const K2Job *__restrict__ jobs,
 #pragma unroll
                             for (int q = 0; q < W; ++q) v[q] = 0u;
                         } else {
-                            lds<W>(base + c[h].x, v);
+                            lds<W>(pa[h], v);
                         }
                         const unsigned copy = (c[h].w >> 16) & 0x3FFFu;
 #pragma unroll
                         for (int q = 0; q < W; ++q) {
                             const bool first = fw[q] == 0u;
-                            fw[q] = first ? (v[q] ^ m) : fw[q];
+                            fw[q] = first ? (v[q] ^ ma[h]) : fw[q];
                             fc[q] = first ? copy : fc[q];
                         }
                     }
+                    advance();
                     continue;
                 }
                 // every lane's loads first (A straight into its accumulator)
 #pragma unroll
                 for (int h = 0; h < L; ++h) {
-                    if (!(c[h].w & K2_A_ACC)) lds<W>(base + c[h].x, acc[h]);
-                    lds<W>(base + c[h].y, b[h]);
+                    if (!(c[h].w & K2_A_ACC)) lds<W>(pa[h], acc[h]);
+                    lds<W>(pb[h], b[h]);
                 }
-                if constexpr (L >= 2) {
-                    // masks from the msb of ctl bytes 3 / 2 / 1 (NEG_A, NEG_B,
-                    // XOR; packed by k2_group_prepare), one PRMT each:
-                    // u = A ^ ma, t = B ^ mb, result = s ? u ^ t : u & t
-#pragma unroll
-                    for (int h = 0; h < L; ++h) {
-                        unsigned ma, mb, ms;
-                        asm("prmt.b32 %0, %1, 0, 0xBBBB;" : "=r"(ma) : "r"(c[h].w));
-                        asm("prmt.b32 %0, %1, 0, 0xAAAA;" : "=r"(mb) : "r"(c[h].w));
-                        asm("prmt.b32 %0, %1, 0, 0x9999;" : "=r"(ms) : "r"(c[h].w));
-#pragma unroll
-                        for (int q = 0; q < W; ++q) {
-                            const unsigned u = acc[h][q] ^ ma, tt = b[h][q] ^ mb;
-                            unsigned r;  // s ? u ^ t : u & t as one LOP3 (0x68 over u, t, s)
-                            asm("lop3.b32 %0, %1, %2, %3, 0x68;" : "=r"(r) : "r"(u), "r"(tt), "r"(ms));
-                            acc[h][q] = r;
-                        }
-                    }
-                } else {
-#pragma unroll
-                    for (int h = 0; h < L; ++h) {
-                        const unsigned ma = (unsigned)((int)c[h].w >> 31);         // NEG_A mirrored in bit 31
-                        const unsigned mb = (unsigned)((int)(c[h].w << 1) >> 31);  // NEG_B in bit 30
-                        if (c[h].w & K2_XOR) {
-#pragma unroll
-                            for (int q = 0; q < W; ++q) acc[h][q] = acc[h][q] ^ b[h][q] ^ ma;
-                        } else {
-#pragma unroll
-                            for (int q = 0; q < W; ++q) acc[h][q] = (acc[h][q] ^ ma) & (b[h][q] ^ mb);
-                        }
-                    }
-                }
+                // u = A ^ ma, t = B ^ mb, result = s ? u ^ t : u & t
 #pragma unroll
                 for (int h = 0; h < L; ++h)
-                    if (c[h].w & K2_STORE) sts<W>(base + c[h].z, acc[h]);
+#pragma unroll
+                    for (int q = 0; q < W; ++q) {
+                        const unsigned u = acc[h][q] ^ ma[h], tt = b[h][q] ^ mb[h];
+                        unsigned r;  // one LOP3 (0x68 over u, t, s)
+                        asm("lop3.b32 %0, %1, %2, %3, 0x68;" : "=r"(r) : "r"(u), "r"(tt), "r"(ms[h]));
+                        acc[h][q] = r;
+                    }
+#pragma unroll
+                for (int h = 0; h < L; ++h)
+                    if (c[h].w & K2_STORE) sts<W>(pd[h], acc[h]);
+                advance();
             }
             unsigned any = 0;
 #pragma unroll
