@@ -172,6 +172,27 @@ int32_t es_map_pipes_k(const es_prog *prog, int32_t k, int32_t *lop3, int32_t *i
     for (size_t p = 0; (p = body.find("mad.lo.s32 %esq", p)) != std::string::npos; ++p) ++ni;
     if (lop3) *lop3 = nl;
     if (imad) *imad = ni;
+    if (getenv("ES_LUTCAT")) {
+        const int N = (int)net.is_const.size();
+        std::vector<uint8_t> sel(N, 0);
+        for (int j = 6; j <= net.num_pis; ++j) sel[j] = !net.is_const[j];
+        int cat[4][4] = {};
+        for (const Lut &L : net.luts) {
+            bool u = true;
+            for (int q = 0; q < 3; ++q) u = u && sel[L.leaf[q]];
+            sel[L.node] = u;
+            int nd = 0, nu = 0;
+            for (int kk = 0; kk < 3; ++kk) {
+                bool dep = false;
+                for (int i = 0; i < 8; ++i)
+                    if (((L.tt >> i) & 1) != ((L.tt >> (i ^ (1 << kk))) & 1)) dep = true;
+                if (dep) { ++nd; nu += sel[L.leaf[kk]]; }
+            }
+            cat[nd][nu]++;
+        }
+        for (int a = 0; a < 4; ++a) for (int b = 0; b <= a; ++b)
+            if (cat[a][b]) fprintf(stderr, "deps=%d uniform=%d : %d\n", a, b, cat[a][b]);
+    }
     return ES_OK;
 }
 

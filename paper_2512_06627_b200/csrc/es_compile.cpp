@@ -332,9 +332,26 @@ void map_luts(const Dag &dag, LutNet *net) {
 
     // cover: best cut per node, then exact-area recovery
     std::vector<int> best(N, 0), mref(N, 0);
-    std::function<int(int, const Cut &)> ref_cut, deref_cut;
+    // word-uniform nodes (support avoids the lane PIs): a 2-input LUT over
+    // one of them is an FMA-pipe IMAD in emit_body_ptx, so it costs the ALU
+    // pipe nothing; `imad_cost` weighs it in the area recovery
+    std::vector<uint8_t> uni(N, 0);
+    for (int j = kLanePis + 1; j <= P; ++j) uni[j] = 1;
+    for (int v = FG; v < N; ++v) {
+        if (!cone[v] || isc[v]) continue;
+        const int g = v - FG;
+        auto u_of = [&](int a) { return isc[a] ? (cv[a] == 0u || cv[a] == ~0u) : uni[a] != 0; };
+        uni[v] = u_of(dag.f0[g]) && u_of(dag.f1[g]);
+    }
+    static const float imad_cost = getenv("ES_IMAD_COST") ? (float)atof(getenv("ES_IMAD_COST")) : 1.0f;
+    auto cut_cost = [&](const Cut &c) -> float {
+        if (imad_cost == 1.0f || c.n != 2) return 1.0f;
+        const bool s0 = !isc[c.leaf[0]] && uni[c.leaf[0]], s1 = !isc[c.leaf[1]] && uni[c.leaf[1]];
+        return (s0 || s1) ? imad_cost : 1.0f;
+    };
+    std::function<float(int, const Cut &)> ref_cut, deref_cut;
     ref_cut = [&](int v, const Cut &c) {
-        int area = 1;
+        float area = cut_cost(c);
         for (int q = 0; q < c.n; ++q) {
             int l = c.leaf[q];
             if (is_gate_lut(l) && mref[l]++ == 0) area += ref_cut(l, cuts[l][best[l]]);
@@ -342,7 +359,7 @@ void map_luts(const Dag &dag, LutNet *net) {
         return area;
     };
     deref_cut = [&](int v, const Cut &c) {
-        int area = 1;
+        float area = cut_cost(c);
         for (int q = 0; q < c.n; ++q) {
             int l = c.leaf[q];
             if (is_gate_lut(l) && --mref[l] == 0) area += deref_cut(l, cuts[l][best[l]]);
@@ -360,11 +377,12 @@ void map_luts(const Dag &dag, LutNet *net) {
             for (int v = FG; v < N; ++v) {
                 if (!is_gate_lut(v) || mref[v] == 0) continue;
                 deref_cut(v, cuts[v][best[v]]);
-                int bi = best[v], ba = 1 << 30;
+                int bi = best[v];
+                float ba = 1e30f;
                 float baf = 1e30f;
                 const int nc = (int)cuts[v].size() - 1;  // exclude trivial
                 for (int ci = 0; ci < nc; ++ci) {
-                    int a = ref_cut(v, cuts[v][ci]);
+                    float a = ref_cut(v, cuts[v][ci]);
                     deref_cut(v, cuts[v][ci]);
                     if (a < ba || (a == ba && cuts[v][ci].af < baf)) { ba = a; bi = ci; baf = cuts[v][ci].af; }
                 }
