@@ -363,6 +363,13 @@ int32_t es_map_stats_kc(const es_prog *prog, int32_t k, int32_t copies, int32_t 
                         int32_t *peak_live);
 int32_t es_map_eval_kc(const es_prog *prog, int32_t k, int32_t copies, uint64_t w0, uint64_t nw,
                        uint32_t *out_words);
+/* The K1 body alone (the LOP3/IMAD block es_emit_ptx_k splices into the
+ * skeleton; inputs %lo %hi %one, outputs %o [%c]) with the shared-memory
+ * overflow slots of es_spill.cpp applied for a register budget of
+ * `spill_budget` values (0: none) at `block_threads` threads.  slots = the
+ * shared-memory words per thread it needs (may be NULL).  buf NULL -> size. */
+int64_t es_emit_body_k(const es_prog *prog, int32_t k, int32_t spill_budget, int32_t block_threads,
+                       int32_t *slots, char *buf, int64_t cap);
 int64_t es_jit_check_k(const es_prog *prog, int32_t k, int32_t block_threads, int32_t *regs_per_thread,
                        int32_t *spill_bytes, char *log, int64_t log_cap);
 /* Split build without a GPU: the k-cofactor body cut into `parts` phases,

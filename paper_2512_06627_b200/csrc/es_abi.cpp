@@ -172,28 +172,25 @@ int32_t es_map_pipes_k(const es_prog *prog, int32_t k, int32_t *lop3, int32_t *i
     for (size_t p = 0; (p = body.find("mad.lo.s32 %esq", p)) != std::string::npos; ++p) ++ni;
     if (lop3) *lop3 = nl;
     if (imad) *imad = ni;
-    if (getenv("ES_LUTCAT")) {
-        const int N = (int)net.is_const.size();
-        std::vector<uint8_t> sel(N, 0);
-        for (int j = 6; j <= net.num_pis; ++j) sel[j] = !net.is_const[j];
-        int cat[4][4] = {};
-        for (const Lut &L : net.luts) {
-            bool u = true;
-            for (int q = 0; q < 3; ++q) u = u && sel[L.leaf[q]];
-            sel[L.node] = u;
-            int nd = 0, nu = 0;
-            for (int kk = 0; kk < 3; ++kk) {
-                bool dep = false;
-                for (int i = 0; i < 8; ++i)
-                    if (((L.tt >> i) & 1) != ((L.tt >> (i ^ (1 << kk))) & 1)) dep = true;
-                if (dep) { ++nd; nu += sel[L.leaf[kk]]; }
-            }
-            cat[nd][nu]++;
-        }
-        for (int a = 0; a < 4; ++a) for (int b = 0; b <= a; ++b)
-            if (cat[a][b]) fprintf(stderr, "deps=%d uniform=%d : %d\n", a, b, cat[a][b]);
-    }
     return ES_OK;
+}
+
+int64_t es_emit_body_k(const es_prog *prog, int32_t k, int32_t spill_budget, int32_t block_threads,
+                       int32_t *slots, char *buf, int64_t cap) {
+    LutNet net;
+    int rc = map_prog(prog, &net, k);
+    if (rc != ES_OK) return rc;
+    const bool multi = net.outs.size() > 1 || !net.cof_pis.empty();
+    std::string body = emit_body_ptx(net, multi ? std::vector<std::string>{"%o", "%c"} : std::vector<std::string>{"%o"},
+                                     "%lo", "%hi", "%one");
+    SpillStats ss;
+    if (spill_budget > 0) body = spill_body(body, spill_budget, block_threads > 0 ? block_threads : 256, &ss);
+    if (slots) *slots = ss.slots;
+    const int64_t n = (int64_t)body.size() + 1;
+    if (!buf) return n;
+    if (cap < n) { set_error("buffer too small"); return ES_E_BAD_ARG; }
+    memcpy(buf, body.c_str(), (size_t)n);
+    return n;
 }
 
 int32_t es_map_eval(const es_prog *prog, uint64_t w0, uint64_t nw, uint32_t *out_words) {

@@ -762,7 +762,7 @@ std::string emit_body_ptx(const LutNet &net, const std::vector<std::string> &out
     s << "{\n";
     if (!net.luts.empty()) s << ".reg .b32 %esq<" << net.luts.size() << ">;\n";
     if (!consts.empty()) s << ".reg .b32 %esk<" << consts.size() << ">;\n";
-    s << ".reg .b32 %esm<" << (P + 1) << ">;\n.reg .b32 %esb<" << N << ">;\n";
+    s << ".reg .b32 %esm<" << (P + 1) << ">;\n.reg .b32 %esp<" << (P + 1) << ">;\n.reg .b32 %esb<" << N << ">;\n";
     if (!coef.empty()) s << ".reg .b32 %esc<" << coef.size() << ">;\n";
     for (size_t k = 0; k < consts.size(); ++k) s << "mov.b32 %esk" << k << ", " << consts[k] << ";\n";
     if (imad) s << ".reg .b32 %esneg1;\nneg.s32 %esneg1, " << one << ";\n";
@@ -772,12 +772,13 @@ std::string emit_body_ptx(const LutNet &net, const std::vector<std::string> &out
         if (!pi_mask[j]) continue;
         const int bit = net.pi_bit[j];  // bit of the kernel's word index
         const std::string &src = bit < 32 ? wlo : whi;
+        // (through a temporary, so every %es value has one definition: es_spill.cpp)
         if (imad) {  // mask on the FMA pipe: bit to the sign by a multiply, spread by mul.hi
-            s << "mul.lo.u32 %esm" << j << ", " << src << ", " << (1u << (31 - (bit & 31))) << ";\n";
-            s << "mul.hi.s32 %esm" << j << ", %esm" << j << ", " << one << ";\n";
+            s << "mul.lo.u32 %esp" << j << ", " << src << ", " << (1u << (31 - (bit & 31))) << ";\n";
+            s << "mul.hi.s32 %esm" << j << ", %esp" << j << ", " << one << ";\n";
         } else {
-            s << "shl.b32 %esm" << j << ", " << src << ", " << (31 - (bit & 31)) << ";\n";
-            s << "shr.s32 %esm" << j << ", %esm" << j << ", 31;\n";
+            s << "shl.b32 %esp" << j << ", " << src << ", " << (31 - (bit & 31)) << ";\n";
+            s << "shr.s32 %esm" << j << ", %esp" << j << ", 31;\n";
         }
     }
     s << body.str();

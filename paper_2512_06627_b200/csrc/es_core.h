@@ -160,6 +160,21 @@ struct ImadPlan {
 // sel[v]: v is word-uniform (a PI >= 6 or a LUT over such nodes).
 bool plan_imad(const Lut &L, const std::vector<uint8_t> &sel, ImadPlan *pl);
 
+// Shared-memory overflow slots for the K1 body (es_spill.cpp): rewrite a
+// body from emit_body_ptx so that at most `budget` %es values are live in
+// registers anywhere in the schedule (Belady eviction); evicted values are
+// stored once (at the first eviction) to a per-thread slot of the dynamic
+// shared array es_slots (slot s of thread t at (s*threads + t)*4) and
+// reloaded before later uses.  Returns the body unchanged (slots 0) when
+// nothing has to move.
+struct SpillStats {
+    int slots = 0;   // shared-memory words per thread
+    int loads = 0;   // ld.shared per iteration
+    int stores = 0;  // st.shared per iteration
+    int peak = 0;    // register-resident values at the peak (<= budget)
+};
+std::string spill_body(const std::string &body, int budget, int threads, SpillStats *st);
+
 // Split build of the K1 body (es_split.cpp): the LUT sequence cut into
 // `parts` phases, each one a separately compiled PTX module holding one
 // device function, so ptxas runs on the phases in parallel and the linker

@@ -68,6 +68,20 @@ bool splice_body(const LutNet &net, int threads, std::string *ptx, std::string *
     }
     const std::vector<std::string> outs(a.begin(), a.begin() + nout);
     std::string body = emit_body_ptx(net, outs, a[nout], a[nout + 1], a[nout + 2]);
+    if (const char *e = getenv("ES_K1_SPILL_R")) {  // shared-memory overflow slots (es_spill.cpp)
+        SpillStats ss;
+        body = spill_body(body, atoi(e), threads, &ss);
+        if (ss.slots > 0) {
+            const size_t hdr = s.find('\n', s.find(".address_size 64")) + 1;
+            s.insert(hdr, ".extern .shared .align 16 .b8 es_slots[];\n");
+            at = s.find(marker);
+            eol = s.find('\n', at);
+            if (region_bytes) *region_bytes = ss.slots * threads * 4;
+        }
+        if (getenv("ES_VERBOSE"))
+            fprintf(stderr, "[es] K1 spill budget %s: %d slots, %d loads, %d stores per iteration\n", e, ss.slots,
+                    ss.loads, ss.stores);
+    }
     s.replace(at, eol - at, body);
     if (const char *m = getenv("ES_MAXNREG")) {  // experiment: register cap for occupancy
         const size_t mt = s.find(".maxntid");
@@ -318,7 +332,9 @@ int split_to_cubin(const std::string &skel, const std::vector<std::string> &phas
         const std::string nm = "es_mod" + std::to_string(m);
         lr = nvJitLinkAddData(h, NVJITLINK_INPUT_CUBIN, objs[m].data(), objs[m].size(), nm.c_str());
     }
+    const double tc = now_ms();
     if (lr == NVJITLINK_SUCCESS) lr = nvJitLinkComplete(h);
+    if (getenv("ES_VERBOSE")) fprintf(stderr, "[es] split link: create+add %.1f ms, complete %.1f ms\n", tc - tl, now_ms() - tc);
     if (lr != NVJITLINK_SUCCESS) {
         size_t n = 0;
         nvJitLinkGetErrorLogSize(h, &n);
