@@ -93,9 +93,11 @@ typedef struct es_run_opts {
     int32_t n_devices;      /* > 0: sweep on devices[0..n_devices) (one host thread each; an
                              * ordinal may repeat); 0: on `device` only */
     const int32_t *devices;
-    int32_t jit_parts;      /* K1 build: 0 = policy (cold runs split the body so ptxas compiles
-                             * its phases on parallel host threads), 1 = one straight-line body,
-                             * >= 2 = split into that many phases */
+    int32_t jit_parts;      /* K1 build: 0 = policy (cold runs write the body's SASS directly
+                             * or split it so ptxas compiles its phases on parallel host threads),
+                             * 1 = one straight-line body, >= 2 = split into that many phases,
+                             * -1 = direct SASS, no ptxas (es_sass.cpp; a program that does not
+                             * fit its template gets the split build) */
 } es_run_opts;
 
 /*
@@ -139,7 +141,8 @@ typedef struct es_result {
     int32_t phase2_cofactor_pis;/* cofactor PIs of the second phase's variant (phases == 2) */
     int32_t phase2_copies;      /* > 0: the second phase ran the first phase's cofactor set
                                  * restricted to copies 0..phase2_copies-1 */
-    int32_t jit_parts;          /* K1: phases of the kernel's split build (1: one body) */
+    int32_t jit_parts;          /* K1: phases of the kernel's split build (1: one body; -1: direct
+                                 * SASS, jit_opt 0) */
 } es_result;
 
 /*
@@ -370,6 +373,15 @@ int32_t es_map_eval_kc(const es_prog *prog, int32_t k, int32_t copies, uint64_t 
  * shared-memory words per thread it needs (may be NULL).  buf NULL -> size. */
 int64_t es_emit_body_k(const es_prog *prog, int32_t k, int32_t spill_budget, int32_t block_threads,
                        int32_t *slots, char *buf, int64_t cap);
+/* The direct-SASS K1 cubin for `prog` with k cofactor PIs (es_sass.cpp; no
+ * ptxas): the K1 skeleton ptxas compiled at build time with the program's
+ * own sm_100a body written over its placeholder function.  block_threads:
+ * 128 (k = 0) or 256 (k > 0).  stats (may be NULL): body instructions, LOP3,
+ * IMAD, peak registers, modelled issue cycles, and the template's word-index
+ * (lo, hi) and result (o0, o1) registers.  Returns the cubin's size (buf
+ * NULL) or < 0 when the program does not fit a template. */
+int64_t es_sass_cubin(const es_prog *prog, int32_t k, int32_t block_threads, int32_t *stats /* 9 */,
+                      char *buf, int64_t cap);
 int64_t es_jit_check_k(const es_prog *prog, int32_t k, int32_t block_threads, int32_t *regs_per_thread,
                        int32_t *spill_bytes, char *log, int64_t log_cap);
 /* Split build without a GPU: the k-cofactor body cut into `parts` phases,

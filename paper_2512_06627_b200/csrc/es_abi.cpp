@@ -193,6 +193,33 @@ int64_t es_emit_body_k(const es_prog *prog, int32_t k, int32_t spill_budget, int
     return n;
 }
 
+int64_t es_sass_cubin(const es_prog *prog, int32_t k, int32_t block_threads, int32_t *stats, char *buf,
+                      int64_t cap) {
+    LutNet net;
+    int rc = map_prog(prog, &net, k);
+    if (rc != ES_OK) return rc;
+    std::vector<char> cubin;
+    SassStats ss;
+    std::string err;
+    if (!sass_direct_cubin(net, block_threads, &cubin, &ss, &err)) { set_error(err); return ES_E_BAD_ARG; }
+    if (stats) {
+        stats[0] = ss.instrs;
+        stats[1] = ss.lop3;
+        stats[2] = ss.imad;
+        stats[3] = ss.regs_peak;
+        stats[4] = ss.cycles;
+        stats[5] = ss.reg_lo;
+        stats[6] = ss.reg_hi;
+        stats[7] = ss.reg_o0;
+        stats[8] = ss.reg_o1;
+    }
+    const int64_t n = (int64_t)cubin.size();
+    if (!buf) return n;
+    if (cap < n) { set_error("buffer too small"); return ES_E_BAD_ARG; }
+    memcpy(buf, cubin.data(), (size_t)n);
+    return n;
+}
+
 int32_t es_map_eval(const es_prog *prog, uint64_t w0, uint64_t nw, uint32_t *out_words) {
     return es_map_eval_k(prog, 0, w0, nw, out_words);
 }

@@ -357,6 +357,59 @@ int split_to_cubin(const std::string &skel, const std::vector<std::string> &phas
 
 int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std::string *err,
             int opt, int parts) {
+    if (opt == kJitDirect) {  // direct SASS (es_sass.cpp): no ptxas
+        auto t0 = now_ms();
+        std::vector<char> cubin;
+        SassStats ss;
+        std::string e2;
+        if (sass_direct_cubin(net, threads, &cubin, &ss, &e2)) {
+            const std::string img(cubin.begin(), cubin.end());
+            const uint64_t key = fnv1a(img) ^ 0xD1EC7ull << 40 ^ (uint64_t)(uint32_t)threads;
+            const uint64_t h2 = second_hash(img);
+            {
+                std::lock_guard<std::mutex> lk(g_jit_mu);
+                auto it = g_cache.find(key);
+                if (it != g_cache.end() && it->second->ptx_h2 == h2 && it->second->ptx_len == img.size()) {
+                    *out = it->second;
+                    *jit_ms = 0.0;
+                    return ES_OK;
+                }
+            }
+            JitKernel *k = new JitKernel();
+            k->threads = threads;
+            k->block = threads;
+            k->opt = kJitDirect;
+            k->parts = 1;
+            k->ptx_h2 = h2;
+            k->ptx_len = img.size();
+            cudaError_t e = cudaLibraryLoadData(&k->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+            if (e == cudaSuccess) e = cudaLibraryGetKernel(&k->kernel, k->lib, "es_k1");
+            if (e != cudaSuccess) {
+                *err = std::string("direct SASS load: ") + cudaGetErrorString(e);
+                if (k->lib) cudaLibraryUnload(k->lib);
+                delete k;
+                return ES_E_CUDA;
+            }
+            cudaFuncAttributes fa{};
+            if (cudaFuncGetAttributes(&fa, (const void *)k->kernel) == cudaSuccess) k->regs = fa.numRegs;
+            *jit_ms = now_ms() - t0;
+            k->jit_ms = *jit_ms;
+            if (getenv("ES_VERBOSE"))
+                fprintf(stderr, "[es] direct SASS: %d instrs (%d LOP3, %d IMAD), %d regs, %.2f ms\n", ss.instrs, ss.lop3,
+                        ss.imad, ss.regs_peak, *jit_ms);
+            std::lock_guard<std::mutex> lk(g_jit_mu);
+            auto it = g_cache.find(key);
+            if (it != g_cache.end()) g_uncached.push_back(k);
+            else g_cache[key] = k;
+            *out = k;
+            return ES_OK;
+        }
+        // no template for this variant, or the body does not fit one: the
+        // split build (cold) or the one-body -O1 build
+        const int P = (int)std::min(8u, std::max(1u, std::thread::hardware_concurrency() / 2));
+        opt = P >= 2 ? -P : 1;
+        parts = P >= 2 ? P : 1;
+    }
     std::string ptx;
     std::string skel;
     std::vector<std::string> phases;

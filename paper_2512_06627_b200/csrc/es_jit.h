@@ -11,6 +11,13 @@
 
 namespace es {
 
+// Build level of a direct-SASS kernel (es_sass.cpp): below every ptxas level
+// (a request for it is met by any compiled kernel, and a ptxas build of the
+// same program later replaces it -- tier-up).
+constexpr int kJitDirect = -1000;
+// Whether a direct-SASS template exists for this K1 variant.
+bool sass_template_exists(int threads, bool multi);
+
 struct JitKernel {
     cudaLibrary_t lib = nullptr;
     cudaKernel_t kernel = nullptr;
@@ -52,5 +59,18 @@ void parse_ptxas_info(const std::string &info, int *regs, int *spill_bytes);
 int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std::string *err,
             int opt = 3, int parts = 1);
 void jit_clear();
+
+// Direct-SASS K1 build (es_sass.cpp): the body lowered, scheduled, register-
+// allocated and encoded by the library and patched into a placeholder skeleton
+// that ptxas compiled at build time -- no ptxas at run time.  False (with
+// `err`) when the variant has no template or the body does not fit it.
+struct SassStats {
+    int instrs = 0;      // body instructions
+    int lop3 = 0, imad = 0;
+    int regs_peak = 0;   // simultaneously allocated registers
+    int cycles = 0;      // issue cycles of one iteration, one warp alone (model)
+    int reg_lo = 0, reg_hi = 0, reg_o0 = 0, reg_o1 = 0;  // the template's interface registers
+};
+bool sass_direct_cubin(const LutNet &net, int threads, std::vector<char> *cubin, SassStats *st, std::string *err);
 
 }  // namespace es

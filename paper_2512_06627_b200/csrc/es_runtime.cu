@@ -1532,6 +1532,14 @@ static double est_jit_ms(const LutNet &n, int opt = 3) {
     return (opt >= 3 ? 0.09 : 0.056) * std::max(1.0, p * p) * (double)n.luts.size();
 }
 constexpr double kO1Slowdown = 1.07;
+// Direct SASS (es_sass.cpp): ~2 ms from LUT network to loaded module, the
+// kernel slower than ptxas's by this factor (B200, mult16: k=0 12.0 vs 10.5 ms at
+// -O1, k=4 2.69 vs 2.35 ms at -O3)
+constexpr double kDirectJitMs = 2.0;
+static double direct_slowdown() {
+    static const double v = getenv("ES_DIRECT_SLOW") ? atof(getenv("ES_DIRECT_SLOW")) : 1.15;
+    return v;
+}
 
 // Split build (es_split.cpp, build level -P): ptxas on P phase modules in
 // parallel host threads, then one nvJitLink.  Fitted on the B200 box (16
@@ -1564,14 +1572,25 @@ static int k1_opt(const MappedProg &mp, const LutNet &n, const JitKernel *have, 
         *cost = (have && have->opt >= -parts ? 0.0 : est_split_jit_ms(n, parts)) + sweep * split_slowdown(parts);
         return -parts;
     }
+    const bool direct_ok = sass_template_exists(have ? have->block : o.block_threads > 0 ? o.block_threads
+                                                     : n.cof_pis.empty() ? 128 : 256,
+                                                 n.outs.size() > 1 || !n.cof_pis.empty());
+    if (o.jit_parts == -1) {  // forced direct SASS (falls back to a ptxas build when it does not fit)
+        *cost = (have ? 0.0 : kDirectJitMs) + sweep * direct_slowdown();
+        return kJitDirect;
+    }
     if (tput) { *cost = sweep; return 3; }
     const double reuse = 1.0 + mp.runs;  // doubling rule: expect as many more runs as so far
     int best = 3;
     *cost = 1e300;
-    for (int opt : {3, 1, -parts}) {
+    for (int opt : {3, 1, -parts, kJitDirect}) {
         if (opt == 0) continue;  // no split candidate
-        const double jit = (have && have->opt >= opt) ? 0.0 : opt < 0 ? est_split_jit_ms(n, parts) : est_jit_ms(n, opt);
-        const double slow = opt == 3 ? 1.0 : opt == 1 ? kO1Slowdown : kO1Slowdown * split_slowdown(parts);
+        if (opt == kJitDirect && (!direct_ok || o.jit_parts >= 1)) continue;
+        const double jit = (have && have->opt >= opt) ? 0.0
+                           : opt == kJitDirect ? kDirectJitMs
+                           : opt < 0 ? est_split_jit_ms(n, parts) : est_jit_ms(n, opt);
+        const double slow = opt == 3 ? 1.0 : opt == 1 ? kO1Slowdown
+                            : opt == kJitDirect ? direct_slowdown() : kO1Slowdown * split_slowdown(parts);
         const double c = jit + sweep * reuse * slow;
         if (c < *cost) { *cost = c; best = opt; }
     }
@@ -1686,8 +1705,8 @@ static int run_k1_job(MappedProg &mp, const LutNet &net, const es_run_opts &o, c
     r->jit_ms += jit_ms;
     r->regs_per_thread = pl.jk->regs;
     r->cofactor_pis = pl.cof_n;
-    r->jit_opt = pl.jk->opt < 0 ? 1 : pl.jk->opt;
-    r->jit_parts = pl.jk->parts;
+    r->jit_opt = pl.jk->opt == kJitDirect ? 0 : pl.jk->opt < 0 ? 1 : pl.jk->opt;
+    r->jit_parts = pl.jk->opt == kJitDirect ? -1 : pl.jk->parts;
     r->num_luts = (int)net.luts.size();
     r->n_devices = n_dev;
     r->phases = 1;
@@ -1936,7 +1955,8 @@ int run_batch_jit(int n_jobs, const es_prog *progs, const es_run_opts *opts, es_
     es_run_opts o{};
     if (opts) o = *opts;
     o.engine = ES_ENGINE_JIT;
-    if (o.jit_parts == 0) o.jit_parts = 1;  // the jobs already compile on parallel host threads
+    // the jobs already compile on parallel host threads: one-body ptxas builds,
+    // or direct SASS where the policy prefers it (jit_parts 0 keeps that open)
     const double t0 = now_ms();
     const double deadline = o.budget_s >= 0 && opts ? t0 + 1e3 * o.budget_s : -1.0;
     int sms = 0;

@@ -250,8 +250,8 @@ def _opts(device: int, engine: str, budget: float | None, cancel_addr, slice_ms:
     o.block_threads = block_threads
     o.flags = 0
     o.cofactor_pis = _cofactor_code(cofactor)
-    if jit_parts < 0:
-        raise ValueError("jit_parts must be >= 0")
+    if jit_parts < -1:
+        raise ValueError("jit_parts must be >= -1")
     o.jit_parts = jit_parts
     if devices:
         arr = (ctypes.c_int32 * len(devices))(*[int(d) for d in devices])
@@ -304,10 +304,12 @@ def run_exhaustive(p, workers: int = 1, budget: float | None = None, cancel=None
     word shared over NVLink stops every GPU once a smaller pattern cannot
     exist.  ``"all"`` = every visible GPU.  Default: ``device`` alone.
 
-    ``jit_parts`` (JIT engine): 0 lets the policy split a cold program's
-    kernel body into phases that ptxas compiles on parallel host threads
-    (es_split.cpp), 1 keeps one straight-line body, >= 2 forces that many
-    phases.
+    ``jit_parts`` (JIT engine): 0 lets the policy pick the build -- for a
+    cold program the direct-SASS kernel (es_sass.cpp: the body encoded by the
+    library itself, no ptxas) or a body split into phases that ptxas compiles
+    on parallel host threads (es_split.cpp), tiering up to ptxas -O3 as the
+    program is re-run; 1 keeps one straight-line ptxas body, >= 2 forces that
+    many phases, -1 forces direct SASS.
     """
     if workers < 1:
         raise ValueError("workers must be >= 1")

@@ -1,0 +1,173 @@
+"""Direct-SASS K1 build (csrc/es_sass.cpp, sass_template.py): no GPU needed.
+
+The library lowers a program to sm_100a machine code and patches it into a
+skeleton cubin that ptxas compiled at build time.  Here the patched cubin is
+disassembled with cuobjdump -- so the encodings are checked by NVIDIA's own
+decoder -- and the decoded body (from the placeholder's first slot to the
+branch to its RET) is interpreted over numpy words and compared with the CPU
+model of the mapped program (es.map_eval), for one-output bodies (128-thread
+skeleton) and cofactored multi-copy bodies (256-thread skeleton, first
+failing copy and its number).  Timing (stall counts) is only exercised on the
+GPU: tests/test_sass_gpu.py."""
+import ctypes
+import re
+import shutil
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_2512_06627_b200 import _native as N
+from paper_2512_06627_b200 import es
+from paper_2512_06627_b200 import miter as M
+
+M32 = np.uint64(0xFFFFFFFF)
+CUOBJDUMP = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+
+
+def sass_cubin(p, k, threads):
+    L = N.lib()
+    st = (ctypes.c_int32 * 9)()
+    n = N.check(L.es_sass_cubin(ctypes.byref(p.as_struct()), k, threads, st, None, 0))
+    buf = ctypes.create_string_buffer(n)
+    N.check(L.es_sass_cubin(ctypes.byref(p.as_struct()), k, threads, st, buf, n))
+    keys = ("instrs", "lop3", "imad", "regs_peak", "cycles", "lo", "hi", "o0", "o1")
+    return buf.raw[:n], dict(zip(keys, list(st)))
+
+
+def body_sass(cubin, tmp_path):
+    path = tmp_path / "k1_direct.cubin"
+    path.write_bytes(cubin)
+    out = subprocess.run([CUOBJDUMP, "-sass", str(path)], capture_output=True, text=True, check=True).stdout
+    ins = [(int(a, 16), t.strip()) for a, t in re.findall(r"/\*([0-9a-f]{4,6})\*/\s+([^;]*);", out)]
+    call = [t for a, t in ins if t.startswith("CALL.REL")]
+    assert len(call) == 1
+    start = int(call[0].split()[-1], 16)
+    body = []
+    for a, t in ins:
+        if a < start:
+            continue
+        if t.startswith("BRA"):
+            ret = int(t.split()[-1], 16)
+            assert any(a2 == ret and t2.startswith("RET.REL") for a2, t2 in ins)
+            return body
+        body.append(t)
+    raise AssertionError("no branch to the RET after the body")
+
+
+def interpret(body, regs):
+    R = dict(regs)
+    T = len(next(iter(regs.values())))
+
+    def opnd(x):
+        x = x.strip()
+        if x == "RZ":
+            return np.zeros(T, np.uint64)
+        if x.startswith("R"):  # (the return-address registers are not modelled: 0)
+            return R.get(int(x[1:]), np.zeros(T, np.uint64))
+        v = int(x, 16) if "0x" in x else int(x)
+        return np.full(T, v & 0xFFFFFFFF, np.uint64)
+
+    def s32(v):
+        return v.astype(np.uint32).astype(np.int32).astype(np.int64)
+
+    for t in body:
+        op, _, rest = t.partition(" ")
+        ops = [o.strip() for o in rest.split(",")]
+        if op == "NOP":
+            continue
+        d = int(ops[0][1:])
+        if op == "LOP3.LUT":
+            a, b, c = (opnd(o) for o in ops[1:4])
+            lut = int(ops[4], 16)
+            r = np.zeros(T, np.uint64)
+            for i in range(8):
+                if (lut >> i) & 1:
+                    r |= (a if i & 4 else ~a) & (b if i & 2 else ~b) & (c if i & 1 else ~c)
+            R[d] = r & M32
+        elif op.startswith("IMAD"):
+            assert op in ("IMAD", "IMAD.SHL", "IMAD.MOV", "IMAD.IADD"), op
+            a, b, c = (s32(opnd(o)) for o in ops[1:4])
+            R[d] = ((a * b + c) & 0xFFFFFFFF).astype(np.uint64)
+        elif op == "SHF.R.S32.HI":
+            assert ops[1] == "RZ" and ops[2] == "0x1f"
+            R[d] = ((s32(opnd(ops[3])) >> 31) & 0xFFFFFFFF).astype(np.uint64)
+        elif op == "MOV":
+            R[d] = opnd(ops[1])
+        else:
+            raise AssertionError(f"unexpected instruction in the body: {t}")
+    return R
+
+
+def expand(wk, cof_pis, copy):
+    """Full word index of kernel word wk in cofactor copy `copy`."""
+    x = int(wk)
+    for b, j in enumerate(sorted(cof_pis)):
+        s = j - 6
+        x = ((x >> s) << (s + 1)) | (x & ((1 << s) - 1)) | (((copy >> b) & 1) << s)
+    return x
+
+
+def check(x, k, threads, tmp_path, n_words=64, seed=0):
+    p = es.compile_program(x)
+    cubin, st = sass_cubin(p, k, threads)
+    body = body_sass(cubin, tmp_path)
+    assert len(body) == st["instrs"]
+    ms = es.map_stats(p, k)
+    cof = ms["cofactor_pis"]
+    kbits = max(p.num_pis - 5 - len(cof), 0)
+    rng = np.random.default_rng(seed)
+    wk = rng.integers(0, 1 << kbits, size=n_words, dtype=np.uint64) if kbits else np.zeros(n_words, np.uint64)
+    R = interpret(body, {st["lo"]: wk & M32, st["hi"]: wk >> np.uint64(32)})
+    if not cof:
+        want = np.array([es.map_eval(p, int(w), 1, k)[0] for w in wk], np.uint64)
+        np.testing.assert_array_equal(R[st["o0"]], want)
+        return st, want
+    fw_want, fc_want = [], []
+    for w in wk:
+        fw = fc = 0
+        for c in range(1 << len(cof)):
+            v = int(es.map_eval(p, expand(w, cof, c), 1, k)[0])
+            if v:
+                fw, fc = v, c
+                break
+        fw_want.append(fw)
+        fc_want.append(fc)
+    fw_want = np.array(fw_want, np.uint64)
+    np.testing.assert_array_equal(R[st["o0"]], fw_want)
+    hit = fw_want != 0
+    np.testing.assert_array_equal(R[st["o1"]][hit], np.array(fc_want, np.uint64)[hit])
+    return st, fw_want
+
+
+@pytest.mark.parametrize("name,x", [
+    ("adder8", M.gen_adder_miter(8)),
+    ("mult8", M.gen_multiplier_miter(8, "array", "booth")),
+    ("mult8_fault", M.flip_gate(M.gen_multiplier_miter(8, "array", "booth"), 300)),
+    ("mult12", M.gen_multiplier_miter(12, "array", "wallace")),
+])
+def test_direct_sass_single_output(name, x, tmp_path):
+    st, out = check(x, 0, 128, tmp_path)
+    assert st["lop3"] > 0
+    if name.endswith("fault"):
+        assert out.any()
+
+
+@pytest.mark.parametrize("k", [1, 3, 4])
+def test_direct_sass_cofactor_copies(k, tmp_path):
+    x = M.flip_gate(M.gen_multiplier_miter(8, "array", "booth"), 300)
+    st, out = check(x, k, 256, tmp_path, n_words=16)
+    assert st["imad"] > 0 and out.any()
+
+
+def test_direct_sass_mult16_fits_templates(tmp_path):
+    """The bench miter's k=0 and k=4 bodies fit the templates' registers and
+    slots and decode to the expected instruction mix."""
+    p = es.compile_program(M.gen_multiplier_miter(16, "array", "booth"))
+    for k, t in ((0, 128), (4, 256)):
+        cubin, st = sass_cubin(p, k, t)
+        pipes = es.map_pipes(p, k)
+        # every LUT is one LOP3 or IMAD; PI masks, coefficients and the fold add a few
+        assert st["lop3"] + st["imad"] >= pipes["lop3"] + pipes["imad"]
+        assert st["regs_peak"] <= 232
+    check(M.gen_multiplier_miter(16, "array", "booth"), 0, 128, tmp_path, n_words=8)
