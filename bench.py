@@ -569,7 +569,8 @@ def measure_sweep(local: int) -> dict:
     """the whole sweep with the ES engine (sweep.py:292-409)
     on the config-2/3 multiplier miters -- K3 simulation and classes, C++
     extraction, batched K2 / parallel-JIT K1 pair checks, final obligation.
-    Cold = first sweep of the miter in this process (JIT included)."""
+    Cold = first sweep of the miter in this process (JIT included); warm =
+    the best of three repeats."""
     from paper_2512_06627_b200 import miter as M
     from paper_2512_06627_b200.sweep import SweepConfig, sweep
 
@@ -579,10 +580,16 @@ def measure_sweep(local: int) -> dict:
         t = time.perf_counter()
         r = sweep(x, SweepConfig(device=local))
         cold = 1e3 * (time.perf_counter() - t)
-        t = time.perf_counter()
-        sweep(x, SweepConfig(device=local))
-        warm = 1e3 * (time.perf_counter() - t)
-        out[name] = {"verdict": r.verdict, "cold_ms": cold, "warm_ms": warm,
+        # repeat sweeps: the second one still pays the policy's tier-up (deeper
+        # cofactor variants mapped and built because the sub-miters re-run);
+        # warm = the best of three repeats (kernels built and tiered up)
+        reps = []
+        for _ in range(3):
+            t = time.perf_counter()
+            sweep(x, SweepConfig(device=local))
+            reps.append(1e3 * (time.perf_counter() - t))
+        warm = min(reps)
+        out[name] = {"verdict": r.verdict, "cold_ms": cold, "warm_ms": warm, "repeat_ms": reps,
                      "pairs_checked": r.stats["engine_calls"], "merges": r.stats["merges"],
                      "reference_sweep_s_1_thread_build_container": {"mult12": 6.78, "mult16": 376.89}[name]}
     return out

@@ -1536,6 +1536,7 @@ constexpr double kO1Slowdown = 1.07;
 // kernel slower than ptxas's by this factor (B200, mult16: k=0 12.0 vs 10.5 ms at
 // -O1, k=4 2.69 vs 2.35 ms at -O3)
 constexpr double kDirectJitMs = 2.0;
+constexpr int kDirectMaxLive = 215;
 static double direct_slowdown() {
     static const double v = getenv("ES_DIRECT_SLOW") ? atof(getenv("ES_DIRECT_SLOW")) : 1.15;
     return v;
@@ -1548,7 +1549,11 @@ static double direct_slowdown() {
 // module load and per-module ptxas start-up), and the sweep runs 1 + 0.09 P
 // times the one-body kernel's time (shared-memory slot traffic at the cuts).
 // mult16 k=0: J1 95 ms -> P=8 50 ms, sweep 10.5 -> 18.0 ms.
+// es_run_opts.flags bit set by run_batch_jit: its jobs already compile on
+// parallel host threads, so none of them may split (internal, not in the ABI)
+constexpr int32_t kFlagNoSplit = 1 << 30;
 static int split_parts(const LutNet &n, const es_run_opts &o) {
+    if (o.flags & kFlagNoSplit) return 0;
     int P = o.jit_parts >= 2 ? o.jit_parts : 0;
     if (const char *e = getenv("ES_JIT_PARTS")) P = atoi(e);
     if (P == 0) P = (int)std::min(8u, std::max(1u, std::thread::hardware_concurrency() / 2));
@@ -1572,7 +1577,10 @@ static int k1_opt(const MappedProg &mp, const LutNet &n, const JitKernel *have, 
         *cost = (have && have->opt >= -parts ? 0.0 : est_split_jit_ms(n, parts)) + sweep * split_slowdown(parts);
         return -parts;
     }
-    const bool direct_ok = sass_template_exists(have ? have->block : o.block_threads > 0 ? o.block_threads
+    // direct SASS: a template for the variant and a live set that fits its
+    // ~230 registers with the masks and coefficients (mult16 k=4: 212 LUT
+    // values fit, k=5's 446 do not)
+    const bool direct_ok = n.peak_live <= kDirectMaxLive && sass_template_exists(have ? have->block : o.block_threads > 0 ? o.block_threads
                                                      : n.cof_pis.empty() ? 128 : 256,
                                                  n.outs.size() > 1 || !n.cof_pis.empty());
     if (o.jit_parts == -1) {  // forced direct SASS (falls back to a ptxas build when it does not fit)
@@ -1620,15 +1628,27 @@ static int choose_cofactors(MappedProg &mp, const es_run_opts &o, int sms, int *
     // latency mode: a short sweep is JIT-bound; don't even map the variants
     if (!tput && sweep0 * (1 + mp.runs) < 0.1 * est_jit_ms(net0)) return fixed(0);
     int best = 0, worse = 0;
-    double best_cost = 1e300;
+    double best_cost = 1e300, prev_cost = 0, map_ms = 0;
     for (int k = 0; k <= kmax; ++k) {
+        const double tm = now_ms();
         const LutNet &n = mp.variant(k);
+        const double this_map = now_ms() - tm;  // 0 when the variant was mapped before
         if ((int)n.cof_pis.size() != k) break;  // fewer candidate PIs than k
         const int ok = k1_opt(mp, n, mp.jk(n, k1_threads(o, k)), P, sms, tput, &cost, o);
         if (cost < best_cost) { best_cost = cost; best = k; *opt = ok; worse = 0; }
         // latency mode: the JIT term grows with k, so two deeper variants that
         // do not pay end the search (mapping k=3..5 costs ~40 ms on mult16)
         else if (!tput && ++worse >= 2) break;
+        if (!tput && k > 0 && this_map > 0) {
+            // mapping the next variant costs about twice this one (the
+            // expansion doubles); stop when that exceeds what it can save
+            // at the rate the last step saved (direct SASS makes the JIT
+            // term flat, so host mapping time is what bounds the search)
+            map_ms = this_map;
+            const double gain = std::max(0.0, prev_cost - cost);
+            if (2.0 * map_ms > 0.5 * gain) break;
+        }
+        prev_cost = cost;
     }
     return best;
 }
@@ -1956,7 +1976,8 @@ int run_batch_jit(int n_jobs, const es_prog *progs, const es_run_opts *opts, es_
     if (opts) o = *opts;
     o.engine = ES_ENGINE_JIT;
     // the jobs already compile on parallel host threads: one-body ptxas builds,
-    // or direct SASS where the policy prefers it (jit_parts 0 keeps that open)
+    // or direct SASS where the policy prefers it, never split builds
+    o.flags |= kFlagNoSplit;
     const double t0 = now_ms();
     const double deadline = o.budget_s >= 0 && opts ? t0 + 1e3 * o.budget_s : -1.0;
     int sms = 0;
