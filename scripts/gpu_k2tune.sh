@@ -1,13 +1,6 @@
 cd "${GRAFT_REPO_ROOT:-.}"; mkdir -p gpurun_out
-O=gpurun_out/k2tune.txt; : > $O
-run() { echo "$*" >> $O; env "$@" timeout 300 python scripts/probe_cones.py >> $O 2>&1; }
-run ES_K2_BIGPEN=2.5
-run ES_K2_BIGPEN=1.5
-run ES_K2_BIGPEN=2.0
-run ES_K2_BIGPEN=3.0
-run ES_K2_MIDPEN=1.0
-run ES_K2_MIDPEN=1.3
-run ES_K2_MAXSLOTS=144
-run ES_K2_MAXSLOTS=208
-run ES_K2_LANES=1
-run ES_K2_LANES=4
+O=gpurun_out/k2chain.txt; : > $O
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+timeout 300 python scripts/probe_cones.py >> $O 2>&1
+ES_K2_LANES=4 timeout 300 python scripts/probe_cones.py >> $O 2>&1
+timeout 900 python -m pytest tests/test_config4_gpu.py tests/test_cones.py tests/test_k2prog.py tests/test_gpu_parity.py -x -q -m gpu >> $O 2>&1
