@@ -453,6 +453,44 @@ def measure_cones(steps: int, warmup: int, rank: int = 0, world: int = 1, count:
     return out
 
 
+def measure_cones_eq(steps: int, warmup: int, cpu_seconds: float = 0.0) -> dict:
+    """The EQ-heavy config-4 variant: the candidate pairs
+    the sweep sends after its 64-word simulation of the configs[2] miter
+    alone (cones.sweep_round_batch, sweep.py:313-345) -- mostly EQ cones that
+    must be swept completely.  Same measurement as measure_cones, every
+    result checked against the oracle."""
+    from paper_2512_06627_b200 import cones, shard
+
+    t = time.perf_counter()
+    batch = cones.sweep_round_batch()
+    build_ms = 1e3 * (time.perf_counter() - t)  # simulate, classes, extract, compile, K2 programs
+    for _ in range(warmup):
+        res = batch.run_arrays()
+    dev_ms, wall_ms = [], []
+    for _ in range(steps):
+        t = time.perf_counter()
+        res = batch.run_arrays()
+        wall_ms.append(1e3 * (time.perf_counter() - t))
+        dev_ms.append(float(res["device_ms"].max()))
+    work, eq, neq = cones_work(batch, res)
+    dev_s = statistics.mean(dev_ms) * 1e-3
+    model = k2_smem_model(batch, res)
+    smem_bps, _ = shard.smem_peak(0)
+    roof = {"bound": "smem", "unit": "GB/s", "peak": smem_bps / 1e9, "achieved": model["bytes"] / dev_s / 1e9,
+            "achieved_def": "as for config 4 (k2_smem_model)", "groups": model["groups"]}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    out = {"workload": "config 4, EQ-heavy: the 16x16 array-vs-Booth miter's own candidate pairs after a "
+                       "64-word simulation (sweep.py:313-345), distinct 14-24-PI cones, one batched launch",
+           "jobs": len(batch), "eq": eq, "neq": neq, "gate_patterns": work, "roofline": roof,
+           "device_ms": statistics.mean(dev_ms), "e2e_ms": statistics.mean(wall_ms),
+           "host_build_ms": build_ms, "e2e_with_build_ms": statistics.mean(wall_ms) + build_ms,
+           "value": work / dev_s, "e2e_value": work / (statistics.mean(wall_ms) * 1e-3),
+           "oracle_check": cones_oracle_check(batch, res)}
+    if cpu_seconds > 0:
+        out["cpu_baseline"] = cones_cpu_baseline(batch, cpu_seconds)
+    return out
+
+
 def _ref_cone_worker(args):
     """One process of the N-process reference harness: es_check(workers=1) on
     its share of the cones (the reference's own call, es.py:342)."""
@@ -928,6 +966,7 @@ def run_local(args, devs: list[int]) -> None:
         extras["cones"] = {"workload": "config 4: ~10k candidate-pair cones (14-24 PIs) of "
                                        "16x16 multiplier miters, one batched launch",
                            **measure_cones(5, 2, cpu_seconds=cs)}
+        extras["cones_eq"] = measure_cones_eq(5, 2, cpu_seconds=cs)
         line["other_configs"] = extras
     print(json.dumps(line), flush=True)
 

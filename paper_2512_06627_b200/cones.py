@@ -389,6 +389,40 @@ def config4_batch(count: int = 10_000, lo: int = 14, hi: int = 24, seed: int = 0
     return head
 
 
+def sweep_round_batch(miter=None, words: int = 64, lo: int = 14, hi: int = 24, seed: int = 0,
+                      threads: int = 0) -> NativeBatch:
+    """The EQ-heavy variant of config 4: the candidate pairs the
+    sweep itself sends after its 64-word random simulation (sweep.py:313-345)
+    of ONE miter (default the configs[2] array-vs-Booth 16x16), every pair of
+    a class whose cone has lo..hi PIs, distinct cones only.  A 64-word
+    simulation leaves few false candidates, so most of these are EQ and must
+    be swept completely."""
+    from . import miter as M
+
+    m = miter if miter is not None else M.gen_multiplier_miter(16, "array", "booth")
+    sup = support_masks(m)
+    pairs = []
+    for cls in candidate_classes(m, words, seed):
+        nodes = [n for n, _ in cls if sup[n].bit_count() <= hi]
+        pol = dict(cls)
+        for i in range(len(nodes)):
+            for j in range(i + 1, len(nodes)):
+                a, b = nodes[i], nodes[j]
+                if lo <= (sup[a] | sup[b]).bit_count() <= hi:
+                    pairs.append((a, b, pol[a] != pol[b]))
+    nb = NativeBatch(m, pairs, threads=threads)
+    tab = nb.table()
+    seen, keep = set(), []
+    for i in range(len(nb)):
+        h = int(tab["hash"][i])
+        if lo <= tab["num_pis"][i] <= hi and h not in seen:
+            seen.add(h)
+            keep.append(i)
+    nb.select(keep)
+    nb.prepare(threads)
+    return nb
+
+
 def config4_cones(count: int = 10_000, lo: int = 14, hi: int = 24, seed: int = 0):
     """The config-4 workload as Python SubMiters (tests, small counts)."""
     subs = []

@@ -121,3 +121,17 @@ def test_config4_batch_vs_single_runs(gpu):
         sm = b.submiter(i)
         r = es.run_exhaustive(es.compile_program(sm.circuit), engine="jit")
         assert (r.verdict, r.witness_index) == (res[i].verdict, res[i].witness_index), i
+
+
+def test_sweep_round_batch_shape():
+    """The EQ-heavy config-4 variant's cones: distinct, 14-24 PIs, from the
+    configs[2] miter's own 64-word candidate classes."""
+    import numpy as np
+
+    from paper_2512_06627_b200 import cones
+
+    b = cones.sweep_round_batch()
+    tab = b.table()
+    assert len(b) > 100
+    assert tab["num_pis"].min() >= 14 and tab["num_pis"].max() <= 24
+    assert len(np.unique(tab["hash"])) == len(b)

@@ -47,3 +47,14 @@ def test_config4_repeatable(gpu, batch, oracle_results):
     """Three back-to-back batched verdicts (programs cached after the first)."""
     for _ in range(3):
         assert not _compare(batch, batch.run_arrays(), oracle_results)
+
+
+def test_config4_eq_heavy_sweep_round(gpu):
+    """The EQ-heavy variant: the sweep's own candidate pairs
+    after a 64-word simulation of the configs[2] miter (sweep.py:313-345),
+    mostly EQ cones swept to exhaustion, every result against the oracle."""
+    b = cones.sweep_round_batch()
+    refs = O.run_packed_batch([b.packed(i) for i in range(len(b))])
+    rec = b.run_arrays()
+    assert not _compare(b, rec, refs)
+    assert int((rec["verdict"] == 0).sum()) > len(b) // 2  # EQ-heavy
