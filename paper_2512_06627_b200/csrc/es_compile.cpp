@@ -488,14 +488,31 @@ void map_luts(const Dag &dag, LutNet *net) {
             const int C = (int)outs.size();
             int kb = 0;
             while ((1 << kb) < C) ++kb;
-            std::vector<int32_t> rev;
-            for (int c = 0; c < (1 << kb); ++c) {
-                int r = 0;
-                for (int b = 0; b < kb; ++b) r |= ((c >> b) & 1) << (kb - 1 - b);
-                if (r < C) rev.push_back(outs[r]);
-            }
-            std::vector<int> o2 = dfs(rev);
-            if (peak_of(o2) < peak_of(order)) order.swap(o2);
+            // Generalised: the copies are visited as the leaves of a binary
+            // tree that splits on the cofactor PIs in some order (bit-reversed
+            // = split on PI 0 first).  Logic depending on a set S of cofactor
+            // PIs stays live while the copies matching S's values are visited,
+            // so the split order decides the live set; try every order of up
+            // to 4 PIs (24) and keep the smallest peak.  (5 PIs, 120 orders:
+            // mult16 k=5 446 -> 322 live values, but a k=5 body is ~150 KB of
+            // SASS and instruction-fetch bound -- ncu stall no_instruction
+            // 2.98 per issue, 4.5 ms vs 2.35 at k=4 -- so not worth the
+            // mapping time.)
+            std::vector<int> perm(kb);
+            for (int b = 0; b < kb; ++b) perm[b] = b;
+            int best_peak = peak_of(order);
+            do {
+                std::vector<int32_t> seq;
+                for (int c = 0; c < (1 << kb); ++c) {
+                    // the c-th leaf: bit t of c (MSB first) is the value of PI perm[t]
+                    int r = 0;
+                    for (int t = 0; t < kb; ++t) r |= ((c >> (kb - 1 - t)) & 1) << perm[t];
+                    if (r < C) seq.push_back(outs[r]);
+                }
+                std::vector<int> o2 = dfs(seq);
+                const int pk = peak_of(o2);
+                if (pk < best_peak) { best_peak = pk; order.swap(o2); }
+            } while (kb <= 4 && std::next_permutation(perm.begin(), perm.end()));
         }
         if (getenv("ES_LIST_SCHED")) {
             // experiment: greedy list scheduling, prefer the ready node that frees most
