@@ -107,3 +107,28 @@ def test_device_resident(gpu):
     torch.cuda.synchronize()
     assert np.array_equal(d_out.cpu().numpy().view(np.uint64), O.simulate(m, pw))
     ds.close()
+
+
+def test_large_drives(gpu):
+    """Drives of >= 16,384 words (one lane per word, L2-sized word tiles):
+    node matrices, classes and the device-resident path equal the numpy
+    oracle's, including odd word counts (a partial last CTA)."""
+    import torch
+    rng = random.Random(11)
+    for k in range(3):
+        x = random_xag(rng.randint(6, 30), rng.randint(200, 2500), 500 + k)
+        pw = sim.random_pi_words(x.num_pis, rng.choice([16384, 16411, 20000]), k)
+        assert np.array_equal(sim.simulate(x, pw), O.simulate(x, pw))
+    m = M.gen_multiplier_miter(16, "array", "booth")
+    pw = sim.random_pi_words(m.num_pis, 16389, 4)
+    want = O.simulate(m, pw)
+    assert np.array_equal(sim.simulate(m, pw), want)
+    assert [c.members for c in sim.pe_classes(m, pi_words=pw)] == O.pe_classes(want)
+    nn = 1 + m.num_pis + len(m.gates)
+    d_pi = torch.from_numpy(pw.view(np.int64)).cuda()
+    d_out = torch.empty((nn, pw.shape[1]), dtype=torch.int64, device="cuda")
+    ds = sim.DeviceSim(m)
+    ds.run(d_pi.data_ptr(), pw.shape[1], d_out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert np.array_equal(d_out.cpu().numpy().view(np.uint64), want)
+    ds.close()
