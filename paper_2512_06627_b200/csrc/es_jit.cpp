@@ -355,6 +355,8 @@ int split_to_cubin(const std::string &skel, const std::vector<std::string> &phas
     return ES_OK;
 }
 
+thread_local bool t_batch_jit = false;
+
 int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std::string *err,
             int opt, int parts) {
     if (opt == kJitDirect) {  // direct SASS (es_sass.cpp): no ptxas
@@ -405,8 +407,11 @@ int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std
             return ES_OK;
         }
         // no template for this variant, or the body does not fit one: the
-        // split build (cold) or the one-body -O1 build
-        const int P = (int)std::min(8u, std::max(1u, std::thread::hardware_concurrency() / 2));
+        // split build (a cold single run) or the one-body -O1 build (a batch,
+        // whose jobs already compile on parallel threads)
+        if (getenv("ES_VERBOSE"))
+            fprintf(stderr, "[es] direct SASS not possible (%s, peak live %d): ptxas build\n", e2.c_str(), net.peak_live);
+        const int P = t_batch_jit ? 1 : (int)std::min(8u, std::max(1u, std::thread::hardware_concurrency() / 2));
         opt = P >= 2 ? -P : 1;
         parts = P >= 2 ? P : 1;
     }

@@ -59,6 +59,9 @@ void parse_ptxas_info(const std::string &info, int *regs, int *spill_bytes);
 int jit_get(const LutNet &net, int threads, JitKernel **out, double *jit_ms, std::string *err,
             int opt = 3, int parts = 1);
 void jit_clear();
+// set on the threads of a batched K1 run (run_batch_jit): a failed direct-SASS
+// build falls back to one ptxas body, never a split build
+extern thread_local bool t_batch_jit;
 
 // Direct-SASS K1 build (es_sass.cpp): the body lowered, scheduled, register-
 // allocated and encoded by the library and patched into a placeholder skeleton

@@ -1407,6 +1407,7 @@ struct MappedProg {
     std::map<std::pair<VariantKey, int>, JitKernel *> jks;
     std::map<int, std::vector<int32_t>> ranks;  // max_pi -> the cheapest word PIs (<= max_pi), by fanout
     int runs = 0;                    // K1 runs so far (the reuse estimate of the auto policy)
+    int batch_k = -1, batch_opt = 0; // the depth / build a batch's compile thread chose (run_batch_jit)
     std::shared_ptr<K2Prog> k2;      // interpreter program (its own cofactor depth), on demand
     bool k2_searched = false;        // built with the cofactor-depth search
     int k2_runs = 0;
@@ -1589,13 +1590,21 @@ static int k1_opt(const MappedProg &mp, const LutNet &n, const JitKernel *have, 
     }
     if (tput) { *cost = sweep; return 3; }
     const double reuse = 1.0 + mp.runs;  // doubling rule: expect as many more runs as so far
+    // a batch compiles its jobs on every host thread while the device sweeps
+    // earlier ones: a direct build (~1-3 ms) costs the device ~1/threads of
+    // its time; a ptxas build (0.1-1 s) would still hold up the jobs queued
+    // behind it, so a batch only takes one for a variant direct SASS cannot
+    // hold, at its full cost
+    const bool batch = (o.flags & kFlagNoSplit) != 0;
+    const double jit_scale = batch ? 1.0 / std::max(1u, std::thread::hardware_concurrency()) : 1.0;
     int best = 3;
     *cost = 1e300;
     for (int opt : {3, 1, -parts, kJitDirect}) {
         if (opt == 0) continue;  // no split candidate
         if (opt == kJitDirect && (!direct_ok || o.jit_parts >= 1)) continue;
+        if (batch && direct_ok && opt != kJitDirect && !(have && have->opt >= opt)) continue;
         const double jit = (have && have->opt >= opt) ? 0.0
-                           : opt == kJitDirect ? kDirectJitMs
+                           : opt == kJitDirect ? jit_scale * kDirectJitMs
                            : opt < 0 ? est_split_jit_ms(n, parts) : est_jit_ms(n, opt);
         const double slow = opt == 3 ? 1.0 : opt == 1 ? kO1Slowdown
                             : opt == kJitDirect ? direct_slowdown() : kO1Slowdown * split_slowdown(parts);
@@ -1626,7 +1635,9 @@ static int choose_cofactors(MappedProg &mp, const es_run_opts &o, int sms, int *
     const LutNet &net0 = mp.variant(0);
     const double sweep0 = est_sweep_ms(net0, P, sms);
     // latency mode: a short sweep is JIT-bound; don't even map the variants
-    if (!tput && sweep0 * (1 + mp.runs) < 0.1 * est_jit_ms(net0)) return fixed(0);
+    // (not in a batch: its compiles and mappings overlap the device)
+    const bool batch = (o.flags & kFlagNoSplit) != 0;
+    if (!tput && !batch && sweep0 * (1 + mp.runs) < 0.1 * est_jit_ms(net0)) return fixed(0);
     int best = 0, worse = 0;
     double best_cost = 1e300, prev_cost = 0, map_ms = 0;
     for (int k = 0; k <= kmax; ++k) {
@@ -1643,8 +1654,10 @@ static int choose_cofactors(MappedProg &mp, const es_run_opts &o, int sms, int *
             // mapping the next variant costs about twice this one (the
             // expansion doubles); stop when that exceeds what it can save
             // at the rate the last step saved (direct SASS makes the JIT
-            // term flat, so host mapping time is what bounds the search)
-            map_ms = this_map;
+            // term flat, so host mapping time is what bounds the search).
+            // A batch maps its jobs on every host thread while the device
+            // sweeps: its mapping costs the device 1/threads of its time.
+            map_ms = this_map * (batch ? 1.0 / std::max(1u, std::thread::hardware_concurrency()) : 1.0);
             const double gain = std::max(0.0, prev_cost - cost);
             if (2.0 * map_ms > 0.5 * gain) break;
         }
@@ -1956,11 +1969,21 @@ int run_one(const es_prog *prog, const es_run_opts *opts, es_result *out) {
         std::lock_guard<std::mutex> lk(mp->mu);
         const double tc = now_ms();
         int opt = 3;
-        const int k = choose_cofactors(*mp, o, c->sms * (int)cs.size(), &opt);
+        // a batch job runs what its compile thread chose and built (searching
+        // again here would find the variants mapped and pick anew, compiling
+        // on this thread while the device waits)
+        const bool prechosen = t_batch_jit && mp->batch_k >= 0;
+        const int k = prechosen ? mp->batch_k : choose_cofactors(*mp, o, c->sms * (int)cs.size(), &opt);
+        if (prechosen) opt = mp->batch_opt;
+        mp->batch_k = -1;
         const LutNet &kn = mp->variant(k);
         out->compile_ms += now_ms() - tc;
         rc = run_k1_job(*mp, kn, o, cs, deadline, opt, out);
         mp->runs++;
+        if (getenv("ES_VERBOSE"))
+            fprintf(stderr, "[es] K1 run: %d PIs, %d gates, k=%d build %d, jit %.2f ms, device %.3f ms, %s\n",
+                    prog->num_pis, G, k, opt, out->jit_ms, out->device_ms,
+                    out->verdict == ES_EXHAUSTED_ZERO ? "EQ" : out->verdict == ES_COUNTEREXAMPLE ? "CEX" : "stop");
     }
     out->wall_ms = now_ms() - t0;
     return rc;
@@ -1994,6 +2017,7 @@ int run_batch_jit(int n_jobs, const es_prog *progs, const es_run_opts *opts, es_
         rcv.notify_all();
     };
     auto warm = [&]() {
+        t_batch_jit = true;
         const bool dev_ok = cudaSetDevice(o.device) == cudaSuccess;
         for (;;) {
             const int i = next.fetch_add(1);
@@ -2004,6 +2028,8 @@ int run_batch_jit(int n_jobs, const es_prog *progs, const es_run_opts *opts, es_
                     std::lock_guard<std::mutex> lk(mp->mu);
                     int opt = 3;
                     const int k = choose_cofactors(*mp, o, sms * (int)run_devices(o).size(), &opt);
+                    mp->batch_k = k;  // the run on the main thread uses this decision
+                    mp->batch_opt = opt;
                     const LutNet &net = mp->variant(k);
                     const int threads = k1_threads(o, k);
                     JitKernel *&have = mp->jk(net, threads);
@@ -2029,7 +2055,9 @@ int run_batch_jit(int n_jobs, const es_prog *progs, const es_run_opts *opts, es_
         }
         es_run_opts oi = o;
         if (deadline >= 0) oi.budget_s = std::max(0.0, (deadline - now_ms()) * 1e-3);
+        t_batch_jit = true;
         rc = run_one(&progs[i], &oi, &outs[i]);
+        t_batch_jit = false;
     }
     next.store(n_jobs);  // on an error, stop compiling what will not run
     for (auto &x : th) x.join();

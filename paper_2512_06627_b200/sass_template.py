@@ -27,6 +27,10 @@ import subprocess
 
 CHAIN = 20000      # chain instructions (the slot capacity is ~CHAIN + 2 * LIVE)
 LIVE = 230         # values the placeholder keeps live (register clobber set)
+# placeholder sizes built per skeleton: the library patches the smallest one
+# the body fits, because the driver's module load time grows with the cubin
+# (a sweep loads one module per sub-miter on 16 host threads)
+CHAINS = (1500, 5000, 20000)
 
 
 # marker constants: the placeholder XORs its inputs and outputs with them, so
@@ -34,7 +38,7 @@ LIVE = 230         # values the placeholder keeps live (register clobber set)
 MARK_LO, MARK_HI, MARK_O0, MARK_O1 = 0x11111111, 0x22222222, 0x33333333, 0x44444444
 
 
-def _placeholder_func(multi: bool) -> str:
+def _placeholder_func(multi: bool, chain: int = CHAIN) -> str:
     rng = random.Random(12345)
     L = [".func (.param .b64 es_pr) es_body(.param .b32 es_pw0, .param .b32 es_pw1, .param .b32 es_pw2)", "{",
          f".reg .b32 %a<{LIVE}>;", ".reg .b32 %lo, %hi, %one, %v, %u, %o0, %o1;", ".reg .b64 %r;",
@@ -44,7 +48,7 @@ def _placeholder_func(multi: bool) -> str:
         L.append(f"lop3.b32 %a{i}, %u, %a{i - 1}, %a{i - 2}, {1 + i % 250};")
         L.append(f"add.u32 %u, %u, %a{i};")
     L.append("mov.b32 %v, %u;")
-    for i in range(CHAIN):
+    for i in range(chain):
         L.append(f"lop3.b32 %v, %v, %a{(i * 7) % LIVE}, %a{(i * 13 + 5) % LIVE}, {rng.randrange(1, 255)};")
     for i in range(LIVE):
         L.append(f"xor.b32 %v, %v, %a{i};")
@@ -55,7 +59,7 @@ def _placeholder_func(multi: bool) -> str:
     return "\n".join(L) + "\n"
 
 
-def placeholder_ptx(skeleton_ptx: str, multi: bool) -> str:
+def placeholder_ptx(skeleton_ptx: str, multi: bool, chain: int = CHAIN) -> str:
     """The skeleton with its ES_BODY marker replaced by a call to es_body."""
     m = re.search(r"// ES_BODY ([^\n]*)\n", skeleton_ptx)
     assert m, "skeleton without ES_BODY"
@@ -70,7 +74,7 @@ def placeholder_ptx(skeleton_ptx: str, multi: bool) -> str:
     call.append("}")
     body = skeleton_ptx[:m.start()] + "\n".join(call) + "\n" + skeleton_ptx[m.end():]
     hdr = body.index("\n", body.index(".address_size 64")) + 1
-    return body[:hdr] + _placeholder_func(multi) + body[hdr:]
+    return body[:hdr] + _placeholder_func(multi, chain) + body[hdr:]
 
 
 def _sections(cubin: bytes):
@@ -172,30 +176,35 @@ def analyse(cubin_path: str, cuobjdump: str, multi: bool) -> dict:
 
 
 def build_templates(build_dir: str, variants, ptxas: str, cuobjdump: str, arch: str = "sm_100a") -> str:
-    """Compile the placeholder skeletons; write k1_sass_templates.inc."""
-    out = []
+    """Compile the placeholder skeletons (every variant x every size in
+    CHAINS); write k1_sass_templates.inc with the table kSassTemplates."""
+    out, names = [], []
     for threads, multi in variants:
         skel = open(os.path.join(build_dir, f"k1_skeleton_{threads}_{int(multi)}.ptx")).read()
-        ptx = os.path.join(build_dir, f"k1_sass_{threads}_{int(multi)}.ptx")
-        cub = os.path.join(build_dir, f"k1_sass_{threads}_{int(multi)}.cubin")
-        open(ptx, "w").write(placeholder_ptx(skel, multi))
-        subprocess.run([ptxas, f"-arch={arch}", "-O3", ptx, "-o", cub], check=True, capture_output=True)
-        info = analyse(cub, cuobjdump, multi)
-        data = no_opportunistic_finalization(open(cub, "rb").read())
-        text_off = _elf_text_offset(data, ".text.es_k1")
-        # the RET encoding (its register field is rewritten to ret_reg at run time)
-        ret_off = text_off + info["end"]
-        lo, hi = struct.unpack_from("<QQ", data, ret_off)
-        clob = [0, 0, 0, 0]
-        for r in info["clobber"]:
-            clob[r // 64] |= 1 << (r % 64)
-        nm = f"kSass{threads}_{int(multi)}"
-        out.append(f"static const unsigned char {nm}_cubin[] = {{{','.join(str(b) for b in data)}}};\n")
-        out.append(
-            f"static const SassTemplate {nm} = {{{nm}_cubin, sizeof({nm}_cubin), {threads}, {int(multi)}, "
-            f"{text_off}ull, {info['start']}ull, {info['end']}ull, {info['ret_reg']}, {info['ret_pair']}, "
-            f"{info['lo']}, {info['hi']}, {info['o0']}, {info['o1']}, {lo}ull, {hi}ull, "
-            f"{{{', '.join(f'{c}ull' for c in clob)}}}}};\n")
+        for chain in CHAINS:
+            tag = f"{threads}_{int(multi)}_{chain}"
+            ptx = os.path.join(build_dir, f"k1_sass_{tag}.ptx")
+            cub = os.path.join(build_dir, f"k1_sass_{tag}.cubin")
+            open(ptx, "w").write(placeholder_ptx(skel, multi, chain))
+            subprocess.run([ptxas, f"-arch={arch}", "-O3", ptx, "-o", cub], check=True, capture_output=True)
+            info = analyse(cub, cuobjdump, multi)
+            data = no_opportunistic_finalization(open(cub, "rb").read())
+            text_off = _elf_text_offset(data, ".text.es_k1")
+            # the RET encoding (its register field is rewritten to ret_reg at run time)
+            ret_off = text_off + info["end"]
+            lo, hi = struct.unpack_from("<QQ", data, ret_off)
+            clob = [0, 0, 0, 0]
+            for r in info["clobber"]:
+                clob[r // 64] |= 1 << (r % 64)
+            nm = f"kSass{tag}"
+            names.append(nm)
+            out.append(f"static const unsigned char {nm}_cubin[] = {{{','.join(str(b) for b in data)}}};\n")
+            out.append(
+                f"static const SassTemplate {nm} = {{{nm}_cubin, sizeof({nm}_cubin), {threads}, {int(multi)}, "
+                f"{text_off}ull, {info['start']}ull, {info['end']}ull, {info['ret_reg']}, {info['ret_pair']}, "
+                f"{info['lo']}, {info['hi']}, {info['o0']}, {info['o1']}, {lo}ull, {hi}ull, "
+                f"{{{', '.join(f'{c}ull' for c in clob)}}}}};\n")
+    out.append("static const SassTemplate *const kSassTemplates[] = {" + ", ".join(f"&{n}" for n in names) + "};\n")
     inc = os.path.join(build_dir, "k1_sass_templates.inc")
     with open(inc, "w") as fh:
         fh.write("// generated by sass_template.py (build time) -- do not edit\n")
