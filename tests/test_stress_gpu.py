@@ -1,5 +1,5 @@
 """Randomised parity on the GPU (a short run of scripts/stress_parity.py):
-every engine and cofactor / ptxas-level policy returns the oracle's
+every engine and cofactor / build policy (direct SASS included) returns the oracle's
 canonical minimum-index witness on fault miters with deep witnesses."""
 import importlib.util
 import os
@@ -24,7 +24,7 @@ def test_random_fault_miters_all_engines(gpu, seed):
         _, ref_w, _ = O.min_witness(O.compile_program(x))
         n_neq += ref_w is not None
         p = es.compile_program(x)
-        for engine, cof in SP.MODES:
-            r = es.run_exhaustive(p, engine=engine, cofactor=cof)
-            assert r.witness_index == ref_w, (name, x.num_pis, engine, cof, r.witness_index, ref_w)
+        for engine, cof, parts in SP.MODES:  # (direct-SASS builds first: jit_parts -1)
+            r = es.run_exhaustive(p, engine=engine, cofactor=cof, jit_parts=parts)
+            assert r.witness_index == ref_w, (name, x.num_pis, engine, cof, parts, r.witness_index, ref_w)
     assert n_neq > 0
