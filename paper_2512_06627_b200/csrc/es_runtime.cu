@@ -798,7 +798,9 @@ static int sweep_k1(const K1Plan &pl, int G, const es_run_opts &o, const std::ve
         CK(cudaSetDevice(cs[d]->dev));
         cs[d]->h_pin[0] = init_best;
         CK(cudaMemcpyAsync(cs[d]->d_best, cs[d]->h_pin, 8, cudaMemcpyHostToDevice, cs[d]->stream));
-        CK(cudaStreamSynchronize(cs[d]->stream));  // armed before any device launches
+        // armed before any device launches: one device's launches follow the
+        // copy in stream order; other devices' streams need the host to wait
+        if (n > 1) CK(cudaStreamSynchronize(cs[d]->stream));
     }
     // slice size (in this device's chunk slots) from a conservative rate estimate
     const bool sliced = deadline >= 0 || o.cancel_flag != nullptr;
@@ -918,7 +920,8 @@ static int sweep_k1(const K1Plan &pl, int G, const es_run_opts &o, const std::ve
         for (auto &t : th) t.join();
     }
     if (err.load() != ES_OK) { set_error(err_msg); return err.load(); }
-    if (shared) {  // final value of the shared word (every device has synchronised)
+    if (shared && n > 1) {  // final value of the shared word (every device has synchronised;
+                            // one device's last slice already copied it back)
         CK(cudaSetDevice(cs[0]->dev));
         CK(cudaMemcpy(cs[0]->h_pin, cs[0]->d_best, 8, cudaMemcpyDeviceToHost));
         lower(cs[0]->h_pin[0]);
@@ -1437,16 +1440,32 @@ struct MappedProg {
         return jks[{{n.cof_pis, (int)n.copy_ids.size()}, k1_slot(threads)}];
     }
 };
+// Hash of every program array, 8 bytes a step in four independent lanes (a
+// warm call hashes mult16's 54 KB of arrays; byte-wise FNV-1a took ~70 us).
+// A hit is confirmed against the stored arrays, so the hash only routes.
 static uint64_t prog_hash(const es_prog &p) {
-    uint64_t h = 1469598103934665603ull;
+    uint64_t lane[4] = {0x9E3779B97F4A7C15ull, 0xC2B2AE3D27D4EB4Full, 0x165667B19E3779F9ull, 0x27D4EB2F165667C5ull};
     auto mix = [&](const void *d, size_t n) {
         const unsigned char *b = (const unsigned char *)d;
-        for (size_t i = 0; i < n; ++i) { h ^= b[i]; h *= 1099511628211ull; }
+        size_t i = 0;
+        for (; i + 32 <= n; i += 32)
+            for (int q = 0; q < 4; ++q) {
+                uint64_t w;
+                std::memcpy(&w, b + i + 8 * q, 8);
+                lane[q] = (lane[q] ^ w) * 0x9FB21C651E98DF25ull;
+                lane[q] ^= lane[q] >> 29;
+            }
+        uint64_t t = n;
+        for (; i < n; ++i) t = (t ^ b[i]) * 1099511628211ull;
+        lane[0] = (lane[0] ^ t) * 0x9FB21C651E98DF25ull;
+        lane[0] ^= lane[0] >> 29;
     };
     mix(&p.num_instrs, 4); mix(&p.num_registers, 4); mix(&p.num_pis, 4);
     const size_t n = (size_t)p.num_instrs;
     mix(p.op, n); mix(p.dst, 4 * n); mix(p.src0, 4 * n); mix(p.neg0, n);
     mix(p.src1, 4 * n); mix(p.neg1, n); mix(p.pi, 4 * n);
+    uint64_t h = lane[0];
+    for (int q = 1; q < 4; ++q) h = (h ^ lane[q]) * 0x9FB21C651E98DF25ull, h ^= h >> 31;
     return h;
 }
 
@@ -1462,17 +1481,32 @@ static std::vector<uint8_t> prog_sig(const es_prog &p) {
     return v;
 }
 
+// p's arrays equal a stored signature (compared in place, no copy)
+static bool sig_equal(const es_prog &p, const std::vector<uint8_t> &sig) {
+    const size_t n = (size_t)p.num_instrs;
+    if (sig.size() != 12 + n * 19) return false;
+    const uint8_t *d = sig.data();
+    auto same = [&](const void *s, size_t b) {
+        const bool e = std::memcmp(d, s, b) == 0;
+        d += b;
+        return e;
+    };
+    return same(&p.num_instrs, 4) && same(&p.num_registers, 4) && same(&p.num_pis, 4) && same(p.op, n) &&
+           same(p.dst, 4 * n) && same(p.src0, 4 * n) && same(p.neg0, n) && same(p.src1, 4 * n) &&
+           same(p.neg1, n) && same(p.pi, 4 * n);
+}
+
 static std::mutex g_mapped_mu;
 static std::vector<std::pair<uint64_t, std::shared_ptr<MappedProg>>> g_mapped;
 
 static int get_mapped(const es_prog &p, std::shared_ptr<MappedProg> *out) {
     const uint64_t key = prog_hash(p);
-    std::vector<uint8_t> sig = prog_sig(p);
     {
         std::lock_guard<std::mutex> lk(g_mapped_mu);
         for (auto &kv : g_mapped)  // hash hit + identical arrays (no collision risk)
-            if (kv.first == key && kv.second->sig == sig) { *out = kv.second; return ES_OK; }
+            if (kv.first == key && sig_equal(p, kv.second->sig)) { *out = kv.second; return ES_OK; }
     }
+    std::vector<uint8_t> sig = prog_sig(p);
     Dag dag;
     std::string err;
     int rc = build_dag(p, &dag, &err);
