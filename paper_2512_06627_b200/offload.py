@@ -68,10 +68,11 @@ def analytic_es_time(num_gates: int, num_pis: int, alpha: float = ALPHA, beta: i
 
 def device_es_time(num_gates: int, num_pis: int) -> float:
     """This engine's estimate on one B200 (seconds): the better of the
-    interpreter (~1e14 gate-patterns/s with cofactor copies) and the JIT
-    kernel (~0.15 s of compile, then ~1.2e15 gate-patterns/s)."""
+    interpreter (~1e14 gate-patterns/s with cofactor copies) and the K1
+    kernel built directly as SASS (~2 ms from program to loaded module,
+    then ~1.2e15 gate-patterns/s at k = 0 -- DESIGN §3 K1-direct)."""
     work = float(num_gates) * 2.0 ** num_pis
-    return min(work / 1e14, 0.15 + work / 1.2e15)
+    return min(work / 1e14, 0.002 + work / 1.2e15)
 
 
 def selection_plan(cost_sat: float, cost_es: float, n: int) -> EnginePlan:
