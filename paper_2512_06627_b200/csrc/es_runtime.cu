@@ -1939,9 +1939,11 @@ int run_one(const es_prog *prog, const es_run_opts *opts, es_result *out) {
     int engine = o.engine;
     if (engine == ES_ENGINE_AUTO) {
         // The interpreter needs no JIT, the straight-line kernel sweeps ~40x
-        // faster once compiled.  Estimates (round-1 B200 measurements): K2
-        // ~5e13 gate-patterns/s (mult12: 2.5e10 in 0.45 ms), K1 ~2e15 plus
-        // ~0.02 ms of launch, ptxas ~0.04 ms per gate at -O1 (mult16: 95 ms).
+        // faster once compiled.  Estimates (B200 measurements): K2 ~5e13
+        // gate-patterns/s (mult12: 2.5e10 in 0.45 ms), K1 ~2e15 plus ~0.02 ms
+        // of launch; building K1 costs mapping (~1.2 us per gate: mult16 3.3
+        // ms) plus the direct-SASS build (~1-2 ms; ptxas, 0.04 ms per gate at
+        // -O1, only when the body does not fit a template).
         // Big sweeps go to K1; small ones to K1 when it is already compiled
         // or, in throughput mode, when its sweep is faster (JIT ignored);
         // otherwise by the doubling rule on the program's run count, so a
@@ -1956,7 +1958,7 @@ int run_one(const es_prog *prog, const es_run_opts *opts, es_result *out) {
             reuse += mp->runs + mp->k2_runs;
         }
         const bool tput = o.cofactor_pis == ES_COFACTOR_THROUGHPUT;
-        const double jit_ms = compiled ? 0.0 : 0.04 * G;
+        const double jit_ms = compiled ? 0.0 : kDirectJitMs + 0.0012 * G;
         if (work >= 4e12) engine = ES_ENGINE_JIT;
         else if (tput || compiled) engine = k1_ms < k2_ms ? ES_ENGINE_JIT : ES_ENGINE_INTERP;
         else engine = jit_ms + k1_ms * reuse < k2_ms * reuse ? ES_ENGINE_JIT : ES_ENGINE_INTERP;
