@@ -359,6 +359,14 @@ void emit_k2_lanes(const Dag &dag, const Outs &outs, const std::vector<int> &ord
             kp->gates.push_back(rec[h]);
         }
     }
+    // every gate record of a multi-lane step stores (es_k2d has no store
+    // test): results nobody reads, and the NOP lanes', go to one dummy slot
+    const int dummy = top++;
+    for (K2Gate &g : kp->gates)
+        if (!(g.ctl & K2_OUT) && !(g.ctl & K2_STORE)) {
+            g.d = (uint32_t)dummy;
+            kp->stores++;
+        }
     kp->num_slots = top;
 }
 

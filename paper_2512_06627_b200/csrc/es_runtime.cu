@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(128) es_k2d(const K2Job *__restrict__ jobs,
                     }
 #pragma unroll
                 for (int h = 0; h < L; ++h)
-                    if (c[h].w & K2_STORE) sts<W>(pd[h], acc[h]);
+                    sts<W>(pd[h], acc[h]);  // (unread results go to the program's dummy slot)
                 advance();
             }
             unsigned any = 0;
