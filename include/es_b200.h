@@ -402,6 +402,10 @@ int64_t es_jit_check(const es_prog *prog, int32_t block_threads, int32_t *regs_p
  * lane-op evaluates one 2/3-input gate over 32 patterns).  The roofline
  * denominator of the bench. */
 int32_t es_alu_peak(int32_t device, double *lane_ops_per_s, double *ms);
+/* Measured FMA-pipe integer peak: lane-IMAD operations per second (the K1
+ * body's x*S+T LUTs and their coefficients; the second integer pipe K1 is
+ * bound by). */
+int32_t es_fma_peak(int32_t device, double *lane_ops_per_s, double *ms);
 /* Measured shared-memory load bandwidth of the whole GPU (bytes/s): the
  * denominator of the K2 interpreter's shared-memory roofline. */
 int32_t es_smem_peak(int32_t device, double *bytes_per_s, double *ms);

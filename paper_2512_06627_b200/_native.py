@@ -33,7 +33,7 @@ ENGINES = {"auto": ENGINE_AUTO, "jit": ENGINE_JIT, "interp": ENGINE_INTERP}
 # every symbol include/es_b200.h declares
 EXPORTS = ("es_compile", "es_run", "es_run_batch", "es_session_open", "es_session_geometry",
            "es_session_launch", "es_session_close", "es_map_stats", "es_map_pipes", "es_map_eval", "es_k2_stats", "es_k2_eval",
-           "es_emit_ptx", "es_jit_check", "es_alu_peak", "es_smem_peak", "es_batch_extract", "es_batch_size",
+           "es_emit_ptx", "es_jit_check", "es_alu_peak", "es_fma_peak", "es_smem_peak", "es_batch_extract", "es_batch_size",
            "es_batch_info", "es_batch_table", "es_batch_k2_stats", "es_batch_k2_traffic", "es_xag_eval", "es_batch_xag", "es_batch_select", "es_batch_run", "es_batch_merge", "es_batch_free",
            "es_ipc_alloc", "es_ipc_open", "es_ipc_close", "es_word_write", "es_word_read",
            "es_map_stats_k", "es_map_pipes_k", "es_map_eval_k", "es_map_stats_kc", "es_map_eval_kc", "es_emit_ptx_k", "es_emit_body_k", "es_sass_cubin", "es_jit_check_k", "es_jit_check_split",
@@ -175,6 +175,9 @@ def lib():
         L.es_smem_peak.argtypes = [ctypes.c_int32, ctypes.POINTER(ctypes.c_double),
                                    ctypes.POINTER(ctypes.c_double)]
         L.es_smem_peak.restype = ctypes.c_int32
+        L.es_fma_peak.argtypes = [ctypes.c_int32, ctypes.POINTER(ctypes.c_double),
+                                  ctypes.POINTER(ctypes.c_double)]
+        L.es_fma_peak.restype = ctypes.c_int32
         L.es_alu_peak.argtypes = [ctypes.c_int32, ctypes.POINTER(ctypes.c_double),
                                   ctypes.POINTER(ctypes.c_double)]
         L.es_alu_peak.restype = ctypes.c_int32

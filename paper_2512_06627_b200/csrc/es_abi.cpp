@@ -31,6 +31,7 @@ int session_launch(void *s, void *stream, uint64_t *best_dev, uint64_t chunk_beg
 void session_close(void *s);
 void runtime_shutdown();
 int alu_peak(int dev, double *lane_ops_per_s, double *ms_out);
+int fma_peak(int dev, double *lane_ops_per_s, double *ms_out);
 int smem_peak(int dev, double *bytes_per_s, double *ms_out);
 int ipc_alloc(int dev, void **ptr, unsigned char *handle);
 int ipc_open(int dev, const unsigned char *handle, void **ptr);
@@ -514,6 +515,11 @@ int64_t es_aiger_write(int32_t num_pis, int32_t num_gates, const uint8_t *kind, 
 int32_t es_alu_peak(int32_t device, double *lane_ops_per_s, double *ms) {
     if (!lane_ops_per_s) return ES_E_BAD_ARG;
     return alu_peak(device, lane_ops_per_s, ms);
+}
+
+int32_t es_fma_peak(int32_t device, double *lane_ops_per_s, double *ms) {
+    if (!lane_ops_per_s) return ES_E_BAD_ARG;
+    return fma_peak(device, lane_ops_per_s, ms);
 }
 
 int32_t es_smem_peak(int32_t device, double *bytes_per_s, double *ms) {

@@ -479,6 +479,29 @@ __global__ void __launch_bounds__(256) es_alu_peak_kernel(unsigned *sink, int it
 
 int alu_peak(int dev, double *lane_ops_per_s, double *ms_out);
 
+// FMA-pipe integer peak: 8 independent IMAD chains per thread (the K1 body's
+// x*S+T LUTs and coefficients run there; B200 issues IMAD at half the LOP3
+// rate, so the two integer pipes bound K1 together).  The multiplier is
+// opaque (from the seed) so ptxas cannot strength-reduce the chains.
+__global__ void __launch_bounds__(256) es_imad_peak_kernel(unsigned *sink, int iters, unsigned seed) {
+    unsigned a0 = seed ^ threadIdx.x, a1 = a0 * 3u, a2 = a0 * 5u, a3 = a0 * 7u;
+    unsigned a4 = a0 * 11u, a5 = a0 * 13u, a6 = a0 * 17u, a7 = a0 * 19u;
+    const unsigned m = seed | 0x10001u;
+#define ES_MAD(d, x, y) asm volatile("mad.lo.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(x), "r"(m), "r"(y))
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            ES_MAD(a0, a0, a1); ES_MAD(a1, a1, a2); ES_MAD(a2, a2, a3); ES_MAD(a3, a3, a4);
+            ES_MAD(a4, a4, a5); ES_MAD(a5, a5, a6); ES_MAD(a6, a6, a7); ES_MAD(a7, a7, a0);
+        }
+    }
+#undef ES_MAD
+    const unsigned r = a0 ^ a1 ^ a2 ^ a3 ^ a4 ^ a5 ^ a6 ^ a7;
+    if (r == 0x9E3779B9u) sink[0] = r;
+}
+
+int fma_peak(int dev, double *lane_ops_per_s, double *ms_out);
+
 // *w = min(*w, *v): folds the other devices' minimum into a device-local word
 // (multi-GPU sweep without peer access)
 __global__ void es_word_min_kernel(unsigned long long *w, const unsigned long long *v) { atomicMin(w, *v); }
@@ -2216,6 +2239,27 @@ void session_close(void *sp) {
     cudaSetDevice(s->dev);
     if (s->d_counter) cudaFree(s->d_counter);
     delete s;
+}
+
+int fma_peak(int dev, double *lane_ops_per_s, double *ms_out) {
+    CtxLease lease;
+    int rc = lease.acquire(dev);
+    if (rc != ES_OK) return rc;
+    Ctx *c = lease.c;
+    const int threads = 256, iters = 2048;
+    const int grid = c->sms * 8;
+    unsigned *sink = c->d_counter + 8;
+    es_imad_peak_kernel<<<grid, threads, 0, c->stream>>>(sink, 64, 1u);  // warm-up
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(c->ev_start, c->stream));
+    es_imad_peak_kernel<<<grid, threads, 0, c->stream>>>(sink, iters, 1u);
+    CK(cudaEventRecord(c->ev_stop, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, c->ev_start, c->ev_stop));
+    *lane_ops_per_s = (double)grid * threads * (double)iters * 64.0 / (ms * 1e-3);
+    if (ms_out) *ms_out = ms;
+    return ES_OK;
 }
 
 int alu_peak(int dev, double *lane_ops_per_s, double *ms_out) {

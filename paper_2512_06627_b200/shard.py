@@ -150,6 +150,13 @@ def alu_peak(device: int = 0) -> tuple[float, float]:
     return v.value, ms.value
 
 
+def fma_peak(device: int = 0) -> tuple[float, float]:
+    """Measured lane-IMAD/s of the device's FMA pipe (and the ms)."""
+    v, ms = ctypes.c_double(), ctypes.c_double()
+    N.check(N.lib().es_fma_peak(device, ctypes.byref(v), ctypes.byref(ms)))
+    return v.value, ms.value
+
+
 def smem_peak(device: int = 0) -> tuple[float, float]:
     """Measured shared-memory load bytes/s of the device (and the ms)."""
     v, ms = ctypes.c_double(), ctypes.c_double()
