@@ -737,10 +737,17 @@ std::string emit_body_ptx(const LutNet &net, const std::vector<std::string> &out
         if (a == 0 && b == -1) {  // -bit = mask
             const std::string m = name(u);
             body << "mov.b32 " << r << ", " << m << ";\n";
-        } else {
+        } else if (a == 0 && b == 1) {
             const std::string bt = bit_of(u);  // may emit; keep it out of the line below
-            if (a == 0 && b == 1) body << "mov.b32 " << r << ", " << bt << ";\n";
-            else body << "mad.lo.s32 " << r << ", " << bt << ", " << (b - a) << ", " << a << ";\n";
+            body << "mov.b32 " << r << ", " << bt << ";\n";
+        } else {
+            // a + (b - a) * bit = mask * (a - b) + a straight from the mask (no
+            // separate bit), the factor an opaque register so the multiply
+            // stays an IMAD on the FMA pipe
+            const std::string m = name(u);
+            const int f = a - b;  // in {-2, -1, 1, 2}
+            const std::string fr = f == -1 ? "%esneg1" : f == 1 ? one : f == 2 ? "%escf2" : "%escg2";
+            body << "mad.lo.s32 " << r << ", " << m << ", " << fr << ", " << a << ";\n";
         }
         return r;
     };
@@ -782,7 +789,9 @@ std::string emit_body_ptx(const LutNet &net, const std::vector<std::string> &out
     s << ".reg .b32 %esm<" << (P + 1) << ">;\n.reg .b32 %esp<" << (P + 1) << ">;\n.reg .b32 %esb<" << N << ">;\n";
     if (!coef.empty()) s << ".reg .b32 %esc<" << coef.size() << ">;\n";
     for (size_t k = 0; k < consts.size(); ++k) s << "mov.b32 %esk" << k << ", " << consts[k] << ";\n";
-    if (imad) s << ".reg .b32 %esneg1;\nneg.s32 %esneg1, " << one << ";\n";
+    if (imad)
+        s << ".reg .b32 %esneg1, %escf2, %escg2;\nneg.s32 %esneg1, " << one << ";\nadd.s32 %escf2, " << one << ", "
+          << one << ";\nneg.s32 %escg2, %escf2;\n";
     if (multi)
         s << ".reg .pred %espz;\n.reg .b32 %est;\nmov.b32 " << outs[0] << ", 0;\nmov.b32 " << outs[1] << ", 0;\n";
     for (int j = 6; j <= P; ++j) {

@@ -77,7 +77,7 @@ def run_body(text, wlo, whi, threads, slots):
             R[d] = (val(ops[1]).astype(np.uint64) << np.uint64(int(ops[2])) & M32).astype(np.uint32)
         elif op == "shr.s32":
             R[d] = (sval(ops[1]) >> int(ops[2])).astype(np.uint32)
-        elif op == "add.u32":
+        elif op in ("add.u32", "add.s32"):
             R[d] = ((val(ops[1]).astype(np.uint64) + val(ops[2]).astype(np.uint64)) & M32).astype(np.uint32)
         elif op == "setp.eq.b32":
             pred[d] = val(ops[1]) == val(ops[2])
