@@ -36,7 +36,7 @@ EXPORTS = ("es_compile", "es_run", "es_run_batch", "es_session_open", "es_sessio
            "es_emit_ptx", "es_jit_check", "es_alu_peak", "es_fma_peak", "es_smem_peak", "es_batch_extract", "es_batch_size",
            "es_batch_info", "es_batch_table", "es_batch_k2_stats", "es_batch_k2_traffic", "es_xag_eval", "es_batch_xag", "es_batch_select", "es_batch_run", "es_batch_merge", "es_batch_free",
            "es_ipc_alloc", "es_ipc_open", "es_ipc_close", "es_word_write", "es_word_read",
-           "es_map_stats_k", "es_map_pipes_k", "es_map_eval_k", "es_map_stats_kc", "es_map_eval_kc", "es_emit_ptx_k", "es_emit_body_k", "es_sass_cubin", "es_jit_check_k", "es_jit_check_split",
+           "es_map_stats_k", "es_map_pipes_k", "es_map_eval_k", "es_map_stats_kc", "es_map_eval_kc", "es_emit_ptx_k", "es_emit_body_k", "es_sass_cubin", "es_k4_cubin", "es_jit_check_k", "es_jit_check_split",
            "es_k2_eval_k", "es_k2_cofactor_pis", "es_batch_prepare",
            "es_sim", "es_sim_ones", "es_sim_device", "es_sim_prog_free", "es_sim_classes", "es_sim_levels",
            "es_aiger_parse", "es_detect_xors", "es_xag_size", "es_xag_read", "es_xag_free",
@@ -161,6 +161,8 @@ def lib():
         L.es_emit_ptx_k.restype = ctypes.c_int64
         L.es_sass_cubin.argtypes = [ctypes.POINTER(EsProg), _I, _I, _P, ctypes.c_char_p, ctypes.c_int64]
         L.es_sass_cubin.restype = ctypes.c_int64
+        L.es_k4_cubin.argtypes = [ctypes.POINTER(EsProg), _I, _P, _P, ctypes.c_char_p, ctypes.c_int64]
+        L.es_k4_cubin.restype = ctypes.c_int64
         L.es_emit_body_k.argtypes = [ctypes.POINTER(EsProg), _I, _I, _I, _P, ctypes.c_char_p, ctypes.c_int64]
         L.es_emit_body_k.restype = ctypes.c_int64
         L.es_jit_check_k.argtypes = [ctypes.POINTER(EsProg), _I, _I, _P, _P, ctypes.c_char_p,

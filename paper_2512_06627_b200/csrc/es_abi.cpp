@@ -221,6 +221,38 @@ int64_t es_sass_cubin(const es_prog *prog, int32_t k, int32_t block_threads, int
     return n;
 }
 
+int64_t es_k4_cubin(const es_prog *progs, int32_t n, const int32_t *cof_k, int32_t *stats, char *buf,
+                    int64_t cap) {
+    if (!progs || n <= 0 || n > k4_max_bodies()) { set_error("bad argument"); return ES_E_BAD_ARG; }
+    std::vector<std::vector<uint64_t>> code(n);
+    SassStats ss;
+    for (int i = 0; i < n; ++i) {
+        LutNet net;
+        int rc = map_prog(&progs[i], &net, cof_k ? cof_k[i] : 0);
+        if (rc != ES_OK) return rc;
+        std::string err;
+        if (!k4_body(net, &code[i], &ss, &err)) { set_error(err); return ES_E_BAD_ARG; }
+        if (stats) stats[4 * i] = ss.instrs;
+    }
+    if (stats) {
+        stats[4 * n] = ss.reg_lo;
+        stats[4 * n + 1] = ss.reg_hi;
+        stats[4 * n + 2] = ss.reg_o0;
+        stats[4 * n + 3] = ss.reg_o1;
+    }
+    std::vector<const std::vector<uint64_t> *> bodies;
+    for (auto &c : code) bodies.push_back(&c);
+    std::vector<char> cubin;
+    std::vector<uint32_t> entry;
+    std::string err;
+    if (!k4_module(bodies, &cubin, &entry, &err)) { set_error(err); return ES_E_BAD_ARG; }
+    const int64_t sz = (int64_t)cubin.size();
+    if (!buf) return sz;
+    if (cap < sz) { set_error("buffer too small"); return ES_E_BAD_ARG; }
+    memcpy(buf, cubin.data(), (size_t)sz);
+    return sz;
+}
+
 int32_t es_map_eval(const es_prog *prog, uint64_t w0, uint64_t nw, uint32_t *out_words) {
     return es_map_eval_k(prog, 0, w0, nw, out_words);
 }

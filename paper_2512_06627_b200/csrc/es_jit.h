@@ -75,5 +75,13 @@ struct SassStats {
     int reg_lo = 0, reg_hi = 0, reg_o0 = 0, reg_o1 = 0;  // the template's interface registers
 };
 bool sass_direct_cubin(const LutNet &net, int threads, std::vector<char> *cubin, SassStats *st, std::string *err);
+// K4 (k4_skeleton.cu): one job's body for the multi-body skeleton (encoded
+// (lo, hi) words, position-independent), and a module of bodies behind the
+// skeleton's indirect branch (body i = jump-table entry i)
+bool k4_body(const LutNet &net, std::vector<uint64_t> *words, SassStats *st, std::string *err);
+bool k4_module(const std::vector<const std::vector<uint64_t> *> &bodies, std::vector<char> *cubin,
+               std::vector<uint32_t> *entry, std::string *err);
+int k4_body_capacity();  // instruction slots of one module
+int k4_max_bodies();     // bodies per module
 
 }  // namespace es

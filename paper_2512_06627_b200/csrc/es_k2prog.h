@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <memory>
 #include <vector>
 
 #include "es_core.h"
@@ -31,6 +32,15 @@ struct K2Gate {
 };
 static_assert(sizeof(K2Gate) == 16, "K2Gate is the 16-byte device record");
 
+// K4 body of a job (es_sass.cpp k4_body): the job's direct-SASS code for the
+// K4 multi-body skeleton, built once per program and kept with it.
+struct K4Body {
+    std::vector<uint64_t> code;  // encoded instructions, (lo, hi) pairs
+    uint64_t hash = 0;           // of `code` (module cache key)
+    int instrs = 0;
+    bool ok = false;             // false: no body (too many registers / slots)
+};
+
 struct K2Prog {
     int num_pis = 0;
     int num_slots = 0;              // PI slots + gate slots
@@ -44,6 +54,7 @@ struct K2Prog {
     // to L OUT records (the rest NOPs).  Every lane's operands are read
     // before any result of the step is stored.
     int lanes = 1;
+    mutable std::shared_ptr<K4Body> k4;  // built on demand by a batch run (run_k2)
 };
 
 // Launch group of a program: the widest words-per-thread W (4, 2, 1) at which

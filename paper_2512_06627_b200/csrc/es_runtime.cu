@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <unordered_map>
 #include <memory>
 #include <condition_variable>
 #include <mutex>
@@ -80,6 +81,25 @@ struct K2Item {
     int job;
 };
 
+// K4 (k4_skeleton.cu, es_sass.cpp): many jobs' straight-line bodies in one
+// module behind an indirect branch; the job and parameter layouts mirror the
+// skeleton's K4Job / K4Params (items are K2Items)
+struct K4JobD {
+    unsigned long long *best;
+    unsigned *swept;
+    unsigned long long total_words;
+    unsigned valid_mask;
+    unsigned body;
+    int cof_n;
+    unsigned char cof_pos[8];
+};
+struct K4ParamsD {
+    const K4JobD *jobs;
+    const K2Item *items;
+    unsigned long long n_items;
+    unsigned *counter;
+    unsigned one;
+};
 __constant__ unsigned c_lane_mask[5] = {0xAAAAAAAAu, 0xCCCCCCCCu, 0xF0F0F0F0u, 0xFF00FF00u,
                                         0xFFFF0000u};
 
@@ -540,8 +560,8 @@ struct Ctx {
     unsigned *d_counter = nullptr;         // [2] per in-flight slice
     unsigned long long *h_pin = nullptr;   // [4]
     cudaEvent_t ev_start = nullptr, ev_stop = nullptr, ev_slice[2] = {nullptr, nullptr};
-    cudaStream_t side[3] = {nullptr, nullptr, nullptr};  // concurrent K2 launch groups
-    cudaEvent_t ev_side[3] = {nullptr, nullptr, nullptr};
+    cudaStream_t side[4] = {nullptr, nullptr, nullptr, nullptr};  // concurrent K2 launch groups + K4
+    cudaEvent_t ev_side[4] = {nullptr, nullptr, nullptr, nullptr};
     uint4 *h_stage = nullptr;  // pinned staging of K2 program records (grown on demand)
     size_t stage_cap = 0;      // in records
 };
@@ -587,7 +607,7 @@ int make_ctx(int dev, Ctx *c) {
     CK(cudaEventCreate(&c->ev_stop));
     CK(cudaEventCreateWithFlags(&c->ev_slice[0], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_slice[1], cudaEventDisableTiming));
-    for (int q = 0; q < 3; ++q) {
+    for (int q = 0; q < 4; ++q) {
         CK(cudaStreamCreateWithFlags(&c->side[q], cudaStreamNonBlocking));
         CK(cudaEventCreate(&c->ev_side[q]));
     }
@@ -1253,6 +1273,216 @@ static void k2_group_results(const K2Group &gp, const es_prog *progs, const K2Pr
     }
 }
 
+// ---------------------------------------------------------------- K4
+// Which interpreter jobs get a straight-line body: num_pis >= ES_K4_MIN_PIS
+// (default 20; ES_K4=0 turns K4 off).  Smaller jobs' sweeps are a few items
+// and the body's host cost (mapping + lowering, ~1 ms) would not pay.
+static int k4_min_pis() {
+    static const int v = [] {
+        const char *e = getenv("ES_K4");
+        if (e && atoi(e) == 0) return 1 << 20;
+        const char *m = getenv("ES_K4_MIN_PIS");
+        return m ? atoi(m) : 20;
+    }();
+    return v;
+}
+
+struct K4Mod {
+    cudaLibrary_t lib = nullptr;
+    cudaKernel_t kern = nullptr;
+};
+static std::mutex g_k4_mu;
+static std::unordered_map<uint64_t, K4Mod> g_k4_mods;  // key: hash of the module's body hashes
+
+struct K4Launch {
+    std::vector<int> jobs_idx;
+    cudaKernel_t kern = nullptr;
+    std::vector<K4JobD> jobs;
+    std::vector<K2Item> items;
+    std::vector<uint64_t> n_items, item_words;
+    std::vector<unsigned long long> h_best;
+    std::vector<unsigned> h_swept;
+    uint8_t *d_buf = nullptr;
+    K4JobD *d_jobs = nullptr;
+    K2Item *d_items = nullptr;
+    unsigned long long *d_best = nullptr;
+    unsigned *d_swept = nullptr;
+    unsigned *d_counter = nullptr;
+    int instrs = 0;
+};
+
+static uint64_t hash_words(const std::vector<uint64_t> &w) {
+    uint64_t h = 0x9E3779B97F4A7C15ull ^ w.size();
+    for (uint64_t x : w) {
+        h ^= x + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+        h *= 0xff51afd7ed558ccdull;
+    }
+    return h;
+}
+
+// bodies for the candidate jobs (built once per program, in parallel), then
+// modules of up to k4_max_bodies() bodies, each loaded once (cached by its
+// bodies' hashes); `mods` receives the jobs that got a body, by module
+static int k4_prepare(const es_prog *progs, const K2Prog *const *kps, const std::vector<int> &cand,
+                      std::vector<K4Launch> *mods) {
+    NvtxRange nvtx("es_k4_prepare");
+    parallel_for((int)cand.size(), [&](int q) {
+        const int j = cand[q];
+        const K2Prog &kp = *kps[j];
+        if (kp.k4) return;
+        auto b = std::make_shared<K4Body>();
+        Dag dag;
+        std::string err;
+        if (build_dag(progs[j], &dag, &err) == ES_OK) {
+            LutNet net;
+            map_cofactored(dag, kp.cof_pis, &net);
+            SassStats st;
+            if (k4_body(net, &b->code, &st, &err)) {
+                b->ok = true;
+                b->instrs = st.instrs;
+                b->hash = hash_words(b->code);
+            }
+        }
+        kp.k4 = b;
+    });
+    const int cap = k4_body_capacity(), maxb = k4_max_bodies();
+    K4Launch cur;
+    int slots = 0;
+    std::vector<const std::vector<uint64_t> *> bodies;
+    auto flush = [&]() -> int {
+        if (cur.jobs_idx.empty()) return ES_OK;
+        uint64_t key = 0x84222325CBF29CE4ull;
+        for (int j : cur.jobs_idx) key = (key ^ kps[j]->k4->hash) * 0x100000001B3ull + 0x9E37;
+        std::lock_guard<std::mutex> lk(g_k4_mu);
+        auto it = g_k4_mods.find(key);
+        if (it == g_k4_mods.end()) {
+            std::vector<char> cubin;
+            std::vector<uint32_t> entry;
+            std::string err;
+            if (!k4_module(bodies, &cubin, &entry, &err)) { set_error(err); return ES_E_CUDA; }
+            K4Mod m;
+            CK(cudaLibraryLoadData(&m.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+            CK(cudaLibraryGetKernel(&m.kern, m.lib, "es_k4"));
+            it = g_k4_mods.emplace(key, m).first;
+        }
+        cur.kern = it->second.kern;
+        mods->push_back(std::move(cur));
+        cur = K4Launch();
+        bodies.clear();
+        slots = 0;
+        return ES_OK;
+    };
+    for (int j : cand) {
+        const K4Body &b = *kps[j]->k4;
+        if (!b.ok) continue;
+        const int need = (int)b.code.size() / 2 + 1;
+        if (!cur.jobs_idx.empty() && ((int)cur.jobs_idx.size() >= maxb || slots + need > cap)) {
+            int rc = flush();
+            if (rc != ES_OK) return rc;
+        }
+        cur.jobs_idx.push_back(j);
+        bodies.push_back(&b.code);
+        slots += need;
+        cur.instrs += b.instrs;
+    }
+    return flush();
+}
+
+// a module's job table and items (round-robin across its jobs, K2's item
+// sizing), uploaded and launched on `st`
+static int k4_launch(K4Launch &m, const es_prog *progs, const K2Prog *const *kps, Ctx *c, cudaStream_t st) {
+    const int T = 256, G = (int)m.jobs_idx.size();
+    auto kwords = [&](int q) {
+        const int j = m.jobs_idx[q];
+        return 1ull << std::max(progs[j].num_pis - 5 - (int)kps[j]->cof_pis.size(), 0);
+    };
+    uint64_t iw = 4096;
+    for (;;) {
+        uint64_t cnt = 0;
+        for (int q = 0; q < G; ++q) {
+            const uint64_t tw = kwords(q);
+            cnt += (tw + std::min(tw, iw) - 1) / std::min(tw, iw);
+        }
+        if (cnt >= (uint64_t)c->sms * 8 || iw <= (uint64_t)T) break;
+        iw >>= 1;
+    }
+    m.jobs.assign(G, K4JobD{});
+    m.n_items.assign(G, 0);
+    m.item_words.assign(G, 0);
+    m.h_best.assign(G, 0);
+    m.h_swept.assign(G, 0);
+    uint64_t max_items = 0;
+    for (int q = 0; q < G; ++q) {
+        const uint64_t tw = kwords(q);
+        m.item_words[q] = std::min<uint64_t>(tw, iw);
+        m.n_items[q] = (tw + m.item_words[q] - 1) / m.item_words[q];
+        max_items = std::max(max_items, m.n_items[q]);
+    }
+    m.items.clear();
+    for (uint64_t r = 0; r < max_items; ++r)
+        for (int q = 0; q < G; ++q)
+            if (r < m.n_items[q]) {
+                const uint64_t w0 = r * m.item_words[q];
+                m.items.push_back(K2Item{w0, (unsigned)std::min<uint64_t>(m.item_words[q], kwords(q) - w0), q});
+            }
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const size_t jobs_b = (size_t)G * sizeof(K4JobD), items_b = m.items.size() * sizeof(K2Item);
+    const size_t best_b = (size_t)G * 8, swept_b = (size_t)G * 4;
+    CK(cudaMallocAsync(&m.d_buf, al(jobs_b) + al(items_b) + al(best_b) + al(swept_b) + 256, st));
+    m.d_jobs = (K4JobD *)m.d_buf;
+    m.d_items = (K2Item *)(m.d_buf + al(jobs_b));
+    m.d_best = (unsigned long long *)(m.d_buf + al(jobs_b) + al(items_b));
+    m.d_swept = (unsigned *)(m.d_buf + al(jobs_b) + al(items_b) + al(best_b));
+    m.d_counter = (unsigned *)(m.d_buf + al(jobs_b) + al(items_b) + al(best_b) + al(swept_b));
+    for (int q = 0; q < G; ++q) {
+        const int j = m.jobs_idx[q];
+        K4JobD &J = m.jobs[q];
+        J.best = m.d_best + q;
+        J.swept = m.d_swept + q;
+        J.total_words = kwords(q);
+        J.valid_mask = lane_valid_mask(progs[j].num_pis);
+        J.body = (unsigned)q;
+        J.cof_n = (int)kps[j]->cof_pis.size();
+        for (int b = 0; b < J.cof_n; ++b) J.cof_pos[b] = (unsigned char)(kps[j]->cof_pis[b] - 1);
+        m.h_best[q] = 1ull << progs[j].num_pis;
+    }
+    CK(cudaMemcpyAsync(m.d_jobs, m.jobs.data(), jobs_b, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(m.d_items, m.items.data(), items_b, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(m.d_best, m.h_best.data(), best_b, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(m.d_swept, 0, al(swept_b) + 256, st));  // swept counts and the item counter
+    K4ParamsD p{m.d_jobs, m.d_items, (unsigned long long)m.items.size(), m.d_counter, 1u};
+    void *args[] = {&p};
+    const int grid = (int)std::min<uint64_t>(m.items.size(), (uint64_t)c->sms);
+    CK(cudaLaunchKernel((const void *)m.kern, dim3(grid), dim3(T), args, 0, st));
+    return ES_OK;
+}
+
+// es_result of a module's jobs (a whole, unsliced launch: k2_group_results'
+// rules with every item completed)
+static void k4_results(const K4Launch &m, const es_prog *progs, const K2Prog *const *kps, es_result *outs) {
+    for (size_t q = 0; q < m.jobs_idx.size(); ++q) {
+        const int j = m.jobs_idx[q];
+        es_result *r = &outs[j];
+        const int P = progs[j].num_pis;
+        const uint64_t sentinel = 1ull << P;
+        r->engine = ES_ENGINE_JIT;
+        r->launches += 1;
+        r->num_luts = kps[j]->k4->instrs;
+        r->regs_per_thread = 255;
+        const uint64_t item_patterns = (m.item_words[q] * 32) << kps[j]->cof_pis.size();
+        r->patterns_swept = std::min<uint64_t>((uint64_t)m.h_swept[q] * item_patterns, sentinel);
+        if (m.h_best[q] < sentinel) {
+            r->verdict = ES_COUNTEREXAMPLE;
+            r->witness_index = m.h_best[q];
+            r->witness_minimal = 1;
+            r->patterns_evaluated = ref_patterns_for_hit(m.h_best[q], P);
+        } else {
+            r->verdict = ES_EXHAUSTED_ZERO;
+            r->patterns_evaluated = sentinel;
+        }
+    }
+}
+
 static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &active_in,
                   const es_run_opts &o, Ctx *c, double deadline, es_result *outs,
                   const K2Prog *const *prebuilt = nullptr, std::vector<int> *unfit = nullptr) {
@@ -1305,6 +1535,28 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
         unfit->push_back(j);
     }
     if (active.empty()) return ES_OK;
+    const bool sliced = deadline >= 0 || o.cancel_flag != nullptr;
+    // K4: jobs with enough words get a straight-line body (one launch per
+    // module of bodies, on its own stream, concurrent with the K2 groups)
+    std::vector<K4Launch> k4mods;
+    double t_k4 = 0;
+    if (!sliced && o.engine != ES_ENGINE_INTERP) {
+        std::vector<int> cand;
+        for (int j : active)
+            if (progs[j].num_pis >= k4_min_pis()) cand.push_back(j);
+        if (!cand.empty()) {
+            const double tk = now_ms();
+            int rc = k4_prepare(progs, kps, cand, &k4mods);
+            if (rc != ES_OK) return rc;
+            std::vector<uint8_t> on_k4(n_jobs, 0);
+            for (const K4Launch &m : k4mods)
+                for (int j : m.jobs_idx) on_k4[j] = 1;
+            active.erase(std::remove_if(active.begin(), active.end(), [&](int j) { return on_k4[j] != 0; }),
+                         active.end());
+            t_k4 = now_ms() - tk;
+        }
+    }
+    if (active.empty() && k4mods.empty()) return ES_OK;
     // launch groups by slot count: small programs get 4 words per thread
     std::vector<K2Group> groups(3);
     for (int j : active) {
@@ -1326,7 +1578,6 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
         CK(cudaMallocHost(&c->h_stage, cap * sizeof(uint4)));
         c->stage_cap = cap;
     }
-    const bool sliced = deadline >= 0 || o.cancel_flag != nullptr;
     bool stopped = false;
     int stop_reason = 0;
     float dev_ms = 0;
@@ -1350,12 +1601,23 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
         // all groups at once, one side stream each, each launched as soon as
         // its host image is ready, the largest programs first (their group is
         // the long pole; the smaller groups' host work overlaps it); device
-        // time = makespan from the first upload
+        // time = makespan from the first upload.  K4 modules go first, in
+        // turn on their own stream.
+        if (!k4mods.empty()) {
+            t1 = now_ms();
+            CK(cudaEventRecord(c->ev_start, c->stream));
+            CK(cudaStreamWaitEvent(c->side[3], c->ev_start, 0));
+            for (K4Launch &m : k4mods) {
+                int rc = k4_launch(m, progs, kps, c, c->side[3]);
+                if (rc != ES_OK) return rc;
+            }
+            CK(cudaEventRecord(c->ev_side[3], c->side[3]));
+        }
         for (size_t gi = 0; gi < groups.size(); ++gi) {
             const size_t g = groups.size() - 1 - gi;
             int rc = k2_group_prepare(groups[g], progs, kps, c, c->h_stage + stage_off[g], c->stream);
             if (rc != ES_OK) return rc;
-            if (gi == 0) {
+            if (gi == 0 && k4mods.empty()) {
                 t1 = now_ms();
                 CK(cudaEventRecord(c->ev_start, c->stream));
             }
@@ -1371,10 +1633,16 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
         // join only now: a join inside the loop would order the next group's
         // allocation (on the main stream) after this group's kernel
         for (size_t g = 0; g < groups.size(); ++g) CK(cudaStreamWaitEvent(c->stream, c->ev_side[g], 0));
+        if (!k4mods.empty()) CK(cudaStreamWaitEvent(c->stream, c->ev_side[3], 0));
         CK(cudaStreamSynchronize(c->stream));
         for (size_t g = 0; g < groups.size(); ++g) {
             float ms = 0;
             CK(cudaEventElapsedTime(&ms, c->ev_start, c->ev_side[g]));
+            dev_ms = std::max(dev_ms, ms);
+        }
+        if (!k4mods.empty()) {
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, c->ev_start, c->ev_side[3]));
             dev_ms = std::max(dev_ms, ms);
         }
     } else {
@@ -1398,9 +1666,26 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
         CK(cudaMemcpyAsync(gp.h_swept.data(), gp.d_swept, gp.h_swept.size() * 4, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaFreeAsync(gp.d_buf, c->stream));
     }
+    for (K4Launch &m : k4mods) {
+        CK(cudaMemcpyAsync(m.h_best.data(), m.d_best, m.h_best.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(m.h_swept.data(), m.d_swept, m.h_swept.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaFreeAsync(m.d_buf, c->stream));
+    }
     CK(cudaStreamSynchronize(c->stream));
     for (K2Group &gp : groups) k2_group_results(gp, progs, kps, stopped, stop_reason, outs);
+    for (const K4Launch &m : k4mods) k4_results(m, progs, kps, outs);
     for (int j : active) outs[j].device_ms = dev_ms;
+    for (const K4Launch &m : k4mods)
+        for (int j : m.jobs_idx) outs[j].device_ms = dev_ms;
+    if (verbose && !k4mods.empty()) {
+        float ms = -1;
+        cudaEventElapsedTime(&ms, c->ev_start, c->ev_side[3]);
+        size_t nj = 0, ni = 0;
+        int ins = 0;
+        for (const K4Launch &m : k4mods) { nj += m.jobs_idx.size(); ni += m.items.size(); ins += m.instrs; }
+        fprintf(stderr, "[es k4] modules=%zu jobs=%zu items=%zu body-instrs=%d | bodies+modules %.2fms, "
+                        "K4 %.2fms\n", k4mods.size(), nj, ni, ins, t_k4, ms);
+    }
     if (verbose)
         for (size_t g = 0; g < groups.size(); ++g) {
             const K2Group &gp = groups[g];
@@ -2396,7 +2681,7 @@ void runtime_shutdown() {
         cudaEventDestroy(c->ev_stop);
         cudaEventDestroy(c->ev_slice[0]);
         cudaEventDestroy(c->ev_slice[1]);
-        for (int q = 0; q < 3; ++q) {
+        for (int q = 0; q < 4; ++q) {
             cudaStreamDestroy(c->side[q]);
             cudaEventDestroy(c->ev_side[q]);
         }

@@ -179,10 +179,14 @@ bool emit_split_ptx(const LutNet &net, int threads, int parts, const std::string
             if (ca == 0 && cb == -1) {
                 const std::string m = name(u);
                 body << "mov.b32 " << r << ", " << m << ";\n";
-            } else {
+            } else if (ca == 0 && cb == 1) {
                 const std::string bt = bit_of(u);
-                if (ca == 0 && cb == 1) body << "mov.b32 " << r << ", " << bt << ";\n";
-                else body << "mad.lo.s32 " << r << ", " << bt << ", " << (cb - ca) << ", " << ca << ";\n";
+                body << "mov.b32 " << r << ", " << bt << ";\n";
+            } else {  // mask * (ca - cb) + ca, as emit_body_ptx
+                const std::string m = name(u);
+                const int f = ca - cb;
+                const std::string fr = f == -1 ? "%esneg1" : f == 1 ? "%esone" : f == 2 ? "%escf2" : "%escg2";
+                body << "mad.lo.s32 " << r << ", " << m << ", " << fr << ", " << ca << ";\n";
             }
             coef[key] = r;
             return r;
@@ -249,7 +253,9 @@ bool emit_split_ptx(const LutNet &net, int threads, int parts, const std::string
         if (!coef.empty()) s << ".reg .b32 %esc<" << coef.size() << ">;\n";
         s << ".reg .b32 %est, %eso0, %eso1;\n.reg .pred %espz;\n.reg .b64 %esr;\n";
         for (size_t k = 0; k < consts.size(); ++k) s << "mov.b32 %esk" << k << ", " << consts[k] << ";\n";
-        if (imad) s << ".reg .b32 %esneg1;\nneg.s32 %esneg1, %esone;\n";
+        if (imad)
+            s << ".reg .b32 %esneg1, %escf2, %escg2;\nneg.s32 %esneg1, %esone;\nadd.s32 %escf2, %esone, %esone;\n"
+                 "neg.s32 %escg2, %escf2;\n";
         for (int j = 6; j <= P; ++j) {
             if (!pi_mask[j]) continue;
             const int bit = net.pi_bit[j];

@@ -1,0 +1,113 @@
+// k4_skeleton.cu -- K4, many sub-miters' straight-line bodies in one kernel
+// (sm_100a).
+//
+// K2 interprets every gate of every job from shared memory (three mask
+// decodes, three LOP3s and two or three slot accesses per gate-word); K1 runs
+// one program's LUTs as straight-line LOP3 / IMAD code (~0.7 instruction per
+// gate-word) but one program per module.  K4 is K1's code at K2's job
+// granularity: a module holds the direct-SASS bodies (es_sass.cpp) of many
+// jobs behind one placeholder device function that starts with an indirect
+// branch (`brx.idx.uni` over a jump table in the constant bank); the host
+// writes each job's body over the placeholder's slots and the table entry
+// the job's `body` index selects (sass_template.py builds this skeleton with
+// its placeholder once, at build time).  Everything around the body follows
+// es_k2d (es_runtime.cu):
+//
+//  * work items (<= 2^chunk words of one job) are dealt round-robin across
+//    jobs; a CTA claims items in order from a device counter and skips an
+//    item whose first pattern lies above the job's current minimum, so a
+//    job's every item below its final minimum is swept and the answer is
+//    the reference's workers=1 witness (es.py:297-320);
+//  * one thread evaluates one kernel word per body call; the body returns
+//    the first failing cofactor copy's output word and that copy's number
+//    (es_sass.cpp's branch-free fold), the warp reduces the minimum pattern
+//    and one lane atomicMins it into the job's word.
+//
+// Compiled at BUILD time to PTX (build.py) with the ES_BODY marker, which
+// sass_template.py replaces by the call to the placeholder.
+
+struct K4Job {
+    unsigned long long *best;    // min failing pattern, sentinel 2^n
+    unsigned *swept;             // items evaluated (not skipped)
+    unsigned long long total_words;  // kernel words (cofactor PIs excluded)
+    unsigned valid_mask;         // pattern bits of a word that exist (n < 5)
+    unsigned body;               // jump-table index of the job's body
+    int cof_n;                   // cofactor PIs (2^cof_n copies per call)
+    unsigned char cof_pos[8];    // their pattern bits (PI - 1), ascending
+};
+
+struct K4Item {
+    unsigned long long w0;
+    unsigned n_words;
+    int job;
+};
+
+struct K4Params {
+    const K4Job *jobs;
+    const K4Item *items;
+    unsigned long long n_items;
+    unsigned *counter;
+    unsigned one;                // == 1, opaque (IMAD coefficients)
+};
+
+__device__ __forceinline__ unsigned long long k4_expand(unsigned long long x, const K4Job &job) {
+#pragma unroll 1
+    for (int i = 0; i < job.cof_n; ++i) {
+        const unsigned s = job.cof_pos[i];
+        x = ((x >> s) << (s + 1)) | (x & ((1ull << s) - 1ull));
+    }
+    return x;
+}
+
+extern "C" __global__ void __launch_bounds__(ES_THREADS)
+es_k4(const K4Params p)
+{
+    __shared__ unsigned long long s_item;
+    const unsigned t = threadIdx.x, lane = t & 31u;
+    const unsigned long long kStop = ~0ull, kSkip = ~0ull - 1;
+    for (;;) {
+        if (t == 0) {
+            unsigned long long k = atomicAdd(p.counter, 1u);
+            if (k >= p.n_items) {
+                k = kStop;
+            } else {
+                const K4Item it = p.items[k];
+                const K4Job &jb = p.jobs[it.job];
+                if (k4_expand(it.w0 << 5, jb) > *(volatile unsigned long long *)jb.best) k = kSkip;
+                else atomicAdd(jb.swept, 1u);
+            }
+            s_item = k;
+        }
+        __syncthreads();
+        const unsigned long long k = s_item;
+        __syncthreads();
+        if (k == kStop) break;
+        if (k == kSkip) continue;
+        const K4Item it = p.items[k];
+        const K4Job job = p.jobs[it.job];
+#pragma unroll 1
+        for (unsigned wb = 0; wb < it.n_words; wb += ES_THREADS) {
+            const unsigned long long w = it.w0 + wb + t;
+            unsigned out, copy;
+            asm volatile("// ES_BODY %0 %1 %2 %3 %4 %5"
+                         : "=r"(out), "=r"(copy)
+                         : "r"((unsigned)w), "r"((unsigned)(w >> 32)), "r"(p.one), "r"(job.body));
+            out &= job.valid_mask;
+            if (w >= job.total_words || wb + t >= it.n_words) out = 0u;
+            if (__ballot_sync(0xffffffffu, out != 0u)) {
+                unsigned long long cand = ~0ull;
+                if (out) {
+                    cand = k4_expand((w << 5) | (unsigned long long)(__ffs(out) - 1), job);
+                    for (int b = 0; b < job.cof_n; ++b)
+                        if ((copy >> b) & 1u) cand |= 1ull << job.cof_pos[b];
+                }
+#pragma unroll
+                for (int off = 16; off; off >>= 1) {
+                    const unsigned long long o = __shfl_xor_sync(0xffffffffu, cand, off);
+                    cand = o < cand ? o : cand;
+                }
+                if (lane == 0) atomicMin(job.best, cand);
+            }
+        }
+    }
+}

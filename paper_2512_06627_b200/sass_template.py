@@ -77,6 +77,172 @@ def placeholder_ptx(skeleton_ptx: str, multi: bool, chain: int = CHAIN) -> str:
     return body[:hdr] + _placeholder_func(multi, chain) + body[hdr:]
 
 
+# ---------------------------------------------------------------- K4
+# K4 (k4_skeleton.cu): one module holds many jobs' bodies.  The placeholder
+# takes a fourth argument (the body's .text offset, written by the host into
+# the job table) and dispatches with brx.idx.uni over K4_TARGETS labels;
+# ptxas records the branch and its targets in EIATTR_INDIRECT_BRANCH_TARGETS,
+# which the library rewrites for the bodies it places.
+K4_THREADS = 256
+K4_TARGETS = 128
+K4_CHAIN = 40000
+MARK_IDX = 0x55555555
+EIATTR_INDIRECT_BRANCH_TARGETS = 0x34
+
+
+def _placeholder_func_k4(targets: int = K4_TARGETS, chain: int = K4_CHAIN) -> str:
+    rng = random.Random(4321)
+    L = [".func (.param .b64 es_pr) es_body(.param .b32 es_pw0, .param .b32 es_pw1, .param .b32 es_pw2, "
+         ".param .b32 es_pw3)", "{",
+         f".reg .b32 %a<{LIVE}>;", ".reg .b32 %lo, %hi, %one, %idx, %v, %u, %o0, %o1;", ".reg .b64 %r;",
+         "ld.param.b32 %lo, [es_pw0];", "ld.param.b32 %hi, [es_pw1];", "ld.param.b32 %one, [es_pw2];",
+         "ld.param.b32 %idx, [es_pw3];",
+         f"xor.b32 %a0, %lo, {MARK_LO};", f"xor.b32 %a1, %hi, {MARK_HI};", f"xor.b32 %a2, %idx, {MARK_IDX};",
+         "mov.b32 %u, %one;"]
+    for i in range(3, LIVE):
+        L.append(f"lop3.b32 %a{i}, %u, %a{i - 1}, %a{i - 2}, {1 + i % 250};")
+        L.append(f"add.u32 %u, %u, %a{i};")
+    L.append("mov.b32 %v, %u;")
+    L.append("es_tab: .branchtargets " + ", ".join(f"es_L{m}" for m in range(targets)) + ";")
+    L.append("brx.idx.uni %idx, es_tab;")
+    per = chain // targets
+    for m in range(targets):
+        L.append(f"es_L{m}:")
+        for i in range(per):
+            L.append(f"lop3.b32 %v, %v, %a{(i * 7 + m) % LIVE}, %a{(i * 13 + 5 + m) % LIVE}, {rng.randrange(1, 255)};")
+        L.append("bra.uni es_END;")
+    L.append("es_END:")
+    for i in range(LIVE):
+        L.append(f"xor.b32 %v, %v, %a{i};")
+    L.append(f"xor.b32 %o0, %v, {MARK_O0};")
+    L.append(f"xor.b32 %o1, %u, {MARK_O1};")
+    L += ["mov.b64 %r, {%o0, %o1};", "st.param.b64 [es_pr], %r;", "ret;", "}"]
+    return "\n".join(L) + "\n"
+
+
+def placeholder_ptx_k4(skeleton_ptx: str, targets: int = K4_TARGETS, chain: int = K4_CHAIN) -> str:
+    m = re.search(r"// ES_BODY ([^\n]*)\n", skeleton_ptx)
+    assert m, "K4 skeleton without ES_BODY"
+    regs = m.group(1).split()
+    outs, (wlo, whi, one, idx) = regs[:2], regs[2:6]
+    call = ["{", ".reg .b64 %esret;", ".param .b32 es_a0;", ".param .b32 es_a1;", ".param .b32 es_a2;",
+            ".param .b32 es_a3;", ".param .b64 es_r;", f"st.param.b32 [es_a0], {wlo};",
+            f"st.param.b32 [es_a1], {whi};", f"st.param.b32 [es_a2], {one};", f"st.param.b32 [es_a3], {idx};",
+            "call.uni (es_r), es_body, (es_a0, es_a1, es_a2, es_a3);", "ld.param.b64 %esret, [es_r];",
+            f"mov.b64 {{{outs[0]}, {outs[1]}}}, %esret;", "}"]
+    body = skeleton_ptx[:m.start()] + "\n".join(call) + "\n" + skeleton_ptx[m.end():]
+    hdr = body.index("\n", body.index(".address_size 64")) + 1
+    return body[:hdr] + _placeholder_func_k4(targets, chain) + body[hdr:]
+
+
+def _nv_info_attr(cubin: bytes, section: str, attr: int) -> tuple[int, int]:
+    """(file offset, size) of the payload of attribute `attr` in an .nv.info section."""
+    for name, _, off, size in _sections(cubin):
+        if name != section:
+            continue
+        i = off
+        while i < off + size:
+            fmt, at = cubin[i], cubin[i + 1]
+            if fmt == 0x04:
+                sz, = struct.unpack_from("<H", cubin, i + 2)
+                if at == attr:
+                    return i + 4, sz
+                i += 4 + sz
+            else:
+                i += 4
+    raise RuntimeError(f"attribute 0x{attr:x} not in {section}")
+
+
+def analyse_k4(cubin_path: str, cuobjdump: str) -> dict:
+    sass = subprocess.run([cuobjdump, "-sass", cubin_path], capture_output=True, text=True, check=True).stdout
+    ins = [(int(a, 16), t) for a, t in _INS.findall(sass)]
+    calls = [(i, a, t) for i, (a, t) in enumerate(ins) if t.startswith("CALL.REL")]
+    assert len(calls) == 1, "K4 placeholder: expected one CALL"
+    ci, ca, ct = calls[0]
+    start = int(ct.split()[-1], 16)
+    rets = [(a, t) for a, t in ins if a >= start and t.startswith("RET.REL")]
+    assert rets, "K4 placeholder: no RET"
+    end = rets[0][0]
+    mpair = re.match(r"RET\.REL\.NODEC R(\d+) 0x0$", rets[0][1])
+    assert mpair, f"K4 placeholder: unexpected return {rets[0][1]}"
+    ret_pair = int(mpair.group(1))
+    setup = [re.match(rf"MOV R(\d+), 0x{ca + 16:x}$", t) for a, t in ins[max(0, ci - 16):ci]]
+    setup = [m for m in setup if m]
+    assert setup, "K4 placeholder: return-address register not set up by the caller"
+    ret_reg = int(setup[-1].group(1))
+    body = [t for a, t in ins if start <= a < end]
+    written = set()
+    for t in body:
+        assert not t.startswith(("STL", "LDL", "CALL", "RET")), f"K4 placeholder: unexpected {t}"
+        m = re.match(r"(?:@!?U?P\d+\s+)?[A-Z0-9_.]+\s+R(\d+)", t)
+        if m:
+            written.add(int(m.group(1)))
+            if t.split()[0] in ("IMAD.WIDE", "IMAD.WIDE.U32") or ".64" in t.split()[0]:
+                written.add(int(m.group(1)) + 1)
+    _, lo = _marked(body, MARK_LO)
+    _, hi = _marked(body, MARK_HI)
+    o0, _ = _marked(body, MARK_O0)
+    o1 = _marked(body, MARK_O1)[0]
+    # the body index arrives in a uniform register (brx.idx.uni); the dispatch
+    # is ptxas's own: idx * 4 -> jump-table load from c[0x2] -> sign-extended
+    # pair -> BRXU.  Those four instructions are re-emitted at the placeholder's
+    # first slot, the BRXU offset rebased.
+    mi = [t for t in body if f"0x{MARK_IDX:x}" in t]
+    assert len(mi) == 1 and mi[0].startswith("ULOP3.LUT"), f"K4 placeholder: idx marker {mi}"
+    idx = int(re.findall(r"\bUR(\d+)\b", mi[0])[1])
+    fn = [(a, t) for a, t in ins if start <= a < end]
+    brx = [(a, t) for a, t in fn if t.startswith("BRX")]
+    assert len(brx) == 1 and brx[0][1].startswith("BRXU UR"), f"K4 placeholder: dispatch {brx}"
+    tr = int(re.match(r"BRXU UR(\d+) ", brx[0][1]).group(1))
+    ldc = [(a, t) for a, t in fn if re.match(rf"LDCU UR{tr}, c\[0x2\]\[UR(\d+)\]$", t)]
+    assert len(ldc) == 1, f"K4 placeholder: table load {ldc}"
+    ir = int(re.match(r"LDCU UR\d+, c\[0x2\]\[UR(\d+)\]$", ldc[0][1]).group(1))
+    shl = [(a, t) for a, t in fn if t == f"USHF.L.U32 UR{ir}, UR{idx}, 0x2, URZ" and a < ldc[0][0]]
+    sra = [(a, t) for a, t in fn if t == f"USHF.R.S32.HI UR{tr + 1}, URZ, 0x1f, UR{tr}" and ldc[0][0] < a < brx[0][0]]
+    assert len(shl) >= 1 and len(sra) == 1, f"K4 placeholder: dispatch {shl} {sra}"
+    clobber = sorted(written - {ret_reg, lo, hi, 1, 255})
+    assert ret_reg not in (lo, hi, o0, o1) and o0 in clobber and o1 in clobber
+    assert ret_pair + 1 in clobber and (ret_pair == ret_reg or ret_pair in clobber)
+    assert not {ret_pair, ret_pair + 1} & {o0, o1, lo, hi}
+    return {"start": start, "end": end, "ret_reg": ret_reg, "ret_pair": ret_pair, "lo": lo, "hi": hi,
+            "idx": idx, "o0": o0, "o1": o1, "clobber": clobber,
+            "dispatch": [shl[-1][0], ldc[0][0], sra[0][0], brx[0][0]]}
+
+
+def build_k4_template(build_dir: str, ptxas: str, cuobjdump: str, arch: str = "sm_100a") -> str:
+    """Compile the K4 placeholder skeleton; write k4_sass_template.inc."""
+    skel = open(os.path.join(build_dir, f"k4_skeleton_{K4_THREADS}.ptx")).read()
+    ptx = os.path.join(build_dir, "k4_sass.ptx")
+    cub = os.path.join(build_dir, "k4_sass.cubin")
+    open(ptx, "w").write(placeholder_ptx_k4(skel))
+    subprocess.run([ptxas, f"-arch={arch}", "-O3", ptx, "-o", cub], check=True, capture_output=True)
+    info = analyse_k4(cub, cuobjdump)
+    data = no_opportunistic_finalization(open(cub, "rb").read())
+    text_off = _elf_text_offset(data, ".text.es_k4")
+    ibt_off, ibt_size = _nv_info_attr(data, ".nv.info.es_k4", EIATTR_INDIRECT_BRANCH_TARGETS)
+    off0, _, count = struct.unpack_from("<III", data, ibt_off)
+    assert count == K4_TARGETS and ibt_size == 12 + 4 * count, (count, ibt_size)
+    tab = [(o, sz) for n, _, o, sz in _sections(data) if n == ".nv.constant2.es_k4"]
+    assert len(tab) == 1 and tab[0][1] == 4 * K4_TARGETS, f"K4 placeholder: jump table {tab}"
+    assert not [n for n, _, o, sz in _sections(data) if n == ".rela.nv.constant2.es_k4" and sz]
+    clob = [0, 0, 0, 0]
+    for r in info["clobber"]:
+        clob[r // 64] |= 1 << (r % 64)
+    disp = []
+    for a in info["dispatch"]:
+        disp += list(struct.unpack_from("<QQ", data, text_off + a))
+    out = [f"static const unsigned char kSassK4_cubin[] = {{{','.join(str(b) for b in data)}}};\n",
+           f"static const K4Template kSassK4 = {{kSassK4_cubin, sizeof(kSassK4_cubin), {K4_THREADS}, "
+           f"{text_off}ull, {info['start']}ull, {info['end']}ull, {info['ret_reg']}, {info['ret_pair']}, "
+           f"{info['lo']}, {info['hi']}, {info['o0']}, {info['o1']}, {ibt_off}ull, {count}, {tab[0][0]}ull, "
+           f"{{{', '.join(f'{c}ull' for c in clob)}}}, {{{', '.join(f'{x}ull' for x in disp)}}}}};\n"]
+    inc = os.path.join(build_dir, "k4_sass_template.inc")
+    with open(inc, "w") as fh:
+        fh.write("// generated by sass_template.py (build time) -- do not edit\n")
+        fh.writelines(out)
+    return inc
+
+
 def _sections(cubin: bytes):
     """(name, type, file offset, size) of every section of a 64-bit ELF."""
     shoff, = struct.unpack_from("<Q", cubin, 0x28)
