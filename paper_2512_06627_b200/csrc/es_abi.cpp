@@ -22,6 +22,7 @@ void set_error(const std::string &m) { t_err = m; }
 
 int run_one(const es_prog *prog, const es_run_opts *opts, es_result *out);
 int run_batch_jit(int n_jobs, const es_prog *progs, const es_run_opts *opts, es_result *outs);
+void k4_prebuild(int n, const es_prog *progs, const K2Prog *const *kps);
 int run_batch(int n_jobs, const es_prog *progs, const es_run_opts *opts, es_result *outs,
               const K2Prog *const *prebuilt = nullptr);
 int session_open(const es_prog *prog, const es_run_opts *opts, void **out);
@@ -578,8 +579,17 @@ int32_t es_batch_prepare(es_batch *bp, int32_t n_threads) {
     Batch *bt = (Batch *)bp;
     if (!bt) { set_error("bad argument"); return ES_E_BAD_ARG; }
     const int rc = prepare_k2(bt->subs, n_threads);
-    if (rc != ES_OK) set_error("malformed sub-miter program");
-    return rc;
+    if (rc != ES_OK) { set_error("malformed sub-miter program"); return rc; }
+    // and the K4 straight-line bodies of the jobs with enough words
+    std::vector<es_prog> progs(bt->subs.size());
+    std::vector<const K2Prog *> kps(bt->subs.size(), nullptr);
+    for (size_t i = 0; i < bt->subs.size(); ++i) {
+        if (bt->subs[i].too_many_inputs) continue;
+        progs[i] = bt->subs[i].view();
+        kps[i] = &bt->subs[i].k2;
+    }
+    k4_prebuild((int)progs.size(), progs.data(), kps.data());
+    return ES_OK;
 }
 
 int32_t es_xag_eval(int32_t num_pis, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,

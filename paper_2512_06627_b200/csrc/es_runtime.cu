@@ -85,8 +85,6 @@ struct K2Item {
 // module behind an indirect branch; the job and parameter layouts mirror the
 // skeleton's K4Job / K4Params (items are K2Items)
 struct K4JobD {
-    unsigned long long *best;
-    unsigned *swept;
     unsigned long long total_words;
     unsigned valid_mask;
     unsigned body;
@@ -97,6 +95,8 @@ struct K4ParamsD {
     const K4JobD *jobs;
     const K2Item *items;
     unsigned long long n_items;
+    unsigned long long *best;
+    unsigned *swept;
     unsigned *counter;
     unsigned one;
 };
@@ -1275,39 +1275,70 @@ static void k2_group_results(const K2Group &gp, const es_prog *progs, const K2Pr
 
 // ---------------------------------------------------------------- K4
 // Which interpreter jobs get a straight-line body: num_pis >= ES_K4_MIN_PIS
-// (default 20; ES_K4=0 turns K4 off).  Smaller jobs' sweeps are a few items
-// and the body's host cost (mapping + lowering, ~1 ms) would not pay.
+// (default 18; ES_K4=0 turns K4 off).  Smaller jobs' sweeps are a few items
+// and the body's host cost (mapping + lowering, ~1 ms of one core) would not
+// pay.  Measured on config 4 (device ms, best of 4): min 16 / 18 / 20 / 22 ->
+// 1.88 / 1.91 / 2.39 / 3.56 (240K-slot modules; K2 alone 11.6).
 static int k4_min_pis() {
     static const int v = [] {
         const char *e = getenv("ES_K4");
         if (e && atoi(e) == 0) return 1 << 20;
         const char *m = getenv("ES_K4_MIN_PIS");
-        return m ? atoi(m) : 20;
+        return m ? atoi(m) : 18;
     }();
     return v;
 }
 
+// A loaded module and, per device, its job table + items (position-
+// independent, uploaded once) and the per-job sentinels best starts from
+struct K4Img {
+    int dev = -1;
+    uint8_t *d_img = nullptr;                  // jobs, then items
+    unsigned long long *d_best0 = nullptr;     // per job: 2^num_pis
+};
 struct K4Mod {
     cudaLibrary_t lib = nullptr;
     cudaKernel_t kern = nullptr;
-};
-static std::mutex g_k4_mu;
-static std::unordered_map<uint64_t, K4Mod> g_k4_mods;  // key: hash of the module's body hashes
-
-struct K4Launch {
-    std::vector<int> jobs_idx;
-    cudaKernel_t kern = nullptr;
+    int G = 0;
+    std::vector<uint64_t> n_items, item_words;
     std::vector<K4JobD> jobs;
     std::vector<K2Item> items;
-    std::vector<uint64_t> n_items, item_words;
-    std::vector<unsigned long long> h_best;
-    std::vector<unsigned> h_swept;
-    uint8_t *d_buf = nullptr;
-    K4JobD *d_jobs = nullptr;
-    K2Item *d_items = nullptr;
-    unsigned long long *d_best = nullptr;
-    unsigned *d_swept = nullptr;
-    unsigned *d_counter = nullptr;
+    std::vector<K4Img> imgs;
+    int users = 0;  // runs holding it (under g_k4_mu)
+};
+static std::mutex g_k4_mu;
+static double g_k4_t[3];  // ES_VERBOSE: ms in module build / library load / context load
+static std::unordered_map<uint64_t, std::unique_ptr<K4Mod>> g_k4_mods;  // key: the bodies' hashes
+// bound on loaded modules (~2.3 MB of code each): a long sweep makes new
+// ones every round; modules no run holds are unloaded past it
+constexpr size_t kK4MaxModules = 192;
+
+static void k4_evict_locked() {
+    if (g_k4_mods.size() <= kK4MaxModules) return;
+    for (auto it = g_k4_mods.begin(); it != g_k4_mods.end() && g_k4_mods.size() > kK4MaxModules / 2;) {
+        K4Mod &m = *it->second;
+        if (m.users) { ++it; continue; }
+        for (K4Img &x : m.imgs) cudaFree(x.d_img);
+        cudaLibraryUnload(m.lib);
+        it = g_k4_mods.erase(it);
+    }
+}
+
+// a run's hold on its modules (released when the run ends)
+struct K4Hold {
+    std::vector<K4Mod *> mods;
+    ~K4Hold() {
+        std::lock_guard<std::mutex> lk(g_k4_mu);
+        for (K4Mod *m : mods) --m->users;
+    }
+};
+
+// one module launch of a run: its cached module and this run's scratch
+struct K4Launch {
+    std::vector<int> jobs_idx;
+    K4Mod *mod = nullptr;
+    const K4Img *img = nullptr;
+    size_t scratch_job0 = 0;  // first job slot of the run's best / swept arrays
     int instrs = 0;
 };
 
@@ -1320,16 +1351,61 @@ static uint64_t hash_words(const std::vector<uint64_t> &w) {
     return h;
 }
 
-// bodies for the candidate jobs (built once per program, in parallel), then
-// modules of up to k4_max_bodies() bodies, each loaded once (cached by its
-// bodies' hashes); `mods` receives the jobs that got a body, by module
-static int k4_prepare(const es_prog *progs, const K2Prog *const *kps, const std::vector<int> &cand,
-                      std::vector<K4Launch> *mods) {
-    NvtxRange nvtx("es_k4_prepare");
-    parallel_for((int)cand.size(), [&](int q) {
-        const int j = cand[q];
+// a module's host image: job table and items, round-robin across its jobs
+// (K2's item sizing: 4096 words, halved until >= 8 items per SM)
+static void k4_image(K4Mod &m, const std::vector<int> &jobs_idx, const es_prog *progs,
+                     const K2Prog *const *kps, int sms) {
+    const int T = 256, G = (int)jobs_idx.size();
+    m.G = G;
+    auto kwords = [&](int q) {
+        const int j = jobs_idx[q];
+        return 1ull << std::max(progs[j].num_pis - 5 - (int)kps[j]->cof_pis.size(), 0);
+    };
+    uint64_t iw = 4096;
+    for (;;) {
+        uint64_t cnt = 0;
+        for (int q = 0; q < G; ++q) {
+            const uint64_t tw = kwords(q);
+            cnt += (tw + std::min(tw, iw) - 1) / std::min(tw, iw);
+        }
+        if (cnt >= (uint64_t)sms * 8 || iw <= (uint64_t)T) break;
+        iw >>= 1;
+    }
+    m.jobs.assign(G, K4JobD{});
+    m.n_items.assign(G, 0);
+    m.item_words.assign(G, 0);
+    uint64_t max_items = 0;
+    for (int q = 0; q < G; ++q) {
+        const int j = jobs_idx[q];
+        const uint64_t tw = kwords(q);
+        m.item_words[q] = std::min<uint64_t>(tw, iw);
+        m.n_items[q] = (tw + m.item_words[q] - 1) / m.item_words[q];
+        max_items = std::max(max_items, m.n_items[q]);
+        K4JobD &J = m.jobs[q];
+        J.total_words = tw;
+        J.valid_mask = lane_valid_mask(progs[j].num_pis);
+        J.body = (unsigned)q;
+        J.cof_n = (int)kps[j]->cof_pis.size();
+        for (int b = 0; b < J.cof_n; ++b) J.cof_pos[b] = (unsigned char)(kps[j]->cof_pis[b] - 1);
+    }
+    m.items.clear();
+    for (uint64_t r = 0; r < max_items; ++r)
+        for (int q = 0; q < G; ++q)
+            if (r < m.n_items[q]) {
+                const uint64_t w0 = r * m.item_words[q];
+                m.items.push_back(K2Item{w0, (unsigned)std::min<uint64_t>(m.item_words[q], kwords(q) - w0), q});
+            }
+}
+
+// K4 bodies of the jobs that lack one, on all host cores (a job whose body
+// does not fit gets ok = false and stays on K2)
+static void k4_build_bodies(const es_prog *progs, const K2Prog *const *kps, const std::vector<int> &jobs) {
+    std::vector<int> todo;
+    for (int j : jobs)
+        if (!kps[j]->k4) todo.push_back(j);
+    parallel_for((int)todo.size(), [&](int q) {
+        const int j = todo[q];
         const K2Prog &kp = *kps[j];
-        if (kp.k4) return;
         auto b = std::make_shared<K4Body>();
         Dag dag;
         std::string err;
@@ -1345,27 +1421,89 @@ static int k4_prepare(const es_prog *progs, const K2Prog *const *kps, const std:
         }
         kp.k4 = b;
     });
+}
+
+// es_batch_prepare: the bodies of the jobs K4 would take, ahead of the first run
+void k4_prebuild(int n, const es_prog *progs, const K2Prog *const *kps) {
+    std::vector<int> cand;
+    for (int j = 0; j < n; ++j)
+        if (kps[j] && progs[j].num_pis >= k4_min_pis() && k2_fits(*kps[j])) cand.push_back(j);
+    k4_build_bodies(progs, kps, cand);
+}
+
+// bodies for the candidate jobs (built once per program, in parallel), then
+// modules of up to k4_max_bodies() bodies; each module is built, loaded and
+// imaged on the device once (cached by its bodies' hashes), so a warm run
+// only looks them up
+static int k4_prepare(const es_prog *progs, const K2Prog *const *kps, const std::vector<int> &cand, Ctx *c,
+                      std::vector<K4Launch> *mods, K4Hold *hold) {
+    NvtxRange nvtx("es_k4_prepare");
+    k4_build_bodies(progs, kps, cand);
     const int cap = k4_body_capacity(), maxb = k4_max_bodies();
     K4Launch cur;
     int slots = 0;
+    size_t job0 = 0;
     std::vector<const std::vector<uint64_t> *> bodies;
     auto flush = [&]() -> int {
         if (cur.jobs_idx.empty()) return ES_OK;
+        // (the body fixes the logic; the word count and copy layout come
+        // from num_pis and the cofactor PIs, which an unused PI leaves out
+        // of the code)
         uint64_t key = 0x84222325CBF29CE4ull;
-        for (int j : cur.jobs_idx) key = (key ^ kps[j]->k4->hash) * 0x100000001B3ull + 0x9E37;
+        for (int j : cur.jobs_idx) {
+            key = (key ^ kps[j]->k4->hash) * 0x100000001B3ull + 0x9E37;
+            key = (key ^ (uint64_t)progs[j].num_pis) * 0x100000001B3ull;
+            for (int32_t pi : kps[j]->cof_pis) key = (key ^ (uint64_t)pi) * 0x100000001B3ull;
+        }
         std::lock_guard<std::mutex> lk(g_k4_mu);
         auto it = g_k4_mods.find(key);
         if (it == g_k4_mods.end()) {
+            k4_evict_locked();
             std::vector<char> cubin;
             std::vector<uint32_t> entry;
             std::string err;
+            const double ta = now_ms();
             if (!k4_module(bodies, &cubin, &entry, &err)) { set_error(err); return ES_E_CUDA; }
-            K4Mod m;
-            CK(cudaLibraryLoadData(&m.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
-            CK(cudaLibraryGetKernel(&m.kern, m.lib, "es_k4"));
-            it = g_k4_mods.emplace(key, m).first;
+            auto m = std::make_unique<K4Mod>();
+            const double tb = now_ms();
+            CK(cudaLibraryLoadData(&m->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+            CK(cudaLibraryGetKernel(&m->kern, m->lib, "es_k4"));
+            g_k4_t[0] += tb - ta;
+            g_k4_t[1] += now_ms() - tb;
+            k4_image(*m, cur.jobs_idx, progs, kps, c->sms);
+            it = g_k4_mods.emplace(key, std::move(m)).first;
         }
-        cur.kern = it->second.kern;
+        K4Mod &m = *it->second;
+        const K4Img *img = nullptr;
+        for (const K4Img &x : m.imgs)
+            if (x.dev == c->dev) img = &x;
+        if (!img) {
+            // load the module into this context now (lazy loading would do it
+            // inside the first launch) and upload its image
+            cudaFuncAttributes fa;
+            const double tc = now_ms();
+            CK(cudaFuncGetAttributes(&fa, (const void *)m.kern));
+            g_k4_t[2] += now_ms() - tc;
+            K4Img x;
+            x.dev = c->dev;
+            const size_t jb = ((size_t)m.G * sizeof(K4JobD) + 255) & ~(size_t)255;
+            const size_t ib = m.items.size() * sizeof(K2Item);
+            CK(cudaMalloc(&x.d_img, jb + ib + (size_t)m.G * 8));
+            CK(cudaMemcpy(x.d_img, m.jobs.data(), (size_t)m.G * sizeof(K4JobD), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(x.d_img + jb, m.items.data(), ib, cudaMemcpyHostToDevice));
+            x.d_best0 = (unsigned long long *)(x.d_img + jb + ib);
+            std::vector<unsigned long long> b0(m.G);
+            for (int q = 0; q < m.G; ++q) b0[q] = 1ull << progs[cur.jobs_idx[q]].num_pis;
+            CK(cudaMemcpy(x.d_best0, b0.data(), b0.size() * 8, cudaMemcpyHostToDevice));
+            m.imgs.push_back(x);
+            img = &m.imgs.back();
+        }
+        ++m.users;
+        hold->mods.push_back(&m);
+        cur.mod = &m;
+        cur.img = img;
+        cur.scratch_job0 = job0;
+        job0 += cur.jobs_idx.size();
         mods->push_back(std::move(cur));
         cur = K4Launch();
         bodies.clear();
@@ -1388,99 +1526,70 @@ static int k4_prepare(const es_prog *progs, const K2Prog *const *kps, const std:
     return flush();
 }
 
-// a module's job table and items (round-robin across its jobs, K2's item
-// sizing), uploaded and launched on `st`
-static int k4_launch(K4Launch &m, const es_prog *progs, const K2Prog *const *kps, Ctx *c, cudaStream_t st) {
-    const int T = 256, G = (int)m.jobs_idx.size();
-    auto kwords = [&](int q) {
-        const int j = m.jobs_idx[q];
-        return 1ull << std::max(progs[j].num_pis - 5 - (int)kps[j]->cof_pis.size(), 0);
-    };
-    uint64_t iw = 4096;
-    for (;;) {
-        uint64_t cnt = 0;
-        for (int q = 0; q < G; ++q) {
-            const uint64_t tw = kwords(q);
-            cnt += (tw + std::min(tw, iw) - 1) / std::min(tw, iw);
-        }
-        if (cnt >= (uint64_t)c->sms * 8 || iw <= (uint64_t)T) break;
-        iw >>= 1;
-    }
-    m.jobs.assign(G, K4JobD{});
-    m.n_items.assign(G, 0);
-    m.item_words.assign(G, 0);
-    m.h_best.assign(G, 0);
-    m.h_swept.assign(G, 0);
-    uint64_t max_items = 0;
-    for (int q = 0; q < G; ++q) {
-        const uint64_t tw = kwords(q);
-        m.item_words[q] = std::min<uint64_t>(tw, iw);
-        m.n_items[q] = (tw + m.item_words[q] - 1) / m.item_words[q];
-        max_items = std::max(max_items, m.n_items[q]);
-    }
-    m.items.clear();
-    for (uint64_t r = 0; r < max_items; ++r)
-        for (int q = 0; q < G; ++q)
-            if (r < m.n_items[q]) {
-                const uint64_t w0 = r * m.item_words[q];
-                m.items.push_back(K2Item{w0, (unsigned)std::min<uint64_t>(m.item_words[q], kwords(q) - w0), q});
-            }
+// the run's scratch for every module (best from the modules' sentinels,
+// swept and counters zero), then one launch per module, all on `st`
+struct K4Scratch {
+    uint8_t *d = nullptr;
+    unsigned long long *best = nullptr;
+    unsigned *swept = nullptr, *counter = nullptr;
+    std::vector<unsigned long long> h_best;
+    std::vector<unsigned> h_swept;
+};
+static int k4_launch_all(std::vector<K4Launch> &mods, K4Scratch &sc, Ctx *c, cudaStream_t st) {
+    size_t nj = 0;
+    for (const K4Launch &m : mods) nj += m.jobs_idx.size();
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-    const size_t jobs_b = (size_t)G * sizeof(K4JobD), items_b = m.items.size() * sizeof(K2Item);
-    const size_t best_b = (size_t)G * 8, swept_b = (size_t)G * 4;
-    CK(cudaMallocAsync(&m.d_buf, al(jobs_b) + al(items_b) + al(best_b) + al(swept_b) + 256, st));
-    m.d_jobs = (K4JobD *)m.d_buf;
-    m.d_items = (K2Item *)(m.d_buf + al(jobs_b));
-    m.d_best = (unsigned long long *)(m.d_buf + al(jobs_b) + al(items_b));
-    m.d_swept = (unsigned *)(m.d_buf + al(jobs_b) + al(items_b) + al(best_b));
-    m.d_counter = (unsigned *)(m.d_buf + al(jobs_b) + al(items_b) + al(best_b) + al(swept_b));
-    for (int q = 0; q < G; ++q) {
-        const int j = m.jobs_idx[q];
-        K4JobD &J = m.jobs[q];
-        J.best = m.d_best + q;
-        J.swept = m.d_swept + q;
-        J.total_words = kwords(q);
-        J.valid_mask = lane_valid_mask(progs[j].num_pis);
-        J.body = (unsigned)q;
-        J.cof_n = (int)kps[j]->cof_pis.size();
-        for (int b = 0; b < J.cof_n; ++b) J.cof_pos[b] = (unsigned char)(kps[j]->cof_pis[b] - 1);
-        m.h_best[q] = 1ull << progs[j].num_pis;
+    CK(cudaMallocAsync(&sc.d, al(nj * 8) + al(nj * 4) + al(mods.size() * 4), st));
+    sc.best = (unsigned long long *)sc.d;
+    sc.swept = (unsigned *)(sc.d + al(nj * 8));
+    sc.counter = (unsigned *)(sc.d + al(nj * 8) + al(nj * 4));
+    CK(cudaMemsetAsync(sc.swept, 0, al(nj * 4) + al(mods.size() * 4), st));
+    for (const K4Launch &m : mods)
+        CK(cudaMemcpyAsync(sc.best + m.scratch_job0, m.img->d_best0, m.jobs_idx.size() * 8,
+                           cudaMemcpyDeviceToDevice, st));
+    for (size_t i = 0; i < mods.size(); ++i) {
+        const K4Launch &m = mods[i];
+        const size_t jb = ((size_t)m.mod->G * sizeof(K4JobD) + 255) & ~(size_t)255;
+        K4ParamsD p{(const K4JobD *)m.img->d_img, (const K2Item *)(m.img->d_img + jb),
+                    (unsigned long long)m.mod->items.size(), sc.best + m.scratch_job0, sc.swept + m.scratch_job0,
+                    sc.counter + i, 1u};
+        void *args[] = {&p};
+        const int grid = (int)std::min<uint64_t>(m.mod->items.size(), (uint64_t)c->sms);
+        CK(cudaLaunchKernel((const void *)m.mod->kern, dim3(grid), dim3(256), args, 0, st));
     }
-    CK(cudaMemcpyAsync(m.d_jobs, m.jobs.data(), jobs_b, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(m.d_items, m.items.data(), items_b, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(m.d_best, m.h_best.data(), best_b, cudaMemcpyHostToDevice, st));
-    CK(cudaMemsetAsync(m.d_swept, 0, al(swept_b) + 256, st));  // swept counts and the item counter
-    K4ParamsD p{m.d_jobs, m.d_items, (unsigned long long)m.items.size(), m.d_counter, 1u};
-    void *args[] = {&p};
-    const int grid = (int)std::min<uint64_t>(m.items.size(), (uint64_t)c->sms);
-    CK(cudaLaunchKernel((const void *)m.kern, dim3(grid), dim3(T), args, 0, st));
+    sc.h_best.resize(nj);
+    sc.h_swept.resize(nj);
     return ES_OK;
 }
 
-// es_result of a module's jobs (a whole, unsliced launch: k2_group_results'
+// es_result of the modules' jobs (a whole, unsliced launch: k2_group_results'
 // rules with every item completed)
-static void k4_results(const K4Launch &m, const es_prog *progs, const K2Prog *const *kps, es_result *outs) {
-    for (size_t q = 0; q < m.jobs_idx.size(); ++q) {
-        const int j = m.jobs_idx[q];
-        es_result *r = &outs[j];
-        const int P = progs[j].num_pis;
-        const uint64_t sentinel = 1ull << P;
-        r->engine = ES_ENGINE_JIT;
-        r->launches += 1;
-        r->num_luts = kps[j]->k4->instrs;
-        r->regs_per_thread = 255;
-        const uint64_t item_patterns = (m.item_words[q] * 32) << kps[j]->cof_pis.size();
-        r->patterns_swept = std::min<uint64_t>((uint64_t)m.h_swept[q] * item_patterns, sentinel);
-        if (m.h_best[q] < sentinel) {
-            r->verdict = ES_COUNTEREXAMPLE;
-            r->witness_index = m.h_best[q];
-            r->witness_minimal = 1;
-            r->patterns_evaluated = ref_patterns_for_hit(m.h_best[q], P);
-        } else {
-            r->verdict = ES_EXHAUSTED_ZERO;
-            r->patterns_evaluated = sentinel;
+static void k4_results(const std::vector<K4Launch> &mods, const K4Scratch &sc, const es_prog *progs,
+                       const K2Prog *const *kps, es_result *outs) {
+    for (const K4Launch &m : mods)
+        for (size_t q = 0; q < m.jobs_idx.size(); ++q) {
+            const int j = m.jobs_idx[q];
+            es_result *r = &outs[j];
+            const int P = progs[j].num_pis;
+            const uint64_t sentinel = 1ull << P;
+            const unsigned long long best = sc.h_best[m.scratch_job0 + q];
+            r->engine = ES_ENGINE_JIT;
+            r->launches += 1;
+            r->num_luts = kps[j]->k4->instrs;
+            r->regs_per_thread = 255;
+            const uint64_t item_patterns = (m.mod->item_words[q] * 32) << kps[j]->cof_pis.size();
+            r->patterns_swept = std::min<uint64_t>((uint64_t)sc.h_swept[m.scratch_job0 + q] * item_patterns,
+                                                   sentinel);
+            if (best < sentinel) {
+                r->verdict = ES_COUNTEREXAMPLE;
+                r->witness_index = best;
+                r->witness_minimal = 1;
+                r->patterns_evaluated = ref_patterns_for_hit(best, P);
+            } else {
+                r->verdict = ES_EXHAUSTED_ZERO;
+                r->patterns_evaluated = sentinel;
+            }
         }
-    }
 }
 
 static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &active_in,
@@ -1539,6 +1648,8 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
     // K4: jobs with enough words get a straight-line body (one launch per
     // module of bodies, on its own stream, concurrent with the K2 groups)
     std::vector<K4Launch> k4mods;
+    K4Hold k4hold;
+    K4Scratch k4sc;
     double t_k4 = 0;
     if (!sliced && o.engine != ES_ENGINE_INTERP) {
         std::vector<int> cand;
@@ -1546,7 +1657,7 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
             if (progs[j].num_pis >= k4_min_pis()) cand.push_back(j);
         if (!cand.empty()) {
             const double tk = now_ms();
-            int rc = k4_prepare(progs, kps, cand, &k4mods);
+            int rc = k4_prepare(progs, kps, cand, c, &k4mods, &k4hold);
             if (rc != ES_OK) return rc;
             std::vector<uint8_t> on_k4(n_jobs, 0);
             for (const K4Launch &m : k4mods)
@@ -1607,10 +1718,8 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
             t1 = now_ms();
             CK(cudaEventRecord(c->ev_start, c->stream));
             CK(cudaStreamWaitEvent(c->side[3], c->ev_start, 0));
-            for (K4Launch &m : k4mods) {
-                int rc = k4_launch(m, progs, kps, c, c->side[3]);
-                if (rc != ES_OK) return rc;
-            }
+            int rc = k4_launch_all(k4mods, k4sc, c, c->side[3]);
+            if (rc != ES_OK) return rc;
             CK(cudaEventRecord(c->ev_side[3], c->side[3]));
         }
         for (size_t gi = 0; gi < groups.size(); ++gi) {
@@ -1666,14 +1775,15 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
         CK(cudaMemcpyAsync(gp.h_swept.data(), gp.d_swept, gp.h_swept.size() * 4, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaFreeAsync(gp.d_buf, c->stream));
     }
-    for (K4Launch &m : k4mods) {
-        CK(cudaMemcpyAsync(m.h_best.data(), m.d_best, m.h_best.size() * 8, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaMemcpyAsync(m.h_swept.data(), m.d_swept, m.h_swept.size() * 4, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaFreeAsync(m.d_buf, c->stream));
+    if (!k4mods.empty()) {
+        CK(cudaMemcpyAsync(k4sc.h_best.data(), k4sc.best, k4sc.h_best.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(k4sc.h_swept.data(), k4sc.swept, k4sc.h_swept.size() * 4, cudaMemcpyDeviceToHost,
+                           c->stream));
+        CK(cudaFreeAsync(k4sc.d, c->stream));
     }
     CK(cudaStreamSynchronize(c->stream));
     for (K2Group &gp : groups) k2_group_results(gp, progs, kps, stopped, stop_reason, outs);
-    for (const K4Launch &m : k4mods) k4_results(m, progs, kps, outs);
+    if (!k4mods.empty()) k4_results(k4mods, k4sc, progs, kps, outs);
     for (int j : active) outs[j].device_ms = dev_ms;
     for (const K4Launch &m : k4mods)
         for (int j : m.jobs_idx) outs[j].device_ms = dev_ms;
@@ -1682,9 +1792,10 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
         cudaEventElapsedTime(&ms, c->ev_start, c->ev_side[3]);
         size_t nj = 0, ni = 0;
         int ins = 0;
-        for (const K4Launch &m : k4mods) { nj += m.jobs_idx.size(); ni += m.items.size(); ins += m.instrs; }
+        for (const K4Launch &m : k4mods) { nj += m.jobs_idx.size(); ni += m.mod->items.size(); ins += m.instrs; }
         fprintf(stderr, "[es k4] modules=%zu jobs=%zu items=%zu body-instrs=%d | bodies+modules %.2fms, "
-                        "K4 %.2fms\n", k4mods.size(), nj, ni, ins, t_k4, ms);
+                        "K4 %.2fms | cumulative build %.1f load %.1f ctx-load %.1f ms\n", k4mods.size(), nj, ni,
+                ins, t_k4, ms, g_k4_t[0], g_k4_t[1], g_k4_t[2]);
     }
     if (verbose)
         for (size_t g = 0; g < groups.size(); ++g) {
@@ -2669,6 +2780,14 @@ int word_io(int dev, void *ptr, uint64_t *value, int write) {
 }
 
 void runtime_shutdown() {
+    {
+        std::lock_guard<std::mutex> lk(g_k4_mu);
+        for (auto &kv : g_k4_mods) {
+            for (K4Img &x : kv.second->imgs) cudaFree(x.d_img);
+            cudaLibraryUnload(kv.second->lib);
+        }
+        g_k4_mods.clear();
+    }
     std::lock_guard<std::mutex> lk(g_ctx_mu);
     for (Ctx *c : g_ctx_all) {
         cudaSetDevice(c->dev);

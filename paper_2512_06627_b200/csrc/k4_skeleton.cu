@@ -27,8 +27,6 @@
 // sass_template.py replaces by the call to the placeholder.
 
 struct K4Job {
-    unsigned long long *best;    // min failing pattern, sentinel 2^n
-    unsigned *swept;             // items evaluated (not skipped)
     unsigned long long total_words;  // kernel words (cofactor PIs excluded)
     unsigned valid_mask;         // pattern bits of a word that exist (n < 5)
     unsigned body;               // jump-table index of the job's body
@@ -42,10 +40,14 @@ struct K4Item {
     int job;
 };
 
+// jobs and items are a module's persistent image (built once, position-
+// independent); best / swept / counter are this run's scratch
 struct K4Params {
     const K4Job *jobs;
     const K4Item *items;
     unsigned long long n_items;
+    unsigned long long *best;    // per job: min failing pattern, sentinel 2^n
+    unsigned *swept;             // per job: items evaluated (not skipped)
     unsigned *counter;
     unsigned one;                // == 1, opaque (IMAD coefficients)
 };
@@ -73,8 +75,8 @@ es_k4(const K4Params p)
             } else {
                 const K4Item it = p.items[k];
                 const K4Job &jb = p.jobs[it.job];
-                if (k4_expand(it.w0 << 5, jb) > *(volatile unsigned long long *)jb.best) k = kSkip;
-                else atomicAdd(jb.swept, 1u);
+                if (k4_expand(it.w0 << 5, jb) > *(volatile unsigned long long *)(p.best + it.job)) k = kSkip;
+                else atomicAdd(p.swept + it.job, 1u);
             }
             s_item = k;
         }
@@ -106,7 +108,7 @@ es_k4(const K4Params p)
                     const unsigned long long o = __shfl_xor_sync(0xffffffffu, cand, off);
                     cand = o < cand ? o : cand;
                 }
-                if (lane == 0) atomicMin(job.best, cand);
+                if (lane == 0) atomicMin(p.best + it.job, cand);
             }
         }
     }

@@ -59,8 +59,19 @@ def _placeholder_func(multi: bool, chain: int = CHAIN) -> str:
     return "\n".join(L) + "\n"
 
 
+def _strip_debug(ptx: str) -> str:
+    """The skeleton PTX without line info: with it ptxas embeds the whole
+    placeholder PTX as .nv_debug_ptx_txt (1.4 MB of a 2.3 MB K4 cubin), which
+    every module load would carry for code the host overwrites anyway."""
+    i = ptx.find("\t.section\t.debug_str")
+    if i >= 0:
+        ptx = ptx[:i]
+    return "\n".join(l for l in ptx.split("\n") if l.lstrip().split(maxsplit=1)[:1] not in ([".loc"], [".file"])) + "\n"
+
+
 def placeholder_ptx(skeleton_ptx: str, multi: bool, chain: int = CHAIN) -> str:
     """The skeleton with its ES_BODY marker replaced by a call to es_body."""
+    skeleton_ptx = _strip_debug(skeleton_ptx)
     m = re.search(r"// ES_BODY ([^\n]*)\n", skeleton_ptx)
     assert m, "skeleton without ES_BODY"
     regs = m.group(1).split()
@@ -84,8 +95,8 @@ def placeholder_ptx(skeleton_ptx: str, multi: bool, chain: int = CHAIN) -> str:
 # ptxas records the branch and its targets in EIATTR_INDIRECT_BRANCH_TARGETS,
 # which the library rewrites for the bodies it places.
 K4_THREADS = 256
-K4_TARGETS = 128
-K4_CHAIN = 40000
+K4_TARGETS = 512
+K4_CHAIN = 240000
 MARK_IDX = 0x55555555
 EIATTR_INDIRECT_BRANCH_TARGETS = 0x34
 
@@ -121,6 +132,7 @@ def _placeholder_func_k4(targets: int = K4_TARGETS, chain: int = K4_CHAIN) -> st
 
 
 def placeholder_ptx_k4(skeleton_ptx: str, targets: int = K4_TARGETS, chain: int = K4_CHAIN) -> str:
+    skeleton_ptx = _strip_debug(skeleton_ptx)
     m = re.search(r"// ES_BODY ([^\n]*)\n", skeleton_ptx)
     assert m, "K4 skeleton without ES_BODY"
     regs = m.group(1).split()

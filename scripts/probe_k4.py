@@ -10,6 +10,9 @@ import numpy as np
 from paper_2512_06627_b200 import cones
 
 b = cones.config4_batch(10_000)
+t = time.perf_counter()
+b.prepare()
+prep_ms = (time.perf_counter() - t) * 1e3
 ref = b.run_arrays(engine="interp")
 keys = ("verdict", "witness_index", "patterns_evaluated")
 dev, api = [], []
@@ -23,4 +26,4 @@ for rep in range(5):
 eng = np.bincount(rec["engine"], minlength=3)
 print(f"K4={os.environ.get('ES_K4', '1')} min_pis={os.environ.get('ES_K4_MIN_PIS', '20')} "
       f"device first {dev[0]:.2f} best {min(dev[1:]):.2f} ms | API first {api[0]:.1f} best {min(api[1:]):.1f} ms "
-      f"| engines {eng.tolist()} | interp-only device {float(ref['device_ms'].max()):.2f} ms", flush=True)
+      f"| prepare {prep_ms:.0f} ms | engines {eng.tolist()} | interp-only device {float(ref['device_ms'].max()):.2f} ms", flush=True)
