@@ -19,11 +19,12 @@
 
 namespace es {
 
-// Run fn(0..n-1) on all host cores (one thread per 256 items at most).
+// Run fn(0..n-1) on all host cores (one thread per `grain` items at most:
+// 256 for cheap items, 1 for items of a millisecond, e.g. K4 bodies).
 template <class F>
-inline void parallel_for(int n, F fn) {
+inline void parallel_for(int n, F fn, int grain = 256) {
     const int nt = (int)std::min<int>(std::max(1u, std::thread::hardware_concurrency()),
-                                      std::max(1, n / 256));
+                                      std::max(1, n / std::max(1, grain)));
     std::atomic<int> next{0};
     auto work = [&]() {
         for (;;) {

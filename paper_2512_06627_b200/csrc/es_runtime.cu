@@ -1420,7 +1420,7 @@ static void k4_build_bodies(const es_prog *progs, const K2Prog *const *kps, cons
             }
         }
         kp.k4 = b;
-    });
+    }, 1);
 }
 
 // es_batch_prepare: the bodies of the jobs K4 would take, ahead of the first run

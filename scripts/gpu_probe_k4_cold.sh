@@ -1,0 +1,3 @@
+cd "${GRAFT_REPO_ROOT:-.}"; mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+(ES_VERBOSE=1 timeout 600 python scripts/probe_k4_cold.py; ES_K4=0 timeout 600 python scripts/probe_k4_cold.py) > gpurun_out/probe_k4_cold.txt 2>&1
