@@ -384,13 +384,14 @@ int64_t es_sass_cubin(const es_prog *prog, int32_t k, int32_t block_threads, int
                       char *buf, int64_t cap);
 /* A K4 module without a GPU (k4_skeleton.cu, es_sass.cpp): the direct-SASS
  * bodies of n programs (program i with cof_k[i] cofactor PIs, the same PI
- * choice as es_sass_cubin) written behind the K4 skeleton's indirect branch;
- * body i is jump-table entry i.  stats (n x 4, may be NULL): per body its
+ * choice as es_sass_cubin) written behind the K4 skeleton's indirect branch
+ * of template `variant` (0: one CTA per SM, ~230 body registers; 1: two CTAs,
+ * ~90); body i is jump-table entry i.  stats (n x 4, may be NULL): per body its
  * instructions, then the template's word-index (lo, hi) and result (o0) ...
  * as es_sass_cubin's fields 5..8 in stats[4 * n .. 4 * n + 3].  Returns the
  * cubin's size (buf NULL) or < 0 (a body does not fit). */
-int64_t es_k4_cubin(const es_prog *progs, int32_t n, const int32_t *cof_k, int32_t *stats, char *buf,
-                    int64_t cap);
+int64_t es_k4_cubin(const es_prog *progs, int32_t n, const int32_t *cof_k, int32_t variant, int32_t *stats,
+                    char *buf, int64_t cap);
 int64_t es_jit_check_k(const es_prog *prog, int32_t k, int32_t block_threads, int32_t *regs_per_thread,
                        int32_t *spill_bytes, char *log, int64_t log_cap);
 /* Split build without a GPU: the k-cofactor body cut into `parts` phases,

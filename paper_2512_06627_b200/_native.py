@@ -161,7 +161,7 @@ def lib():
         L.es_emit_ptx_k.restype = ctypes.c_int64
         L.es_sass_cubin.argtypes = [ctypes.POINTER(EsProg), _I, _I, _P, ctypes.c_char_p, ctypes.c_int64]
         L.es_sass_cubin.restype = ctypes.c_int64
-        L.es_k4_cubin.argtypes = [ctypes.POINTER(EsProg), _I, _P, _P, ctypes.c_char_p, ctypes.c_int64]
+        L.es_k4_cubin.argtypes = [ctypes.POINTER(EsProg), _I, _P, _I, _P, ctypes.c_char_p, ctypes.c_int64]
         L.es_k4_cubin.restype = ctypes.c_int64
         L.es_emit_body_k.argtypes = [ctypes.POINTER(EsProg), _I, _I, _I, _P, ctypes.c_char_p, ctypes.c_int64]
         L.es_emit_body_k.restype = ctypes.c_int64

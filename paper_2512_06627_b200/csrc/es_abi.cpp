@@ -222,9 +222,12 @@ int64_t es_sass_cubin(const es_prog *prog, int32_t k, int32_t block_threads, int
     return n;
 }
 
-int64_t es_k4_cubin(const es_prog *progs, int32_t n, const int32_t *cof_k, int32_t *stats, char *buf,
-                    int64_t cap) {
-    if (!progs || n <= 0 || n > k4_max_bodies()) { set_error("bad argument"); return ES_E_BAD_ARG; }
+int64_t es_k4_cubin(const es_prog *progs, int32_t n, const int32_t *cof_k, int32_t variant, int32_t *stats,
+                    char *buf, int64_t cap) {
+    if (!progs || n <= 0 || variant < 0 || variant >= k4_variants() || n > k4_max_bodies(variant)) {
+        set_error("bad argument");
+        return ES_E_BAD_ARG;
+    }
     std::vector<std::vector<uint64_t>> code(n);
     SassStats ss;
     for (int i = 0; i < n; ++i) {
@@ -232,7 +235,8 @@ int64_t es_k4_cubin(const es_prog *progs, int32_t n, const int32_t *cof_k, int32
         int rc = map_prog(&progs[i], &net, cof_k ? cof_k[i] : 0);
         if (rc != ES_OK) return rc;
         std::string err;
-        if (!k4_body(net, &code[i], &ss, &err)) { set_error(err); return ES_E_BAD_ARG; }
+        int used = 0;
+        if (!k4_body(net, variant, &code[i], &ss, &used, &err)) { set_error(err); return ES_E_BAD_ARG; }
         if (stats) stats[4 * i] = ss.instrs;
     }
     if (stats) {
@@ -246,7 +250,7 @@ int64_t es_k4_cubin(const es_prog *progs, int32_t n, const int32_t *cof_k, int32
     std::vector<char> cubin;
     std::vector<uint32_t> entry;
     std::string err;
-    if (!k4_module(bodies, &cubin, &entry, &err)) { set_error(err); return ES_E_BAD_ARG; }
+    if (!k4_module(bodies, variant, &cubin, &entry, &err)) { set_error(err); return ES_E_BAD_ARG; }
     const int64_t sz = (int64_t)cubin.size();
     if (!buf) return sz;
     if (cap < sz) { set_error("buffer too small"); return ES_E_BAD_ARG; }

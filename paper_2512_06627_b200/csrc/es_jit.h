@@ -78,10 +78,16 @@ bool sass_direct_cubin(const LutNet &net, int threads, std::vector<char> *cubin,
 // K4 (k4_skeleton.cu): one job's body for the multi-body skeleton (encoded
 // (lo, hi) words, position-independent), and a module of bodies behind the
 // skeleton's indirect branch (body i = jump-table entry i)
-bool k4_body(const LutNet &net, std::vector<uint64_t> *words, SassStats *st, std::string *err);
-bool k4_module(const std::vector<const std::vector<uint64_t> *> &bodies, std::vector<char> *cubin,
+// Template variants differ in CTAs per SM (k4_blocks: 1 = ~230 body
+// registers, 2 = ~90); k4_body with variant < 0 picks the most-CTA variant
+// the body's registers fit and returns it in *used.
+int k4_variants();
+int k4_blocks(int variant);
+bool k4_body(const LutNet &net, int variant, std::vector<uint64_t> *words, SassStats *st, int *used,
+             std::string *err);
+bool k4_module(const std::vector<const std::vector<uint64_t> *> &bodies, int variant, std::vector<char> *cubin,
                std::vector<uint32_t> *entry, std::string *err);
-int k4_body_capacity();  // instruction slots of one module
-int k4_max_bodies();     // bodies per module
+int k4_body_capacity(int variant);  // instruction slots of one module
+int k4_max_bodies(int variant);     // bodies per module
 
 }  // namespace es

@@ -38,6 +38,7 @@ struct K4Body {
     std::vector<uint64_t> code;  // encoded instructions, (lo, hi) pairs
     uint64_t hash = 0;           // of `code` (module cache key)
     int instrs = 0;
+    int variant = 0;             // K4 template variant (es_jit.h k4_blocks)
     bool ok = false;             // false: no body (too many registers / slots)
 };
 

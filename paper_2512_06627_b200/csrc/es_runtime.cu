@@ -560,8 +560,9 @@ struct Ctx {
     unsigned *d_counter = nullptr;         // [2] per in-flight slice
     unsigned long long *h_pin = nullptr;   // [4]
     cudaEvent_t ev_start = nullptr, ev_stop = nullptr, ev_slice[2] = {nullptr, nullptr};
-    cudaStream_t side[4] = {nullptr, nullptr, nullptr, nullptr};  // concurrent K2 launch groups + K4
-    cudaEvent_t ev_side[4] = {nullptr, nullptr, nullptr, nullptr};
+    // concurrent K2 launch groups [0, 3) and K4 module launches [3, 7)
+    cudaStream_t side[7] = {};
+    cudaEvent_t ev_side[7] = {};
     uint4 *h_stage = nullptr;  // pinned staging of K2 program records (grown on demand)
     size_t stage_cap = 0;      // in records
 };
@@ -607,7 +608,7 @@ int make_ctx(int dev, Ctx *c) {
     CK(cudaEventCreate(&c->ev_stop));
     CK(cudaEventCreateWithFlags(&c->ev_slice[0], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_slice[1], cudaEventDisableTiming));
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < 7; ++q) {
         CK(cudaStreamCreateWithFlags(&c->side[q], cudaStreamNonBlocking));
         CK(cudaEventCreate(&c->ev_side[q]));
     }
@@ -1299,8 +1300,9 @@ struct K4Img {
 struct K4Mod {
     cudaLibrary_t lib = nullptr;
     cudaKernel_t kern = nullptr;
+    int variant = 0, blocks = 1;
     int G = 0;
-    std::vector<uint64_t> n_items, item_words;
+    std::vector<uint64_t> n_items;
     std::vector<K4JobD> jobs;
     std::vector<K2Item> items;
     std::vector<K4Img> imgs;
@@ -1351,50 +1353,59 @@ static uint64_t hash_words(const std::vector<uint64_t> &w) {
     return h;
 }
 
-// a module's host image: job table and items, round-robin across its jobs
-// (K2's item sizing: 4096 words, halved until >= 8 items per SM)
+// a module's host image: job table and items of kK4ItemWords words (a CTA
+// claims one and runs kK4ItemWords / 256 body calls per thread; fixed 4096
+// measured 2.48 ms on config 4 against 1.76 with K2's halving rule, 8192 /
+// 16384: 3.27 / 3.78).  Order:
+// every job's first item round-robin -- a non-equivalent job usually settles
+// its minimum there and its later items are skipped -- then the rest job by
+// job, so the CTAs sweeping a job share its body in L2 (job-major
+// throughout measured 1.9x slower on config 4: non-equivalent jobs' items
+// claimed before their minimum lands)
+constexpr uint64_t kK4ItemWords = 4096;
 static void k4_image(K4Mod &m, const std::vector<int> &jobs_idx, const es_prog *progs,
                      const K2Prog *const *kps, int sms) {
-    const int T = 256, G = (int)jobs_idx.size();
+    const int G = (int)jobs_idx.size();
     m.G = G;
     auto kwords = [&](int q) {
         const int j = jobs_idx[q];
         return 1ull << std::max(progs[j].num_pis - 5 - (int)kps[j]->cof_pis.size(), 0);
     };
-    uint64_t iw = 4096;
+    // halved (down to one CTA pass) until the module has >= 8 items per resident CTA
+    uint64_t iw = getenv("ES_K4_ITEM") ? (uint64_t)atoi(getenv("ES_K4_ITEM")) : kK4ItemWords;
     for (;;) {
         uint64_t cnt = 0;
         for (int q = 0; q < G; ++q) {
             const uint64_t tw = kwords(q);
             cnt += (tw + std::min(tw, iw) - 1) / std::min(tw, iw);
         }
-        if (cnt >= (uint64_t)sms * 8 || iw <= (uint64_t)T) break;
+        if (cnt >= (uint64_t)sms * 8 || iw <= 256) break;
         iw >>= 1;
     }
     m.jobs.assign(G, K4JobD{});
     m.n_items.assign(G, 0);
-    m.item_words.assign(G, 0);
-    uint64_t max_items = 0;
     for (int q = 0; q < G; ++q) {
         const int j = jobs_idx[q];
-        const uint64_t tw = kwords(q);
-        m.item_words[q] = std::min<uint64_t>(tw, iw);
-        m.n_items[q] = (tw + m.item_words[q] - 1) / m.item_words[q];
-        max_items = std::max(max_items, m.n_items[q]);
         K4JobD &J = m.jobs[q];
-        J.total_words = tw;
+        J.total_words = kwords(q);
         J.valid_mask = lane_valid_mask(progs[j].num_pis);
         J.body = (unsigned)q;
         J.cof_n = (int)kps[j]->cof_pis.size();
         for (int b = 0; b < J.cof_n; ++b) J.cof_pos[b] = (unsigned char)(kps[j]->cof_pis[b] - 1);
     }
     m.items.clear();
-    for (uint64_t r = 0; r < max_items; ++r)
-        for (int q = 0; q < G; ++q)
-            if (r < m.n_items[q]) {
-                const uint64_t w0 = r * m.item_words[q];
-                m.items.push_back(K2Item{w0, (unsigned)std::min<uint64_t>(m.item_words[q], kwords(q) - w0), q});
-            }
+    for (int q = 0; q < G; ++q) {
+        const uint64_t tw = kwords(q);
+        m.items.push_back(K2Item{0, (unsigned)std::min(tw, iw), q});
+        m.n_items[q] = 1;
+    }
+    for (int q = 0; q < G; ++q) {
+        const uint64_t tw = kwords(q);
+        for (uint64_t w0 = std::min(tw, iw); w0 < tw; w0 += iw) {
+            m.items.push_back(K2Item{w0, (unsigned)std::min(iw, tw - w0), q});
+            m.n_items[q]++;
+        }
+    }
 }
 
 // K4 bodies of the jobs that lack one, on all host cores (a job whose body
@@ -1413,7 +1424,7 @@ static void k4_build_bodies(const es_prog *progs, const K2Prog *const *kps, cons
             LutNet net;
             map_cofactored(dag, kp.cof_pis, &net);
             SassStats st;
-            if (k4_body(net, &b->code, &st, &err)) {
+            if (k4_body(net, -1, &b->code, &st, &b->variant, &err)) {
                 b->ok = true;
                 b->instrs = st.instrs;
                 b->hash = hash_words(b->code);
@@ -1439,7 +1450,7 @@ static int k4_prepare(const es_prog *progs, const K2Prog *const *kps, const std:
                       std::vector<K4Launch> *mods, K4Hold *hold) {
     NvtxRange nvtx("es_k4_prepare");
     k4_build_bodies(progs, kps, cand);
-    const int cap = k4_body_capacity(), maxb = k4_max_bodies();
+    int variant = 0;
     K4Launch cur;
     int slots = 0;
     size_t job0 = 0;
@@ -1463,14 +1474,16 @@ static int k4_prepare(const es_prog *progs, const K2Prog *const *kps, const std:
             std::vector<uint32_t> entry;
             std::string err;
             const double ta = now_ms();
-            if (!k4_module(bodies, &cubin, &entry, &err)) { set_error(err); return ES_E_CUDA; }
+            if (!k4_module(bodies, variant, &cubin, &entry, &err)) { set_error(err); return ES_E_CUDA; }
             auto m = std::make_unique<K4Mod>();
             const double tb = now_ms();
             CK(cudaLibraryLoadData(&m->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
             CK(cudaLibraryGetKernel(&m->kern, m->lib, "es_k4"));
             g_k4_t[0] += tb - ta;
             g_k4_t[1] += now_ms() - tb;
-            k4_image(*m, cur.jobs_idx, progs, kps, c->sms);
+            m->variant = variant;
+            m->blocks = k4_blocks(variant);
+            k4_image(*m, cur.jobs_idx, progs, kps, c->sms * m->blocks);
             it = g_k4_mods.emplace(key, std::move(m)).first;
         }
         K4Mod &m = *it->second;
@@ -1510,20 +1523,25 @@ static int k4_prepare(const es_prog *progs, const K2Prog *const *kps, const std:
         slots = 0;
         return ES_OK;
     };
-    for (int j : cand) {
-        const K4Body &b = *kps[j]->k4;
-        if (!b.ok) continue;
-        const int need = (int)b.code.size() / 2 + 1;
-        if (!cur.jobs_idx.empty() && ((int)cur.jobs_idx.size() >= maxb || slots + need > cap)) {
-            int rc = flush();
-            if (rc != ES_OK) return rc;
+    for (variant = 0; variant < k4_variants(); ++variant) {  // one run of modules per template variant
+        const int cap = k4_body_capacity(variant), maxb = k4_max_bodies(variant);
+        for (int j : cand) {
+            const K4Body &b = *kps[j]->k4;
+            if (!b.ok || b.variant != variant) continue;
+            const int need = (int)b.code.size() / 2 + 1;
+            if (!cur.jobs_idx.empty() && ((int)cur.jobs_idx.size() >= maxb || slots + need > cap)) {
+                int rc = flush();
+                if (rc != ES_OK) return rc;
+            }
+            cur.jobs_idx.push_back(j);
+            bodies.push_back(&b.code);
+            slots += need;
+            cur.instrs += b.instrs;
         }
-        cur.jobs_idx.push_back(j);
-        bodies.push_back(&b.code);
-        slots += need;
-        cur.instrs += b.instrs;
+        int rc = flush();
+        if (rc != ES_OK) return rc;
     }
-    return flush();
+    return ES_OK;
 }
 
 // the run's scratch for every module (best from the modules' sentinels,
@@ -1535,6 +1553,7 @@ struct K4Scratch {
     std::vector<unsigned long long> h_best;
     std::vector<unsigned> h_swept;
 };
+constexpr int kK4Streams = 4;  // module launches round-robin over side[3..6]: one module's tail overlaps the next
 static int k4_launch_all(std::vector<K4Launch> &mods, K4Scratch &sc, Ctx *c, cudaStream_t st) {
     size_t nj = 0;
     for (const K4Launch &m : mods) nj += m.jobs_idx.size();
@@ -1547,6 +1566,8 @@ static int k4_launch_all(std::vector<K4Launch> &mods, K4Scratch &sc, Ctx *c, cud
     for (const K4Launch &m : mods)
         CK(cudaMemcpyAsync(sc.best + m.scratch_job0, m.img->d_best0, m.jobs_idx.size() * 8,
                            cudaMemcpyDeviceToDevice, st));
+    CK(cudaEventRecord(c->ev_side[3], st));
+    for (int q = 1; q < kK4Streams; ++q) CK(cudaStreamWaitEvent(c->side[3 + q], c->ev_side[3], 0));
     for (size_t i = 0; i < mods.size(); ++i) {
         const K4Launch &m = mods[i];
         const size_t jb = ((size_t)m.mod->G * sizeof(K4JobD) + 255) & ~(size_t)255;
@@ -1554,9 +1575,11 @@ static int k4_launch_all(std::vector<K4Launch> &mods, K4Scratch &sc, Ctx *c, cud
                     (unsigned long long)m.mod->items.size(), sc.best + m.scratch_job0, sc.swept + m.scratch_job0,
                     sc.counter + i, 1u};
         void *args[] = {&p};
-        const int grid = (int)std::min<uint64_t>(m.mod->items.size(), (uint64_t)c->sms);
-        CK(cudaLaunchKernel((const void *)m.mod->kern, dim3(grid), dim3(256), args, 0, st));
+        const int grid = (int)std::min<uint64_t>(m.mod->items.size(), (uint64_t)c->sms * m.mod->blocks);
+        CK(cudaLaunchKernel((const void *)m.mod->kern, dim3(grid), dim3(256), args, 0,
+                            c->side[3 + (int)(i % kK4Streams)]));
     }
+    for (int q = 0; q < kK4Streams; ++q) CK(cudaEventRecord(c->ev_side[3 + q], c->side[3 + q]));
     sc.h_best.resize(nj);
     sc.h_swept.resize(nj);
     return ES_OK;
@@ -1577,9 +1600,9 @@ static void k4_results(const std::vector<K4Launch> &mods, const K4Scratch &sc, c
             r->launches += 1;
             r->num_luts = kps[j]->k4->instrs;
             r->regs_per_thread = 255;
-            const uint64_t item_patterns = (m.mod->item_words[q] * 32) << kps[j]->cof_pis.size();
-            r->patterns_swept = std::min<uint64_t>((uint64_t)sc.h_swept[m.scratch_job0 + q] * item_patterns,
-                                                   sentinel);
+            // swept = kernel words of the evaluated items, each 32 patterns x 2^k copies
+            r->patterns_swept = std::min<uint64_t>(((uint64_t)sc.h_swept[m.scratch_job0 + q] * 32)
+                                                       << kps[j]->cof_pis.size(), sentinel);
             if (best < sentinel) {
                 r->verdict = ES_COUNTEREXAMPLE;
                 r->witness_index = best;
@@ -1720,7 +1743,6 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
             CK(cudaStreamWaitEvent(c->side[3], c->ev_start, 0));
             int rc = k4_launch_all(k4mods, k4sc, c, c->side[3]);
             if (rc != ES_OK) return rc;
-            CK(cudaEventRecord(c->ev_side[3], c->side[3]));
         }
         for (size_t gi = 0; gi < groups.size(); ++gi) {
             const size_t g = groups.size() - 1 - gi;
@@ -1742,18 +1764,20 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
         // join only now: a join inside the loop would order the next group's
         // allocation (on the main stream) after this group's kernel
         for (size_t g = 0; g < groups.size(); ++g) CK(cudaStreamWaitEvent(c->stream, c->ev_side[g], 0));
-        if (!k4mods.empty()) CK(cudaStreamWaitEvent(c->stream, c->ev_side[3], 0));
+        if (!k4mods.empty())
+            for (int q = 0; q < kK4Streams; ++q) CK(cudaStreamWaitEvent(c->stream, c->ev_side[3 + q], 0));
         CK(cudaStreamSynchronize(c->stream));
         for (size_t g = 0; g < groups.size(); ++g) {
             float ms = 0;
             CK(cudaEventElapsedTime(&ms, c->ev_start, c->ev_side[g]));
             dev_ms = std::max(dev_ms, ms);
         }
-        if (!k4mods.empty()) {
-            float ms = 0;
-            CK(cudaEventElapsedTime(&ms, c->ev_start, c->ev_side[3]));
-            dev_ms = std::max(dev_ms, ms);
-        }
+        if (!k4mods.empty())
+            for (int q = 0; q < kK4Streams; ++q) {
+                float ms = 0;
+                CK(cudaEventElapsedTime(&ms, c->ev_start, c->ev_side[3 + q]));
+                dev_ms = std::max(dev_ms, ms);
+            }
     } else {
         // budget / cancel: groups in turn, in slices, checking between slices
         for (K2Group &gp : groups) {
@@ -1789,7 +1813,11 @@ static int run_k2(int n_jobs, const es_prog *progs, const std::vector<int> &acti
         for (int j : m.jobs_idx) outs[j].device_ms = dev_ms;
     if (verbose && !k4mods.empty()) {
         float ms = -1;
-        cudaEventElapsedTime(&ms, c->ev_start, c->ev_side[3]);
+        for (int q = 0; q < kK4Streams; ++q) {
+            float x = -1;
+            cudaEventElapsedTime(&x, c->ev_start, c->ev_side[3 + q]);
+            ms = std::max(ms, x);
+        }
         size_t nj = 0, ni = 0;
         int ins = 0;
         for (const K4Launch &m : k4mods) { nj += m.jobs_idx.size(); ni += m.mod->items.size(); ins += m.instrs; }
@@ -2800,7 +2828,7 @@ void runtime_shutdown() {
         cudaEventDestroy(c->ev_stop);
         cudaEventDestroy(c->ev_slice[0]);
         cudaEventDestroy(c->ev_slice[1]);
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < 7; ++q) {
             cudaStreamDestroy(c->side[q]);
             cudaEventDestroy(c->ev_side[q]);
         }

@@ -13,11 +13,14 @@
 // its placeholder once, at build time).  Everything around the body follows
 // es_k2d (es_runtime.cu):
 //
-//  * work items (<= 2^chunk words of one job) are dealt round-robin across
-//    jobs; a CTA claims items in order from a device counter and skips an
-//    item whose first pattern lies above the job's current minimum, so a
-//    job's every item below its final minimum is swept and the answer is
-//    the reference's workers=1 witness (es.py:297-320);
+//  * work items (a run of one job's words) come in the host's order: every
+//    job's first item round-robin, then the rest job by job; a CTA claims
+//    items in order from a device counter and skips an item whose first
+//    pattern lies above the job's current minimum, so a job's every item
+//    below its final minimum is swept and the answer is the reference's
+//    workers=1 witness (es.py:297-320).  The whole CTA runs one job's body at
+//    a time: warps of one SM on different bodies thrash the 32 KB L1.5
+//    instruction cache (per-warp claims measured 7x slower on config 4);
 //  * one thread evaluates one kernel word per body call; the body returns
 //    the first failing cofactor copy's output word and that copy's number
 //    (es_sass.cpp's branch-free fold), the warp reduces the minimum pattern
@@ -47,7 +50,7 @@ struct K4Params {
     const K4Item *items;
     unsigned long long n_items;
     unsigned long long *best;    // per job: min failing pattern, sentinel 2^n
-    unsigned *swept;             // per job: items evaluated (not skipped)
+    unsigned *swept;             // per job: kernel words of the items evaluated (not skipped)
     unsigned *counter;
     unsigned one;                // == 1, opaque (IMAD coefficients)
 };
@@ -61,7 +64,11 @@ __device__ __forceinline__ unsigned long long k4_expand(unsigned long long x, co
     return x;
 }
 
-extern "C" __global__ void __launch_bounds__(ES_THREADS)
+#ifndef ES_MIN_BLOCKS
+#define ES_MIN_BLOCKS 1  // 2: the 128-register variant (two CTAs per SM)
+#endif
+
+extern "C" __global__ void __launch_bounds__(ES_THREADS, ES_MIN_BLOCKS)
 es_k4(const K4Params p)
 {
     __shared__ unsigned long long s_item;
@@ -76,7 +83,7 @@ es_k4(const K4Params p)
                 const K4Item it = p.items[k];
                 const K4Job &jb = p.jobs[it.job];
                 if (k4_expand(it.w0 << 5, jb) > *(volatile unsigned long long *)(p.best + it.job)) k = kSkip;
-                else atomicAdd(p.swept + it.job, 1u);
+                else atomicAdd(p.swept + it.job, it.n_words);
             }
             s_item = k;
         }

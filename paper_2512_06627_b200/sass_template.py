@@ -97,11 +97,16 @@ def placeholder_ptx(skeleton_ptx: str, multi: bool, chain: int = CHAIN) -> str:
 K4_THREADS = 256
 K4_TARGETS = 512
 K4_CHAIN = 240000
+# (min CTAs per SM, live values of the placeholder, chain): the 1-CTA variant
+# gives a body ~230 registers; the 2-CTA one (__launch_bounds__(256, 2),
+# 128 registers) doubles the warps per SM for the bodies that fit it
+K4_VARIANTS = ((1, 230, 240000), (2, 96, 160000))
 MARK_IDX = 0x55555555
 EIATTR_INDIRECT_BRANCH_TARGETS = 0x34
 
 
-def _placeholder_func_k4(targets: int = K4_TARGETS, chain: int = K4_CHAIN) -> str:
+def _placeholder_func_k4(targets: int = K4_TARGETS, chain: int = K4_CHAIN, live: int = LIVE) -> str:
+    LIVE = live
     rng = random.Random(4321)
     L = [".func (.param .b64 es_pr) es_body(.param .b32 es_pw0, .param .b32 es_pw1, .param .b32 es_pw2, "
          ".param .b32 es_pw3)", "{",
@@ -131,7 +136,8 @@ def _placeholder_func_k4(targets: int = K4_TARGETS, chain: int = K4_CHAIN) -> st
     return "\n".join(L) + "\n"
 
 
-def placeholder_ptx_k4(skeleton_ptx: str, targets: int = K4_TARGETS, chain: int = K4_CHAIN) -> str:
+def placeholder_ptx_k4(skeleton_ptx: str, targets: int = K4_TARGETS, chain: int = K4_CHAIN,
+                       live: int = LIVE) -> str:
     skeleton_ptx = _strip_debug(skeleton_ptx)
     m = re.search(r"// ES_BODY ([^\n]*)\n", skeleton_ptx)
     assert m, "K4 skeleton without ES_BODY"
@@ -144,7 +150,7 @@ def placeholder_ptx_k4(skeleton_ptx: str, targets: int = K4_TARGETS, chain: int 
             f"mov.b64 {{{outs[0]}, {outs[1]}}}, %esret;", "}"]
     body = skeleton_ptx[:m.start()] + "\n".join(call) + "\n" + skeleton_ptx[m.end():]
     hdr = body.index("\n", body.index(".address_size 64")) + 1
-    return body[:hdr] + _placeholder_func_k4(targets, chain) + body[hdr:]
+    return body[:hdr] + _placeholder_func_k4(targets, chain, live) + body[hdr:]
 
 
 def _nv_info_attr(cubin: bytes, section: str, attr: int) -> tuple[int, int]:
@@ -222,38 +228,44 @@ def analyse_k4(cubin_path: str, cuobjdump: str) -> dict:
 
 
 def build_k4_template(build_dir: str, ptxas: str, cuobjdump: str, arch: str = "sm_100a") -> str:
-    """Compile the K4 placeholder skeleton; write k4_sass_template.inc."""
-    skel = open(os.path.join(build_dir, f"k4_skeleton_{K4_THREADS}.ptx")).read()
-    ptx = os.path.join(build_dir, "k4_sass.ptx")
-    cub = os.path.join(build_dir, "k4_sass.cubin")
-    open(ptx, "w").write(placeholder_ptx_k4(skel))
-    subprocess.run([ptxas, f"-arch={arch}", "-O3", ptx, "-o", cub], check=True, capture_output=True)
-    info = analyse_k4(cub, cuobjdump)
-    data = no_opportunistic_finalization(open(cub, "rb").read())
-    text_off = _elf_text_offset(data, ".text.es_k4")
-    ibt_off, ibt_size = _nv_info_attr(data, ".nv.info.es_k4", EIATTR_INDIRECT_BRANCH_TARGETS)
-    off0, _, count = struct.unpack_from("<III", data, ibt_off)
-    assert count == K4_TARGETS and ibt_size == 12 + 4 * count, (count, ibt_size)
-    tab = [(o, sz) for n, _, o, sz in _sections(data) if n == ".nv.constant2.es_k4"]
-    assert len(tab) == 1 and tab[0][1] == 4 * K4_TARGETS, f"K4 placeholder: jump table {tab}"
-    assert not [n for n, _, o, sz in _sections(data) if n == ".rela.nv.constant2.es_k4" and sz]
-    clob = [0, 0, 0, 0]
-    for r in info["clobber"]:
-        clob[r // 64] |= 1 << (r % 64)
-    disp = []
-    for a in info["dispatch"]:
-        disp += list(struct.unpack_from("<QQ", data, text_off + a))
-    out = [f"static const unsigned char kSassK4_cubin[] = {{{','.join(str(b) for b in data)}}};\n",
-           f"static const K4Template kSassK4 = {{kSassK4_cubin, sizeof(kSassK4_cubin), {K4_THREADS}, "
-           f"{text_off}ull, {info['start']}ull, {info['end']}ull, {info['ret_reg']}, {info['ret_pair']}, "
-           f"{info['lo']}, {info['hi']}, {info['o0']}, {info['o1']}, {ibt_off}ull, {count}, {tab[0][0]}ull, "
-           f"{{{', '.join(f'{c}ull' for c in clob)}}}, {{{', '.join(f'{x}ull' for x in disp)}}}}};\n"]
+    """Compile the K4 placeholder skeletons (K4_VARIANTS); write
+    k4_sass_template.inc with the table kSassK4Variants."""
+    out, names = [], []
+    for blocks, live, chain in K4_VARIANTS:
+        skel = open(os.path.join(build_dir, f"k4_skeleton_{K4_THREADS}_{blocks}.ptx")).read()
+        ptx = os.path.join(build_dir, f"k4_sass_{blocks}.ptx")
+        cub = os.path.join(build_dir, f"k4_sass_{blocks}.cubin")
+        open(ptx, "w").write(placeholder_ptx_k4(skel, K4_TARGETS, chain, live))
+        subprocess.run([ptxas, f"-arch={arch}", "-O3", ptx, "-o", cub], check=True, capture_output=True)
+        info = analyse_k4(cub, cuobjdump)
+        data = no_opportunistic_finalization(open(cub, "rb").read())
+        text_off = _elf_text_offset(data, ".text.es_k4")
+        ibt_off, ibt_size = _nv_info_attr(data, ".nv.info.es_k4", EIATTR_INDIRECT_BRANCH_TARGETS)
+        off0, _, count = struct.unpack_from("<III", data, ibt_off)
+        assert count == K4_TARGETS and ibt_size == 12 + 4 * count, (count, ibt_size)
+        tab = [(o, sz) for n, _, o, sz in _sections(data) if n == ".nv.constant2.es_k4"]
+        assert len(tab) == 1 and tab[0][1] == 4 * K4_TARGETS, f"K4 placeholder: jump table {tab}"
+        assert not [n for n, _, o, sz in _sections(data) if n == ".rela.nv.constant2.es_k4" and sz]
+        clob = [0, 0, 0, 0]
+        for r in info["clobber"]:
+            clob[r // 64] |= 1 << (r % 64)
+        disp = []
+        for a in info["dispatch"]:
+            disp += list(struct.unpack_from("<QQ", data, text_off + a))
+        nm = f"kSassK4_{blocks}"
+        names.append(nm)
+        out.append(f"static const unsigned char {nm}_cubin[] = {{{','.join(str(b) for b in data)}}};\n")
+        out.append(
+            f"static const K4Template {nm} = {{{nm}_cubin, sizeof({nm}_cubin), {K4_THREADS}, {blocks}, "
+            f"{text_off}ull, {info['start']}ull, {info['end']}ull, {info['ret_reg']}, {info['ret_pair']}, "
+            f"{info['lo']}, {info['hi']}, {info['o0']}, {info['o1']}, {ibt_off}ull, {count}, {tab[0][0]}ull, "
+            f"{{{', '.join(f'{c}ull' for c in clob)}}}, {{{', '.join(f'{x}ull' for x in disp)}}}}};\n")
+    out.append("static const K4Template *const kSassK4Variants[] = {" + ", ".join(f"&{n}" for n in names) + "};\n")
     inc = os.path.join(build_dir, "k4_sass_template.inc")
     with open(inc, "w") as fh:
         fh.write("// generated by sass_template.py (build time) -- do not edit\n")
         fh.writelines(out)
     return inc
-
 
 def _sections(cubin: bytes):
     """(name, type, file offset, size) of every section of a 64-bit ELF."""
