@@ -132,3 +132,20 @@ def test_large_drives(gpu):
     torch.cuda.synchronize()
     assert np.array_equal(d_out.cpu().numpy().view(np.uint64), want)
     ds.close()
+
+
+@pytest.mark.parametrize("pipe", ["0", "1"])
+def test_batch_schedules_and_lanes(gpu, monkeypatch, pipe):
+    """Both batch schedules (level batches; the distance-2 list schedule of
+    the software-pipelined kernel, ES_SIM_PIPE) at every lanes-per-word count
+    (ES_SIM_G) equal the numpy oracle, on random XAGs (ragged last batches,
+    duplicate fanins, narrow tails) and the configs[2] miter."""
+    monkeypatch.setenv("ES_SIM_PIPE", pipe)
+    rng = random.Random(29)
+    cases = [random_xag(rng.randint(2, 24), rng.randint(1, 1500), 900 + k) for k in range(4)]
+    cases.append(M.gen_multiplier_miter(16, "array", "booth"))
+    for g in ("1", "2", "4", "8"):
+        monkeypatch.setenv("ES_SIM_G", g)
+        for k, x in enumerate(cases):
+            pw = sim.random_pi_words(x.num_pis, rng.choice([1, 33, 300, 2051]), k)
+            assert np.array_equal(sim.simulate(x, pw), O.simulate(x, pw)), (pipe, g, k)
