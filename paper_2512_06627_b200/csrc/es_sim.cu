@@ -100,6 +100,57 @@ __global__ void __launch_bounds__(256) es_sim_kernel(const SimRec *__restrict__ 
     }
 }
 
+// Software-pipelined variant (SimProg::pipe): the host schedules batches so
+// that batch t+1 reads no row written by batch t (every fanin was stored two
+// or more batches earlier), so each thread issues batch t+1's fanin loads
+// before it computes and stores batch t -- two batches' loads in flight, one
+// round trip per two batches on the level chain instead of one per batch.
+template <int G>
+__global__ void __launch_bounds__(256) es_sim_pipe_kernel(const SimRec *__restrict__ recs, int n_batches,
+                                                          long long w_begin, long long w_end,
+                                                          long long words,
+                                                          unsigned long long *__restrict__ vals) {
+    constexpr int U = kSimU / G;
+    const int gi = threadIdx.x % G;
+    const long long w = w_begin + ((long long)blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const bool active = w < w_end;
+    if (__all_sync(0xffffffffu, !active) || n_batches <= 0) return;
+    unsigned long long x[U], y[U];
+    uint32_t d[U], f[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const SimRec r = recs[gi + u * G];
+        d[u] = r.d; f[u] = r.f;
+        x[u] = active ? vals[(long long)r.a * words + w] : 0ull;
+        y[u] = active ? vals[(long long)r.b * words + w] : 0ull;
+    }
+    for (int bt = 0; bt < n_batches; ++bt) {
+        unsigned long long nx[U], ny[U];
+        uint32_t nd[U], nf[U];
+        const bool more = bt + 1 < n_batches;
+        const SimRec *rb = recs + (more ? bt + 1 : bt) * kSimU + gi;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const SimRec r = rb[u * G];
+            nd[u] = r.d; nf[u] = r.f;
+            nx[u] = (active && more) ? vals[(long long)r.a * words + w] : 0ull;
+            ny[u] = (active && more) ? vals[(long long)r.b * words + w] : 0ull;
+        }
+        if (active) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (f[u] & 8u) continue;
+                const unsigned long long xa = (f[u] & 2u) ? ~x[u] : x[u];
+                const unsigned long long yb = (f[u] & 4u) ? ~y[u] : y[u];
+                vals[(long long)d[u] * words + w] = (f[u] & 1u) ? (xa ^ yb) : (xa & yb);
+            }
+        }
+        if (G > 1) __syncwarp();
+#pragma unroll
+        for (int u = 0; u < U; ++u) { x[u] = nx[u]; y[u] = ny[u]; d[u] = nd[u]; f[u] = nf[u]; }
+    }
+}
+
 // per node: polarity (bit 7 of word 0) and a 64-bit hash of the canonical row
 __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
     x ^= x >> 33; x *= 0xff51afd7ed558ccdull;
@@ -155,9 +206,78 @@ __global__ void es_verify_kernel(const unsigned long long *__restrict__ vals, lo
 }
 
 struct SimProg {
-    std::vector<SimRec> recs;  // whole batches
+    std::vector<SimRec> recs;  // whole batches: the level schedule, then the distance-2 one
     int levels = 0;
+    size_t n_level = 0;  // records of the level schedule (es_sim_kernel)
 };
+
+// Distance-2 list schedule (appended after the level batches): a gate may go into batch t once
+// both fanins were written in batches <= t-2 (PIs/constant: always); up to
+// kSimU ready gates per batch, longest path to a sink first.
+void schedule_pipe(int FG, int32_t num_gates, const uint8_t *kind, const uint32_t *in0,
+                   const uint32_t *in1, SimProg *sp) {
+    constexpr int D = 2;
+    const int NG = num_gates;
+    std::vector<int> fo_start(NG + 1, 0), fo(2 * (size_t)NG), pend(NG, 0), height(NG, 0), bidx(NG, 0);
+    for (int g = 0; g < NG; ++g)
+        for (uint32_t l : {in0[g], in1[g]}) {
+            const int a = (int)(l >> 1) - FG;
+            if (a >= 0) { fo_start[a + 1]++; pend[g]++; }
+        }
+    for (int g = 0; g < NG; ++g) fo_start[g + 1] += fo_start[g];
+    {
+        std::vector<int> fill(fo_start.begin(), fo_start.end() - 1);
+        for (int g = 0; g < NG; ++g)
+            for (uint32_t l : {in0[g], in1[g]}) {
+                const int a = (int)(l >> 1) - FG;
+                if (a >= 0) fo[fill[a]++] = g;
+            }
+    }
+    for (int g = NG - 1; g >= 0; --g)
+        for (uint32_t l : {in0[g], in1[g]}) {
+            const int a = (int)(l >> 1) - FG;
+            if (a >= 0) height[a] = std::max(height[a], height[g] + 1);
+        }
+    std::vector<std::vector<int>> bucket(1);
+    for (int g = 0; g < NG; ++g)
+        if (pend[g] == 0) bucket[0].push_back(g);
+    std::priority_queue<std::pair<int, int>> ready;  // (height, -gate)
+    int placed = 0;
+    for (int t = 0; placed < NG; ++t) {
+        if ((int)bucket.size() > t)
+            for (int g : bucket[t]) ready.push({height[g], -g});
+        std::vector<int> batch;
+        while (!ready.empty() && (int)batch.size() < kSimU) {
+            batch.push_back(-ready.top().second);
+            ready.pop();
+        }
+        for (int g : batch) {
+            bidx[g] = t;
+            SimRec r{};
+            r.a = in0[g] >> 1;
+            r.b = in1[g] >> 1;
+            r.d = (uint32_t)(FG + g);
+            r.f = (kind[g] ? 1u : 0u) | ((in0[g] & 1) ? 2u : 0u) | ((in1[g] & 1) ? 4u : 0u);
+            sp->recs.push_back(r);
+        }
+        placed += (int)batch.size();
+        for (int g : batch)
+            for (int e = fo_start[g]; e < fo_start[g + 1]; ++e) {
+                const int o = fo[e];
+                if (--pend[o]) continue;
+                int rt = 0;
+                for (uint32_t l : {in0[o], in1[o]}) {
+                    const int a = (int)(l >> 1) - FG;
+                    if (a >= 0) rt = std::max(rt, bidx[a] + D);
+                }
+                if ((int)bucket.size() <= rt) bucket.resize(rt + 1);
+                bucket[rt].push_back(o);
+            }
+        // an empty batch still occupies batch index t (the distance rule counts batches)
+        if (batch.empty()) sp->recs.push_back(SimRec{0, 0, 0, 8u});
+        while (sp->recs.size() % kSimU) sp->recs.push_back(SimRec{0, 0, 0, 8u});
+    }
+}
 
 // Levelised gate list: level(v) = 1 + max level of its gate fanins; gates
 // sorted by (level, node), each level cut into batches of kSimU (the last
@@ -195,6 +315,8 @@ int build_sim_prog(int32_t num_pis, int32_t num_gates, const uint8_t *kind, cons
         }
         while (sp->recs.size() % kSimU) sp->recs.push_back(SimRec{0, 0, 0, 8u});
     }
+    sp->n_level = sp->recs.size();
+    schedule_pipe(FG, num_gates, kind, in0, in1, sp);
     return ES_OK;
 }
 
@@ -248,8 +370,19 @@ int sim_enqueue(const SimProg &sp, const SimRec *d_recs, int num_pis, long long 
         int G = nw <= 8192 ? 8 : nw <= 16384 ? 4 : nw <= 32768 ? 2 : 1;
         if (const char *e = getenv("ES_SIM_G")) G = atoi(e);
         const long long grid = (nw * G + T - 1) / T;
-        const int nb = (int)(sp.recs.size() / kSimU);
-        if (G == 8) es_sim_kernel<8><<<(unsigned)grid, T, 0, st>>>(d_recs, nb, w0, w1, words, d_vals);
+        // software-pipelined kernel for tiles of <= 16,384 words (mult16, us,
+        // level / pipelined at the default G: 64 words 112/109, 4,096: 154/147,
+        // 16,384: 227/204; 65,536 words (G = 1): 532/840, G = 2 647)
+        bool pipe = nw <= 16384;
+        if (const char *e = getenv("ES_SIM_PIPE")) pipe = atoi(e) != 0;
+        const int nb = (int)((pipe ? sp.recs.size() - sp.n_level : sp.n_level) / kSimU);
+        if (pipe) {
+            const SimRec *pr = d_recs + sp.n_level;
+            if (G == 8) es_sim_pipe_kernel<8><<<(unsigned)grid, T, 0, st>>>(pr, nb, w0, w1, words, d_vals);
+            else if (G == 4) es_sim_pipe_kernel<4><<<(unsigned)grid, T, 0, st>>>(pr, nb, w0, w1, words, d_vals);
+            else if (G == 2) es_sim_pipe_kernel<2><<<(unsigned)grid, T, 0, st>>>(pr, nb, w0, w1, words, d_vals);
+            else es_sim_pipe_kernel<1><<<(unsigned)grid, T, 0, st>>>(pr, nb, w0, w1, words, d_vals);
+        } else if (G == 8) es_sim_kernel<8><<<(unsigned)grid, T, 0, st>>>(d_recs, nb, w0, w1, words, d_vals);
         else if (G == 4) es_sim_kernel<4><<<(unsigned)grid, T, 0, st>>>(d_recs, nb, w0, w1, words, d_vals);
         else if (G == 2) es_sim_kernel<2><<<(unsigned)grid, T, 0, st>>>(d_recs, nb, w0, w1, words, d_vals);
         else es_sim_kernel<1><<<(unsigned)grid, T, 0, st>>>(d_recs, nb, w0, w1, words, d_vals);
